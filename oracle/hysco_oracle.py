@@ -1,0 +1,530 @@
+"""CPU fp64 oracle for the PyHySCO GN-PCG hot path (arXiv 2403.10706).
+
+TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference leg may import this module.  The product path
+(paper_2403_10706_b200, libhysco.so) never imports, links or calls it, and it
+shares no code with the CUDA path.
+
+Plain, slow, obviously-correct NumPy float64, written from PAPER.md (cited as
+P:<line>) in the paper's order and notation.  Where the paper is silent or
+garbled the reading taken is named R<n>; every reading is listed in DESIGN.md
+§"Readings of the paper".
+
+Conventions: the phase-encoding (PE) axis is the last axis.  Images
+live on cells (n1, n2, n3); the field map b lives on the e3-staggered grid
+(n1, n2, n3+1): cell centres in dims 1-2, nodes in dim 3.  b is in mm (R2).
+Node l sits at l*h3, cell k is centred at (k+1/2)*h3.
+
+Pins: every function here is checked in tests/test_oracle_*.py against closed
+forms, invariants, brute force and the hand-derived worked example in
+tests/golden/.  The one result with no independent pin is the field map after
+a fixed number of GN-PCG iterations on a synthetic pair (parity unpinned as a
+whole; pinned only through its pinned pieces), see DESIGN.md.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+ALPHA_DEFAULT = 300.0   # P:100 "we fix alpha=300"
+BETA_DEFAULT = 1e-4     # P:100 "and beta=1e-4"
+
+# ---------------------------------------------------------------------------
+# Linear operators of the discretization
+# ---------------------------------------------------------------------------
+
+
+def avg_pe(b):
+    """Averaging operator A: nodes -> cell centres along PE."""
+    return 0.5 * (b[..., :-1] + b[..., 1:])
+
+
+def avg_pe_T(y):
+    """A^T: cells -> nodes."""
+    out = np.zeros(y.shape[:-1] + (y.shape[-1] + 1,))
+    out[..., :-1] += 0.5 * y
+    out[..., 1:] += 0.5 * y
+    return out
+
+
+def diff_pe(b, h3):
+    """Finite-difference operator D: (Db)_k = (b_{k+1} - b_k)/h3, dimensionless (R2)."""
+    return (b[..., 1:] - b[..., :-1]) / h3
+
+
+def diff_pe_T(y, h3):
+    """D^T: cells -> nodes."""
+    out = np.zeros(y.shape[:-1] + (y.shape[-1] + 1,))
+    out[..., :-1] -= y / h3
+    out[..., 1:] += y / h3
+    return out
+
+
+def short_diff(b, axis):
+    """Short forward difference along `axis` (n-1 differences), no scaling."""
+    return np.diff(b, axis=axis)
+
+
+def short_diff_T(y, axis):
+    """Adjoint of short_diff along `axis`."""
+    shp = list(y.shape)
+    shp[axis] += 1
+    out = np.zeros(shp)
+    lo = [slice(None)] * y.ndim
+    hi = [slice(None)] * y.ndim
+    lo[axis] = slice(0, -1)
+    hi[axis] = slice(1, None)
+    out[tuple(lo)] -= y
+    out[tuple(hi)] += y
+    return out
+
+
+def laplacian(b, h):
+    """H b: negative Laplacian on the node array, L = sum_d D_d^T D_d / h_d^2 (Eq.(5), R3).
+
+    Homogeneous Neumann (short differences), symmetric positive semi-definite,
+    constants in the null space.
+    """
+    out = np.zeros(b.shape)
+    for ax in range(3):
+        out += short_diff_T(short_diff(b, ax), ax) / h[ax] ** 2
+    return out
+
+
+def smoothness_quadform(b, h):
+    """b^T L b = sum_d ||D_d b||^2 / h_d^2."""
+    return sum(float(np.sum(short_diff(b, ax) ** 2)) / h[ax] ** 2 for ax in range(3))
+
+
+# ---------------------------------------------------------------------------
+# Image model: 1D piecewise-linear interpolation along PE (R5)
+# ---------------------------------------------------------------------------
+
+
+def interp_pe(f, u):
+    """Evaluate the piecewise-linear (hat-function) model of each column of f.
+
+    f : (..., n3) samples at index positions 0..n3-1 (cell centres).
+    u : (..., n3) query positions in index units (centre k at u = k).
+    Model (R5): f(u) = sum_k f_k max(0, 1 - |u - k|), i.e. zero beyond one cell
+    past the outer centres.  Returns (value, slope per index unit), the slope
+    being the right-hand one at breakpoints.
+    """
+    n3 = f.shape[-1]
+    fl = np.floor(u).astype(np.int64)
+    t = u - fl
+
+    def take(idx):
+        ok = (idx >= 0) & (idx < n3)
+        v = np.take_along_axis(f, np.clip(idx, 0, n3 - 1), axis=-1)
+        return np.where(ok, v, 0.0)
+
+    f0 = take(fl)
+    f1 = take(fl + 1)
+    return (1.0 - t) * f0 + t * f1, f1 - f0
+
+
+# ---------------------------------------------------------------------------
+# Barrier phi (Eq.(3))
+# ---------------------------------------------------------------------------
+
+
+def phi(z):
+    """phi(z) = z^4/(1 - z^2) on (-1,1), +inf otherwise."""
+    z = np.asarray(z, dtype=np.float64)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        return np.where(np.abs(z) < 1.0, z ** 4 / (1.0 - z ** 2), np.inf)
+
+
+def dphi(z):
+    """phi'(z) = 2 z^3 (2 - z^2)/(1 - z^2)^2."""
+    z = np.asarray(z, dtype=np.float64)
+    return 2.0 * z ** 3 * (2.0 - z ** 2) / (1.0 - z ** 2) ** 2
+
+
+def d2phi(z):
+    """phi''(z) = 2 z^2 (6 - 3 z^2 + z^4)/(1 - z^2)^3  (>= 0 on (-1,1))."""
+    z = np.asarray(z, dtype=np.float64)
+    return 2.0 * z ** 2 * (6.0 - 3.0 * z ** 2 + z ** 4) / (1.0 - z ** 2) ** 3
+
+
+# ---------------------------------------------------------------------------
+# Mass-preserving transform (Eq.(1))
+# ---------------------------------------------------------------------------
+
+
+def mp_transform(I, b, h3, sign):
+    """T[I, b, sign*v] at the cell centres: I(x + sign*b(x) v) * (1 + sign*d_v b)(x).
+
+    Geometric term via the averaging operator, modulation via the finite
+    difference operator, both at cell centres.
+    """
+    n3 = I.shape[-1]
+    k = np.arange(n3, dtype=np.float64)
+    u = k + sign * avg_pe(b) / h3
+    val, _ = interp_pe(np.asarray(I, np.float64), u)
+    return val * (1.0 + sign * diff_pe(b, h3))
+
+
+def apply_correction(Ip, Im, b, h3):
+    """Jacobian-modulation correction: the two corrected images."""
+    return mp_transform(Ip, b, h3, +1.0), mp_transform(Im, b, h3, -1.0)
+
+
+# ---------------------------------------------------------------------------
+# Objective J = D + alpha S + beta P, gradient, GN Hessian
+# ---------------------------------------------------------------------------
+
+
+class EvalState:
+    """Everything evaluate() produces; the GN Hessian is applied from it."""
+    pass
+
+
+def evaluate(Ip, Im, b, h, alpha=ALPHA_DEFAULT, beta=BETA_DEFAULT):
+    """Discrete objective (Eq.(6)) with gradient and GN-Hessian parts.
+
+    D = hd/2 sum_k r_k^2, r = T[I+,b,v] - T[I-,b,-v]      (Eq.(2), midpoint rule P:105)
+    S = hd/2 b^T L b                                       (Eq.(5))
+    P = hd/2 sum_k phi((Db)_k)                             (Eq.(3), midpoint rule, R4)
+    J = D + alpha S + beta P                               (Eq.(4)/(6))
+    Infeasible (some |Db| >= 1): J = +inf, no gradient (R4, Eq.(3) "infinity else").
+    """
+    Ip = np.asarray(Ip, np.float64)
+    Im = np.asarray(Im, np.float64)
+    b = np.asarray(b, np.float64)
+    h1, h2, h3 = (float(v) for v in h)
+    hd = h1 * h2 * h3
+    n3 = Ip.shape[-1]
+    k = np.arange(n3, dtype=np.float64)
+
+    st = EvalState()
+    st.h, st.hd, st.alpha, st.beta = (h1, h2, h3), hd, alpha, beta
+    Ab = avg_pe(b)
+    Db = diff_pe(b, h3)
+    st.Db = Db
+    st.infeasible = bool(np.any(np.abs(Db) >= 1.0))
+
+    up, um = k + Ab / h3, k - Ab / h3
+    vp, sp = interp_pe(Ip, up)          # value, slope per index unit
+    vm, sm = interp_pe(Im, um)
+    Tp = vp * (1.0 + Db)
+    Tm = vm * (1.0 - Db)
+    r = Tp - Tm
+    st.r = r
+
+    st.D = 0.5 * hd * float(np.sum(r * r))
+    st.S = 0.5 * hd * smoothness_quadform(b, (h1, h2, h3))
+    if st.infeasible:
+        st.P = np.inf
+        st.J = np.inf
+        st.grad = None
+        return st
+    st.P = 0.5 * hd * float(np.sum(phi(Db)))
+    st.J = st.D + alpha * st.S + beta * st.P
+
+    # Residual Jacobian J_r q = g*(A q) + s*(D q)  (product rule on Eq.(1))
+    st.g = (sp / h3) * (1.0 + Db) + (sm / h3) * (1.0 - Db)
+    st.s = vp + vm
+    st.d2phi = d2phi(Db)
+    st.b = b
+    # grad J = hd J_r^T r + alpha hd L b + beta (hd/2) D^T phi'(Db)
+    st.grad = (hd * (avg_pe_T(st.g * r) + diff_pe_T(st.s * r, h3))
+               + alpha * hd * laplacian(b, (h1, h2, h3))
+               + beta * 0.5 * hd * diff_pe_T(dphi(Db), h3))
+    return st
+
+
+def residual_jac(st, q):
+    """J_r q."""
+    return st.g * avg_pe(q) + st.s * diff_pe(q, st.h[2])
+
+
+def residual_jac_T(st, y):
+    """J_r^T y."""
+    return avg_pe_T(st.g * y) + diff_pe_T(st.s * y, st.h[2])
+
+
+def hessvec(st, q):
+    """GN Hessian matvec (R12):
+
+    H_J q = hd J_r^T J_r q + alpha hd L q + beta (hd/2) D^T diag(phi''(Db)) D q.
+    """
+    h3 = st.h[2]
+    q = np.asarray(q, np.float64)
+    return (st.hd * residual_jac_T(st, residual_jac(st, q))
+            + st.alpha * st.hd * laplacian(q, st.h)
+            + st.beta * 0.5 * st.hd * diff_pe_T(st.d2phi * diff_pe(q, h3), h3))
+
+
+def hess_diag(st):
+    """diag(H_J): the Jacobi preconditioner (R13).
+
+    diag(J_r^T J_r)_l = sum_k (J_r)_{k,l}^2 = a_l^2 + c_{l-1}^2 with
+    a_k = dr_k/db_k = g_k/2 - s_k/h3, c_k = dr_k/db_{k+1} = g_k/2 + s_k/h3;
+    diag(L)_l = sum_d (#neighbours of l along d)/h_d^2;
+    diag(D^T Phi D)_l = (phi''_{l-1} + phi''_l)/h3^2.
+    """
+    h1, h2, h3 = st.h
+    a = st.g / 2.0 - st.s / h3
+    c = st.g / 2.0 + st.s / h3
+    shp = st.b.shape
+    dJ = np.zeros(shp)
+    dJ[..., :-1] += a ** 2
+    dJ[..., 1:] += c ** 2
+    dB = np.zeros(shp)
+    dB[..., :-1] += st.d2phi / h3 ** 2
+    dB[..., 1:] += st.d2phi / h3 ** 2
+    dL = np.zeros(shp)
+    for ax, hh in enumerate((h1, h2, h3)):
+        n = shp[ax]
+        cnt = np.full(n, 2.0)
+        if n == 1:
+            cnt[:] = 0.0
+        else:
+            cnt[0] = cnt[-1] = 1.0
+        sh = [1, 1, 1]
+        sh[ax] = n
+        dL = dL + cnt.reshape(sh) / hh ** 2
+    return st.hd * dJ + st.alpha * st.hd * dL + st.beta * 0.5 * st.hd * dB
+
+
+# ---------------------------------------------------------------------------
+# PCG: up to maxit iterations, stop if relative residual < tol
+# ---------------------------------------------------------------------------
+
+
+def pcg(Hmul, rhs, Mdiag, maxit=10, tol=0.1, fixed=False):
+    """Jacobi-preconditioned CG (Hestenes-Stiefel / Saad Alg. 9.1), x0 = 0 (R14).
+
+    Returns (x, iterations, matvecs, final relative residual ||r||/||r0||).
+    In fixed mode all maxit iterations run (parity / timing mode, R14).
+    """
+    x = np.zeros_like(rhs)
+    r = rhs.copy()
+    r0 = float(np.linalg.norm(r))
+    if r0 == 0.0:
+        return x, 0, 0, 0.0
+    z = r / Mdiag
+    p = z.copy()
+    rz = float(np.sum(r * z))
+    it = 0
+    rel = 1.0
+    for it in range(1, maxit + 1):
+        Hp = Hmul(p)
+        pHp = float(np.sum(p * Hp))
+        if pHp <= 0.0:
+            it -= 1
+            break
+        a = rz / pHp
+        x = x + a * p
+        r = r - a * Hp
+        rel = float(np.linalg.norm(r)) / r0
+        if not fixed and rel < tol:
+            break
+        z = r / Mdiag
+        rz_new = float(np.sum(r * z))
+        p = z + (rz_new / rz) * p
+        rz = rz_new
+    return x, it, it, rel
+
+
+# ---------------------------------------------------------------------------
+# Optimal-transport initialisation
+# ---------------------------------------------------------------------------
+
+
+def ot_shift(Ip, Im, eps=1e-3):
+    """Positivity shift (R6): one global shift common to both images,
+    min -> eps * (max - min).  Returns None when both images are constant."""
+    m0 = min(float(np.min(Ip)), float(np.min(Im)))
+    M0 = max(float(np.max(Ip)), float(np.max(Im)))
+    if M0 == m0:
+        return None
+    return -m0 + eps * (M0 - m0)
+
+
+def cdf(col):
+    """C(x) = sum_{j<x} w(j), x = 0..m, of the unit-mass measure w (R7); C(m) = 1 exactly."""
+    w = col / np.sum(col)
+    C = np.concatenate([[0.0], np.cumsum(w)])
+    C[-1] = 1.0
+    return C
+
+
+def quantile(C, r):
+    """Pseudo-inverse C^{-1}(r) = min{x : C(x) >= r} made piecewise linear (R8).
+
+    Q(r) = 0 for r <= 0; otherwise x* = min{x in 1..m : C(x) >= r} and
+    Q(r) = x* - 1 + (r - C(x*-1)) / (C(x*) - C(x*-1)).
+    """
+    r = np.asarray(r, np.float64)
+    m = len(C) - 1
+    out = np.zeros(r.shape)
+    for idx in np.ndindex(r.shape):
+        rv = r[idx]
+        if rv <= 0.0:
+            out[idx] = 0.0
+            continue
+        xs = m
+        for x in range(1, m + 1):           # the min-definition, literally
+            if C[x] >= rv:
+                xs = x
+                break
+        out[idx] = xs - 1 + (rv - C[xs - 1]) / (C[xs] - C[xs - 1])
+    return out
+
+
+def quantile_vec(C, r):
+    """Vectorised quantile(): identical definition via searchsorted (left = min{x: C(x) >= r})."""
+    r = np.asarray(r, np.float64)
+    m = len(C) - 1
+    xs = np.searchsorted(C[1:], r, side="left") + 1
+    xs = np.clip(xs, 1, m)
+    with np.errstate(divide="ignore", invalid="ignore"):   # 0/0 only where r <= 0 (masked)
+        q = xs - 1 + (r - C[xs - 1]) / (C[xs] - C[xs - 1])
+    return np.where(r <= 0.0, 0.0, q)
+
+
+def ot_column(ip, im, h3, vec=True):
+    """b0 on the nodes of one column (R9).
+
+    T+ = Q_half o C+, T- = Q_half o C-, Q_half = (Q+ + Q-)/2, and the field map
+    is the average of the displacements of T+ and -T-: b0 = h3 (T- - T+)/2.
+    """
+    Cp, Cm = cdf(ip), cdf(im)
+    Q = quantile_vec if vec else quantile
+
+    def Qh(r):
+        return 0.5 * (Q(Cp, r) + Q(Cm, r))
+
+    Tp = Qh(Cp)
+    Tm = Qh(Cm)
+    return h3 * (Tm - Tp) / 2.0
+
+
+def gaussian_weights_1d(sigma=1.0):
+    """Normalised 3-tap Gaussian (3x3x3 kernel, standard deviation 1.0)."""
+    w = np.exp(-np.array([-1.0, 0.0, 1.0]) ** 2 / (2.0 * sigma ** 2))
+    return w / w.sum()
+
+
+def blur3(b, sigma=1.0):
+    """3x3x3 Gaussian blur applied with an FFT (periodic) convolution, as the
+    paper's FFT3D operator does (R11)."""
+    w = gaussian_weights_1d(sigma)
+    K3 = w[:, None, None] * w[None, :, None] * w[None, None, :]
+    Kp = np.zeros(b.shape)
+    for a in range(3):
+        for c in range(3):
+            for e in range(3):
+                Kp[(a - 1) % b.shape[0], (c - 1) % b.shape[1], (e - 1) % b.shape[2]] += K3[a, c, e]
+    return np.real(np.fft.ifftn(np.fft.fftn(b) * np.fft.fftn(Kp)))
+
+
+def ot_init(Ip, Im, h3, eps=1e-3, blur=True, feas_cap=0.95, vec=True):
+    """Parallelised OT initialisation, steps (c2).1-6 of DESIGN.md.
+
+    Returns (b0, info) with info = {"max_Db_raw": ..., "scaled": bool}.
+    """
+    Ip = np.asarray(Ip, np.float64)
+    Im = np.asarray(Im, np.float64)
+    n1, n2, n3 = Ip.shape
+    b0 = np.zeros((n1, n2, n3 + 1))
+    info = {"max_Db_raw": 0.0, "scaled": False}
+    shift = ot_shift(Ip, Im, eps)
+    if shift is None:
+        return b0, info
+    ip, im = Ip + shift, Im + shift
+    for i in range(n1):
+        for j in range(n2):
+            b0[i, j] = ot_column(ip[i, j], im[i, j], h3, vec=vec)
+    if blur:
+        b0 = blur3(b0)
+    mx = float(np.max(np.abs(diff_pe(b0, h3)))) if n3 > 0 else 0.0
+    info["max_Db_raw"] = mx
+    if mx >= feas_cap:                           # R10 feasibility guard
+        b0 = b0 * (feas_cap / mx)
+        info["scaled"] = True
+    return b0, info
+
+
+# ---------------------------------------------------------------------------
+# Gauss-Newton with Armijo line search (R14-R16)
+# ---------------------------------------------------------------------------
+
+STOP_MAXITER, STOP_GRAD, STOP_DJ, STOP_DB, STOP_LSFAIL, STOP_INFEASIBLE = 0, 1, 2, 3, 4, 5
+
+
+def gauss_newton(Ip, Im, b0, h, alpha=ALPHA_DEFAULT, beta=BETA_DEFAULT, max_gn=10,
+                 max_pcg=10, pcg_tol=0.1, fixed=True, c1=1e-4, ls_max=10,
+                 tol_grad_rel=1e-2, tol_dJ_rel=1e-4, tol_db_rel=1e-3, log=None):
+    """b_{k+1} = b_k + gamma_k q_k with H_J q_k = -grad J (Eq.(7)).
+
+    fixed=True: exactly max_gn GN steps of exactly max_pcg PCG iterations
+    (parity / timing mode, R14, R16); fixed=False: the paper's stopping rules
+    with DESIGN.md's tolerances (R16).
+    """
+    b = np.asarray(b0, np.float64).copy()
+    st = evaluate(Ip, Im, b, h, alpha, beta)
+    rep = {"gn_iters": 0, "f_evals": 1, "h_evals": 0, "pcg_iters": 0,
+           "stop_reason": STOP_MAXITER, "history": []}
+    if st.infeasible:
+        rep["stop_reason"] = STOP_INFEASIBLE
+        rep.update(J=st.J, D=st.D, S=st.S, P=st.P, grad_norm=np.nan)
+        return b, st, rep
+    g0 = float(np.linalg.norm(st.grad))
+    for it in range(max_gn):
+        M = hess_diag(st)
+        q, npcg, nmv, rel = pcg(lambda v: hessvec(st, v), -st.grad, M, max_pcg, pcg_tol, fixed)
+        rep["h_evals"] += nmv
+        rep["pcg_iters"] += npcg
+        gq = float(np.sum(st.grad * q))
+        gamma = 1.0
+        accepted = False
+        for _ in range(ls_max):                     # Armijo (R15)
+            bt = b + gamma * q
+            stt = evaluate(Ip, Im, bt, h, alpha, beta)
+            rep["f_evals"] += 1
+            if (not stt.infeasible) and stt.J <= st.J + c1 * gamma * gq:
+                accepted = True
+                break
+            gamma *= 0.5
+        if not accepted:
+            rep["stop_reason"] = STOP_LSFAIL
+            break
+        J_old = st.J
+        b, st = bt, stt
+        rep["gn_iters"] += 1
+        rep["history"].append({"J": st.J, "D": st.D, "S": st.S, "P": st.P, "gamma": gamma,
+                               "pcg_iters": npcg, "relres": rel})
+        if log is not None:
+            log(rep["history"][-1])
+        if not fixed:
+            if float(np.linalg.norm(st.grad)) <= tol_grad_rel * g0:
+                rep["stop_reason"] = STOP_GRAD
+                break
+            if abs(J_old - st.J) <= tol_dJ_rel * abs(J_old):
+                rep["stop_reason"] = STOP_DJ
+                break
+            if float(np.max(np.abs(gamma * q))) <= tol_db_rel * h[2]:
+                rep["stop_reason"] = STOP_DB
+                break
+    rep.update(J=st.J, D=st.D, S=st.S, P=st.P, grad_norm=float(np.linalg.norm(st.grad)))
+    return b, st, rep
+
+
+def correct_pair(Ip, Im, h, alpha=ALPHA_DEFAULT, beta=BETA_DEFAULT, max_gn=10, max_pcg=10,
+                 fixed=True, blur=True, eps=1e-3):
+    """The whole path: OT init (+blur, guard) -> GN-PCG -> Jacobian-modulation apply."""
+    b0, _ = ot_init(Ip, Im, h[2], eps=eps, blur=blur)
+    b, st, rep = gauss_newton(Ip, Im, b0, h, alpha, beta, max_gn=max_gn, max_pcg=max_pcg,
+                              fixed=fixed)
+    Tp, Tm = apply_correction(Ip, Im, b, h[2])
+    return b0, b, Tp, Tm, rep
+
+
+def relative_improvement(Ip, Im, Tp, Tm):
+    """100 (1 - SSD(T+ - T-)/SSD(I+ - I-))."""
+    Ip = np.asarray(Ip, np.float64)
+    Im = np.asarray(Im, np.float64)
+    return 100.0 * (1.0 - float(np.sum((Tp - Tm) ** 2)) / float(np.sum((Ip - Im) ** 2)))
