@@ -1,0 +1,322 @@
+#!/usr/bin/env python
+"""bench.py — volume pairs corrected per second (HCP 3T shape) on N B200s.
+
+A step = the whole hot path for the pairs each
+rank owns: OT init + blur + guard -> 10 GN x 10 Jacobi-PCG (+Armijo) -> apply,
+one hysco_correct() call through the C ABI (one CUDA-graph launch).  Inputs
+are already resident in HBM (device timing, CUDA events on the context
+stream, L2 flushed by a 256 MiB write between timed steps); `e2e` is the same
+metric through hysco_correct_host() with pinned host buffers (H2D of the pair
+and D2H of b and the two corrected images inside the timed region).
+
+Multi-GPU (torchrun, one process per GPU): pairs are independent (BASELINE.json
+configs[3], "batch ... split across GPUs"), so each rank corrects its own
+pairs with no data-path collective ("scaling": "weak"); timing is the max over
+ranks of the device-timed region.
+
+--impl reference: the CPU fp64 oracle (oracle/), as it stands, on the host
+cores — the reference arm of this tier.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import phantom  # noqa: E402
+
+METRIC = "volume pairs corrected/sec (HCP 3T shape)"
+UNIT = "pairs/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="hysco", choices=["hysco", "reference"])
+    ap.add_argument("--config", default="C2_hcp3t", choices=sorted(phantom.CONFIGS))
+    ap.add_argument("--batch", type=int, default=1, help="pairs per GPU per step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-reps", type=int, default=20)
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    return ap.parse_args()
+
+
+def workload_desc(cfg, batch):
+    shape, h, seed = phantom.CONFIGS[cfg]
+    return {"workload": f"{cfg}: {shape[0]}x{shape[1]}x{shape[2]} cells (PE last), h={tuple(round(v, 4) for v in h)} mm, "
+                        "OT+blur+guard -> fixed 10 GN x 10 Jacobi-PCG + Armijo -> Jacobian-modulation apply",
+            "pairs_per_gpu": batch, "seed": seed, "alpha": 300.0, "beta": 1e-4,
+            "l2": "flushed (256 MiB write) between timed steps"}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.p = None
+
+    def _read(self):
+        for line in self.p.stdout:
+            self.rows.append([v.strip() for v in line.split(",")])
+
+    def stop(self):
+        if not self.p:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            self.p.wait(2)
+        except Exception:
+            self.p.kill()
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows if len(r) >= 9 for k in range(4)
+                          if r[5 + k].lower() in ("active", "1")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ---------------------------------------------------------------- CPU oracle timing (reference)
+
+def oracle_sample(pair, planes=None):
+    """Time the oracle (as it stands) on a bounded sample of the workload and
+    extrapolate seconds per pair = t_OT + 10 t_GN + t_apply, scaled by the
+    fraction of planes sampled.  Returns (seconds_per_pair, description)."""
+    from oracle import hysco_oracle as O
+    n1 = pair.Ip.shape[0]
+    planes = n1 if planes is None else max(2, min(n1, planes))
+    Ip = pair.Ip[:planes].astype(np.float64)
+    Im = pair.Im[:planes].astype(np.float64)
+    h = pair.h
+    t0 = time.perf_counter()
+    b0, _ = O.ot_init(Ip, Im, h[2])
+    t1 = time.perf_counter()
+    b, st, rep = O.gauss_newton(Ip, Im, b0, h, max_gn=1, max_pcg=10, fixed=True)
+    t2 = time.perf_counter()
+    O.apply_correction(Ip, Im, b, h[2])
+    t3 = time.perf_counter()
+    scale = n1 / planes
+    per_pair = ((t1 - t0) + 10 * (t2 - t1) + (t3 - t2)) * scale
+    desc = (f"oracle OT+blur, 1 GN step (10 PCG + Armijo eval), apply on {planes}/{n1} planes of the "
+            f"{pair.Ip.shape} pair; per pair = (t_OT + 10 t_GN + t_apply) x {scale:.3g}")
+    return per_pair, desc, t3 - t0
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    shape, h, seed = phantom.CONFIGS[args.config]
+    pair = phantom.make_pair(shape, h, seed)
+    # bounded: size the sample so (steps + warmup) samples take ~2 minutes
+    per_plane = None
+    probe, _, tp = oracle_sample(pair, planes=8)
+    per_plane = tp / 8
+    planes = int(max(2, min(shape[0], 120.0 / max(args.steps + args.warmup, 1) / per_plane)))
+    for _ in range(args.warmup):
+        oracle_sample(pair, planes)
+    vals, ms = [], []
+    desc = ""
+    for _ in range(args.steps):
+        spp, desc, wall = oracle_sample(pair, planes)
+        vals.append(spp)
+        ms.append(wall * 1e3)
+    spp = float(np.mean(vals))
+    v = 1.0 / spp
+    cores = 1
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.mean(ms)),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload_desc(args.config, 1),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU path
+
+def run_hysco(args):
+    import torch
+    from paper_2403_10706_b200 import hysco as H
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    shape, h, seed = phantom.CONFIGS[args.config]
+    n1, n2, n3 = shape
+    B = args.batch
+    pairs = [phantom.make_pair(shape, h, seed + 1000 * rank + k) for k in range(B)]
+    Ip_h = np.stack([p.Ip for p in pairs])
+    Im_h = np.stack([p.Im for p in pairs])
+    Ip = torch.from_numpy(Ip_h).to(dev)
+    Im = torch.from_numpy(Im_h).to(dev)
+    stream = torch.cuda.current_stream(dev)
+    ctx = H.hysco_create(shape, h, B, device=local, stream=stream.cuda_stream)
+    H.hysco_bind_images(ctx, Ip, Im)
+    b = torch.zeros((B, n1, n2, n3 + 1), dtype=torch.float32, device=dev)
+    Tp = torch.zeros((B, n1, n2, n3), dtype=torch.float32, device=dev)
+    Tm = torch.zeros_like(Tp)
+    flush = torch.empty(256 << 18, dtype=torch.float32, device=dev)   # 256 MiB > 126 MB L2
+
+    for _ in range(max(args.warmup, 0)):
+        H.hysco_correct(ctx, b, Tp, Tm, batch=B)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches = 0
+    reps = None
+    for k in range(args.steps):
+        flush.zero_()
+        ev[k][0].record(stream)
+        reps, inf = H.hysco_correct(ctx, b, Tp, Tm, batch=B)
+        ev[k][1].record(stream)
+        launches += H.hysco_last_launch_count(ctx)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    clocks = clk.stop()
+    step_ms = [a.elapsed_time(z) for a, z in ev]
+    total_ms = float(np.sum(step_ms))
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    total_max = float(t.item())
+    value = world * B * args.steps / (total_max / 1e3)
+    ms_per_step = total_max / args.steps
+
+    # ---- roofline: hot kernels re-launched on the same stream/config/buffers, CUDA events
+    prof_cold = H.hysco_profile_kernels(ctx, args.profile_reps, flush_l2=True)
+    prof_warm = H.hysco_profile_kernels(ctx, args.profile_reps, flush_l2=False)
+    Nn, Nc = B * n1 * n2 * (n3 + 1), B * n1 * n2 * n3
+    r0 = reps[0]
+    per_step = {"matvec": r0["h_evals"], "pcg_update": r0["pcg_iters"], "pcg_dir": r0["pcg_iters"],
+                "eval": r0["f_evals"]}
+    algo_bytes = {"matvec": 16 * Nn, "pcg_update": 28 * Nn, "pcg_dir": 16 * Nn, "eval": 16 * Nn + 8 * Nc}
+    share = {k: prof_warm[k] * per_step[k] / ms_per_step for k in per_step}
+    dom = max(share, key=share.get)
+    peak, peak_src = peaks()
+    ach = algo_bytes[dom] / (prof_cold[dom] * 1e-3) / 1e9
+    traffic = None
+    try:
+        summ = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        traffic = summ.get("kernels", {}).get(dom, {}).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    step_bytes = sum(algo_bytes[k] * per_step[k] for k in per_step)
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak, "traffic": traffic, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": algo_bytes[dom],
+                "avg_launch_ms_cold_l2": prof_cold[dom], "avg_launch_ms_warm_l2": prof_warm[dom],
+                "achieved_warm_l2": algo_bytes[dom] / (prof_warm[dom] * 1e-3) / 1e9,
+                "kernel_share_of_step": share,
+                "step_effective_gbs": step_bytes / (ms_per_step * 1e-3) / 1e9}
+
+    # ---- e2e through the host entry point (pinned buffers)
+    hIp = torch.from_numpy(Ip_h).pin_memory()
+    hIm = torch.from_numpy(Im_h).pin_memory()
+    hb = torch.empty((B, n1, n2, n3 + 1), dtype=torch.float32).pin_memory()
+    hTp = torch.empty((B, n1, n2, n3), dtype=torch.float32).pin_memory()
+    hTm = torch.empty_like(hTp).pin_memory()
+    for _ in range(2):
+        H.hysco_correct_host(ctx, hIp, hIm, hb, hTp, hTm, batch=B)
+    e2e_ms = []
+    for _ in range(max(1, args.e2e_steps)):
+        flush.zero_()
+        a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        H.hysco_correct_host(ctx, hIp, hIm, hb, hTp, hTm, batch=B)
+        z.record(stream)
+        z.synchronize()
+        e2e_ms.append(a.elapsed_time(z))
+    te = torch.tensor([float(np.sum(e2e_ms))], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+    e2e_val = world * B * len(e2e_ms) / (float(te.item()) / 1e3)
+    e2e = {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 2 * Nc * 4,
+           "d2h_bytes_per_step": (Nn + 2 * Nc) * 4, "ms_per_step": float(te.item()) / len(e2e_ms)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        os.environ.setdefault("OMP_NUM_THREADS", "1")
+        spp, desc, _ = oracle_sample(pairs[0])
+        cpu = {"value": 1.0 / spp, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
+               "threads_note": "NumPy elementwise, single-threaded (OMP_NUM_THREADS=1)",
+               "host_cpus": os.cpu_count()}
+
+    H.hysco_destroy(ctx)
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": dict(workload_desc(args.config, B), parallelism=f"dp{world} (independent pairs per rank)"),
+                "clocks": clocks, "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
+                "cpu_baseline": cpu,
+                "solver": {k: r0[k] for k in ("gn_iters", "f_evals", "h_evals", "pcg_iters", "stop", "J")},
+                "paper_context": {"seconds_per_pair": 4.38, "pairs_per_s": 1 / 4.38,
+                                  "hardware": "GPU inferred RTX A6000, fp32, real HCP 3T data",
+                                  "source": "PAPER.md Table 3 (P:476)"}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_hysco(args)
+
+
+if __name__ == "__main__":
+    main()

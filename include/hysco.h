@@ -1,0 +1,199 @@
+/*
+ * hysco.h — C ABI of libhysco.so, the B200 (sm_100a) hot path of PyHySCO's
+ * field-map estimation for reversed-gradient-polarity EPI correction
+ * (arXiv 2403.10706; PAPER.md cited as P:<line>, readings R<n> in DESIGN.md).
+ *
+ * The problem: given two images I+ and I- acquired with opposite
+ * phase-encoding (PE) direction +-v, find the field map b minimising
+ *
+ *   J(b) = D(b) + alpha S(b) + beta P(b)                              Eq.(4)/(6)
+ *   D    = 1/2 || I+(x + b v)(1 + d_v b) - I-(x - b v)(1 - d_v b) ||^2   Eq.(1)-(2)
+ *   S    = (h1 h2 h3 / 2) b^T L b, L the negative Laplacian             Eq.(5)
+ *   P    = 1/2 sum phi(d_v b),  phi(z) = z^4/(1 - z^2) on (-1,1)         Eq.(3)
+ *
+ * with a 1D optimal-transport initial guess per PE column, a
+ * Gauss-Newton / Jacobi-PCG solve and a Jacobian-modulation
+ * correction.
+ *
+ * Layout contract (the PE axis is permuted to be last):
+ *   images : C-contiguous [batch][n1][n2][n3]     ("cells")
+ *   b, q   : C-contiguous [batch][n1][n2][n3+1]   ("nodes", e3-staggered grid)
+ *   element type = the context's dtype (float for HYSCO_F32, double for
+ *   HYSCO_F64); b is in mm along +v (R2).  Device pointers must be 16-byte
+ *   aligned and must not alias each other unless stated.
+ *
+ * Streams: every call is ordered on the stream given at hysco_create.  Calls
+ * that return host scalars (objective_grad, solve, correct*) synchronise that
+ * stream before returning.  A context is not thread-safe; distinct contexts
+ * are independent.  Ownership: the caller owns all I/O buffers; images are
+ * BORROWED by hysco_bind_images and must stay valid and unmodified until the
+ * next bind or destroy; the context owns all scratch (allocated at create,
+ * never during a solve).
+ *
+ * Errors: status codes only, nothing is thrown across the ABI; the message of
+ * the last failure is returned by hysco_last_error().  A CUDA error poisons
+ * the context (every later call returns HYSCO_ERR_CUDA).  Infeasibility
+ * (|d_v b| >= 1 somewhere, phi = +inf) is a state, not an error.
+ */
+#ifndef HYSCO_H
+#define HYSCO_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define HYSCO_API __attribute__((visibility("default")))
+#else
+#define HYSCO_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hysco_ctx_s* hysco_ctx;
+
+typedef enum {
+    HYSCO_OK = 0,
+    HYSCO_INFEASIBLE = 1,    /* state: some |Db| >= 1, J = +inf (Eq.(3))       */
+    HYSCO_ERR_ARG = -1,      /* NULL / misaligned pointer, bad option value     */
+    HYSCO_ERR_SHAPE = -2,    /* bad sizes in hysco_config                       */
+    HYSCO_ERR_STATE = -3,    /* e.g. hessvec before a feasible objective_grad   */
+    HYSCO_ERR_CUDA = -4,     /* CUDA runtime error (context poisoned)           */
+    HYSCO_ERR_NCCL = -5,     /* reserved for the multi-GPU slab path            */
+    HYSCO_ERR_NOMEM = -6     /* device allocation failed at create              */
+} hysco_status;
+
+typedef enum { HYSCO_F32 = 0, HYSCO_F64 = 1 } hysco_dtype;
+
+/* Problem description.  One context holds `batch` independent pairs of the
+ * same shape and voxel size (Table 1 shapes; batched DP). */
+typedef struct {
+    int64_t n1, n2, n3;      /* cells per pair, PE = n3 (last, contiguous); n3 >= 2, n1,n2 >= 1 */
+    int64_t batch;           /* pairs, >= 1                                       */
+    double h1, h2, h3;       /* voxel size in mm, > 0                             */
+    double alpha, beta;      /* weights of S and P; paper: 300 and 1e-4   */
+    int32_t dtype;           /* hysco_dtype                                       */
+    int32_t device;          /* CUDA device ordinal                               */
+} hysco_config;
+
+/* OT initialisation options. */
+typedef struct {
+    double eps;              /* positivity shift, fraction of the pair's range (R6); default 1e-3 */
+    int32_t blur;            /* 1: 3x3x3 Gaussian, sigma = 1 voxel, periodic (R11)          */
+    double feas_cap;         /* if max|Db0| >= feas_cap, scale b0 to feas_cap (R10); default 0.95  */
+} hysco_ot_opts;
+
+/* GN-PCG options (R14-R16). */
+typedef struct {
+    int32_t max_gn;          /* Gauss-Newton iterations (fixed mode: exactly this many)   */
+    int32_t max_pcg;         /* PCG iterations per GN step, paper: 10             */
+    double pcg_rtol;         /* early stop if ||r||/||r0|| < pcg_rtol, paper: 0.1 */
+    int32_t fixed_iters;     /* 1: no early stops (parity / timing), 0: paper stop rules  */
+    int32_t ls_max;          /* Armijo halvings, default 10 (R15)                          */
+    double armijo_c1;        /* Armijo constant, default 1e-4 (R15)                        */
+    double tol_grad_rel;     /* stop if ||grad|| <= tol * ||grad(b0)|| (R16), default 1e-2 */
+    double tol_dJ_rel;       /* stop if |J_old - J| <= tol * |J_old| (R16), default 1e-4    */
+    double tol_db_rel;       /* stop if max|gamma q| <= tol * h3 (R16), default 1e-3        */
+    int32_t armijo;          /* 1 (default): Armijo sufficient decrease (R15);
+                                0: accept the full step unless infeasible, halving only for
+                                feasibility — the parity mode of DESIGN.md R15, which keeps
+                                the accept decision free of fp32-vs-fp64 rounding of J      */
+} hysco_solve_opts;
+
+enum { HYSCO_STOP_MAXITER = 0, HYSCO_STOP_GRAD = 1, HYSCO_STOP_DJ = 2, HYSCO_STOP_DB = 3,
+       HYSCO_STOP_LSFAIL = 4, HYSCO_STOP_INFEASIBLE = 5 };
+
+/* Per-pair result of a solve (OptimizationLogger analogue; T4 counters P:519). */
+typedef struct {
+    int32_t gn_iters;        /* accepted GN steps                        */
+    int32_t f_evals;         /* objective evaluations incl. the first    */
+    int32_t h_evals;         /* Hessian matvecs                          */
+    int32_t pcg_iters;       /* total PCG iterations                     */
+    int32_t stop_reason;     /* HYSCO_STOP_*                             */
+    int32_t ls_halvings;     /* total Armijo halvings                    */
+    double J, D, S, P;       /* objective parts at the returned b        */
+    double grad_norm;        /* ||grad J|| at the returned b             */
+    double last_relres;      /* ||r||/||r0|| of the last PCG solve       */
+} hysco_report;
+
+/* Fills the defaults named above (R6, R10, R11, R14-R16). */
+HYSCO_API void hysco_default_solve_opts(hysco_solve_opts* o);
+HYSCO_API void hysco_default_ot_opts(hysco_ot_opts* o);
+
+/* Create a context: validates cfg, allocates all scratch on cfg->device, and
+ * binds `cuda_stream` (a cudaStream_t, not the legacy NULL stream: solves are
+ * captured into CUDA graphs; NULL = the context creates and owns a
+ * non-blocking stream).  Returns HYSCO_ERR_SHAPE / HYSCO_ERR_ARG for invalid
+ * cfg, HYSCO_ERR_NOMEM if the scratch does not fit, *out = NULL on failure. */
+HYSCO_API hysco_status hysco_create(const hysco_config* cfg, void* cuda_stream, hysco_ctx* out);
+
+/* Borrow the image pair (device, [batch][n1][n2][n3] of dtype). */
+HYSCO_API hysco_status hysco_bind_images(hysco_ctx ctx, const void* d_Iplus, const void* d_Iminus);
+
+/* OT initial field map + optional blur + feasibility guard
+ * (R10).  d_b_out: device nodes [batch][n1][n2][n3+1].  opts NULL = defaults. */
+HYSCO_API hysco_status hysco_ot_init(hysco_ctx ctx, const hysco_ot_opts* opts, void* d_b_out);
+
+/* Objective at b (Eq.(6)); JDSP (host, [batch][4] = J, D, S, P) and, when
+ * non-NULL, the gradient (device nodes).  Also stores the GN-Hessian parts at
+ * b for hysco_hessvec / hysco_hess_diag.  Returns HYSCO_INFEASIBLE (J = +inf,
+ * grad not written) if any pair is infeasible. */
+HYSCO_API hysco_status hysco_objective_grad(hysco_ctx ctx, const void* d_b, double* JDSP, void* d_grad);
+
+/* Hq = H_J q: GN data term + alpha hd L + beta barrier'', at the b
+ * of the last successful objective_grad (else HYSCO_ERR_STATE).  d_q, d_Hq:
+ * device nodes; must not alias. */
+HYSCO_API hysco_status hysco_hessvec(hysco_ctx ctx, const void* d_q, void* d_Hq);
+
+/* diag(H_J), the Jacobi preconditioner, device nodes. */
+HYSCO_API hysco_status hysco_hess_diag(hysco_ctx ctx, void* d_diag);
+
+/* Gauss-Newton with Jacobi-PCG and Armijo from b (in/out, device
+ * nodes).  reports: host array [batch] (may be NULL).  The whole solve runs as
+ * one CUDA graph with device-side control flow.  Returns HYSCO_INFEASIBLE
+ * without iterating if some pair's b is infeasible. */
+HYSCO_API hysco_status hysco_solve(hysco_ctx ctx, void* d_b_inout, const hysco_solve_opts* opts,
+                         hysco_report* reports);
+
+/* Jacobian-modulation correction: the two corrected images
+ * T[I+, b, v], T[I-, b, -v] (device cells). */
+HYSCO_API hysco_status hysco_apply(hysco_ctx ctx, const void* d_b, void* d_Iplus_corr, void* d_Iminus_corr);
+
+/* The whole path in one call on device buffers: OT init (+blur, guard) ->
+ * GN-PCG -> apply.  Any output pointer may be NULL. */
+HYSCO_API hysco_status hysco_correct(hysco_ctx ctx, const hysco_ot_opts* ot, const hysco_solve_opts* so,
+                           void* d_b_out, void* d_Iplus_corr, void* d_Iminus_corr,
+                           hysco_report* reports);
+
+/* Same on HOST buffers (pinned for full speed): copies the pair in, runs the
+ * path, copies b and the corrected pair out.  The images are copied into
+ * context-owned device memory (re-binding the context to it).  Outputs may be
+ * NULL. */
+HYSCO_API hysco_status hysco_correct_host(hysco_ctx ctx, const void* h_Iplus, const void* h_Iminus,
+                                const hysco_ot_opts* ot, const hysco_solve_opts* so,
+                                void* h_b_out, void* h_Iplus_corr, void* h_Iminus_corr,
+                                hysco_report* reports);
+
+/* Number of kernel launches issued by the last solve / correct call (graph
+ * nodes executed, counted on the device). */
+HYSCO_API int64_t hysco_last_launch_count(hysco_ctx ctx);
+
+/* Profiling hook for the roofline figures: after a solve, re-launches each
+ * hot kernel `reps` times on the context stream in the solve's launch
+ * configuration and on its buffers, timing each launch with CUDA events.
+ * avg_ms (host, [HYSCO_NPROF]) receives the mean launch duration of:
+ * [0] matvec (A5, PCG mode), [1] pcg_update (A6), [2] pcg_dir, [3] eval (A4).
+ * flush_l2 != 0: a 256 MiB scratch write (> the 126 MB L2) precedes every
+ * timed launch (outside the events), i.e. cold-cache HBM-bound timings.
+ * Clobbers the PCG scratch (not b, not the images). */
+enum { HYSCO_PROF_MATVEC = 0, HYSCO_PROF_UPDATE = 1, HYSCO_PROF_DIR = 2, HYSCO_PROF_EVAL = 3, HYSCO_NPROF = 4 };
+HYSCO_API hysco_status hysco_profile_kernels(hysco_ctx ctx, int32_t reps, int32_t flush_l2, double* avg_ms);
+
+HYSCO_API const char* hysco_last_error(hysco_ctx ctx);
+HYSCO_API hysco_status hysco_destroy(hysco_ctx ctx);
+HYSCO_API int32_t hysco_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HYSCO_H */

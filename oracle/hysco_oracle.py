@@ -457,16 +457,17 @@ STOP_MAXITER, STOP_GRAD, STOP_DJ, STOP_DB, STOP_LSFAIL, STOP_INFEASIBLE = 0, 1, 
 
 def gauss_newton(Ip, Im, b0, h, alpha=ALPHA_DEFAULT, beta=BETA_DEFAULT, max_gn=10,
                  max_pcg=10, pcg_tol=0.1, fixed=True, c1=1e-4, ls_max=10,
-                 tol_grad_rel=1e-2, tol_dJ_rel=1e-4, tol_db_rel=1e-3, log=None):
+                 tol_grad_rel=1e-2, tol_dJ_rel=1e-4, tol_db_rel=1e-3, log=None, armijo=True):
     """b_{k+1} = b_k + gamma_k q_k with H_J q_k = -grad J (Eq.(7)).
 
     fixed=True: exactly max_gn GN steps of exactly max_pcg PCG iterations
     (parity / timing mode, R14, R16); fixed=False: the paper's stopping rules
-    with DESIGN.md's tolerances (R16).
+    with DESIGN.md's tolerances (R16).  armijo=False accepts the full step
+    unless infeasible (halving only for feasibility): the parity mode of R15.
     """
     b = np.asarray(b0, np.float64).copy()
     st = evaluate(Ip, Im, b, h, alpha, beta)
-    rep = {"gn_iters": 0, "f_evals": 1, "h_evals": 0, "pcg_iters": 0,
+    rep = {"gn_iters": 0, "f_evals": 1, "h_evals": 0, "pcg_iters": 0, "ls_halvings": 0,
            "stop_reason": STOP_MAXITER, "history": []}
     if st.infeasible:
         rep["stop_reason"] = STOP_INFEASIBLE
@@ -481,13 +482,15 @@ def gauss_newton(Ip, Im, b0, h, alpha=ALPHA_DEFAULT, beta=BETA_DEFAULT, max_gn=1
         gq = float(np.sum(st.grad * q))
         gamma = 1.0
         accepted = False
-        for _ in range(ls_max):                     # Armijo (R15)
+        for t in range(ls_max):                     # Armijo (R15)
             bt = b + gamma * q
             stt = evaluate(Ip, Im, bt, h, alpha, beta)
             rep["f_evals"] += 1
-            if (not stt.infeasible) and stt.J <= st.J + c1 * gamma * gq:
+            if (not stt.infeasible) and (not armijo or stt.J <= st.J + c1 * gamma * gq):
                 accepted = True
                 break
+            if t + 1 < ls_max:
+                rep["ls_halvings"] += 1
             gamma *= 0.5
         if not accepted:
             rep["stop_reason"] = STOP_LSFAIL
@@ -514,11 +517,11 @@ def gauss_newton(Ip, Im, b0, h, alpha=ALPHA_DEFAULT, beta=BETA_DEFAULT, max_gn=1
 
 
 def correct_pair(Ip, Im, h, alpha=ALPHA_DEFAULT, beta=BETA_DEFAULT, max_gn=10, max_pcg=10,
-                 fixed=True, blur=True, eps=1e-3):
+                 fixed=True, blur=True, eps=1e-3, armijo=True):
     """The whole path: OT init (+blur, guard) -> GN-PCG -> Jacobian-modulation apply."""
     b0, _ = ot_init(Ip, Im, h[2], eps=eps, blur=blur)
     b, st, rep = gauss_newton(Ip, Im, b0, h, alpha, beta, max_gn=max_gn, max_pcg=max_pcg,
-                              fixed=fixed)
+                              fixed=fixed, armijo=armijo)
     Tp, Tm = apply_correction(Ip, Im, b, h[2])
     return b0, b, Tp, Tm, rep
 

@@ -1,0 +1,37 @@
+"""Build libhysco.so in-tree for sm_100a (nvcc; no JIT, no torch extension)."""
+import os
+import subprocess
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+SRC = os.path.join(PKG, "csrc", "hysco_api.cu")
+DEPS = [os.path.join(PKG, "csrc", f) for f in ("hysco_api.cu", "hysco_common.cuh", "hysco_kernels.cuh")] + \
+       [os.path.join(ROOT, "include", "hysco.h")]
+LIB = os.path.join(PKG, "libhysco.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
+         "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "-shared",
+         "-I" + os.path.join(ROOT, "include")]
+
+
+def needs_build():
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    return any(os.path.getmtime(d) > t for d in DEPS)
+
+
+def build(force=False, verbose=False):
+    """Compile csrc/ into paper_2403_10706_b200/libhysco.so; returns the path."""
+    if force or needs_build():
+        cmd = [NVCC] + FLAGS + ["-o", LIB + ".tmp", SRC]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.run(cmd, check=True)
+        os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force=True, verbose=True)

@@ -1,0 +1,808 @@
+// hysco_api.cu — C ABI of libhysco.so (declared in include/hysco.h).
+//
+// Host side: context, memory plan (all scratch allocated at create), and the
+// orchestration of the GN-PCG solve as ONE CUDA graph whose
+// Gauss-Newton, PCG and Armijo loops are device-side conditional WHILE nodes
+// (no host synchronisation inside a solve).  A host-loop fallback with the
+// same kernels exists for drivers without conditional nodes (HYSCO_NO_GRAPH=1
+// forces it).
+#include "hysco.h"
+#include "hysco_kernels.cuh"
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <functional>
+#include <string>
+#include <vector>
+
+using namespace hysco;
+
+namespace {
+
+enum { B_B = 0, B_BOLD, B_GRAD, B_DT, B_ET, B_X, B_R, B_P, B_HP, B_TMP, NBUF };
+
+struct GraphKey {
+    int kind;                 // 1 = solve, 2 = correct
+    SolveParams sp;
+    int blur;
+    const void* ptr[8];
+};
+
+}  // namespace
+
+struct hysco_ctx_s {
+    hysco_config cfg{};
+    Geom g{};
+    int nsm = 0;
+    size_t esz = 4;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    const void* Ip = nullptr;
+    const void* Im = nullptr;
+    void* buf[NBUF] = {};
+    void* own_Ip = nullptr;   // host-entry image copies
+    void* own_Im = nullptr;
+    void* own_Tp = nullptr;   // host-entry corrected images
+    void* own_Tm = nullptr;
+    PairState* st = nullptr;
+    PairState* h_st = nullptr;          // pinned mirror
+    double* part = nullptr;
+    unsigned* ctr = nullptr;
+    unsigned* gctr = nullptr;
+    unsigned long long* launches = nullptr;
+    unsigned long long* h_launches = nullptr;
+    unsigned* dcond = nullptr;
+    unsigned* h_cond = nullptr;
+    Ctl ctl{};
+    int gx_nodes = 1, gx_cells = 1, gx_eval = 1, gx_apply = 1, gx_ot = 1;
+    size_t smem_eval = 0, smem_ot = 0;
+    bool state_valid = false;
+    bool poisoned = false;
+    bool no_graph = false;
+    bool graph_broken = false;
+    std::string err;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    GraphKey key{};
+    bool have_key = false;
+    long long last_launches = 0;
+    void* flush = nullptr;    // profiling-only L2 flush scratch
+};
+
+static hysco_status set_err(hysco_ctx c, hysco_status s, const std::string& m) {
+    if (c) c->err = m;
+    return s;
+}
+
+static hysco_status cuda_fail(hysco_ctx c, cudaError_t e, const char* what, int line) {
+    char b[512];
+    snprintf(b, sizeof b, "CUDA error %d (%s) at %s [hysco_api.cu:%d]", (int)e, cudaGetErrorString(e), what, line);
+    cudaGetLastError();
+    if (c) {
+        c->poisoned = true;
+        c->err = b;
+    }
+    return HYSCO_ERR_CUDA;
+}
+
+#define CK(call)                                                             \
+    do {                                                                     \
+        cudaError_t e_ = (call);                                             \
+        if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call, __LINE__);   \
+    } while (0)
+
+#define CHECK_CTX()                                                                          \
+    do {                                                                                     \
+        if (!ctx) return HYSCO_ERR_ARG;                                                      \
+        if (ctx->poisoned) return HYSCO_ERR_CUDA;                                            \
+        cudaError_t e0_ = cudaSetDevice(ctx->cfg.device);                                    \
+        if (e0_ != cudaSuccess) return cuda_fail(ctx, e0_, "cudaSetDevice", __LINE__);       \
+    } while (0)
+
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+static SolveParams to_params(const hysco_solve_opts& o, const hysco_ot_opts& t) {
+    SolveParams s{};
+    s.max_gn = o.max_gn;
+    s.max_pcg = o.max_pcg;
+    s.fixed = o.fixed_iters ? 1 : 0;
+    s.ls_max = o.ls_max;
+    s.pcg_rtol = o.pcg_rtol;
+    s.c1 = o.armijo_c1;
+    s.tol_grad_rel = o.tol_grad_rel;
+    s.tol_dJ_rel = o.tol_dJ_rel;
+    s.tol_db_rel = o.tol_db_rel;
+    s.armijo = o.armijo ? 1 : 0;
+    s.feas_cap = t.feas_cap;
+    s.ot_eps = t.eps;
+    return s;
+}
+
+static hysco_status check_opts(hysco_ctx ctx, const hysco_solve_opts& o, const hysco_ot_opts& t) {
+    if (o.max_gn < 0 || o.max_pcg < 1 || o.ls_max < 1 || !(o.pcg_rtol >= 0) || !(o.armijo_c1 >= 0))
+        return set_err(ctx, HYSCO_ERR_ARG, "bad hysco_solve_opts");
+    if (!(t.eps >= 0) || !(t.feas_cap > 0)) return set_err(ctx, HYSCO_ERR_ARG, "bad hysco_ot_opts");
+    return HYSCO_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Kernel launchers (typed)
+// ---------------------------------------------------------------------------
+template <typename T>
+struct L {
+    static T* b(hysco_ctx c, int k) { return static_cast<T*>(c->buf[k]); }
+
+    static void eval(hysco_ctx c, const SolveParams& sp, int mode, const T* bsrc) {
+        eval_kernel<T><<<dim3(c->gx_eval, c->cfg.batch), 256, c->smem_eval, c->stream>>>(
+            c->g, c->ctl, sp, mode, (const T*)c->Ip, (const T*)c->Im, bsrc, b(c, B_GRAD), b(c, B_DT), b(c, B_ET));
+    }
+    static void pcg_init(hysco_ctx c) {
+        pcg_init_kernel<T><<<dim3(c->gx_nodes, c->cfg.batch), 256, 0, c->stream>>>(
+            c->g, c->ctl, b(c, B_GRAD), b(c, B_DT), b(c, B_X), b(c, B_R), b(c, B_P));
+    }
+    static void pcg_iter(hysco_ctx c, const SolveParams& sp) {
+        dim3 gr(c->gx_nodes, c->cfg.batch);
+        matvec_kernel<T, true><<<gr, 256, 0, c->stream>>>(c->g, c->ctl, b(c, B_DT), b(c, B_ET), b(c, B_P), b(c, B_HP));
+        pcg_update_kernel<T><<<gr, 256, 0, c->stream>>>(c->g, c->ctl, sp, b(c, B_DT), b(c, B_P), b(c, B_HP),
+                                                          b(c, B_X), b(c, B_R));
+        pcg_dir_kernel<T><<<gr, 256, 0, c->stream>>>(c->g, c->ctl, b(c, B_DT), b(c, B_R), b(c, B_P));
+    }
+    static void trial_init(hysco_ctx c) {
+        trial_init_kernel<T><<<dim3(c->gx_nodes, c->cfg.batch), 256, 0, c->stream>>>(
+            c->g, c->ctl, b(c, B_GRAD), b(c, B_X), b(c, B_B), b(c, B_BOLD));
+    }
+    static void ls_body(hysco_ctx c, const SolveParams& sp) {
+        eval(c, sp, EVAL_TRIAL, b(c, B_B));
+        ls_retry_kernel<T><<<dim3(c->gx_nodes, c->cfg.batch), 256, 0, c->stream>>>(c->g, c->ctl, b(c, B_X),
+                                                                                    b(c, B_BOLD), b(c, B_B));
+    }
+    static void gn_tail(hysco_ctx c) { gn_tail_kernel<<<1, 32, 0, c->stream>>>(c->ctl, (int)c->cfg.batch); }
+    static void matvec_plain(hysco_ctx c, const T* q, T* Hq) {
+        matvec_kernel<T, false><<<dim3(c->gx_nodes, c->cfg.batch), 256, 0, c->stream>>>(c->g, c->ctl, b(c, B_DT),
+                                                                                       b(c, B_ET), q, Hq);
+    }
+    static void diag(hysco_ctx c, T* out) {
+        hess_diag_kernel<T><<<dim3(c->gx_nodes, c->cfg.batch), 256, 0, c->stream>>>(c->g, c->ctl, b(c, B_DT), out);
+    }
+    static void apply(hysco_ctx c, const T* bsrc, T* Tp, T* Tm) {
+        apply_kernel<T><<<dim3(c->gx_apply, c->cfg.batch), 256, c->smem_eval, c->stream>>>(
+            c->g, c->ctl, (const T*)c->Ip, (const T*)c->Im, bsrc, Tp, Tm);
+    }
+    // OT init (+blur, guard) into buffer B_B
+    static void ot(hysco_ctx c, const SolveParams& sp, int blur) {
+        const T* Ip = (const T*)c->Ip;
+        const T* Im = (const T*)c->Im;
+        dim3 gn(c->gx_nodes, c->cfg.batch);
+        ot_minmax_kernel<T><<<dim3(c->gx_cells, c->cfg.batch), 256, 0, c->stream>>>(c->g, c->ctl, sp, Ip, Im);
+        T* dst = blur ? b(c, B_TMP) : b(c, B_B);
+        ot_column_kernel<T><<<dim3(c->gx_ot, c->cfg.batch), 256, c->smem_ot, c->stream>>>(c->g, c->ctl, Ip, Im, dst);
+        if (blur) {
+            const double e = exp(-0.5), w0 = e / (1.0 + 2.0 * e), w1 = 1.0 / (1.0 + 2.0 * e);
+            blur_axis_kernel<T><<<gn, 256, 0, c->stream>>>(c->g, c->ctl, 0, w0, w1, b(c, B_TMP), b(c, B_R));
+            blur_axis_kernel<T><<<gn, 256, 0, c->stream>>>(c->g, c->ctl, 1, w0, w1, b(c, B_R), b(c, B_P));
+            blur_axis_kernel<T><<<gn, 256, 0, c->stream>>>(c->g, c->ctl, 2, w0, w1, b(c, B_P), b(c, B_B));
+        }
+        guard_max_kernel<T><<<gn, 256, 0, c->stream>>>(c->g, c->ctl, sp, b(c, B_B));
+        guard_scale_kernel<T><<<gn, 256, 0, c->stream>>>(c->g, c->ctl, b(c, B_B));
+    }
+};
+
+// ---------------------------------------------------------------------------
+// Runner: the same control structure either captured into a CUDA graph with
+// conditional WHILE nodes, or executed with host-side loops.
+// ---------------------------------------------------------------------------
+struct Runner {
+    hysco_ctx c;
+    bool graph;
+    cudaGraph_t cur = nullptr;
+    std::vector<cudaGraphNode_t> tail;
+    cudaError_t err = cudaSuccess;
+
+    void seq(const std::function<void()>& fn) {
+        if (err != cudaSuccess) return;
+        if (!graph) {
+            fn();
+            err = cudaGetLastError();
+            return;
+        }
+        err = cudaStreamBeginCaptureToGraph(c->stream, cur, tail.data(), nullptr, tail.size(),
+                                            cudaStreamCaptureModeRelaxed);
+        if (err != cudaSuccess) return;
+        fn();
+        cudaError_t le = cudaGetLastError();
+        cudaStreamCaptureStatus cs;
+        const cudaGraphNode_t* deps = nullptr;
+        size_t nd = 0;
+        cudaError_t e2 = cudaStreamGetCaptureInfo(c->stream, &cs, nullptr, nullptr, &deps, &nd);
+        std::vector<cudaGraphNode_t> nt;
+        if (e2 == cudaSuccess) nt.assign(deps, deps + nd);
+        cudaGraph_t out = nullptr;
+        cudaError_t e3 = cudaStreamEndCapture(c->stream, &out);
+        err = le != cudaSuccess ? le : (e2 != cudaSuccess ? e2 : e3);
+        tail = nt;
+    }
+    void handle(int slot) {
+        if (err != cudaSuccess || !graph) return;
+        cudaGraphConditionalHandle h;
+        err = cudaGraphConditionalHandleCreate(&h, cur, 0, 0);
+        if (err == cudaSuccess) c->ctl.h[slot] = h;
+    }
+    void loop(int slot, const std::function<void()>& body) {
+        if (err != cudaSuccess) return;
+        if (!graph) {
+            for (int guard = 0; guard < 1000000; guard++) {
+                err = cudaMemcpyAsync(c->h_cond + slot, c->dcond + slot, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                                      c->stream);
+                if (err == cudaSuccess) err = cudaStreamSynchronize(c->stream);
+                if (err != cudaSuccess || c->h_cond[slot] == 0) return;
+                body();
+                if (err != cudaSuccess) return;
+            }
+            return;
+        }
+        cudaGraphNodeParams np{};
+        np.type = cudaGraphNodeTypeConditional;
+        np.conditional.handle = c->ctl.h[slot];
+        np.conditional.type = cudaGraphCondTypeWhile;
+        np.conditional.size = 1;
+        cudaGraphNode_t node;
+        err = cudaGraphAddNode(&node, cur, tail.data(), tail.size(), &np);
+        if (err != cudaSuccess) return;
+        cudaGraph_t saved = cur;
+        cur = np.conditional.phGraph_out[0];
+        tail.clear();
+        body();
+        cur = saved;
+        tail.assign(1, node);
+    }
+};
+
+// GN-PCG solve on buffer B_B, the structure of DESIGN.md "Solve graph".
+template <typename T>
+static void gn_sequence(Runner& r, const SolveParams& sp) {
+    hysco_ctx c = r.c;
+    r.handle(COND_GN);
+    r.seq([&] { L<T>::eval(c, sp, EVAL_GN_START, L<T>::b(c, B_B)); });
+    r.loop(COND_GN, [&] {
+        r.handle(COND_PCG);
+        r.handle(COND_LS);
+        r.seq([&] { L<T>::pcg_init(c); });
+        r.loop(COND_PCG, [&] { r.seq([&] { L<T>::pcg_iter(c, sp); }); });
+        r.seq([&] { L<T>::trial_init(c); });
+        r.loop(COND_LS, [&] { r.seq([&] { L<T>::ls_body(c, sp); }); });
+        r.seq([&] { L<T>::gn_tail(c); });
+    });
+}
+
+// Build (kind 1: solve b in place; kind 2: correct = OT + solve + apply) and
+// run either as a cached graph or host-looped.
+template <typename T>
+static hysco_status run_path(hysco_ctx ctx, const GraphKey& key, void* b_io, void* b_out, void* Tp, void* Tm) {
+    const size_t nb = (size_t)ctx->cfg.batch * ctx->g.Nn * ctx->esz;
+    auto body = [&](Runner& r) {
+        if (key.kind == 1) {
+            r.seq([&] { cudaMemcpyAsync(ctx->buf[B_B], b_io, nb, cudaMemcpyDeviceToDevice, ctx->stream); });
+        } else {
+            r.seq([&] { L<T>::ot(ctx, key.sp, key.blur); });
+        }
+        gn_sequence<T>(r, key.sp);
+        r.seq([&] {
+            if (key.kind == 1) {
+                cudaMemcpyAsync(b_io, ctx->buf[B_B], nb, cudaMemcpyDeviceToDevice, ctx->stream);
+            } else {
+                if (Tp || Tm) L<T>::apply(ctx, L<T>::b(ctx, B_B), (T*)Tp, (T*)Tm);
+                if (b_out) cudaMemcpyAsync(b_out, ctx->buf[B_B], nb, cudaMemcpyDeviceToDevice, ctx->stream);
+            }
+        });
+    };
+    CK(cudaMemsetAsync(ctx->launches, 0, sizeof(unsigned long long), ctx->stream));
+    bool use_graph = !ctx->no_graph && !ctx->graph_broken;
+    if (use_graph) {
+        bool hit = ctx->have_key && memcmp(&ctx->key, &key, sizeof key) == 0 && ctx->exec;
+        if (!hit) {
+            if (ctx->exec) cudaGraphExecDestroy(ctx->exec);
+            if (ctx->graph) cudaGraphDestroy(ctx->graph);
+            ctx->exec = nullptr;
+            ctx->graph = nullptr;
+            ctx->have_key = false;
+            Runner r{ctx, true};
+            r.err = cudaGraphCreate(&ctx->graph, 0);
+            r.cur = ctx->graph;
+            ctx->ctl.use_graph = 1;
+            body(r);
+            ctx->ctl.use_graph = 0;
+            if (r.err == cudaSuccess) r.err = cudaGraphInstantiate(&ctx->exec, ctx->graph, 0);
+            if (r.err != cudaSuccess) {
+                // conditional nodes unavailable: fall back to host loops for this context
+                cudaStreamCaptureStatus cs;
+                if (cudaStreamIsCapturing(ctx->stream, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+                    cudaGraph_t tmp;
+                    cudaStreamEndCapture(ctx->stream, &tmp);
+                }
+                cudaGetLastError();
+                if (ctx->exec) cudaGraphExecDestroy(ctx->exec);
+                if (ctx->graph) cudaGraphDestroy(ctx->graph);
+                ctx->exec = nullptr;
+                ctx->graph = nullptr;
+                ctx->graph_broken = true;
+                char m[256];
+                snprintf(m, sizeof m, "graph build failed (%s); using host loops", cudaGetErrorString(r.err));
+                ctx->err = m;
+                use_graph = false;
+            } else {
+                ctx->key = key;
+                ctx->have_key = true;
+            }
+        }
+        if (use_graph) CK(cudaGraphLaunch(ctx->exec, ctx->stream));
+    }
+    if (!use_graph) {
+        Runner r{ctx, false};
+        ctx->ctl.use_graph = 0;
+        body(r);
+        if (r.err != cudaSuccess) return cuda_fail(ctx, r.err, "host-loop solve", __LINE__);
+    }
+    CK(cudaMemcpyAsync(ctx->h_st, ctx->st, sizeof(PairState) * ctx->cfg.batch, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->h_launches, ctx->launches, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->last_launches = (long long)*ctx->h_launches;
+    return HYSCO_OK;
+}
+
+static void fill_reports(hysco_ctx ctx, hysco_report* rep, bool* any_infeasible_start) {
+    bool inf = false;
+    for (int p = 0; p < ctx->cfg.batch; p++) {
+        const PairState& s = ctx->h_st[p];
+        if (s.stop_reason == STOP_INFEASIBLE) inf = true;
+        if (!rep) continue;
+        hysco_report& r = rep[p];
+        r.gn_iters = s.gn_k;
+        r.f_evals = s.f_evals;
+        r.h_evals = s.h_evals;
+        r.pcg_iters = s.pcg_iters;
+        r.stop_reason = s.stop_reason;
+        r.ls_halvings = s.ls_halvings;
+        r.J = s.J;
+        r.D = s.D;
+        r.S = s.S;
+        r.P = s.P;
+        r.grad_norm = sqrt(s.gnorm2);
+        r.last_relres = s.relres;
+    }
+    if (any_infeasible_start) *any_infeasible_start = inf;
+}
+
+template <typename K>
+static int occ_blocks(K kernel, int threads, size_t smem) {
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem) != cudaSuccess || n < 1) n = 1;
+    return n;
+}
+
+template <typename T>
+static hysco_status setup_typed(hysco_ctx ctx) {
+    const Geom& g = ctx->g;
+    const long long batch = ctx->cfg.batch;
+    ctx->smem_eval = (size_t)8 * (2 * g.n3 + g.P) * sizeof(T);
+    ctx->smem_ot = (size_t)8 * 2 * g.P * sizeof(double);
+    if (ctx->smem_eval > 227 * 1024 || ctx->smem_ot > 227 * 1024)
+        return set_err(ctx, HYSCO_ERR_SHAPE, "n3 too large for the column-in-shared-memory kernels");
+    CK(cudaFuncSetAttribute(eval_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->smem_eval));
+    CK(cudaFuncSetAttribute(apply_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->smem_eval));
+    CK(cudaFuncSetAttribute(ot_column_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->smem_ot));
+    auto per_pair = [&](long long work_blocks, int occ) {
+        long long cap = ((long long)ctx->nsm * occ + batch - 1) / batch;
+        long long gx = work_blocks < cap ? work_blocks : cap;
+        return (int)(gx < 1 ? 1 : gx);
+    };
+    int occ_n = occ_blocks(pcg_update_kernel<T>, 256, 0);
+    int occ_m = occ_blocks(matvec_kernel<T, true>, 256, 0);
+    if (occ_m < occ_n) occ_n = occ_m;
+    ctx->gx_nodes = per_pair((g.Nn + 255) / 256, occ_n);
+    ctx->gx_cells = per_pair((g.Nc + 255) / 256, occ_n);
+    ctx->gx_eval = per_pair((g.ncol + 7) / 8, occ_blocks(eval_kernel<T>, 256, ctx->smem_eval));
+    ctx->gx_apply = per_pair((g.ncol + 7) / 8, occ_blocks(apply_kernel<T>, 256, ctx->smem_eval));
+    ctx->gx_ot = per_pair((g.ncol + 7) / 8, occ_blocks(ot_column_kernel<T>, 256, ctx->smem_ot));
+    int mx = ctx->gx_nodes;
+    for (int v : {ctx->gx_cells, ctx->gx_eval, ctx->gx_apply, ctx->gx_ot}) mx = v > mx ? v : mx;
+    ctx->ctl.part_stride = mx * 8;
+    return HYSCO_OK;
+}
+
+extern "C" {
+
+void hysco_default_solve_opts(hysco_solve_opts* o) {
+    if (!o) return;
+    o->max_gn = 10;
+    o->max_pcg = 10;
+    o->pcg_rtol = 0.1;
+    o->fixed_iters = 1;
+    o->ls_max = 10;
+    o->armijo_c1 = 1e-4;
+    o->tol_grad_rel = 1e-2;
+    o->tol_dJ_rel = 1e-4;
+    o->tol_db_rel = 1e-3;
+    o->armijo = 1;
+}
+
+void hysco_default_ot_opts(hysco_ot_opts* o) {
+    if (!o) return;
+    o->eps = 1e-3;
+    o->blur = 1;
+    o->feas_cap = 0.95;
+}
+
+int32_t hysco_version(void) { return 1; }
+
+hysco_status hysco_create(const hysco_config* cfg, void* cuda_stream, hysco_ctx* out) {
+    if (!cfg || !out) return HYSCO_ERR_ARG;
+    *out = nullptr;
+    if (cfg->n1 < 1 || cfg->n2 < 1 || cfg->n3 < 2 || cfg->batch < 1 || cfg->n3 > 8192 ||
+        cfg->n1 * cfg->n2 * (cfg->n3 + 1) > (1ll << 40))
+        return HYSCO_ERR_SHAPE;
+    if (!(cfg->h1 > 0 && cfg->h2 > 0 && cfg->h3 > 0) || !(cfg->alpha >= 0) || !(cfg->beta >= 0))
+        return HYSCO_ERR_ARG;
+    if (cfg->dtype != HYSCO_F32 && cfg->dtype != HYSCO_F64) return HYSCO_ERR_ARG;
+    hysco_ctx ctx = new hysco_ctx_s();
+    ctx->cfg = *cfg;
+    ctx->esz = cfg->dtype == HYSCO_F64 ? 8 : 4;
+    const char* ng = getenv("HYSCO_NO_GRAPH");
+    ctx->no_graph = ng && ng[0] == '1';
+    Geom& g = ctx->g;
+    g.n1 = (int)cfg->n1;
+    g.n2 = (int)cfg->n2;
+    g.n3 = (int)cfg->n3;
+    g.P = g.n3 + 1;
+    g.ncol = cfg->n1 * cfg->n2;
+    g.Nc = g.ncol * g.n3;
+    g.Nn = g.ncol * g.P;
+    g.h1 = cfg->h1;
+    g.h2 = cfg->h2;
+    g.h3 = cfg->h3;
+    g.hd = cfg->h1 * cfg->h2 * cfg->h3;
+    g.alpha = cfg->alpha;
+    g.beta = cfg->beta;
+    g.ahd = cfg->alpha * g.hd;
+    g.bh2 = 0.5 * cfg->beta * g.hd;
+    g.ih1sq = 1.0 / (cfg->h1 * cfg->h1);
+    g.ih2sq = 1.0 / (cfg->h2 * cfg->h2);
+    g.ih3sq = 1.0 / (cfg->h3 * cfg->h3);
+    g.ih3 = 1.0 / cfg->h3;
+
+    hysco_status st;
+    auto bail = [&](hysco_status s) {
+        hysco_destroy(ctx);
+        return s;
+    };
+    {
+        cudaError_t e = cudaSetDevice(cfg->device);
+        if (e != cudaSuccess) return bail(cuda_fail(ctx, e, "cudaSetDevice", __LINE__));
+        e = cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, cfg->device);
+        if (e != cudaSuccess) return bail(cuda_fail(ctx, e, "cudaDeviceGetAttribute", __LINE__));
+        if (cuda_stream) {
+            ctx->stream = (cudaStream_t)cuda_stream;
+        } else {
+            e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+            if (e != cudaSuccess) return bail(cuda_fail(ctx, e, "cudaStreamCreate", __LINE__));
+            ctx->own_stream = true;
+        }
+    }
+    st = cfg->dtype == HYSCO_F64 ? setup_typed<double>(ctx) : setup_typed<float>(ctx);
+    if (st != HYSCO_OK) return bail(st);
+    const size_t nn = (size_t)cfg->batch * g.Nn * ctx->esz, nc = (size_t)cfg->batch * g.Nc * ctx->esz;
+    auto dalloc = [&](void** p, size_t n) -> bool {
+        cudaError_t e = cudaMalloc(p, n);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            ctx->err = "cudaMalloc failed";
+            return false;
+        }
+        return true;
+    };
+    for (int k = 0; k < NBUF; k++)
+        if (!dalloc(&ctx->buf[k], nn)) return bail(HYSCO_ERR_NOMEM);
+    if (!dalloc(&ctx->own_Ip, nc) || !dalloc(&ctx->own_Im, nc) || !dalloc(&ctx->own_Tp, nc) ||
+        !dalloc(&ctx->own_Tm, nc))
+        return bail(HYSCO_ERR_NOMEM);
+    if (!dalloc((void**)&ctx->st, sizeof(PairState) * cfg->batch) ||
+        !dalloc((void**)&ctx->part, sizeof(double) * ctx->ctl.part_stride * cfg->batch) ||
+        !dalloc((void**)&ctx->ctr, sizeof(unsigned) * cfg->batch) || !dalloc((void**)&ctx->gctr, sizeof(unsigned)) ||
+        !dalloc((void**)&ctx->launches, sizeof(unsigned long long)) ||
+        !dalloc((void**)&ctx->dcond, sizeof(unsigned) * NCOND))
+        return bail(HYSCO_ERR_NOMEM);
+    if (cudaMallocHost((void**)&ctx->h_st, sizeof(PairState) * cfg->batch) != cudaSuccess ||
+        cudaMallocHost((void**)&ctx->h_launches, sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMallocHost((void**)&ctx->h_cond, sizeof(unsigned) * NCOND) != cudaSuccess) {
+        cudaGetLastError();
+        return bail(HYSCO_ERR_NOMEM);
+    }
+    cudaMemset(ctx->st, 0, sizeof(PairState) * cfg->batch);
+    cudaMemset(ctx->ctr, 0, sizeof(unsigned) * cfg->batch);
+    cudaMemset(ctx->gctr, 0, sizeof(unsigned));
+    cudaMemset(ctx->launches, 0, sizeof(unsigned long long));
+    cudaMemset(ctx->dcond, 0, sizeof(unsigned) * NCOND);
+    {
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) return bail(cuda_fail(ctx, e, "create sync", __LINE__));
+    }
+    ctx->ctl.st = ctx->st;
+    ctx->ctl.part = ctx->part;
+    ctx->ctl.ctr = ctx->ctr;
+    ctx->ctl.gctr = ctx->gctr;
+    ctx->ctl.launches = ctx->launches;
+    ctx->ctl.dcond = ctx->dcond;
+    ctx->ctl.use_graph = 0;
+    *out = ctx;
+    return HYSCO_OK;
+}
+
+hysco_status hysco_bind_images(hysco_ctx ctx, const void* d_Iplus, const void* d_Iminus) {
+    CHECK_CTX();
+    if (!d_Iplus || !d_Iminus || !aligned16(d_Iplus) || !aligned16(d_Iminus))
+        return set_err(ctx, HYSCO_ERR_ARG, "image pointers must be non-NULL and 16-byte aligned");
+    if (d_Iplus != ctx->Ip || d_Iminus != ctx->Im) ctx->have_key = false;   // graphs bake pointers
+    ctx->Ip = d_Iplus;
+    ctx->Im = d_Iminus;
+    ctx->state_valid = false;
+    return HYSCO_OK;
+}
+
+static hysco_status need_images(hysco_ctx ctx) {
+    if (!ctx->Ip || !ctx->Im) return set_err(ctx, HYSCO_ERR_STATE, "no images bound (hysco_bind_images)");
+    return HYSCO_OK;
+}
+
+hysco_status hysco_ot_init(hysco_ctx ctx, const hysco_ot_opts* opts, void* d_b_out) {
+    CHECK_CTX();
+    if (hysco_status s = need_images(ctx)) return s;
+    if (!d_b_out || !aligned16(d_b_out)) return set_err(ctx, HYSCO_ERR_ARG, "d_b_out must be 16-byte aligned");
+    hysco_ot_opts o;
+    hysco_default_ot_opts(&o);
+    if (opts) o = *opts;
+    hysco_solve_opts so;
+    hysco_default_solve_opts(&so);
+    if (hysco_status s = check_opts(ctx, so, o)) return s;
+    SolveParams sp = to_params(so, o);
+    if (ctx->cfg.dtype == HYSCO_F64) L<double>::ot(ctx, sp, o.blur);
+    else L<float>::ot(ctx, sp, o.blur);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(d_b_out, ctx->buf[B_B], (size_t)ctx->cfg.batch * ctx->g.Nn * ctx->esz,
+                       cudaMemcpyDeviceToDevice, ctx->stream));
+    return HYSCO_OK;
+}
+
+hysco_status hysco_objective_grad(hysco_ctx ctx, const void* d_b, double* JDSP, void* d_grad) {
+    CHECK_CTX();
+    if (hysco_status s = need_images(ctx)) return s;
+    if (!d_b || !aligned16(d_b) || (d_grad && !aligned16(d_grad)))
+        return set_err(ctx, HYSCO_ERR_ARG, "pointers must be 16-byte aligned");
+    const size_t nb = (size_t)ctx->cfg.batch * ctx->g.Nn * ctx->esz;
+    SolveParams sp{};
+    CK(cudaMemcpyAsync(ctx->buf[B_B], d_b, nb, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (ctx->cfg.dtype == HYSCO_F64) L<double>::eval(ctx, sp, EVAL_PLAIN, (const double*)ctx->buf[B_B]);
+    else L<float>::eval(ctx, sp, EVAL_PLAIN, (const float*)ctx->buf[B_B]);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(ctx->h_st, ctx->st, sizeof(PairState) * ctx->cfg.batch, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    bool inf = false;
+    for (int p = 0; p < ctx->cfg.batch; p++) {
+        const PairState& s = ctx->h_st[p];
+        inf = inf || s.infeasible;
+        if (JDSP) {
+            JDSP[4 * p + 0] = s.J;
+            JDSP[4 * p + 1] = s.D;
+            JDSP[4 * p + 2] = s.S;
+            JDSP[4 * p + 3] = s.P;
+        }
+    }
+    ctx->state_valid = !inf;
+    if (inf) return HYSCO_INFEASIBLE;
+    if (d_grad) {
+        CK(cudaMemcpyAsync(d_grad, ctx->buf[B_GRAD], nb, cudaMemcpyDeviceToDevice, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
+    return HYSCO_OK;
+}
+
+hysco_status hysco_hessvec(hysco_ctx ctx, const void* d_q, void* d_Hq) {
+    CHECK_CTX();
+    if (!ctx->state_valid) return set_err(ctx, HYSCO_ERR_STATE, "hessvec needs a feasible objective_grad first");
+    if (!d_q || !d_Hq || !aligned16(d_q) || !aligned16(d_Hq) || d_q == d_Hq)
+        return set_err(ctx, HYSCO_ERR_ARG, "d_q/d_Hq must be distinct, 16-byte aligned");
+    if (ctx->cfg.dtype == HYSCO_F64) L<double>::matvec_plain(ctx, (const double*)d_q, (double*)d_Hq);
+    else L<float>::matvec_plain(ctx, (const float*)d_q, (float*)d_Hq);
+    CK(cudaGetLastError());
+    return HYSCO_OK;
+}
+
+hysco_status hysco_hess_diag(hysco_ctx ctx, void* d_diag) {
+    CHECK_CTX();
+    if (!ctx->state_valid) return set_err(ctx, HYSCO_ERR_STATE, "hess_diag needs a feasible objective_grad first");
+    if (!d_diag || !aligned16(d_diag)) return set_err(ctx, HYSCO_ERR_ARG, "d_diag must be 16-byte aligned");
+    if (ctx->cfg.dtype == HYSCO_F64) L<double>::diag(ctx, (double*)d_diag);
+    else L<float>::diag(ctx, (float*)d_diag);
+    CK(cudaGetLastError());
+    return HYSCO_OK;
+}
+
+hysco_status hysco_apply(hysco_ctx ctx, const void* d_b, void* d_Iplus_corr, void* d_Iminus_corr) {
+    CHECK_CTX();
+    if (hysco_status s = need_images(ctx)) return s;
+    if (!d_b || !aligned16(d_b) || (d_Iplus_corr && !aligned16(d_Iplus_corr)) ||
+        (d_Iminus_corr && !aligned16(d_Iminus_corr)))
+        return set_err(ctx, HYSCO_ERR_ARG, "pointers must be 16-byte aligned");
+    if (ctx->cfg.dtype == HYSCO_F64) L<double>::apply(ctx, (const double*)d_b, (double*)d_Iplus_corr, (double*)d_Iminus_corr);
+    else L<float>::apply(ctx, (const float*)d_b, (float*)d_Iplus_corr, (float*)d_Iminus_corr);
+    CK(cudaGetLastError());
+    return HYSCO_OK;
+}
+
+static hysco_status solve_common(hysco_ctx ctx, int kind, const hysco_ot_opts* ot, const hysco_solve_opts* so,
+                                 void* b_io, void* b_out, void* Tp, void* Tm, hysco_report* reports) {
+    hysco_solve_opts o;
+    hysco_default_solve_opts(&o);
+    if (so) o = *so;
+    hysco_ot_opts t;
+    hysco_default_ot_opts(&t);
+    if (ot) t = *ot;
+    if (hysco_status s = check_opts(ctx, o, t)) return s;
+    GraphKey key;
+    memset(&key, 0, sizeof key);
+    key.kind = kind;
+    key.sp = to_params(o, t);
+    key.blur = t.blur ? 1 : 0;
+    key.ptr[0] = ctx->Ip;
+    key.ptr[1] = ctx->Im;
+    key.ptr[2] = b_io;
+    key.ptr[3] = b_out;
+    key.ptr[4] = Tp;
+    key.ptr[5] = Tm;
+    hysco_status s = ctx->cfg.dtype == HYSCO_F64 ? run_path<double>(ctx, key, b_io, b_out, Tp, Tm)
+                                                 : run_path<float>(ctx, key, b_io, b_out, Tp, Tm);
+    if (s != HYSCO_OK) return s;
+    bool inf = false;
+    fill_reports(ctx, reports, &inf);
+    ctx->state_valid = !inf;
+    return inf ? HYSCO_INFEASIBLE : HYSCO_OK;
+}
+
+hysco_status hysco_solve(hysco_ctx ctx, void* d_b_inout, const hysco_solve_opts* opts, hysco_report* reports) {
+    CHECK_CTX();
+    if (hysco_status s = need_images(ctx)) return s;
+    if (!d_b_inout || !aligned16(d_b_inout)) return set_err(ctx, HYSCO_ERR_ARG, "d_b_inout must be 16-byte aligned");
+    return solve_common(ctx, 1, nullptr, opts, d_b_inout, nullptr, nullptr, nullptr, reports);
+}
+
+hysco_status hysco_correct(hysco_ctx ctx, const hysco_ot_opts* ot, const hysco_solve_opts* so, void* d_b_out,
+                           void* d_Iplus_corr, void* d_Iminus_corr, hysco_report* reports) {
+    CHECK_CTX();
+    if (hysco_status s = need_images(ctx)) return s;
+    for (void* p : {d_b_out, d_Iplus_corr, d_Iminus_corr})
+        if (p && !aligned16(p)) return set_err(ctx, HYSCO_ERR_ARG, "output pointers must be 16-byte aligned");
+    return solve_common(ctx, 2, ot, so, nullptr, d_b_out, d_Iplus_corr, d_Iminus_corr, reports);
+}
+
+hysco_status hysco_correct_host(hysco_ctx ctx, const void* h_Iplus, const void* h_Iminus, const hysco_ot_opts* ot,
+                                const hysco_solve_opts* so, void* h_b_out, void* h_Iplus_corr, void* h_Iminus_corr,
+                                hysco_report* reports) {
+    CHECK_CTX();
+    if (!h_Iplus || !h_Iminus) return set_err(ctx, HYSCO_ERR_ARG, "host images must be non-NULL");
+    const size_t nc = (size_t)ctx->cfg.batch * ctx->g.Nc * ctx->esz;
+    const size_t nn = (size_t)ctx->cfg.batch * ctx->g.Nn * ctx->esz;
+    CK(cudaMemcpyAsync(ctx->own_Ip, h_Iplus, nc, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->own_Im, h_Iminus, nc, cudaMemcpyHostToDevice, ctx->stream));
+    if (hysco_status s = hysco_bind_images(ctx, ctx->own_Ip, ctx->own_Im)) return s;
+    hysco_status s = solve_common(ctx, 2, ot, so, nullptr, nullptr, h_Iplus_corr ? ctx->own_Tp : nullptr,
+                                  h_Iminus_corr ? ctx->own_Tm : nullptr, reports);
+    if (s < 0) return s;
+    if (h_b_out) CK(cudaMemcpyAsync(h_b_out, ctx->buf[B_B], nn, cudaMemcpyDeviceToHost, ctx->stream));
+    if (h_Iplus_corr) CK(cudaMemcpyAsync(h_Iplus_corr, ctx->own_Tp, nc, cudaMemcpyDeviceToHost, ctx->stream));
+    if (h_Iminus_corr) CK(cudaMemcpyAsync(h_Iminus_corr, ctx->own_Tm, nc, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return s;
+}
+
+int64_t hysco_last_launch_count(hysco_ctx ctx) { return ctx ? ctx->last_launches : -1; }
+
+}  // extern "C"
+
+template <typename T>
+static hysco_status profile_typed(hysco_ctx ctx, int reps, int flush_l2, double* avg_ms) {
+    // force the PCG kernels active (they early-exit on finished pairs)
+    CK(cudaMemcpyAsync(ctx->h_st, ctx->st, sizeof(PairState) * ctx->cfg.batch, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (int p = 0; p < ctx->cfg.batch; p++) {
+        ctx->h_st[p].pcg_active = 1;
+        ctx->h_st[p].alpha_c = 0.0;     // x, r unchanged by update
+        ctx->h_st[p].beta_c = 0.0;
+        ctx->h_st[p].rz = 1.0;
+        ctx->h_st[p].rr0 = 1.0;
+    }
+    SolveParams sp{};
+    sp.max_pcg = 1 << 30;
+    sp.fixed = 1;
+    const size_t flush_bytes = (size_t)256 << 20;
+    if (flush_l2 && !ctx->flush) CK(cudaMalloc(&ctx->flush, flush_bytes));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    dim3 gr(ctx->gx_nodes, ctx->cfg.batch);
+    for (int k = 0; k < HYSCO_NPROF; k++) {
+        double acc = 0;
+        for (int r = 0; r < reps; r++) {
+            CK(cudaMemcpyAsync(ctx->st, ctx->h_st, sizeof(PairState) * ctx->cfg.batch, cudaMemcpyHostToDevice,
+                               ctx->stream));
+            if (flush_l2) CK(cudaMemsetAsync(ctx->flush, r & 0xff, flush_bytes, ctx->stream));
+            CK(cudaEventRecord(e0, ctx->stream));
+            switch (k) {
+                case HYSCO_PROF_MATVEC:
+                    matvec_kernel<T, true><<<gr, 256, 0, ctx->stream>>>(ctx->g, ctx->ctl, L<T>::b(ctx, B_DT),
+                                                                      L<T>::b(ctx, B_ET), L<T>::b(ctx, B_P),
+                                                                      L<T>::b(ctx, B_HP));
+                    break;
+                case HYSCO_PROF_UPDATE:
+                    pcg_update_kernel<T><<<gr, 256, 0, ctx->stream>>>(ctx->g, ctx->ctl, sp, L<T>::b(ctx, B_DT),
+                                                                     L<T>::b(ctx, B_P), L<T>::b(ctx, B_HP),
+                                                                     L<T>::b(ctx, B_X), L<T>::b(ctx, B_R));
+                    break;
+                case HYSCO_PROF_DIR:
+                    pcg_dir_kernel<T><<<gr, 256, 0, ctx->stream>>>(ctx->g, ctx->ctl, L<T>::b(ctx, B_DT),
+                                                                  L<T>::b(ctx, B_R), L<T>::b(ctx, B_P));
+                    break;
+                default:
+                    L<T>::eval(ctx, sp, EVAL_PLAIN, L<T>::b(ctx, B_B));
+            }
+            CK(cudaGetLastError());
+            CK(cudaEventRecord(e1, ctx->stream));
+            CK(cudaEventSynchronize(e1));
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+            acc += ms;
+        }
+        avg_ms[k] = acc / reps;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    // restore a consistent Hessian state at the current b
+    L<T>::eval(ctx, sp, EVAL_PLAIN, L<T>::b(ctx, B_B));
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(ctx->stream));
+    return HYSCO_OK;
+}
+
+extern "C" {
+
+hysco_status hysco_profile_kernels(hysco_ctx ctx, int32_t reps, int32_t flush_l2, double* avg_ms) {
+    CHECK_CTX();
+    if (hysco_status s = need_images(ctx)) return s;
+    if (reps < 1 || !avg_ms) return set_err(ctx, HYSCO_ERR_ARG, "reps >= 1 and avg_ms[HYSCO_NPROF] required");
+    return ctx->cfg.dtype == HYSCO_F64 ? profile_typed<double>(ctx, reps, flush_l2, avg_ms)
+                                       : profile_typed<float>(ctx, reps, flush_l2, avg_ms);
+}
+
+const char* hysco_last_error(hysco_ctx ctx) { return ctx ? ctx->err.c_str() : "NULL context"; }
+
+hysco_status hysco_destroy(hysco_ctx ctx) {
+    if (!ctx) return HYSCO_ERR_ARG;
+    cudaSetDevice(ctx->cfg.device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->exec) cudaGraphExecDestroy(ctx->exec);
+    if (ctx->graph) cudaGraphDestroy(ctx->graph);
+    for (int k = 0; k < NBUF; k++)
+        if (ctx->buf[k]) cudaFree(ctx->buf[k]);
+    for (void* p : {ctx->own_Ip, ctx->own_Im, ctx->own_Tp, ctx->own_Tm, (void*)ctx->st, (void*)ctx->part,
+                    (void*)ctx->ctr, (void*)ctx->gctr, (void*)ctx->launches, (void*)ctx->dcond})
+        if (p) cudaFree(p);
+    if (ctx->flush) cudaFree(ctx->flush);
+    if (ctx->h_st) cudaFreeHost(ctx->h_st);
+    if (ctx->h_launches) cudaFreeHost(ctx->h_launches);
+    if (ctx->h_cond) cudaFreeHost(ctx->h_cond);
+    if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    cudaGetLastError();
+    delete ctx;
+    return HYSCO_OK;
+}
+
+}  // extern "C"

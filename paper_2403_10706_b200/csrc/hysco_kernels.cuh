@@ -1,0 +1,706 @@
+// hysco_kernels.cuh — sm_100a kernels of the GN-PCG field-map solve.
+//
+// Paper: PAPER.md (arXiv 2403.10706), cited P:<line>; readings R<n> in DESIGN.md.
+// All kernels are HBM/L2-bandwidth-bound stencil, scan and gather work: no
+// dense contraction exists on this path, so there are no tensor-core kernels
+// (DESIGN.md "Roofline").  Reductions are deterministic (pair_reduce).
+#pragma once
+
+#include "hysco_common.cuh"
+
+namespace hysco {
+
+// ---------------------------------------------------------------------------
+// 1D piecewise-linear image model along PE (hat functions, R5)
+// value at u = k + del (index units, centre k at integer k) and the slope per
+// index unit (right-hand at breakpoints).  del is cell-relative (H3 in
+// SURVEY.md): the fractional part is formed from the small displacement, not
+// from an absolute coordinate, which keeps fp32 accurate.
+// ---------------------------------------------------------------------------
+// The interpolated VALUE is always formed in fp64: after a good OT start the
+// residual r = T+ - T- is a small difference of ~1e3-sized values, and an
+// fp32 value costs ~3e-5 relative error in grad J at the 3T shape (DESIGN.md
+// "Precision").  Images stay fp32 in HBM; the slope is returned in T.
+template <typename T>
+__device__ __forceinline__ void interp_from(const T* __restrict__ s, int n3, int kk, T t, double& val, T& slope) {
+    const T v0 = (kk >= 0 && kk < n3) ? s[kk] : T(0);
+    const T v1 = (kk + 1 >= 0 && kk + 1 < n3) ? s[kk + 1] : T(0);
+    const double td = (double)t;
+    val = (1.0 - td) * (double)v0 + td * (double)v1;
+    slope = v1 - v0;
+}
+
+// Query at u = k + sign * Ab / h3 (A b at the cell centre, in voxels).
+// fp32: floor/fraction taken from the small cell-relative offset (accurate t).
+// fp64: from the absolute index coordinate, the oracle's exact arithmetic, so
+// the one-sided slope chosen at an interpolation kink (|offset| below the
+// rounding of k) is the same decision on both sides (R5).
+__device__ __forceinline__ void interp_col(const float* __restrict__ s, int n3, int k, float Ab, float sign,
+                                           const Geom& g, double& val, float& slope) {
+    float del = sign * Ab * (float)g.ih3;
+    del = fminf(fmaxf(del, (float)-(n3 + 2)), (float)(n3 + 2));   // infeasible b can push far out
+    const float fl = floorf(del);
+    interp_from(s, n3, k + (int)fl, del - fl, val, slope);
+}
+__device__ __forceinline__ void interp_col(const double* __restrict__ s, int n3, int k, double Ab, double sign,
+                                           const Geom& g, double& val, double& slope) {
+    double u = (double)k + sign * (Ab / g.h3);
+    u = fmin(fmax(u, -2.0 * (n3 + 2)), 2.0 * (n3 + 2));
+    const double fl = floor(u);
+    interp_from(s, n3, (int)fl, u - fl, val, slope);
+}
+
+// (b_{k+1} - b_k)/h3: fp64 divides like the oracle, fp32 multiplies.
+__device__ __forceinline__ float diff_h3(float b0, float b1, const Geom& g) { return (b1 - b0) * (float)g.ih3; }
+__device__ __forceinline__ double diff_h3(double b0, double b1, const Geom& g) { return (b1 - b0) / g.h3; }
+
+// diag of the in-plane (dims 1,2) Neumann Laplacian at column (i, j) (R3)
+__device__ __forceinline__ double diag_lxy(const Geom& g, int i, int j) {
+    return (double)((i > 0) + (i < g.n1 - 1)) * g.ih1sq + (double)((j > 0) + (j < g.n2 - 1)) * g.ih2sq;
+}
+
+enum { EVAL_PLAIN = 0, EVAL_GN_START = 1, EVAL_TRIAL = 2 };
+
+// ---------------------------------------------------------------------------
+// A4 fused evaluation: one warp per PE column, the
+// column of I+, I-, b staged in shared memory.  Per cell: Ab, Db, both
+// gathers with slopes, residual r, GN Jacobian row (a, c), phi, phi', phi''.
+// Per node: grad J (data + alpha hd L b + barrier), folded tridiagonal
+// Hessian (dt: diagonal incl. alpha hd L_PE; et: super-diagonal incl.
+// -alpha hd / h3^2) — DESIGN.md "Folded GN Hessian".  Scalars D, S, P and
+// ||grad||^2 reduce per pair; TRIAL mode also takes the Armijo decision (R15).
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) eval_kernel(Geom g, Ctl c, SolveParams sp, int mode,
+                                                   const T* __restrict__ Ip, const T* __restrict__ Im,
+                                                   const T* __restrict__ bb, T* __restrict__ grad,
+                                                   T* __restrict__ dt, T* __restrict__ et) {
+    count_launch(c);
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+    const int pair = blockIdx.y;
+    const int n3 = g.n3, P = g.P, n2 = g.n2;
+    T* sIp = reinterpret_cast<T*>(smem_raw) + (size_t)wid * (2 * n3 + P);
+    T* sIm = sIp + n3;
+    T* sb = sIm + n3;
+
+    bool active = true;
+    if (mode == EVAL_TRIAL) active = c.st[pair].ls_active != 0;
+
+    const T* Ipp = Ip + (size_t)pair * g.Nc;
+    const T* Imp = Im + (size_t)pair * g.Nc;
+    const T* bp = bb + (size_t)pair * g.Nn;
+    T* gp = grad + (size_t)pair * g.Nn;
+    T* dp = dt + (size_t)pair * g.Nn;
+    T* ep = et + (size_t)pair * g.Nn;
+
+    const T hd = (T)g.hd, ahd = (T)g.ahd, bh2 = (T)g.bh2;
+    const T ih3 = (T)g.ih3, ih3sq = (T)g.ih3sq, ih1sq = (T)g.ih1sq, ih2sq = (T)g.ih2sq;
+    const long long sI = (long long)n2 * P;   // node stride along dim 1
+
+    double aD = 0, aS = 0, aP = 0, aG = 0, aInf = 0;
+    if (active) {
+        for (long long col = (long long)blockIdx.x * nwb + wid; col < g.ncol; col += (long long)gridDim.x * nwb) {
+            const T* ip = Ipp + col * n3;
+            const T* im = Imp + col * n3;
+            const T* bc = bp + col * P;
+            for (int k = lane; k < n3; k += 32) {
+                sIp[k] = ip[k];
+                sIm[k] = im[k];
+            }
+            for (int l = lane; l < P; l += 32) sb[l] = bc[l];
+            __syncwarp();
+            const int i = (int)(col / n2), j = (int)(col - (long long)i * n2);
+            const bool him = i > 0, hip = i < g.n1 - 1, hjm = j > 0, hjp = j < n2 - 1;
+            T cr_c = 0, c2_c = 0, p1_c = 0, p2_c = 0;   // carry: cell (base-1) -> node base
+            for (int base = 0; base < P; base += 32) {
+                const int l = base + lane;
+                T ar = 0, a2 = 0, cr = 0, c2 = 0, p1 = 0, p2 = 0, ev = 0;
+                if (l < n3) {
+                    const T b0 = sb[l], b1 = sb[l + 1];
+                    const T Ab = T(0.5) * (b0 + b1);          // averaging operator A
+                    const T Db = diff_h3(b0, b1, g);          // finite difference D
+                    double vp, vm;
+                    T spl, sml;
+                    interp_col(sIp, n3, l, Ab, T(1), g, vp, spl);    // I+(x + b)
+                    interp_col(sIm, n3, l, Ab, T(-1), g, vm, sml);   // I-(x - b)
+                    const T opd = T(1) + Db, omd = T(1) - Db;
+                    const double Dbd = (double)Db;
+                    const double rd = vp * (1.0 + Dbd) - vm * (1.0 - Dbd);  // Eq.(1)-(2) residual (fp64)
+                    const T r = (T)rd;
+                    const T gg = (spl * opd + sml * omd) * ih3;
+                    const T s = (T)(vp + vm);
+                    const T a = gg * T(0.5) - s * ih3;        // dr_k/db_k
+                    const T cc = gg * T(0.5) + s * ih3;       // dr_k/db_{k+1}
+                    aD += rd * rd;
+                    const double dd = (double)(b1 - b0);
+                    aS += dd * dd * g.ih3sq;
+                    if (fabs(Db) >= T(1)) {
+                        aInf = 1.0;                           // phi = +inf (Eq.(3))
+                    } else {
+                        const T z2 = Db * Db, om = T(1) - z2;
+                        aP += (double)(z2 * z2 / om);
+                        p1 = T(2) * Db * z2 * (T(2) - z2) / (om * om);
+                        p2 = T(2) * z2 * (T(6) - T(3) * z2 + z2 * z2) / (om * om * om);
+                    }
+                    ar = a * r;
+                    a2 = a * a;
+                    cr = cc * r;
+                    c2 = cc * cc;
+                    ev = hd * a * cc - bh2 * p2 * ih3sq - ahd * ih3sq;
+                }
+                T pcr = __shfl_up_sync(FULL, cr, 1), pc2 = __shfl_up_sync(FULL, c2, 1);
+                T pp1 = __shfl_up_sync(FULL, p1, 1), pp2 = __shfl_up_sync(FULL, p2, 1);
+                if (lane == 0) {
+                    pcr = cr_c;
+                    pc2 = c2_c;
+                    pp1 = p1_c;
+                    pp2 = p2_c;
+                }
+                cr_c = __shfl_sync(FULL, cr, 31);
+                c2_c = __shfl_sync(FULL, c2, 31);
+                p1_c = __shfl_sync(FULL, p1, 31);
+                p2_c = __shfl_sync(FULL, p2, 31);
+                if (l < P) {
+                    const T bl = sb[l];
+                    T lpe = 0, l1 = 0, l2 = 0;
+                    if (l > 0) lpe += bl - sb[l - 1];
+                    if (l < n3) lpe += bl - sb[l + 1];
+                    const T* bn = bc + l;
+                    if (him) l1 += bl - bn[-sI];
+                    if (hip) {
+                        const T v = bn[sI];
+                        l1 += bl - v;
+                        aS += (double)(v - bl) * (double)(v - bl) * g.ih1sq;
+                    }
+                    if (hjm) l2 += bl - bn[-P];
+                    if (hjp) {
+                        const T v = bn[P];
+                        l2 += bl - v;
+                        aS += (double)(v - bl) * (double)(v - bl) * g.ih2sq;
+                    }
+                    const T Lb = lpe * ih3sq + l1 * ih1sq + l2 * ih2sq;
+                    const T gv = hd * (pcr + ar) + ahd * Lb + bh2 * (pp1 - p1) * ih3;
+                    const T dv = hd * (pc2 + a2) + bh2 * (pp2 + p2) * ih3sq + ahd * T((l > 0) + (l < n3)) * ih3sq;
+                    const long long o = col * P + l;
+                    gp[o] = gv;
+                    dp[o] = dv;
+                    ep[o] = (l < n3) ? ev : T(0);
+                    aG += (double)gv * (double)gv;
+                }
+            }
+            __syncwarp();
+        }
+    }
+    double v[5] = {aD, aS, aP, aG, aInf}, tot[5];
+    if (!pair_reduce<5, 0x10u>(c, v, tot)) return;
+    if (threadIdx.x != 0) return;
+    PairState& s = c.st[pair];
+    if (active) {
+        const bool inf = tot[4] > 0.0;
+        s.D = 0.5 * g.hd * tot[0];
+        s.S = 0.5 * g.hd * tot[1];
+        s.P = inf ? INFINITY : 0.5 * g.hd * tot[2];
+        s.infeasible = inf ? 1 : 0;
+        s.J = inf ? INFINITY : s.D + g.alpha * s.S + g.beta * s.P;
+        s.gnorm2 = tot[3];
+    }
+    if (mode == EVAL_GN_START) {
+        s.f_evals = 1;
+        s.h_evals = 0;
+        s.pcg_iters = 0;
+        s.ls_halvings = 0;
+        s.gn_k = 0;
+        s.J_acc = s.J;
+        s.J_prev = s.J;
+        s.g0norm = sqrt(s.gnorm2);
+        s.relres = 0.0;
+        s.stop_reason = s.infeasible ? STOP_INFEASIBLE : STOP_MAXITER;
+        s.gn_active = (!s.infeasible && sp.max_gn > 0) ? 1 : 0;
+        s.pcg_active = 0;
+        s.ls_active = 0;
+        if (last_pair(c)) set_cond(c, COND_GN, any_pair(c, gridDim.y, [](volatile PairState* q) { return q->gn_active != 0; }));
+    } else if (mode == EVAL_TRIAL) {
+        if (active) {
+            if (s.ls_restore) {                       // line search failed: state restored at b_old
+                s.ls_active = 0;
+                s.gn_active = 0;
+            } else {
+                s.f_evals += 1;
+                if (!s.infeasible && (!sp.armijo || s.J <= s.J_acc + sp.c1 * s.gamma * s.gq)) {   // Armijo (R15)
+                    s.J_prev = s.J_acc;
+                    s.J_acc = s.J;
+                    s.gn_k += 1;
+                    s.ls_active = 0;
+                    int stop = -1;
+                    if (!sp.fixed) {                  // R16 stopping rules
+                        if (sqrt(s.gnorm2) <= sp.tol_grad_rel * s.g0norm) stop = STOP_GRAD;
+                        else if (fabs(s.J_prev - s.J) <= sp.tol_dJ_rel * fabs(s.J_prev)) stop = STOP_DJ;
+                        else if (s.gamma * s.qmax <= sp.tol_db_rel * g.h3) stop = STOP_DB;
+                    }
+                    if (stop >= 0) {
+                        s.stop_reason = stop;
+                        s.gn_active = 0;
+                    } else {
+                        s.gn_active = s.gn_k < sp.max_gn ? 1 : 0;
+                    }
+                } else {
+                    s.ls_tries += 1;
+                    if (s.ls_tries < sp.ls_max) {
+                        s.gamma *= 0.5;
+                        s.ls_halvings += 1;
+                    } else {
+                        s.stop_reason = STOP_LSFAIL;
+                        s.ls_restore = 1;             // next pass: b = b_old, re-evaluate, stop
+                    }
+                }
+            }
+        }
+        if (last_pair(c)) set_cond(c, COND_LS, any_pair(c, gridDim.y, [](volatile PairState* q) { return q->ls_active != 0; }));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// A5 GN Hessian matvec on the folded form:
+//   Hq = tridiag_PE(dt, et) q + alpha hd L_xy q     (L_xy: in-plane Neumann)
+// PCG mode also reduces p.Hp and forms alpha_c = (r.z)/(p.Hp) per pair.
+// ---------------------------------------------------------------------------
+template <typename T, bool PCG>
+__global__ void __launch_bounds__(256) matvec_kernel(Geom g, Ctl c, const T* __restrict__ dt,
+                                                     const T* __restrict__ et, const T* __restrict__ q,
+                                                     T* __restrict__ Hq) {
+    count_launch(c);
+    const int pair = blockIdx.y;
+    bool active = true;
+    if (PCG) active = c.st[pair].pcg_active != 0;
+    const size_t po = (size_t)pair * g.Nn;
+    const T* dp = dt + po;
+    const T* ep = et + po;
+    const T* qp = q + po;
+    T* hp = Hq + po;
+    const T ahd = (T)g.ahd, ih1sq = (T)g.ih1sq, ih2sq = (T)g.ih2sq;
+    const long long sI = (long long)g.n2 * g.P;
+    double acc = 0;
+    if (active) {
+        for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < g.Nn;
+             t += (long long)gridDim.x * blockDim.x) {
+            const NodeIdx ix = node_idx(g, t);
+            const T qv = qp[t];
+            T h = dp[t] * qv;
+            if (ix.l > 0) h += ep[t - 1] * qp[t - 1];
+            if (ix.l < g.n3) h += ep[t] * qp[t + 1];
+            T l1 = 0, l2 = 0;
+            if (ix.i > 0) l1 += qv - qp[t - sI];
+            if (ix.i < g.n1 - 1) l1 += qv - qp[t + sI];
+            if (ix.j > 0) l2 += qv - qp[t - g.P];
+            if (ix.j < g.n2 - 1) l2 += qv - qp[t + g.P];
+            h += ahd * (l1 * ih1sq + l2 * ih2sq);
+            hp[t] = h;
+            if (PCG) acc += (double)qv * (double)h;
+        }
+    }
+    if (!PCG) return;
+    double v[1] = {acc}, tot[1];
+    if (!pair_reduce<1, 0u>(c, v, tot)) return;
+    if (threadIdx.x != 0 || !active) return;
+    PairState& s = c.st[pair];
+    if (tot[0] <= 0.0) {          // breakdown: stop PCG, keep x (oracle pcg(): "if pHp <= 0: break")
+        s.alpha_c = 0.0;
+        s.pcg_active = 0;
+    } else {
+        s.alpha_c = s.rz / tot[0];
+        s.h_evals += 1;
+    }
+}
+
+// Jacobi preconditioner M = diag(H_J) = dt + alpha hd diag(L_xy) (R13)
+template <typename T>
+__device__ __forceinline__ T jacobi(const Geom& g, const T* dp, long long t) {
+    const NodeIdx ix = node_idx(g, t);
+    return dp[t] + (T)(g.ahd * diag_lxy(g, ix.i, ix.j));
+}
+
+// PCG start (R14): x = 0, r = -grad, z = r/M, p = z; r.z and r.r per pair.
+template <typename T>
+__global__ void __launch_bounds__(256) pcg_init_kernel(Geom g, Ctl c, const T* __restrict__ grad,
+                                                       const T* __restrict__ dt, T* __restrict__ x,
+                                                       T* __restrict__ r, T* __restrict__ p) {
+    count_launch(c);
+    const int pair = blockIdx.y;
+    const bool active = c.st[pair].gn_active != 0;
+    const size_t po = (size_t)pair * g.Nn;
+    double arz = 0, arr = 0;
+    if (active) {
+        for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < g.Nn;
+             t += (long long)gridDim.x * blockDim.x) {
+            const T rv = -grad[po + t];
+            const T z = rv / jacobi(g, dt + po, t);
+            x[po + t] = T(0);
+            r[po + t] = rv;
+            p[po + t] = z;
+            arz += (double)rv * (double)z;
+            arr += (double)rv * (double)rv;
+        }
+    }
+    double v[2] = {arz, arr}, tot[2];
+    if (!pair_reduce<2, 0u>(c, v, tot)) return;
+    if (threadIdx.x != 0) return;
+    PairState& s = c.st[pair];
+    if (active) {
+        s.rz = tot[0];
+        s.rr0 = tot[1];
+        s.rr = tot[1];
+        s.pcg_k = 0;
+        s.beta_c = 0.0;
+        s.relres = tot[1] > 0.0 ? 1.0 : 0.0;
+        s.pcg_active = tot[1] > 0.0 ? 1 : 0;
+    } else {
+        s.pcg_active = 0;
+    }
+    if (last_pair(c)) set_cond(c, COND_PCG, any_pair(c, gridDim.y, [](volatile PairState* q) { return q->pcg_active != 0; }));
+}
+
+// A6 PCG update: x += a p, r -= a Hp, z = r/M; r.z, r.r; beta; stop test.
+template <typename T>
+__global__ void __launch_bounds__(256) pcg_update_kernel(Geom g, Ctl c, SolveParams sp,
+                                                         const T* __restrict__ dt, const T* __restrict__ p,
+                                                         const T* __restrict__ Hp, T* __restrict__ x,
+                                                         T* __restrict__ r) {
+    count_launch(c);
+    const int pair = blockIdx.y;
+    const bool active = c.st[pair].pcg_active != 0;
+    const T a = (T)c.st[pair].alpha_c;
+    const size_t po = (size_t)pair * g.Nn;
+    double arz = 0, arr = 0;
+    if (active) {
+        for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < g.Nn;
+             t += (long long)gridDim.x * blockDim.x) {
+            const size_t o = po + t;
+            x[o] = x[o] + a * p[o];
+            const T rv = r[o] - a * Hp[o];
+            r[o] = rv;
+            const T z = rv / jacobi(g, dt + po, t);
+            arz += (double)rv * (double)z;
+            arr += (double)rv * (double)rv;
+        }
+    }
+    double v[2] = {arz, arr}, tot[2];
+    if (!pair_reduce<2, 0u>(c, v, tot)) return;
+    if (threadIdx.x != 0) return;
+    PairState& s = c.st[pair];
+    if (active) {
+        s.pcg_k += 1;
+        s.pcg_iters += 1;
+        s.rr = tot[1];
+        s.relres = sqrt(tot[1] / s.rr0);
+        s.beta_c = tot[0] / s.rz;
+        s.rz = tot[0];
+        if (s.pcg_k >= sp.max_pcg || (!sp.fixed && s.relres < sp.pcg_rtol)) s.pcg_active = 0;
+    }
+    if (last_pair(c)) set_cond(c, COND_PCG, any_pair(c, gridDim.y, [](volatile PairState* q) { return q->pcg_active != 0; }));
+}
+
+// New search direction p = z + beta p (z = r/M recomputed, not stored).
+template <typename T>
+__global__ void __launch_bounds__(256) pcg_dir_kernel(Geom g, Ctl c, const T* __restrict__ dt,
+                                                      const T* __restrict__ r, T* __restrict__ p) {
+    count_launch(c);
+    const int pair = blockIdx.y;
+    if (!c.st[pair].pcg_active) return;
+    const T be = (T)c.st[pair].beta_c;
+    const size_t po = (size_t)pair * g.Nn;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < g.Nn;
+         t += (long long)gridDim.x * blockDim.x) {
+        const size_t o = po + t;
+        p[o] = r[o] / jacobi(g, dt + po, t) + be * p[o];
+    }
+}
+
+// A7 start of the Armijo search: g.q, max|q|, b_old = b, b = b + q (gamma = 1).
+template <typename T>
+__global__ void __launch_bounds__(256) trial_init_kernel(Geom g, Ctl c, const T* __restrict__ grad,
+                                                         const T* __restrict__ q, T* __restrict__ b,
+                                                         T* __restrict__ bold) {
+    count_launch(c);
+    const int pair = blockIdx.y;
+    const bool active = c.st[pair].gn_active != 0;
+    const size_t po = (size_t)pair * g.Nn;
+    double agq = 0, aqm = 0;
+    if (active) {
+        for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < g.Nn;
+             t += (long long)gridDim.x * blockDim.x) {
+            const size_t o = po + t;
+            const T qv = q[o];
+            agq += (double)grad[o] * (double)qv;
+            aqm = fmax(aqm, (double)fabs(qv));
+            const T bv = b[o];
+            bold[o] = bv;
+            b[o] = bv + qv;
+        }
+    }
+    double v[2] = {agq, aqm}, tot[2];
+    if (!pair_reduce<2, 0x2u>(c, v, tot)) return;
+    if (threadIdx.x != 0) return;
+    PairState& s = c.st[pair];
+    if (active) {
+        s.gq = tot[0];
+        s.qmax = tot[1];
+        s.gamma = 1.0;
+        s.ls_tries = 0;
+        s.ls_restore = 0;
+        s.ls_active = 1;
+    } else {
+        s.ls_active = 0;
+    }
+    if (last_pair(c)) set_cond(c, COND_LS, any_pair(c, gridDim.y, [](volatile PairState* q2) { return q2->ls_active != 0; }));
+}
+
+// Armijo retry / restore: b = b_old + gamma q, or b = b_old after a failed search.
+template <typename T>
+__global__ void __launch_bounds__(256) ls_retry_kernel(Geom g, Ctl c, const T* __restrict__ q,
+                                                       const T* __restrict__ bold, T* __restrict__ b) {
+    count_launch(c);
+    const int pair = blockIdx.y;
+    const PairState& s = c.st[pair];
+    if (!s.ls_active) return;
+    const bool restore = s.ls_restore != 0;
+    const T gm = (T)s.gamma;
+    const size_t po = (size_t)pair * g.Nn;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < g.Nn;
+         t += (long long)gridDim.x * blockDim.x) {
+        const size_t o = po + t;
+        b[o] = restore ? bold[o] : bold[o] + gm * q[o];
+    }
+}
+
+// End of a GN step: loop condition = any pair still iterating.
+__global__ void gn_tail_kernel(Ctl c, int batch) {
+    count_launch(c);
+    if (threadIdx.x == 0)
+        set_cond(c, COND_GN, any_pair(c, batch, [](volatile PairState* q) { return q->gn_active != 0; }));
+}
+
+// diag(H_J) output for hysco_hess_diag.
+template <typename T>
+__global__ void hess_diag_kernel(Geom g, Ctl c, const T* __restrict__ dt, T* __restrict__ out) {
+    count_launch(c);
+    const size_t po = (size_t)blockIdx.y * g.Nn;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < g.Nn;
+         t += (long long)gridDim.x * blockDim.x)
+        out[po + t] = jacobi(g, dt + po, t);
+}
+
+// ---------------------------------------------------------------------------
+// A9 Jacobian-modulation correction: T+ = I+(x+b)(1+Db), T- = I-(x-b)(1-Db)
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) apply_kernel(Geom g, Ctl c, const T* __restrict__ Ip,
+                                                    const T* __restrict__ Im, const T* __restrict__ bb,
+                                                    T* __restrict__ Tp, T* __restrict__ Tm) {
+    count_launch(c);
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+    const int pair = blockIdx.y;
+    const int n3 = g.n3, P = g.P;
+    T* sIp = reinterpret_cast<T*>(smem_raw) + (size_t)wid * (2 * n3 + P);
+    T* sIm = sIp + n3;
+    T* sb = sIm + n3;
+    const size_t pc = (size_t)pair * g.Nc, pn = (size_t)pair * g.Nn;
+    for (long long col = (long long)blockIdx.x * nwb + wid; col < g.ncol; col += (long long)gridDim.x * nwb) {
+        const size_t oc = pc + col * n3, on = pn + col * P;
+        for (int k = lane; k < n3; k += 32) {
+            sIp[k] = Ip[oc + k];
+            sIm[k] = Im[oc + k];
+        }
+        for (int l = lane; l < P; l += 32) sb[l] = bb[on + l];
+        __syncwarp();
+        for (int k = lane; k < n3; k += 32) {
+            const T b0 = sb[k], b1 = sb[k + 1];
+            const T Db = diff_h3(b0, b1, g);
+            const T Ab = T(0.5) * (b0 + b1);
+            double vp, vm;
+            T sp, sm;
+            interp_col(sIp, n3, k, Ab, T(1), g, vp, sp);
+            interp_col(sIm, n3, k, Ab, T(-1), g, vm, sm);
+            if (Tp) Tp[oc + k] = (T)(vp * (double)(T(1) + Db));
+            if (Tm) Tm[oc + k] = (T)(vm * (double)(T(1) - Db));
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// A1 OT initialisation
+// ---------------------------------------------------------------------------
+
+// Positivity shift (R6): per pair, min/max over I+ and I-.
+template <typename T>
+__global__ void __launch_bounds__(256) ot_minmax_kernel(Geom g, Ctl c, SolveParams sp, const T* __restrict__ Ip,
+                                                        const T* __restrict__ Im) {
+    count_launch(c);
+    const int pair = blockIdx.y;
+    const size_t pc = (size_t)pair * g.Nc;
+    double mn = -INFINITY, mx = -INFINITY;   // max of (-v) and max of v
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < g.Nc;
+         t += (long long)gridDim.x * blockDim.x) {
+        const double a = (double)Ip[pc + t], b = (double)Im[pc + t];
+        mn = fmax(mn, fmax(-a, -b));
+        mx = fmax(mx, fmax(a, b));
+    }
+    double v[2] = {mn, mx}, tot[2];
+    if (!pair_reduce<2, 0x3u>(c, v, tot)) return;
+    if (threadIdx.x != 0) return;
+    PairState& s = c.st[pair];
+    s.vmin = -tot[0];
+    s.vmax = tot[1];
+    s.degenerate = (s.vmax == s.vmin) ? 1 : 0;
+    s.shift = -s.vmin + sp.ot_eps * (s.vmax - s.vmin);
+}
+
+// Pseudo-inverse of a piecewise-linear CDF (R8):
+// Q(r) = 0 for r <= 0, else x* = min{x in 1..m : C(x) >= r} and
+// Q(r) = x* - 1 + (r - C(x*-1)) / (C(x*) - C(x*-1)).
+__device__ __forceinline__ double ot_quantile(const double* __restrict__ C, int m, double r) {
+    if (r <= 0.0) return 0.0;
+    int lo = 1, hi = m;                 // C[m] = 1 >= r
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (C[mid] >= r) hi = mid;
+        else lo = mid + 1;
+    }
+    return (double)(lo - 1) + (r - C[lo - 1]) / (C[lo] - C[lo - 1]);
+}
+
+// One warp per PE column: fp64 warp-scan CDFs of the shifted, unit-mass
+// columns (R7), quantile search, b0 = h3 (T- - T+)/2 (R9).
+template <typename T>
+__global__ void __launch_bounds__(256) ot_column_kernel(Geom g, Ctl c, const T* __restrict__ Ip,
+                                                        const T* __restrict__ Im, T* __restrict__ b0) {
+    count_launch(c);
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+    const int pair = blockIdx.y;
+    const int n3 = g.n3, P = g.P;
+    double* Cp = reinterpret_cast<double*>(smem_raw) + (size_t)wid * 2 * P;
+    double* Cm = Cp + P;
+    const size_t pc = (size_t)pair * g.Nc, pn = (size_t)pair * g.Nn;
+    const double shift = c.st[pair].shift;
+    const bool degen = c.st[pair].degenerate != 0;
+    for (long long col = (long long)blockIdx.x * nwb + wid; col < g.ncol; col += (long long)gridDim.x * nwb) {
+        const T* ip = Ip + pc + col * n3;
+        const T* im = Im + pc + col * n3;
+        T* bo = b0 + pn + col * P;
+        if (degen) {
+            for (int l = lane; l < P; l += 32) bo[l] = T(0);
+            continue;
+        }
+        double tp = 0, tm = 0;
+        for (int k = lane; k < n3; k += 32) {
+            tp += (double)ip[k] + shift;
+            tm += (double)im[k] + shift;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            tp += __shfl_xor_sync(FULL, tp, o);
+            tm += __shfl_xor_sync(FULL, tm, o);
+        }
+        double carp = 0, carm = 0;
+        for (int base = 0; base < n3; base += 32) {
+            const int k = base + lane;
+            double wp = 0, wm = 0;
+            if (k < n3) {
+                wp = ((double)ip[k] + shift) / tp;
+                wm = ((double)im[k] + shift) / tm;
+            }
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double up = __shfl_up_sync(FULL, wp, o), um = __shfl_up_sync(FULL, wm, o);
+                if (lane >= o) {
+                    wp += up;
+                    wm += um;
+                }
+            }
+            if (k < n3) {
+                Cp[k + 1] = carp + wp;
+                Cm[k + 1] = carm + wm;
+            }
+            carp += __shfl_sync(FULL, wp, 31);
+            carm += __shfl_sync(FULL, wm, 31);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            Cp[0] = 0.0;
+            Cm[0] = 0.0;
+            Cp[n3] = 1.0;
+            Cm[n3] = 1.0;
+        }
+        __syncwarp();
+        for (int l = lane; l < P; l += 32) {
+            const double rp = Cp[l], rm = Cm[l];
+            const double Tpl = 0.5 * (ot_quantile(Cp, n3, rp) + ot_quantile(Cm, n3, rp));   // T+ = Q_half o C+
+            const double Tml = 0.5 * (ot_quantile(Cp, n3, rm) + ot_quantile(Cm, n3, rm));   // T- = Q_half o C-
+            bo[l] = (T)(g.h3 * (Tml - Tpl) * 0.5);
+        }
+        __syncwarp();
+    }
+}
+
+// 3-tap periodic Gaussian along one axis of the node array (R11).
+template <typename T>
+__global__ void __launch_bounds__(256) blur_axis_kernel(Geom g, Ctl c, int axis, double w0, double w1,
+                                                        const T* __restrict__ in, T* __restrict__ out) {
+    count_launch(c);
+    const size_t po = (size_t)blockIdx.y * g.Nn;
+    const T a = (T)w0, m = (T)w1;
+    const long long sI = (long long)g.n2 * g.P;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < g.Nn;
+         t += (long long)gridDim.x * blockDim.x) {
+        const NodeIdx ix = node_idx(g, t);
+        long long tm, tp;
+        if (axis == 0) {
+            tm = t + (long long)(((ix.i + g.n1 - 1) % g.n1) - ix.i) * sI;
+            tp = t + (long long)(((ix.i + 1) % g.n1) - ix.i) * sI;
+        } else if (axis == 1) {
+            tm = t + (long long)(((ix.j + g.n2 - 1) % g.n2) - ix.j) * g.P;
+            tp = t + (long long)(((ix.j + 1) % g.n2) - ix.j) * g.P;
+        } else {
+            tm = t + (((ix.l + g.P - 1) % g.P) - ix.l);
+            tp = t + (((ix.l + 1) % g.P) - ix.l);
+        }
+        out[po + t] = a * in[po + tm] + m * in[po + t] + a * in[po + tp];
+    }
+}
+
+// Feasibility guard (R10): max |Db| per pair; scale to feas_cap if reached.
+template <typename T>
+__global__ void __launch_bounds__(256) guard_max_kernel(Geom g, Ctl c, SolveParams sp, const T* __restrict__ b) {
+    count_launch(c);
+    const int pair = blockIdx.y;
+    const size_t po = (size_t)pair * g.Nn;
+    double mx = 0.0;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < g.Nn;
+         t += (long long)gridDim.x * blockDim.x) {
+        const long long l = t % g.P;
+        if (l < g.n3) mx = fmax(mx, fabs((double)(b[po + t + 1] - b[po + t])) / g.h3);
+    }
+    double v[1] = {mx}, tot[1];
+    if (!pair_reduce<1, 0x1u>(c, v, tot)) return;
+    if (threadIdx.x != 0) return;
+    PairState& s = c.st[pair];
+    s.maxDb = tot[0];
+    s.scale = (tot[0] >= sp.feas_cap) ? sp.feas_cap / tot[0] : 1.0;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) guard_scale_kernel(Geom g, Ctl c, T* __restrict__ b) {
+    count_launch(c);
+    const int pair = blockIdx.y;
+    const double sc = c.st[pair].scale;
+    if (sc == 1.0) return;
+    const size_t po = (size_t)pair * g.Nn;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < g.Nn;
+         t += (long long)gridDim.x * blockDim.x)
+        b[po + t] = (T)((double)b[po + t] * sc);
+}
+
+}  // namespace hysco

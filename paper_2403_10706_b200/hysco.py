@@ -1,0 +1,230 @@
+"""Thin ctypes binding of libhysco.so (include/hysco.h) — argument marshalling only.
+
+Every step of the path runs in the CUDA kernels behind the C ABI.  torch is
+used only to hold device memory and streams; there is no CPU fallback: if the
+extension is missing this module raises at import-use time.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libhysco.so")
+
+HYSCO_OK, HYSCO_INFEASIBLE = 0, 1
+HYSCO_ERR_ARG, HYSCO_ERR_SHAPE, HYSCO_ERR_STATE, HYSCO_ERR_CUDA, HYSCO_ERR_NCCL, HYSCO_ERR_NOMEM = -1, -2, -3, -4, -5, -6
+HYSCO_F32, HYSCO_F64 = 0, 1
+STOP_NAMES = {0: "maxiter", 1: "grad", 2: "dJ", 3: "db", 4: "ls_fail", 5: "infeasible"}
+
+EXPORTED = ["hysco_default_solve_opts", "hysco_default_ot_opts", "hysco_create", "hysco_bind_images",
+            "hysco_ot_init", "hysco_objective_grad", "hysco_hessvec", "hysco_hess_diag", "hysco_solve",
+            "hysco_apply", "hysco_correct", "hysco_correct_host", "hysco_last_launch_count",
+            "hysco_last_error", "hysco_destroy", "hysco_version", "hysco_profile_kernels"]
+PROF_NAMES = ["matvec", "pcg_update", "pcg_dir", "eval"]
+
+
+class HyscoError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"hysco status {status}: {msg}")
+        self.status = status
+
+
+class hysco_config(ctypes.Structure):
+    _fields_ = [("n1", ctypes.c_int64), ("n2", ctypes.c_int64), ("n3", ctypes.c_int64),
+                ("batch", ctypes.c_int64), ("h1", ctypes.c_double), ("h2", ctypes.c_double),
+                ("h3", ctypes.c_double), ("alpha", ctypes.c_double), ("beta", ctypes.c_double),
+                ("dtype", ctypes.c_int32), ("device", ctypes.c_int32)]
+
+
+class hysco_ot_opts(ctypes.Structure):
+    _fields_ = [("eps", ctypes.c_double), ("blur", ctypes.c_int32), ("feas_cap", ctypes.c_double)]
+
+
+class hysco_solve_opts(ctypes.Structure):
+    _fields_ = [("max_gn", ctypes.c_int32), ("max_pcg", ctypes.c_int32), ("pcg_rtol", ctypes.c_double),
+                ("fixed_iters", ctypes.c_int32), ("ls_max", ctypes.c_int32), ("armijo_c1", ctypes.c_double),
+                ("tol_grad_rel", ctypes.c_double), ("tol_dJ_rel", ctypes.c_double),
+                ("tol_db_rel", ctypes.c_double), ("armijo", ctypes.c_int32)]
+
+
+class hysco_report(ctypes.Structure):
+    _fields_ = [("gn_iters", ctypes.c_int32), ("f_evals", ctypes.c_int32), ("h_evals", ctypes.c_int32),
+                ("pcg_iters", ctypes.c_int32), ("stop_reason", ctypes.c_int32), ("ls_halvings", ctypes.c_int32),
+                ("J", ctypes.c_double), ("D", ctypes.c_double), ("S", ctypes.c_double), ("P", ctypes.c_double),
+                ("grad_norm", ctypes.c_double), ("last_relres", ctypes.c_double)]
+
+    def as_dict(self):
+        d = {k: getattr(self, k) for k, _ in self._fields_}
+        d["stop"] = STOP_NAMES.get(self.stop_reason, "?")
+        return d
+
+
+_lib = None
+
+
+def lib():
+    """Load the in-tree libhysco.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2403_10706_b200.build` "
+                          "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, st = ctypes.c_void_p, ctypes.c_int
+    L.hysco_default_solve_opts.argtypes = [ctypes.POINTER(hysco_solve_opts)]
+    L.hysco_default_solve_opts.restype = None
+    L.hysco_default_ot_opts.argtypes = [ctypes.POINTER(hysco_ot_opts)]
+    L.hysco_default_ot_opts.restype = None
+    L.hysco_create.argtypes = [ctypes.POINTER(hysco_config), vp, ctypes.POINTER(vp)]
+    L.hysco_bind_images.argtypes = [vp, vp, vp]
+    L.hysco_ot_init.argtypes = [vp, ctypes.POINTER(hysco_ot_opts), vp]
+    L.hysco_objective_grad.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_double), vp]
+    L.hysco_hessvec.argtypes = [vp, vp, vp]
+    L.hysco_hess_diag.argtypes = [vp, vp]
+    L.hysco_solve.argtypes = [vp, vp, ctypes.POINTER(hysco_solve_opts), ctypes.POINTER(hysco_report)]
+    L.hysco_apply.argtypes = [vp, vp, vp, vp]
+    L.hysco_correct.argtypes = [vp, ctypes.POINTER(hysco_ot_opts), ctypes.POINTER(hysco_solve_opts), vp, vp, vp,
+                                ctypes.POINTER(hysco_report)]
+    L.hysco_correct_host.argtypes = [vp, vp, vp, ctypes.POINTER(hysco_ot_opts), ctypes.POINTER(hysco_solve_opts),
+                                     vp, vp, vp, ctypes.POINTER(hysco_report)]
+    for f in ("hysco_create", "hysco_bind_images", "hysco_ot_init", "hysco_objective_grad", "hysco_hessvec",
+              "hysco_hess_diag", "hysco_solve", "hysco_apply", "hysco_correct", "hysco_correct_host",
+              "hysco_destroy"):
+        getattr(L, f).restype = st
+    L.hysco_destroy.argtypes = [vp]
+    L.hysco_last_launch_count.argtypes = [vp]
+    L.hysco_last_launch_count.restype = ctypes.c_int64
+    L.hysco_last_error.argtypes = [vp]
+    L.hysco_last_error.restype = ctypes.c_char_p
+    L.hysco_profile_kernels.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_double)]
+    L.hysco_profile_kernels.restype = st
+    L.hysco_version.argtypes = []
+    L.hysco_version.restype = ctypes.c_int32
+    _lib = L
+    return L
+
+
+def _ptr(t):
+    """Device/host pointer of a torch tensor or numpy array (must be contiguous)."""
+    if t is None:
+        return None
+    if isinstance(t, np.ndarray):
+        assert t.flags["C_CONTIGUOUS"]
+        return t.ctypes.data
+    assert t.is_contiguous(), "tensors must be C-contiguous"
+    return t.data_ptr()
+
+
+def _check(ctx, s, ok=(HYSCO_OK,)):
+    if s not in ok:
+        msg = lib().hysco_last_error(ctx).decode() if ctx else ""
+        raise HyscoError(s, msg)
+    return s
+
+
+def default_solve_opts(**kw):
+    o = hysco_solve_opts()
+    lib().hysco_default_solve_opts(ctypes.byref(o))
+    for k, v in kw.items():
+        setattr(o, k, v)
+    return o
+
+
+def default_ot_opts(**kw):
+    o = hysco_ot_opts()
+    lib().hysco_default_ot_opts(ctypes.byref(o))
+    for k, v in kw.items():
+        setattr(o, k, v)
+    return o
+
+
+# ---- C-ABI mirrors (same names) -------------------------------------------
+
+def hysco_create(shape, h, batch=1, alpha=300.0, beta=1e-4, dtype=HYSCO_F32, device=0, stream=None):
+    cfg = hysco_config(int(shape[0]), int(shape[1]), int(shape[2]), int(batch), float(h[0]), float(h[1]),
+                       float(h[2]), float(alpha), float(beta), int(dtype), int(device))
+    out = ctypes.c_void_p()
+    s = lib().hysco_create(ctypes.byref(cfg), stream, ctypes.byref(out))
+    if s != HYSCO_OK:
+        raise HyscoError(s, "hysco_create failed")
+    return out.value
+
+
+def hysco_bind_images(ctx, Ip, Im):
+    _check(ctx, lib().hysco_bind_images(ctx, _ptr(Ip), _ptr(Im)))
+
+
+def hysco_ot_init(ctx, b_out, opts=None):
+    _check(ctx, lib().hysco_ot_init(ctx, ctypes.byref(opts) if opts is not None else None, _ptr(b_out)))
+
+
+def hysco_objective_grad(ctx, b, grad_out=None, batch=1):
+    jdsp = (ctypes.c_double * (4 * batch))()
+    s = _check(ctx, lib().hysco_objective_grad(ctx, _ptr(b), jdsp, _ptr(grad_out)), (HYSCO_OK, HYSCO_INFEASIBLE))
+    return np.array(jdsp[:]).reshape(batch, 4), s == HYSCO_INFEASIBLE
+
+
+def hysco_hessvec(ctx, q, Hq_out):
+    _check(ctx, lib().hysco_hessvec(ctx, _ptr(q), _ptr(Hq_out)))
+
+
+def hysco_hess_diag(ctx, diag_out):
+    _check(ctx, lib().hysco_hess_diag(ctx, _ptr(diag_out)))
+
+
+def hysco_solve(ctx, b_inout, opts=None, batch=1):
+    reps = (hysco_report * batch)()
+    s = _check(ctx, lib().hysco_solve(ctx, _ptr(b_inout), ctypes.byref(opts) if opts is not None else None, reps),
+               (HYSCO_OK, HYSCO_INFEASIBLE))
+    return [r.as_dict() for r in reps], s == HYSCO_INFEASIBLE
+
+
+def hysco_apply(ctx, b, Ip_corr, Im_corr):
+    _check(ctx, lib().hysco_apply(ctx, _ptr(b), _ptr(Ip_corr), _ptr(Im_corr)))
+
+
+def hysco_correct(ctx, b_out=None, Ip_corr=None, Im_corr=None, ot_opts=None, solve_opts=None, batch=1):
+    reps = (hysco_report * batch)()
+    s = _check(ctx, lib().hysco_correct(ctx, ctypes.byref(ot_opts) if ot_opts is not None else None,
+                                        ctypes.byref(solve_opts) if solve_opts is not None else None,
+                                        _ptr(b_out), _ptr(Ip_corr), _ptr(Im_corr), reps),
+               (HYSCO_OK, HYSCO_INFEASIBLE))
+    return [r.as_dict() for r in reps], s == HYSCO_INFEASIBLE
+
+
+def hysco_correct_host(ctx, Ip, Im, b_out=None, Ip_corr=None, Im_corr=None, ot_opts=None, solve_opts=None,
+                       batch=1):
+    reps = (hysco_report * batch)()
+    s = _check(ctx, lib().hysco_correct_host(ctx, _ptr(Ip), _ptr(Im),
+                                             ctypes.byref(ot_opts) if ot_opts is not None else None,
+                                             ctypes.byref(solve_opts) if solve_opts is not None else None,
+                                             _ptr(b_out), _ptr(Ip_corr), _ptr(Im_corr), reps),
+               (HYSCO_OK, HYSCO_INFEASIBLE))
+    return [r.as_dict() for r in reps], s == HYSCO_INFEASIBLE
+
+
+def hysco_last_launch_count(ctx):
+    return int(lib().hysco_last_launch_count(ctx))
+
+
+def hysco_profile_kernels(ctx, reps=20, flush_l2=True):
+    out = (ctypes.c_double * len(PROF_NAMES))()
+    _check(ctx, lib().hysco_profile_kernels(ctx, int(reps), int(bool(flush_l2)), out))
+    return dict(zip(PROF_NAMES, out[:]))
+
+
+def hysco_last_error(ctx):
+    return lib().hysco_last_error(ctx).decode()
+
+
+def hysco_destroy(ctx):
+    if ctx:
+        lib().hysco_destroy(ctx)
+
+
+def hysco_version():
+    return int(lib().hysco_version())

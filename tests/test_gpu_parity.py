@@ -1,0 +1,364 @@
+"""GPU parity: libhysco (CUDA, through the C ABI) vs the CPU fp64 oracle.
+
+Both sides read the same seeded fp32 (or fp64) inputs from synth/.  Metric
+(R18): relative L2 error per output array, relative error per scalar.
+Tolerances (BASELINE.json north_star):
+  fp32 kernels <= 1e-5, fp32 field map / corrected images after fixed
+  10 GN x 10 PCG <= 1e-4; fp64 build: kernels <= 1e-11, solve <= 1e-9.
+"""
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import hysco_oracle as O          # noqa: E402
+from paper_2403_10706_b200 import hysco as H  # noqa: E402
+from synth import phantom                      # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda:0"
+# fp64 OT: the quantile's slope is 1/(cell mass), ~1e4-1e5 for cells near the
+# positivity shift, so a different (equally valid) summation order of the
+# prefix sums moves b0 by ~1e-11 relative: gate at 1e-9.
+TOL = {H.HYSCO_F32: dict(kernel=1e-5, solve=1e-4, ot=1e-5),
+       H.HYSCO_F64: dict(kernel=1e-11, solve=1e-9, ot=1e-9)}
+TD = {H.HYSCO_F32: torch.float32, H.HYSCO_F64: torch.float64}
+ND = {H.HYSCO_F32: np.float32, H.HYSCO_F64: np.float64}
+
+
+def rel(a, ref):
+    a = np.asarray(a, np.float64)
+    ref = np.asarray(ref, np.float64)
+    n = np.linalg.norm(ref)
+    return np.linalg.norm(a - ref) / (n if n > 0 else 1.0)
+
+
+def relS(a, ref):
+    return abs(a - ref) / max(abs(ref), 1e-300)
+
+
+class Ctx:
+    """One libhysco context over a batch of pairs (inputs already rounded to dtype)."""
+
+    def __init__(self, Ips, Ims, h, dtype=H.HYSCO_F32, alpha=300.0, beta=1e-4):
+        self.dtype = dtype
+        self.shape = Ips[0].shape
+        self.batch = len(Ips)
+        self.h = h
+        self.Ip = torch.from_numpy(np.stack(Ips).astype(ND[dtype])).to(DEV)
+        self.Im = torch.from_numpy(np.stack(Ims).astype(ND[dtype])).to(DEV)
+        self.ctx = H.hysco_create(self.shape, h, self.batch, alpha, beta, dtype=dtype)
+        H.hysco_bind_images(self.ctx, self.Ip, self.Im)
+
+    def nodes(self, a=None):
+        n1, n2, n3 = self.shape
+        if a is None:
+            return torch.zeros((self.batch, n1, n2, n3 + 1), dtype=TD[self.dtype], device=DEV)
+        return torch.from_numpy(np.ascontiguousarray(np.asarray(a).reshape(self.batch, n1, n2, n3 + 1))
+                                .astype(ND[self.dtype])).to(DEV)
+
+    def cells(self):
+        return torch.zeros((self.batch,) + tuple(self.shape), dtype=TD[self.dtype], device=DEV)
+
+    def close(self):
+        H.hysco_destroy(self.ctx)
+
+    @staticmethod
+    def np(t):
+        return t.detach().cpu().numpy().astype(np.float64)
+
+
+def rnd(x, dtype):
+    return np.asarray(x).astype(ND[dtype]).astype(np.float64)
+
+
+def ls_mode(dtype):
+    """Armijo's accept test compares J values whose difference falls below fp32
+    resolution in late fixed-count GN steps, so fp32 parity runs use the
+    full-step-unless-infeasible mode on BOTH sides (R15 parity mode); the fp64
+    build keeps Armijo and must take the same decisions as the oracle."""
+    return 1 if dtype == H.HYSCO_F64 else 0
+
+
+SHAPES = [
+    ("C1", (16, 16, 8), (1.25, 1.25, 1.25), 0),
+    ("ragged", (5, 7, 37), (1.1, 0.9, 1.3), 5),      # n3+1 not a multiple of 32, odd everything
+    ("col", (1, 3, 70), (1.0, 2.0, 1.5), 6),        # n1 = 1 (no dim-1 neighbours), 3 chunks of 32
+]
+
+
+@pytest.fixture(scope="module", params=SHAPES, ids=[s[0] for s in SHAPES])
+def pair(request):
+    _, shape, h, seed = request.param
+    p = phantom.make_pair(shape, h, seed)
+    return p
+
+
+@pytest.mark.parametrize("dtype", [H.HYSCO_F32, H.HYSCO_F64], ids=["f32", "f64"])
+@pytest.mark.parametrize("blur", [0, 1])
+def test_ot_init_parity(pair, dtype, blur):
+    Ip, Im = rnd(pair.Ip, dtype), rnd(pair.Im, dtype)
+    c = Ctx([Ip], [Im], pair.h, dtype)
+    b = c.nodes()
+    H.hysco_ot_init(c.ctx, b, H.default_ot_opts(blur=blur))
+    ref, _ = O.ot_init(Ip, Im, pair.h[2], blur=bool(blur))
+    assert rel(c.np(b)[0], ref) <= TOL[dtype]["ot"]
+    c.close()
+
+
+@pytest.mark.parametrize("dtype", [H.HYSCO_F32, H.HYSCO_F64], ids=["f32", "f64"])
+@pytest.mark.parametrize("where", ["ot", "random"])
+def test_objective_gradient_hessian_parity(pair, dtype, where):
+    Ip, Im = rnd(pair.Ip, dtype), rnd(pair.Im, dtype)
+    n1, n2, n3 = pair.Ip.shape
+    if where == "ot":
+        b, _ = O.ot_init(Ip, Im, pair.h[2])
+    else:
+        b = phantom.random_feasible_b(pair.Ip.shape, pair.h[2], seed=42)
+    b = rnd(b, dtype)
+    c = Ctx([Ip], [Im], pair.h, dtype)
+    g = c.nodes()
+    jdsp, inf = H.hysco_objective_grad(c.ctx, c.nodes(b), g)
+    assert not inf
+    st = O.evaluate(Ip, Im, b, pair.h)
+    tol = TOL[dtype]["kernel"]
+    for k, name in enumerate("JDSP"):
+        assert relS(jdsp[0, k], getattr(st, name)) <= tol, name
+    assert rel(c.np(g)[0], st.grad) <= tol
+    q = np.random.default_rng(3).standard_normal(b.shape)
+    q = rnd(q, dtype)
+    Hq = c.nodes()
+    H.hysco_hessvec(c.ctx, c.nodes(q), Hq)
+    assert rel(c.np(Hq)[0], O.hessvec(st, q)) <= tol
+    d = c.nodes()
+    H.hysco_hess_diag(c.ctx, d)
+    assert rel(c.np(d)[0], O.hess_diag(st)) <= tol
+    c.close()
+
+
+@pytest.mark.parametrize("dtype", [H.HYSCO_F32, H.HYSCO_F64], ids=["f32", "f64"])
+def test_apply_parity(pair, dtype):
+    Ip, Im = rnd(pair.Ip, dtype), rnd(pair.Im, dtype)
+    b = rnd(phantom.random_feasible_b(pair.Ip.shape, pair.h[2], seed=7, amp=0.5), dtype)
+    c = Ctx([Ip], [Im], pair.h, dtype)
+    Tp, Tm = c.cells(), c.cells()
+    H.hysco_apply(c.ctx, c.nodes(b), Tp, Tm)
+    rp, rm = O.apply_correction(Ip, Im, b, pair.h[2])
+    assert rel(c.np(Tp)[0], rp) <= TOL[dtype]["kernel"]
+    assert rel(c.np(Tm)[0], rm) <= TOL[dtype]["kernel"]
+    c.close()
+
+
+@pytest.mark.parametrize("dtype", [H.HYSCO_F32, H.HYSCO_F64], ids=["f32", "f64"])
+def test_solve_fixed_parity(pair, dtype):
+    """Fixed 10 GN x 10 PCG from the same b0: field map and objective (BASELINE configs[0])."""
+    Ip, Im = rnd(pair.Ip, dtype), rnd(pair.Im, dtype)
+    b0, _ = O.ot_init(Ip, Im, pair.h[2])
+    b0 = rnd(b0, dtype)
+    c = Ctx([Ip], [Im], pair.h, dtype)
+    b = c.nodes(b0)
+    reps, inf = H.hysco_solve(c.ctx, b, H.default_solve_opts(armijo=ls_mode(dtype)))
+    assert not inf
+    bref, st, rep = O.gauss_newton(Ip, Im, b0, pair.h, fixed=True, armijo=bool(ls_mode(dtype)))
+    r = reps[0]
+    assert (r["gn_iters"], r["pcg_iters"], r["h_evals"], r["f_evals"], r["ls_halvings"]) == \
+        (rep["gn_iters"], rep["pcg_iters"], rep["h_evals"], rep["f_evals"], rep["ls_halvings"])
+    assert rel(c.np(b)[0], bref) <= TOL[dtype]["solve"]
+    assert relS(r["J"], rep["J"]) <= TOL[dtype]["solve"]
+    c.close()
+
+
+@pytest.mark.parametrize("dtype", [H.HYSCO_F32, H.HYSCO_F64], ids=["f32", "f64"])
+def test_correct_pipeline_parity(pair, dtype):
+    """The whole path: OT + blur + guard -> 10x10 GN-PCG -> apply."""
+    Ip, Im = rnd(pair.Ip, dtype), rnd(pair.Im, dtype)
+    c = Ctx([Ip], [Im], pair.h, dtype)
+    b, Tp, Tm = c.nodes(), c.cells(), c.cells()
+    reps, inf = H.hysco_correct(c.ctx, b, Tp, Tm, solve_opts=H.default_solve_opts(armijo=ls_mode(dtype)))
+    assert not inf
+    b0r, bref, Tpr, Tmr, rep = O.correct_pair(Ip, Im, pair.h, armijo=bool(ls_mode(dtype)))
+    assert reps[0]["ls_halvings"] == rep["ls_halvings"]
+    tol = TOL[dtype]["solve"]
+    assert rel(c.np(b)[0], bref) <= tol
+    assert rel(c.np(Tp)[0], Tpr) <= tol and rel(c.np(Tm)[0], Tmr) <= tol
+    n = H.hysco_last_launch_count(c.ctx)
+    # 7 OT kernels + 1 eval + 10 x (pcg_init + 10 x 3 + trial_init + eval + retry + tail) + apply
+    assert n == 7 + 1 + 10 * (1 + 30 + 1 + 2 + 1) + 1 + 2 * reps[0]["ls_halvings"]
+    c.close()
+
+
+def test_batch_pairs_independent():
+    pairs = [phantom.make_pair((6, 5, 24), (1.2, 1.0, 1.1), 100 + k) for k in range(3)]
+    c = Ctx([p.Ip for p in pairs], [p.Im for p in pairs], pairs[0].h)
+    b, Tp, Tm = c.nodes(), c.cells(), c.cells()
+    reps, inf = H.hysco_correct(c.ctx, b, Tp, Tm, batch=3, solve_opts=H.default_solve_opts(armijo=0))
+    for k, p in enumerate(pairs):
+        _, bref, Tpr, _, rep = O.correct_pair(p.Ip.astype(np.float64), p.Im.astype(np.float64), p.h,
+                                              armijo=False)
+        assert rel(c.np(b)[k], bref) <= 1e-4
+        assert rel(c.np(Tp)[k], Tpr) <= 1e-4
+        assert reps[k]["gn_iters"] == 10
+    c.close()
+
+
+@pytest.mark.parametrize("dtype", [H.HYSCO_F64])
+def test_production_mode_decisions_match(dtype):
+    """Paper stop rules (PCG rtol 0.1, R16 GN tests): same decisions in fp64."""
+    p = phantom.make_pair((12, 10, 32), (1.25, 1.25, 1.25), 9)
+    Ip, Im = p.Ip.astype(np.float64), p.Im.astype(np.float64)
+    b0, _ = O.ot_init(Ip, Im, p.h[2])
+    c = Ctx([Ip], [Im], p.h, dtype)
+    b = c.nodes(b0)
+    so = H.default_solve_opts(fixed_iters=0, max_gn=30)
+    reps, _ = H.hysco_solve(c.ctx, b, so)
+    bref, st, rep = O.gauss_newton(Ip, Im, b0, p.h, max_gn=30, fixed=False)
+    r = reps[0]
+    assert r["stop_reason"] == rep["stop_reason"]
+    assert (r["gn_iters"], r["pcg_iters"], r["f_evals"]) == (rep["gn_iters"], rep["pcg_iters"], rep["f_evals"])
+    assert r["pcg_iters"] < 10 * r["gn_iters"]          # early PCG stops actually happened
+    assert rel(c.np(b)[0], bref) <= 1e-9
+    c.close()
+
+
+def test_identical_images_and_constant_images():
+    I = phantom.make_pair((6, 6, 16), (1, 1, 1), 3).Ip
+    c = Ctx([I], [I], (1.0, 1.0, 1.0))
+    b, Tp, Tm = c.nodes(), c.cells(), c.cells()
+    reps, inf = H.hysco_correct(c.ctx, b, Tp, Tm)
+    assert not inf and np.all(c.np(b) == 0) and reps[0]["J"] == 0
+    assert np.array_equal(c.np(Tp)[0], I.astype(np.float64))
+    c.close()
+    K = np.full((4, 4, 8), 3.0, np.float32)
+    c = Ctx([K], [K], (1.0, 1.0, 1.0))
+    b = c.nodes(np.ones((4, 4, 9)))
+    H.hysco_ot_init(c.ctx, b)
+    assert np.all(c.np(b) == 0)
+    c.close()
+
+
+def test_infeasible_and_state_errors():
+    p = phantom.make_pair((4, 4, 8), (1, 1, 1), 1)
+    c = Ctx([p.Ip], [p.Im], (1.0, 1.0, 1.0))
+    q = c.nodes()
+    with pytest.raises(H.HyscoError) as e:
+        H.hysco_hessvec(c.ctx, q, c.nodes())
+    assert e.value.status == H.HYSCO_ERR_STATE
+    bad = np.zeros((4, 4, 9))
+    bad[1, 2, 4] = 1.5                                       # |Db| = 1.5 >= 1
+    jdsp, inf = H.hysco_objective_grad(c.ctx, c.nodes(bad))
+    assert inf and np.isinf(jdsp[0, 0])
+    with pytest.raises(H.HyscoError) as e:
+        H.hysco_hessvec(c.ctx, q, c.nodes())
+    assert e.value.status == H.HYSCO_ERR_STATE
+    reps, inf = H.hysco_solve(c.ctx, c.nodes(bad))
+    assert inf and reps[0]["stop"] == "infeasible" and reps[0]["gn_iters"] == 0
+    c.close()
+
+
+def test_armijo_halving_matches_oracle():
+    """A direction that overshoots: construct with a tiny alpha so the GN step
+    is long and the barrier rejects gamma = 1 (R15); fp64 decisions must match."""
+    p = phantom.make_pair((6, 6, 20), (1.0, 1.0, 1.0), 21)
+    Ip, Im = p.Ip.astype(np.float64), p.Im.astype(np.float64)
+    b0 = np.zeros((6, 6, 21))
+    c = Ctx([Ip], [Im], p.h, H.HYSCO_F64, alpha=1e-3, beta=1e-6)
+    b = c.nodes(b0)
+    reps, _ = H.hysco_solve(c.ctx, b, H.default_solve_opts(max_gn=4))
+    bref, st, rep = O.gauss_newton(Ip, Im, b0, p.h, alpha=1e-3, beta=1e-6, max_gn=4)
+    r = reps[0]
+    assert (r["gn_iters"], r["f_evals"], r["stop_reason"]) == (rep["gn_iters"], rep["f_evals"], rep["stop_reason"])
+    assert rel(c.np(b)[0], bref) <= 1e-9
+    c.close()
+
+
+def test_graph_and_host_loop_bitwise_equal(monkeypatch):
+    p = phantom.make_pair((8, 6, 30), (1.25, 1.25, 1.25), 4)
+    out = []
+    for ng in ("0", "1"):
+        monkeypatch.setenv("HYSCO_NO_GRAPH", ng)
+        c = Ctx([p.Ip], [p.Im], p.h)
+        b, Tp, Tm = c.nodes(), c.cells(), c.cells()
+        reps, _ = H.hysco_correct(c.ctx, b, Tp, Tm)
+        out.append((c.np(b), c.np(Tp), reps[0]["J"]))
+        c.close()
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+    assert out[0][2] == out[1][2]
+
+
+def test_repeat_calls_deterministic_and_host_entry_equal():
+    p = phantom.make_pair((10, 9, 40), (1.25, 1.25, 1.25), 8)
+    c = Ctx([p.Ip], [p.Im], p.h)
+    b1, b2 = c.nodes(), c.nodes()
+    H.hysco_correct(c.ctx, b1)
+    H.hysco_correct(c.ctx, b2)
+    assert torch.equal(b1, b2)
+    hb = np.zeros((1, 10, 9, 41), np.float32)
+    hTp = np.zeros((1, 10, 9, 40), np.float32)
+    H.hysco_correct_host(c.ctx, np.ascontiguousarray(p.Ip[None]), np.ascontiguousarray(p.Im[None]), hb, hTp, None)
+    assert np.array_equal(hb, c.np(b1).astype(np.float32))
+    c.close()
+
+
+# ---------------------------------------------------------------- full size (BASELINE configs[1])
+
+@pytest.fixture(scope="module")
+def hcp3t():
+    return phantom.make_config("C2_hcp3t")
+
+
+def test_hcp3t_kernels_parity(hcp3t):
+    """3T shape, the launch configuration bench.py times: OT (all columns), eval,
+    hessvec at the OT b against the oracle evaluated on the full volume."""
+    p = hcp3t
+    Ip, Im = p.Ip.astype(np.float64), p.Im.astype(np.float64)
+    c = Ctx([p.Ip], [p.Im], p.h)
+    b = c.nodes()
+    H.hysco_ot_init(c.ctx, b)
+    b0, _ = O.ot_init(Ip, Im, p.h[2])
+    assert rel(c.np(b)[0], b0) <= 1e-5
+    b0 = rnd(b0, H.HYSCO_F32)
+    g = c.nodes()
+    jdsp, _ = H.hysco_objective_grad(c.ctx, c.nodes(b0), g)
+    st = O.evaluate(Ip, Im, b0, p.h)
+    assert relS(jdsp[0, 0], st.J) <= 1e-5
+    assert rel(c.np(g)[0], st.grad) <= 1e-5
+    q = rnd(np.random.default_rng(1).standard_normal(b0.shape), H.HYSCO_F32)
+    Hq = c.nodes()
+    H.hysco_hessvec(c.ctx, c.nodes(q), Hq)
+    assert rel(c.np(Hq)[0], O.hessvec(st, q)) <= 1e-5
+    c.close()
+
+
+def test_hcp3t_one_gn_step_parity(hcp3t):
+    p = hcp3t
+    Ip, Im = p.Ip.astype(np.float64), p.Im.astype(np.float64)
+    b0, _ = O.ot_init(Ip, Im, p.h[2])
+    b0 = rnd(b0, H.HYSCO_F32)
+    c = Ctx([p.Ip], [p.Im], p.h)
+    b = c.nodes(b0)
+    reps, _ = H.hysco_solve(c.ctx, b, H.default_solve_opts(max_gn=1, armijo=0))
+    bref, st, rep = O.gauss_newton(Ip, Im, b0, p.h, max_gn=1, armijo=False)
+    assert rel(c.np(b)[0], bref) <= 1e-4 and relS(reps[0]["J"], rep["J"]) <= 1e-5
+    c.close()
+
+
+def test_hcp3t_full_correct_properties(hcp3t):
+    """Full default path at 3T: work counters are the fixed 10 x 10 schedule and
+    the correction recovers the analytic pair (RelImp)."""
+    p = hcp3t
+    c = Ctx([p.Ip], [p.Im], p.h)
+    b, Tp, Tm = c.nodes(), c.cells(), c.cells()
+    reps, inf = H.hysco_correct(c.ctx, b, Tp, Tm)
+    r = reps[0]
+    assert not inf and r["gn_iters"] == 10 and r["pcg_iters"] == 100 and r["h_evals"] == 100
+    ri = O.relative_improvement(p.Ip, p.Im, c.np(Tp)[0], c.np(Tm)[0])
+    assert ri > 99.0
+    # J decreased from the OT start
+    b0 = c.nodes()
+    H.hysco_ot_init(c.ctx, b0)
+    j0, _ = H.hysco_objective_grad(c.ctx, b0)
+    assert r["J"] < j0[0, 0]
+    c.close()
