@@ -81,10 +81,13 @@ def full(rep, out):
 
 def launches(path, out):
     rows = list(csv.reader(open(path)))
-    hdr = rows[0]
+    h0 = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    hdr = rows[h0]
     ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
     agg = {}
-    for r in rows[1:]:
+    for r in rows[h0 + 1:]:
+        if len(r) != len(hdr):
+            continue
         name = r[ki].split("(")[0].replace("void ", "").split("<")[0].split("::")[-1]
         t = float(r[vi].replace(",", "")) * (1e-3 if r[ui] == "ns" else 1.0 if r[ui] in ("us", "usecond") else 1e3)
         a = agg.setdefault(name, {"launches": 0, "total_us": 0.0})
