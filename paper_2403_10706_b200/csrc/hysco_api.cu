@@ -55,7 +55,8 @@ struct hysco_ctx_s {
     unsigned* dcond = nullptr;
     unsigned* h_cond = nullptr;
     Ctl ctl{};
-    int gx_nodes = 1, gx_cells = 1, gx_eval = 1, gx_apply = 1, gx_ot = 1;
+    int gx_nodes = 1, gx_mv = 1, gx_cells = 1, gx_eval = 1, gx_apply = 1, gx_ot = 1;
+    int nch = 5;              // 32-node chunks per column segment of the node kernels
     size_t smem_eval = 0, smem_ot = 0;
     bool state_valid = false;
     bool poisoned = false;
@@ -68,6 +69,12 @@ struct hysco_ctx_s {
     bool have_key = false;
     long long last_launches = 0;
     void* flush = nullptr;    // profiling-only L2 flush scratch
+    // on-chip-resident PCG (hysco_resident.cuh): fp32, one CTA per SM
+    bool resident = false;
+    int res_k = 0, res_nbmax = 0, res_grid = 0;
+    size_t res_smem = 0;
+    double* res_part = nullptr;
+    unsigned* res_bar = nullptr;
 };
 
 static hysco_status set_err(hysco_ctx c, hysco_status s, const std::string& m) {
@@ -129,6 +136,34 @@ static hysco_status check_opts(hysco_ctx ctx, const hysco_solve_opts& o, const h
 // ---------------------------------------------------------------------------
 // Kernel launchers (typed)
 // ---------------------------------------------------------------------------
+// Node kernels take the number of 32-node chunks per column segment (NCH) as a
+// compile-time parameter; pick_nch() chooses it from P = n3+1.
+#define NCH_SWITCH(nch, ...)                      \
+    switch (nch) {                                \
+        case 2: {                                 \
+            constexpr int NCH = 2;                \
+            __VA_ARGS__;                          \
+        } break;                                  \
+        case 4: {                                 \
+            constexpr int NCH = 4;                \
+            __VA_ARGS__;                          \
+        } break;                                  \
+        case 5: {                                 \
+            constexpr int NCH = 5;                \
+            __VA_ARGS__;                          \
+        } break;                                  \
+        case 7: {                                 \
+            constexpr int NCH = 7;                \
+            __VA_ARGS__;                          \
+        } break;                                  \
+        default: {                                \
+            constexpr int NCH = 8;                \
+            __VA_ARGS__;                          \
+        } break;                                  \
+    }
+
+static int pick_nch(int P) { return P <= 64 ? 2 : P <= 128 ? 4 : P <= 160 ? 5 : P <= 224 ? 7 : 8; }
+
 template <typename T>
 struct L {
     static T* b(hysco_ctx c, int k) { return static_cast<T*>(c->buf[k]); }
@@ -138,32 +173,36 @@ struct L {
             c->g, c->ctl, sp, mode, (const T*)c->Ip, (const T*)c->Im, bsrc, b(c, B_GRAD), b(c, B_DT), b(c, B_ET));
     }
     static void pcg_init(hysco_ctx c) {
-        pcg_init_kernel<T><<<dim3(c->gx_nodes, c->cfg.batch), 256, 0, c->stream>>>(
-            c->g, c->ctl, b(c, B_GRAD), b(c, B_DT), b(c, B_X), b(c, B_R), b(c, B_P));
+        NCH_SWITCH(c->nch, pcg_init_kernel<T, NCH><<<dim3(c->gx_nodes, c->cfg.batch), 256, 0, c->stream>>>(
+                               c->g, c->ctl, b(c, B_GRAD), b(c, B_DT), b(c, B_X), b(c, B_R), b(c, B_P)));
     }
     static void pcg_iter(hysco_ctx c, const SolveParams& sp) {
         dim3 gr(c->gx_nodes, c->cfg.batch);
-        matvec_kernel<T, true><<<gr, 256, 0, c->stream>>>(c->g, c->ctl, b(c, B_DT), b(c, B_ET), b(c, B_P), b(c, B_HP));
-        pcg_update_kernel<T><<<gr, 256, 0, c->stream>>>(c->g, c->ctl, sp, b(c, B_DT), b(c, B_P), b(c, B_HP),
-                                                          b(c, B_X), b(c, B_R));
-        pcg_dir_kernel<T><<<gr, 256, 0, c->stream>>>(c->g, c->ctl, b(c, B_DT), b(c, B_R), b(c, B_P));
+        NCH_SWITCH(c->nch,
+                   matvec_kernel<T, NCH, true><<<dim3(c->gx_mv, c->cfg.batch), 256, 0, c->stream>>>(
+                       c->g, c->ctl, b(c, B_DT), b(c, B_ET), b(c, B_P), b(c, B_HP));
+                   pcg_update_kernel<T, NCH><<<gr, 256, 0, c->stream>>>(c->g, c->ctl, sp, b(c, B_DT), b(c, B_P),
+                                                                       b(c, B_HP), b(c, B_X), b(c, B_R));
+                   pcg_dir_kernel<T, NCH><<<gr, 256, 0, c->stream>>>(c->g, c->ctl, b(c, B_DT), b(c, B_R),
+                                                                    b(c, B_P)));
     }
     static void trial_init(hysco_ctx c) {
-        trial_init_kernel<T><<<dim3(c->gx_nodes, c->cfg.batch), 256, 0, c->stream>>>(
-            c->g, c->ctl, b(c, B_GRAD), b(c, B_X), b(c, B_B), b(c, B_BOLD));
+        NCH_SWITCH(c->nch, trial_init_kernel<T, NCH><<<dim3(c->gx_nodes, c->cfg.batch), 256, 0, c->stream>>>(
+                               c->g, c->ctl, b(c, B_GRAD), b(c, B_X), b(c, B_B), b(c, B_BOLD)));
     }
     static void ls_body(hysco_ctx c, const SolveParams& sp) {
         eval(c, sp, EVAL_TRIAL, b(c, B_B));
-        ls_retry_kernel<T><<<dim3(c->gx_nodes, c->cfg.batch), 256, 0, c->stream>>>(c->g, c->ctl, b(c, B_X),
-                                                                                    b(c, B_BOLD), b(c, B_B));
+        NCH_SWITCH(c->nch, ls_retry_kernel<T, NCH><<<dim3(c->gx_nodes, c->cfg.batch), 256, 0, c->stream>>>(
+                               c->g, c->ctl, b(c, B_X), b(c, B_BOLD), b(c, B_B)));
     }
     static void gn_tail(hysco_ctx c) { gn_tail_kernel<<<1, 32, 0, c->stream>>>(c->ctl, (int)c->cfg.batch); }
     static void matvec_plain(hysco_ctx c, const T* q, T* Hq) {
-        matvec_kernel<T, false><<<dim3(c->gx_nodes, c->cfg.batch), 256, 0, c->stream>>>(c->g, c->ctl, b(c, B_DT),
-                                                                                       b(c, B_ET), q, Hq);
+        NCH_SWITCH(c->nch, matvec_kernel<T, NCH, false><<<dim3(c->gx_mv, c->cfg.batch), 256, 0, c->stream>>>(
+                               c->g, c->ctl, b(c, B_DT), b(c, B_ET), q, Hq));
     }
     static void diag(hysco_ctx c, T* out) {
-        hess_diag_kernel<T><<<dim3(c->gx_nodes, c->cfg.batch), 256, 0, c->stream>>>(c->g, c->ctl, b(c, B_DT), out);
+        NCH_SWITCH(c->nch, hess_diag_kernel<T, NCH><<<dim3(c->gx_nodes, c->cfg.batch), 256, 0, c->stream>>>(
+                               c->g, c->ctl, b(c, B_DT), out));
     }
     static void apply(hysco_ctx c, const T* bsrc, T* Tp, T* Tm) {
         apply_kernel<T><<<dim3(c->gx_apply, c->cfg.batch), 256, c->smem_eval, c->stream>>>(
@@ -179,12 +218,12 @@ struct L {
         ot_column_kernel<T><<<dim3(c->gx_ot, c->cfg.batch), 256, c->smem_ot, c->stream>>>(c->g, c->ctl, Ip, Im, dst);
         if (blur) {
             const double e = exp(-0.5), w0 = e / (1.0 + 2.0 * e), w1 = 1.0 / (1.0 + 2.0 * e);
-            blur_axis_kernel<T><<<gn, 256, 0, c->stream>>>(c->g, c->ctl, 0, w0, w1, b(c, B_TMP), b(c, B_R));
-            blur_axis_kernel<T><<<gn, 256, 0, c->stream>>>(c->g, c->ctl, 1, w0, w1, b(c, B_R), b(c, B_P));
-            blur_axis_kernel<T><<<gn, 256, 0, c->stream>>>(c->g, c->ctl, 2, w0, w1, b(c, B_P), b(c, B_B));
+            blur_axis_kernel<T, 1><<<gn, 256, 0, c->stream>>>(c->g, c->ctl, 0, w0, w1, b(c, B_TMP), b(c, B_R));
+            blur_axis_kernel<T, 1><<<gn, 256, 0, c->stream>>>(c->g, c->ctl, 1, w0, w1, b(c, B_R), b(c, B_P));
+            blur_axis_kernel<T, 1><<<gn, 256, 0, c->stream>>>(c->g, c->ctl, 2, w0, w1, b(c, B_P), b(c, B_B));
         }
-        guard_max_kernel<T><<<gn, 256, 0, c->stream>>>(c->g, c->ctl, sp, b(c, B_B));
-        guard_scale_kernel<T><<<gn, 256, 0, c->stream>>>(c->g, c->ctl, b(c, B_B));
+        guard_max_kernel<T, 1><<<gn, 256, 0, c->stream>>>(c->g, c->ctl, sp, b(c, B_B));
+        guard_scale_kernel<T, 1><<<gn, 256, 0, c->stream>>>(c->g, c->ctl, b(c, B_B));
     }
 };
 
@@ -258,6 +297,94 @@ struct Runner {
     }
 };
 
+// Resident PCG (fp32): K = node slots per thread, a compile-time parameter.
+#define RES_K_SWITCH(k, ...)                                                   \
+    switch (k) {                                                               \
+        case 4: { constexpr int RK = 4; __VA_ARGS__; } break;                  \
+        case 8: { constexpr int RK = 8; __VA_ARGS__; } break;                  \
+        case 12: { constexpr int RK = 12; __VA_ARGS__; } break;                \
+        case 16: { constexpr int RK = 16; __VA_ARGS__; } break;                \
+        case 20: { constexpr int RK = 20; __VA_ARGS__; } break;                \
+        default: { constexpr int RK = 24; __VA_ARGS__; } break;                \
+    }
+
+static void launch_resident(hysco_ctx c, const SolveParams& sp, int pair) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(c->res_grid, 1, 1);
+    cfg.blockDim = dim3(RES_THREADS, 1, 1);
+    cfg.dynamicSmemBytes = c->res_smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    float* const* B = reinterpret_cast<float* const*>(c->buf);
+    if (sp.fixed) {
+        RES_K_SWITCH(c->res_k, cudaLaunchKernelEx(&cfg, pcg_resident_kernel<RK, true>, c->g, c->ctl, sp, pair,
+                                                  (const float*)B[B_GRAD], (const float*)B[B_DT],
+                                                  (const float*)B[B_ET], B[B_X], B[B_P], c->res_part,
+                                                  c->res_bar, c->res_nbmax));
+    } else {
+        RES_K_SWITCH(c->res_k, cudaLaunchKernelEx(&cfg, pcg_resident_kernel<RK, false>, c->g, c->ctl, sp, pair,
+                                                  (const float*)B[B_GRAD], (const float*)B[B_DT],
+                                                  (const float*)B[B_ET], B[B_X], B[B_P], c->res_part,
+                                                  c->res_bar, c->res_nbmax));
+    }
+}
+
+// Decide whether the PCG state of one pair fits on chip.
+static void setup_resident(hysco_ctx ctx) {
+    ctx->resident = false;
+    const char* e = getenv("HYSCO_NO_RESIDENT");
+    if ((e && e[0] == '1') || ctx->cfg.dtype != HYSCO_F32) return;
+    const Geom& g = ctx->g;
+    const int G = ctx->nsm;
+    if (g.ncol < G) return;
+    const long long ncl_max = (g.ncol + G - 1) / G;
+    const long long nbmax = ncl_max * g.P;
+    const long long need_k = (nbmax + RES_THREADS - 1) / RES_THREADS;
+    if (need_k > 24) return;
+    int k = need_k <= 4 ? 4 : need_k <= 8 ? 8 : need_k <= 12 ? 12 : need_k <= 16 ? 16 : need_k <= 20 ? 20 : 24;
+    const long long knt = (long long)k * RES_THREADS;   // slots per CTA incl. padding
+    const size_t smem = (size_t)(knt + 1) * 3 * sizeof(float) + (size_t)((knt + g.P - 1) / g.P) * sizeof(int) + 32;
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->cfg.device);
+    cudaFuncAttributes fa{};
+    RES_K_SWITCH(k, cudaFuncGetAttributes(&fa, pcg_resident_kernel<RK, false>));
+    if (smem + fa.sharedSizeBytes > (size_t)optin) return;
+    cudaError_t err = cudaSuccess;
+    RES_K_SWITCH(k, {
+        err = cudaFuncSetAttribute(pcg_resident_kernel<RK, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem);
+        if (err == cudaSuccess)
+            err = cudaFuncSetAttribute(pcg_resident_kernel<RK, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+    });
+    if (err != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    int occ = 0;
+    RES_K_SWITCH(k, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pcg_resident_kernel<RK, false>, RES_THREADS,
+                                                                  smem));
+    if (occ < 1) {
+        cudaGetLastError();
+        return;
+    }
+    if (cudaMalloc(&ctx->res_part, sizeof(double) * 8 * G) != cudaSuccess ||
+        cudaMalloc(&ctx->res_bar, sizeof(unsigned) * 2) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    cudaMemset(ctx->res_bar, 0, sizeof(unsigned) * 2);
+    ctx->res_k = k;
+    ctx->res_nbmax = (int)nbmax;
+    ctx->res_grid = G;
+    ctx->res_smem = smem;
+    ctx->resident = true;
+}
+
 // GN-PCG solve on buffer B_B, the structure of DESIGN.md "Solve graph".
 template <typename T>
 static void gn_sequence(Runner& r, const SolveParams& sp) {
@@ -267,8 +394,14 @@ static void gn_sequence(Runner& r, const SolveParams& sp) {
     r.loop(COND_GN, [&] {
         r.handle(COND_PCG);
         r.handle(COND_LS);
-        r.seq([&] { L<T>::pcg_init(c); });
-        r.loop(COND_PCG, [&] { r.seq([&] { L<T>::pcg_iter(c, sp); }); });
+        if (c->resident) {
+            r.seq([&] {
+                for (int p = 0; p < c->cfg.batch; p++) launch_resident(c, sp, p);
+            });
+        } else {
+            r.seq([&] { L<T>::pcg_init(c); });
+            r.loop(COND_PCG, [&] { r.seq([&] { L<T>::pcg_iter(c, sp); }); });
+        }
         r.seq([&] { L<T>::trial_init(c); });
         r.loop(COND_LS, [&] { r.seq([&] { L<T>::ls_body(c, sp); }); });
         r.seq([&] { L<T>::gn_tail(c); });
@@ -397,16 +530,22 @@ static hysco_status setup_typed(hysco_ctx ctx) {
         long long gx = work_blocks < cap ? work_blocks : cap;
         return (int)(gx < 1 ? 1 : gx);
     };
-    int occ_n = occ_blocks(pcg_update_kernel<T>, 256, 0);
-    int occ_m = occ_blocks(matvec_kernel<T, true>, 256, 0);
-    if (occ_m < occ_n) occ_n = occ_m;
-    ctx->gx_nodes = per_pair((g.Nn + 255) / 256, occ_n);
+    ctx->nch = pick_nch(g.P);
+    int occ_n = 8, occ_m = 8;
+    NCH_SWITCH(ctx->nch, {
+        occ_n = occ_blocks(pcg_update_kernel<T, NCH>, 256, 0);
+        const int o2 = occ_blocks(pcg_init_kernel<T, NCH>, 256, 0);
+        if (o2 < occ_n) occ_n = o2;
+        occ_m = occ_blocks(matvec_kernel<T, NCH, true>, 256, 0);
+    });
+    ctx->gx_nodes = per_pair((g.ncol + 7) / 8, occ_n);
+    ctx->gx_mv = per_pair((g.ncol + 7) / 8, occ_m);
     ctx->gx_cells = per_pair((g.Nc + 255) / 256, occ_n);
     ctx->gx_eval = per_pair((g.ncol + 7) / 8, occ_blocks(eval_kernel<T>, 256, ctx->smem_eval));
     ctx->gx_apply = per_pair((g.ncol + 7) / 8, occ_blocks(apply_kernel<T>, 256, ctx->smem_eval));
     ctx->gx_ot = per_pair((g.ncol + 7) / 8, occ_blocks(ot_column_kernel<T>, 256, ctx->smem_ot));
     int mx = ctx->gx_nodes;
-    for (int v : {ctx->gx_cells, ctx->gx_eval, ctx->gx_apply, ctx->gx_ot}) mx = v > mx ? v : mx;
+    for (int v : {ctx->gx_mv, ctx->gx_cells, ctx->gx_eval, ctx->gx_apply, ctx->gx_ot}) mx = v > mx ? v : mx;
     ctx->ctl.part_stride = mx * 8;
     return HYSCO_OK;
 }
@@ -534,6 +673,7 @@ hysco_status hysco_create(const hysco_config* cfg, void* cuda_stream, hysco_ctx*
     ctx->ctl.launches = ctx->launches;
     ctx->ctl.dcond = ctx->dcond;
     ctx->ctl.use_graph = 0;
+    setup_resident(ctx);
     *out = ctx;
     return HYSCO_OK;
 }
@@ -738,18 +878,20 @@ static hysco_status profile_typed(hysco_ctx ctx, int reps, int flush_l2, double*
             CK(cudaEventRecord(e0, ctx->stream));
             switch (k) {
                 case HYSCO_PROF_MATVEC:
-                    matvec_kernel<T, true><<<gr, 256, 0, ctx->stream>>>(ctx->g, ctx->ctl, L<T>::b(ctx, B_DT),
-                                                                      L<T>::b(ctx, B_ET), L<T>::b(ctx, B_P),
-                                                                      L<T>::b(ctx, B_HP));
+                    NCH_SWITCH(ctx->nch, matvec_kernel<T, NCH, true><<<dim3(ctx->gx_mv, ctx->cfg.batch), 256, 0,
+                                                                       ctx->stream>>>(
+                                             ctx->g, ctx->ctl, L<T>::b(ctx, B_DT), L<T>::b(ctx, B_ET),
+                                             L<T>::b(ctx, B_P), L<T>::b(ctx, B_HP)));
                     break;
                 case HYSCO_PROF_UPDATE:
-                    pcg_update_kernel<T><<<gr, 256, 0, ctx->stream>>>(ctx->g, ctx->ctl, sp, L<T>::b(ctx, B_DT),
-                                                                     L<T>::b(ctx, B_P), L<T>::b(ctx, B_HP),
-                                                                     L<T>::b(ctx, B_X), L<T>::b(ctx, B_R));
+                    NCH_SWITCH(ctx->nch, pcg_update_kernel<T, NCH><<<gr, 256, 0, ctx->stream>>>(
+                                             ctx->g, ctx->ctl, sp, L<T>::b(ctx, B_DT), L<T>::b(ctx, B_P),
+                                             L<T>::b(ctx, B_HP), L<T>::b(ctx, B_X), L<T>::b(ctx, B_R)));
                     break;
                 case HYSCO_PROF_DIR:
-                    pcg_dir_kernel<T><<<gr, 256, 0, ctx->stream>>>(ctx->g, ctx->ctl, L<T>::b(ctx, B_DT),
-                                                                  L<T>::b(ctx, B_R), L<T>::b(ctx, B_P));
+                    NCH_SWITCH(ctx->nch, pcg_dir_kernel<T, NCH><<<gr, 256, 0, ctx->stream>>>(
+                                             ctx->g, ctx->ctl, L<T>::b(ctx, B_DT), L<T>::b(ctx, B_R),
+                                             L<T>::b(ctx, B_P)));
                     break;
                 default:
                     L<T>::eval(ctx, sp, EVAL_PLAIN, L<T>::b(ctx, B_B));
@@ -796,6 +938,8 @@ hysco_status hysco_destroy(hysco_ctx ctx) {
                     (void*)ctx->ctr, (void*)ctx->gctr, (void*)ctx->launches, (void*)ctx->dcond})
         if (p) cudaFree(p);
     if (ctx->flush) cudaFree(ctx->flush);
+    if (ctx->res_part) cudaFree(ctx->res_part);
+    if (ctx->res_bar) cudaFree(ctx->res_bar);
     if (ctx->h_st) cudaFreeHost(ctx->h_st);
     if (ctx->h_launches) cudaFreeHost(ctx->h_launches);
     if (ctx->h_cond) cudaFreeHost(ctx->h_cond);

@@ -261,236 +261,6 @@ __global__ void __launch_bounds__(256) eval_kernel(Geom g, Ctl c, SolveParams sp
 }
 
 // ---------------------------------------------------------------------------
-// A5 GN Hessian matvec on the folded form:
-//   Hq = tridiag_PE(dt, et) q + alpha hd L_xy q     (L_xy: in-plane Neumann)
-// PCG mode also reduces p.Hp and forms alpha_c = (r.z)/(p.Hp) per pair.
-// ---------------------------------------------------------------------------
-template <typename T, bool PCG>
-__global__ void __launch_bounds__(256) matvec_kernel(Geom g, Ctl c, const T* __restrict__ dt,
-                                                     const T* __restrict__ et, const T* __restrict__ q,
-                                                     T* __restrict__ Hq) {
-    count_launch(c);
-    const int pair = blockIdx.y;
-    bool active = true;
-    if (PCG) active = c.st[pair].pcg_active != 0;
-    const size_t po = (size_t)pair * g.Nn;
-    const T* dp = dt + po;
-    const T* ep = et + po;
-    const T* qp = q + po;
-    T* hp = Hq + po;
-    const T ahd = (T)g.ahd, ih1sq = (T)g.ih1sq, ih2sq = (T)g.ih2sq;
-    const long long sI = (long long)g.n2 * g.P;
-    double acc = 0;
-    if (active) {
-        for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < g.Nn;
-             t += (long long)gridDim.x * blockDim.x) {
-            const NodeIdx ix = node_idx(g, t);
-            const T qv = qp[t];
-            T h = dp[t] * qv;
-            if (ix.l > 0) h += ep[t - 1] * qp[t - 1];
-            if (ix.l < g.n3) h += ep[t] * qp[t + 1];
-            T l1 = 0, l2 = 0;
-            if (ix.i > 0) l1 += qv - qp[t - sI];
-            if (ix.i < g.n1 - 1) l1 += qv - qp[t + sI];
-            if (ix.j > 0) l2 += qv - qp[t - g.P];
-            if (ix.j < g.n2 - 1) l2 += qv - qp[t + g.P];
-            h += ahd * (l1 * ih1sq + l2 * ih2sq);
-            hp[t] = h;
-            if (PCG) acc += (double)qv * (double)h;
-        }
-    }
-    if (!PCG) return;
-    double v[1] = {acc}, tot[1];
-    if (!pair_reduce<1, 0u>(c, v, tot)) return;
-    if (threadIdx.x != 0 || !active) return;
-    PairState& s = c.st[pair];
-    if (tot[0] <= 0.0) {          // breakdown: stop PCG, keep x (oracle pcg(): "if pHp <= 0: break")
-        s.alpha_c = 0.0;
-        s.pcg_active = 0;
-    } else {
-        s.alpha_c = s.rz / tot[0];
-        s.h_evals += 1;
-    }
-}
-
-// Jacobi preconditioner M = diag(H_J) = dt + alpha hd diag(L_xy) (R13)
-template <typename T>
-__device__ __forceinline__ T jacobi(const Geom& g, const T* dp, long long t) {
-    const NodeIdx ix = node_idx(g, t);
-    return dp[t] + (T)(g.ahd * diag_lxy(g, ix.i, ix.j));
-}
-
-// PCG start (R14): x = 0, r = -grad, z = r/M, p = z; r.z and r.r per pair.
-template <typename T>
-__global__ void __launch_bounds__(256) pcg_init_kernel(Geom g, Ctl c, const T* __restrict__ grad,
-                                                       const T* __restrict__ dt, T* __restrict__ x,
-                                                       T* __restrict__ r, T* __restrict__ p) {
-    count_launch(c);
-    const int pair = blockIdx.y;
-    const bool active = c.st[pair].gn_active != 0;
-    const size_t po = (size_t)pair * g.Nn;
-    double arz = 0, arr = 0;
-    if (active) {
-        for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < g.Nn;
-             t += (long long)gridDim.x * blockDim.x) {
-            const T rv = -grad[po + t];
-            const T z = rv / jacobi(g, dt + po, t);
-            x[po + t] = T(0);
-            r[po + t] = rv;
-            p[po + t] = z;
-            arz += (double)rv * (double)z;
-            arr += (double)rv * (double)rv;
-        }
-    }
-    double v[2] = {arz, arr}, tot[2];
-    if (!pair_reduce<2, 0u>(c, v, tot)) return;
-    if (threadIdx.x != 0) return;
-    PairState& s = c.st[pair];
-    if (active) {
-        s.rz = tot[0];
-        s.rr0 = tot[1];
-        s.rr = tot[1];
-        s.pcg_k = 0;
-        s.beta_c = 0.0;
-        s.relres = tot[1] > 0.0 ? 1.0 : 0.0;
-        s.pcg_active = tot[1] > 0.0 ? 1 : 0;
-    } else {
-        s.pcg_active = 0;
-    }
-    if (last_pair(c)) set_cond(c, COND_PCG, any_pair(c, gridDim.y, [](volatile PairState* q) { return q->pcg_active != 0; }));
-}
-
-// A6 PCG update: x += a p, r -= a Hp, z = r/M; r.z, r.r; beta; stop test.
-template <typename T>
-__global__ void __launch_bounds__(256) pcg_update_kernel(Geom g, Ctl c, SolveParams sp,
-                                                         const T* __restrict__ dt, const T* __restrict__ p,
-                                                         const T* __restrict__ Hp, T* __restrict__ x,
-                                                         T* __restrict__ r) {
-    count_launch(c);
-    const int pair = blockIdx.y;
-    const bool active = c.st[pair].pcg_active != 0;
-    const T a = (T)c.st[pair].alpha_c;
-    const size_t po = (size_t)pair * g.Nn;
-    double arz = 0, arr = 0;
-    if (active) {
-        for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < g.Nn;
-             t += (long long)gridDim.x * blockDim.x) {
-            const size_t o = po + t;
-            x[o] = x[o] + a * p[o];
-            const T rv = r[o] - a * Hp[o];
-            r[o] = rv;
-            const T z = rv / jacobi(g, dt + po, t);
-            arz += (double)rv * (double)z;
-            arr += (double)rv * (double)rv;
-        }
-    }
-    double v[2] = {arz, arr}, tot[2];
-    if (!pair_reduce<2, 0u>(c, v, tot)) return;
-    if (threadIdx.x != 0) return;
-    PairState& s = c.st[pair];
-    if (active) {
-        s.pcg_k += 1;
-        s.pcg_iters += 1;
-        s.rr = tot[1];
-        s.relres = sqrt(tot[1] / s.rr0);
-        s.beta_c = tot[0] / s.rz;
-        s.rz = tot[0];
-        if (s.pcg_k >= sp.max_pcg || (!sp.fixed && s.relres < sp.pcg_rtol)) s.pcg_active = 0;
-    }
-    if (last_pair(c)) set_cond(c, COND_PCG, any_pair(c, gridDim.y, [](volatile PairState* q) { return q->pcg_active != 0; }));
-}
-
-// New search direction p = z + beta p (z = r/M recomputed, not stored).
-template <typename T>
-__global__ void __launch_bounds__(256) pcg_dir_kernel(Geom g, Ctl c, const T* __restrict__ dt,
-                                                      const T* __restrict__ r, T* __restrict__ p) {
-    count_launch(c);
-    const int pair = blockIdx.y;
-    if (!c.st[pair].pcg_active) return;
-    const T be = (T)c.st[pair].beta_c;
-    const size_t po = (size_t)pair * g.Nn;
-    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < g.Nn;
-         t += (long long)gridDim.x * blockDim.x) {
-        const size_t o = po + t;
-        p[o] = r[o] / jacobi(g, dt + po, t) + be * p[o];
-    }
-}
-
-// A7 start of the Armijo search: g.q, max|q|, b_old = b, b = b + q (gamma = 1).
-template <typename T>
-__global__ void __launch_bounds__(256) trial_init_kernel(Geom g, Ctl c, const T* __restrict__ grad,
-                                                         const T* __restrict__ q, T* __restrict__ b,
-                                                         T* __restrict__ bold) {
-    count_launch(c);
-    const int pair = blockIdx.y;
-    const bool active = c.st[pair].gn_active != 0;
-    const size_t po = (size_t)pair * g.Nn;
-    double agq = 0, aqm = 0;
-    if (active) {
-        for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < g.Nn;
-             t += (long long)gridDim.x * blockDim.x) {
-            const size_t o = po + t;
-            const T qv = q[o];
-            agq += (double)grad[o] * (double)qv;
-            aqm = fmax(aqm, (double)fabs(qv));
-            const T bv = b[o];
-            bold[o] = bv;
-            b[o] = bv + qv;
-        }
-    }
-    double v[2] = {agq, aqm}, tot[2];
-    if (!pair_reduce<2, 0x2u>(c, v, tot)) return;
-    if (threadIdx.x != 0) return;
-    PairState& s = c.st[pair];
-    if (active) {
-        s.gq = tot[0];
-        s.qmax = tot[1];
-        s.gamma = 1.0;
-        s.ls_tries = 0;
-        s.ls_restore = 0;
-        s.ls_active = 1;
-    } else {
-        s.ls_active = 0;
-    }
-    if (last_pair(c)) set_cond(c, COND_LS, any_pair(c, gridDim.y, [](volatile PairState* q2) { return q2->ls_active != 0; }));
-}
-
-// Armijo retry / restore: b = b_old + gamma q, or b = b_old after a failed search.
-template <typename T>
-__global__ void __launch_bounds__(256) ls_retry_kernel(Geom g, Ctl c, const T* __restrict__ q,
-                                                       const T* __restrict__ bold, T* __restrict__ b) {
-    count_launch(c);
-    const int pair = blockIdx.y;
-    const PairState& s = c.st[pair];
-    if (!s.ls_active) return;
-    const bool restore = s.ls_restore != 0;
-    const T gm = (T)s.gamma;
-    const size_t po = (size_t)pair * g.Nn;
-    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < g.Nn;
-         t += (long long)gridDim.x * blockDim.x) {
-        const size_t o = po + t;
-        b[o] = restore ? bold[o] : bold[o] + gm * q[o];
-    }
-}
-
-// End of a GN step: loop condition = any pair still iterating.
-__global__ void gn_tail_kernel(Ctl c, int batch) {
-    count_launch(c);
-    if (threadIdx.x == 0)
-        set_cond(c, COND_GN, any_pair(c, batch, [](volatile PairState* q) { return q->gn_active != 0; }));
-}
-
-// diag(H_J) output for hysco_hess_diag.
-template <typename T>
-__global__ void hess_diag_kernel(Geom g, Ctl c, const T* __restrict__ dt, T* __restrict__ out) {
-    count_launch(c);
-    const size_t po = (size_t)blockIdx.y * g.Nn;
-    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < g.Nn;
-         t += (long long)gridDim.x * blockDim.x)
-        out[po + t] = jacobi(g, dt + po, t);
-}
-
-// ---------------------------------------------------------------------------
 // A9 Jacobian-modulation correction: T+ = I+(x+b)(1+Db), T- = I-(x-b)(1-Db)
 // ---------------------------------------------------------------------------
 template <typename T>
@@ -645,62 +415,7 @@ __global__ void __launch_bounds__(256) ot_column_kernel(Geom g, Ctl c, const T* 
     }
 }
 
-// 3-tap periodic Gaussian along one axis of the node array (R11).
-template <typename T>
-__global__ void __launch_bounds__(256) blur_axis_kernel(Geom g, Ctl c, int axis, double w0, double w1,
-                                                        const T* __restrict__ in, T* __restrict__ out) {
-    count_launch(c);
-    const size_t po = (size_t)blockIdx.y * g.Nn;
-    const T a = (T)w0, m = (T)w1;
-    const long long sI = (long long)g.n2 * g.P;
-    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < g.Nn;
-         t += (long long)gridDim.x * blockDim.x) {
-        const NodeIdx ix = node_idx(g, t);
-        long long tm, tp;
-        if (axis == 0) {
-            tm = t + (long long)(((ix.i + g.n1 - 1) % g.n1) - ix.i) * sI;
-            tp = t + (long long)(((ix.i + 1) % g.n1) - ix.i) * sI;
-        } else if (axis == 1) {
-            tm = t + (long long)(((ix.j + g.n2 - 1) % g.n2) - ix.j) * g.P;
-            tp = t + (long long)(((ix.j + 1) % g.n2) - ix.j) * g.P;
-        } else {
-            tm = t + (((ix.l + g.P - 1) % g.P) - ix.l);
-            tp = t + (((ix.l + 1) % g.P) - ix.l);
-        }
-        out[po + t] = a * in[po + tm] + m * in[po + t] + a * in[po + tp];
-    }
-}
-
-// Feasibility guard (R10): max |Db| per pair; scale to feas_cap if reached.
-template <typename T>
-__global__ void __launch_bounds__(256) guard_max_kernel(Geom g, Ctl c, SolveParams sp, const T* __restrict__ b) {
-    count_launch(c);
-    const int pair = blockIdx.y;
-    const size_t po = (size_t)pair * g.Nn;
-    double mx = 0.0;
-    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < g.Nn;
-         t += (long long)gridDim.x * blockDim.x) {
-        const long long l = t % g.P;
-        if (l < g.n3) mx = fmax(mx, fabs((double)(b[po + t + 1] - b[po + t])) / g.h3);
-    }
-    double v[1] = {mx}, tot[1];
-    if (!pair_reduce<1, 0x1u>(c, v, tot)) return;
-    if (threadIdx.x != 0) return;
-    PairState& s = c.st[pair];
-    s.maxDb = tot[0];
-    s.scale = (tot[0] >= sp.feas_cap) ? sp.feas_cap / tot[0] : 1.0;
-}
-
-template <typename T>
-__global__ void __launch_bounds__(256) guard_scale_kernel(Geom g, Ctl c, T* __restrict__ b) {
-    count_launch(c);
-    const int pair = blockIdx.y;
-    const double sc = c.st[pair].scale;
-    if (sc == 1.0) return;
-    const size_t po = (size_t)pair * g.Nn;
-    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < g.Nn;
-         t += (long long)gridDim.x * blockDim.x)
-        b[po + t] = (T)((double)b[po + t] * sc);
-}
-
 }  // namespace hysco
+
+#include "hysco_nodes.cuh"
+#include "hysco_resident.cuh"
