@@ -75,6 +75,7 @@ struct hysco_ctx_s {
     size_t res_smem = 0;
     double* res_part = nullptr;
     unsigned* res_bar = nullptr;
+    float* res_pg = nullptr;     // ghost-padded global copy of p (halo source)
 };
 
 static hysco_status set_err(hysco_ctx c, hysco_status s, const std::string& m) {
@@ -323,12 +324,12 @@ static void launch_resident(hysco_ctx c, const SolveParams& sp, int pair) {
     if (sp.fixed) {
         RES_K_SWITCH(c->res_k, cudaLaunchKernelEx(&cfg, pcg_resident_kernel<RK, true>, c->g, c->ctl, sp, pair,
                                                   (const float*)B[B_GRAD], (const float*)B[B_DT],
-                                                  (const float*)B[B_ET], B[B_X], B[B_P], c->res_part,
+                                                  (const float*)B[B_ET], B[B_X], c->res_pg, c->res_part,
                                                   c->res_bar, c->res_nbmax));
     } else {
         RES_K_SWITCH(c->res_k, cudaLaunchKernelEx(&cfg, pcg_resident_kernel<RK, false>, c->g, c->ctl, sp, pair,
                                                   (const float*)B[B_GRAD], (const float*)B[B_DT],
-                                                  (const float*)B[B_ET], B[B_X], B[B_P], c->res_part,
+                                                  (const float*)B[B_ET], B[B_X], c->res_pg, c->res_part,
                                                   c->res_bar, c->res_nbmax));
     }
 }
@@ -347,7 +348,7 @@ static void setup_resident(hysco_ctx ctx) {
     if (need_k > 24) return;
     int k = need_k <= 4 ? 4 : need_k <= 8 ? 8 : need_k <= 12 ? 12 : need_k <= 16 ? 16 : need_k <= 20 ? 20 : 24;
     const long long knt = (long long)k * RES_THREADS;   // slots per CTA incl. padding
-    const size_t smem = (size_t)(knt + 1) * 3 * sizeof(float) + (size_t)((knt + g.P - 1) / g.P) * sizeof(int) + 32;
+    const size_t smem = (size_t)(3 * knt + 2 * g.P + 8) * sizeof(float);   // layout: hysco_resident.cuh
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->cfg.device);
     cudaFuncAttributes fa{};
@@ -372,12 +373,15 @@ static void setup_resident(hysco_ctx ctx) {
         cudaGetLastError();
         return;
     }
+    const size_t ghost = res_ghost_pair_floats(g) * ctx->cfg.batch * sizeof(float);
     if (cudaMalloc(&ctx->res_part, sizeof(double) * 8 * G) != cudaSuccess ||
-        cudaMalloc(&ctx->res_bar, sizeof(unsigned) * 2) != cudaSuccess) {
+        cudaMalloc(&ctx->res_bar, sizeof(unsigned) * 2) != cudaSuccess ||
+        cudaMalloc(&ctx->res_pg, ghost) != cudaSuccess) {
         cudaGetLastError();
         return;
     }
     cudaMemset(ctx->res_bar, 0, sizeof(unsigned) * 2);
+    cudaMemset(ctx->res_pg, 0, ghost);   // ghost planes stay zero forever
     ctx->res_k = k;
     ctx->res_nbmax = (int)nbmax;
     ctx->res_grid = G;
@@ -940,6 +944,7 @@ hysco_status hysco_destroy(hysco_ctx ctx) {
     if (ctx->flush) cudaFree(ctx->flush);
     if (ctx->res_part) cudaFree(ctx->res_part);
     if (ctx->res_bar) cudaFree(ctx->res_bar);
+    if (ctx->res_pg) cudaFree(ctx->res_pg);
     if (ctx->h_st) cudaFreeHost(ctx->h_st);
     if (ctx->h_launches) cudaFreeHost(ctx->h_launches);
     if (ctx->h_cond) cudaFreeHost(ctx->h_cond);
