@@ -173,6 +173,66 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------- roofline
+
+# FP32 pipe peak for the ALU-bound path: 148 SMs x 128 FP32 lanes x 2 flop/FMA x
+# 1.965 GHz (B200_PROFILING.md: 148 SMs, clocks.max.sm 1965 MHz; 4 SMSPs x 32
+# FP32 lanes per SM) = 74.4 TFLOP/s.  DESIGN.md §10.
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+# algorithmic fp32 flops per node per PCG iteration of the resident kernel:
+# matvec 14 (M p, 2 PE FMAs, 3 in-plane adds, 2 FMAs, p.Hp), update 10, direction 4
+RESIDENT_FLOPS_PER_NODE_ITER = 28
+
+
+def roofline_entry(H, ctx, args, r0, B, shape, ms_per_step):
+    """The kernel with the largest share of a step, timed by hysco_profile_kernels
+    (each hot kernel re-launched on the context stream, same grid and buffers,
+    CUDA events per launch; cold = L2 flushed before each launch)."""
+    n1, n2, n3 = shape
+    prof_cold = H.hysco_profile_kernels(ctx, args.profile_reps, flush_l2=True)
+    prof_warm = H.hysco_profile_kernels(ctx, args.profile_reps, flush_l2=False)
+    Nn, Nc = B * n1 * n2 * (n3 + 1), B * n1 * n2 * n3
+    resident = prof_warm["pcg_resident"] > 0
+    gn = r0["gn_iters"]
+    if resident:   # one cooperative launch per GN step runs all PCG iterations on chip
+        per_step = {"pcg_resident": gn, "eval": r0["f_evals"], "trial_init": gn}
+    else:
+        per_step = {"matvec": r0["h_evals"], "pcg_update": r0["pcg_iters"], "pcg_dir": r0["pcg_iters"],
+                    "eval": r0["f_evals"], "trial_init": gn}
+    algo_bytes = {"matvec": 16 * Nn, "pcg_update": 28 * Nn, "pcg_dir": 16 * Nn, "eval": 16 * Nn + 8 * Nc,
+                  "trial_init": 20 * Nn}
+    share = {k: prof_warm[k] * per_step[k] / ms_per_step for k in per_step}
+    dom = max(share, key=share.get)
+    traffic = None
+    try:
+        summ = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        traffic = summ.get("kernels", {}).get(dom, {}).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    hbm_peak, peak_src = peaks()
+    out = {"kernel": dom, "kernel_share_of_step": share, "traffic": traffic,
+           "avg_launch_ms_cold_l2": prof_cold[dom], "avg_launch_ms_warm_l2": prof_warm[dom],
+           "launches_per_step": per_step}
+    if dom == "pcg_resident":
+        # No HBM-bound work (state lives in registers + shared memory): ALU roofline.
+        flops = RESIDENT_FLOPS_PER_NODE_ITER * Nn * (r0["pcg_iters"] / max(gn, 1))
+        ach = flops / (prof_warm[dom] * 1e-3) / 1e12
+        out.update({"bound": "alu", "achieved": ach, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
+                    "frac": ach / FP32_PEAK_TFLOPS, "algorithmic_flops_per_launch": flops,
+                    "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 x 1.965 GHz (DESIGN.md §10)",
+                    "note": "latency/grid-barrier bound on chip; see DESIGN.md §7"})
+    else:
+        ach = algo_bytes[dom] / (prof_cold[dom] * 1e-3) / 1e9
+        out.update({"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
+                    "algorithmic_bytes_per_launch": algo_bytes[dom], "peak_source": peak_src,
+                    "achieved_warm_l2": algo_bytes[dom] / (prof_warm[dom] * 1e-3) / 1e9})
+    # the HBM-bound kernels of the step, for context
+    out["hbm_kernels"] = {k: {"GBps_cold": algo_bytes[k] / (prof_cold[k] * 1e-3) / 1e9,
+                              "frac_cold": algo_bytes[k] / (prof_cold[k] * 1e-3) / 1e9 / hbm_peak}
+                          for k in ("eval", "trial_init", "matvec", "pcg_update", "pcg_dir")}
+    return out
+
+
 # ---------------------------------------------------------------- GPU path
 
 def run_hysco(args):
@@ -234,32 +294,9 @@ def run_hysco(args):
     value = world * B * args.steps / (total_max / 1e3)
     ms_per_step = total_max / args.steps
 
-    # ---- roofline: hot kernels re-launched on the same stream/config/buffers, CUDA events
-    prof_cold = H.hysco_profile_kernels(ctx, args.profile_reps, flush_l2=True)
-    prof_warm = H.hysco_profile_kernels(ctx, args.profile_reps, flush_l2=False)
-    Nn, Nc = B * n1 * n2 * (n3 + 1), B * n1 * n2 * n3
+    roofline = roofline_entry(H, ctx, args, reps[0], B, (n1, n2, n3), ms_per_step)
     r0 = reps[0]
-    per_step = {"matvec": r0["h_evals"], "pcg_update": r0["pcg_iters"], "pcg_dir": r0["pcg_iters"],
-                "eval": r0["f_evals"]}
-    algo_bytes = {"matvec": 16 * Nn, "pcg_update": 28 * Nn, "pcg_dir": 16 * Nn, "eval": 16 * Nn + 8 * Nc}
-    share = {k: prof_warm[k] * per_step[k] / ms_per_step for k in per_step}
-    dom = max(share, key=share.get)
-    peak, peak_src = peaks()
-    ach = algo_bytes[dom] / (prof_cold[dom] * 1e-3) / 1e9
-    traffic = None
-    try:
-        summ = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
-        traffic = summ.get("kernels", {}).get(dom, {}).get("dram_bytes_per_launch")
-    except Exception:
-        pass
-    step_bytes = sum(algo_bytes[k] * per_step[k] for k in per_step)
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
-                "frac": ach / peak, "traffic": traffic, "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": algo_bytes[dom],
-                "avg_launch_ms_cold_l2": prof_cold[dom], "avg_launch_ms_warm_l2": prof_warm[dom],
-                "achieved_warm_l2": algo_bytes[dom] / (prof_warm[dom] * 1e-3) / 1e9,
-                "kernel_share_of_step": share,
-                "step_effective_gbs": step_bytes / (ms_per_step * 1e-3) / 1e9}
+    Nn, Nc = B * n1 * n2 * (n3 + 1), B * n1 * n2 * n3
 
     # ---- e2e through the host entry point (pinned buffers)
     hIp = torch.from_numpy(Ip_h).pin_memory()

@@ -182,11 +182,14 @@ HYSCO_API int64_t hysco_last_launch_count(hysco_ctx ctx);
  * hot kernel `reps` times on the context stream in the solve's launch
  * configuration and on its buffers, timing each launch with CUDA events.
  * avg_ms (host, [HYSCO_NPROF]) receives the mean launch duration of:
- * [0] matvec (A5, PCG mode), [1] pcg_update (A6), [2] pcg_dir, [3] eval (A4).
+ * [0] matvec (A5, PCG mode), [1] pcg_update (A6), [2] pcg_dir, [3] eval (A4),
+ * [4] the on-chip-resident PCG (one launch = one GN step's 10-iteration PCG
+ * solve per pair; -1 if this context does not use it), [5] trial_init (A7).
  * flush_l2 != 0: a 256 MiB scratch write (> the 126 MB L2) precedes every
  * timed launch (outside the events), i.e. cold-cache HBM-bound timings.
  * Clobbers the PCG scratch (not b, not the images). */
-enum { HYSCO_PROF_MATVEC = 0, HYSCO_PROF_UPDATE = 1, HYSCO_PROF_DIR = 2, HYSCO_PROF_EVAL = 3, HYSCO_NPROF = 4 };
+enum { HYSCO_PROF_MATVEC = 0, HYSCO_PROF_UPDATE = 1, HYSCO_PROF_DIR = 2, HYSCO_PROF_EVAL = 3,
+       HYSCO_PROF_RESIDENT = 4, HYSCO_PROF_TRIAL = 5, HYSCO_NPROF = 6 };
 HYSCO_API hysco_status hysco_profile_kernels(hysco_ctx ctx, int32_t reps, int32_t flush_l2, double* avg_ms);
 
 HYSCO_API const char* hysco_last_error(hysco_ctx ctx);

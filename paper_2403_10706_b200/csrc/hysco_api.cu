@@ -170,8 +170,9 @@ struct L {
     static T* b(hysco_ctx c, int k) { return static_cast<T*>(c->buf[k]); }
 
     static void eval(hysco_ctx c, const SolveParams& sp, int mode, const T* bsrc) {
-        eval_kernel<T><<<dim3(c->gx_eval, c->cfg.batch), 256, c->smem_eval, c->stream>>>(
-            c->g, c->ctl, sp, mode, (const T*)c->Ip, (const T*)c->Im, bsrc, b(c, B_GRAD), b(c, B_DT), b(c, B_ET));
+        NCH_SWITCH(c->nch, eval_kernel<T, NCH><<<dim3(c->gx_eval, c->cfg.batch), 256, c->smem_eval, c->stream>>>(
+                               c->g, c->ctl, sp, mode, (const T*)c->Ip, (const T*)c->Im, bsrc, b(c, B_GRAD),
+                               b(c, B_DT), b(c, B_ET)));
     }
     static void pcg_init(hysco_ctx c) {
         NCH_SWITCH(c->nch, pcg_init_kernel<T, NCH><<<dim3(c->gx_nodes, c->cfg.batch), 256, 0, c->stream>>>(
@@ -522,11 +523,12 @@ template <typename T>
 static hysco_status setup_typed(hysco_ctx ctx) {
     const Geom& g = ctx->g;
     const long long batch = ctx->cfg.batch;
-    ctx->smem_eval = (size_t)8 * (2 * g.n3 + g.P) * sizeof(T);
+    ctx->smem_eval = (size_t)8 * (2 * g.n3 + 5 * g.P) * sizeof(T);   // eval / apply column staging
     ctx->smem_ot = (size_t)8 * 2 * g.P * sizeof(double);
     if (ctx->smem_eval > 227 * 1024 || ctx->smem_ot > 227 * 1024)
         return set_err(ctx, HYSCO_ERR_SHAPE, "n3 too large for the column-in-shared-memory kernels");
-    CK(cudaFuncSetAttribute(eval_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->smem_eval));
+    NCH_SWITCH(pick_nch(g.P), CK(cudaFuncSetAttribute(eval_kernel<T, NCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                      (int)ctx->smem_eval)));
     CK(cudaFuncSetAttribute(apply_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->smem_eval));
     CK(cudaFuncSetAttribute(ot_column_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->smem_ot));
     auto per_pair = [&](long long work_blocks, int occ) {
@@ -545,7 +547,9 @@ static hysco_status setup_typed(hysco_ctx ctx) {
     ctx->gx_nodes = per_pair((g.ncol + 7) / 8, occ_n);
     ctx->gx_mv = per_pair((g.ncol + 7) / 8, occ_m);
     ctx->gx_cells = per_pair((g.Nc + 255) / 256, occ_n);
-    ctx->gx_eval = per_pair((g.ncol + 7) / 8, occ_blocks(eval_kernel<T>, 256, ctx->smem_eval));
+    int occ_e = 1;
+    NCH_SWITCH(ctx->nch, occ_e = occ_blocks(eval_kernel<T, NCH>, 256, ctx->smem_eval));
+    ctx->gx_eval = per_pair((g.ncol + 7) / 8, occ_e);
     ctx->gx_apply = per_pair((g.ncol + 7) / 8, occ_blocks(apply_kernel<T>, 256, ctx->smem_eval));
     ctx->gx_ot = per_pair((g.ncol + 7) / 8, occ_blocks(ot_column_kernel<T>, 256, ctx->smem_ot));
     int mx = ctx->gx_nodes;
@@ -859,6 +863,7 @@ static hysco_status profile_typed(hysco_ctx ctx, int reps, int flush_l2, double*
     CK(cudaStreamSynchronize(ctx->stream));
     for (int p = 0; p < ctx->cfg.batch; p++) {
         ctx->h_st[p].pcg_active = 1;
+        ctx->h_st[p].gn_active = 1;     // resident PCG / trial_init run only for iterating pairs
         ctx->h_st[p].alpha_c = 0.0;     // x, r unchanged by update
         ctx->h_st[p].beta_c = 0.0;
         ctx->h_st[p].rz = 1.0;
@@ -897,6 +902,18 @@ static hysco_status profile_typed(hysco_ctx ctx, int reps, int flush_l2, double*
                                              ctx->g, ctx->ctl, L<T>::b(ctx, B_DT), L<T>::b(ctx, B_R),
                                              L<T>::b(ctx, B_P)));
                     break;
+                case HYSCO_PROF_RESIDENT: {
+                    if (!ctx->resident) break;
+                    SolveParams rp = sp;
+                    rp.max_pcg = 10;          // one GN step's PCG solve
+                    for (int p = 0; p < ctx->cfg.batch; p++) launch_resident(ctx, rp, p);
+                    break;
+                }
+                case HYSCO_PROF_TRIAL:
+                    NCH_SWITCH(ctx->nch, trial_init_kernel<T, NCH><<<gr, 256, 0, ctx->stream>>>(
+                                             ctx->g, ctx->ctl, L<T>::b(ctx, B_GRAD), L<T>::b(ctx, B_X),
+                                             L<T>::b(ctx, B_TMP), L<T>::b(ctx, B_BOLD)));
+                    break;
                 default:
                     L<T>::eval(ctx, sp, EVAL_PLAIN, L<T>::b(ctx, B_B));
             }
@@ -907,7 +924,7 @@ static hysco_status profile_typed(hysco_ctx ctx, int reps, int flush_l2, double*
             CK(cudaEventElapsedTime(&ms, e0, e1));
             acc += ms;
         }
-        avg_ms[k] = acc / reps;
+        avg_ms[k] = (k == HYSCO_PROF_RESIDENT && !ctx->resident) ? -1.0 : acc / reps;
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);

@@ -70,8 +70,51 @@ enum { EVAL_PLAIN = 0, EVAL_GN_START = 1, EVAL_TRIAL = 2 };
 // -alpha hd / h3^2) — DESIGN.md "Folded GN Hessian".  Scalars D, S, P and
 // ||grad||^2 reduce per pair; TRIAL mode also takes the Armijo decision (R15).
 // ---------------------------------------------------------------------------
+// One cell's two gathers (I+ at k + Ab/h3, I- at k - Ab/h3): values in fp64,
+// slopes (per index unit) in T.  fp32: floor/fraction from the cell-relative
+// offset and v0 + t (v1 - v0) with the difference exact in fp64; fp64: the
+// oracle's arithmetic (absolute coordinate, (1-t) v0 + t v1), see R5.
+__device__ __forceinline__ void gather_pm(const float* __restrict__ sIp, const float* __restrict__ sIm, int n3, int k,
+                                          float Ab, const Geom& g, double& vp, double& vm, float& spl, float& sml) {
+    float del = Ab * (float)g.ih3;
+    del = fminf(fmaxf(del, (float)-(n3 + 2)), (float)(n3 + 2));
+    {
+        const float fl = floorf(del);
+        const int kk = k + (int)fl;
+        const float v0 = (kk >= 0 && kk < n3) ? sIp[kk] : 0.f;
+        const float v1 = (kk + 1 >= 0 && kk + 1 < n3) ? sIp[kk + 1] : 0.f;
+        const double d = (double)v1 - (double)v0;
+        vp = fma((double)(del - fl), d, (double)v0);
+        spl = (float)d;
+    }
+    {
+        const float md = -del;
+        const float fl = floorf(md);
+        const int kk = k + (int)fl;
+        const float v0 = (kk >= 0 && kk < n3) ? sIm[kk] : 0.f;
+        const float v1 = (kk + 1 >= 0 && kk + 1 < n3) ? sIm[kk + 1] : 0.f;
+        const double d = (double)v1 - (double)v0;
+        vm = fma((double)(md - fl), d, (double)v0);
+        sml = (float)d;
+    }
+}
+__device__ __forceinline__ void gather_pm(const double* __restrict__ sIp, const double* __restrict__ sIm, int n3, int k,
+                                          double Ab, const Geom& g, double& vp, double& vm, double& spl, double& sml) {
+    interp_col(sIp, n3, k, Ab, 1.0, g, vp, spl);
+    interp_col(sIm, n3, k, Ab, -1.0, g, vm, sml);
+}
+
+// phi, phi', phi'' (Eq.(3)) for |z| < 1 with one reciprocal of (1 - z^2).
 template <typename T>
-__global__ void __launch_bounds__(256) eval_kernel(Geom g, Ctl c, SolveParams sp, int mode,
+__device__ __forceinline__ void phi3(T z, T& f0, T& f1, T& f2) {
+    const T z2 = z * z, inv = T(1) / (T(1) - z2);
+    f0 = z2 * z2 * inv;
+    f1 = T(2) * z * z2 * (T(2) - z2) * inv * inv;
+    f2 = T(2) * z2 * (T(6) - T(3) * z2 + z2 * z2) * inv * inv * inv;
+}
+
+template <typename T, int NCH>
+__global__ void __launch_bounds__(256, 4) eval_kernel(Geom g, Ctl c, SolveParams sp, int mode,
                                                    const T* __restrict__ Ip, const T* __restrict__ Im,
                                                    const T* __restrict__ bb, T* __restrict__ grad,
                                                    T* __restrict__ dt, T* __restrict__ et) {
@@ -80,19 +123,18 @@ __global__ void __launch_bounds__(256) eval_kernel(Geom g, Ctl c, SolveParams sp
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwb = blockDim.x >> 5;
     const int pair = blockIdx.y;
     const int n3 = g.n3, P = g.P, n2 = g.n2;
-    T* sIp = reinterpret_cast<T*>(smem_raw) + (size_t)wid * (2 * n3 + P);
+    // per warp: I+, I-, b of the column and b of its four in-plane neighbour
+    // columns, all staged before any compute (every load of a column in flight)
+    T* sIp = reinterpret_cast<T*>(smem_raw) + (size_t)wid * (2 * n3 + 5 * P);
     T* sIm = sIp + n3;
     T* sb = sIm + n3;
+    T* sbim = sb + P;
+    T* sbip = sbim + P;
+    T* sbjm = sbip + P;
+    T* sbjp = sbjm + P;
 
     bool active = true;
     if (mode == EVAL_TRIAL) active = c.st[pair].ls_active != 0;
-
-    const T* Ipp = Ip + (size_t)pair * g.Nc;
-    const T* Imp = Im + (size_t)pair * g.Nc;
-    const T* bp = bb + (size_t)pair * g.Nn;
-    T* gp = grad + (size_t)pair * g.Nn;
-    T* dp = dt + (size_t)pair * g.Nn;
-    T* ep = et + (size_t)pair * g.Nn;
 
     const T hd = (T)g.hd, ahd = (T)g.ahd, bh2 = (T)g.bh2;
     const T ih3 = (T)g.ih3, ih3sq = (T)g.ih3sq, ih1sq = (T)g.ih1sq, ih2sq = (T)g.ih2sq;
@@ -101,94 +143,106 @@ __global__ void __launch_bounds__(256) eval_kernel(Geom g, Ctl c, SolveParams sp
     double aD = 0, aS = 0, aP = 0, aG = 0, aInf = 0;
     if (active) {
         for (long long col = (long long)blockIdx.x * nwb + wid; col < g.ncol; col += (long long)gridDim.x * nwb) {
-            const T* ip = Ipp + col * n3;
-            const T* im = Imp + col * n3;
-            const T* bc = bp + col * P;
+            const T* ip = Ip + (size_t)pair * g.Nc + col * n3;
+            const T* im = Im + (size_t)pair * g.Nc + col * n3;
+            const size_t ob = (size_t)pair * g.Nn + (size_t)col * P;
+            const T* bc = bb + ob;
+            T* gc = grad + ob;
+            T* dc = dt + ob;
+            T* ec = et + ob;
+            const int i = (int)(col / n2), j = (int)(col - (long long)i * n2);
+            const bool him = i > 0, hip = i < g.n1 - 1, hjm = j > 0, hjp = j < n2 - 1;
             for (int k = lane; k < n3; k += 32) {
                 sIp[k] = ip[k];
                 sIm[k] = im[k];
             }
-            for (int l = lane; l < P; l += 32) sb[l] = bc[l];
+            for (int l = lane; l < P; l += 32) {
+                sb[l] = bc[l];
+                if (him) sbim[l] = bc[l - sI];
+                if (hip) sbip[l] = bc[l + sI];
+                if (hjm) sbjm[l] = bc[l - P];
+                if (hjp) sbjp[l] = bc[l + P];
+            }
             __syncwarp();
-            const int i = (int)(col / n2), j = (int)(col - (long long)i * n2);
-            const bool him = i > 0, hip = i < g.n1 - 1, hjm = j > 0, hjp = j < n2 - 1;
-            T cr_c = 0, c2_c = 0, p1_c = 0, p2_c = 0;   // carry: cell (base-1) -> node base
-            for (int base = 0; base < P; base += 32) {
-                const int l = base + lane;
-                T ar = 0, a2 = 0, cr = 0, c2 = 0, p1 = 0, p2 = 0, ev = 0;
-                if (l < n3) {
-                    const T b0 = sb[l], b1 = sb[l + 1];
-                    const T Ab = T(0.5) * (b0 + b1);          // averaging operator A
-                    const T Db = diff_h3(b0, b1, g);          // finite difference D
-                    double vp, vm;
-                    T spl, sml;
-                    interp_col(sIp, n3, l, Ab, T(1), g, vp, spl);    // I+(x + b)
-                    interp_col(sIm, n3, l, Ab, T(-1), g, vm, sml);   // I-(x - b)
-                    const T opd = T(1) + Db, omd = T(1) - Db;
-                    const double Dbd = (double)Db;
-                    const double rd = vp * (1.0 + Dbd) - vm * (1.0 - Dbd);  // Eq.(1)-(2) residual (fp64)
-                    const T r = (T)rd;
-                    const T gg = (spl * opd + sml * omd) * ih3;
-                    const T s = (T)(vp + vm);
-                    const T a = gg * T(0.5) - s * ih3;        // dr_k/db_k
-                    const T cc = gg * T(0.5) + s * ih3;       // dr_k/db_{k+1}
-                    aD += rd * rd;
-                    const double dd = (double)(b1 - b0);
-                    aS += dd * dd * g.ih3sq;
-                    if (fabs(Db) >= T(1)) {
-                        aInf = 1.0;                           // phi = +inf (Eq.(3))
-                    } else {
-                        const T z2 = Db * Db, om = T(1) - z2;
-                        aP += (double)(z2 * z2 / om);
-                        p1 = T(2) * Db * z2 * (T(2) - z2) / (om * om);
-                        p2 = T(2) * z2 * (T(6) - T(3) * z2 + z2 * z2) / (om * om * om);
+            T fS = 0, fG = 0, fP = 0;                 // per-lane partials of this column
+            T cr_c = 0, c2_c = 0, p1_c = 0, p2_c = 0;   // carry: cell (chunk start - 1) -> node
+            for (int seg = 0; seg < P; seg += 32 * NCH) {
+#pragma unroll
+                for (int m = 0; m < NCH; m++) {
+                    const int l = seg + 32 * m + lane;
+                    T ar = 0, a2 = 0, cr = 0, c2 = 0, p1 = 0, p2 = 0, ev = 0;
+                    if (l < n3) {
+                        const T b0 = sb[l], b1 = sb[l + 1];
+                        const T Ab = T(0.5) * (b0 + b1);          // averaging operator A
+                        const T Db = diff_h3(b0, b1, g);          // finite difference D
+                        double vp, vm;
+                        T spl, sml;
+                        gather_pm(sIp, sIm, n3, l, Ab, g, vp, vm, spl, sml);   // I+(x + b), I-(x - b)
+                        const double Dbd = (double)Db;
+                        const double rd = vp * (1.0 + Dbd) - vm * (1.0 - Dbd);  // Eq.(1)-(2) residual (fp64)
+                        const T r = (T)rd;
+                        const T gg = (spl * (T(1) + Db) + sml * (T(1) - Db)) * ih3;
+                        const T s = (T)(vp + vm);
+                        const T a = gg * T(0.5) - s * ih3;        // dr_k/db_k
+                        const T cc = gg * T(0.5) + s * ih3;       // dr_k/db_{k+1}
+                        aD = fma(rd, rd, aD);
+                        const T dd = b1 - b0;
+                        fS += dd * dd * ih3sq;
+                        if (fabs(Db) >= T(1)) {
+                            aInf = 1.0;                           // phi = +inf (Eq.(3))
+                        } else {
+                            T f0;
+                            phi3(Db, f0, p1, p2);
+                            fP += f0;
+                        }
+                        ar = a * r;
+                        a2 = a * a;
+                        cr = cc * r;
+                        c2 = cc * cc;
+                        ev = hd * a * cc - bh2 * p2 * ih3sq - ahd * ih3sq;
                     }
-                    ar = a * r;
-                    a2 = a * a;
-                    cr = cc * r;
-                    c2 = cc * cc;
-                    ev = hd * a * cc - bh2 * p2 * ih3sq - ahd * ih3sq;
-                }
-                T pcr = __shfl_up_sync(FULL, cr, 1), pc2 = __shfl_up_sync(FULL, c2, 1);
-                T pp1 = __shfl_up_sync(FULL, p1, 1), pp2 = __shfl_up_sync(FULL, p2, 1);
-                if (lane == 0) {
-                    pcr = cr_c;
-                    pc2 = c2_c;
-                    pp1 = p1_c;
-                    pp2 = p2_c;
-                }
-                cr_c = __shfl_sync(FULL, cr, 31);
-                c2_c = __shfl_sync(FULL, c2, 31);
-                p1_c = __shfl_sync(FULL, p1, 31);
-                p2_c = __shfl_sync(FULL, p2, 31);
-                if (l < P) {
-                    const T bl = sb[l];
-                    T lpe = 0, l1 = 0, l2 = 0;
-                    if (l > 0) lpe += bl - sb[l - 1];
-                    if (l < n3) lpe += bl - sb[l + 1];
-                    const T* bn = bc + l;
-                    if (him) l1 += bl - bn[-sI];
-                    if (hip) {
-                        const T v = bn[sI];
-                        l1 += bl - v;
-                        aS += (double)(v - bl) * (double)(v - bl) * g.ih1sq;
+                    T pcr = __shfl_up_sync(FULL, cr, 1), pc2 = __shfl_up_sync(FULL, c2, 1);
+                    T pp1 = __shfl_up_sync(FULL, p1, 1), pp2 = __shfl_up_sync(FULL, p2, 1);
+                    if (lane == 0) {
+                        pcr = cr_c;
+                        pc2 = c2_c;
+                        pp1 = p1_c;
+                        pp2 = p2_c;
                     }
-                    if (hjm) l2 += bl - bn[-P];
-                    if (hjp) {
-                        const T v = bn[P];
-                        l2 += bl - v;
-                        aS += (double)(v - bl) * (double)(v - bl) * g.ih2sq;
+                    cr_c = __shfl_sync(FULL, cr, 31);
+                    c2_c = __shfl_sync(FULL, c2, 31);
+                    p1_c = __shfl_sync(FULL, p1, 31);
+                    p2_c = __shfl_sync(FULL, p2, 31);
+                    if (l < P) {
+                        const T bl = sb[l];
+                        T lpe = 0, l1 = 0, l2 = 0;
+                        if (l > 0) lpe += bl - sb[l - 1];
+                        if (l < n3) lpe += bl - sb[l + 1];
+                        if (him) l1 += bl - sbim[l];
+                        if (hip) {
+                            const T v = sbip[l];
+                            l1 += bl - v;
+                            fS += (v - bl) * (v - bl) * ih1sq;
+                        }
+                        if (hjm) l2 += bl - sbjm[l];
+                        if (hjp) {
+                            const T v = sbjp[l];
+                            l2 += bl - v;
+                            fS += (v - bl) * (v - bl) * ih2sq;
+                        }
+                        const T Lb = lpe * ih3sq + l1 * ih1sq + l2 * ih2sq;
+                        const T gv = hd * (pcr + ar) + ahd * Lb + bh2 * (pp1 - p1) * ih3;
+                        const T dv = hd * (pc2 + a2) + bh2 * (pp2 + p2) * ih3sq + ahd * T((l > 0) + (l < n3)) * ih3sq;
+                        gc[l] = gv;
+                        dc[l] = dv;
+                        ec[l] = (l < n3) ? ev : T(0);
+                        fG += gv * gv;
                     }
-                    const T Lb = lpe * ih3sq + l1 * ih1sq + l2 * ih2sq;
-                    const T gv = hd * (pcr + ar) + ahd * Lb + bh2 * (pp1 - p1) * ih3;
-                    const T dv = hd * (pc2 + a2) + bh2 * (pp2 + p2) * ih3sq + ahd * T((l > 0) + (l < n3)) * ih3sq;
-                    const long long o = col * P + l;
-                    gp[o] = gv;
-                    dp[o] = dv;
-                    ep[o] = (l < n3) ? ev : T(0);
-                    aG += (double)gv * (double)gv;
                 }
             }
+            aS += (double)fS;
+            aG += (double)fG;
+            aP += (double)fP;
             __syncwarp();
         }
     }

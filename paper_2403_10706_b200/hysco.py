@@ -23,7 +23,7 @@ EXPORTED = ["hysco_default_solve_opts", "hysco_default_ot_opts", "hysco_create",
             "hysco_ot_init", "hysco_objective_grad", "hysco_hessvec", "hysco_hess_diag", "hysco_solve",
             "hysco_apply", "hysco_correct", "hysco_correct_host", "hysco_last_launch_count",
             "hysco_last_error", "hysco_destroy", "hysco_version", "hysco_profile_kernels"]
-PROF_NAMES = ["matvec", "pcg_update", "pcg_dir", "eval"]
+PROF_NAMES = ["matvec", "pcg_update", "pcg_dir", "eval", "pcg_resident", "trial_init"]
 
 
 class HyscoError(RuntimeError):

@@ -102,5 +102,22 @@ def launches(path, out):
         print(f"{k:30s} n={a['launches']:5d} avg {a['avg_us']:8.2f} us share {a['share'] * 100:5.1f}%")
 
 
+def merge(out, *summaries):
+    """profiles/ncu_summary.json: per kernel, the latest capture's DRAM bytes per
+    launch (bench.py's roofline `traffic`), time and source report."""
+    res = {"kernels": {}}
+    for path in summaries:
+        d = json.load(open(path))
+        for k, e in d["summary"].items():
+            res["kernels"][k] = {"dram_bytes_per_launch": e.get("dram_bytes_per_launch"),
+                                 "time_us": e.get("time_us"), "dram_GBps": e.get("dram_GBps"),
+                                 "source": path}
+    json.dump(res, open(out, "w"), indent=1)
+    print(json.dumps(res, indent=1))
+
+
 if __name__ == "__main__":
-    {"full": full, "launches": launches}[sys.argv[1]](sys.argv[2], sys.argv[3])
+    if sys.argv[1] == "merge":
+        merge(sys.argv[2], *sys.argv[3:])
+    else:
+        {"full": full, "launches": launches}[sys.argv[1]](sys.argv[2], sys.argv[3])
