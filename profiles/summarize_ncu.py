@@ -109,7 +109,7 @@ def merge(out, *summaries):
     for path in summaries:
         d = json.load(open(path))
         for k, e in d["summary"].items():
-            res["kernels"][k] = {"dram_bytes_per_launch": e.get("dram_bytes_per_launch"),
+            res["kernels"][k[:-7] if k.endswith("_kernel") else k] = {"dram_bytes_per_launch": e.get("dram_bytes_per_launch"),
                                  "time_us": e.get("time_us"), "dram_GBps": e.get("dram_GBps"),
                                  "source": path}
     json.dump(res, open(out, "w"), indent=1)
