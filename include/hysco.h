@@ -192,6 +192,38 @@ enum { HYSCO_PROF_MATVEC = 0, HYSCO_PROF_UPDATE = 1, HYSCO_PROF_DIR = 2, HYSCO_P
        HYSCO_PROF_RESIDENT = 4, HYSCO_PROF_TRIAL = 5, HYSCO_NPROF = 6 };
 HYSCO_API hysco_status hysco_profile_kernels(hysco_ctx ctx, int32_t reps, int32_t flush_l2, double* avg_ms);
 
+/* ---- Multi-GPU slab decomposition along dim 1 (north_star:
+ * "Large volumes are partitioned ... as slabs along a non-phase-encoding axis",
+ * one-plane halo of the in-plane Laplacian over NCCL, allreduced PCG scalars).
+ * A slab context owns global planes [i0, i0 + cfg->n1) of n1_global; its
+ * images and node arrays are the rank-local slabs ([batch][cfg->n1][n2][...]).
+ * Slab contexts run hysco_solve / hysco_correct / hysco_correct_host (every
+ * rank calls them collectively); the other per-kernel calls return
+ * HYSCO_ERR_STATE on slab contexts.  Results equal the single-GPU solve up to
+ * reduction order. */
+
+/* NCCL unique id (rank 0), to be broadcast to the other ranks by the caller. */
+HYSCO_API hysco_status hysco_nccl_unique_id(unsigned char id_out[128]);
+
+/* One rank of an NCCL slab group (one process per GPU).  nranks == 1 needs no id. */
+HYSCO_API hysco_status hysco_create_slab(const hysco_config* cfg, int32_t rank, int32_t nranks, int64_t n1_global,
+                                         int64_t i0, const unsigned char* nccl_id, void* cuda_stream, hysco_ctx* out);
+
+/* Single-GPU loopback group: cfg describes the WHOLE volume; it is split into
+ * nranks contiguous slabs (rank r owns planes [n1 r / nranks, n1 (r+1) / nranks)),
+ * out[nranks] receives the contexts (one stream, halo exchange by device copies,
+ * allreduce by a fixed-order device sum).  For testing the slab path on one GPU. */
+HYSCO_API hysco_status hysco_create_loopback(const hysco_config* cfg, int32_t nranks, void* cuda_stream,
+                                             hysco_ctx* out);
+
+/* Run a loopback group (all ranks, in rank order); per-rank device pointers. */
+HYSCO_API hysco_status hysco_group_correct(hysco_ctx* ctxs, int32_t nranks, const hysco_ot_opts* ot,
+                                           const hysco_solve_opts* so, void* const* d_b_out,
+                                           void* const* d_Iplus_corr, void* const* d_Iminus_corr,
+                                           hysco_report* reports);
+HYSCO_API hysco_status hysco_group_solve(hysco_ctx* ctxs, int32_t nranks, void* const* d_b_inout,
+                                         const hysco_solve_opts* so, hysco_report* reports);
+
 HYSCO_API const char* hysco_last_error(hysco_ctx ctx);
 HYSCO_API hysco_status hysco_destroy(hysco_ctx ctx);
 HYSCO_API int32_t hysco_version(void);

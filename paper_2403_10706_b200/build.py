@@ -5,7 +5,7 @@ import subprocess
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 SRC = os.path.join(PKG, "csrc", "hysco_api.cu")
-DEPS = [os.path.join(PKG, "csrc", f) for f in ("hysco_api.cu", "hysco_common.cuh", "hysco_kernels.cuh")] + \
+DEPS = [os.path.join(PKG, "csrc", f) for f in sorted(os.listdir(os.path.join(PKG, "csrc")))] + \
        [os.path.join(ROOT, "include", "hysco.h")]
 LIB = os.path.join(PKG, "libhysco.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -25,7 +25,7 @@ def needs_build():
 def build(force=False, verbose=False):
     """Compile csrc/ into paper_2403_10706_b200/libhysco.so; returns the path."""
     if force or needs_build():
-        cmd = [NVCC] + FLAGS + ["-o", LIB + ".tmp", SRC]
+        cmd = [NVCC] + FLAGS + ["-o", LIB + ".tmp", SRC, "-lnccl"]
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)

@@ -9,6 +9,8 @@
 #include "hysco.h"
 #include "hysco_kernels.cuh"
 
+#include <nccl.h>
+
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -76,6 +78,11 @@ struct hysco_ctx_s {
     double* res_part = nullptr;
     unsigned* res_bar = nullptr;
     float* res_pg = nullptr;     // ghost-padded global copy of p (halo source)
+    // slab decomposition (multi-rank)
+    size_t plane_off = 0;        // elements from a pair's buffer start to local plane 0
+    int rank = 0, nranks = 1;
+    double* red = nullptr;       // [2][batch][RED_W] pair totals for the allreduce
+    struct CommBase* comm = nullptr;
 };
 
 static hysco_status set_err(hysco_ctx c, hysco_status s, const std::string& m) {
@@ -167,7 +174,7 @@ static int pick_nch(int P) { return P <= 64 ? 2 : P <= 128 ? 4 : P <= 160 ? 5 : 
 
 template <typename T>
 struct L {
-    static T* b(hysco_ctx c, int k) { return static_cast<T*>(c->buf[k]); }
+    static T* b(hysco_ctx c, int k) { return static_cast<T*>(c->buf[k]) + c->plane_off; }
 
     static void eval(hysco_ctx c, const SolveParams& sp, int mode, const T* bsrc) {
         NCH_SWITCH(c->nch, eval_kernel<T, NCH><<<dim3(c->gx_eval, c->cfg.batch), 256, c->smem_eval, c->stream>>>(
@@ -390,6 +397,300 @@ static void setup_resident(hysco_ctx ctx) {
     ctx->resident = true;
 }
 
+// ---------------------------------------------------------------------------
+// Slab decomposition along dim 1.  Each rank's
+// context owns planes [i0, i0 + n1) of every pair; node arrays carry one halo
+// plane below and above.  Before every in-plane Laplacian application (eval
+// on b, matvec on p, the periodic blur pass along dim 1) the boundary planes
+// are exchanged; after every reduction the pair totals are allreduced and
+// decide_kernel takes the (identical) decision on every rank.  Multi-rank
+// solves are host-orchestrated (loop conditions read back per iteration);
+// two transports: NCCL (one process per GPU) and a single-GPU loopback group
+// (several contexts on one stream) that tests the same kernels and exchanges.
+// ---------------------------------------------------------------------------
+struct CommBase {
+    virtual ~CommBase() {}
+    virtual cudaError_t halo(std::vector<hysco_ctx>& R, int k, bool periodic) = 0;
+    virtual cudaError_t allreduce(std::vector<hysco_ctx>& R, bool with_max) = 0;
+};
+
+// user node array (dense [batch][Nn]) <-> internal buffer (pair stride ps, halo planes)
+static cudaError_t copy_nodes(hysco_ctx c, void* dst, const void* src, bool to_internal, cudaMemcpyKind kind) {
+    const size_t w = (size_t)c->g.Nn * c->esz;
+    if (c->g.ps == c->g.Nn && c->plane_off == 0)
+        return cudaMemcpyAsync(dst, src, (size_t)c->cfg.batch * w, kind, c->stream);
+    const size_t pitch = (size_t)c->g.ps * c->esz, off = c->plane_off * c->esz;
+    if (to_internal)
+        return cudaMemcpy2DAsync((char*)dst + off, pitch, src, w, w, c->cfg.batch, kind, c->stream);
+    return cudaMemcpy2DAsync(dst, w, (const char*)src + off, pitch, w, c->cfg.batch, kind, c->stream);
+}
+
+__global__ void loopback_reduce_kernel(double* const* bufs, int nr, int n, int with_max) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        double s = 0, m = -INFINITY;
+        for (int r = 0; r < nr; r++) {          // fixed rank order: deterministic
+            s += bufs[r][i];
+            if (with_max) m = fmax(m, bufs[r][n + i]);
+        }
+        for (int r = 0; r < nr; r++) {
+            bufs[r][i] = s;
+            if (with_max) bufs[r][n + i] = m;
+        }
+    }
+}
+
+struct LoopbackComm : CommBase {
+    std::vector<hysco_ctx> members;    // rank order; all on one device and one stream
+    double** d_ptrs = nullptr;
+    int refs = 0;                      // member contexts alive
+    cudaStream_t stream = nullptr;     // shared by the members; owned here if created here
+    bool own_stream = false;
+    ~LoopbackComm() override {
+        if (d_ptrs) cudaFree(d_ptrs);
+        if (own_stream && stream) cudaStreamDestroy(stream);
+    }
+    cudaError_t halo(std::vector<hysco_ctx>& R, int k, bool periodic) override {
+        const int n = (int)members.size();
+        for (int r = 0; r < n; r++) {
+            hysco_ctx c = members[r];
+            const size_t plane = (size_t)c->g.n2 * c->g.P * c->esz;
+            for (int p = 0; p < c->cfg.batch; p++) {
+                char* base = (char*)c->buf[k] + (size_t)p * c->g.ps * c->esz;
+                const int lo = r > 0 ? r - 1 : (periodic ? n - 1 : -1);
+                const int hi = r < n - 1 ? r + 1 : (periodic ? 0 : -1);
+                if (lo >= 0) {   // lower halo <- last plane of rank lo
+                    hysco_ctx d = members[lo];
+                    const char* src = (const char*)d->buf[k] + (size_t)p * d->g.ps * d->esz + d->plane_off * d->esz +
+                                      (size_t)(d->g.n1 - 1) * plane;
+                    cudaError_t e = cudaMemcpyAsync(base, src, plane, cudaMemcpyDeviceToDevice, c->stream);
+                    if (e != cudaSuccess) return e;
+                }
+                if (hi >= 0) {   // upper halo <- first plane of rank hi
+                    hysco_ctx d = members[hi];
+                    const char* src = (const char*)d->buf[k] + (size_t)p * d->g.ps * d->esz + d->plane_off * d->esz;
+                    cudaError_t e = cudaMemcpyAsync(base + c->plane_off * c->esz + (size_t)c->g.n1 * plane, src, plane,
+                                                    cudaMemcpyDeviceToDevice, c->stream);
+                    if (e != cudaSuccess) return e;
+                }
+            }
+        }
+        (void)R;
+        return cudaSuccess;
+    }
+    cudaError_t allreduce(std::vector<hysco_ctx>& R, bool with_max) override {
+        hysco_ctx c = members[0];
+        loopback_reduce_kernel<<<1, 256, 0, c->stream>>>(d_ptrs, (int)members.size(), (int)(c->cfg.batch * RED_W),
+                                                         with_max ? 1 : 0);
+        (void)R;
+        return cudaGetLastError();
+    }
+};
+
+struct NcclComm : CommBase {
+    ncclComm_t comm = nullptr;
+    int rank = 0, n = 1;
+    ncclResult_t last = ncclSuccess;
+    ~NcclComm() override {
+        if (comm) ncclCommDestroy(comm);
+    }
+    cudaError_t halo(std::vector<hysco_ctx>& R, int k, bool periodic) override {
+        hysco_ctx c = R[0];
+        const size_t cnt = (size_t)c->g.n2 * c->g.P;
+        const ncclDataType_t ty = c->esz == 8 ? ncclDouble : ncclFloat;
+        const int lo = rank > 0 ? rank - 1 : (periodic ? n - 1 : -1);
+        const int hi = rank < n - 1 ? rank + 1 : (periodic ? 0 : -1);
+        if (n == 1) {                      // periodic self-ring without NCCL
+            if (!periodic) return cudaSuccess;
+            for (int p = 0; p < c->cfg.batch; p++) {
+                char* base = (char*)c->buf[k] + (size_t)p * c->g.ps * c->esz;
+                char* own = base + c->plane_off * c->esz;
+                const size_t pb = cnt * c->esz;
+                cudaMemcpyAsync(base, own + (size_t)(c->g.n1 - 1) * pb, pb, cudaMemcpyDeviceToDevice, c->stream);
+                cudaMemcpyAsync(own + (size_t)c->g.n1 * pb, own, pb, cudaMemcpyDeviceToDevice, c->stream);
+            }
+            return cudaGetLastError();
+        }
+        // phase A: first plane -> lower neighbour, upper halo <- upper neighbour;
+        // phase B: last plane -> upper neighbour, lower halo <- lower neighbour
+        // (this order keeps per-peer send/recv matching right for 2-rank rings)
+        if ((last = ncclGroupStart()) != ncclSuccess) return cudaErrorUnknown;
+        for (int ph = 0; ph < 2; ph++)
+            for (int p = 0; p < c->cfg.batch; p++) {
+                char* base = (char*)c->buf[k] + (size_t)p * c->g.ps * c->esz;
+                char* own = base + c->plane_off * c->esz;
+                const size_t pb = cnt * c->esz;
+                if (ph == 0) {
+                    if (lo >= 0) last = ncclSend(own, cnt, ty, lo, comm, c->stream);
+                    if (hi >= 0) last = ncclRecv(own + (size_t)c->g.n1 * pb, cnt, ty, hi, comm, c->stream);
+                } else {
+                    if (hi >= 0) last = ncclSend(own + (size_t)(c->g.n1 - 1) * pb, cnt, ty, hi, comm, c->stream);
+                    if (lo >= 0) last = ncclRecv(base, cnt, ty, lo, comm, c->stream);
+                }
+            }
+        if ((last = ncclGroupEnd()) != ncclSuccess) return cudaErrorUnknown;
+        return cudaSuccess;
+    }
+    cudaError_t allreduce(std::vector<hysco_ctx>& R, bool with_max) override {
+        hysco_ctx c = R[0];
+        if (n == 1) return cudaSuccess;
+        const size_t cnt = (size_t)c->cfg.batch * RED_W;
+        if ((last = ncclAllReduce(c->red, c->red, cnt, ncclDouble, ncclSum, comm, c->stream)) != ncclSuccess)
+            return cudaErrorUnknown;
+        if (with_max && (last = ncclAllReduce(c->red + cnt, c->red + cnt, cnt, ncclDouble, ncclMax, comm, c->stream)) !=
+                            ncclSuccess)
+            return cudaErrorUnknown;
+        return cudaSuccess;
+    }
+};
+
+// Host-orchestrated multi-rank path: `R` = the contexts this process drives
+// (one for NCCL, all ranks for the loopback group).
+template <typename T>
+struct SlabRun {
+    std::vector<hysco_ctx>& R;
+    CommBase* comm;
+    SolveParams sp;
+    cudaError_t err = cudaSuccess;
+
+    void ok(cudaError_t e) {
+        if (err == cudaSuccess && e != cudaSuccess) err = e;
+    }
+    template <typename F>
+    void each(F fn) {
+        for (hysco_ctx c : R) fn(c);
+        ok(cudaGetLastError());
+    }
+    void reduce_decide(int op, int mode, bool with_max) {
+        ok(comm->allreduce(R, with_max));
+        each([&](hysco_ctx c) {
+            decide_kernel<<<1, 256, 0, c->stream>>>(c->g, c->ctl, sp, op, mode, (int)c->cfg.batch);
+        });
+    }
+    bool cond(int slot) {
+        hysco_ctx c = R[0];
+        ok(cudaMemcpyAsync(c->h_cond + slot, c->dcond + slot, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
+        for (hysco_ctx d : R) ok(cudaStreamSynchronize(d->stream));
+        return err == cudaSuccess && c->h_cond[slot] != 0;
+    }
+    static dim3 gn(hysco_ctx c) { return dim3(c->gx_nodes, c->cfg.batch); }
+
+    void ot(int blur) {
+        each([&](hysco_ctx c) {
+            ot_minmax_kernel<T><<<dim3(c->gx_cells, c->cfg.batch), 256, 0, c->stream>>>(c->g, c->ctl, sp,
+                                                                                         (const T*)c->Ip,
+                                                                                         (const T*)c->Im);
+        });
+        reduce_decide(OP_MINMAX, 0, true);
+        each([&](hysco_ctx c) {
+            ot_column_kernel<T><<<dim3(c->gx_ot, c->cfg.batch), 256, c->smem_ot, c->stream>>>(
+                c->g, c->ctl, (const T*)c->Ip, (const T*)c->Im, L<T>::b(c, blur ? B_TMP : B_B));
+        });
+        if (blur) {
+            const double e = exp(-0.5), w0 = e / (1.0 + 2.0 * e), w1 = 1.0 / (1.0 + 2.0 * e);
+            ok(comm->halo(R, B_TMP, true));
+            each([&](hysco_ctx c) {
+                blur_axis_kernel<T, 1><<<gn(c), 256, 0, c->stream>>>(c->g, c->ctl, 0, w0, w1, L<T>::b(c, B_TMP),
+                                                                    L<T>::b(c, B_R));
+                blur_axis_kernel<T, 1><<<gn(c), 256, 0, c->stream>>>(c->g, c->ctl, 1, w0, w1, L<T>::b(c, B_R),
+                                                                    L<T>::b(c, B_P));
+                blur_axis_kernel<T, 1><<<gn(c), 256, 0, c->stream>>>(c->g, c->ctl, 2, w0, w1, L<T>::b(c, B_P),
+                                                                    L<T>::b(c, B_B));
+            });
+        }
+        each([&](hysco_ctx c) {
+            guard_max_kernel<T, 1><<<gn(c), 256, 0, c->stream>>>(c->g, c->ctl, sp, L<T>::b(c, B_B));
+        });
+        reduce_decide(OP_GUARD, 0, true);
+        each([&](hysco_ctx c) { guard_scale_kernel<T, 1><<<gn(c), 256, 0, c->stream>>>(c->g, c->ctl, L<T>::b(c, B_B)); });
+    }
+    void eval(int mode) {
+        ok(comm->halo(R, B_B, false));
+        each([&](hysco_ctx c) { L<T>::eval(c, sp, mode, L<T>::b(c, B_B)); });
+        reduce_decide(OP_EVAL, mode, false);
+    }
+    void gn() {
+        eval(EVAL_GN_START);
+        while (cond(COND_GN)) {
+            each([&](hysco_ctx c) {
+                NCH_SWITCH(c->nch, pcg_init_kernel<T, NCH><<<gn(c), 256, 0, c->stream>>>(
+                                       c->g, c->ctl, L<T>::b(c, B_GRAD), L<T>::b(c, B_DT), L<T>::b(c, B_X),
+                                       L<T>::b(c, B_R), L<T>::b(c, B_P)));
+            });
+            reduce_decide(OP_PCG_INIT, 0, false);
+            while (cond(COND_PCG)) {
+                ok(comm->halo(R, B_P, false));
+                each([&](hysco_ctx c) {
+                    NCH_SWITCH(c->nch, matvec_kernel<T, NCH, true><<<dim3(c->gx_mv, c->cfg.batch), 256, 0, c->stream>>>(
+                                           c->g, c->ctl, L<T>::b(c, B_DT), L<T>::b(c, B_ET), L<T>::b(c, B_P),
+                                           L<T>::b(c, B_HP)));
+                });
+                reduce_decide(OP_MATVEC, 0, false);
+                each([&](hysco_ctx c) {
+                    NCH_SWITCH(c->nch, pcg_update_kernel<T, NCH><<<gn(c), 256, 0, c->stream>>>(
+                                           c->g, c->ctl, sp, L<T>::b(c, B_DT), L<T>::b(c, B_P), L<T>::b(c, B_HP),
+                                           L<T>::b(c, B_X), L<T>::b(c, B_R)));
+                });
+                reduce_decide(OP_UPDATE, 0, false);
+                each([&](hysco_ctx c) {
+                    NCH_SWITCH(c->nch, pcg_dir_kernel<T, NCH><<<gn(c), 256, 0, c->stream>>>(
+                                           c->g, c->ctl, L<T>::b(c, B_DT), L<T>::b(c, B_R), L<T>::b(c, B_P)));
+                });
+                if (err != cudaSuccess) return;
+            }
+            each([&](hysco_ctx c) {
+                NCH_SWITCH(c->nch, trial_init_kernel<T, NCH><<<gn(c), 256, 0, c->stream>>>(
+                                       c->g, c->ctl, L<T>::b(c, B_GRAD), L<T>::b(c, B_X), L<T>::b(c, B_B),
+                                       L<T>::b(c, B_BOLD)));
+            });
+            reduce_decide(OP_TRIAL, 0, true);
+            while (cond(COND_LS)) {
+                eval(EVAL_TRIAL);
+                each([&](hysco_ctx c) {
+                    NCH_SWITCH(c->nch, ls_retry_kernel<T, NCH><<<gn(c), 256, 0, c->stream>>>(
+                                           c->g, c->ctl, L<T>::b(c, B_X), L<T>::b(c, B_BOLD), L<T>::b(c, B_B)));
+                });
+                if (err != cudaSuccess) return;
+            }
+            each([&](hysco_ctx c) { gn_tail_kernel<<<1, 32, 0, c->stream>>>(c->ctl, (int)c->cfg.batch); });
+            if (err != cudaSuccess) return;
+        }
+    }
+};
+
+// kind 1: solve from b (per-rank user arrays b_io[r]); kind 2: OT + solve + apply.
+template <typename T>
+static hysco_status run_slab_path(std::vector<hysco_ctx>& R, CommBase* comm, int kind, const SolveParams& sp,
+                                  int blur, void* const* b_io, void* const* b_out, void* const* Tp, void* const* Tm) {
+    SlabRun<T> run{R, comm, sp};
+    for (size_t r = 0; r < R.size(); r++) {
+        hysco_ctx c = R[r];
+        run.ok(cudaMemsetAsync(c->launches, 0, sizeof(unsigned long long), c->stream));
+        if (kind == 1) run.ok(copy_nodes(c, c->buf[B_B], b_io[r], true, cudaMemcpyDeviceToDevice));
+    }
+    if (kind == 2) run.ot(blur);
+    run.gn();
+    for (size_t r = 0; r < R.size(); r++) {
+        hysco_ctx c = R[r];
+        if (kind == 1) run.ok(copy_nodes(c, b_io[r], c->buf[B_B], false, cudaMemcpyDeviceToDevice));
+        if (kind == 2) {
+            if ((Tp && Tp[r]) || (Tm && Tm[r]))
+                L<T>::apply(c, L<T>::b(c, B_B), (T*)(Tp ? Tp[r] : nullptr), (T*)(Tm ? Tm[r] : nullptr));
+            if (b_out && b_out[r]) run.ok(copy_nodes(c, b_out[r], c->buf[B_B], false, cudaMemcpyDeviceToDevice));
+        }
+        run.ok(cudaGetLastError());
+        run.ok(cudaMemcpyAsync(c->h_st, c->st, sizeof(PairState) * c->cfg.batch, cudaMemcpyDeviceToHost, c->stream));
+        run.ok(cudaMemcpyAsync(c->h_launches, c->launches, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                               c->stream));
+    }
+    for (hysco_ctx c : R) run.ok(cudaStreamSynchronize(c->stream));
+    if (run.err != cudaSuccess) {
+        for (hysco_ctx c : R) cuda_fail(c, run.err, "slab solve", __LINE__);
+        return HYSCO_ERR_CUDA;
+    }
+    for (hysco_ctx c : R) c->last_launches = (long long)*c->h_launches;
+    return HYSCO_OK;
+}
+
 // GN-PCG solve on buffer B_B, the structure of DESIGN.md "Solve graph".
 template <typename T>
 static void gn_sequence(Runner& r, const SolveParams& sp) {
@@ -583,7 +884,15 @@ void hysco_default_ot_opts(hysco_ot_opts* o) {
 
 int32_t hysco_version(void) { return 1; }
 
-hysco_status hysco_create(const hysco_config* cfg, void* cuda_stream, hysco_ctx* out) {
+}  // extern "C"
+
+// Slab of a multi-rank decomposition along dim 1.
+struct SlabSpec {
+    int rank, nranks;
+    long long n1g, i0;
+};
+
+static hysco_status create_impl(const hysco_config* cfg, const SlabSpec* slab, void* cuda_stream, hysco_ctx* out) {
     if (!cfg || !out) return HYSCO_ERR_ARG;
     *out = nullptr;
     if (cfg->n1 < 1 || cfg->n2 < 1 || cfg->n3 < 2 || cfg->batch < 1 || cfg->n3 > 8192 ||
@@ -617,6 +926,24 @@ hysco_status hysco_create(const hysco_config* cfg, void* cuda_stream, hysco_ctx*
     g.ih2sq = 1.0 / (cfg->h2 * cfg->h2);
     g.ih3sq = 1.0 / (cfg->h3 * cfg->h3);
     g.ih3 = 1.0 / cfg->h3;
+    g.ps = g.Nn;
+    g.i0 = 0;
+    g.n1g = g.n1;
+    g.slab = 0;
+    if (slab) {
+        if (slab->nranks < 1 || slab->rank < 0 || slab->rank >= slab->nranks || slab->i0 < 0 ||
+            slab->i0 + cfg->n1 > slab->n1g) {
+            delete ctx;
+            return HYSCO_ERR_SHAPE;
+        }
+        g.i0 = (int)slab->i0;
+        g.n1g = (int)slab->n1g;
+        g.slab = 1;
+        g.ps = (long long)(g.n1 + 2) * g.n2 * g.P;      // one halo plane below and above
+        ctx->plane_off = (size_t)g.n2 * g.P;
+        ctx->rank = slab->rank;
+        ctx->nranks = slab->nranks;
+    }
 
     hysco_status st;
     auto bail = [&](hysco_status s) {
@@ -638,7 +965,7 @@ hysco_status hysco_create(const hysco_config* cfg, void* cuda_stream, hysco_ctx*
     }
     st = cfg->dtype == HYSCO_F64 ? setup_typed<double>(ctx) : setup_typed<float>(ctx);
     if (st != HYSCO_OK) return bail(st);
-    const size_t nn = (size_t)cfg->batch * g.Nn * ctx->esz, nc = (size_t)cfg->batch * g.Nc * ctx->esz;
+    const size_t nn = (size_t)cfg->batch * g.ps * ctx->esz, nc = (size_t)cfg->batch * g.Nc * ctx->esz;
     auto dalloc = [&](void** p, size_t n) -> bool {
         cudaError_t e = cudaMalloc(p, n);
         if (e != cudaSuccess) {
@@ -657,8 +984,11 @@ hysco_status hysco_create(const hysco_config* cfg, void* cuda_stream, hysco_ctx*
         !dalloc((void**)&ctx->part, sizeof(double) * ctx->ctl.part_stride * cfg->batch) ||
         !dalloc((void**)&ctx->ctr, sizeof(unsigned) * cfg->batch) || !dalloc((void**)&ctx->gctr, sizeof(unsigned)) ||
         !dalloc((void**)&ctx->launches, sizeof(unsigned long long)) ||
-        !dalloc((void**)&ctx->dcond, sizeof(unsigned) * NCOND))
+        !dalloc((void**)&ctx->dcond, sizeof(unsigned) * NCOND) ||
+        !dalloc((void**)&ctx->red, sizeof(double) * 2 * RED_W * cfg->batch))
         return bail(HYSCO_ERR_NOMEM);
+    if (g.slab)   // halo planes must start at zero (Neumann ends never read them, blur ring does)
+        for (int k = 0; k < NBUF; k++) cudaMemset(ctx->buf[k], 0, nn);
     if (cudaMallocHost((void**)&ctx->h_st, sizeof(PairState) * cfg->batch) != cudaSuccess ||
         cudaMallocHost((void**)&ctx->h_launches, sizeof(unsigned long long)) != cudaSuccess ||
         cudaMallocHost((void**)&ctx->h_cond, sizeof(unsigned) * NCOND) != cudaSuccess) {
@@ -681,9 +1011,17 @@ hysco_status hysco_create(const hysco_config* cfg, void* cuda_stream, hysco_ctx*
     ctx->ctl.launches = ctx->launches;
     ctx->ctl.dcond = ctx->dcond;
     ctx->ctl.use_graph = 0;
-    setup_resident(ctx);
+    ctx->ctl.red = ctx->red;
+    ctx->ctl.defer = g.slab ? 1 : 0;     // slab runs are host-orchestrated: always decide after the allreduce
+    if (!g.slab) setup_resident(ctx);
     *out = ctx;
     return HYSCO_OK;
+}
+
+extern "C" {
+
+hysco_status hysco_create(const hysco_config* cfg, void* cuda_stream, hysco_ctx* out) {
+    return create_impl(cfg, nullptr, cuda_stream, out);
 }
 
 hysco_status hysco_bind_images(hysco_ctx ctx, const void* d_Iplus, const void* d_Iminus) {
@@ -704,6 +1042,7 @@ static hysco_status need_images(hysco_ctx ctx) {
 
 hysco_status hysco_ot_init(hysco_ctx ctx, const hysco_ot_opts* opts, void* d_b_out) {
     CHECK_CTX();
+    if (ctx->g.slab) return set_err(ctx, HYSCO_ERR_STATE, "slab contexts support solve / correct / correct_host");
     if (hysco_status s = need_images(ctx)) return s;
     if (!d_b_out || !aligned16(d_b_out)) return set_err(ctx, HYSCO_ERR_ARG, "d_b_out must be 16-byte aligned");
     hysco_ot_opts o;
@@ -723,6 +1062,7 @@ hysco_status hysco_ot_init(hysco_ctx ctx, const hysco_ot_opts* opts, void* d_b_o
 
 hysco_status hysco_objective_grad(hysco_ctx ctx, const void* d_b, double* JDSP, void* d_grad) {
     CHECK_CTX();
+    if (ctx->g.slab) return set_err(ctx, HYSCO_ERR_STATE, "slab contexts support solve / correct / correct_host");
     if (hysco_status s = need_images(ctx)) return s;
     if (!d_b || !aligned16(d_b) || (d_grad && !aligned16(d_grad)))
         return set_err(ctx, HYSCO_ERR_ARG, "pointers must be 16-byte aligned");
@@ -756,6 +1096,7 @@ hysco_status hysco_objective_grad(hysco_ctx ctx, const void* d_b, double* JDSP, 
 
 hysco_status hysco_hessvec(hysco_ctx ctx, const void* d_q, void* d_Hq) {
     CHECK_CTX();
+    if (ctx->g.slab) return set_err(ctx, HYSCO_ERR_STATE, "slab contexts support solve / correct / correct_host");
     if (!ctx->state_valid) return set_err(ctx, HYSCO_ERR_STATE, "hessvec needs a feasible objective_grad first");
     if (!d_q || !d_Hq || !aligned16(d_q) || !aligned16(d_Hq) || d_q == d_Hq)
         return set_err(ctx, HYSCO_ERR_ARG, "d_q/d_Hq must be distinct, 16-byte aligned");
@@ -767,6 +1108,7 @@ hysco_status hysco_hessvec(hysco_ctx ctx, const void* d_q, void* d_Hq) {
 
 hysco_status hysco_hess_diag(hysco_ctx ctx, void* d_diag) {
     CHECK_CTX();
+    if (ctx->g.slab) return set_err(ctx, HYSCO_ERR_STATE, "slab contexts support solve / correct / correct_host");
     if (!ctx->state_valid) return set_err(ctx, HYSCO_ERR_STATE, "hess_diag needs a feasible objective_grad first");
     if (!d_diag || !aligned16(d_diag)) return set_err(ctx, HYSCO_ERR_ARG, "d_diag must be 16-byte aligned");
     if (ctx->cfg.dtype == HYSCO_F64) L<double>::diag(ctx, (double*)d_diag);
@@ -777,6 +1119,7 @@ hysco_status hysco_hess_diag(hysco_ctx ctx, void* d_diag) {
 
 hysco_status hysco_apply(hysco_ctx ctx, const void* d_b, void* d_Iplus_corr, void* d_Iminus_corr) {
     CHECK_CTX();
+    if (ctx->g.slab) return set_err(ctx, HYSCO_ERR_STATE, "slab contexts support solve / correct / correct_host");
     if (hysco_status s = need_images(ctx)) return s;
     if (!d_b || !aligned16(d_b) || (d_Iplus_corr && !aligned16(d_Iplus_corr)) ||
         (d_Iminus_corr && !aligned16(d_Iminus_corr)))
@@ -807,8 +1150,21 @@ static hysco_status solve_common(hysco_ctx ctx, int kind, const hysco_ot_opts* o
     key.ptr[3] = b_out;
     key.ptr[4] = Tp;
     key.ptr[5] = Tm;
-    hysco_status s = ctx->cfg.dtype == HYSCO_F64 ? run_path<double>(ctx, key, b_io, b_out, Tp, Tm)
-                                                 : run_path<float>(ctx, key, b_io, b_out, Tp, Tm);
+    hysco_status s;
+    if (ctx->g.slab) {
+        if (!dynamic_cast<NcclComm*>(ctx->comm))
+            return set_err(ctx, HYSCO_ERR_STATE, "loopback slab contexts are driven with hysco_group_*");
+        std::vector<hysco_ctx> R{ctx};
+        void* const bi[1] = {b_io};
+        void* const bo[1] = {b_out};
+        void* const tp[1] = {Tp};
+        void* const tm[1] = {Tm};
+        s = ctx->cfg.dtype == HYSCO_F64 ? run_slab_path<double>(R, ctx->comm, kind, key.sp, key.blur, bi, bo, tp, tm)
+                                        : run_slab_path<float>(R, ctx->comm, kind, key.sp, key.blur, bi, bo, tp, tm);
+    } else {
+        s = ctx->cfg.dtype == HYSCO_F64 ? run_path<double>(ctx, key, b_io, b_out, Tp, Tm)
+                                        : run_path<float>(ctx, key, b_io, b_out, Tp, Tm);
+    }
     if (s != HYSCO_OK) return s;
     bool inf = false;
     fill_reports(ctx, reports, &inf);
@@ -845,7 +1201,8 @@ hysco_status hysco_correct_host(hysco_ctx ctx, const void* h_Iplus, const void* 
     hysco_status s = solve_common(ctx, 2, ot, so, nullptr, nullptr, h_Iplus_corr ? ctx->own_Tp : nullptr,
                                   h_Iminus_corr ? ctx->own_Tm : nullptr, reports);
     if (s < 0) return s;
-    if (h_b_out) CK(cudaMemcpyAsync(h_b_out, ctx->buf[B_B], nn, cudaMemcpyDeviceToHost, ctx->stream));
+    if (h_b_out) CK(copy_nodes(ctx, h_b_out, ctx->buf[B_B], false, cudaMemcpyDeviceToHost));
+    (void)nn;
     if (h_Iplus_corr) CK(cudaMemcpyAsync(h_Iplus_corr, ctx->own_Tp, nc, cudaMemcpyDeviceToHost, ctx->stream));
     if (h_Iminus_corr) CK(cudaMemcpyAsync(h_Iminus_corr, ctx->own_Tm, nc, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -853,6 +1210,125 @@ hysco_status hysco_correct_host(hysco_ctx ctx, const void* h_Iplus, const void* 
 }
 
 int64_t hysco_last_launch_count(hysco_ctx ctx) { return ctx ? ctx->last_launches : -1; }
+
+hysco_status hysco_nccl_unique_id(unsigned char id_out[128]) {
+    if (!id_out) return HYSCO_ERR_ARG;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return HYSCO_ERR_NCCL;
+    static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id size");
+    memcpy(id_out, &id, 128);
+    return HYSCO_OK;
+}
+
+hysco_status hysco_create_slab(const hysco_config* cfg, int32_t rank, int32_t nranks, int64_t n1_global, int64_t i0,
+                               const unsigned char* nccl_id, void* cuda_stream, hysco_ctx* out) {
+    if (!cfg || !out || (nranks > 1 && !nccl_id)) return HYSCO_ERR_ARG;
+    SlabSpec sl{rank, nranks, n1_global, i0};
+    hysco_status st = create_impl(cfg, &sl, cuda_stream, out);
+    if (st != HYSCO_OK) return st;
+    hysco_ctx ctx = *out;
+    NcclComm* nc = new NcclComm();
+    nc->rank = rank;
+    nc->n = nranks;
+    ctx->comm = nc;
+    if (nranks > 1) {
+        ncclUniqueId id;
+        memcpy(&id, nccl_id, 128);
+        if (ncclCommInitRank(&nc->comm, nranks, id, rank) != ncclSuccess) {
+            ctx->err = "ncclCommInitRank failed";
+            hysco_destroy(ctx);
+            *out = nullptr;
+            return HYSCO_ERR_NCCL;
+        }
+    }
+    return HYSCO_OK;
+}
+
+hysco_status hysco_create_loopback(const hysco_config* cfg, int32_t nranks, void* cuda_stream, hysco_ctx* out) {
+    if (!cfg || !out || nranks < 1 || nranks > cfg->n1) return HYSCO_ERR_ARG;
+    LoopbackComm* lb = new LoopbackComm();
+    cudaStream_t stream = (cudaStream_t)cuda_stream;
+    bool own = false;
+    if (!stream) {
+        if (cudaSetDevice(cfg->device) != cudaSuccess || cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking) != cudaSuccess) {
+            delete lb;
+            cudaGetLastError();
+            return HYSCO_ERR_CUDA;
+        }
+        own = true;
+    }
+    for (int r = 0; r < nranks; r++) {
+        const int64_t i0 = cfg->n1 * r / nranks, i1 = cfg->n1 * (r + 1) / nranks;
+        hysco_config c = *cfg;
+        c.n1 = i1 - i0;
+        SlabSpec sl{r, nranks, cfg->n1, i0};
+        hysco_status st = create_impl(&c, &sl, stream, &out[r]);
+        if (st != HYSCO_OK) {
+            if (r == 0) {
+                delete lb;                       // no member holds it yet
+            } else {
+                for (int q = 0; q < r; q++) hysco_destroy(out[q]);   // the last one frees lb
+            }
+            return st;
+        }
+        out[r]->comm = lb;
+        lb->members.push_back(out[r]);
+        lb->refs++;
+    }
+    lb->stream = stream;                   // destroyed with the last member (~LoopbackComm)
+    lb->own_stream = own;
+    std::vector<double*> ptrs;
+    for (auto* m : lb->members) ptrs.push_back(m->red);
+    if (cudaMalloc(&lb->d_ptrs, sizeof(double*) * nranks) != cudaSuccess ||
+        cudaMemcpy(lb->d_ptrs, ptrs.data(), sizeof(double*) * nranks, cudaMemcpyHostToDevice) != cudaSuccess) {
+        for (int q = 0; q < nranks; q++) hysco_destroy(out[q]);
+        return HYSCO_ERR_NOMEM;
+    }
+    return HYSCO_OK;
+}
+
+static hysco_status group_common(hysco_ctx* ctxs, int32_t n, int kind, const hysco_ot_opts* ot,
+                                 const hysco_solve_opts* so, void* const* b_io, void* const* b_out,
+                                 void* const* Tp, void* const* Tm, hysco_report* reports) {
+    if (!ctxs || n < 1) return HYSCO_ERR_ARG;
+    LoopbackComm* lb = dynamic_cast<LoopbackComm*>(ctxs[0]->comm);
+    if (!lb || (int)lb->members.size() != n) return set_err(ctxs[0], HYSCO_ERR_STATE, "not a loopback group");
+    for (int r = 0; r < n; r++) {
+        hysco_ctx ctx = ctxs[r];
+        if (ctx != lb->members[r]) return set_err(ctxs[0], HYSCO_ERR_ARG, "contexts must be passed in rank order");
+        if (ctx->poisoned) return HYSCO_ERR_CUDA;
+        if (hysco_status s = need_images(ctx)) return s;
+    }
+    hysco_solve_opts o;
+    hysco_default_solve_opts(&o);
+    if (so) o = *so;
+    hysco_ot_opts t;
+    hysco_default_ot_opts(&t);
+    if (ot) t = *ot;
+    if (hysco_status s = check_opts(ctxs[0], o, t)) return s;
+    std::vector<hysco_ctx> R(ctxs, ctxs + n);
+    cudaSetDevice(ctxs[0]->cfg.device);
+    const SolveParams sp = to_params(o, t);
+    hysco_status s = ctxs[0]->cfg.dtype == HYSCO_F64
+                         ? run_slab_path<double>(R, lb, kind, sp, t.blur ? 1 : 0, b_io, b_out, Tp, Tm)
+                         : run_slab_path<float>(R, lb, kind, sp, t.blur ? 1 : 0, b_io, b_out, Tp, Tm);
+    if (s != HYSCO_OK) return s;
+    bool inf = false;
+    fill_reports(ctxs[0], reports, &inf);
+    return inf ? HYSCO_INFEASIBLE : HYSCO_OK;
+}
+
+hysco_status hysco_group_correct(hysco_ctx* ctxs, int32_t nranks, const hysco_ot_opts* ot, const hysco_solve_opts* so,
+                                 void* const* d_b_out, void* const* d_Iplus_corr, void* const* d_Iminus_corr,
+                                 hysco_report* reports) {
+    return group_common(ctxs, nranks, 2, ot, so, nullptr, d_b_out, d_Iplus_corr, d_Iminus_corr, reports);
+}
+
+hysco_status hysco_group_solve(hysco_ctx* ctxs, int32_t nranks, void* const* d_b_inout, const hysco_solve_opts* so,
+                               hysco_report* reports) {
+    if (!d_b_inout) return HYSCO_ERR_ARG;
+    return group_common(ctxs, nranks, 1, nullptr, so, d_b_inout, nullptr, nullptr, nullptr, reports);
+}
 
 }  // extern "C"
 
@@ -962,6 +1438,16 @@ hysco_status hysco_destroy(hysco_ctx ctx) {
     if (ctx->res_part) cudaFree(ctx->res_part);
     if (ctx->res_bar) cudaFree(ctx->res_bar);
     if (ctx->res_pg) cudaFree(ctx->res_pg);
+    if (ctx->red) cudaFree(ctx->red);
+    if (ctx->comm) {
+        if (LoopbackComm* lb = dynamic_cast<LoopbackComm*>(ctx->comm)) {
+            for (auto& m : lb->members)
+                if (m == ctx) m = nullptr;
+            if (--lb->refs == 0) delete lb;
+        } else {
+            delete ctx->comm;
+        }
+    }
     if (ctx->h_st) cudaFreeHost(ctx->h_st);
     if (ctx->h_launches) cudaFreeHost(ctx->h_launches);
     if (ctx->h_cond) cudaFreeHost(ctx->h_cond);

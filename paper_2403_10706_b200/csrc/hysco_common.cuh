@@ -23,7 +23,16 @@ struct Geom {
     double ahd;          // alpha * hd
     double bh2;          // beta * hd / 2
     double ih1sq, ih2sq, ih3sq, ih3;
+    // slab decomposition along dim 1: this rank owns global
+    // planes [i0, i0 + n1) of n1g; node arrays then carry one halo plane on
+    // each side and a pair stride ps = (n1 + 2) n2 P (ps = Nn without slabs).
+    long long ps;
+    int i0, n1g, slab;
 };
+
+// in-plane neighbours along dim 1 exist (homogeneous Neumann, R3), global index
+__device__ __forceinline__ bool has_im(const Geom& g, int i) { return g.i0 + i > 0; }
+__device__ __forceinline__ bool has_ip(const Geom& g, int i) { return g.i0 + i < g.n1g - 1; }
 
 // Device-resident per-pair solver state (no host round trip during a solve).
 struct PairState {
@@ -64,7 +73,11 @@ struct Ctl {
     cudaGraphConditionalHandle h[NCOND];
     int use_graph;                 // 1: set graph conditionals from device code
     int part_stride;               // doubles per pair in `part`
+    int defer;                     // 1 (multi-rank): last blocks store pair totals in `red`,
+                                   //   decisions run in decide_kernel after the allreduce
+    double* red;                   // [batch][RED_W] pair totals (multi-rank)
 };
+constexpr int RED_W = 8;
 
 enum { STOP_MAXITER = 0, STOP_GRAD = 1, STOP_DJ = 2, STOP_DB = 3, STOP_LSFAIL = 4, STOP_INFEASIBLE = 5 };
 
@@ -179,6 +192,25 @@ __device__ __forceinline__ NodeIdx node_idx(const Geom& g, long long t) {
     r.i = (int)(r.col / g.n2);
     r.j = (int)(r.col - (long long)r.i * g.n2);
     return r;
+}
+
+}  // namespace hysco
+
+namespace hysco {
+
+// ---------------------------------------------------------------------------
+// Device-side decisions that follow each reduction (GN / PCG / Armijo control,
+// OT shift, guard).  Single rank: called by the reducing kernel's last block.
+// Multi-rank (Ctl::defer): the last block stores the pair totals in `red`
+// (sums in red[pair][.], maxima in red[batch + pair][.]); the host allreduces
+// them and decide_kernel calls the same function on the global totals.
+// ---------------------------------------------------------------------------
+enum { OP_EVAL = 0, OP_PCG_INIT = 1, OP_MATVEC = 2, OP_UPDATE = 3, OP_TRIAL = 4, OP_MINMAX = 5, OP_GUARD = 6 };
+
+// store totals for the allreduce: k < nsum -> sum part, else max part
+__device__ __forceinline__ void store_red(const Ctl& c, int pair, int batch, const double* tot, int nsum, int nmax) {
+    for (int k = 0; k < nsum; k++) c.red[(size_t)pair * RED_W + k] = tot[k];
+    for (int k = 0; k < nmax; k++) c.red[(size_t)(batch + pair) * RED_W + k] = tot[nsum + k];
 }
 
 }  // namespace hysco

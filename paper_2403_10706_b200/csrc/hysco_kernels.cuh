@@ -55,11 +55,77 @@ __device__ __forceinline__ float diff_h3(float b0, float b1, const Geom& g) { re
 __device__ __forceinline__ double diff_h3(double b0, double b1, const Geom& g) { return (b1 - b0) / g.h3; }
 
 // diag of the in-plane (dims 1,2) Neumann Laplacian at column (i, j) (R3)
-__device__ __forceinline__ double diag_lxy(const Geom& g, int i, int j) {
-    return (double)((i > 0) + (i < g.n1 - 1)) * g.ih1sq + (double)((j > 0) + (j < g.n2 - 1)) * g.ih2sq;
+__device__ __forceinline__ double diag_lxy(const Geom& g, int i, int j) {   // i: local plane
+    return (double)(has_im(g, i) + has_ip(g, i)) * g.ih1sq + (double)((j > 0) + (j < g.n2 - 1)) * g.ih2sq;
 }
 
 enum { EVAL_PLAIN = 0, EVAL_GN_START = 1, EVAL_TRIAL = 2 };
+
+// After an evaluation: objective parts (Eq.(2)-(6)), then GN start / Armijo
+// acceptance (R15) and the R16 stop rules.  tot = [sum r^2, b^T L b, sum phi,
+// ||grad||^2, infeasible (> 0 if any |Db| >= 1)].
+__device__ inline void decide_eval(const Geom& g, const Ctl& c, const SolveParams& sp, int mode, PairState& s,
+                                   const double* tot) {
+    const bool active = (mode != EVAL_TRIAL) || s.ls_active;
+    if (active) {
+        const bool inf = tot[4] > 0.0;
+        s.D = 0.5 * g.hd * tot[0];
+        s.S = 0.5 * g.hd * tot[1];
+        s.P = inf ? INFINITY : 0.5 * g.hd * tot[2];
+        s.infeasible = inf ? 1 : 0;
+        s.J = inf ? INFINITY : s.D + g.alpha * s.S + g.beta * s.P;
+        s.gnorm2 = tot[3];
+    }
+    if (mode == EVAL_GN_START) {
+        s.f_evals = 1;
+        s.h_evals = 0;
+        s.pcg_iters = 0;
+        s.ls_halvings = 0;
+        s.gn_k = 0;
+        s.J_acc = s.J;
+        s.J_prev = s.J;
+        s.g0norm = sqrt(s.gnorm2);
+        s.relres = 0.0;
+        s.stop_reason = s.infeasible ? STOP_INFEASIBLE : STOP_MAXITER;
+        s.gn_active = (!s.infeasible && sp.max_gn > 0) ? 1 : 0;
+        s.pcg_active = 0;
+        s.ls_active = 0;
+    } else if (mode == EVAL_TRIAL && active) {
+        if (s.ls_restore) {                       // line search failed: state restored at b_old
+            s.ls_active = 0;
+            s.gn_active = 0;
+        } else {
+            s.f_evals += 1;
+            if (!s.infeasible && (!sp.armijo || s.J <= s.J_acc + sp.c1 * s.gamma * s.gq)) {   // Armijo (R15)
+                s.J_prev = s.J_acc;
+                s.J_acc = s.J;
+                s.gn_k += 1;
+                s.ls_active = 0;
+                int stop = -1;
+                if (!sp.fixed) {                  // R16 stopping rules
+                    if (sqrt(s.gnorm2) <= sp.tol_grad_rel * s.g0norm) stop = STOP_GRAD;
+                    else if (fabs(s.J_prev - s.J) <= sp.tol_dJ_rel * fabs(s.J_prev)) stop = STOP_DJ;
+                    else if (s.gamma * s.qmax <= sp.tol_db_rel * g.h3) stop = STOP_DB;
+                }
+                if (stop >= 0) {
+                    s.stop_reason = stop;
+                    s.gn_active = 0;
+                } else {
+                    s.gn_active = s.gn_k < sp.max_gn ? 1 : 0;
+                }
+            } else {
+                s.ls_tries += 1;
+                if (s.ls_tries < sp.ls_max) {
+                    s.gamma *= 0.5;
+                    s.ls_halvings += 1;
+                } else {
+                    s.stop_reason = STOP_LSFAIL;
+                    s.ls_restore = 1;             // next pass: b = b_old, re-evaluate, stop
+                }
+            }
+        }
+    }
+}
 
 // ---------------------------------------------------------------------------
 // A4 fused evaluation: one warp per PE column, the
@@ -145,13 +211,13 @@ __global__ void __launch_bounds__(256, 4) eval_kernel(Geom g, Ctl c, SolveParams
         for (long long col = (long long)blockIdx.x * nwb + wid; col < g.ncol; col += (long long)gridDim.x * nwb) {
             const T* ip = Ip + (size_t)pair * g.Nc + col * n3;
             const T* im = Im + (size_t)pair * g.Nc + col * n3;
-            const size_t ob = (size_t)pair * g.Nn + (size_t)col * P;
+            const size_t ob = (size_t)pair * g.ps + (size_t)col * P;
             const T* bc = bb + ob;
             T* gc = grad + ob;
             T* dc = dt + ob;
             T* ec = et + ob;
             const int i = (int)(col / n2), j = (int)(col - (long long)i * n2);
-            const bool him = i > 0, hip = i < g.n1 - 1, hjm = j > 0, hjp = j < n2 - 1;
+            const bool him = has_im(g, i), hip = has_ip(g, i), hjm = j > 0, hjp = j < n2 - 1;
             for (int k = lane; k < n3; k += 32) {
                 sIp[k] = ip[k];
                 sIm[k] = im[k];
@@ -249,69 +315,15 @@ __global__ void __launch_bounds__(256, 4) eval_kernel(Geom g, Ctl c, SolveParams
     double v[5] = {aD, aS, aP, aG, aInf}, tot[5];
     if (!pair_reduce<5, 0x10u>(c, v, tot)) return;
     if (threadIdx.x != 0) return;
-    PairState& s = c.st[pair];
-    if (active) {
-        const bool inf = tot[4] > 0.0;
-        s.D = 0.5 * g.hd * tot[0];
-        s.S = 0.5 * g.hd * tot[1];
-        s.P = inf ? INFINITY : 0.5 * g.hd * tot[2];
-        s.infeasible = inf ? 1 : 0;
-        s.J = inf ? INFINITY : s.D + g.alpha * s.S + g.beta * s.P;
-        s.gnorm2 = tot[3];
+    if (c.defer) {                       // multi-rank: decide after the allreduce (inf flag summed)
+        store_red(c, pair, gridDim.y, tot, 5, 0);
+        return;
     }
-    if (mode == EVAL_GN_START) {
-        s.f_evals = 1;
-        s.h_evals = 0;
-        s.pcg_iters = 0;
-        s.ls_halvings = 0;
-        s.gn_k = 0;
-        s.J_acc = s.J;
-        s.J_prev = s.J;
-        s.g0norm = sqrt(s.gnorm2);
-        s.relres = 0.0;
-        s.stop_reason = s.infeasible ? STOP_INFEASIBLE : STOP_MAXITER;
-        s.gn_active = (!s.infeasible && sp.max_gn > 0) ? 1 : 0;
-        s.pcg_active = 0;
-        s.ls_active = 0;
-        if (last_pair(c)) set_cond(c, COND_GN, any_pair(c, gridDim.y, [](volatile PairState* q) { return q->gn_active != 0; }));
-    } else if (mode == EVAL_TRIAL) {
-        if (active) {
-            if (s.ls_restore) {                       // line search failed: state restored at b_old
-                s.ls_active = 0;
-                s.gn_active = 0;
-            } else {
-                s.f_evals += 1;
-                if (!s.infeasible && (!sp.armijo || s.J <= s.J_acc + sp.c1 * s.gamma * s.gq)) {   // Armijo (R15)
-                    s.J_prev = s.J_acc;
-                    s.J_acc = s.J;
-                    s.gn_k += 1;
-                    s.ls_active = 0;
-                    int stop = -1;
-                    if (!sp.fixed) {                  // R16 stopping rules
-                        if (sqrt(s.gnorm2) <= sp.tol_grad_rel * s.g0norm) stop = STOP_GRAD;
-                        else if (fabs(s.J_prev - s.J) <= sp.tol_dJ_rel * fabs(s.J_prev)) stop = STOP_DJ;
-                        else if (s.gamma * s.qmax <= sp.tol_db_rel * g.h3) stop = STOP_DB;
-                    }
-                    if (stop >= 0) {
-                        s.stop_reason = stop;
-                        s.gn_active = 0;
-                    } else {
-                        s.gn_active = s.gn_k < sp.max_gn ? 1 : 0;
-                    }
-                } else {
-                    s.ls_tries += 1;
-                    if (s.ls_tries < sp.ls_max) {
-                        s.gamma *= 0.5;
-                        s.ls_halvings += 1;
-                    } else {
-                        s.stop_reason = STOP_LSFAIL;
-                        s.ls_restore = 1;             // next pass: b = b_old, re-evaluate, stop
-                    }
-                }
-            }
-        }
-        if (last_pair(c)) set_cond(c, COND_LS, any_pair(c, gridDim.y, [](volatile PairState* q) { return q->ls_active != 0; }));
-    }
+    decide_eval(g, c, sp, mode, c.st[pair], tot);
+    if (mode == EVAL_GN_START && last_pair(c))
+        set_cond(c, COND_GN, any_pair(c, gridDim.y, [](volatile PairState* q) { return q->gn_active != 0; }));
+    if (mode == EVAL_TRIAL && last_pair(c))
+        set_cond(c, COND_LS, any_pair(c, gridDim.y, [](volatile PairState* q) { return q->ls_active != 0; }));
 }
 
 // ---------------------------------------------------------------------------
@@ -329,7 +341,7 @@ __global__ void __launch_bounds__(256) apply_kernel(Geom g, Ctl c, const T* __re
     T* sIp = reinterpret_cast<T*>(smem_raw) + (size_t)wid * (2 * n3 + P);
     T* sIm = sIp + n3;
     T* sb = sIm + n3;
-    const size_t pc = (size_t)pair * g.Nc, pn = (size_t)pair * g.Nn;
+    const size_t pc = (size_t)pair * g.Nc, pn = (size_t)pair * g.ps;
     for (long long col = (long long)blockIdx.x * nwb + wid; col < g.ncol; col += (long long)gridDim.x * nwb) {
         const size_t oc = pc + col * n3, on = pn + col * P;
         for (int k = lane; k < n3; k += 32) {
@@ -357,6 +369,14 @@ __global__ void __launch_bounds__(256) apply_kernel(Geom g, Ctl c, const T* __re
 // A1 OT initialisation
 // ---------------------------------------------------------------------------
 
+// positivity shift (R6): tot = [max(-v), max(v)] over both images of the pair
+__device__ inline void decide_minmax(const SolveParams& sp, PairState& s, const double* tot) {
+    s.vmin = -tot[0];
+    s.vmax = tot[1];
+    s.degenerate = (s.vmax == s.vmin) ? 1 : 0;
+    s.shift = -s.vmin + sp.ot_eps * (s.vmax - s.vmin);
+}
+
 // Positivity shift (R6): per pair, min/max over I+ and I-.
 template <typename T>
 __global__ void __launch_bounds__(256) ot_minmax_kernel(Geom g, Ctl c, SolveParams sp, const T* __restrict__ Ip,
@@ -374,11 +394,11 @@ __global__ void __launch_bounds__(256) ot_minmax_kernel(Geom g, Ctl c, SolvePara
     double v[2] = {mn, mx}, tot[2];
     if (!pair_reduce<2, 0x3u>(c, v, tot)) return;
     if (threadIdx.x != 0) return;
-    PairState& s = c.st[pair];
-    s.vmin = -tot[0];
-    s.vmax = tot[1];
-    s.degenerate = (s.vmax == s.vmin) ? 1 : 0;
-    s.shift = -s.vmin + sp.ot_eps * (s.vmax - s.vmin);
+    if (c.defer) {
+        store_red(c, pair, gridDim.y, tot, 0, 2);
+        return;
+    }
+    decide_minmax(sp, c.st[pair], tot);
 }
 
 // Pseudo-inverse of a piecewise-linear CDF (R8):
@@ -407,7 +427,7 @@ __global__ void __launch_bounds__(256) ot_column_kernel(Geom g, Ctl c, const T* 
     const int n3 = g.n3, P = g.P;
     double* Cp = reinterpret_cast<double*>(smem_raw) + (size_t)wid * 2 * P;
     double* Cm = Cp + P;
-    const size_t pc = (size_t)pair * g.Nc, pn = (size_t)pair * g.Nn;
+    const size_t pc = (size_t)pair * g.Nc, pn = (size_t)pair * g.ps;
     const double shift = c.st[pair].shift;
     const bool degen = c.st[pair].degenerate != 0;
     for (long long col = (long long)blockIdx.x * nwb + wid; col < g.ncol; col += (long long)gridDim.x * nwb) {
@@ -473,3 +493,54 @@ __global__ void __launch_bounds__(256) ot_column_kernel(Geom g, Ctl c, const T* 
 
 #include "hysco_nodes.cuh"
 #include "hysco_resident.cuh"
+
+namespace hysco {
+
+// Multi-rank decisions (Ctl::defer): one thread per pair applies the decision
+// of `op` to the allreduced totals, then the loop condition is set (host-read
+// mirror `dcond`; multi-rank solves are host-orchestrated).
+__global__ void decide_kernel(Geom g, Ctl c, SolveParams sp, int op, int mode, int batch) {
+    count_launch(c);
+    for (int p = threadIdx.x; p < batch; p += blockDim.x) {
+        double tot[RED_W];
+        const double* rs = c.red + (size_t)p * RED_W;
+        const double* rm = c.red + (size_t)(batch + p) * RED_W;
+        PairState& s = c.st[p];
+        switch (op) {
+            case OP_EVAL:
+                for (int k = 0; k < 5; k++) tot[k] = rs[k];
+                decide_eval(g, c, sp, mode, s, tot);
+                break;
+            case OP_PCG_INIT:
+                decide_pcg_init(s, rs);
+                break;
+            case OP_MATVEC:
+                decide_matvec(s, rs);
+                break;
+            case OP_UPDATE:
+                decide_update(sp, s, rs);
+                break;
+            case OP_TRIAL:
+                tot[0] = rs[0];
+                tot[1] = rm[0];
+                decide_trial(s, tot);
+                break;
+            case OP_MINMAX:
+                decide_minmax(sp, s, rm);
+                break;
+            default:
+                decide_guard(sp, s, rm);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (op == OP_EVAL && mode == EVAL_GN_START)
+            set_cond(c, COND_GN, any_pair(c, batch, [](volatile PairState* q) { return q->gn_active != 0; }));
+        if ((op == OP_EVAL && mode == EVAL_TRIAL) || op == OP_TRIAL)
+            set_cond(c, COND_LS, any_pair(c, batch, [](volatile PairState* q) { return q->ls_active != 0; }));
+        if (op == OP_PCG_INIT || op == OP_UPDATE)
+            set_cond(c, COND_PCG, any_pair(c, batch, [](volatile PairState* q) { return q->pcg_active != 0; }));
+    }
+}
+
+}  // namespace hysco

@@ -27,8 +27,8 @@ __device__ __forceinline__ ColInfo col_info(const Geom& g, long long col) {
     c.off = col * g.P;
     c.i = (int)(col / g.n2);
     c.j = (int)(col - (long long)c.i * g.n2);
-    c.him = c.i > 0;
-    c.hip = c.i < g.n1 - 1;
+    c.him = has_im(g, c.i);
+    c.hip = has_ip(g, c.i);
     c.hjm = c.j > 0;
     c.hjp = c.j < g.n2 - 1;
     return c;
@@ -57,6 +57,62 @@ __device__ __forceinline__ void pe_neighbours(const T (&v)[NCH], T (&vm)[NCH], T
     }
 }
 
+// ---- decisions after the PCG / Armijo / guard reductions (see hysco_common.cuh)
+// matvec: alpha_c = (r.z)/(p.Hp); breakdown if p.Hp <= 0 (oracle pcg(): keep x)
+__device__ inline void decide_matvec(PairState& s, const double* tot) {
+    if (!s.pcg_active) return;
+    if (tot[0] <= 0.0) {
+        s.alpha_c = 0.0;
+        s.pcg_active = 0;
+    } else {
+        s.alpha_c = s.rz / tot[0];
+        s.h_evals += 1;
+    }
+}
+// PCG start (R14): tot = [r.z, r.r]
+__device__ inline void decide_pcg_init(PairState& s, const double* tot) {
+    if (s.gn_active) {
+        s.rz = tot[0];
+        s.rr0 = tot[1];
+        s.rr = tot[1];
+        s.pcg_k = 0;
+        s.beta_c = 0.0;
+        s.relres = tot[1] > 0.0 ? 1.0 : 0.0;
+        s.pcg_active = tot[1] > 0.0 ? 1 : 0;
+    } else {
+        s.pcg_active = 0;
+    }
+}
+// PCG update: tot = [r.z, r.r]; beta and the relative-residual stop
+__device__ inline void decide_update(const SolveParams& sp, PairState& s, const double* tot) {
+    if (!s.pcg_active) return;
+    s.pcg_k += 1;
+    s.pcg_iters += 1;
+    s.rr = tot[1];
+    s.relres = sqrt(tot[1] / s.rr0);
+    s.beta_c = tot[0] / s.rz;
+    s.rz = tot[0];
+    if (s.pcg_k >= sp.max_pcg || (!sp.fixed && s.relres < sp.pcg_rtol)) s.pcg_active = 0;
+}
+// Armijo start (R15): tot = [grad.q, max|q|]
+__device__ inline void decide_trial(PairState& s, const double* tot) {
+    if (s.gn_active) {
+        s.gq = tot[0];
+        s.qmax = tot[1];
+        s.gamma = 1.0;
+        s.ls_tries = 0;
+        s.ls_restore = 0;
+        s.ls_active = 1;
+    } else {
+        s.ls_active = 0;
+    }
+}
+// feasibility guard (R10): tot = [max |Db0|]
+__device__ inline void decide_guard(const SolveParams& sp, PairState& s, const double* tot) {
+    s.maxDb = tot[0];
+    s.scale = (tot[0] >= sp.feas_cap) ? sp.feas_cap / tot[0] : 1.0;
+}
+
 // ---------------------------------------------------------------------------
 // A5 GN Hessian matvec, folded form:
 //   Hq = dt q + et_{l-1} q_{l-1} + et_l q_{l+1} + alpha hd L_xy q
@@ -71,7 +127,7 @@ __global__ void __launch_bounds__(256) matvec_kernel(Geom g, Ctl c, const T* __r
     const int pair = blockIdx.y;
     bool active = true;
     if (PCG) active = c.st[pair].pcg_active != 0;
-    const size_t po = (size_t)pair * g.Nn;
+    const size_t po = (size_t)pair * g.ps;
     const T ahd = (T)g.ahd, ih1sq = (T)g.ih1sq, ih2sq = (T)g.ih2sq;
     const long long sI = (long long)g.n2 * g.P;
     const int P = g.P;
@@ -120,15 +176,12 @@ __global__ void __launch_bounds__(256) matvec_kernel(Geom g, Ctl c, const T* __r
     if (!PCG) return;
     double v[1] = {acc}, tot[1];
     if (!pair_reduce<1, 0u>(c, v, tot)) return;
-    if (threadIdx.x != 0 || !active) return;
-    PairState& s = c.st[pair];
-    if (tot[0] <= 0.0) {          // breakdown: stop PCG, keep x (oracle pcg(): "if pHp <= 0: break")
-        s.alpha_c = 0.0;
-        s.pcg_active = 0;
-    } else {
-        s.alpha_c = s.rz / tot[0];
-        s.h_evals += 1;
+    if (threadIdx.x != 0) return;
+    if (c.defer) {
+        store_red(c, pair, gridDim.y, tot, 1, 0);
+        return;
     }
+    decide_matvec(c.st[pair], tot);
 }
 
 // Jacobi preconditioner M = diag(H_J) = dt + alpha hd diag(L_xy) (R13);
@@ -146,7 +199,7 @@ __global__ void __launch_bounds__(256) pcg_init_kernel(Geom g, Ctl c, const T* _
     const int lane = threadIdx.x & 31;
     const int pair = blockIdx.y;
     const bool active = c.st[pair].gn_active != 0;
-    const size_t po = (size_t)pair * g.Nn;
+    const size_t po = (size_t)pair * g.ps;
     const int P = g.P;
     double arz = 0, arr = 0;
     if (active) {
@@ -181,18 +234,11 @@ __global__ void __launch_bounds__(256) pcg_init_kernel(Geom g, Ctl c, const T* _
     double v[2] = {arz, arr}, tot[2];
     if (!pair_reduce<2, 0u>(c, v, tot)) return;
     if (threadIdx.x != 0) return;
-    PairState& s = c.st[pair];
-    if (active) {
-        s.rz = tot[0];
-        s.rr0 = tot[1];
-        s.rr = tot[1];
-        s.pcg_k = 0;
-        s.beta_c = 0.0;
-        s.relres = tot[1] > 0.0 ? 1.0 : 0.0;
-        s.pcg_active = tot[1] > 0.0 ? 1 : 0;
-    } else {
-        s.pcg_active = 0;
+    if (c.defer) {
+        store_red(c, pair, gridDim.y, tot, 2, 0);
+        return;
     }
+    decide_pcg_init(c.st[pair], tot);
     if (last_pair(c)) set_cond(c, COND_PCG, any_pair(c, gridDim.y, [](volatile PairState* q) { return q->pcg_active != 0; }));
 }
 
@@ -207,7 +253,7 @@ __global__ void __launch_bounds__(256) pcg_update_kernel(Geom g, Ctl c, SolvePar
     const int pair = blockIdx.y;
     const bool active = c.st[pair].pcg_active != 0;
     const T a = (T)c.st[pair].alpha_c;
-    const size_t po = (size_t)pair * g.Nn;
+    const size_t po = (size_t)pair * g.ps;
     const int P = g.P;
     double arz = 0, arr = 0;
     if (active) {
@@ -245,16 +291,11 @@ __global__ void __launch_bounds__(256) pcg_update_kernel(Geom g, Ctl c, SolvePar
     double v[2] = {arz, arr}, tot[2];
     if (!pair_reduce<2, 0u>(c, v, tot)) return;
     if (threadIdx.x != 0) return;
-    PairState& s = c.st[pair];
-    if (active) {
-        s.pcg_k += 1;
-        s.pcg_iters += 1;
-        s.rr = tot[1];
-        s.relres = sqrt(tot[1] / s.rr0);
-        s.beta_c = tot[0] / s.rz;
-        s.rz = tot[0];
-        if (s.pcg_k >= sp.max_pcg || (!sp.fixed && s.relres < sp.pcg_rtol)) s.pcg_active = 0;
+    if (c.defer) {
+        store_red(c, pair, gridDim.y, tot, 2, 0);
+        return;
     }
+    decide_update(sp, c.st[pair], tot);
     if (last_pair(c)) set_cond(c, COND_PCG, any_pair(c, gridDim.y, [](volatile PairState* q) { return q->pcg_active != 0; }));
 }
 
@@ -267,7 +308,7 @@ __global__ void __launch_bounds__(256) pcg_dir_kernel(Geom g, Ctl c, const T* __
     const int pair = blockIdx.y;
     if (!c.st[pair].pcg_active) return;
     const T be = (T)c.st[pair].beta_c;
-    const size_t po = (size_t)pair * g.Nn;
+    const size_t po = (size_t)pair * g.ps;
     const int P = g.P;
     HYSCO_FOR_COLS(g) {
         const ColInfo ci = col_info(g, col);
@@ -301,7 +342,7 @@ __global__ void __launch_bounds__(256) trial_init_kernel(Geom g, Ctl c, const T*
     const int lane = threadIdx.x & 31;
     const int pair = blockIdx.y;
     const bool active = c.st[pair].gn_active != 0;
-    const size_t po = (size_t)pair * g.Nn;
+    const size_t po = (size_t)pair * g.ps;
     const int P = g.P;
     double agq = 0, aqm = 0;
     if (active) {
@@ -333,17 +374,11 @@ __global__ void __launch_bounds__(256) trial_init_kernel(Geom g, Ctl c, const T*
     double v[2] = {agq, aqm}, tot[2];
     if (!pair_reduce<2, 0x2u>(c, v, tot)) return;
     if (threadIdx.x != 0) return;
-    PairState& s = c.st[pair];
-    if (active) {
-        s.gq = tot[0];
-        s.qmax = tot[1];
-        s.gamma = 1.0;
-        s.ls_tries = 0;
-        s.ls_restore = 0;
-        s.ls_active = 1;
-    } else {
-        s.ls_active = 0;
+    if (c.defer) {
+        store_red(c, pair, gridDim.y, tot, 1, 1);
+        return;
     }
+    decide_trial(c.st[pair], tot);
     if (last_pair(c)) set_cond(c, COND_LS, any_pair(c, gridDim.y, [](volatile PairState* q2) { return q2->ls_active != 0; }));
 }
 
@@ -358,7 +393,7 @@ __global__ void __launch_bounds__(256) ls_retry_kernel(Geom g, Ctl c, const T* _
     if (!s.ls_active) return;
     const bool restore = s.ls_restore != 0;
     const T gm = (T)s.gamma;
-    const size_t po = (size_t)pair * g.Nn;
+    const size_t po = (size_t)pair * g.ps;
     const int P = g.P;
     HYSCO_FOR_COLS(g) {
         const size_t o = po + (size_t)col * P;
@@ -384,7 +419,7 @@ template <typename T, int NCH>
 __global__ void __launch_bounds__(256) hess_diag_kernel(Geom g, Ctl c, const T* __restrict__ dt, T* __restrict__ out) {
     count_launch(c);
     const int lane = threadIdx.x & 31;
-    const size_t po = (size_t)blockIdx.y * g.Nn;
+    const size_t po = (size_t)blockIdx.y * g.ps;
     const int P = g.P;
     HYSCO_FOR_COLS(g) {
         const ColInfo ci = col_info(g, col);
@@ -400,7 +435,7 @@ __global__ void __launch_bounds__(256) blur_axis_kernel(Geom g, Ctl c, int axis,
                                                         const T* __restrict__ in, T* __restrict__ out) {
     count_launch(c);
     const int lane = threadIdx.x & 31;
-    const size_t po = (size_t)blockIdx.y * g.Nn;
+    const size_t po = (size_t)blockIdx.y * g.ps;
     const T a = (T)w0, mid = (T)w1;
     const int P = g.P;
     HYSCO_FOR_COLS(g) {
@@ -414,7 +449,10 @@ __global__ void __launch_bounds__(256) blur_axis_kernel(Geom g, Ctl c, int axis,
             }
         } else {
             long long cm_, cp_;
-            if (axis == 0) {
+            if (axis == 0 && g.slab) {      // periodic ring across ranks: halo planes hold the wrap
+                cm_ = ci.off - (long long)g.n2 * P;
+                cp_ = ci.off + (long long)g.n2 * P;
+            } else if (axis == 0) {
                 cm_ = (long long)(((ci.i + g.n1 - 1) % g.n1) * g.n2 + ci.j) * P;
                 cp_ = (long long)(((ci.i + 1) % g.n1) * g.n2 + ci.j) * P;
             } else {
@@ -434,7 +472,7 @@ __global__ void __launch_bounds__(256) guard_max_kernel(Geom g, Ctl c, SolvePara
     count_launch(c);
     const int lane = threadIdx.x & 31;
     const int pair = blockIdx.y;
-    const size_t po = (size_t)pair * g.Nn;
+    const size_t po = (size_t)pair * g.ps;
     const int P = g.P;
     double mx = 0.0;
     HYSCO_FOR_COLS(g) {
@@ -444,9 +482,11 @@ __global__ void __launch_bounds__(256) guard_max_kernel(Geom g, Ctl c, SolvePara
     double v[1] = {mx}, tot[1];
     if (!pair_reduce<1, 0x1u>(c, v, tot)) return;
     if (threadIdx.x != 0) return;
-    PairState& s = c.st[pair];
-    s.maxDb = tot[0];
-    s.scale = (tot[0] >= sp.feas_cap) ? sp.feas_cap / tot[0] : 1.0;
+    if (c.defer) {
+        store_red(c, pair, gridDim.y, tot, 0, 1);
+        return;
+    }
+    decide_guard(sp, c.st[pair], tot);
 }
 
 template <typename T, int NCH>
@@ -456,7 +496,7 @@ __global__ void __launch_bounds__(256) guard_scale_kernel(Geom g, Ctl c, T* __re
     const int pair = blockIdx.y;
     const double sc = c.st[pair].scale;
     if (sc == 1.0) return;
-    const size_t po = (size_t)pair * g.Nn;
+    const size_t po = (size_t)pair * g.ps;
     const int P = g.P;
     HYSCO_FOR_COLS(g) {
         T* bc = b + po + (size_t)col * P;

@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
     const long long c1 = (long long)(blockIdx.x + 1) * g.ncol / gridDim.x;
     const int ncl = (int)(c1 - c0);
     const int Nb = ncl * P;
-    const size_t n0 = (size_t)pair * g.Nn + (size_t)c0 * P;
+    const size_t n0 = (size_t)pair * g.ps + (size_t)c0 * P;
     const int sI = n2 * P;
     const float wi = (float)(g.ahd * g.ih1sq), wj = (float)(g.ahd * g.ih2sq);
     // this CTA's first node in the ghost-padded global copy of p

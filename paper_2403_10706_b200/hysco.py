@@ -22,7 +22,9 @@ STOP_NAMES = {0: "maxiter", 1: "grad", 2: "dJ", 3: "db", 4: "ls_fail", 5: "infea
 EXPORTED = ["hysco_default_solve_opts", "hysco_default_ot_opts", "hysco_create", "hysco_bind_images",
             "hysco_ot_init", "hysco_objective_grad", "hysco_hessvec", "hysco_hess_diag", "hysco_solve",
             "hysco_apply", "hysco_correct", "hysco_correct_host", "hysco_last_launch_count",
-            "hysco_last_error", "hysco_destroy", "hysco_version", "hysco_profile_kernels"]
+            "hysco_last_error", "hysco_destroy", "hysco_version", "hysco_profile_kernels",
+            "hysco_nccl_unique_id", "hysco_create_slab", "hysco_create_loopback", "hysco_group_correct",
+            "hysco_group_solve"]
 PROF_NAMES = ["matvec", "pcg_update", "pcg_dir", "eval", "pcg_resident", "trial_init"]
 
 
@@ -102,6 +104,20 @@ def lib():
     L.hysco_last_error.restype = ctypes.c_char_p
     L.hysco_profile_kernels.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_double)]
     L.hysco_profile_kernels.restype = st
+    L.hysco_nccl_unique_id.argtypes = [ctypes.c_char_p]
+    L.hysco_nccl_unique_id.restype = st
+    L.hysco_create_slab.argtypes = [ctypes.POINTER(hysco_config), ctypes.c_int32, ctypes.c_int32, ctypes.c_int64,
+                                    ctypes.c_int64, ctypes.c_char_p, vp, ctypes.POINTER(vp)]
+    L.hysco_create_slab.restype = st
+    L.hysco_create_loopback.argtypes = [ctypes.POINTER(hysco_config), ctypes.c_int32, vp, ctypes.POINTER(vp)]
+    L.hysco_create_loopback.restype = st
+    L.hysco_group_correct.argtypes = [ctypes.POINTER(vp), ctypes.c_int32, ctypes.POINTER(hysco_ot_opts),
+                                      ctypes.POINTER(hysco_solve_opts), ctypes.POINTER(vp), ctypes.POINTER(vp),
+                                      ctypes.POINTER(vp), ctypes.POINTER(hysco_report)]
+    L.hysco_group_correct.restype = st
+    L.hysco_group_solve.argtypes = [ctypes.POINTER(vp), ctypes.c_int32, ctypes.POINTER(vp),
+                                    ctypes.POINTER(hysco_solve_opts), ctypes.POINTER(hysco_report)]
+    L.hysco_group_solve.restype = st
     L.hysco_version.argtypes = []
     L.hysco_version.restype = ctypes.c_int32
     _lib = L
@@ -215,6 +231,73 @@ def hysco_profile_kernels(ctx, reps=20, flush_l2=True):
     out = (ctypes.c_double * len(PROF_NAMES))()
     _check(ctx, lib().hysco_profile_kernels(ctx, int(reps), int(bool(flush_l2)), out))
     return dict(zip(PROF_NAMES, out[:]))
+
+
+def _cfg(shape, h, batch, alpha, beta, dtype, device):
+    return hysco_config(int(shape[0]), int(shape[1]), int(shape[2]), int(batch), float(h[0]), float(h[1]),
+                        float(h[2]), float(alpha), float(beta), int(dtype), int(device))
+
+
+def slab_bounds(n1, nranks, rank):
+    """Planes [i0, i1) of `rank` in a split of n1 planes over nranks (as hysco_create_loopback)."""
+    return n1 * rank // nranks, n1 * (rank + 1) // nranks
+
+
+def hysco_nccl_unique_id():
+    buf = ctypes.create_string_buffer(128)
+    s = lib().hysco_nccl_unique_id(buf)
+    if s != HYSCO_OK:
+        raise HyscoError(s, "ncclGetUniqueId failed")
+    return bytes(buf.raw)
+
+
+def hysco_create_slab(shape_local, h, rank, nranks, n1_global, i0, nccl_id=None, batch=1, alpha=300.0, beta=1e-4,
+                      dtype=HYSCO_F32, device=0, stream=None):
+    cfg = _cfg(shape_local, h, batch, alpha, beta, dtype, device)
+    out = ctypes.c_void_p()
+    s = lib().hysco_create_slab(ctypes.byref(cfg), int(rank), int(nranks), int(n1_global), int(i0),
+                                nccl_id, stream, ctypes.byref(out))
+    if s != HYSCO_OK:
+        raise HyscoError(s, "hysco_create_slab failed")
+    return out.value
+
+
+def hysco_create_loopback(shape, h, nranks, batch=1, alpha=300.0, beta=1e-4, dtype=HYSCO_F32, device=0,
+                          stream=None):
+    cfg = _cfg(shape, h, batch, alpha, beta, dtype, device)
+    out = (ctypes.c_void_p * nranks)()
+    s = lib().hysco_create_loopback(ctypes.byref(cfg), int(nranks), stream, out)
+    if s != HYSCO_OK:
+        raise HyscoError(s, "hysco_create_loopback failed")
+    return [out[r] for r in range(nranks)]
+
+
+def _ptrs(ts, n):
+    arr = (ctypes.c_void_p * n)()
+    for r in range(n):
+        arr[r] = _ptr(ts[r]) if ts is not None and ts[r] is not None else None
+    return arr
+
+
+def hysco_group_correct(ctxs, b_out=None, Ip_corr=None, Im_corr=None, ot_opts=None, solve_opts=None, batch=1):
+    n = len(ctxs)
+    cs = (ctypes.c_void_p * n)(*ctxs)
+    reps = (hysco_report * batch)()
+    s = _check(ctxs[0], lib().hysco_group_correct(cs, n, ctypes.byref(ot_opts) if ot_opts is not None else None,
+                                                  ctypes.byref(solve_opts) if solve_opts is not None else None,
+                                                  _ptrs(b_out, n), _ptrs(Ip_corr, n), _ptrs(Im_corr, n), reps),
+               (HYSCO_OK, HYSCO_INFEASIBLE))
+    return [r.as_dict() for r in reps], s == HYSCO_INFEASIBLE
+
+
+def hysco_group_solve(ctxs, b_inout, solve_opts=None, batch=1):
+    n = len(ctxs)
+    cs = (ctypes.c_void_p * n)(*ctxs)
+    reps = (hysco_report * batch)()
+    s = _check(ctxs[0], lib().hysco_group_solve(cs, n, _ptrs(b_inout, n),
+                                                ctypes.byref(solve_opts) if solve_opts is not None else None, reps),
+               (HYSCO_OK, HYSCO_INFEASIBLE))
+    return [r.as_dict() for r in reps], s == HYSCO_INFEASIBLE
 
 
 def hysco_last_error(ctx):

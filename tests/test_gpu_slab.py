@@ -1,0 +1,131 @@
+"""Slab decomposition along dim 1 on one GPU.
+
+A loopback group (hysco_create_loopback: nranks contexts, one stream, halo
+planes exchanged by device copies, pair totals allreduced by a fixed-order
+device sum) runs the same kernels, halo exchanges and deferred decisions as
+an NCCL group.  Its result must equal the single-context solve up to
+reduction order, and the oracle within the parity tolerances.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import hysco_oracle as O          # noqa: E402
+from paper_2403_10706_b200 import hysco as H  # noqa: E402
+from synth import phantom                      # noqa: E402
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+TD = {H.HYSCO_F32: torch.float32, H.HYSCO_F64: torch.float64}
+ND = {H.HYSCO_F32: np.float32, H.HYSCO_F64: np.float64}
+
+
+def rel(a, ref):
+    a, ref = np.asarray(a, np.float64), np.asarray(ref, np.float64)
+    return np.linalg.norm(a - ref) / max(np.linalg.norm(ref), 1e-300)
+
+
+def single(Ip, Im, h, dtype, so, batch):
+    n1, n2, n3 = Ip.shape[1:]
+    ctx = H.hysco_create((n1, n2, n3), h, batch, dtype=dtype)
+    tIp = torch.from_numpy(Ip.astype(ND[dtype])).to(DEV)
+    tIm = torch.from_numpy(Im.astype(ND[dtype])).to(DEV)
+    H.hysco_bind_images(ctx, tIp, tIm)
+    b = torch.zeros((batch, n1, n2, n3 + 1), dtype=TD[dtype], device=DEV)
+    Tp = torch.zeros((batch, n1, n2, n3), dtype=TD[dtype], device=DEV)
+    Tm = torch.zeros_like(Tp)
+    reps, _ = H.hysco_correct(ctx, b, Tp, Tm, solve_opts=so, batch=batch)
+    H.hysco_destroy(ctx)
+    return b.cpu().numpy(), Tp.cpu().numpy(), Tm.cpu().numpy(), reps
+
+
+def grouped(Ip, Im, h, dtype, so, batch, nranks):
+    n1, n2, n3 = Ip.shape[1:]
+    ctxs = H.hysco_create_loopback((n1, n2, n3), h, nranks, batch=batch, dtype=dtype)
+    keep, bs, tps, tms = [], [], [], []
+    for r, c in enumerate(ctxs):
+        i0, i1 = H.slab_bounds(n1, nranks, r)
+        tIp = torch.from_numpy(np.ascontiguousarray(Ip[:, i0:i1]).astype(ND[dtype])).to(DEV)
+        tIm = torch.from_numpy(np.ascontiguousarray(Im[:, i0:i1]).astype(ND[dtype])).to(DEV)
+        keep += [tIp, tIm]
+        H.hysco_bind_images(c, tIp, tIm)
+        bs.append(torch.zeros((batch, i1 - i0, n2, n3 + 1), dtype=TD[dtype], device=DEV))
+        tps.append(torch.zeros((batch, i1 - i0, n2, n3), dtype=TD[dtype], device=DEV))
+        tms.append(torch.zeros((batch, i1 - i0, n2, n3), dtype=TD[dtype], device=DEV))
+    reps, _ = H.hysco_group_correct(ctxs, bs, tps, tms, solve_opts=so, batch=batch)
+    n_launch = [H.hysco_last_launch_count(c) for c in ctxs]
+    for c in ctxs:
+        H.hysco_destroy(c)
+    cat = lambda ts: np.concatenate([t.cpu().numpy() for t in ts], axis=1)  # noqa: E731
+    return cat(bs), cat(tps), cat(tms), reps, n_launch
+
+
+@pytest.mark.parametrize("nranks", [1, 2, 4])
+def test_loopback_slabs_equal_single_f64(nranks):
+    p = phantom.make_config("C1_16x16x8")
+    Ip, Im = p.Ip[None].astype(np.float64), p.Im[None].astype(np.float64)
+    so = H.default_solve_opts()            # real Armijo: decisions must match exactly in fp64
+    b1, tp1, tm1, r1 = single(Ip, Im, p.h, H.HYSCO_F64, so, 1)
+    b2, tp2, tm2, r2, nl = grouped(Ip, Im, p.h, H.HYSCO_F64, so, 1, nranks)
+    assert (r2[0]["gn_iters"], r2[0]["pcg_iters"], r2[0]["f_evals"], r2[0]["ls_halvings"]) == \
+        (r1[0]["gn_iters"], r1[0]["pcg_iters"], r1[0]["f_evals"], r1[0]["ls_halvings"])
+    assert rel(b2, b1) <= 1e-11 and rel(tp2, tp1) <= 1e-11 and rel(tm2, tm1) <= 1e-11
+    assert abs(r2[0]["J"] - r1[0]["J"]) <= 1e-11 * abs(r1[0]["J"])
+    assert all(n > 0 for n in nl)
+
+
+def test_loopback_slabs_ragged_batch_f32_vs_oracle():
+    pairs = [phantom.make_pair((7, 6, 37), (1.1, 0.9, 1.3), 40 + k) for k in range(2)]
+    Ip = np.stack([q.Ip for q in pairs])
+    Im = np.stack([q.Im for q in pairs])
+    h = pairs[0].h
+    so = H.default_solve_opts(armijo=0)
+    b1, tp1, _, _ = single(Ip, Im, h, H.HYSCO_F32, so, 2)
+    b2, tp2, _, reps, _ = grouped(Ip, Im, h, H.HYSCO_F32, so, 2, 3)      # planes split 2 / 2 / 3
+    assert rel(b2, b1) <= 1e-5 and rel(tp2, tp1) <= 1e-5
+    for k, q in enumerate(pairs):
+        _, bref, tpr, _, rep = O.correct_pair(q.Ip.astype(np.float64), q.Im.astype(np.float64), h, armijo=False)
+        assert rel(b2[k], bref) <= 1e-4 and rel(tp2[k], tpr) <= 1e-4
+        assert reps[k]["gn_iters"] == rep["gn_iters"]
+
+
+def test_loopback_single_plane_slabs_periodic_blur():
+    """Every rank owns one plane: the periodic blur ring and the Neumann ends
+    are all exchange-driven."""
+    p = phantom.make_pair((4, 5, 20), (1.0, 1.2, 1.1), 77)
+    Ip, Im = p.Ip[None].astype(np.float64), p.Im[None].astype(np.float64)
+    so = H.default_solve_opts(max_gn=3)
+    b1, tp1, _, _ = single(Ip, Im, p.h, H.HYSCO_F64, so, 1)
+    b2, tp2, _, _, _ = grouped(Ip, Im, p.h, H.HYSCO_F64, so, 1, 4)
+    assert rel(b2, b1) <= 1e-11 and rel(tp2, tp1) <= 1e-11
+
+
+def test_nccl_slab_one_rank_equals_single():
+    p = phantom.make_config("C1_16x16x8")
+    n1, n2, n3 = p.Ip.shape
+    so = H.default_solve_opts(armijo=0)
+    b1, tp1, _, r1 = single(p.Ip[None], p.Im[None], p.h, H.HYSCO_F32, so, 1)
+    ctx = H.hysco_create_slab((n1, n2, n3), p.h, 0, 1, n1, 0)
+    tIp = torch.from_numpy(p.Ip[None]).to(DEV)
+    tIm = torch.from_numpy(p.Im[None]).to(DEV)
+    H.hysco_bind_images(ctx, tIp, tIm)
+    b = torch.zeros((1, n1, n2, n3 + 1), device=DEV)
+    Tp = torch.zeros((1, n1, n2, n3), device=DEV)
+    reps, _ = H.hysco_correct(ctx, b, Tp, None, solve_opts=so)
+    assert rel(b.cpu().numpy(), b1) <= 1e-5 and rel(Tp.cpu().numpy(), tp1) <= 1e-5
+    assert reps[0]["gn_iters"] == r1[0]["gn_iters"]
+    # per-kernel calls are not available on slab contexts
+    with pytest.raises(H.HyscoError) as e:
+        H.hysco_apply(ctx, b, Tp, None)
+    assert e.value.status == H.HYSCO_ERR_STATE
+    H.hysco_destroy(ctx)
+
+
+def test_loopback_hcp3t_four_slabs():
+    p = phantom.make_config("C2_hcp3t")
+    so = H.default_solve_opts(armijo=0, max_gn=3)
+    b1, tp1, _, r1 = single(p.Ip[None], p.Im[None], p.h, H.HYSCO_F32, so, 1)
+    b2, tp2, _, r2, _ = grouped(p.Ip[None], p.Im[None], p.h, H.HYSCO_F32, so, 1, 4)
+    assert rel(b2, b1) <= 1e-5 and rel(tp2, tp1) <= 1e-5
+    assert r2[0]["pcg_iters"] == r1[0]["pcg_iters"] == 30
