@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-reps", type=int, default=20)
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--slab", action="store_true",
+                    help="partition ONE pair of --config into slabs along dim 1 across the ranks (configs[4])")
     return ap.parse_args()
 
 
@@ -347,10 +349,86 @@ def run_hysco(args):
         torch.distributed.destroy_process_group()
 
 
+def run_slab(args):
+    """Strong scaling of ONE large pair (BASELINE.json configs[4]): rank r owns
+    planes slab_bounds(n1, N, r) of dim 1; libhysco exchanges one halo plane and
+    allreduces the per-pair scalars over NCCL."""
+    import torch
+    from paper_2403_10706_b200 import dist as D
+    from paper_2403_10706_b200 import hysco as H
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    shape, h, seed = phantom.CONFIGS[args.config]
+    n1, n2, n3 = shape
+    i0, i1 = D.slab_bounds(n1, world, rank)
+    pair = phantom.make_pair(shape, h, seed, planes=(i0, i1))
+    nid = D.share_nccl_id() if world > 1 else None
+    stream = torch.cuda.current_stream(dev)
+    ctx = H.hysco_create_slab((i1 - i0, n2, n3), h, rank, world, n1, i0, nid, device=local,
+                              stream=stream.cuda_stream)
+    Ip = torch.from_numpy(pair.Ip[None]).to(dev)
+    Im = torch.from_numpy(pair.Im[None]).to(dev)
+    H.hysco_bind_images(ctx, Ip, Im)
+    b = torch.zeros((1, i1 - i0, n2, n3 + 1), dtype=torch.float32, device=dev)
+    Tp = torch.zeros((1, i1 - i0, n2, n3), dtype=torch.float32, device=dev)
+    Tm = torch.zeros_like(Tp)
+    flush = torch.empty(256 << 18, dtype=torch.float32, device=dev)
+    for _ in range(max(args.warmup, 0)):
+        H.hysco_correct(ctx, b, Tp, Tm)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)
+    step_ms = []
+    launches = 0
+    reps = None
+    for _ in range(args.steps):
+        flush.zero_()
+        a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        reps, _ = H.hysco_correct(ctx, b, Tp, Tm)
+        z.record(stream)
+        z.synchronize()
+        step_ms.append(a.elapsed_time(z))
+        launches += H.hysco_last_launch_count(ctx)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = clk.stop()
+    total = D.max_over_ranks(float(np.sum(step_ms)), device=dev)
+    value = args.steps / (total / 1e3)
+    Nn = n1 * n2 * (n3 + 1)
+    # algorithmic bytes of one fixed 10 x 10 solve, streaming kernels (DESIGN.md §7)
+    r0 = reps[0]
+    step_bytes = (r0["pcg_iters"] * 60 + r0["f_evals"] * 24 + r0["gn_iters"] * 28 + 40) * Nn
+    if rank == 0:
+        line = {"metric": "volume pairs corrected/sec (slab-partitioned large pair)", "value": value,
+                "unit": "pairs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": total / args.steps, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": dict(workload_desc(args.config, 1), parallelism=f"slab{world} along dim 1 (NCCL halo + allreduce)"),
+                "clocks": clocks, "gpu_launches": launches,
+                "step_effective_gbs_per_gpu": step_bytes / world / (total / args.steps * 1e-3) / 1e9,
+                "solver": {k: r0[k] for k in ("gn_iters", "f_evals", "h_evals", "pcg_iters", "stop", "J")}}
+        print(json.dumps(line), flush=True)
+    H.hysco_destroy(ctx)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.slab:
+        run_slab(args)
     else:
         run_hysco(args)
 

@@ -99,8 +99,11 @@ class _Field:
         return self.kappa * b, self.kappa * db
 
 
-def make_pair(shape, h, seed, max_dv=0.4, noise=0.0, chunk=32) -> Pair:
-    """Generate one seeded pair.  shape = (n1, n2, n3) with PE last; h in mm."""
+def make_pair(shape, h, seed, max_dv=0.4, noise=0.0, chunk=32, planes=None) -> Pair:
+    """Generate one seeded pair.  shape = (n1, n2, n3) with PE last; h in mm.
+    planes = (i0, i1): only those planes of dim 1 (a slab of the same volume;
+    equal to the corresponding planes of the full generation up to the Newton
+    stopping tolerance, 1e-12 mm)."""
     n1, n2, n3 = (int(v) for v in shape)
     h = tuple(float(v) for v in h)
     L = np.array([n1 * h[0], n2 * h[1], n3 * h[2]])
@@ -122,16 +125,19 @@ def make_pair(shape, h, seed, max_dv=0.4, noise=0.0, chunk=32) -> Pair:
 
     x3c = (np.arange(n3) + 0.5) * h[2]
     x3n = np.arange(n3 + 1) * h[2]
-    Ip = np.empty((n1, n2, n3), np.float64)
-    Im = np.empty((n1, n2, n3), np.float64)
-    It = np.empty((n1, n2, n3), np.float64)
-    bt = np.empty((n1, n2, n3 + 1), np.float64)
-    for i0 in range(0, n1, chunk):
-        X1, X2 = np.meshgrid(x1c[i0:i0 + chunk], x2c, indexing="ij")
+    p0, p1 = (0, n1) if planes is None else (int(planes[0]), int(planes[1]))
+    m1 = p1 - p0
+    Ip = np.empty((m1, n2, n3), np.float64)
+    Im = np.empty((m1, n2, n3), np.float64)
+    It = np.empty((m1, n2, n3), np.float64)
+    bt = np.empty((m1, n2, n3 + 1), np.float64)
+    for a0 in range(0, m1, chunk):
+        i0 = p0 + a0
+        X1, X2 = np.meshgrid(x1c[i0:min(i0 + chunk, p1)], x2c, indexing="ij")
         X1e, X2e = X1[..., None], X2[..., None]
         amp = [a[..., None] for a in fld.inplane(X1, X2)]
-        It[i0:i0 + chunk] = _image(X1e, X2e, x3c[None, None, :], L, g)
-        bt[i0:i0 + chunk] = fld.eval(amp, x3n[None, None, :])[0]
+        It[a0:a0 + chunk] = _image(X1e, X2e, x3c[None, None, :], L, g)
+        bt[a0:a0 + chunk] = fld.eval(amp, x3n[None, None, :])[0]
         y = np.broadcast_to(x3c[None, None, :], X1.shape + (n3,))
         for sgn, out in ((1.0, Ip), (-1.0, Im)):
             # Newton on x + sgn*b(x) = y (monotone since |d3 b| <= 0.4 < 1)
@@ -143,8 +149,9 @@ def make_pair(shape, h, seed, max_dv=0.4, noise=0.0, chunk=32) -> Pair:
                 if float(np.abs(res).max()) < 1e-12:
                     break
             b, db = fld.eval(amp, x)
-            out[i0:i0 + chunk] = _image(X1e, X2e, x, L, g) / (1.0 + sgn * db)
+            out[a0:a0 + chunk] = _image(X1e, X2e, x, L, g) / (1.0 + sgn * db)
     if noise > 0.0:
+        assert planes is None, "noise is drawn for the whole volume"
         nrng = np.random.default_rng(seed + 7919)
         Ip += nrng.normal(0.0, noise * 1000.0, Ip.shape)
         Im += nrng.normal(0.0, noise * 1000.0, Im.shape)
