@@ -119,7 +119,7 @@ __device__ inline void decide_guard(const SolveParams& sp, PairState& s, const d
 // PCG mode also reduces p.Hp and forms alpha_c = (r.z)/(p.Hp) per pair.
 // ---------------------------------------------------------------------------
 template <typename T, int NCH, bool PCG>
-__global__ void __launch_bounds__(256) matvec_kernel(Geom g, Ctl c, const T* __restrict__ dt,
+__global__ void __launch_bounds__(256, (NCH <= 5 ? 4 : 3)) matvec_kernel(Geom g, Ctl c, const T* __restrict__ dt,
                                                      const T* __restrict__ et, const T* __restrict__ q,
                                                      T* __restrict__ Hq) {
     count_launch(c);
@@ -155,16 +155,25 @@ __global__ void __launch_bounds__(256) matvec_kernel(Geom g, Ctl c, const T* __r
                     l1[m] = (ci.him ? qv[m] - a : T(0)) + (ci.hip ? qv[m] - b : T(0));
                     l2[m] = (ci.hjm ? qv[m] - e : T(0)) + (ci.hjp ? qv[m] - f : T(0));
                 }
-                T qm[NCH], qp[NCH], em[NCH], ep_[NCH];
-                pe_neighbours<NCH>(qv, qm, qp, qc, seg, P);
-                pe_neighbours<NCH>(ev, em, ep_, ec, seg, P);
+                // PE neighbours inline per chunk (shuffles; chunk edges from the
+                // neighbouring chunk's lane 31 / lane 0, segment edges from memory)
 #pragma unroll
                 for (int m = 0; m < NCH; m++) {
                     const int l = seg + 32 * m + lane;
+                    T qm = __shfl_up_sync(FULL, qv[m], 1), em = __shfl_up_sync(FULL, ev[m], 1);
+                    T qp = __shfl_down_sync(FULL, qv[m], 1);
+                    const T qprev = __shfl_sync(FULL, qv[m > 0 ? m - 1 : 0], 31);
+                    const T eprev = __shfl_sync(FULL, ev[m > 0 ? m - 1 : 0], 31);
+                    const T qnext = __shfl_sync(FULL, qv[m + 1 < NCH ? m + 1 : m], 0);
+                    if (lane == 0) {
+                        qm = m > 0 ? qprev : ((l > 0 && l - 1 < P) ? qc[l - 1] : T(0));
+                        em = m > 0 ? eprev : ((l > 0 && l - 1 < P) ? ec[l - 1] : T(0));
+                    }
+                    if (lane == 31) qp = m + 1 < NCH ? qnext : ((l + 1 < P) ? qc[l + 1] : T(0));
                     if (l < P) {
                         T h = dv[m] * qv[m];
-                        if (l > 0) h += em[m] * qm[m];
-                        if (l < g.n3) h += ev[m] * qp[m];
+                        if (l > 0) h += em * qm;
+                        if (l < g.n3) h += ev[m] * qp;
                         h += ahd * (l1[m] * ih1sq + l2[m] * ih2sq);
                         hc[l] = h;
                         if (PCG) acc += (double)qv[m] * (double)h;
@@ -244,7 +253,7 @@ __global__ void __launch_bounds__(256) pcg_init_kernel(Geom g, Ctl c, const T* _
 
 // A6 PCG update: x += a p, r -= a Hp, z = r/M; r.z, r.r; beta; stop test.
 template <typename T, int NCH>
-__global__ void __launch_bounds__(256) pcg_update_kernel(Geom g, Ctl c, SolveParams sp,
+__global__ void __launch_bounds__(256, 4) pcg_update_kernel(Geom g, Ctl c, SolveParams sp,
                                                          const T* __restrict__ dt, const T* __restrict__ p,
                                                          const T* __restrict__ Hp, T* __restrict__ x,
                                                          T* __restrict__ r) {
