@@ -333,12 +333,12 @@ static void launch_resident(hysco_ctx c, const SolveParams& sp, int pair) {
         RES_K_SWITCH(c->res_k, cudaLaunchKernelEx(&cfg, pcg_resident_kernel<RK, true>, c->g, c->ctl, sp, pair,
                                                   (const float*)B[B_GRAD], (const float*)B[B_DT],
                                                   (const float*)B[B_ET], B[B_X], c->res_pg, c->res_part,
-                                                  c->res_bar, c->res_nbmax));
+                                                  c->res_bar, c->res_nbmax, (unsigned long long*)nullptr));
     } else {
         RES_K_SWITCH(c->res_k, cudaLaunchKernelEx(&cfg, pcg_resident_kernel<RK, false>, c->g, c->ctl, sp, pair,
                                                   (const float*)B[B_GRAD], (const float*)B[B_DT],
                                                   (const float*)B[B_ET], B[B_X], c->res_pg, c->res_part,
-                                                  c->res_bar, c->res_nbmax));
+                                                  c->res_bar, c->res_nbmax, (unsigned long long*)nullptr));
     }
 }
 

@@ -21,6 +21,9 @@
 namespace hysco {
 
 constexpr int RES_THREADS = 768;
+#ifndef RES_XPOS
+#define RES_XPOS 0
+#endif
 
 // Compiler-only memory fence between the unrolled node slots: keeps ptxas from
 // hoisting every slot's loads to the top (which blows the 80-register budget
@@ -51,6 +54,11 @@ __device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
     return old;
 }
+// x += v at L2 with no return value: the owner is the only writer of x, so
+// the sum is the plain fp32 x + fl(a p) and no load latency is exposed.
+__device__ __forceinline__ void red_add(float* p, float v) {
+    asm volatile("red.relaxed.gpu.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
 __device__ __forceinline__ void red_release(unsigned* p, unsigned v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -62,8 +70,19 @@ __device__ __forceinline__ void grid_barrier(unsigned*, unsigned*) { cooperative
 
 // Block-reduce NV doubles, publish per-CTA partials, barrier, and fold all
 // partials in fixed order (identically in every CTA).  Result in out[] (all threads).
+// Optional phase trace (tools/res_trace.cu): thread 0 of every CTA stamps the
+// global timer at phase boundaries of the first 16 iterations.
+__device__ __forceinline__ void res_stamp(unsigned long long* tr) {
+    if (tr && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        *tr = t;
+    }
+}
+
 template <int NV>
-__device__ __forceinline__ void grid_reduce(double (&v)[NV], double* __restrict__ part, unsigned* bar, double (&out)[NV]) {
+__device__ __forceinline__ void grid_reduce(double (&v)[NV], double* __restrict__ part, unsigned* bar, double (&out)[NV],
+                                            unsigned long long* tr = nullptr) {
     __shared__ double sred[NV][32];
     __shared__ double stot[NV];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -80,6 +99,7 @@ __device__ __forceinline__ void grid_reduce(double (&v)[NV], double* __restrict_
         for (int w = 0; w < nw; w++) x += sred[threadIdx.x][w];
         part[blockIdx.x * NV + threadIdx.x] = x;
     }
+    res_stamp(tr);                         // all warps of this CTA are done with the phase
     grid_barrier(bar, bar + 1);
     if (wid == 0) {
 #pragma unroll
@@ -94,6 +114,51 @@ __device__ __forceinline__ void grid_reduce(double (&v)[NV], double* __restrict_
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < NV; k++) out[k] = stot[k];
+}
+
+// Split form of grid_reduce: publish this CTA's partials and arrive (returns
+// the arrival token), do independent work, then reduce_finish waits and folds
+// all partials in the same fixed order.
+template <int NV>
+__device__ __forceinline__ unsigned reduce_arrive(double (&v)[NV], double* __restrict__ part,
+                                                  const cooperative_groups::grid_group& grid) {
+    __shared__ double sred2[NV][32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int k = 0; k < NV; k++) {
+        double x = v[k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
+        if (lane == 0) sred2[k][wid] = x;
+    }
+    __syncthreads();
+    if (threadIdx.x < NV) {
+        double x = 0;
+        for (int w = 0; w < nw; w++) x += sred2[threadIdx.x][w];
+        part[blockIdx.x * NV + threadIdx.x] = x;
+    }
+    return grid.barrier_arrive();
+}
+
+template <int NV>
+__device__ __forceinline__ void reduce_finish(unsigned tok, const double* __restrict__ part,
+                                              const cooperative_groups::grid_group& grid, double (&out)[NV]) {
+    __shared__ double stot2[NV];
+    grid.barrier_wait(std::move(tok));
+    if ((threadIdx.x >> 5) == 0) {
+        const int lane = threadIdx.x & 31;
+#pragma unroll
+        for (int k = 0; k < NV; k++) {
+            double x = 0;
+            for (int b = lane; b < (int)gridDim.x; b += 32) x += __ldcg(&part[b * NV + k]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
+            if (lane == 0) stot2[k] = x;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < NV; k++) out[k] = stot2[k];
 }
 
 // Per-column flags of the CTA's columns: bits 0-3 = in-plane neighbour exists
@@ -132,7 +197,8 @@ template <int K, bool FIXED>
 __global__ void __launch_bounds__(RES_THREADS, 1)
     pcg_resident_kernel(Geom g, Ctl c, SolveParams sp, int pair, const float* __restrict__ grad,
                         const float* __restrict__ dt, const float* __restrict__ et, float* __restrict__ x,
-                        float* __restrict__ pgh, double* __restrict__ gpart, unsigned* bar, int nbmax) {
+                        float* __restrict__ pgh, double* __restrict__ gpart, unsigned* bar, int nbmax,
+                        unsigned long long* trace = nullptr) {
     count_launch(c);
     if (!c.st[pair].gn_active) return;       // uniform over the grid
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -207,7 +273,13 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
     double relres = rr0 > 0 ? 1.0 : 0.0;
     int k_it = 0, hev = 0;
     if (rr0 > 0.0) {
+        cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+        unsigned tok3 = 0;                    // pending split barrier "new p published"
+        bool pend3 = false;
         for (k_it = 0; k_it < sp.max_pcg;) {
+            unsigned long long* tr = (trace && k_it < 16) ? trace + ((size_t)blockIdx.x * 16 + k_it) * 8 : nullptr;
+            res_stamp(tr);
+            if (pend3) grid.barrier_wait(std::move(tok3));
             // j-halo columns (c0-1 and c1) from the global copy; zeros off the ends
             for (int t = threadIdx.x; t < 2 * P; t += NT) {
                 const bool nxt = t >= P;
@@ -218,6 +290,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
                 sp_[(nxt ? Nb : -P) + l] = v;
             }
             __syncthreads();
+            res_stamp(tr ? tr + 1 : nullptr);
             // ---- Hp = M p + et_{l-1} p_{l-1} + et_l p_{l+1} - alpha hd sum_inplane p_nb / h^2
             float fpq = 0.f;
             {
@@ -247,53 +320,73 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
                 }
             }
             double v1[1] = {(double)fpq}, t1[1];
-            grid_reduce<1>(v1, part1, bar, t1);
+            grid_reduce<1>(v1, part1, bar, t1, tr ? tr + 2 : nullptr);
+            res_stamp(tr ? tr + 3 : nullptr);
             if (t1[0] <= 0.0) break;                  // breakdown (oracle pcg(): keep x)
             hev += 1;
             const float a = (float)(rz / t1[0]);
-            // ---- x += a p, r -= a Hp, z = r/M; r.z, r.r
+            // ---- r -= a Hp, z = r/M (kept in the dead Hp registers); r.z, r.r
             float frz2 = 0.f, frr2 = 0.f;
             {
                 const int tid = opaque(threadIdx.x);
-                const unsigned mv = (unsigned)opaque((int)mval);
-                float* xt = xl + tid;
-                const float* s0 = sp_ + tid;
                 const float* m0 = sM + tid;
 #pragma unroll
                 for (int k = 0; k < K; k++) {
-                    const int o = k * NT;
-                    if (mv & (1u << k)) xt[o] = fmaf(a, s0[o], xt[o]);
                     const float rn = fmaf(-a, hv[k], r[k]);
                     r[k] = rn;
-                    const float z = precond(rn, m0[o]);
+                    const float z = precond(rn, m0[k * NT]);
+                    hv[k] = z;
                     frz2 = fmaf(rn, z, frz2);
                     frr2 = fmaf(rn, rn, frr2);
                 }
             }
             double v3[2] = {(double)frz2, (double)frr2}, t3[2];
-            grid_reduce<2>(v3, part2, bar, t3);
+            const unsigned tok2 = reduce_arrive<2>(v3, part2, grid);
+            res_stamp(tr ? tr + 4 : nullptr);
+            // ---- x += a p while the r.z / r.r partials gather (fire-and-forget L2
+            // adds; x feeds no reduction)
+#if RES_XPOS == 0
+            {
+                const int tid = opaque(threadIdx.x);
+                const unsigned mv = (unsigned)opaque((int)mval);
+                float* xt = xl + tid;
+                const float* s0 = sp_ + tid;
+#pragma unroll
+                for (int k = 0; k < K; k++)
+                    if (mv & (1u << k)) red_add(xt + k * NT, a * s0[k * NT]);
+            }
+#endif
+            reduce_finish<2>(tok2, part2, grid, t3);
+            res_stamp(tr ? tr + 5 : nullptr);
             k_it += 1;
             relres = sqrt(t3[1] / rr0);
             const double beta = t3[0] / rz;
             rz = t3[0];
-            if (k_it >= sp.max_pcg || (!sp.fixed && relres < sp.pcg_rtol)) break;
-            // ---- p = z + beta p (own columns; the global copy feeds the neighbours' halo)
+            const bool last = k_it >= sp.max_pcg || (!sp.fixed && relres < sp.pcg_rtol);
+            // ---- p = z + beta p on own columns and on the global halo copy
             const float be = (float)beta;
             {
                 const int tid = opaque(threadIdx.x);
                 const unsigned mv = (unsigned)opaque((int)mval);
                 float* s0 = sp_ + tid;
                 float* gt = pgc + tid;
-                const float* m0 = sM + tid;
+                float* xt = xl + tid;
 #pragma unroll
                 for (int k = 0; k < K; k++) {
                     const int o = k * NT;
-                    const float pn = fmaf(be, s0[o], precond(r[k], m0[o]));
-                    s0[o] = pn;
-                    if (mv & (1u << k)) gt[o] = pn;
+                    const float pv = s0[o];
+                    if (RES_XPOS == 1 && (mv & (1u << k))) red_add(xt + o, a * pv);
+                    if (!last) {
+                        const float pn = fmaf(be, pv, hv[k]);
+                        s0[o] = pn;
+                        if (mv & (1u << k)) gt[o] = pn;
+                    }
                 }
             }
-            grid_barrier(bar, bar + 1);
+            if (last) break;
+            res_stamp(tr ? tr + 6 : nullptr);
+            tok3 = grid.barrier_arrive();
+            pend3 = true;
         }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {

@@ -1,0 +1,103 @@
+// res_trace.cu — phase timeline of the resident PCG kernel on a 3T-shaped
+// problem (diagnostic; not part of the library).  Each CTA's thread 0 stamps
+// %globaltimer at the phase boundaries of every iteration; we print, per
+// phase, the mean over iterations of (last CTA end - first CTA start) and of
+// the per-CTA durations, which separates compute from barrier skew.
+// build: nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a \
+//        -I paper_2403_10706_b200/csrc -I include -o tools/res_trace tools/res_trace.cu
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include <algorithm>
+#include "hysco_kernels.cuh"
+
+using namespace hysco;
+
+int main(int argc, char** argv) {
+    int n1 = 168, n2 = 111, n3 = 144;
+    if (argc > 3) { n1 = atoi(argv[1]); n2 = atoi(argv[2]); n3 = atoi(argv[3]); }
+    Geom g{};
+    g.n1 = n1; g.n2 = n2; g.n3 = n3; g.P = n3 + 1; g.ncol = (long long)n1 * n2;
+    g.Nc = g.ncol * n3; g.Nn = g.ncol * g.P; g.ps = g.Nn; g.i0 = 0; g.n1g = n1; g.slab = 0;
+    g.h1 = g.h2 = g.h3 = 1.25; g.hd = 1.25 * 1.25 * 1.25; g.alpha = 300; g.beta = 1e-4;
+    g.ahd = g.alpha * g.hd; g.bh2 = 0.5e-4 * g.hd;
+    g.ih1sq = g.ih2sq = g.ih3sq = 1 / (1.25 * 1.25); g.ih3 = 1 / 1.25;
+    int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    const int G = nsm, NT = RES_THREADS, K = 24;
+    const long long ncl = (g.ncol + G - 1) / G, knt = (long long)K * NT;
+    if (ncl * g.P > knt) { printf("does not fit K=24\n"); return 1; }
+    size_t Nn = g.Nn;
+    std::vector<float> hdt(Nn), het(Nn), hg(Nn);
+    srand(1);
+    for (size_t t = 0; t < Nn; t++) {
+        hdt[t] = 1e5f + 1e4f * (rand() / (float)RAND_MAX);
+        het[t] = ((t % g.P) == (size_t)n3) ? 0.f : -300.f - 4e4f * (rand() / (float)RAND_MAX);
+        hg[t] = (rand() / (float)RAND_MAX) - 0.5f;
+    }
+    float *dt, *et, *grad, *x, *pgh;
+    cudaMalloc(&dt, Nn * 4); cudaMalloc(&et, Nn * 4); cudaMalloc(&grad, Nn * 4); cudaMalloc(&x, Nn * 4);
+    size_t ghost = res_ghost_pair_floats(g);
+    cudaMalloc(&pgh, ghost * 4); cudaMemset(pgh, 0, ghost * 4);
+    cudaMemcpy(dt, hdt.data(), Nn * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(et, het.data(), Nn * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(grad, hg.data(), Nn * 4, cudaMemcpyHostToDevice);
+    PairState* st; cudaMalloc(&st, sizeof(PairState));
+    PairState hs{}; hs.gn_active = 1; cudaMemcpy(st, &hs, sizeof hs, cudaMemcpyHostToDevice);
+    unsigned long long* launches; cudaMalloc(&launches, 8);
+    double* part; cudaMalloc(&part, sizeof(double) * 8 * G);
+    unsigned* bar; cudaMalloc(&bar, 8); cudaMemset(bar, 0, 8);
+    unsigned long long* trace; cudaMalloc(&trace, sizeof(unsigned long long) * G * 16 * 8);
+    cudaMemset(trace, 0, sizeof(unsigned long long) * G * 16 * 8);
+    Ctl c{}; c.st = st; c.launches = launches;
+    SolveParams sp{}; sp.max_pcg = 10; sp.fixed = 1;
+    const size_t smem = (size_t)(3 * knt + 2 * g.P + 8) * sizeof(float);
+    cudaFuncSetAttribute(pcg_resident_kernel<24, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(G); cfg.blockDim = dim3(NT); cfg.dynamicSmemBytes = smem; cfg.stream = 0;
+    cudaLaunchAttribute at[1]; at[0].id = cudaLaunchAttributeCooperative; at[0].val.cooperative = 1;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    float ms_notrace = 0, ms_trace = 0;
+    for (int rep = 0; rep < 3; rep++) {
+        cudaEventRecord(e0);
+        cudaLaunchKernelEx(&cfg, pcg_resident_kernel<24, true>, g, c, sp, 0, (const float*)grad, (const float*)dt,
+                           (const float*)et, x, pgh, part, bar, 0, (unsigned long long*)nullptr);
+        cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms_notrace, e0, e1);
+    }
+    cudaEventRecord(e0);
+    cudaLaunchKernelEx(&cfg, pcg_resident_kernel<24, true>, g, c, sp, 0, (const float*)grad, (const float*)dt,
+                       (const float*)et, x, pgh, part, bar, 0, trace);
+    cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms_trace, e0, e1);
+    printf("err=%s  kernel %.1f us (untraced), %.1f us (traced), grid %d x %d, K %d\n",
+           cudaGetErrorString(cudaGetLastError()), ms_notrace * 1e3, ms_trace * 1e3, G, NT, K);
+    std::vector<unsigned long long> ht((size_t)G * 16 * 8);
+    cudaMemcpy(ht.data(), trace, ht.size() * 8, cudaMemcpyDeviceToHost);
+    const char* names[9] = {"iter start", "p-barrier + j-halo", "Hp done (CTA)", "reduce #1 done",
+                            "U-phase, arrive #2", "x upd + reduce #2", "D-phase, arrive #3", "(unused)",
+                            "next iter start"};
+    // per phase k -> k+1: span = max_cta(t[k+1]) - min_cta(t[k]); cta = mean over CTAs of (t[k+1]-t[k])
+    for (int k = 0; k < 7; k++) {
+        double span = 0, mean_cta = 0, max_cta = 0, min_cta = 1e30;
+        int nit = 0;
+        for (int it = 1; it < 9; it++) {
+            unsigned long long mn = ~0ull, mx = 0;
+            double acc = 0, mxd = 0, mnd = 1e30;
+            for (int b = 0; b < G; b++) {
+                unsigned long long a = ht[((size_t)b * 16 + it) * 8 + k];
+                unsigned long long z = k < 6 ? ht[((size_t)b * 16 + it) * 8 + k + 1] : ht[((size_t)b * 16 + it + 1) * 8];
+                mn = std::min(mn, a); mx = std::max(mx, z);
+                double d = (double)(z - a); acc += d; mxd = std::max(mxd, d); mnd = std::min(mnd, d);
+            }
+            span += (double)(mx - mn); mean_cta += acc / G; max_cta += mxd; min_cta = std::min(min_cta, mnd); nit++;
+        }
+        printf("%-22s -> %-22s span %7.2f us | per-CTA mean %7.2f max %7.2f min %7.2f us\n", names[k], names[k == 6 ? 8 : k + 1],
+               span / nit / 1e3, mean_cta / nit / 1e3, max_cta / nit / 1e3, min_cta / 1e3);
+    }
+    // iteration period
+    double per = 0;
+    for (int it = 1; it < 9; it++) per += (double)(ht[(size_t)it * 8 + 0] - ht[(size_t)(it - 1) * 8 + 0]);
+    printf("iteration period (CTA 0): %.2f us\n", per / 8 / 1e3);
+    PairState hs2; cudaMemcpy(&hs2, st, sizeof hs2, cudaMemcpyDeviceToHost);
+    printf("pcg_k %d h_evals %d relres %.3e\n", hs2.pcg_k, hs2.h_evals, hs2.relres);
+    return 0;
+}
