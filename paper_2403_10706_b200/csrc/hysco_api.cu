@@ -824,7 +824,7 @@ template <typename T>
 static hysco_status setup_typed(hysco_ctx ctx) {
     const Geom& g = ctx->g;
     const long long batch = ctx->cfg.batch;
-    ctx->smem_eval = (size_t)8 * (2 * g.n3 + 5 * g.P) * sizeof(T);   // eval / apply column staging
+    ctx->smem_eval = eval_smem_elems(g.n3) * sizeof(T);   // eval tile staging (also covers apply's columns)
     ctx->smem_ot = (size_t)8 * 2 * g.P * sizeof(double);
     if (ctx->smem_eval > 227 * 1024 || ctx->smem_ot > 227 * 1024)
         return set_err(ctx, HYSCO_ERR_SHAPE, "n3 too large for the column-in-shared-memory kernels");

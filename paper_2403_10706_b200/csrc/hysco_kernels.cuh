@@ -128,27 +128,39 @@ __device__ inline void decide_eval(const Geom& g, const Ctl& c, const SolveParam
 }
 
 // ---------------------------------------------------------------------------
-// A4 fused evaluation: one warp per PE column, the
-// column of I+, I-, b staged in shared memory.  Per cell: Ab, Db, both
-// gathers with slopes, residual r, GN Jacobian row (a, c), phi, phi', phi''.
-// Per node: grad J (data + alpha hd L b + barrier), folded tridiagonal
-// Hessian (dt: diagonal incl. alpha hd L_PE; et: super-diagonal incl.
-// -alpha hd / h3^2) — DESIGN.md "Folded GN Hessian".  Scalars D, S, P and
-// ||grad||^2 reduce per pair; TRIAL mode also takes the Armijo decision (R15).
+// A4 fused evaluation.  A CTA takes a tile of EV_CT
+// consecutive columns (one per warp) and stages, with every load of the tile
+// in flight, the b columns c0-1 .. c0+EV_CT (own and j-neighbours, shared
+// between warps), the i-1 / i+1 b columns and the zero-padded I+, I- columns.
+// Per cell: Ab, Db, both gathers with slopes, residual r, GN Jacobian row
+// (a, c), phi, phi', phi''.  Per node: grad J (data + alpha hd L b +
+// barrier), folded tridiagonal Hessian (dt: diagonal incl. alpha hd L_PE;
+// et: super-diagonal incl. -alpha hd / h3^2) -- DESIGN.md "Folded GN Hessian".
+// Scalars D, S, P and ||grad||^2 reduce per pair; TRIAL mode also takes the
+// Armijo decision (R15).
 // ---------------------------------------------------------------------------
-// One cell's two gathers (I+ at k + Ab/h3, I- at k - Ab/h3): values in fp64,
-// slopes (per index unit) in T.  fp32: floor/fraction from the cell-relative
-// offset and v0 + t (v1 - v0) with the difference exact in fp64; fp64: the
-// oracle's arithmetic (absolute coordinate, (1-t) v0 + t v1), see R5.
+constexpr int EV_CT = 8;   // columns per tile = warps per CTA
+
+// Shared-memory elements of one eval tile (hysco_api.cu sizes the launch with this).
+__host__ __device__ inline size_t eval_smem_elems(int n3) {
+    const size_t P = (size_t)n3 + 1;
+    return (3 * EV_CT + 2) * P + 2 * EV_CT * ((size_t)n3 + 4);
+}
+
+// One cell's two gathers (I+ at k + Ab/h3, I- at k - Ab/h3) from columns
+// padded with two zeros on each side (index kk clamped to [-2, n3] reads the
+// same values as the unpadded bounds tests).  Values in fp64, slopes (per
+// index unit) in T.  fp32: floor/fraction from the cell-relative offset and
+// v0 + t (v1 - v0) with the difference exact in fp64; fp64: the oracle's
+// arithmetic (absolute coordinate, (1-t) v0 + t v1), see R5.
 __device__ __forceinline__ void gather_pm(const float* __restrict__ sIp, const float* __restrict__ sIm, int n3, int k,
                                           float Ab, const Geom& g, double& vp, double& vm, float& spl, float& sml) {
     float del = Ab * (float)g.ih3;
     del = fminf(fmaxf(del, (float)-(n3 + 2)), (float)(n3 + 2));
     {
         const float fl = floorf(del);
-        const int kk = k + (int)fl;
-        const float v0 = (kk >= 0 && kk < n3) ? sIp[kk] : 0.f;
-        const float v1 = (kk + 1 >= 0 && kk + 1 < n3) ? sIp[kk + 1] : 0.f;
+        const int kk = min(max(k + (int)fl, -2), n3);
+        const float v0 = sIp[kk], v1 = sIp[kk + 1];
         const double d = (double)v1 - (double)v0;
         vp = fma((double)(del - fl), d, (double)v0);
         spl = (float)d;
@@ -156,18 +168,27 @@ __device__ __forceinline__ void gather_pm(const float* __restrict__ sIp, const f
     {
         const float md = -del;
         const float fl = floorf(md);
-        const int kk = k + (int)fl;
-        const float v0 = (kk >= 0 && kk < n3) ? sIm[kk] : 0.f;
-        const float v1 = (kk + 1 >= 0 && kk + 1 < n3) ? sIm[kk + 1] : 0.f;
+        const int kk = min(max(k + (int)fl, -2), n3);
+        const float v0 = sIm[kk], v1 = sIm[kk + 1];
         const double d = (double)v1 - (double)v0;
         vm = fma((double)(md - fl), d, (double)v0);
         sml = (float)d;
     }
 }
+__device__ __forceinline__ void gather_one(const double* __restrict__ s, int n3, int k, double Ab, double sign,
+                                           const Geom& g, double& val, double& slope) {
+    double u = (double)k + sign * (Ab / g.h3);
+    u = fmin(fmax(u, -2.0 * (n3 + 2)), 2.0 * (n3 + 2));
+    const double fl = floor(u);
+    const int kk = min(max((int)fl, -2), n3);
+    const double t = u - fl, v0 = s[kk], v1 = s[kk + 1];
+    val = (1.0 - t) * v0 + t * v1;
+    slope = v1 - v0;
+}
 __device__ __forceinline__ void gather_pm(const double* __restrict__ sIp, const double* __restrict__ sIm, int n3, int k,
                                           double Ab, const Geom& g, double& vp, double& vm, double& spl, double& sml) {
-    interp_col(sIp, n3, k, Ab, 1.0, g, vp, spl);
-    interp_col(sIm, n3, k, Ab, -1.0, g, vm, sml);
+    gather_one(sIp, n3, k, Ab, 1.0, g, vp, spl);
+    gather_one(sIm, n3, k, Ab, -1.0, g, vm, sml);
 }
 
 // phi, phi', phi'' (Eq.(3)) for |z| < 1 with one reciprocal of (1 - z^2).
@@ -179,6 +200,23 @@ __device__ __forceinline__ void phi3(T z, T& f0, T& f1, T& f2) {
     f2 = T(2) * z2 * (T(6) - T(3) * z2 + z2 * z2) * inv * inv * inv;
 }
 
+// Load NCH x 32 elements of a column (l < len) into registers, then store
+// them to shared memory: all loads of the column are in flight together.
+template <typename T, int NCH>
+__device__ __forceinline__ void stage_col(const T* __restrict__ src, T* dst, int len, int lane) {
+    T v[NCH];
+#pragma unroll
+    for (int m = 0; m < NCH; m++) {
+        const int l = 32 * m + lane;
+        v[m] = l < len ? src[l] : T(0);
+    }
+#pragma unroll
+    for (int m = 0; m < NCH; m++) {
+        const int l = 32 * m + lane;
+        if (l < len) dst[l] = v[m];
+    }
+}
+
 template <typename T, int NCH>
 __global__ void __launch_bounds__(256, 4) eval_kernel(Geom g, Ctl c, SolveParams sp, int mode,
                                                    const T* __restrict__ Ip, const T* __restrict__ Im,
@@ -186,18 +224,22 @@ __global__ void __launch_bounds__(256, 4) eval_kernel(Geom g, Ctl c, SolveParams
                                                    T* __restrict__ dt, T* __restrict__ et) {
     count_launch(c);
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int pair = blockIdx.y;
-    const int n3 = g.n3, P = g.P, n2 = g.n2;
-    // per warp: I+, I-, b of the column and b of its four in-plane neighbour
-    // columns, all staged before any compute (every load of a column in flight)
-    T* sIp = reinterpret_cast<T*>(smem_raw) + (size_t)wid * (2 * n3 + 5 * P);
-    T* sIm = sIp + n3;
-    T* sb = sIm + n3;
-    T* sbim = sb + P;
-    T* sbip = sbim + P;
-    T* sbjm = sbip + P;
-    T* sbjp = sbjm + P;
+    const int n3 = g.n3, P = g.P, n2 = g.n2, IS = n3 + 4;
+    // tile staging: b of columns c0-1 .. c0+EV_CT, b of the i-1 and i+1 columns,
+    // I+ / I- of the tile columns with two zero pads on each side
+    T* sb = reinterpret_cast<T*>(smem_raw);
+    T* sbim = sb + (EV_CT + 2) * P;
+    T* sbip = sbim + EV_CT * P;
+    T* sIp = sbip + EV_CT * P + (size_t)wid * 2 * IS + 2;
+    T* sIm = sIp + IS;
+    if (lane < 2) {
+        sIp[-2 + lane] = T(0);
+        sIp[n3 + lane] = T(0);
+        sIm[-2 + lane] = T(0);
+        sIm[n3 + lane] = T(0);
+    }
 
     bool active = true;
     if (mode == EVAL_TRIAL) active = c.st[pair].ls_active != 0;
@@ -205,111 +247,113 @@ __global__ void __launch_bounds__(256, 4) eval_kernel(Geom g, Ctl c, SolveParams
     const T hd = (T)g.hd, ahd = (T)g.ahd, bh2 = (T)g.bh2;
     const T ih3 = (T)g.ih3, ih3sq = (T)g.ih3sq, ih1sq = (T)g.ih1sq, ih2sq = (T)g.ih2sq;
     const long long sI = (long long)n2 * P;   // node stride along dim 1
+    const T* bp = bb + (size_t)pair * g.ps;
+    const T* ipp = Ip + (size_t)pair * g.Nc;
+    const T* imp = Im + (size_t)pair * g.Nc;
 
     double aD = 0, aS = 0, aP = 0, aG = 0, aInf = 0;
     if (active) {
-        for (long long col = (long long)blockIdx.x * nwb + wid; col < g.ncol; col += (long long)gridDim.x * nwb) {
-            const T* ip = Ip + (size_t)pair * g.Nc + col * n3;
-            const T* im = Im + (size_t)pair * g.Nc + col * n3;
-            const size_t ob = (size_t)pair * g.ps + (size_t)col * P;
-            const T* bc = bb + ob;
-            T* gc = grad + ob;
-            T* dc = dt + ob;
-            T* ec = et + ob;
+        for (long long c0 = (long long)blockIdx.x * EV_CT; c0 < g.ncol; c0 += (long long)gridDim.x * EV_CT) {
+            const long long col = c0 + wid;
+            const bool valid = col < g.ncol;
             const int i = (int)(col / n2), j = (int)(col - (long long)i * n2);
-            const bool him = has_im(g, i), hip = has_ip(g, i), hjm = j > 0, hjp = j < n2 - 1;
-            for (int k = lane; k < n3; k += 32) {
-                sIp[k] = ip[k];
-                sIm[k] = im[k];
+            const bool him = valid && has_im(g, i), hip = valid && has_ip(g, i), hjm = j > 0, hjp = j < n2 - 1;
+            if (valid) {
+                const T* bc = bp + col * P;
+                stage_col<T, NCH>(bc, sb + (wid + 1) * P, P, lane);
+                if (him) stage_col<T, NCH>(bc - sI, sbim + wid * P, P, lane);
+                if (hip) stage_col<T, NCH>(bc + sI, sbip + wid * P, P, lane);
+                stage_col<T, NCH>(ipp + col * n3, sIp, n3, lane);
+                stage_col<T, NCH>(imp + col * n3, sIm, n3, lane);
             }
-            for (int l = lane; l < P; l += 32) {
-                sb[l] = bc[l];
-                if (him) sbim[l] = bc[l - sI];
-                if (hip) sbip[l] = bc[l + sI];
-                if (hjm) sbjm[l] = bc[l - P];
-                if (hjp) sbjp[l] = bc[l + P];
-            }
-            __syncwarp();
-            T fS = 0, fG = 0, fP = 0;                 // per-lane partials of this column
-            T cr_c = 0, c2_c = 0, p1_c = 0, p2_c = 0;   // carry: cell (chunk start - 1) -> node
-            for (int seg = 0; seg < P; seg += 32 * NCH) {
+            if (wid == 0 && c0 > 0) stage_col<T, NCH>(bp + (c0 - 1) * P, sb, P, lane);
+            if (wid == EV_CT - 1 && c0 + EV_CT < g.ncol) stage_col<T, NCH>(bp + (c0 + EV_CT) * P, sb + (EV_CT + 1) * P, P, lane);
+            __syncthreads();
+            if (valid) {
+                T* gc = grad + (size_t)pair * g.ps + col * P;
+                T* dc = dt + (size_t)pair * g.ps + col * P;
+                T* ec = et + (size_t)pair * g.ps + col * P;
+                const T* sbc = sb + (wid + 1) * P;
+                // a missing in-plane neighbour reads the column itself: b - b = 0
+                // adds exactly nothing to L b or to the |grad b|^2 terms (R3)
+                const T* sjm = hjm ? sbc - P : sbc;
+                const T* sjp = hjp ? sbc + P : sbc;
+                const T* sim = him ? sbim + wid * P : sbc;
+                const T* sip = hip ? sbip + wid * P : sbc;
+                T fS = 0, fG = 0, fP = 0;                 // per-lane partials of this column
+                T cr_c = 0, c2_c = 0, p1_c = 0, p2_c = 0;   // lane 0: cell (chunk start - 1) -> node
+                for (int seg = 0; seg < P; seg += 32 * NCH) {
 #pragma unroll
-                for (int m = 0; m < NCH; m++) {
-                    const int l = seg + 32 * m + lane;
-                    T ar = 0, a2 = 0, cr = 0, c2 = 0, p1 = 0, p2 = 0, ev = 0;
-                    if (l < n3) {
-                        const T b0 = sb[l], b1 = sb[l + 1];
-                        const T Ab = T(0.5) * (b0 + b1);          // averaging operator A
-                        const T Db = diff_h3(b0, b1, g);          // finite difference D
-                        double vp, vm;
-                        T spl, sml;
-                        gather_pm(sIp, sIm, n3, l, Ab, g, vp, vm, spl, sml);   // I+(x + b), I-(x - b)
-                        const double Dbd = (double)Db;
-                        const double rd = vp * (1.0 + Dbd) - vm * (1.0 - Dbd);  // Eq.(1)-(2) residual (fp64)
-                        const T r = (T)rd;
-                        const T gg = (spl * (T(1) + Db) + sml * (T(1) - Db)) * ih3;
-                        const T s = (T)(vp + vm);
-                        const T a = gg * T(0.5) - s * ih3;        // dr_k/db_k
-                        const T cc = gg * T(0.5) + s * ih3;       // dr_k/db_{k+1}
-                        aD = fma(rd, rd, aD);
-                        const T dd = b1 - b0;
-                        fS += dd * dd * ih3sq;
-                        if (fabs(Db) >= T(1)) {
-                            aInf = 1.0;                           // phi = +inf (Eq.(3))
-                        } else {
-                            T f0;
-                            phi3(Db, f0, p1, p2);
-                            fP += f0;
+                    for (int m = 0; m < NCH; m++) {
+                        const int l = seg + 32 * m + lane;
+                        T ar = 0, a2 = 0, cr = 0, c2 = 0, p1 = 0, p2 = 0, ev = 0;
+                        if (l < n3) {
+                            const T b0 = sbc[l], b1 = sbc[l + 1];
+                            const T Ab = T(0.5) * (b0 + b1);          // averaging operator A
+                            const T Db = diff_h3(b0, b1, g);          // finite difference D
+                            double vp, vm;
+                            T spl, sml;
+                            gather_pm(sIp, sIm, n3, l, Ab, g, vp, vm, spl, sml);   // I+(x + b), I-(x - b)
+                            const double Dbd = (double)Db;
+                            const double rd = vp * (1.0 + Dbd) - vm * (1.0 - Dbd);  // Eq.(1)-(2) residual (fp64)
+                            const T r = (T)rd;
+                            const T gg = (spl * (T(1) + Db) + sml * (T(1) - Db)) * ih3;
+                            const T s = (T)(vp + vm);
+                            const T a = gg * T(0.5) - s * ih3;        // dr_k/db_k
+                            const T cc = gg * T(0.5) + s * ih3;       // dr_k/db_{k+1}
+                            aD = fma(rd, rd, aD);
+                            const T dd = b1 - b0;
+                            fS += dd * dd * ih3sq;
+                            if (fabs(Db) >= T(1)) {
+                                aInf = 1.0;                           // phi = +inf (Eq.(3))
+                            } else {
+                                T f0;
+                                phi3(Db, f0, p1, p2);
+                                fP += f0;
+                            }
+                            ar = a * r;
+                            a2 = a * a;
+                            cr = cc * r;
+                            c2 = cc * cc;
+                            ev = hd * a * cc - bh2 * p2 * ih3sq - ahd * ih3sq;
                         }
-                        ar = a * r;
-                        a2 = a * a;
-                        cr = cc * r;
-                        c2 = cc * cc;
-                        ev = hd * a * cc - bh2 * p2 * ih3sq - ahd * ih3sq;
-                    }
-                    T pcr = __shfl_up_sync(FULL, cr, 1), pc2 = __shfl_up_sync(FULL, c2, 1);
-                    T pp1 = __shfl_up_sync(FULL, p1, 1), pp2 = __shfl_up_sync(FULL, p2, 1);
-                    if (lane == 0) {
-                        pcr = cr_c;
-                        pc2 = c2_c;
-                        pp1 = p1_c;
-                        pp2 = p2_c;
-                    }
-                    cr_c = __shfl_sync(FULL, cr, 31);
-                    c2_c = __shfl_sync(FULL, c2, 31);
-                    p1_c = __shfl_sync(FULL, p1, 31);
-                    p2_c = __shfl_sync(FULL, p2, 31);
-                    if (l < P) {
-                        const T bl = sb[l];
-                        T lpe = 0, l1 = 0, l2 = 0;
-                        if (l > 0) lpe += bl - sb[l - 1];
-                        if (l < n3) lpe += bl - sb[l + 1];
-                        if (him) l1 += bl - sbim[l];
-                        if (hip) {
-                            const T v = sbip[l];
-                            l1 += bl - v;
-                            fS += (v - bl) * (v - bl) * ih1sq;
+                        // cell l-1 -> node l: one rotation per quantity; lane 0 takes the
+                        // previous chunk's lane 31 (kept from the last rotation)
+                        const T rcr = __shfl_sync(FULL, cr, (lane + 31) & 31);
+                        const T rc2 = __shfl_sync(FULL, c2, (lane + 31) & 31);
+                        const T rp1 = __shfl_sync(FULL, p1, (lane + 31) & 31);
+                        const T rp2 = __shfl_sync(FULL, p2, (lane + 31) & 31);
+                        const T pcr = lane ? rcr : cr_c, pc2 = lane ? rc2 : c2_c;
+                        const T pp1 = lane ? rp1 : p1_c, pp2 = lane ? rp2 : p2_c;
+                        cr_c = rcr;
+                        c2_c = rc2;
+                        p1_c = rp1;
+                        p2_c = rp2;
+                        if (l < P) {
+                            const T bl = sbc[l];
+                            T lpe = 0, l1 = 0, l2 = 0;
+                            if (l > 0) lpe += bl - sbc[l - 1];
+                            if (l < n3) lpe += bl - sbc[l + 1];
+                            const T vip = sip[l], vjp = sjp[l];
+                            l1 = (bl - sim[l]) + (bl - vip);
+                            fS += (vip - bl) * (vip - bl) * ih1sq;
+                            l2 = (bl - sjm[l]) + (bl - vjp);
+                            fS += (vjp - bl) * (vjp - bl) * ih2sq;
+                            const T Lb = lpe * ih3sq + l1 * ih1sq + l2 * ih2sq;
+                            const T gv = hd * (pcr + ar) + ahd * Lb + bh2 * (pp1 - p1) * ih3;
+                            const T dv = hd * (pc2 + a2) + bh2 * (pp2 + p2) * ih3sq + ahd * T((l > 0) + (l < n3)) * ih3sq;
+                            gc[l] = gv;
+                            dc[l] = dv;
+                            ec[l] = (l < n3) ? ev : T(0);
+                            fG += gv * gv;
                         }
-                        if (hjm) l2 += bl - sbjm[l];
-                        if (hjp) {
-                            const T v = sbjp[l];
-                            l2 += bl - v;
-                            fS += (v - bl) * (v - bl) * ih2sq;
-                        }
-                        const T Lb = lpe * ih3sq + l1 * ih1sq + l2 * ih2sq;
-                        const T gv = hd * (pcr + ar) + ahd * Lb + bh2 * (pp1 - p1) * ih3;
-                        const T dv = hd * (pc2 + a2) + bh2 * (pp2 + p2) * ih3sq + ahd * T((l > 0) + (l < n3)) * ih3sq;
-                        gc[l] = gv;
-                        dc[l] = dv;
-                        ec[l] = (l < n3) ? ev : T(0);
-                        fG += gv * gv;
                     }
                 }
+                aS += (double)fS;
+                aG += (double)fG;
+                aP += (double)fP;
             }
-            aS += (double)fS;
-            aG += (double)fG;
-            aP += (double)fP;
-            __syncwarp();
+            __syncthreads();
         }
     }
     double v[5] = {aD, aS, aP, aG, aInf}, tot[5];

@@ -290,11 +290,17 @@ def test_graph_and_host_loop_bitwise_equal(monkeypatch):
     assert out[0][2] == out[1][2]
 
 
-@pytest.mark.parametrize("cfg", ["C1_16x16x8", "C2_hcp3t"])
+# tile orders of the resident PCG (hysco_resident.cuh): rows per strip R = 1
+# (C1), 12 (3T), 4 with square tiles, 4 with ragged tiles (odd n2), and 2 with
+# local neighbours across a strip edge (n2 = 2)
+RESIDENT_CASES = ["C1_16x16x8", "C2_hcp3t", (60, 40, 16), (84, 37, 10), (400, 2, 10)]
+
+
+@pytest.mark.parametrize("cfg", RESIDENT_CASES, ids=[str(c) for c in RESIDENT_CASES])
 def test_resident_pcg_matches_streaming(monkeypatch, cfg):
     """The on-chip-resident PCG (one cooperative launch per GN step) and the
     streaming PCG kernels compute the same iteration (reduction order aside)."""
-    p = phantom.make_config(cfg)
+    p = phantom.make_config(cfg) if isinstance(cfg, str) else phantom.make_pair(cfg, (1.25, 1.25, 1.25), 11)
     out = []
     for nr in ("0", "1"):
         monkeypatch.setenv("HYSCO_NO_RESIDENT", nr)
@@ -304,9 +310,12 @@ def test_resident_pcg_matches_streaming(monkeypatch, cfg):
         out.append((c.np(b)[0], reps[0], H.hysco_last_launch_count(c.ctx)))
         c.close()
     (b_res, r_res, n_res), (b_str, r_str, n_str) = out
+    # fp32 reduction order differs (per-CTA partials vs per-block partials), so
+    # alpha/beta round differently; after 10 unconverged GN steps b and J move
+    # at first order in that rounding -- both gated at the kernel tolerance
     assert rel(b_res, b_str) <= 1e-5
     assert (r_res["pcg_iters"], r_res["h_evals"], r_res["gn_iters"]) == (r_str["pcg_iters"], r_str["h_evals"], r_str["gn_iters"])
-    assert relS(r_res["J"], r_str["J"]) <= 1e-6
+    assert relS(r_res["J"], r_str["J"]) <= 1e-5
     # resident: one PCG launch per GN step instead of pcg_init + 10 x (matvec, update, dir)
     assert n_str - n_res == 10 * 30
 
