@@ -21,14 +21,6 @@
 namespace hysco {
 
 constexpr int RES_THREADS = 768;
-#ifndef RES_XPOS
-#define RES_XPOS 0
-#endif
-
-// Compiler-only memory fence between the unrolled node slots: keeps ptxas from
-// hoisting every slot's loads to the top (which blows the 80-register budget
-// of a 768-thread CTA and spills into an L1 that shared memory has consumed).
-__device__ __forceinline__ void slot_fence() { asm volatile("" ::: "memory"); }
 
 // Opaque copy: stops ptxas from hoisting per-slot index math (and everything
 // derived from it) out of the PCG iteration loop, which would keep ~15
@@ -38,29 +30,10 @@ __device__ __forceinline__ int opaque(int v) {
     asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
     return r;
 }
-template <typename P_>
-__device__ __forceinline__ P_* opaque_ptr(P_* p) {
-    unsigned long long r;
-    asm volatile("mov.b64 %0, %1;" : "=l"(r) : "l"((unsigned long long)p));
-    return reinterpret_cast<P_*>(r);
-}
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
-    unsigned old;
-    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-    return old;
-}
 // x += v at L2 with no return value: the owner is the only writer of x, so
 // the sum is the plain fp32 x + fl(a p) and no load latency is exposed.
 __device__ __forceinline__ void red_add(float* p, float v) {
     asm volatile("red.relaxed.gpu.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
-}
-__device__ __forceinline__ void red_release(unsigned* p, unsigned v) {
-    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 // Grid-wide barrier: the launch is cooperative, so cooperative_groups' grid
@@ -101,15 +74,12 @@ __device__ __forceinline__ void grid_reduce(double (&v)[NV], double* __restrict_
     }
     res_stamp(tr);                         // all warps of this CTA are done with the phase
     grid_barrier(bar, bar + 1);
-    if (wid == 0) {
+    if (wid < NV) {                        // warp k folds value k (fixed order)
+        double x = 0;
+        for (int b = lane; b < (int)gridDim.x; b += 32) x += __ldcg(&part[b * NV + wid]);
 #pragma unroll
-        for (int k = 0; k < NV; k++) {
-            double x = 0;
-            for (int b = lane; b < (int)gridDim.x; b += 32) x += __ldcg(&part[b * NV + k]);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
-            if (lane == 0) stot[k] = x;
-        }
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
+        if (lane == 0) stot[wid] = x;
     }
     __syncthreads();
 #pragma unroll
@@ -145,26 +115,20 @@ __device__ __forceinline__ void reduce_finish(unsigned tok, const double* __rest
                                               const cooperative_groups::grid_group& grid, double (&out)[NV]) {
     __shared__ double stot2[NV];
     grid.barrier_wait(std::move(tok));
-    if ((threadIdx.x >> 5) == 0) {
+    const int wid = threadIdx.x >> 5;
+    if (wid < NV) {                        // warp k folds value k (fixed order)
         const int lane = threadIdx.x & 31;
+        double x = 0;
+        for (int b = lane; b < (int)gridDim.x; b += 32) x += __ldcg(&part[b * NV + wid]);
 #pragma unroll
-        for (int k = 0; k < NV; k++) {
-            double x = 0;
-            for (int b = lane; b < (int)gridDim.x; b += 32) x += __ldcg(&part[b * NV + k]);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
-            if (lane == 0) stot2[k] = x;
-        }
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
+        if (lane == 0) stot2[wid] = x;
     }
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < NV; k++) out[k] = stot2[k];
 }
 
-// Per-column flags of the CTA's columns: bits 0-3 = in-plane neighbour exists
-// (i-1, i+1, j-1, j+1; Neumann, R3), bits 4-7 = that neighbour column is in
-// this CTA's shared memory (else read from the global copy of p).
-enum { NB_IM = 1, NB_IP = 2, NB_JM = 4, NB_JP = 8, LOC_SHIFT = 4 };
 
 // Resident-path preconditioner application: z = r * rcp.approx(M) (~1 ulp;
 // M > 0 is only the Jacobi preconditioner).
@@ -345,7 +309,6 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
             res_stamp(tr ? tr + 4 : nullptr);
             // ---- x += a p while the r.z / r.r partials gather (fire-and-forget L2
             // adds; x feeds no reduction)
-#if RES_XPOS == 0
             {
                 const int tid = opaque(threadIdx.x);
                 const unsigned mv = (unsigned)opaque((int)mval);
@@ -355,14 +318,13 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
                 for (int k = 0; k < K; k++)
                     if (mv & (1u << k)) red_add(xt + k * NT, a * s0[k * NT]);
             }
-#endif
             reduce_finish<2>(tok2, part2, grid, t3);
             res_stamp(tr ? tr + 5 : nullptr);
             k_it += 1;
             relres = sqrt(t3[1] / rr0);
             const double beta = t3[0] / rz;
             rz = t3[0];
-            const bool last = k_it >= sp.max_pcg || (!sp.fixed && relres < sp.pcg_rtol);
+            if (k_it >= sp.max_pcg || (!sp.fixed && relres < sp.pcg_rtol)) break;
             // ---- p = z + beta p on own columns and on the global halo copy
             const float be = (float)beta;
             {
@@ -370,20 +332,14 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
                 const unsigned mv = (unsigned)opaque((int)mval);
                 float* s0 = sp_ + tid;
                 float* gt = pgc + tid;
-                float* xt = xl + tid;
 #pragma unroll
                 for (int k = 0; k < K; k++) {
                     const int o = k * NT;
-                    const float pv = s0[o];
-                    if (RES_XPOS == 1 && (mv & (1u << k))) red_add(xt + o, a * pv);
-                    if (!last) {
-                        const float pn = fmaf(be, pv, hv[k]);
-                        s0[o] = pn;
-                        if (mv & (1u << k)) gt[o] = pn;
-                    }
+                    const float pn = fmaf(be, s0[o], hv[k]);
+                    s0[o] = pn;
+                    if (mv & (1u << k)) gt[o] = pn;
                 }
             }
-            if (last) break;
             res_stamp(tr ? tr + 6 : nullptr);
             tok3 = grid.barrier_arrive();
             pend3 = true;
