@@ -176,10 +176,12 @@ template <typename T>
 struct L {
     static T* b(hysco_ctx c, int k) { return static_cast<T*>(c->buf[k]) + c->plane_off; }
 
-    static void eval(hysco_ctx c, const SolveParams& sp, int mode, const T* bsrc) {
+    // bold / q given: a TRIAL evaluation forms the retry b itself (no ls_retry launch)
+    static void eval(hysco_ctx c, const SolveParams& sp, int mode, const T* bsrc, const T* bold = nullptr,
+                     const T* q = nullptr) {
         NCH_SWITCH(c->nch, eval_kernel<T, NCH><<<dim3(c->gx_eval, c->cfg.batch), 256, c->smem_eval, c->stream>>>(
-                               c->g, c->ctl, sp, mode, (const T*)c->Ip, (const T*)c->Im, bsrc, b(c, B_GRAD),
-                               b(c, B_DT), b(c, B_ET)));
+                               c->g, c->ctl, sp, mode, (const T*)c->Ip, (const T*)c->Im, bsrc, bold, q,
+                               b(c, B_GRAD), b(c, B_DT), b(c, B_ET)));
     }
     static void pcg_init(hysco_ctx c) {
         NCH_SWITCH(c->nch, pcg_init_kernel<T, NCH><<<dim3(c->gx_nodes, c->cfg.batch), 256, 0, c->stream>>>(
@@ -199,12 +201,7 @@ struct L {
         NCH_SWITCH(c->nch, trial_init_kernel<T, NCH><<<dim3(c->gx_nodes, c->cfg.batch), 256, 0, c->stream>>>(
                                c->g, c->ctl, b(c, B_GRAD), b(c, B_X), b(c, B_B), b(c, B_BOLD)));
     }
-    static void ls_body(hysco_ctx c, const SolveParams& sp) {
-        eval(c, sp, EVAL_TRIAL, b(c, B_B));
-        NCH_SWITCH(c->nch, ls_retry_kernel<T, NCH><<<dim3(c->gx_nodes, c->cfg.batch), 256, 0, c->stream>>>(
-                               c->g, c->ctl, b(c, B_X), b(c, B_BOLD), b(c, B_B)));
-    }
-    static void gn_tail(hysco_ctx c) { gn_tail_kernel<<<1, 32, 0, c->stream>>>(c->ctl, (int)c->cfg.batch); }
+    static void ls_body(hysco_ctx c, const SolveParams& sp) { eval(c, sp, EVAL_TRIAL, b(c, B_B), b(c, B_BOLD), b(c, B_X)); }
     static void matvec_plain(hysco_ctx c, const T* q, T* Hq) {
         NCH_SWITCH(c->nch, matvec_kernel<T, NCH, false><<<dim3(c->gx_mv, c->cfg.batch), 256, 0, c->stream>>>(
                                c->g, c->ctl, b(c, B_DT), b(c, B_ET), q, Hq));
@@ -709,8 +706,7 @@ static void gn_sequence(Runner& r, const SolveParams& sp) {
             r.loop(COND_PCG, [&] { r.seq([&] { L<T>::pcg_iter(c, sp); }); });
         }
         r.seq([&] { L<T>::trial_init(c); });
-        r.loop(COND_LS, [&] { r.seq([&] { L<T>::ls_body(c, sp); }); });
-        r.seq([&] { L<T>::gn_tail(c); });
+        r.loop(COND_LS, [&] { r.seq([&] { L<T>::ls_body(c, sp); }); });   // its last eval sets COND_GN
     });
 }
 

@@ -217,10 +217,43 @@ __device__ __forceinline__ void stage_col(const T* __restrict__ src, T* dst, int
     }
 }
 
+// Armijo retry staging: b_t = b_old + gamma q (written back to b for the own
+// columns); a plain b column otherwise.  Branch-free within a column so every
+// load of the column stays in flight.
+template <typename T, int NCH>
+__device__ __forceinline__ void stage_bq(const T* __restrict__ src, const T* __restrict__ q, T gm, T* dst,
+                                         T* __restrict__ gout, int len, int lane) {
+    T v[NCH], w[NCH];
+#pragma unroll
+    for (int m = 0; m < NCH; m++) {
+        const int l = 32 * m + lane;
+        v[m] = l < len ? src[l] : T(0);
+        w[m] = l < len ? q[l] : T(0);
+    }
+#pragma unroll
+    for (int m = 0; m < NCH; m++) {
+        const int l = 32 * m + lane;
+        const T t = fma(gm, w[m], v[m]);
+        if (l < len) dst[l] = t;
+        if (gout && l < len) gout[l] = t;
+    }
+}
+template <typename T, int NCH>
+__device__ __forceinline__ void stage_b(const T* __restrict__ src, const T* __restrict__ q, T gm, T* dst,
+                                        T* __restrict__ gout, int len, int lane) {
+    if (q) stage_bq<T, NCH>(src, q, gm, dst, gout, len, lane);   // uniform branch
+    else stage_col<T, NCH>(src, dst, len, lane);
+}
+
+// bb: the b to evaluate.  EVAL_TRIAL with bold / q given (single-GPU path):
+// after a rejected trial (ls_tries > 0) or for the restore pass, the trial b
+// = b_old + gamma q (gamma = 0 to restore, R15) is formed while staging and
+// written to bb, which replaces the separate retry kernel.
 template <typename T, int NCH>
 __global__ void __launch_bounds__(256, 4) eval_kernel(Geom g, Ctl c, SolveParams sp, int mode,
                                                    const T* __restrict__ Ip, const T* __restrict__ Im,
-                                                   const T* __restrict__ bb, T* __restrict__ grad,
+                                                   const T* bb, const T* __restrict__ bold,
+                                                   const T* __restrict__ q, T* __restrict__ grad,
                                                    T* __restrict__ dt, T* __restrict__ et) {
     count_launch(c);
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -243,11 +276,21 @@ __global__ void __launch_bounds__(256, 4) eval_kernel(Geom g, Ctl c, SolveParams
 
     bool active = true;
     if (mode == EVAL_TRIAL) active = c.st[pair].ls_active != 0;
+    const T* bsrc = bb;
+    const T* qp = nullptr;
+    T* bdst = nullptr;
+    T gm = T(0);
+    if (mode == EVAL_TRIAL && q && (c.st[pair].ls_tries > 0 || c.st[pair].ls_restore)) {
+        bsrc = bold;
+        qp = q + (size_t)pair * g.ps;
+        bdst = const_cast<T*>(bb) + (size_t)pair * g.ps;
+        gm = c.st[pair].ls_restore ? T(0) : (T)c.st[pair].gamma;
+    }
 
     const T hd = (T)g.hd, ahd = (T)g.ahd, bh2 = (T)g.bh2;
     const T ih3 = (T)g.ih3, ih3sq = (T)g.ih3sq, ih1sq = (T)g.ih1sq, ih2sq = (T)g.ih2sq;
     const long long sI = (long long)n2 * P;   // node stride along dim 1
-    const T* bp = bb + (size_t)pair * g.ps;
+    const T* bp = bsrc + (size_t)pair * g.ps;
     const T* ipp = Ip + (size_t)pair * g.Nc;
     const T* imp = Im + (size_t)pair * g.Nc;
 
@@ -260,14 +303,18 @@ __global__ void __launch_bounds__(256, 4) eval_kernel(Geom g, Ctl c, SolveParams
             const bool him = valid && has_im(g, i), hip = valid && has_ip(g, i), hjm = j > 0, hjp = j < n2 - 1;
             if (valid) {
                 const T* bc = bp + col * P;
-                stage_col<T, NCH>(bc, sb + (wid + 1) * P, P, lane);
-                if (him) stage_col<T, NCH>(bc - sI, sbim + wid * P, P, lane);
-                if (hip) stage_col<T, NCH>(bc + sI, sbip + wid * P, P, lane);
+                const T* qc = qp ? qp + col * P : nullptr;
+                stage_b<T, NCH>(bc, qc, gm, sb + (wid + 1) * P, bdst ? bdst + col * P : nullptr, P, lane);
+                if (him) stage_b<T, NCH>(bc - sI, qc ? qc - sI : nullptr, gm, sbim + wid * P, nullptr, P, lane);
+                if (hip) stage_b<T, NCH>(bc + sI, qc ? qc + sI : nullptr, gm, sbip + wid * P, nullptr, P, lane);
                 stage_col<T, NCH>(ipp + col * n3, sIp, n3, lane);
                 stage_col<T, NCH>(imp + col * n3, sIm, n3, lane);
             }
-            if (wid == 0 && c0 > 0) stage_col<T, NCH>(bp + (c0 - 1) * P, sb, P, lane);
-            if (wid == EV_CT - 1 && c0 + EV_CT < g.ncol) stage_col<T, NCH>(bp + (c0 + EV_CT) * P, sb + (EV_CT + 1) * P, P, lane);
+            if (wid == 0 && c0 > 0)
+                stage_b<T, NCH>(bp + (c0 - 1) * P, qp ? qp + (c0 - 1) * P : nullptr, gm, sb, nullptr, P, lane);
+            if (wid == EV_CT - 1 && c0 + EV_CT < g.ncol)
+                stage_b<T, NCH>(bp + (c0 + EV_CT) * P, qp ? qp + (c0 + EV_CT) * P : nullptr, gm, sb + (EV_CT + 1) * P,
+                                nullptr, P, lane);
             __syncthreads();
             if (valid) {
                 T* gc = grad + (size_t)pair * g.ps + col * P;
@@ -366,8 +413,12 @@ __global__ void __launch_bounds__(256, 4) eval_kernel(Geom g, Ctl c, SolveParams
     decide_eval(g, c, sp, mode, c.st[pair], tot);
     if (mode == EVAL_GN_START && last_pair(c))
         set_cond(c, COND_GN, any_pair(c, gridDim.y, [](volatile PairState* q) { return q->gn_active != 0; }));
-    if (mode == EVAL_TRIAL && last_pair(c))
+    if (mode == EVAL_TRIAL && last_pair(c)) {
         set_cond(c, COND_LS, any_pair(c, gridDim.y, [](volatile PairState* q) { return q->ls_active != 0; }));
+        // the GN step ends with the search; its loop condition is final once no
+        // pair searches (ls_retry only moves b), so no separate tail kernel
+        set_cond(c, COND_GN, any_pair(c, gridDim.y, [](volatile PairState* q) { return q->gn_active != 0; }));
+    }
 }
 
 // ---------------------------------------------------------------------------

@@ -185,10 +185,11 @@ def test_correct_pipeline_parity(pair, dtype):
     assert rel(c.np(b)[0], bref) <= tol
     assert rel(c.np(Tp)[0], Tpr) <= tol and rel(c.np(Tm)[0], Tmr) <= tol
     n = H.hysco_last_launch_count(c.ctx)
-    # 7 OT kernels + 1 eval + 10 x (PCG + trial_init + eval + retry + tail) + apply, where PCG is
-    # pcg_init + 10 x (matvec, update, dir) streaming, or 1 launch when the resident PCG applies
+    # 7 OT kernels + 1 eval + 10 x (PCG + trial_init + eval) + apply and one more eval per
+    # Armijo halving, where PCG is pcg_init + 10 x (matvec, update, dir) streaming, or 1
+    # launch when the resident PCG applies
     pcg = 31 if n > 200 else 1
-    assert n == 7 + 1 + 10 * (pcg + 1 + 2 + 1) + 1 + 2 * reps[0]["ls_halvings"]
+    assert n == 7 + 1 + 10 * (pcg + 1 + 1) + 1 + reps[0]["ls_halvings"]
     c.close()
 
 

@@ -48,7 +48,8 @@ int main(int argc, char** argv) {
     unsigned* bar; cudaMalloc(&bar, 8); cudaMemset(bar, 0, 8);
     unsigned long long* trace; cudaMalloc(&trace, sizeof(unsigned long long) * G * 16 * 8);
     cudaMemset(trace, 0, sizeof(unsigned long long) * G * 16 * 8);
-    Ctl c{}; c.st = st; c.launches = launches;
+    unsigned* dcond; cudaMalloc(&dcond, 4 * NCOND);
+    Ctl c{}; c.st = st; c.launches = launches; c.dcond = dcond; c.use_graph = 0;
     SolveParams sp{}; sp.max_pcg = 10; sp.fixed = 1;
     const size_t smem = (size_t)(3 * knt + 2 * g.P + 8) * sizeof(float);
     cudaFuncSetAttribute(pcg_resident_kernel<24, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
