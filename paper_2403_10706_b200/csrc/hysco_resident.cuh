@@ -165,6 +165,8 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
                         unsigned long long* trace = nullptr) {
     count_launch(c);
     if (!c.st[pair].gn_active) return;       // uniform over the grid
+    unsigned long long* trk = trace ? trace + ((size_t)blockIdx.x * 16 + 15) * 8 : nullptr;   // launch-level stamps
+    res_stamp(trk);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int NT = blockDim.x;
     const int KNT = K * NT;
@@ -191,8 +193,10 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
     float* __restrict__ xl = x + n0;
     double* part2 = gpart;                 // [G][2] for r.z, r.r
     double* part1 = gpart + 2 * gridDim.x; // [G][1] for p.Hp
-    FastDiv fdP;
+    FastDiv fdP, fdN2;
     fdP.init((unsigned)P);
+    fdN2.init((unsigned)n2);
+    bool xset = false;                     // x holds alpha_0 p_0 + ... (else still to be zeroed)
 
     if (threadIdx.x == 0) {
         sp_[-P - 1] = 0.f;
@@ -208,8 +212,8 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
         const int n = threadIdx.x + k * NT;
         float rv = 0.f, M = 1.f, e = 0.f;
         if (n < Nb) {
-            const long long col = c0 + fdP.div(n);
-            const int i = (int)(col / n2), j = (int)(col - (long long)i * n2);
+            const int col = (int)c0 + fdP.div(n);
+            const int i = fdN2.div(col), j = col - i * n2;
             M = dt[n0 + n] + (float)(g.ahd * diag_lxy(g, i, j));
             e = et[n0 + n];
             rv = -grad[n0 + n];
@@ -223,15 +227,14 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
         sp_[n] = z;
         r[k] = rv;
         hv[k] = 0.f;
-        if (n < Nb) {
-            pgc[n] = z;
-            xl[n] = 0.f;
-        }
+        if (n < Nb) pgc[n] = z;               // x = 0 is written by the first update (or below)
         frz = fmaf(rv, z, frz);
         frr = fmaf(rv, rv, frr);
     }
     double v2[2] = {(double)frz, (double)frr}, t2[2];
+    res_stamp(trk ? trk + 1 : nullptr);
     grid_reduce<2>(v2, part2, bar, t2);       // also publishes p0 to the neighbours
+    res_stamp(trk ? trk + 2 : nullptr);
     double rz = t2[0];
     const double rr0 = t2[1];
     double relres = rr0 > 0 ? 1.0 : 0.0;
@@ -314,10 +317,17 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
                 const unsigned mv = (unsigned)opaque((int)mval);
                 float* xt = xl + tid;
                 const float* s0 = sp_ + tid;
+                if (xset) {
 #pragma unroll
-                for (int k = 0; k < K; k++)
-                    if (mv & (1u << k)) red_add(xt + k * NT, a * s0[k * NT]);
+                    for (int k = 0; k < K; k++)
+                        if (mv & (1u << k)) red_add(xt + k * NT, a * s0[k * NT]);
+                } else {                      // first update: x_1 = 0 + a p_0 (plain stores)
+#pragma unroll
+                    for (int k = 0; k < K; k++)
+                        if (mv & (1u << k)) xt[k * NT] = 0.f + a * s0[k * NT];
+                }
             }
+            xset = true;
             reduce_finish<2>(tok2, part2, grid, t3);
             res_stamp(tr ? tr + 5 : nullptr);
             k_it += 1;
@@ -345,6 +355,9 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
             pend3 = true;
         }
     }
+    if (!xset)                                // no update happened (r0 = 0 or breakdown): x = 0
+        for (int n = threadIdx.x; n < Nb; n += NT) xl[n] = 0.f;
+    res_stamp(trk ? trk + 3 : nullptr);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         PairState& s = c.st[pair];
         s.rz = rz;

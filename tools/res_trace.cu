@@ -94,6 +94,16 @@ int main(int argc, char** argv) {
         printf("%-22s -> %-22s span %7.2f us | per-CTA mean %7.2f max %7.2f min %7.2f us\n", names[k], names[k == 6 ? 8 : k + 1],
                span / nit / 1e3, mean_cta / nit / 1e3, max_cta / nit / 1e3, min_cta / 1e3);
     }
+    {   // launch-level stamps (slot 15): start, init loads done, init reduce done, loop done
+        double a = 0, b2 = 0, c2 = 0, mx = 0;
+        for (int b = 0; b < G; b++) {
+            const unsigned long long* t = &ht[((size_t)b * 16 + 15) * 8];
+            a += (double)(t[1] - t[0]); b2 += (double)(t[2] - t[1]); c2 += (double)(t[3] - t[2]);
+            mx = std::max(mx, (double)(t[3] - t[0]));
+        }
+        printf("init loads %.2f us, init reduce %.2f us, loop %.2f us (per-CTA means), start->loop end max %.2f us\n",
+               a / G / 1e3, b2 / G / 1e3, c2 / G / 1e3, mx / 1e3);
+    }
     // iteration period
     double per = 0;
     for (int it = 1; it < 9; it++) per += (double)(ht[(size_t)it * 8 + 0] - ht[(size_t)(it - 1) * 8 + 0]);
