@@ -73,11 +73,13 @@ struct hysco_ctx_s {
     void* flush = nullptr;    // profiling-only L2 flush scratch
     // on-chip-resident PCG (hysco_resident.cuh): fp32, one CTA per SM
     bool resident = false;
-    int res_k = 0, res_nbmax = 0, res_grid = 0;
+    int res_k = 0, res_grid = 0;
     size_t res_smem = 0;
     double* res_part = nullptr;
-    unsigned* res_bar = nullptr;
+    unsigned* res_flags = nullptr;   // [G] p-halo flags + [1] launch counter (hysco_resident.cuh)
     float* res_pg = nullptr;     // ghost-padded global copy of p (halo source)
+    float* res_x = nullptr;      // x of one pair in the padded resident layout
+    float res_wi = 0.f, res_wj = 0.f;   // alpha hd / h1^2, alpha hd / h2^2 (in-plane Laplacian weights)
     // slab decomposition (multi-rank)
     size_t plane_off = 0;        // elements from a pair's buffer start to local plane 0
     int rank = 0, nranks = 1;
@@ -308,10 +310,7 @@ struct Runner {
     switch (k) {                                                               \
         case 4: { constexpr int RK = 4; __VA_ARGS__; } break;                  \
         case 8: { constexpr int RK = 8; __VA_ARGS__; } break;                  \
-        case 12: { constexpr int RK = 12; __VA_ARGS__; } break;                \
-        case 16: { constexpr int RK = 16; __VA_ARGS__; } break;                \
-        case 20: { constexpr int RK = 20; __VA_ARGS__; } break;                \
-        default: { constexpr int RK = 24; __VA_ARGS__; } break;                \
+        default: { constexpr int RK = 12; __VA_ARGS__; } break;                \
     }
 
 static void launch_resident(hysco_ctx c, const SolveParams& sp, int pair) {
@@ -329,13 +328,15 @@ static void launch_resident(hysco_ctx c, const SolveParams& sp, int pair) {
     if (sp.fixed) {
         RES_K_SWITCH(c->res_k, cudaLaunchKernelEx(&cfg, pcg_resident_kernel<RK, true>, c->g, c->ctl, sp, pair,
                                                   (const float*)B[B_GRAD], (const float*)B[B_DT],
-                                                  (const float*)B[B_ET], B[B_X], c->res_pg, c->res_part,
-                                                  c->res_bar, c->res_nbmax, (unsigned long long*)nullptr));
+                                                  (const float*)B[B_ET], B[B_X], c->res_x, c->res_pg,
+                                                  c->res_part, c->res_flags, c->res_wi, c->res_wj,
+                                                  (unsigned long long*)nullptr));
     } else {
         RES_K_SWITCH(c->res_k, cudaLaunchKernelEx(&cfg, pcg_resident_kernel<RK, false>, c->g, c->ctl, sp, pair,
                                                   (const float*)B[B_GRAD], (const float*)B[B_DT],
-                                                  (const float*)B[B_ET], B[B_X], c->res_pg, c->res_part,
-                                                  c->res_bar, c->res_nbmax, (unsigned long long*)nullptr));
+                                                  (const float*)B[B_ET], B[B_X], c->res_x, c->res_pg,
+                                                  c->res_part, c->res_flags, c->res_wi, c->res_wj,
+                                                  (unsigned long long*)nullptr));
     }
 }
 
@@ -348,12 +349,11 @@ static void setup_resident(hysco_ctx ctx) {
     const int G = ctx->nsm;
     if (g.ncol < G) return;
     const long long ncl_max = (g.ncol + G - 1) / G;
-    const long long nbmax = ncl_max * g.P;
-    const long long need_k = (nbmax + RES_THREADS - 1) / RES_THREADS;
-    if (need_k > 24) return;
-    int k = need_k <= 4 ? 4 : need_k <= 8 ? 8 : need_k <= 12 ? 12 : need_k <= 16 ? 16 : need_k <= 20 ? 20 : 24;
-    const long long knt = (long long)k * RES_THREADS;   // slots per CTA incl. padding
-    const size_t smem = (size_t)(3 * knt + 2 * g.P + 8) * sizeof(float);   // layout: hysco_resident.cuh
+    const long long nqmax = ncl_max * (res_pad(g.P) / 2);   // node pairs per CTA
+    const long long need_k = (nqmax + RES_THREADS - 1) / RES_THREADS;
+    if (need_k > 12) return;
+    const int k = need_k <= 4 ? 4 : need_k <= 8 ? 8 : 12;
+    const size_t smem = res_smem_bytes(k);   // layout: hysco_resident.cuh
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->cfg.device);
     cudaFuncAttributes fa{};
@@ -378,17 +378,22 @@ static void setup_resident(hysco_ctx ctx) {
         cudaGetLastError();
         return;
     }
-    const size_t ghost = res_ghost_pair_floats(g) * ctx->cfg.batch * sizeof(float);
+    const size_t ghost = (res_ghost_pair_floats(g) * ctx->cfg.batch + res_ghost_slack_floats(k)) * sizeof(float);
     if (cudaMalloc(&ctx->res_part, sizeof(double) * 8 * G) != cudaSuccess ||
-        cudaMalloc(&ctx->res_bar, sizeof(unsigned) * 2) != cudaSuccess ||
-        cudaMalloc(&ctx->res_pg, ghost) != cudaSuccess) {
+        cudaMalloc(&ctx->res_flags, sizeof(unsigned) * (G + 1)) != cudaSuccess ||
+        cudaMalloc(&ctx->res_pg, ghost) != cudaSuccess ||
+        cudaMalloc(&ctx->res_x, (size_t)g.ncol * res_pad(g.P) * sizeof(float)) != cudaSuccess) {
         cudaGetLastError();
         return;
     }
-    cudaMemset(ctx->res_bar, 0, sizeof(unsigned) * 2);
+    cudaMemset(ctx->res_part, 0, sizeof(double) * 8 * G);
+    cudaMemset(ctx->res_flags, 0, sizeof(unsigned) * G);
+    const unsigned first_launch = 1;      // tags of launch 0 would match the zeroed slots
+    cudaMemcpy(ctx->res_flags + G, &first_launch, sizeof(unsigned), cudaMemcpyHostToDevice);
     cudaMemset(ctx->res_pg, 0, ghost);   // ghost planes stay zero forever
     ctx->res_k = k;
-    ctx->res_nbmax = (int)nbmax;
+    ctx->res_wi = (float)(g.ahd * g.ih1sq);
+    ctx->res_wj = (float)(g.ahd * g.ih2sq);
     ctx->res_grid = G;
     ctx->res_smem = smem;
     ctx->resident = true;
@@ -1432,8 +1437,9 @@ hysco_status hysco_destroy(hysco_ctx ctx) {
         if (p) cudaFree(p);
     if (ctx->flush) cudaFree(ctx->flush);
     if (ctx->res_part) cudaFree(ctx->res_part);
-    if (ctx->res_bar) cudaFree(ctx->res_bar);
+    if (ctx->res_flags) cudaFree(ctx->res_flags);
     if (ctx->res_pg) cudaFree(ctx->res_pg);
+    if (ctx->res_x) cudaFree(ctx->res_x);
     if (ctx->red) cudaFree(ctx->red);
     if (ctx->comm) {
         if (LoopbackComm* lb = dynamic_cast<LoopbackComm*>(ctx->comm)) {

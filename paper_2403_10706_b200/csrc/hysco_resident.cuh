@@ -3,24 +3,29 @@
 //
 // Why: a PCG iteration of the streaming kernels moves ~60 B/node through HBM
 // and needs three launches.  For a volume whose PCG state fits the chip
-// (HCP 3T: 2.70 M nodes; per SM 127 columns x 145 nodes), each CTA keeps its
-// contiguous range of PE columns resident for all iterations:
-//   shared memory : p (read by neighbouring threads), dt, et   (12 B/node)
-//   registers     : r and Hp, K slots per thread               ( 8 B/node)
-//   global / L2   : x (read-modify-write, owner only) and a copy of p that
-//                   neighbouring CTAs read for the in-plane Laplacian halo.
-// One CTA per SM (cooperative launch guarantees co-residency); the three
-// reductions of an iteration (p.Hp, r.z, r.r) use a grid barrier and a
-// deterministic fixed-order sum of per-CTA partials that every CTA performs
-// identically, so all CTAs take the same alpha/beta/stop decisions.
-// Arithmetic per node is the streaming kernels' (same formulas and order).
+// (HCP 3T: 2.70 M nodes; per SM 126 columns x 146 padded nodes), each CTA
+// keeps its contiguous range of PE columns resident for all iterations:
+//   shared memory : p (read by neighbouring threads), M = diag(H), et  (12 B/node)
+//   registers     : r and Hp / z, K float2 pairs per thread              ( 8 B/node)
+//   global / L2   : x (L2 adds, owner only, padded layout) and a copy of p
+//                   that neighbouring CTAs read for the in-plane halo.
+// A thread owns pairs of consecutive nodes of one column (columns padded to
+// an even length), so every access is 64-bit and every per-slot offset is a
+// compile-time immediate (NT is a constant).
+// One CTA per SM (cooperative launch guarantees co-residency).  Per iteration:
+//   local Hp part (PE tridiagonal + in-CTA j-neighbours)
+//   wait for the neighbour CTAs' p flags; remote Hp part (i-neighbours and
+//     CTA-boundary j-neighbours from L2); p.Hp -> all-reduce
+//   r, z = r/M, r.z, r.r -> publish;  x += a p (L2 adds);  collect
+//   p = z + beta p (shared + global copy) -> release this CTA's p flag
+// Reductions: deterministic fixed-order fold of per-CTA partials performed
+// identically by every CTA, so all CTAs take the same alpha/beta/stop decisions.
 #pragma once
 
-#include <cooperative_groups.h>
 
 namespace hysco {
 
-constexpr int RES_THREADS = 768;
+constexpr int RES_THREADS = 768;   // 24 warps (6 per SM sub-partition): 80 registers per thread
 
 // Opaque copy: stops ptxas from hoisting per-slot index math (and everything
 // derived from it) out of the PCG iteration loop, which would keep ~15
@@ -30,19 +35,50 @@ __device__ __forceinline__ int opaque(int v) {
     asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
     return r;
 }
-// x += v at L2 with no return value: the owner is the only writer of x, so
-// the sum is the plain fp32 x + fl(a p) and no load latency is exposed.
-__device__ __forceinline__ void red_add(float* p, float v) {
-    asm volatile("red.relaxed.gpu.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+// ---------------------------------------------------------------------------
+// Synchronisation without grid barriers.  The launch is cooperative (all CTAs
+// co-resident), but no cooperative_groups grid sync is used:
+//  * all-reduce: every CTA publishes its fp64 partial with ONE 64-bit store
+//    whose low 8 mantissa bits carry a tag (launch, iteration); readers poll
+//    the slots until every tag matches and fold them in a fixed order.  The
+//    data is its own flag, so an all-reduce costs one publish and one poll
+//    round trip through L2 instead of arrive-atomic + poll + fold.  The tag
+//    perturbs a partial by <= 2^-44 relative; every CTA folds the same tagged
+//    values, so all CTAs still take identical alpha / beta / stop decisions.
+//  * p halo: a CTA releases a per-CTA flag after storing its new p; a reader
+//    acquires only the flags of the CTAs that own its i- / j-neighbour
+//    columns (a neighbourhood wait, not a grid barrier).
+// Slots are reused every iteration without a hazard: a CTA rewrites a slot of
+// reduction R for iteration k+1 only after the next all-reduce of iteration k
+// has completed, which every CTA enters after reading R(k).  A stale slot
+// holds the previous iteration's or the previous launch's tag (the launch
+// counter advances once per launch), never the awaited one.  Polls are
+// bounded: a stall of ~2^26 polls traps (a kernel error, not a hang).
+// ---------------------------------------------------------------------------
+constexpr unsigned RES_SPIN_LIMIT = 1u << 26;
+
+__device__ __forceinline__ unsigned res_tag(unsigned launch, int seq) { return ((launch & 7u) << 5) | ((unsigned)seq & 31u); }
+__device__ __forceinline__ double tag_value(double v, unsigned tag) {
+    return __longlong_as_double((__double_as_longlong(v) & ~0xffll) | (long long)tag);
+}
+__device__ __forceinline__ unsigned value_tag(double v) { return (unsigned)(__double_as_longlong(v) & 0xff); }
+__device__ __forceinline__ double ld_relaxed_f64(const double* p) {
+    double v;
+    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_f64(double* p, double v) {
+    asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Grid-wide barrier: the launch is cooperative, so cooperative_groups' grid
-// sync applies (measured 1.2 us per barrier on B200 with 148 CTAs vs 2.0 us for
-// a hand-written counter/generation barrier; tools/barrier_bench.cu).
-__device__ __forceinline__ void grid_barrier(unsigned*, unsigned*) { cooperative_groups::this_grid().sync(); }
-
-// Block-reduce NV doubles, publish per-CTA partials, barrier, and fold all
-// partials in fixed order (identically in every CTA).  Result in out[] (all threads).
 // Optional phase trace (tools/res_trace.cu): thread 0 of every CTA stamps the
 // global timer at phase boundaries of the first 16 iterations.
 __device__ __forceinline__ void res_stamp(unsigned long long* tr) {
@@ -53,11 +89,10 @@ __device__ __forceinline__ void res_stamp(unsigned long long* tr) {
     }
 }
 
+// Publish this CTA's NV partials (block-reduced in fixed order) with tag.
 template <int NV>
-__device__ __forceinline__ void grid_reduce(double (&v)[NV], double* __restrict__ part, unsigned* bar, double (&out)[NV],
-                                            unsigned long long* tr = nullptr) {
+__device__ __forceinline__ void reduce_publish(double (&v)[NV], double* __restrict__ part, unsigned tag) {
     __shared__ double sred[NV][32];
-    __shared__ double stot[NV];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
     for (int k = 0; k < NV; k++) {
@@ -70,13 +105,43 @@ __device__ __forceinline__ void grid_reduce(double (&v)[NV], double* __restrict_
     if (threadIdx.x < NV) {
         double x = 0;
         for (int w = 0; w < nw; w++) x += sred[threadIdx.x][w];
-        part[blockIdx.x * NV + threadIdx.x] = x;
+        st_relaxed_f64(part + blockIdx.x * NV + threadIdx.x, tag_value(x, tag));
     }
-    res_stamp(tr);                         // all warps of this CTA are done with the phase
-    grid_barrier(bar, bar + 1);
-    if (wid < NV) {                        // warp k folds value k (fixed order)
-        double x = 0;
-        for (int b = lane; b < (int)gridDim.x; b += 32) x += __ldcg(&part[b * NV + wid]);
+}
+
+// Wait for every CTA's tagged partials and fold them in fixed order (warp k
+// folds value k, identically in every CTA).  Result in out[] (all threads).
+template <int NV>
+__device__ __forceinline__ void reduce_collect(const double* __restrict__ part, unsigned tag, double (&out)[NV]) {
+    constexpr int MS = 8;                    // slots per lane: up to 256 CTAs
+    __shared__ double stot[NV];
+    const int wid = threadIdx.x >> 5;
+    if (wid < NV) {
+        const int lane = threadIdx.x & 31, G = gridDim.x;
+        double v[MS];
+        unsigned pending = 0;
+#pragma unroll
+        for (int m = 0; m < MS; m++) {
+            const int b = lane + 32 * m;
+            v[m] = 0.0;
+            if (b < G) {
+                v[m] = ld_relaxed_f64(part + b * NV + wid);
+                if (value_tag(v[m]) != tag) pending |= 1u << m;
+            }
+        }
+        unsigned spins = 0;
+        while (__any_sync(FULL, pending != 0)) {
+            if (++spins > RES_SPIN_LIMIT) __trap();
+#pragma unroll
+            for (int m = 0; m < MS; m++)
+                if (pending & (1u << m)) {
+                    v[m] = ld_relaxed_f64(part + (lane + 32 * m) * NV + wid);
+                    if (value_tag(v[m]) == tag) pending &= ~(1u << m);
+                }
+        }
+        double x = 0.0;
+#pragma unroll
+        for (int m = 0; m < MS; m++) x += v[m];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
         if (lane == 0) stot[wid] = x;
@@ -86,49 +151,31 @@ __device__ __forceinline__ void grid_reduce(double (&v)[NV], double* __restrict_
     for (int k = 0; k < NV; k++) out[k] = stot[k];
 }
 
-// Split form of grid_reduce: publish this CTA's partials and arrive (returns
-// the arrival token), do independent work, then reduce_finish waits and folds
-// all partials in the same fixed order.
-template <int NV>
-__device__ __forceinline__ unsigned reduce_arrive(double (&v)[NV], double* __restrict__ part,
-                                                  const cooperative_groups::grid_group& grid) {
-    __shared__ double sred2[NV][32];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
-    for (int k = 0; k < NV; k++) {
-        double x = v[k];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
-        if (lane == 0) sred2[k][wid] = x;
+// After this CTA's p stores: release its flag (all threads' stores ordered by
+// the CTA barrier, then a gpu-scope release by thread 0).
+__device__ __forceinline__ void halo_release(unsigned* flags, unsigned tag) {
+    __syncthreads();
+    if (threadIdx.x == 0) st_release_u32(flags + blockIdx.x, tag);
+}
+// Before reading neighbours' p: acquire the flags of CTAs [blo, bhi].
+__device__ __forceinline__ void halo_acquire(const unsigned* flags, int blo, int bhi, unsigned tag) {
+    if (threadIdx.x < 32) {
+        for (int b = blo + (int)threadIdx.x; b <= bhi; b += 32) {
+            unsigned spins = 0;
+            while (ld_acquire_u32(flags + b) != tag)
+                if (++spins > RES_SPIN_LIMIT) __trap();
+        }
     }
     __syncthreads();
-    if (threadIdx.x < NV) {
-        double x = 0;
-        for (int w = 0; w < nw; w++) x += sred2[threadIdx.x][w];
-        part[blockIdx.x * NV + threadIdx.x] = x;
-    }
-    return grid.barrier_arrive();
 }
 
-template <int NV>
-__device__ __forceinline__ void reduce_finish(unsigned tok, const double* __restrict__ part,
-                                              const cooperative_groups::grid_group& grid, double (&out)[NV]) {
-    __shared__ double stot2[NV];
-    grid.barrier_wait(std::move(tok));
-    const int wid = threadIdx.x >> 5;
-    if (wid < NV) {                        // warp k folds value k (fixed order)
-        const int lane = threadIdx.x & 31;
-        double x = 0;
-        for (int b = lane; b < (int)gridDim.x; b += 32) x += __ldcg(&part[b * NV + wid]);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
-        if (lane == 0) stot2[wid] = x;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < NV; k++) out[k] = stot2[k];
+// CTA owning column col when ncol columns are split as [b ncol / G, (b+1) ncol / G).
+__device__ __forceinline__ int res_owner(long long col, long long ncol, int G) {
+    int b = (int)((col * G) / ncol);
+    while (b > 0 && (long long)b * ncol / G > col) b--;
+    while (b < G - 1 && (long long)(b + 1) * ncol / G <= col) b++;
+    return b;
 }
-
 
 // Resident-path preconditioner application: z = r * rcp.approx(M) (~1 ulp;
 // M > 0 is only the Jacobi preconditioner).
@@ -138,7 +185,13 @@ __device__ __forceinline__ float precond(float r, float M) {
     return r * inv;
 }
 
-// q = n / d for 0 <= n < 2^31 with a precomputed multiplier (no IDIV in the loop).
+// x += v (2 consecutive floats) at L2, no return value (the owner is the only
+// writer of its x nodes).
+__device__ __forceinline__ void red_add2(float* p, float2 v) {
+    asm volatile("red.relaxed.gpu.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
+}
+
+// q = n / d for 0 <= n < 2^31 with a precomputed multiplier (no IDIV).
 struct FastDiv {
     unsigned m, s;
     __device__ __forceinline__ void init(unsigned d) {
@@ -151,221 +204,312 @@ struct FastDiv {
     __device__ __forceinline__ int div(int n) const { return (int)(__umulhi((unsigned)n, m) >> s); }
 };
 
-// Global copy of p used for the in-plane halo: per pair (n1 + 2) x n2 x P
+// The resident path stores every PE column with Pp = P rounded up to an even
+// node count (zero padding), so a thread handles a pair of consecutive nodes
+// of one column with 64-bit shared / global accesses, and in-plane
+// neighbours (+-Pp, +-n2 Pp) stay 8-byte aligned.  (Groups of 4 would need
+// 3 % more padding at P = 145 and 8 more registers per slot, which does not
+// fit the 80-register budget of 24 warps.)
+__host__ __device__ inline int res_pad(int P) { return (P + 1) & ~1; }
+
+// Global copy of p used for the in-plane halo: per pair (n1 + 2) x n2 x Pp
 // floats with zero ghost planes at i = -1 and i = n1, so an i-neighbour read
 // needs no existence test (a missing Neumann neighbour contributes 0 to the
 // off-diagonal sum; its diagonal share is already excluded from M).
-__host__ __device__ inline size_t res_ghost_pair_floats(const Geom& g) { return (size_t)(g.n1 + 2) * g.n2 * g.P; }
+__host__ __device__ inline size_t res_ghost_pair_floats(const Geom& g) {
+    return (size_t)(g.n1 + 2) * g.n2 * res_pad(g.P);
+}
+// Dynamic shared memory of one CTA: p, M, et with K x NT node pairs each (the
+// slots past the CTA's ncl Pp nodes are zero-padding, so no slot loop needs a
+// branch) and three 2-float zero guards.
+__host__ __device__ inline size_t res_smem_bytes(int K) {
+    return (size_t)(3 * 2 * K * RES_THREADS + 6) * sizeof(float);
+}
+// Slack (floats) after the last pair's ghost copy: the i+1 reads of padding
+// slots of the last CTA stay inside the allocation (their values are unused).
+__host__ __device__ inline size_t res_ghost_slack_floats(int K) { return (size_t)2 * K * RES_THREADS; }
 
-template <int K, bool FIXED>
+// slot-mask fields (bit f + k for slot k < 12): pair valid, j-1 neighbour in
+// this CTA, j+1 in this CTA, j-1 neighbour in the previous CTA, j+1 in the next
+enum { RM_VAL = 0, RM_JML = 12, RM_JPL = 24, RM_JMR = 36, RM_JPR = 48 };
+__device__ __forceinline__ bool mbit(unsigned long long m, int b) { return (m >> b) & 1ull; }
+__device__ __forceinline__ unsigned long long opaque64(unsigned long long v) {
+    unsigned long long r;
+    asm volatile("mov.b64 %0, %1;" : "=l"(r) : "l"(v));
+    return r;
+}
+
+// TRACE: phase stamps for tools/res_trace.cu (compiled out of the library's kernel).
+template <int K, bool FIXED, bool TRACE = false>
 __global__ void __launch_bounds__(RES_THREADS, 1)
     pcg_resident_kernel(Geom g, Ctl c, SolveParams sp, int pair, const float* __restrict__ grad,
                         const float* __restrict__ dt, const float* __restrict__ et, float* __restrict__ x,
-                        float* __restrict__ pgh, double* __restrict__ gpart, unsigned* bar, int nbmax,
-                        unsigned long long* trace = nullptr) {
+                        float* __restrict__ xpad, float* __restrict__ pgh, double* __restrict__ gpart,
+                        unsigned* __restrict__ flags, float wi, float wj, unsigned long long* trace = nullptr) {
+    constexpr int NT = RES_THREADS;
+    static_assert(K <= 12, "slot masks hold 12 slots per field");
     count_launch(c);
     if (!c.st[pair].gn_active) return;       // uniform over the grid
-    unsigned long long* trk = trace ? trace + ((size_t)blockIdx.x * 16 + 15) * 8 : nullptr;   // launch-level stamps
-    res_stamp(trk);
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int NT = blockDim.x;
-    const int KNT = K * NT;
-    const int P = g.P, n2 = g.n2;
-    (void)nbmax;
-    // shared layout (floats): [guard][j-halo: P][own + padding: KNT][next-column halo: P][guard]
-    //                         [M: KNT][guard][et: KNT][guard]
-    // Slots n >= Nb are padding (M = 1, et = 0, r = 0, Hp forced to 0), so the
-    // slot loops need no bounds branch; et at l = n3 is 0, so p_{l-1}/p_{l+1}
-    // across a column boundary contribute nothing and need no PE test.
-    float* sp_ = reinterpret_cast<float*>(smem_raw) + 1 + P;
-    float* sM = sp_ + KNT + P + 1;
-    float* se = sM + KNT + 1;
-
+    unsigned long long* trk = TRACE ? trace + ((size_t)blockIdx.x * 16 + 15) * 8 : nullptr;   // launch-level stamps
+    if constexpr (TRACE) res_stamp(trk);
+    extern __shared__ __align__(16) float smem_f[];
+    const int P = g.P, Pp = res_pad(P), GPC = Pp >> 1, n2 = g.n2;
     const long long c0 = (long long)blockIdx.x * g.ncol / gridDim.x;
     const long long c1 = (long long)(blockIdx.x + 1) * g.ncol / gridDim.x;
     const int ncl = (int)(c1 - c0);
-    const int Nb = ncl * P;
+    const int nq = ncl * GPC;                // node pairs owned by this CTA
+    // shared layout (floats): [guard 2][p: KNT pairs][guard 2][M: KNT pairs][guard 2][et: KNT pairs]
+    // Padding nodes (l >= P, and slots past the CTA's columns) have M = 1,
+    // et = 0, r = 0, so their p and Hp stay exactly 0; et at l = n3 is 0, so
+    // the PE coupling never crosses columns.
+    constexpr int KNT2 = 2 * K * NT;
+    float* sp_ = smem_f + 2;
+    float* sM = sp_ + KNT2 + 2;
+    float* se = sM + KNT2 + 2;
+    float2* sp2 = reinterpret_cast<float2*>(sp_);
+    float2* sM2 = reinterpret_cast<float2*>(sM);
+    float2* se2 = reinterpret_cast<float2*>(se);
     const size_t n0 = (size_t)pair * g.ps + (size_t)c0 * P;
-    const int sI = n2 * P;
-    const float wi = (float)(g.ahd * g.ih1sq), wj = (float)(g.ahd * g.ih2sq);
-    // this CTA's first node in the ghost-padded global copy of p
-    float* __restrict__ pgc = pgh + (size_t)pair * res_ghost_pair_floats(g) + (size_t)(c0 + n2) * P;
-    float* __restrict__ xl = x + n0;
-    double* part2 = gpart;                 // [G][2] for r.z, r.r
-    double* part1 = gpart + 2 * gridDim.x; // [G][1] for p.Hp
-    FastDiv fdP, fdN2;
-    fdP.init((unsigned)P);
-    fdN2.init((unsigned)n2);
-    bool xset = false;                     // x holds alpha_0 p_0 + ... (else still to be zeroed)
+    // this CTA's first node in the ghost-padded global copy of p, and in xpad
+    float2* __restrict__ pgc2 =
+        reinterpret_cast<float2*>(pgh + (size_t)pair * res_ghost_pair_floats(g) + (size_t)(c0 + n2) * Pp);
+    float2* __restrict__ xp2 = reinterpret_cast<float2*>(xpad + (size_t)c0 * Pp);
+    const int sI2 = n2 * GPC;                // i-neighbour distance in node pairs
+    double* part0 = gpart;                   // [G][2] r0.z0, r0.r0
+    double* part1 = gpart + 2 * gridDim.x;   // [G][1] p.Hp
+    double* part2 = gpart + 3 * gridDim.x;   // [G][2] r.z, r.r
+    const int tid = threadIdx.x;
+    // flags[0, G): p-halo flags; flags[G]: launch counter (tags, see above)
+    const unsigned launch = *reinterpret_cast<volatile unsigned*>(flags + gridDim.x);
+    // CTAs owning this CTA's i-neighbour (+-n2) and j-neighbour (+-1) columns
+    const int blo = res_owner(c0 - n2 > 0 ? c0 - n2 : 0, g.ncol, gridDim.x);
+    const int bhi = res_owner(c1 - 1 + n2 < g.ncol ? c1 - 1 + n2 : g.ncol - 1, g.ncol, gridDim.x);
 
-    if (threadIdx.x == 0) {
-        sp_[-P - 1] = 0.f;
-        se[-1] = 0.f;
-        se[KNT] = 0.f;
-    }
-    // per-slot masks (bit k = slot k): node valid, j-1 neighbour exists, j+1 neighbour exists
-    unsigned mval = 0, mjm = 0, mjp = 0;
-    float r[K], hv[K];
+    if (tid < 6) smem_f[tid < 2 ? tid : tid < 4 ? 2 + KNT2 + (tid - 2) : 4 + 2 * KNT2 + (tid - 4)] = 0.f;
+    unsigned long long msk = 0;
+    float2 r[K], hv[K];
     float frz = 0.f, frr = 0.f;
+    {
+        FastDiv fdG, fdN2;
+        fdG.init((unsigned)GPC);
+        fdN2.init((unsigned)n2);
 #pragma unroll
-    for (int k = 0; k < K; k++) {
-        const int n = threadIdx.x + k * NT;
-        float rv = 0.f, M = 1.f, e = 0.f;
-        if (n < Nb) {
-            const int col = (int)c0 + fdP.div(n);
-            const int i = fdN2.div(col), j = col - i * n2;
-            M = dt[n0 + n] + (float)(g.ahd * diag_lxy(g, i, j));
-            e = et[n0 + n];
-            rv = -grad[n0 + n];
-            mval |= 1u << k;
-            if (j > 0) mjm |= 1u << k;
-            if (j < n2 - 1) mjp |= 1u << k;
+        for (int k = 0; k < K; k++) {
+            const int q = tid + k * NT;
+            float2 rv = make_float2(0.f, 0.f), Mv = make_float2(1.f, 1.f), ev = make_float2(0.f, 0.f);
+            if (q < nq) {
+                const int cl = fdG.div(q);
+                const int l0 = 2 * (q - cl * GPC);
+                const long long col = c0 + cl;
+                const int i = fdN2.div((int)col), j = (int)col - i * n2;
+                const float dl = (float)(g.ahd * diag_lxy(g, i, j));
+                const size_t o = n0 + (size_t)cl * P + l0;
+                Mv.x = dt[o] + dl;
+                ev.x = et[o];
+                rv.x = -grad[o];
+                if (l0 + 1 < P) {
+                    Mv.y = dt[o + 1] + dl;
+                    ev.y = et[o + 1];
+                    rv.y = -grad[o + 1];
+                }
+                msk |= 1ull << (RM_VAL + k);
+                if (j > 0) msk |= 1ull << ((cl > 0 ? RM_JML : RM_JMR) + k);
+                if (j < n2 - 1) msk |= 1ull << ((cl < ncl - 1 ? RM_JPL : RM_JPR) + k);
+                const float2 z = make_float2(precond(rv.x, Mv.x), precond(rv.y, Mv.y));
+                frz = fmaf(rv.x, z.x, frz);
+                frz = fmaf(rv.y, z.y, frz);
+                frr = fmaf(rv.x, rv.x, frr);
+                frr = fmaf(rv.y, rv.y, frr);
+                sp2[q] = z;
+                pgc2[q] = z;                   // x = 0 is written by the first update (or below)
+            } else {
+                sp2[q] = rv;
+            }
+            sM2[q] = Mv;
+            se2[q] = ev;
+            r[k] = rv;
+            hv[k] = make_float2(0.f, 0.f);
         }
-        const float z = precond(rv, M);
-        sM[n] = M;
-        se[n] = e;
-        sp_[n] = z;
-        r[k] = rv;
-        hv[k] = 0.f;
-        if (n < Nb) pgc[n] = z;               // x = 0 is written by the first update (or below)
-        frz = fmaf(rv, z, frz);
-        frr = fmaf(rv, rv, frr);
     }
     double v2[2] = {(double)frz, (double)frr}, t2[2];
-    res_stamp(trk ? trk + 1 : nullptr);
-    grid_reduce<2>(v2, part2, bar, t2);       // also publishes p0 to the neighbours
-    res_stamp(trk ? trk + 2 : nullptr);
+    if constexpr (TRACE) res_stamp(trk + 1);
+    halo_release(flags, res_tag(launch, 0));  // p0 published
+    reduce_publish<2>(v2, part0, res_tag(launch, 0));
+    reduce_collect<2>(part0, res_tag(launch, 0), t2);
+    if constexpr (TRACE) res_stamp(trk + 2);
+    // Loop state kept out of registers (the r / Hp slots need 48 of the 80):
+    // rr0 and the last r.r live in shared memory; the H-evaluation count, "x
+    // already set" and "p barrier pending" all equal k_it > 0 / k_it.
+    __shared__ double s_rr0, s_rr;
     double rz = t2[0];
-    const double rr0 = t2[1];
-    double relres = rr0 > 0 ? 1.0 : 0.0;
-    int k_it = 0, hev = 0;
-    if (rr0 > 0.0) {
-        cooperative_groups::grid_group grid = cooperative_groups::this_grid();
-        unsigned tok3 = 0;                    // pending split barrier "new p published"
-        bool pend3 = false;
+    if (tid == 0) {
+        s_rr0 = t2[1];
+        s_rr = t2[1];
+    }
+    int k_it = 0;
+    if (t2[1] > 0.0) {
         for (k_it = 0; k_it < sp.max_pcg;) {
-            unsigned long long* tr = (trace && k_it < 16) ? trace + ((size_t)blockIdx.x * 16 + k_it) * 8 : nullptr;
-            res_stamp(tr);
-            if (pend3) grid.barrier_wait(std::move(tok3));
-            // j-halo columns (c0-1 and c1) from the global copy; zeros off the ends
-            for (int t = threadIdx.x; t < 2 * P; t += NT) {
-                const bool nxt = t >= P;
-                const int l = nxt ? t - P : t;
-                const long long col = nxt ? c1 : c0 - 1;
-                float v = 0.f;
-                if (col >= 0 && col < g.ncol) v = __ldcg(pgc + (nxt ? Nb : -P) + l);
-                sp_[(nxt ? Nb : -P) + l] = v;
-            }
-            __syncthreads();
-            res_stamp(tr ? tr + 1 : nullptr);
-            // ---- Hp = M p + et_{l-1} p_{l-1} + et_l p_{l+1} - alpha hd sum_inplane p_nb / h^2
-            float fpq = 0.f;
+            unsigned long long* tr = (TRACE && k_it < 16) ? trace + ((size_t)blockIdx.x * 16 + k_it) * 8 : nullptr;
+            if constexpr (TRACE) res_stamp(tr);
+            // ---- local part of Hp (own shared memory only; overlaps the p barrier):
+            // M p + et_{l-1} p_{l-1} + et_l p_{l+1} - alpha hd / h2^2 (p_{j-1} + p_{j+1}).
+            // Every slot loop is branch-free (padding slots compute zeros), so
+            // all loads of a phase can be in flight together.
             {
-                const int tid = opaque(threadIdx.x);
-                const unsigned mv = (unsigned)opaque((int)mval), mm = (unsigned)opaque((int)mjm),
-                               mp = (unsigned)opaque((int)mjp);
-                const float* gm = pgc + tid - sI;   // i-1 neighbours (ghost plane at i = -1)
-                const float* gp = pgc + tid + sI;   // i+1 neighbours (ghost plane at i = n1)
-                const float* s0 = sp_ + tid;
-                const float* m0 = sM + tid;
-                const float* e0 = se + tid;
+                const int t0 = opaque(tid);
+                const unsigned long long m = opaque64(msk);
+                const float2* s2 = sp2 + t0;
+                const float2* m2 = sM2 + t0;
+                const float2* e2 = se2 + t0;
+                const float* s1 = sp_ + 2 * t0;
+                const float* e1 = se + 2 * t0;
 #pragma unroll
                 for (int k = 0; k < K; k++) {
                     const int o = k * NT;
-                    const float pv = s0[o];
-                    float h = m0[o] * pv;
-                    h = fmaf(e0[o - 1], s0[o - 1], h);
-                    h = fmaf(e0[o], s0[o + 1], h);
-                    const float si = __ldcg(gm + o) + __ldcg(gp + o);
-                    float sj = 0.f;
-                    if (mm & (1u << k)) sj = s0[o - P];
-                    if (mp & (1u << k)) sj += s0[o + P];
-                    h = fmaf(-wi, si, fmaf(-wj, sj, h));
-                    h = (mv & (1u << k)) ? h : 0.f;
+                    const float2 p = s2[o], M = m2[o], e = e2[o];
+                    const float pm = s1[2 * o - 1], em = e1[2 * o - 1], pn = s1[2 * o + 2];
+                    float2 h;
+                    h.x = fmaf(e.x, p.y, fmaf(em, pm, M.x * p.x));
+                    h.y = fmaf(e.y, pn, fmaf(e.x, p.x, M.y * p.y));
+                    const float2 a = mbit(m, RM_JML + k) ? s2[o - GPC] : make_float2(0.f, 0.f);
+                    const float2 b = mbit(m, RM_JPL + k) ? s2[o + GPC] : make_float2(0.f, 0.f);
+                    h.x = fmaf(-wj, a.x + b.x, h.x);
+                    h.y = fmaf(-wj, a.y + b.y, h.y);
                     hv[k] = h;
-                    fpq = fmaf(pv, h, fpq);
                 }
             }
+            halo_acquire(flags, blo, bhi, res_tag(launch, k_it));   // neighbours' p_k
+            if constexpr (TRACE) res_stamp(tr ? tr + 1 : nullptr);
+            // ---- remote part: i-neighbours (and j-neighbours across the CTA
+            // boundary) from the global copy; p.Hp
+            float fpq = 0.f;
+            {
+                const int t0 = opaque(tid);
+                const unsigned long long m = opaque64(msk);
+                const float2* gc = pgc2 + t0;
+                const float2* s2 = sp2 + t0;
+#pragma unroll
+                for (int k = 0; k < K; k++) {
+                    const int o = k * NT;
+                    const float2 a = __ldcg(gc + o - sI2);
+                    const float2 b = __ldcg(gc + o + sI2);
+                    const float2 c = mbit(m, RM_JMR + k) ? __ldcg(gc + o - GPC) : make_float2(0.f, 0.f);
+                    const float2 d = mbit(m, RM_JPR + k) ? __ldcg(gc + o + GPC) : make_float2(0.f, 0.f);
+                    float2 h = hv[k];
+                    h.x = fmaf(-wi, a.x + b.x, fmaf(-wj, c.x + d.x, h.x));
+                    h.y = fmaf(-wi, a.y + b.y, fmaf(-wj, c.y + d.y, h.y));
+                    const bool v = mbit(m, RM_VAL + k);
+                    h.x = v ? h.x : 0.f;
+                    h.y = v ? h.y : 0.f;
+                    hv[k] = h;
+                    const float2 p = s2[o];
+                    fpq = fmaf(p.x, h.x, fpq);
+                    fpq = fmaf(p.y, h.y, fpq);
+                }
+            }
+            if constexpr (TRACE) res_stamp(tr ? tr + 2 : nullptr);
             double v1[1] = {(double)fpq}, t1[1];
-            grid_reduce<1>(v1, part1, bar, t1, tr ? tr + 2 : nullptr);
-            res_stamp(tr ? tr + 3 : nullptr);
+            reduce_publish<1>(v1, part1, res_tag(launch, k_it));
+            reduce_collect<1>(part1, res_tag(launch, k_it), t1);
+            if constexpr (TRACE) res_stamp(tr ? tr + 3 : nullptr);
             if (t1[0] <= 0.0) break;                  // breakdown (oracle pcg(): keep x)
-            hev += 1;
             const float a = (float)(rz / t1[0]);
             // ---- r -= a Hp, z = r/M (kept in the dead Hp registers); r.z, r.r
             float frz2 = 0.f, frr2 = 0.f;
             {
-                const int tid = opaque(threadIdx.x);
-                const float* m0 = sM + tid;
+                const int t0 = opaque(tid);
+                const float2* m2 = sM2 + t0;
 #pragma unroll
                 for (int k = 0; k < K; k++) {
-                    const float rn = fmaf(-a, hv[k], r[k]);
+                    const float2 M = m2[k * NT];
+                    float2 rn = r[k];
+                    rn.x = fmaf(-a, hv[k].x, rn.x);
+                    rn.y = fmaf(-a, hv[k].y, rn.y);
                     r[k] = rn;
-                    const float z = precond(rn, m0[k * NT]);
+                    const float2 z = make_float2(precond(rn.x, M.x), precond(rn.y, M.y));
                     hv[k] = z;
-                    frz2 = fmaf(rn, z, frz2);
-                    frr2 = fmaf(rn, rn, frr2);
+                    frz2 = fmaf(rn.x, z.x, frz2);
+                    frz2 = fmaf(rn.y, z.y, frz2);
+                    frr2 = fmaf(rn.x, rn.x, frr2);
+                    frr2 = fmaf(rn.y, rn.y, frr2);
                 }
             }
             double v3[2] = {(double)frz2, (double)frr2}, t3[2];
-            const unsigned tok2 = reduce_arrive<2>(v3, part2, grid);
-            res_stamp(tr ? tr + 4 : nullptr);
-            // ---- x += a p while the r.z / r.r partials gather (fire-and-forget L2
-            // adds; x feeds no reduction)
+            reduce_publish<2>(v3, part2, res_tag(launch, k_it));
+            if constexpr (TRACE) res_stamp(tr ? tr + 4 : nullptr);
+            // ---- x += a p while the r.z / r.r partials gather (fire-and-forget
+            // L2 adds; x feeds no reduction)
             {
-                const int tid = opaque(threadIdx.x);
-                const unsigned mv = (unsigned)opaque((int)mval);
-                float* xt = xl + tid;
-                const float* s0 = sp_ + tid;
-                if (xset) {
+                const int t0 = opaque(tid);
+                const unsigned long long m = opaque64(msk);
+                const float2* s2 = sp2 + t0;
+                float2* xt = xp2 + t0;
 #pragma unroll
-                    for (int k = 0; k < K; k++)
-                        if (mv & (1u << k)) red_add(xt + k * NT, a * s0[k * NT]);
-                } else {                      // first update: x_1 = 0 + a p_0 (plain stores)
-#pragma unroll
-                    for (int k = 0; k < K; k++)
-                        if (mv & (1u << k)) xt[k * NT] = 0.f + a * s0[k * NT];
+                for (int k = 0; k < K; k++) {
+                    const float2 p = s2[k * NT];
+                    const float2 v = make_float2(a * p.x, a * p.y);
+                    if (mbit(m, RM_VAL + k)) {
+                        if (k_it > 0) red_add2(reinterpret_cast<float*>(xt + k * NT), v);
+                        else xt[k * NT] = v;  // first update: x_1 = 0 + a p_0
+                    }
                 }
             }
-            xset = true;
-            reduce_finish<2>(tok2, part2, grid, t3);
-            res_stamp(tr ? tr + 5 : nullptr);
+            reduce_collect<2>(part2, res_tag(launch, k_it), t3);
+            if constexpr (TRACE) res_stamp(tr ? tr + 5 : nullptr);
             k_it += 1;
-            relres = sqrt(t3[1] / rr0);
+            if (tid == 0) s_rr = t3[1];
             const double beta = t3[0] / rz;
             rz = t3[0];
-            if (k_it >= sp.max_pcg || (!sp.fixed && relres < sp.pcg_rtol)) break;
+            if (k_it >= sp.max_pcg || (!FIXED && sqrt(t3[1] / s_rr0) < sp.pcg_rtol)) break;
             // ---- p = z + beta p on own columns and on the global halo copy
             const float be = (float)beta;
             {
-                const int tid = opaque(threadIdx.x);
-                const unsigned mv = (unsigned)opaque((int)mval);
-                float* s0 = sp_ + tid;
-                float* gt = pgc + tid;
+                const int t0 = opaque(tid);
+                const unsigned long long m = opaque64(msk);
+                float2* s2 = sp2 + t0;
+                float2* gt = pgc2 + t0;
 #pragma unroll
                 for (int k = 0; k < K; k++) {
                     const int o = k * NT;
-                    const float pn = fmaf(be, s0[o], hv[k]);
-                    s0[o] = pn;
-                    if (mv & (1u << k)) gt[o] = pn;
+                    const float2 p = s2[o], z = hv[k];
+                    const float2 pn = make_float2(fmaf(be, p.x, z.x), fmaf(be, p.y, z.y));
+                    s2[o] = pn;
+                    if (mbit(m, RM_VAL + k)) gt[o] = pn;
                 }
             }
-            res_stamp(tr ? tr + 6 : nullptr);
-            tok3 = grid.barrier_arrive();
-            pend3 = true;
+            if constexpr (TRACE) res_stamp(tr ? tr + 6 : nullptr);
+            halo_release(flags, res_tag(launch, k_it));            // p_{k+1} published
         }
     }
-    if (!xset)                                // no update happened (r0 = 0 or breakdown): x = 0
-        for (int n = threadIdx.x; n < Nb; n += NT) xl[n] = 0.f;
-    res_stamp(trk ? trk + 3 : nullptr);
+    // ---- q = x back to the node layout (each thread reads the pairs it
+    // accumulated itself, so its own L2 adds are ordered before the loads)
+    {
+        FastDiv fdG;
+        fdG.init((unsigned)GPC);
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+            const int q = tid + k * NT;
+            if (q >= nq) continue;
+            const int cl = fdG.div(q);
+            const int l0 = 2 * (q - cl * GPC);
+            const float2 v = k_it > 0 ? __ldcg(xp2 + q) : make_float2(0.f, 0.f);
+            float* xo = x + n0 + (size_t)cl * P + l0;
+            xo[0] = v.x;
+            if (l0 + 1 < P) xo[1] = v.y;
+        }
+    }
+    if constexpr (TRACE) res_stamp(trk + 3);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
+        // every CTA read `launch` before its first publish, which CTA 0 has
+        // collected, so the counter can advance now
+        *reinterpret_cast<volatile unsigned*>(flags + gridDim.x) = launch + 1;
         PairState& s = c.st[pair];
         s.rz = rz;
-        s.rr0 = rr0;
+        s.rr0 = s_rr0;
         s.pcg_k = k_it;
         s.pcg_iters += k_it;
-        s.h_evals += hev;
-        s.relres = relres;
+        s.h_evals += k_it;                   // one H p per completed iteration (a breakdown stops before both)
+        s.relres = s_rr0 > 0.0 ? sqrt(s_rr / s_rr0) : 0.0;
         s.pcg_active = 0;
     }
 }

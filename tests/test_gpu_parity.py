@@ -291,10 +291,12 @@ def test_graph_and_host_loop_bitwise_equal(monkeypatch):
     assert out[0][2] == out[1][2]
 
 
-# tile orders of the resident PCG (hysco_resident.cuh): rows per strip R = 1
-# (C1), 12 (3T), 4 with square tiles, 4 with ragged tiles (odd n2), and 2 with
-# local neighbours across a strip edge (n2 = 2)
-RESIDENT_CASES = ["C1_16x16x8", "C2_hcp3t", (60, 40, 16), (84, 37, 10), (400, 2, 10)]
+# shapes for the resident PCG (hysco_resident.cuh; columns split over 148 CTAs,
+# node pairs with even-padded columns): odd P with one padding node (C1, 3T,
+# (60, 40, 16)), even P without padding ((50, 30, 15)), ragged columns per CTA
+# ((84, 37, 10)), CTA ranges cutting i-rows everywhere with j-neighbours across
+# CTA edges (n2 = 2), and one or two columns per CTA ((25, 8, 24))
+RESIDENT_CASES = ["C1_16x16x8", "C2_hcp3t", (60, 40, 16), (50, 30, 15), (84, 37, 10), (400, 2, 10), (25, 8, 24)]
 
 
 @pytest.mark.parametrize("cfg", RESIDENT_CASES, ids=[str(c) for c in RESIDENT_CASES])

@@ -23,9 +23,9 @@ int main(int argc, char** argv) {
     g.ahd = g.alpha * g.hd; g.bh2 = 0.5e-4 * g.hd;
     g.ih1sq = g.ih2sq = g.ih3sq = 1 / (1.25 * 1.25); g.ih3 = 1 / 1.25;
     int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-    const int G = nsm, NT = RES_THREADS, K = 24;
+    const int G = nsm, NT = RES_THREADS, K = 12;
     const long long ncl = (g.ncol + G - 1) / G, knt = (long long)K * NT;
-    if (ncl * g.P > knt) { printf("does not fit K=24\n"); return 1; }
+    if (ncl * (res_pad(g.P) / 2) > knt) { printf("does not fit K=12\n"); return 1; }
     size_t Nn = g.Nn;
     std::vector<float> hdt(Nn), het(Nn), hg(Nn);
     srand(1);
@@ -34,9 +34,11 @@ int main(int argc, char** argv) {
         het[t] = ((t % g.P) == (size_t)n3) ? 0.f : -300.f - 4e4f * (rand() / (float)RAND_MAX);
         hg[t] = (rand() / (float)RAND_MAX) - 0.5f;
     }
-    float *dt, *et, *grad, *x, *pgh;
+    float *dt, *et, *grad, *x, *pgh, *xpad;
     cudaMalloc(&dt, Nn * 4); cudaMalloc(&et, Nn * 4); cudaMalloc(&grad, Nn * 4); cudaMalloc(&x, Nn * 4);
-    size_t ghost = res_ghost_pair_floats(g);
+    cudaMalloc(&xpad, (size_t)g.ncol * res_pad(g.P) * 4);
+    const float wi = (float)(g.ahd * g.ih1sq), wj = (float)(g.ahd * g.ih2sq);
+    size_t ghost = res_ghost_pair_floats(g) + res_ghost_slack_floats(12);
     cudaMalloc(&pgh, ghost * 4); cudaMemset(pgh, 0, ghost * 4);
     cudaMemcpy(dt, hdt.data(), Nn * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(et, het.data(), Nn * 4, cudaMemcpyHostToDevice);
@@ -45,14 +47,17 @@ int main(int argc, char** argv) {
     PairState hs{}; hs.gn_active = 1; cudaMemcpy(st, &hs, sizeof hs, cudaMemcpyHostToDevice);
     unsigned long long* launches; cudaMalloc(&launches, 8);
     double* part; cudaMalloc(&part, sizeof(double) * 8 * G);
-    unsigned* bar; cudaMalloc(&bar, 8); cudaMemset(bar, 0, 8);
+    unsigned* flags; cudaMalloc(&flags, 4 * (G + 1)); cudaMemset(flags, 0, 4 * (G + 1));
+    cudaMemset(part, 0, sizeof(double) * 8 * G);
+    { unsigned one = 1; cudaMemcpy(flags + G, &one, 4, cudaMemcpyHostToDevice); }
     unsigned long long* trace; cudaMalloc(&trace, sizeof(unsigned long long) * G * 16 * 8);
     cudaMemset(trace, 0, sizeof(unsigned long long) * G * 16 * 8);
     unsigned* dcond; cudaMalloc(&dcond, 4 * NCOND);
     Ctl c{}; c.st = st; c.launches = launches; c.dcond = dcond; c.use_graph = 0;
     SolveParams sp{}; sp.max_pcg = 10; sp.fixed = 1;
-    const size_t smem = (size_t)(3 * knt + 2 * g.P + 8) * sizeof(float);
-    cudaFuncSetAttribute(pcg_resident_kernel<24, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem = res_smem_bytes(12);
+    cudaFuncSetAttribute(pcg_resident_kernel<12, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(pcg_resident_kernel<12, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(G); cfg.blockDim = dim3(NT); cfg.dynamicSmemBytes = smem; cfg.stream = 0;
     cudaLaunchAttribute at[1]; at[0].id = cudaLaunchAttributeCooperative; at[0].val.cooperative = 1;
@@ -61,19 +66,19 @@ int main(int argc, char** argv) {
     float ms_notrace = 0, ms_trace = 0;
     for (int rep = 0; rep < 3; rep++) {
         cudaEventRecord(e0);
-        cudaLaunchKernelEx(&cfg, pcg_resident_kernel<24, true>, g, c, sp, 0, (const float*)grad, (const float*)dt,
-                           (const float*)et, x, pgh, part, bar, 0, (unsigned long long*)nullptr);
+        cudaLaunchKernelEx(&cfg, pcg_resident_kernel<12, true>, g, c, sp, 0, (const float*)grad, (const float*)dt,
+                           (const float*)et, x, xpad, pgh, part, flags, wi, wj, (unsigned long long*)nullptr);
         cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms_notrace, e0, e1);
     }
     cudaEventRecord(e0);
-    cudaLaunchKernelEx(&cfg, pcg_resident_kernel<24, true>, g, c, sp, 0, (const float*)grad, (const float*)dt,
-                       (const float*)et, x, pgh, part, bar, 0, trace);
+    cudaLaunchKernelEx(&cfg, pcg_resident_kernel<12, true, true>, g, c, sp, 0, (const float*)grad, (const float*)dt,
+                       (const float*)et, x, xpad, pgh, part, flags, wi, wj, trace);
     cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms_trace, e0, e1);
     printf("err=%s  kernel %.1f us (untraced), %.1f us (traced), grid %d x %d, K %d\n",
            cudaGetErrorString(cudaGetLastError()), ms_notrace * 1e3, ms_trace * 1e3, G, NT, K);
     std::vector<unsigned long long> ht((size_t)G * 16 * 8);
     cudaMemcpy(ht.data(), trace, ht.size() * 8, cudaMemcpyDeviceToHost);
-    const char* names[9] = {"iter start", "p-barrier + j-halo", "Hp done (CTA)", "reduce #1 done",
+    const char* names[9] = {"iter start", "local Hp + p-barrier", "remote Hp done", "reduce #1 done",
                             "U-phase, arrive #2", "x upd + reduce #2", "D-phase, arrive #3", "(unused)",
                             "next iter start"};
     // per phase k -> k+1: span = max_cta(t[k+1]) - min_cta(t[k]); cta = mean over CTAs of (t[k+1]-t[k])
