@@ -196,8 +196,8 @@ def roofline_entry(H, ctx, args, r0, B, shape, ms_per_step):
     Nn, Nc = B * n1 * n2 * (n3 + 1), B * n1 * n2 * n3
     resident = prof_warm["pcg_resident"] > 0
     gn = r0["gn_iters"]
-    if resident:   # one cooperative launch per GN step runs all PCG iterations on chip
-        per_step = {"pcg_resident": gn, "eval": r0["f_evals"], "trial_init": gn}
+    if resident:   # one cooperative launch per GN step runs all PCG iterations and the Armijo start
+        per_step = {"pcg_resident": gn, "eval": r0["f_evals"]}
     else:
         per_step = {"matvec": r0["h_evals"], "pcg_update": r0["pcg_iters"], "pcg_dir": r0["pcg_iters"],
                     "eval": r0["f_evals"], "trial_init": gn}

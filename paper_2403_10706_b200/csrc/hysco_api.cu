@@ -313,7 +313,9 @@ struct Runner {
         default: { constexpr int RK = 12; __VA_ARGS__; } break;                \
     }
 
-static void launch_resident(hysco_ctx c, const SolveParams& sp, int pair) {
+// bcur / bold: the trial b and b_old the fused Armijo start writes (B_B /
+// B_BOLD in a solve; scratch when profiling).
+static void launch_resident(hysco_ctx c, const SolveParams& sp, int pair, float* bcur, float* bold) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(c->res_grid, 1, 1);
     cfg.blockDim = dim3(RES_THREADS, 1, 1);
@@ -325,18 +327,19 @@ static void launch_resident(hysco_ctx c, const SolveParams& sp, int pair) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     float* const* B = reinterpret_cast<float* const*>(c->buf);
+    const int nb = c->cfg.batch;
     if (sp.fixed) {
         RES_K_SWITCH(c->res_k, cudaLaunchKernelEx(&cfg, pcg_resident_kernel<RK, true>, c->g, c->ctl, sp, pair,
                                                   (const float*)B[B_GRAD], (const float*)B[B_DT],
                                                   (const float*)B[B_ET], B[B_X], c->res_x, c->res_pg,
-                                                  c->res_part, c->res_flags, c->res_wi, c->res_wj,
-                                                  (unsigned long long*)nullptr));
+                                                  c->res_part, c->res_flags, c->res_wi, c->res_wj, bcur, bold,
+                                                  nb, (unsigned long long*)nullptr));
     } else {
         RES_K_SWITCH(c->res_k, cudaLaunchKernelEx(&cfg, pcg_resident_kernel<RK, false>, c->g, c->ctl, sp, pair,
                                                   (const float*)B[B_GRAD], (const float*)B[B_DT],
                                                   (const float*)B[B_ET], B[B_X], c->res_x, c->res_pg,
-                                                  c->res_part, c->res_flags, c->res_wi, c->res_wj,
-                                                  (unsigned long long*)nullptr));
+                                                  c->res_part, c->res_flags, c->res_wi, c->res_wj, bcur, bold,
+                                                  nb, (unsigned long long*)nullptr));
     }
 }
 
@@ -702,15 +705,17 @@ static void gn_sequence(Runner& r, const SolveParams& sp) {
     r.loop(COND_GN, [&] {
         r.handle(COND_PCG);
         r.handle(COND_LS);
-        if (c->resident) {
+        if (c->resident) {   // PCG + the Armijo start (trial_init) in one launch per pair
             r.seq([&] {
-                for (int p = 0; p < c->cfg.batch; p++) launch_resident(c, sp, p);
+                for (int p = 0; p < c->cfg.batch; p++)
+                    launch_resident(c, sp, p, reinterpret_cast<float*>(L<T>::b(c, B_B)),
+                                    reinterpret_cast<float*>(L<T>::b(c, B_BOLD)));
             });
         } else {
             r.seq([&] { L<T>::pcg_init(c); });
             r.loop(COND_PCG, [&] { r.seq([&] { L<T>::pcg_iter(c, sp); }); });
+            r.seq([&] { L<T>::trial_init(c); });
         }
-        r.seq([&] { L<T>::trial_init(c); });
         r.loop(COND_LS, [&] { r.seq([&] { L<T>::ls_body(c, sp); }); });   // its last eval sets COND_GN
     });
 }
@@ -927,6 +932,7 @@ static hysco_status create_impl(const hysco_config* cfg, const SlabSpec* slab, v
     g.ih2sq = 1.0 / (cfg->h2 * cfg->h2);
     g.ih3sq = 1.0 / (cfg->h3 * cfg->h3);
     g.ih3 = 1.0 / cfg->h3;
+    geom_finish(g);
     g.ps = g.Nn;
     g.i0 = 0;
     g.n1g = g.n1;
@@ -1383,7 +1389,9 @@ static hysco_status profile_typed(hysco_ctx ctx, int reps, int flush_l2, double*
                     if (!ctx->resident) break;
                     SolveParams rp = sp;
                     rp.max_pcg = 10;          // one GN step's PCG solve
-                    for (int p = 0; p < ctx->cfg.batch; p++) launch_resident(ctx, rp, p);
+                    for (int p = 0; p < ctx->cfg.batch; p++)   // trial b to scratch: B_B stays
+                        launch_resident(ctx, rp, p, reinterpret_cast<float*>(L<T>::b(ctx, B_TMP)),
+                                        reinterpret_cast<float*>(L<T>::b(ctx, B_HP)));
                     break;
                 }
                 case HYSCO_PROF_TRIAL:

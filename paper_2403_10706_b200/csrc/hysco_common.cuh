@@ -28,7 +28,25 @@ struct Geom {
     // each side and a pair stride ps = (n1 + 2) n2 P (ps = Nn without slabs).
     long long ps;
     int i0, n1g, slab;
+    // fp32 copies of the weights (set by geom_finish): kernels read them as
+    // constant-bank operands instead of converting the doubles per use
+    float f_hd, f_ahd, f_bh2, f_ih1sq, f_ih2sq, f_ih3sq, f_ih3;
 };
+
+// Fill the fp32 copies of Geom's weights (host).
+inline void geom_finish(Geom& g) {
+    g.f_hd = (float)g.hd;
+    g.f_ahd = (float)g.ahd;
+    g.f_bh2 = (float)g.bh2;
+    g.f_ih1sq = (float)g.ih1sq;
+    g.f_ih2sq = (float)g.ih2sq;
+    g.f_ih3sq = (float)g.ih3sq;
+    g.f_ih3 = (float)g.ih3;
+}
+// A weight in the kernel's arithmetic type.
+template <typename T> __device__ __forceinline__ T gw(double d, float f);
+template <> __device__ __forceinline__ float gw<float>(double, float f) { return f; }
+template <> __device__ __forceinline__ double gw<double>(double d, float) { return d; }
 
 // in-plane neighbours along dim 1 exist (homogeneous Neumann, R3), global index
 __device__ __forceinline__ bool has_im(const Geom& g, int i) { return g.i0 + i > 0; }

@@ -37,7 +37,7 @@ __device__ __forceinline__ void interp_from(const T* __restrict__ s, int n3, int
 // rounding of k) is the same decision on both sides (R5).
 __device__ __forceinline__ void interp_col(const float* __restrict__ s, int n3, int k, float Ab, float sign,
                                            const Geom& g, double& val, float& slope) {
-    float del = sign * Ab * (float)g.ih3;
+    float del = sign * Ab * g.f_ih3;
     del = fminf(fmaxf(del, (float)-(n3 + 2)), (float)(n3 + 2));   // infeasible b can push far out
     const float fl = floorf(del);
     interp_from(s, n3, k + (int)fl, del - fl, val, slope);
@@ -51,7 +51,7 @@ __device__ __forceinline__ void interp_col(const double* __restrict__ s, int n3,
 }
 
 // (b_{k+1} - b_k)/h3: fp64 divides like the oracle, fp32 multiplies.
-__device__ __forceinline__ float diff_h3(float b0, float b1, const Geom& g) { return (b1 - b0) * (float)g.ih3; }
+__device__ __forceinline__ float diff_h3(float b0, float b1, const Geom& g) { return (b1 - b0) * g.f_ih3; }
 __device__ __forceinline__ double diff_h3(double b0, double b1, const Geom& g) { return (b1 - b0) / g.h3; }
 
 // diag of the in-plane (dims 1,2) Neumann Laplacian at column (i, j) (R3)
@@ -155,8 +155,9 @@ __host__ __device__ inline size_t eval_smem_elems(int n3) {
 // arithmetic (absolute coordinate, (1-t) v0 + t v1), see R5.
 __device__ __forceinline__ void gather_pm(const float* __restrict__ sIp, const float* __restrict__ sIm, int n3, int k,
                                           float Ab, const Geom& g, double& vp, double& vm, float& spl, float& sml) {
-    float del = Ab * (float)g.ih3;
-    del = fminf(fmaxf(del, (float)-(n3 + 2)), (float)(n3 + 2));
+    float del = Ab * g.f_ih3;
+    const float lim = (float)(n3 + 2);   // infeasible b can push far out
+    del = fminf(fmaxf(del, -lim), lim);
     {
         const float fl = floorf(del);
         const int kk = min(max(k + (int)fl, -2), n3);
@@ -191,10 +192,17 @@ __device__ __forceinline__ void gather_pm(const double* __restrict__ sIp, const 
     gather_one(sIm, n3, k, Ab, -1.0, g, vm, sml);
 }
 
-// phi, phi', phi'' (Eq.(3)) for |z| < 1 with one reciprocal of (1 - z^2).
+// phi, phi', phi'' (Eq.(3)) for |z| < 1 with one reciprocal of (1 - z^2)
+// (fp32: the hardware reciprocal, ~1 ulp; the barrier enters J scaled by beta).
+__device__ __forceinline__ double recip(double x) { return 1.0 / x; }
+__device__ __forceinline__ float recip(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
 template <typename T>
 __device__ __forceinline__ void phi3(T z, T& f0, T& f1, T& f2) {
-    const T z2 = z * z, inv = T(1) / (T(1) - z2);
+    const T z2 = z * z, inv = recip(T(1) - z2);
     f0 = z2 * z2 * inv;
     f1 = T(2) * z * z2 * (T(2) - z2) * inv * inv;
     f2 = T(2) * z2 * (T(6) - T(3) * z2 + z2 * z2) * inv * inv * inv;
@@ -287,8 +295,9 @@ __global__ void __launch_bounds__(256, 4) eval_kernel(Geom g, Ctl c, SolveParams
         gm = c.st[pair].ls_restore ? T(0) : (T)c.st[pair].gamma;
     }
 
-    const T hd = (T)g.hd, ahd = (T)g.ahd, bh2 = (T)g.bh2;
-    const T ih3 = (T)g.ih3, ih3sq = (T)g.ih3sq, ih1sq = (T)g.ih1sq, ih2sq = (T)g.ih2sq;
+    const T hd = gw<T>(g.hd, g.f_hd), ahd = gw<T>(g.ahd, g.f_ahd), bh2 = gw<T>(g.bh2, g.f_bh2);
+    const T ih3 = gw<T>(g.ih3, g.f_ih3), ih3sq = gw<T>(g.ih3sq, g.f_ih3sq);
+    const T ih1sq = gw<T>(g.ih1sq, g.f_ih1sq), ih2sq = gw<T>(g.ih2sq, g.f_ih2sq);
     const long long sI = (long long)n2 * P;   // node stride along dim 1
     const T* bp = bsrc + (size_t)pair * g.ps;
     const T* ipp = Ip + (size_t)pair * g.Nc;
@@ -333,37 +342,38 @@ __global__ void __launch_bounds__(256, 4) eval_kernel(Geom g, Ctl c, SolveParams
 #pragma unroll
                     for (int m = 0; m < NCH; m++) {
                         const int l = seg + 32 * m + lane;
-                        T ar = 0, a2 = 0, cr = 0, c2 = 0, p1 = 0, p2 = 0, ev = 0;
-                        if (l < n3) {
-                            const T b0 = sbc[l], b1 = sbc[l + 1];
-                            const T Ab = T(0.5) * (b0 + b1);          // averaging operator A
-                            const T Db = diff_h3(b0, b1, g);          // finite difference D
-                            double vp, vm;
-                            T spl, sml;
-                            gather_pm(sIp, sIm, n3, l, Ab, g, vp, vm, spl, sml);   // I+(x + b), I-(x - b)
-                            const double Dbd = (double)Db;
-                            const double rd = vp * (1.0 + Dbd) - vm * (1.0 - Dbd);  // Eq.(1)-(2) residual (fp64)
-                            const T r = (T)rd;
-                            const T gg = (spl * (T(1) + Db) + sml * (T(1) - Db)) * ih3;
-                            const T s = (T)(vp + vm);
-                            const T a = gg * T(0.5) - s * ih3;        // dr_k/db_k
-                            const T cc = gg * T(0.5) + s * ih3;       // dr_k/db_{k+1}
+                        // branch-free: lanes past the last cell compute on a clamped
+                        // cell and mask their contributions
+                        const bool cv = l < n3;
+                        const int lc = cv ? l : n3 - 1;
+                        const T b0 = sbc[lc], b1 = sbc[lc + 1];
+                        const T Ab = T(0.5) * (b0 + b1);              // averaging operator A
+                        const T Db = diff_h3(b0, b1, g);              // finite difference D
+                        double vp, vm;
+                        T spl, sml;
+                        gather_pm(sIp, sIm, n3, lc, Ab, g, vp, vm, spl, sml);   // I+(x + b), I-(x - b)
+                        const double Dbd = (double)Db;
+                        const double rd = vp * (1.0 + Dbd) - vm * (1.0 - Dbd);  // Eq.(1)-(2) residual (fp64)
+                        const T r = (T)rd;
+                        const T gg = (spl * (T(1) + Db) + sml * (T(1) - Db)) * ih3;
+                        const T s = (T)(vp + vm);
+                        const T a = gg * T(0.5) - s * ih3;            // dr_k/db_k
+                        const T cc = gg * T(0.5) + s * ih3;           // dr_k/db_{k+1}
+                        const T dd = b1 - b0;
+                        const bool infz = fabs(Db) >= T(1);           // phi = +inf (Eq.(3))
+                        T f0, p1, p2;
+                        phi3(infz ? T(0) : Db, f0, p1, p2);
+                        if (cv) {
                             aD = fma(rd, rd, aD);
-                            const T dd = b1 - b0;
                             fS += dd * dd * ih3sq;
-                            if (fabs(Db) >= T(1)) {
-                                aInf = 1.0;                           // phi = +inf (Eq.(3))
-                            } else {
-                                T f0;
-                                phi3(Db, f0, p1, p2);
-                                fP += f0;
-                            }
-                            ar = a * r;
-                            a2 = a * a;
-                            cr = cc * r;
-                            c2 = cc * cc;
-                            ev = hd * a * cc - bh2 * p2 * ih3sq - ahd * ih3sq;
+                            fP += f0;
+                            if (infz) aInf = 1.0;
                         }
+                        const T ar = cv ? a * r : T(0), a2 = cv ? a * a : T(0);
+                        const T cr = cv ? cc * r : T(0), c2 = cv ? cc * cc : T(0);
+                        p1 = cv ? p1 : T(0);
+                        p2 = cv ? p2 : T(0);
+                        const T ev = hd * a * cc - bh2 * p2 * ih3sq - ahd * ih3sq;
                         // cell l-1 -> node l: one rotation per quantity; lane 0 takes the
                         // previous chunk's lane 31 (kept from the last rotation)
                         const T rcr = __shfl_sync(FULL, cr, (lane + 31) & 31);

@@ -90,7 +90,8 @@ __device__ __forceinline__ void res_stamp(unsigned long long* tr) {
 }
 
 // Publish this CTA's NV partials (block-reduced in fixed order) with tag.
-template <int NV>
+// MAXMASK bit k set: value k is a max-reduction (of values >= 0), else a sum.
+template <int NV, unsigned MAXMASK = 0>
 __device__ __forceinline__ void reduce_publish(double (&v)[NV], double* __restrict__ part, unsigned tag) {
     __shared__ double sred[NV][32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -98,20 +99,21 @@ __device__ __forceinline__ void reduce_publish(double (&v)[NV], double* __restri
     for (int k = 0; k < NV; k++) {
         double x = v[k];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
+        for (int o = 16; o > 0; o >>= 1) x = comb<MAXMASK>(k, x, __shfl_xor_sync(FULL, x, o));
         if (lane == 0) sred[k][wid] = x;
     }
     __syncthreads();
     if (threadIdx.x < NV) {
-        double x = 0;
-        for (int w = 0; w < nw; w++) x += sred[threadIdx.x][w];
-        st_relaxed_f64(part + blockIdx.x * NV + threadIdx.x, tag_value(x, tag));
+        const int k = threadIdx.x;
+        double x = sred[k][0];
+        for (int w = 1; w < nw; w++) x = comb<MAXMASK>(k, x, sred[k][w]);
+        st_relaxed_f64(part + blockIdx.x * NV + k, tag_value(x, tag));
     }
 }
 
 // Wait for every CTA's tagged partials and fold them in fixed order (warp k
 // folds value k, identically in every CTA).  Result in out[] (all threads).
-template <int NV>
+template <int NV, unsigned MAXMASK = 0>
 __device__ __forceinline__ void reduce_collect(const double* __restrict__ part, unsigned tag, double (&out)[NV]) {
     constexpr int MS = 8;                    // slots per lane: up to 256 CTAs
     __shared__ double stot[NV];
@@ -139,11 +141,15 @@ __device__ __forceinline__ void reduce_collect(const double* __restrict__ part, 
                     if (value_tag(v[m]) == tag) pending &= ~(1u << m);
                 }
         }
-        double x = 0.0;
+        const bool mx = (MAXMASK >> wid) & 1u;
+        double x = v[0];
 #pragma unroll
-        for (int m = 0; m < MS; m++) x += v[m];
+        for (int m = 1; m < MS; m++) x = mx ? fmax(x, v[m]) : x + v[m];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
+        for (int o = 16; o > 0; o >>= 1) {
+            const double y = __shfl_xor_sync(FULL, x, o);
+            x = mx ? fmax(x, y) : x + y;
+        }
         if (lane == 0) stot[wid] = x;
     }
     __syncthreads();
@@ -245,11 +251,19 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
     pcg_resident_kernel(Geom g, Ctl c, SolveParams sp, int pair, const float* __restrict__ grad,
                         const float* __restrict__ dt, const float* __restrict__ et, float* __restrict__ x,
                         float* __restrict__ xpad, float* __restrict__ pgh, double* __restrict__ gpart,
-                        unsigned* __restrict__ flags, float wi, float wj, unsigned long long* trace = nullptr) {
+                        unsigned* __restrict__ flags, float wi, float wj, float* __restrict__ bcur,
+                        float* __restrict__ bold, int batch, unsigned long long* trace = nullptr) {
     constexpr int NT = RES_THREADS;
     static_assert(K <= 12, "slot masks hold 12 slots per field");
     count_launch(c);
-    if (!c.st[pair].gn_active) return;       // uniform over the grid
+    if (!c.st[pair].gn_active) {             // uniform over the grid: no step, no search
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            c.st[pair].ls_active = 0;
+            if (pair == batch - 1)
+                set_cond(c, COND_LS, any_pair(c, batch, [](volatile PairState* q2) { return q2->ls_active != 0; }));
+        }
+        return;
+    }
     unsigned long long* trk = TRACE ? trace + ((size_t)blockIdx.x * 16 + 15) * 8 : nullptr;   // launch-level stamps
     if constexpr (TRACE) res_stamp(trk);
     extern __shared__ __align__(16) float smem_f[];
@@ -481,21 +495,66 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
             halo_release(flags, res_tag(launch, k_it));            // p_{k+1} published
         }
     }
-    // ---- q = x back to the node layout (each thread reads the pairs it
-    // accumulated itself, so its own L2 adds are ordered before the loads)
+    // ---- q = x back to the node layout, fused with the start of the Armijo
+    // search (A7; the work of trial_init_kernel): g.q, max|q|,
+    // b_old = b, b = b + q (gamma = 1).  The CTA's nodes are contiguous in the
+    // node layout, so this pass walks them in order (coalesced 128-bit
+    // accesses) and gathers q from the padded xpad (fenced after the L2 adds).
+    double agq = 0.0, aqm = 0.0;
+    __threadfence();
+    __syncthreads();
     {
-        FastDiv fdG;
-        fdG.init((unsigned)GPC);
-#pragma unroll
-        for (int k = 0; k < K; k++) {
-            const int q = tid + k * NT;
-            if (q >= nq) continue;
-            const int cl = fdG.div(q);
-            const int l0 = 2 * (q - cl * GPC);
-            const float2 v = k_it > 0 ? __ldcg(xp2 + q) : make_float2(0.f, 0.f);
-            float* xo = x + n0 + (size_t)cl * P + l0;
-            xo[0] = v.x;
-            if (l0 + 1 < P) xo[1] = v.y;
+        const int Nb = ncl * P;              // this CTA's nodes, from n0
+        FastDiv fdP;
+        fdP.init((unsigned)P);
+        auto qval = [&](int t) -> float {    // q at CTA-local node t
+            if (k_it == 0) return 0.f;
+            const int cl = fdP.div(t);
+            return __ldcg(xpad + (size_t)c0 * Pp + (size_t)cl * Pp + (t - cl * P));
+        };
+        // head: nodes before the first 16-byte boundary of the node arrays
+        const int head = min((int)((4 - (n0 & 3)) & 3), Nb);
+        for (int t = tid; t < head; t += NT) {
+            const size_t o = n0 + t;
+            const float qv = qval(t), bv = bcur[o];
+            agq += (double)grad[o] * (double)qv;
+            aqm = fmax(aqm, (double)fabsf(qv));
+            x[o] = qv;
+            bold[o] = bv;
+            bcur[o] = bv + qv;
+        }
+        const int nv = (Nb - head) >> 2;     // aligned float4 groups
+        for (int v = tid; v < nv; v += NT) {
+            const int t = head + 4 * v;
+            const size_t o = n0 + t;
+            const float4 gv = *reinterpret_cast<const float4*>(grad + o);
+            const float4 bv = *reinterpret_cast<const float4*>(bcur + o);
+            const float4 qv = make_float4(qval(t), qval(t + 1), qval(t + 2), qval(t + 3));
+            agq += (double)gv.x * qv.x + (double)gv.y * qv.y + (double)gv.z * qv.z + (double)gv.w * qv.w;
+            aqm = fmax(aqm, (double)fmaxf(fmaxf(fabsf(qv.x), fabsf(qv.y)), fmaxf(fabsf(qv.z), fabsf(qv.w))));
+            *reinterpret_cast<float4*>(x + o) = qv;
+            *reinterpret_cast<float4*>(bold + o) = bv;
+            *reinterpret_cast<float4*>(bcur + o) =
+                make_float4(bv.x + qv.x, bv.y + qv.y, bv.z + qv.z, bv.w + qv.w);
+        }
+        for (int t = head + 4 * nv + tid; t < Nb; t += NT) {   // tail
+            const size_t o = n0 + t;
+            const float qv = qval(t), bv = bcur[o];
+            agq += (double)grad[o] * (double)qv;
+            aqm = fmax(aqm, (double)fabsf(qv));
+            x[o] = qv;
+            bold[o] = bv;
+            bcur[o] = bv + qv;
+        }
+    }
+    {
+        double v4[2] = {agq, aqm}, t4[2];
+        reduce_publish<2, 0x2u>(v4, part0, res_tag(launch, 31));
+        reduce_collect<2, 0x2u>(part0, res_tag(launch, 31), t4);
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            decide_trial(c.st[pair], t4);
+            if (pair == batch - 1)
+                set_cond(c, COND_LS, any_pair(c, batch, [](volatile PairState* q2) { return q2->ls_active != 0; }));
         }
     }
     if constexpr (TRACE) res_stamp(trk + 3);

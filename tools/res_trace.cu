@@ -21,7 +21,7 @@ int main(int argc, char** argv) {
     g.Nc = g.ncol * n3; g.Nn = g.ncol * g.P; g.ps = g.Nn; g.i0 = 0; g.n1g = n1; g.slab = 0;
     g.h1 = g.h2 = g.h3 = 1.25; g.hd = 1.25 * 1.25 * 1.25; g.alpha = 300; g.beta = 1e-4;
     g.ahd = g.alpha * g.hd; g.bh2 = 0.5e-4 * g.hd;
-    g.ih1sq = g.ih2sq = g.ih3sq = 1 / (1.25 * 1.25); g.ih3 = 1 / 1.25;
+    g.ih1sq = g.ih2sq = g.ih3sq = 1 / (1.25 * 1.25); g.ih3 = 1 / 1.25; geom_finish(g);
     int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
     const int G = nsm, NT = RES_THREADS, K = 12;
     const long long ncl = (g.ncol + G - 1) / G, knt = (long long)K * NT;
@@ -37,6 +37,7 @@ int main(int argc, char** argv) {
     float *dt, *et, *grad, *x, *pgh, *xpad;
     cudaMalloc(&dt, Nn * 4); cudaMalloc(&et, Nn * 4); cudaMalloc(&grad, Nn * 4); cudaMalloc(&x, Nn * 4);
     cudaMalloc(&xpad, (size_t)g.ncol * res_pad(g.P) * 4);
+    float *bb, *bo; cudaMalloc(&bb, Nn * 4); cudaMalloc(&bo, Nn * 4); cudaMemset(bb, 0, Nn * 4);
     const float wi = (float)(g.ahd * g.ih1sq), wj = (float)(g.ahd * g.ih2sq);
     size_t ghost = res_ghost_pair_floats(g) + res_ghost_slack_floats(12);
     cudaMalloc(&pgh, ghost * 4); cudaMemset(pgh, 0, ghost * 4);
@@ -67,12 +68,12 @@ int main(int argc, char** argv) {
     for (int rep = 0; rep < 3; rep++) {
         cudaEventRecord(e0);
         cudaLaunchKernelEx(&cfg, pcg_resident_kernel<12, true>, g, c, sp, 0, (const float*)grad, (const float*)dt,
-                           (const float*)et, x, xpad, pgh, part, flags, wi, wj, (unsigned long long*)nullptr);
+                           (const float*)et, x, xpad, pgh, part, flags, wi, wj, bb, bo, 1, (unsigned long long*)nullptr);
         cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms_notrace, e0, e1);
     }
     cudaEventRecord(e0);
     cudaLaunchKernelEx(&cfg, pcg_resident_kernel<12, true, true>, g, c, sp, 0, (const float*)grad, (const float*)dt,
-                       (const float*)et, x, xpad, pgh, part, flags, wi, wj, trace);
+                       (const float*)et, x, xpad, pgh, part, flags, wi, wj, bb, bo, 1, trace);
     cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms_trace, e0, e1);
     printf("err=%s  kernel %.1f us (untraced), %.1f us (traced), grid %d x %d, K %d\n",
            cudaGetErrorString(cudaGetLastError()), ms_notrace * 1e3, ms_trace * 1e3, G, NT, K);
