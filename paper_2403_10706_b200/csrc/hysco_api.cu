@@ -273,7 +273,10 @@ struct Runner {
         if (err != cudaSuccess || !graph) return;
         cudaGraphConditionalHandle h;
         err = cudaGraphConditionalHandleCreate(&h, cur, 0, 0);
-        if (err == cudaSuccess) c->ctl.h[slot] = h;
+        if (err == cudaSuccess) {
+            c->ctl.h[slot] = h;
+            c->ctl.live |= 1u << slot;
+        }
     }
     void loop(int slot, const std::function<void()>& body) {
         if (err != cudaSuccess) return;
@@ -325,7 +328,7 @@ static void launch_resident(hysco_ctx c, const SolveParams& sp, int pair, float*
     at[0].id = cudaLaunchAttributeCooperative;
     at[0].val.cooperative = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 1;   // co-residency of all CTAs (the spin waits rely on it)
     float* const* B = reinterpret_cast<float* const*>(c->buf);
     const int nb = c->cfg.batch;
     if (sp.fixed) {
@@ -698,24 +701,54 @@ static hysco_status run_slab_path(std::vector<hysco_ctx>& R, CommBase* comm, int
 
 // GN-PCG solve on buffer B_B, the structure of DESIGN.md "Solve graph".
 template <typename T>
+static void pcg_step(Runner& r, const SolveParams& sp, bool unrolled) {
+    hysco_ctx c = r.c;
+    if (c->resident) {   // PCG + the Armijo start (trial_init) in one launch per pair
+        r.seq([&] {
+            for (int p = 0; p < c->cfg.batch; p++)
+                launch_resident(c, sp, p, reinterpret_cast<float*>(L<T>::b(c, B_B)),
+                                reinterpret_cast<float*>(L<T>::b(c, B_BOLD)));
+        });
+    } else if (unrolled) {   // fixed count: max_pcg iterations, kernels of finished pairs exit early
+        r.seq([&] {
+            L<T>::pcg_init(c);
+            for (int k = 0; k < sp.max_pcg; k++) L<T>::pcg_iter(c, sp);
+            L<T>::trial_init(c);
+        });
+    } else {
+        r.handle(COND_PCG);
+        r.seq([&] { L<T>::pcg_init(c); });
+        r.loop(COND_PCG, [&] { r.seq([&] { L<T>::pcg_iter(c, sp); }); });
+        r.seq([&] { L<T>::trial_init(c); });
+    }
+}
+
+// Fixed iteration counts (parity / timing, R14-R16) are unrolled in the graph:
+// max_gn x (PCG step, first Armijo trial) with only the Armijo retries in a
+// conditional WHILE node (usually skipped).  Each conditional node costs
+// ~20-40 us of device-side scheduling on B200 (tools/timeline.py: 3T step
+// gaps 617 -> 82 us), which the unrolled form avoids; kernels of finished
+// pairs exit early.
+// HYSCO_GRAPH_LOOPS=1 forces the WHILE-loop form.
+template <typename T>
 static void gn_sequence(Runner& r, const SolveParams& sp) {
     hysco_ctx c = r.c;
+    const char* e = getenv("HYSCO_GRAPH_LOOPS");
+    if (sp.fixed && r.graph && !(e && e[0] == '1')) {
+        r.seq([&] { L<T>::eval(c, sp, EVAL_GN_START, L<T>::b(c, B_B)); });
+        for (int k = 0; k < sp.max_gn; k++) {
+            pcg_step<T>(r, sp, true);
+            r.handle(COND_LS);
+            r.seq([&] { L<T>::ls_body(c, sp); });                              // first trial (gamma = 1)
+            r.loop(COND_LS, [&] { r.seq([&] { L<T>::ls_body(c, sp); }); });   // halvings, restore
+        }
+        return;
+    }
     r.handle(COND_GN);
     r.seq([&] { L<T>::eval(c, sp, EVAL_GN_START, L<T>::b(c, B_B)); });
     r.loop(COND_GN, [&] {
-        r.handle(COND_PCG);
         r.handle(COND_LS);
-        if (c->resident) {   // PCG + the Armijo start (trial_init) in one launch per pair
-            r.seq([&] {
-                for (int p = 0; p < c->cfg.batch; p++)
-                    launch_resident(c, sp, p, reinterpret_cast<float*>(L<T>::b(c, B_B)),
-                                    reinterpret_cast<float*>(L<T>::b(c, B_BOLD)));
-            });
-        } else {
-            r.seq([&] { L<T>::pcg_init(c); });
-            r.loop(COND_PCG, [&] { r.seq([&] { L<T>::pcg_iter(c, sp); }); });
-            r.seq([&] { L<T>::trial_init(c); });
-        }
+        pcg_step<T>(r, sp, false);
         r.loop(COND_LS, [&] { r.seq([&] { L<T>::ls_body(c, sp); }); });   // its last eval sets COND_GN
     });
 }
@@ -755,6 +788,7 @@ static hysco_status run_path(hysco_ctx ctx, const GraphKey& key, void* b_io, voi
             r.err = cudaGraphCreate(&ctx->graph, 0);
             r.cur = ctx->graph;
             ctx->ctl.use_graph = 1;
+            ctx->ctl.live = 0;
             body(r);
             ctx->ctl.use_graph = 0;
             if (r.err == cudaSuccess) r.err = cudaGraphInstantiate(&ctx->exec, ctx->graph, 0);

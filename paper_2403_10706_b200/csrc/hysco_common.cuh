@@ -90,6 +90,7 @@ struct Ctl {
     unsigned* dcond;               // [NCOND] loop conditions (mirrors of the graph handles)
     cudaGraphConditionalHandle h[NCOND];
     int use_graph;                 // 1: set graph conditionals from device code
+    unsigned live;                 // bit k: h[k] belongs to the graph being built (else only dcond is set)
     int part_stride;               // doubles per pair in `part`
     int defer;                     // 1 (multi-rank): last blocks store pair totals in `red`,
                                    //   decisions run in decide_kernel after the allreduce
@@ -105,7 +106,7 @@ __device__ __forceinline__ void count_launch(const Ctl& c) {
 
 __device__ __forceinline__ void set_cond(const Ctl& c, int slot, unsigned v) {
     c.dcond[slot] = v;
-    if (c.use_graph) cudaGraphSetConditional(c.h[slot], v);
+    if (c.use_graph && ((c.live >> slot) & 1u)) cudaGraphSetConditional(c.h[slot], v);
 }
 
 template <unsigned MAXMASK>
