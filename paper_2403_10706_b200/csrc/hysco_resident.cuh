@@ -424,6 +424,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
             if constexpr (TRACE) res_stamp(tr ? tr + 2 : nullptr);
             double v1[1] = {(double)fpq}, t1[1];
             reduce_publish<1>(v1, part1, res_tag(launch, k_it));
+            if constexpr (TRACE) res_stamp(tr ? tr + 7 : nullptr);
             reduce_collect<1>(part1, res_tag(launch, k_it), t1);
             if constexpr (TRACE) res_stamp(tr ? tr + 3 : nullptr);
             if (t1[0] <= 0.0) break;                  // breakdown (oracle pcg(): keep x)

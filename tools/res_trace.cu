@@ -65,7 +65,7 @@ int main(int argc, char** argv) {
     cfg.attrs = at; cfg.numAttrs = 1;
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     float ms_notrace = 0, ms_trace = 0;
-    for (int rep = 0; rep < 3; rep++) {
+    for (int rep = 0; rep < 7; rep++) {
         cudaEventRecord(e0);
         cudaLaunchKernelEx(&cfg, pcg_resident_kernel<12, true>, g, c, sp, 0, (const float*)grad, (const float*)dt,
                            (const float*)et, x, xpad, pgh, part, flags, wi, wj, bb, bo, 1, (unsigned long long*)nullptr);
@@ -79,25 +79,26 @@ int main(int argc, char** argv) {
            cudaGetErrorString(cudaGetLastError()), ms_notrace * 1e3, ms_trace * 1e3, G, NT, K);
     std::vector<unsigned long long> ht((size_t)G * 16 * 8);
     cudaMemcpy(ht.data(), trace, ht.size() * 8, cudaMemcpyDeviceToHost);
-    const char* names[9] = {"iter start", "local Hp + p-barrier", "remote Hp done", "reduce #1 done",
-                            "U-phase, arrive #2", "x upd + reduce #2", "D-phase, arrive #3", "(unused)",
-                            "next iter start"};
-    // per phase k -> k+1: span = max_cta(t[k+1]) - min_cta(t[k]); cta = mean over CTAs of (t[k+1]-t[k])
-    for (int k = 0; k < 7; k++) {
+    // stamp slots in time order within an iteration; the last phase ends at the next iteration's slot 0
+    const int order[8] = {0, 1, 2, 7, 3, 4, 5, 6};
+    const char* names[8] = {"iter start", "local Hp + halo wait", "remote Hp", "publish #1 (p.Hp)",
+                            "collect #1", "U-phase + publish #2", "x upd + collect #2", "D-phase + release"};
+    // per phase: span = max_cta(end) - min_cta(start); per-CTA mean/max/min of (end - start)
+    for (int k = 0; k < 8; k++) {
         double span = 0, mean_cta = 0, max_cta = 0, min_cta = 1e30;
         int nit = 0;
         for (int it = 1; it < 9; it++) {
             unsigned long long mn = ~0ull, mx = 0;
-            double acc = 0, mxd = 0, mnd = 1e30;
+            double acc = 0, mxd = 0;
             for (int b = 0; b < G; b++) {
-                unsigned long long a = ht[((size_t)b * 16 + it) * 8 + k];
-                unsigned long long z = k < 6 ? ht[((size_t)b * 16 + it) * 8 + k + 1] : ht[((size_t)b * 16 + it + 1) * 8];
+                unsigned long long a = ht[((size_t)b * 16 + it) * 8 + order[k]];
+                unsigned long long z = k < 7 ? ht[((size_t)b * 16 + it) * 8 + order[k + 1]] : ht[((size_t)b * 16 + it + 1) * 8];
                 mn = std::min(mn, a); mx = std::max(mx, z);
-                double d = (double)(z - a); acc += d; mxd = std::max(mxd, d); mnd = std::min(mnd, d);
+                double d = (double)(z - a); acc += d; mxd = std::max(mxd, d); min_cta = std::min(min_cta, d);
             }
-            span += (double)(mx - mn); mean_cta += acc / G; max_cta += mxd; min_cta = std::min(min_cta, mnd); nit++;
+            span += (double)(mx - mn); mean_cta += acc / G; max_cta += mxd; nit++;
         }
-        printf("%-22s -> %-22s span %7.2f us | per-CTA mean %7.2f max %7.2f min %7.2f us\n", names[k], names[k == 6 ? 8 : k + 1],
+        printf("%-24s span %7.2f us | per-CTA mean %7.2f max %7.2f min %7.2f us\n", names[k],
                span / nit / 1e3, mean_cta / nit / 1e3, max_cta / nit / 1e3, min_cta / 1e3);
     }
     {   // launch-level stamps (slot 15): start, init loads done, init reduce done, loop done
