@@ -212,9 +212,9 @@ struct L {
         NCH_SWITCH(c->nch, hess_diag_kernel<T, NCH><<<dim3(c->gx_nodes, c->cfg.batch), 256, 0, c->stream>>>(
                                c->g, c->ctl, b(c, B_DT), out));
     }
-    static void apply(hysco_ctx c, const T* bsrc, T* Tp, T* Tm) {
+    static void apply(hysco_ctx c, const T* bsrc, T* Tp, T* Tm, T* bout = nullptr) {
         apply_kernel<T><<<dim3(c->gx_apply, c->cfg.batch), 256, c->smem_eval, c->stream>>>(
-            c->g, c->ctl, (const T*)c->Ip, (const T*)c->Im, bsrc, Tp, Tm);
+            c->g, c->ctl, (const T*)c->Ip, (const T*)c->Im, bsrc, Tp, Tm, bout);
     }
     // OT init (+blur, guard) into buffer B_B
     static void ot(hysco_ctx c, const SolveParams& sp, int blur) {
@@ -228,9 +228,10 @@ struct L {
             const double e = exp(-0.5), w0 = e / (1.0 + 2.0 * e), w1 = 1.0 / (1.0 + 2.0 * e);
             blur_axis_kernel<T, 1><<<gn, 256, 0, c->stream>>>(c->g, c->ctl, 0, w0, w1, b(c, B_TMP), b(c, B_R));
             blur_axis_kernel<T, 1><<<gn, 256, 0, c->stream>>>(c->g, c->ctl, 1, w0, w1, b(c, B_R), b(c, B_P));
-            blur_axis_kernel<T, 1><<<gn, 256, 0, c->stream>>>(c->g, c->ctl, 2, w0, w1, b(c, B_P), b(c, B_B));
+            blur_pe_guard_kernel<T><<<gn, 256, 0, c->stream>>>(c->g, c->ctl, sp, w0, w1, b(c, B_P), b(c, B_B));
+        } else {
+            guard_max_kernel<T, 1><<<gn, 256, 0, c->stream>>>(c->g, c->ctl, sp, b(c, B_B));
         }
-        guard_max_kernel<T, 1><<<gn, 256, 0, c->stream>>>(c->g, c->ctl, sp, b(c, B_B));
         guard_scale_kernel<T, 1><<<gn, 256, 0, c->stream>>>(c->g, c->ctl, b(c, B_B));
     }
 };
@@ -769,8 +770,8 @@ static hysco_status run_path(hysco_ctx ctx, const GraphKey& key, void* b_io, voi
             if (key.kind == 1) {
                 cudaMemcpyAsync(b_io, ctx->buf[B_B], nb, cudaMemcpyDeviceToDevice, ctx->stream);
             } else {
-                if (Tp || Tm) L<T>::apply(ctx, L<T>::b(ctx, B_B), (T*)Tp, (T*)Tm);
-                if (b_out) cudaMemcpyAsync(b_out, ctx->buf[B_B], nb, cudaMemcpyDeviceToDevice, ctx->stream);
+                if (Tp || Tm) L<T>::apply(ctx, L<T>::b(ctx, B_B), (T*)Tp, (T*)Tm, (T*)b_out);   // also copies b out
+                else if (b_out) cudaMemcpyAsync(b_out, ctx->buf[B_B], nb, cudaMemcpyDeviceToDevice, ctx->stream);
             }
         });
     };

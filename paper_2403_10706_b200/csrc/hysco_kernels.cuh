@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(256, 4) eval_kernel(Geom g, Ctl c, SolveParams
 template <typename T>
 __global__ void __launch_bounds__(256) apply_kernel(Geom g, Ctl c, const T* __restrict__ Ip,
                                                     const T* __restrict__ Im, const T* __restrict__ bb,
-                                                    T* __restrict__ Tp, T* __restrict__ Tm) {
+                                                    T* __restrict__ Tp, T* __restrict__ Tm, T* __restrict__ bout) {
     count_launch(c);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwb = blockDim.x >> 5;
@@ -453,7 +453,11 @@ __global__ void __launch_bounds__(256) apply_kernel(Geom g, Ctl c, const T* __re
             sIp[k] = Ip[oc + k];
             sIm[k] = Im[oc + k];
         }
-        for (int l = lane; l < P; l += 32) sb[l] = bb[on + l];
+        for (int l = lane; l < P; l += 32) {
+            const T v = bb[on + l];
+            sb[l] = v;
+            if (bout) bout[on + l] = v;   // the solve's b output (replaces a device copy)
+        }
         __syncwarp();
         for (int k = lane; k < n3; k += 32) {
             const T b0 = sb[k], b1 = sb[k + 1];
@@ -553,13 +557,14 @@ __global__ void __launch_bounds__(256) ot_column_kernel(Geom g, Ctl c, const T* 
             tp += __shfl_xor_sync(FULL, tp, o);
             tm += __shfl_xor_sync(FULL, tm, o);
         }
+        const double itp = 1.0 / tp, itm = 1.0 / tm;   // unit mass per column
         double carp = 0, carm = 0;
         for (int base = 0; base < n3; base += 32) {
             const int k = base + lane;
             double wp = 0, wm = 0;
             if (k < n3) {
-                wp = ((double)ip[k] + shift) / tp;
-                wm = ((double)im[k] + shift) / tm;
+                wp = ((double)ip[k] + shift) * itp;
+                wm = ((double)im[k] + shift) * itm;
             }
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -586,8 +591,12 @@ __global__ void __launch_bounds__(256) ot_column_kernel(Geom g, Ctl c, const T* 
         __syncwarp();
         for (int l = lane; l < P; l += 32) {
             const double rp = Cp[l], rm = Cm[l];
-            const double Tpl = 0.5 * (ot_quantile(Cp, n3, rp) + ot_quantile(Cm, n3, rp));   // T+ = Q_half o C+
-            const double Tml = 0.5 * (ot_quantile(Cp, n3, rm) + ot_quantile(Cm, n3, rm));   // T- = Q_half o C-
+            // Q+(C+(l)) = l exactly when C+(l-1) < C+(l) (the min-definition then
+            // selects x* = l); likewise Q-(C-(l)); else the search decides
+            const double qpp = (l > 0 && Cp[l - 1] < rp) ? (double)l : ot_quantile(Cp, n3, rp);
+            const double qmm = (l > 0 && Cm[l - 1] < rm) ? (double)l : ot_quantile(Cm, n3, rm);
+            const double Tpl = 0.5 * (qpp + ot_quantile(Cm, n3, rp));   // T+ = Q_half o C+
+            const double Tml = 0.5 * (ot_quantile(Cp, n3, rm) + qmm);   // T- = Q_half o C-
             bo[l] = (T)(g.h3 * (Tml - Tpl) * 0.5);
         }
         __syncwarp();

@@ -498,6 +498,38 @@ __global__ void __launch_bounds__(256) guard_max_kernel(Geom g, Ctl c, SolvePara
     decide_guard(sp, c.st[pair], tot);
 }
 
+// Last blur pass (along PE, periodic) fused with the guard's max |D b0|
+// (R10): each lane forms the blurred node l and l + 1 of its column directly
+// (the difference never needs another lane's output).  Single-GPU path.
+template <typename T>
+__global__ void __launch_bounds__(256) blur_pe_guard_kernel(Geom g, Ctl c, SolveParams sp, double w0, double w1,
+                                                            const T* __restrict__ in, T* __restrict__ out) {
+    count_launch(c);
+    const int lane = threadIdx.x & 31;
+    const int pair = blockIdx.y;
+    const size_t po = (size_t)pair * g.ps;
+    const T a = (T)w0, mid = (T)w1;
+    const int P = g.P;
+    double mx = 0.0;
+    HYSCO_FOR_COLS(g) {
+        const T* cc = in + po + (size_t)col * P;
+        T* oc = out + po + (size_t)col * P;
+        for (int l = lane; l < P; l += 32) {
+            const int lm = l == 0 ? P - 1 : l - 1, lp = l == P - 1 ? 0 : l + 1, lq = lp == P - 1 ? 0 : lp + 1;
+            const T v = a * cc[lm] + mid * cc[l] + a * cc[lp];
+            oc[l] = v;
+            if (l < g.n3) {
+                const T v1 = a * cc[l] + mid * cc[lp] + a * cc[lq];   // blurred node l + 1
+                mx = fmax(mx, fabs((double)(v1 - v)) / g.h3);
+            }
+        }
+    }
+    double v[1] = {mx}, tot[1];
+    if (!pair_reduce<1, 0x1u>(c, v, tot)) return;
+    if (threadIdx.x != 0) return;
+    decide_guard(sp, c.st[pair], tot);
+}
+
 template <typename T, int NCH>
 __global__ void __launch_bounds__(256) guard_scale_kernel(Geom g, Ctl c, T* __restrict__ b) {
     count_launch(c);

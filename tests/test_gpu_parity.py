@@ -185,11 +185,12 @@ def test_correct_pipeline_parity(pair, dtype):
     assert rel(c.np(b)[0], bref) <= tol
     assert rel(c.np(Tp)[0], Tpr) <= tol and rel(c.np(Tm)[0], Tmr) <= tol
     n = H.hysco_last_launch_count(c.ctx)
-    # 7 OT kernels + 1 eval + 10 x (PCG + eval) + apply and one more eval per Armijo
+    # 6 OT kernels (min/max, columns, 2 blur passes, PE blur + guard max, guard scale)
+    # + 1 eval + 10 x (PCG + eval) + apply and one more eval per Armijo
     # halving, where PCG is pcg_init + 10 x (matvec, update, dir) + trial_init streaming,
     # or 1 launch (PCG and the Armijo start) when the resident PCG applies
     pcg = 32 if n > 200 else 1
-    assert n == 7 + 1 + 10 * (pcg + 1) + 1 + reps[0]["ls_halvings"]
+    assert n == 6 + 1 + 10 * (pcg + 1) + 1 + reps[0]["ls_halvings"]
     c.close()
 
 
