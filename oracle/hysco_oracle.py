@@ -288,23 +288,80 @@ def hess_diag(st):
     return st.hd * dJ + st.alpha * st.hd * dL + st.beta * 0.5 * st.hd * dB
 
 
+def hess_block_pe(st):
+    """Per-PE-column tridiagonal block of H_J: the block-diagonal preconditioner
+    "more accurate (yet also more expensive)" than Jacobi (SURVEY §8(f)
+    NEXT-1, reading R20 in DESIGN.md).
+
+    Column block of H_J = its entries between nodes of one PE column.  The
+    in-plane Laplacian couples different columns only, so inside a column it
+    contributes its diagonal alone.  Returns (d, e):
+      d = diag(H_J) (hess_diag, the Jacobi diagonal);
+      e[..., l] = H_J[l, l+1] within the column, l = 0..n3-1:
+        hd (J_r^T J_r)[l, l+1] = hd a_l c_l   (cell l holds a_l at l, c_l at l+1)
+        alpha hd (D3^T D3 / h3^2)[l, l+1] = -alpha hd / h3^2
+        beta hd/2 (D^T diag(phi'') D)[l, l+1] = -beta hd/2 phi''_l / h3^2.
+    """
+    h3 = st.h[2]
+    a = st.g / 2.0 - st.s / h3
+    c = st.g / 2.0 + st.s / h3
+    e = st.hd * a * c - st.alpha * st.hd / h3 ** 2 - st.beta * 0.5 * st.hd * st.d2phi / h3 ** 2
+    return hess_diag(st), e
+
+
+def solve_tridiag_pe(d, e, r):
+    """Solve T z = r for every PE column, T = tridiag(e, d, e) (symmetric,
+    positive definite), by the Thomas algorithm (textbook LU without pivoting):
+    forward  m_0 = d_0, m_l = d_l - e_{l-1}^2 / m_{l-1},
+             y_0 = r_0 / m_0, y_l = (r_l - e_{l-1} y_{l-1}) / m_l;
+    backward z_{n} = y_{n}, z_l = y_l - (e_l / m_l) z_{l+1}."""
+    n = d.shape[-1]
+    m = np.empty_like(d)
+    y = np.empty_like(r)
+    m[..., 0] = d[..., 0]
+    y[..., 0] = r[..., 0] / m[..., 0]
+    for l in range(1, n):
+        m[..., l] = d[..., l] - e[..., l - 1] ** 2 / m[..., l - 1]
+        y[..., l] = (r[..., l] - e[..., l - 1] * y[..., l - 1]) / m[..., l]
+    z = np.empty_like(r)
+    z[..., n - 1] = y[..., n - 1]
+    for l in range(n - 2, -1, -1):
+        z[..., l] = y[..., l] - (e[..., l] / m[..., l]) * z[..., l + 1]
+    return z
+
+
+def make_precond(st, kind="jacobi"):
+    """The PCG preconditioner solve r -> z = M^{-1} r: "jacobi" (P:198-199,
+    R13) or "block" (the per-PE-column tridiagonal block, R20)."""
+    if kind == "jacobi":
+        Md = hess_diag(st)
+        return lambda r: r / Md
+    if kind == "block":
+        d, e = hess_block_pe(st)
+        return lambda r: solve_tridiag_pe(d, e, r)
+    raise ValueError(kind)
+
+
 # ---------------------------------------------------------------------------
 # PCG (P:196-199): up to maxit iterations, stop if relative residual < tol
 # ---------------------------------------------------------------------------
 
 
 def pcg(Hmul, rhs, Mdiag, maxit=10, tol=0.1, fixed=False):
-    """Jacobi-preconditioned CG (Hestenes-Stiefel / Saad Alg. 9.1), x0 = 0 (R14).
+    """Preconditioned CG (Hestenes-Stiefel / Saad Alg. 9.1), x0 = 0 (R14).
 
-    Returns (x, iterations, matvecs, final relative residual ||r||/||r0||).
-    In fixed mode all maxit iterations run (parity / timing mode, R14).
+    Mdiag: the Jacobi diagonal (z = r / Mdiag), or a callable z = M^{-1}(r)
+    (make_precond).  Returns (x, iterations, matvecs, final relative residual
+    ||r||/||r0||).  In fixed mode all maxit iterations run (parity / timing
+    mode, R14).
     """
+    Minv = Mdiag if callable(Mdiag) else (lambda v: v / Mdiag)
     x = np.zeros_like(rhs)
     r = rhs.copy()
     r0 = float(np.linalg.norm(r))
     if r0 == 0.0:
         return x, 0, 0, 0.0
-    z = r / Mdiag
+    z = Minv(r)
     p = z.copy()
     rz = float(np.sum(r * z))
     it = 0
@@ -321,7 +378,7 @@ def pcg(Hmul, rhs, Mdiag, maxit=10, tol=0.1, fixed=False):
         rel = float(np.linalg.norm(r)) / r0
         if not fixed and rel < tol:
             break
-        z = r / Mdiag
+        z = Minv(r)
         rz_new = float(np.sum(r * z))
         p = z + (rz_new / rz) * p
         rz = rz_new
@@ -457,13 +514,15 @@ STOP_MAXITER, STOP_GRAD, STOP_DJ, STOP_DB, STOP_LSFAIL, STOP_INFEASIBLE = 0, 1, 
 
 def gauss_newton(Ip, Im, b0, h, alpha=ALPHA_DEFAULT, beta=BETA_DEFAULT, max_gn=10,
                  max_pcg=10, pcg_tol=0.1, fixed=True, c1=1e-4, ls_max=10,
-                 tol_grad_rel=1e-2, tol_dJ_rel=1e-4, tol_db_rel=1e-3, log=None, armijo=True):
+                 tol_grad_rel=1e-2, tol_dJ_rel=1e-4, tol_db_rel=1e-3, log=None, armijo=True,
+                 precond="jacobi"):
     """b_{k+1} = b_k + gamma_k q_k with H_J q_k = -grad J (Eq.(7)).
 
     fixed=True: exactly max_gn GN steps of exactly max_pcg PCG iterations
     (parity / timing mode, R14, R16); fixed=False: the paper's stopping rules
     with DESIGN.md's tolerances (R16).  armijo=False accepts the full step
     unless infeasible (halving only for feasibility): the parity mode of R15.
+    precond: "jacobi" (the paper's default) or "block" (R20).
     """
     b = np.asarray(b0, np.float64).copy()
     st = evaluate(Ip, Im, b, h, alpha, beta)
@@ -475,7 +534,7 @@ def gauss_newton(Ip, Im, b0, h, alpha=ALPHA_DEFAULT, beta=BETA_DEFAULT, max_gn=1
         return b, st, rep
     g0 = float(np.linalg.norm(st.grad))
     for it in range(max_gn):
-        M = hess_diag(st)
+        M = make_precond(st, precond)
         q, npcg, nmv, rel = pcg(lambda v: hessvec(st, v), -st.grad, M, max_pcg, pcg_tol, fixed)
         rep["h_evals"] += nmv
         rep["pcg_iters"] += npcg
@@ -517,11 +576,11 @@ def gauss_newton(Ip, Im, b0, h, alpha=ALPHA_DEFAULT, beta=BETA_DEFAULT, max_gn=1
 
 
 def correct_pair(Ip, Im, h, alpha=ALPHA_DEFAULT, beta=BETA_DEFAULT, max_gn=10, max_pcg=10,
-                 fixed=True, blur=True, eps=1e-3, armijo=True):
+                 fixed=True, blur=True, eps=1e-3, armijo=True, precond="jacobi"):
     """The whole path: OT init (+blur, guard) -> GN-PCG -> Jacobian-modulation apply."""
     b0, _ = ot_init(Ip, Im, h[2], eps=eps, blur=blur)
     b, st, rep = gauss_newton(Ip, Im, b0, h, alpha, beta, max_gn=max_gn, max_pcg=max_pcg,
-                              fixed=fixed, armijo=armijo)
+                              fixed=fixed, armijo=armijo, precond=precond)
     Tp, Tm = apply_correction(Ip, Im, b, h[2])
     return b0, b, Tp, Tm, rep
 
