@@ -98,7 +98,14 @@ typedef struct {
                                 0: accept the full step unless infeasible, halving only for
                                 feasibility — the parity mode of DESIGN.md R15, which keeps
                                 the accept decision free of fp32-vs-fp64 rounding of J      */
+    int32_t precond;         /* HYSCO_PRECOND_JACOBI (default): z = r / diag(H_J);
+                                HYSCO_PRECOND_PE_BLOCK: z = B^{-1} r with B the per-PE-column
+                                tridiagonal blocks of H_J, the block-diagonal preconditioner
+                                named in P:200 (R20).  PE_BLOCK runs the streaming
+                                PCG kernels and is not available on slab contexts            */
 } hysco_solve_opts;
+
+enum { HYSCO_PRECOND_JACOBI = 0, HYSCO_PRECOND_PE_BLOCK = 1 };
 
 enum { HYSCO_STOP_MAXITER = 0, HYSCO_STOP_GRAD = 1, HYSCO_STOP_DJ = 2, HYSCO_STOP_DB = 3,
        HYSCO_STOP_LSFAIL = 4, HYSCO_STOP_INFEASIBLE = 5 };
@@ -147,6 +154,13 @@ HYSCO_API hysco_status hysco_hessvec(hysco_ctx ctx, const void* d_q, void* d_Hq)
 
 /* diag(H_J), the Jacobi preconditioner, device nodes. */
 HYSCO_API hysco_status hysco_hess_diag(hysco_ctx ctx, void* d_diag);
+
+/* Preconditioner solve z = M^{-1} r at the b of the last successful
+ * objective_grad (else HYSCO_ERR_STATE): kind = HYSCO_PRECOND_JACOBI (M =
+ * diag(H_J)) or HYSCO_PRECOND_PE_BLOCK (M = the per-PE-column
+ * tridiagonal blocks of H_J; Thomas algorithm per column).  d_r, d_z:
+ * device nodes [batch][n1][n2][n3+1]; must not alias.  Not on slab contexts. */
+HYSCO_API hysco_status hysco_precond_solve(hysco_ctx ctx, int kind, const void* d_r, void* d_z);
 
 /* Gauss-Newton with Jacobi-PCG and Armijo from b (in/out, device
  * nodes).  reports: host array [batch] (may be NULL).  The whole solve runs as

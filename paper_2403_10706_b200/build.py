@@ -6,13 +6,28 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 SRC = os.path.join(PKG, "csrc", "hysco_api.cu")
 DEPS = [os.path.join(PKG, "csrc", f) for f in sorted(os.listdir(os.path.join(PKG, "csrc")))] + \
-       [os.path.join(ROOT, "include", "hysco.h")]
+       [os.path.join(ROOT, "include", "hysco.h"), os.path.abspath(__file__)]
 LIB = os.path.join(PKG, "libhysco.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "-shared",
          "-I" + os.path.join(ROOT, "include")]
+
+
+def nccl_dirs():
+    """torch's bundled NCCL (include, lib): libhysco links the same libnccl.so.2
+    torch loads, so the process holds one NCCL whichever library loads first.
+    Falls back to the system NCCL when the wheel is absent."""
+    try:
+        import nvidia.nccl as nn
+        base = list(nn.__path__)[0]
+        inc, libd = os.path.join(base, "include"), os.path.join(base, "lib")
+        if os.path.exists(os.path.join(libd, "libnccl.so.2")) and os.path.exists(os.path.join(inc, "nccl.h")):
+            return inc, libd
+    except Exception:
+        pass
+    return None, None
 
 
 def needs_build():
@@ -25,7 +40,9 @@ def needs_build():
 def build(force=False, verbose=False):
     """Compile csrc/ into paper_2403_10706_b200/libhysco.so; returns the path."""
     if force or needs_build():
-        cmd = [NVCC] + FLAGS + ["-o", LIB + ".tmp", SRC, "-lnccl"]
+        inc, libd = nccl_dirs()
+        nccl = ["-I" + inc, "-L" + libd, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + libd] if inc else ["-lnccl"]
+        cmd = [NVCC] + FLAGS + ["-o", LIB + ".tmp", SRC] + nccl
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)

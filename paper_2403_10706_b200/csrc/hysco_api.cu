@@ -22,7 +22,8 @@ using namespace hysco;
 
 namespace {
 
-enum { B_B = 0, B_BOLD, B_GRAD, B_DT, B_ET, B_X, B_R, B_P, B_HP, B_TMP, NBUF };
+// B_W, B_F: factors of the block preconditioner (R20); B_TMP also holds its z during a solve
+enum { B_B = 0, B_BOLD, B_GRAD, B_DT, B_ET, B_X, B_R, B_P, B_HP, B_TMP, B_W, B_F, NBUF };
 
 struct GraphKey {
     int kind;                 // 1 = solve, 2 = correct
@@ -131,6 +132,7 @@ static SolveParams to_params(const hysco_solve_opts& o, const hysco_ot_opts& t) 
     s.tol_dJ_rel = o.tol_dJ_rel;
     s.tol_db_rel = o.tol_db_rel;
     s.armijo = o.armijo ? 1 : 0;
+    s.precond = o.precond;
     s.feas_cap = t.feas_cap;
     s.ot_eps = t.eps;
     return s;
@@ -140,6 +142,10 @@ static hysco_status check_opts(hysco_ctx ctx, const hysco_solve_opts& o, const h
     if (o.max_gn < 0 || o.max_pcg < 1 || o.ls_max < 1 || !(o.pcg_rtol >= 0) || !(o.armijo_c1 >= 0))
         return set_err(ctx, HYSCO_ERR_ARG, "bad hysco_solve_opts");
     if (!(t.eps >= 0) || !(t.feas_cap > 0)) return set_err(ctx, HYSCO_ERR_ARG, "bad hysco_ot_opts");
+    if (o.precond != HYSCO_PRECOND_JACOBI && o.precond != HYSCO_PRECOND_PE_BLOCK)
+        return set_err(ctx, HYSCO_ERR_ARG, "bad hysco_solve_opts.precond");
+    if (o.precond == HYSCO_PRECOND_PE_BLOCK && ctx->g.slab)
+        return set_err(ctx, HYSCO_ERR_ARG, "the block preconditioner is not available on slab contexts");
     return HYSCO_OK;
 }
 
@@ -198,6 +204,34 @@ struct L {
                                                                        b(c, B_HP), b(c, B_X), b(c, B_R));
                    pcg_dir_kernel<T, NCH><<<gr, 256, 0, c->stream>>>(c->g, c->ctl, b(c, B_DT), b(c, B_R),
                                                                     b(c, B_P)));
+    }
+    // block preconditioner (R20): factor once per GN step, solve per iteration
+    static dim3 gblk(hysco_ctx c) { return dim3((unsigned)((c->g.ncol + BLK_THREADS - 1) / BLK_THREADS), c->cfg.batch); }
+    static void bfac(hysco_ctx c, int need_active) {
+        bfac_kernel<T><<<gblk(c), BLK_THREADS, 0, c->stream>>>(c->g, c->ctl, b(c, B_DT), b(c, B_ET), b(c, B_W),
+                                                               b(c, B_F), need_active);
+    }
+    template <bool INIT>
+    static void psolve(hysco_ctx c, const T* r, T* z, T* p, int need_active) {
+        psolve_kernel<T, INIT><<<gblk(c), BLK_THREADS, 0, c->stream>>>(c->g, c->ctl, b(c, B_ET), b(c, B_W),
+                                                                       b(c, B_F), r, z, p, need_active);
+    }
+    static void pcg_init_blk(hysco_ctx c) {
+        NCH_SWITCH(c->nch, pcg_init_kernel<T, NCH, true><<<dim3(c->gx_nodes, c->cfg.batch), 256, 0, c->stream>>>(
+                               c->g, c->ctl, b(c, B_GRAD), b(c, B_DT), b(c, B_X), b(c, B_R), b(c, B_P)));
+        bfac(c, 1);
+        psolve<true>(c, b(c, B_R), b(c, B_TMP), b(c, B_P), 1);
+    }
+    static void pcg_iter_blk(hysco_ctx c, const SolveParams& sp) {
+        dim3 gr(c->gx_nodes, c->cfg.batch);
+        NCH_SWITCH(c->nch,
+                   matvec_kernel<T, NCH, true><<<dim3(c->gx_mv, c->cfg.batch), 256, 0, c->stream>>>(
+                       c->g, c->ctl, b(c, B_DT), b(c, B_ET), b(c, B_P), b(c, B_HP));
+                   pcg_update_kernel<T, NCH, true><<<gr, 256, 0, c->stream>>>(
+                       c->g, c->ctl, sp, b(c, B_DT), b(c, B_P), b(c, B_HP), b(c, B_X), b(c, B_R)));
+        psolve<false>(c, b(c, B_R), b(c, B_TMP), nullptr, 1);
+        NCH_SWITCH(c->nch, pcg_dir_blk_kernel<T, NCH><<<gr, 256, 0, c->stream>>>(c->g, c->ctl, b(c, B_TMP),
+                                                                                  b(c, B_P)));
     }
     static void trial_init(hysco_ctx c) {
         NCH_SWITCH(c->nch, trial_init_kernel<T, NCH><<<dim3(c->gx_nodes, c->cfg.batch), 256, 0, c->stream>>>(
@@ -704,7 +738,8 @@ static hysco_status run_slab_path(std::vector<hysco_ctx>& R, CommBase* comm, int
 template <typename T>
 static void pcg_step(Runner& r, const SolveParams& sp, bool unrolled) {
     hysco_ctx c = r.c;
-    if (c->resident) {   // PCG + the Armijo start (trial_init) in one launch per pair
+    const bool blk = sp.precond == HYSCO_PRECOND_PE_BLOCK;
+    if (c->resident && !blk) {   // PCG + the Armijo start (trial_init) in one launch per pair
         r.seq([&] {
             for (int p = 0; p < c->cfg.batch; p++)
                 launch_resident(c, sp, p, reinterpret_cast<float*>(L<T>::b(c, B_B)),
@@ -712,14 +747,26 @@ static void pcg_step(Runner& r, const SolveParams& sp, bool unrolled) {
         });
     } else if (unrolled) {   // fixed count: max_pcg iterations, kernels of finished pairs exit early
         r.seq([&] {
-            L<T>::pcg_init(c);
-            for (int k = 0; k < sp.max_pcg; k++) L<T>::pcg_iter(c, sp);
+            if (blk) L<T>::pcg_init_blk(c);
+            else L<T>::pcg_init(c);
+            for (int k = 0; k < sp.max_pcg; k++) {
+                if (blk) L<T>::pcg_iter_blk(c, sp);
+                else L<T>::pcg_iter(c, sp);
+            }
             L<T>::trial_init(c);
         });
     } else {
         r.handle(COND_PCG);
-        r.seq([&] { L<T>::pcg_init(c); });
-        r.loop(COND_PCG, [&] { r.seq([&] { L<T>::pcg_iter(c, sp); }); });
+        r.seq([&] {
+            if (blk) L<T>::pcg_init_blk(c);
+            else L<T>::pcg_init(c);
+        });
+        r.loop(COND_PCG, [&] {
+            r.seq([&] {
+                if (blk) L<T>::pcg_iter_blk(c, sp);
+                else L<T>::pcg_iter(c, sp);
+            });
+        });
         r.seq([&] { L<T>::trial_init(c); });
     }
 }
@@ -914,6 +961,7 @@ void hysco_default_solve_opts(hysco_solve_opts* o) {
     o->tol_dJ_rel = 1e-4;
     o->tol_db_rel = 1e-3;
     o->armijo = 1;
+    o->precond = HYSCO_PRECOND_JACOBI;
 }
 
 void hysco_default_ot_opts(hysco_ot_opts* o) {
@@ -1156,6 +1204,38 @@ hysco_status hysco_hess_diag(hysco_ctx ctx, void* d_diag) {
     if (ctx->cfg.dtype == HYSCO_F64) L<double>::diag(ctx, (double*)d_diag);
     else L<float>::diag(ctx, (float*)d_diag);
     CK(cudaGetLastError());
+    return HYSCO_OK;
+}
+
+hysco_status hysco_precond_solve(hysco_ctx ctx, int kind, const void* d_r, void* d_z) {
+    CHECK_CTX();
+    if (ctx->g.slab) return set_err(ctx, HYSCO_ERR_STATE, "slab contexts support solve / correct / correct_host");
+    if (!ctx->state_valid) return set_err(ctx, HYSCO_ERR_STATE, "precond_solve needs a feasible objective_grad first");
+    if (!d_r || !d_z || !aligned16(d_r) || !aligned16(d_z) || d_r == d_z)
+        return set_err(ctx, HYSCO_ERR_ARG, "d_r, d_z must be distinct 16-byte aligned device pointers");
+    if (kind != HYSCO_PRECOND_JACOBI && kind != HYSCO_PRECOND_PE_BLOCK)
+        return set_err(ctx, HYSCO_ERR_ARG, "bad preconditioner kind");
+    const size_t nb = (size_t)ctx->cfg.batch * ctx->g.Nn * ctx->esz;
+    if (kind == HYSCO_PRECOND_JACOBI) {   // z = r / diag(H_J): diag into B_TMP, then divide
+        if (ctx->cfg.dtype == HYSCO_F64) {
+            L<double>::diag(ctx, L<double>::b(ctx, B_TMP));
+            jacobi_div_kernel<double><<<dim3(ctx->gx_nodes, ctx->cfg.batch), 256, 0, ctx->stream>>>(
+                ctx->g, ctx->ctl, (const double*)d_r, L<double>::b(ctx, B_TMP), (double*)d_z);
+        } else {
+            L<float>::diag(ctx, L<float>::b(ctx, B_TMP));
+            jacobi_div_kernel<float><<<dim3(ctx->gx_nodes, ctx->cfg.batch), 256, 0, ctx->stream>>>(
+                ctx->g, ctx->ctl, (const float*)d_r, L<float>::b(ctx, B_TMP), (float*)d_z);
+        }
+    } else if (ctx->cfg.dtype == HYSCO_F64) {
+        L<double>::bfac(ctx, 0);
+        L<double>::psolve<false>(ctx, (const double*)d_r, (double*)d_z, nullptr, 0);
+    } else {
+        L<float>::bfac(ctx, 0);
+        L<float>::psolve<false>(ctx, (const float*)d_r, (float*)d_z, nullptr, 0);
+    }
+    (void)nb;
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(ctx->stream));
     return HYSCO_OK;
 }
 

@@ -74,6 +74,7 @@ struct PairState {
 struct SolveParams {
     int max_gn, max_pcg, fixed, ls_max;
     int armijo;   // 1: Armijo sufficient decrease (R15); 0: full step unless infeasible (parity mode)
+    int precond;  // 0: Jacobi; 1: per-PE-column tridiagonal blocks (R20)
     double pcg_rtol, c1, tol_grad_rel, tol_dJ_rel, tol_db_rel;
     double feas_cap, ot_eps;
 };

@@ -94,6 +94,26 @@ __device__ inline void decide_update(const SolveParams& sp, PairState& s, const 
     s.rz = tot[0];
     if (s.pcg_k >= sp.max_pcg || (!sp.fixed && s.relres < sp.pcg_rtol)) s.pcg_active = 0;
 }
+// Block-preconditioned PCG (R20): the update reduces only r.r (stop test);
+// the column solve then forms z and r.z, and beta = (r.z)_new / (r.z)_old.
+__device__ inline void decide_update_rr(const SolveParams& sp, PairState& s, const double* tot) {
+    if (!s.pcg_active) return;
+    s.pcg_k += 1;
+    s.pcg_iters += 1;
+    s.rr = tot[0];
+    s.relres = sqrt(tot[0] / s.rr0);
+    if (s.pcg_k >= sp.max_pcg || (!sp.fixed && s.relres < sp.pcg_rtol)) s.pcg_active = 0;
+}
+__device__ inline void decide_psolve(PairState& s, const double* tot, bool init) {
+    if (!s.pcg_active) return;
+    if (init) {
+        s.rz = tot[0];
+        s.beta_c = 0.0;
+    } else {
+        s.beta_c = tot[0] / s.rz;
+        s.rz = tot[0];
+    }
+}
 // Armijo start (R15): tot = [grad.q, max|q|]
 __device__ inline void decide_trial(PairState& s, const double* tot) {
     if (s.gn_active) {
@@ -200,7 +220,9 @@ __device__ __forceinline__ double jacobi_shift(const Geom& g, const ColInfo& ci)
 }
 
 // PCG start (R14): x = 0, r = -grad, z = r/M, p = z; r.z and r.r per pair.
-template <typename T, int NCH>
+// BLK (block preconditioner): x = 0, r = -grad and r.r only; z, p and r.z come
+// from the column solve (psolve_kernel, init mode).
+template <typename T, int NCH, bool BLK = false>
 __global__ void __launch_bounds__(256) pcg_init_kernel(Geom g, Ctl c, const T* __restrict__ grad,
                                                        const T* __restrict__ dt, T* __restrict__ x,
                                                        T* __restrict__ r, T* __restrict__ p) {
@@ -229,11 +251,13 @@ __global__ void __launch_bounds__(256) pcg_init_kernel(Geom g, Ctl c, const T* _
                     const int l = seg + 32 * m + lane;
                     if (l < P) {
                         const T rv = -gv[m];
-                        const T z = rv / (dv[m] + cm);
                         x[o + l] = T(0);
                         r[o + l] = rv;
-                        p[o + l] = z;
-                        arz += (double)rv * (double)z;
+                        if (!BLK) {
+                            const T z = rv / (dv[m] + cm);
+                            p[o + l] = z;
+                            arz += (double)rv * (double)z;
+                        }
                         arr += (double)rv * (double)rv;
                     }
                 }
@@ -247,12 +271,13 @@ __global__ void __launch_bounds__(256) pcg_init_kernel(Geom g, Ctl c, const T* _
         store_red(c, pair, gridDim.y, tot, 2, 0);
         return;
     }
-    decide_pcg_init(c.st[pair], tot);
+    decide_pcg_init(c.st[pair], tot);   // BLK: r.z is replaced by the column solve
     if (last_pair(c)) set_cond(c, COND_PCG, any_pair(c, gridDim.y, [](volatile PairState* q) { return q->pcg_active != 0; }));
 }
 
 // A6 PCG update: x += a p, r -= a Hp, z = r/M; r.z, r.r; beta; stop test.
-template <typename T, int NCH>
+// BLK: r.r only (z and r.z come from psolve_kernel after the stop test).
+template <typename T, int NCH, bool BLK = false>
 __global__ void __launch_bounds__(256, 4) pcg_update_kernel(Geom g, Ctl c, SolveParams sp,
                                                          const T* __restrict__ dt, const T* __restrict__ p,
                                                          const T* __restrict__ Hp, T* __restrict__ x,
@@ -289,8 +314,10 @@ __global__ void __launch_bounds__(256, 4) pcg_update_kernel(Geom g, Ctl c, Solve
                         x[o + l] = xv[m] + a * pv[m];
                         const T rn = rv[m] - a * hv[m];
                         r[o + l] = rn;
-                        const T z = rn / (dv[m] + cm);
-                        arz += (double)rn * (double)z;
+                        if (!BLK) {
+                            const T z = rn / (dv[m] + cm);
+                            arz += (double)rn * (double)z;
+                        }
                         arr += (double)rn * (double)rn;
                     }
                 }
@@ -304,7 +331,12 @@ __global__ void __launch_bounds__(256, 4) pcg_update_kernel(Geom g, Ctl c, Solve
         store_red(c, pair, gridDim.y, tot, 2, 0);
         return;
     }
-    decide_update(sp, c.st[pair], tot);
+    if (BLK) {
+        const double rr[1] = {tot[1]};
+        decide_update_rr(sp, c.st[pair], rr);
+    } else {
+        decide_update(sp, c.st[pair], tot);
+    }
     if (last_pair(c)) set_cond(c, COND_PCG, any_pair(c, gridDim.y, [](volatile PairState* q) { return q->pcg_active != 0; }));
 }
 
@@ -337,6 +369,122 @@ __global__ void __launch_bounds__(256) pcg_dir_kernel(Geom g, Ctl c, const T* __
             for (int m = 0; m < NCH; m++) {
                 const int l = seg + 32 * m + lane;
                 if (l < P) p[o + l] = rv[m] / (dv[m] + cm) + be * pv[m];
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Block preconditioner (R20): B = the per-PE-column tridiagonal blocks
+// of H_J, diag M = dt + alpha hd diag(L_xy) (the Jacobi diagonal), off-diagonal
+// et (folded).  Thomas algorithm, one LANE per column (the column's loads
+// walk consecutive nodes, so each lane stays inside its own cache lines):
+//   factor (once per GN step): m_0 = M_0, m_l = M_l - et_{l-1} f_{l-1},
+//                              w_l = 1/m_l, f_l = et_l w_l;
+//   solve  (per PCG iteration): y_l = (r_l - et_{l-1} y_{l-1}) w_l,
+//                               z_l = y_l - f_l z_{l+1}.
+// ---------------------------------------------------------------------------
+constexpr int BLK_THREADS = 64;   // columns per CTA
+
+template <typename T>
+__global__ void __launch_bounds__(BLK_THREADS) bfac_kernel(Geom g, Ctl c, const T* __restrict__ dt,
+                                                          const T* __restrict__ et, T* __restrict__ w,
+                                                          T* __restrict__ f, int need_active) {
+    count_launch(c);
+    const int pair = blockIdx.y;
+    if (need_active && !c.st[pair].gn_active) return;
+    const long long col = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (col >= g.ncol) return;
+    const ColInfo ci = col_info(g, col);
+    const size_t o = (size_t)pair * g.ps + ci.off;
+    const T cm = (T)jacobi_shift(g, ci);
+    const int P = g.P;
+    T fprev = T(0), eprev = T(0);
+    for (int l = 0; l < P; l++) {
+        const T M = __ldg(dt + o + l) + cm;
+        const T e = __ldg(et + o + l);             // et at l = n3 is 0
+        const T m = M - eprev * fprev;
+        const T wl = T(1) / m;
+        const T fl = e * wl;
+        w[o + l] = wl;
+        f[o + l] = fl;
+        fprev = fl;
+        eprev = e;
+    }
+}
+
+// z = B^{-1} r per column; r.z per pair.  INIT (PCG start) also sets p = z.
+// Exits for pairs whose PCG is not running (pcg_active, else need_active = 0:
+// the standalone hysco_precond_solve).
+template <typename T, bool INIT>
+__global__ void __launch_bounds__(BLK_THREADS) psolve_kernel(Geom g, Ctl c, const T* __restrict__ et,
+                                                            const T* __restrict__ w, const T* __restrict__ f,
+                                                            const T* __restrict__ r, T* __restrict__ z,
+                                                            T* __restrict__ p, int need_active) {
+    count_launch(c);
+    const int pair = blockIdx.y;
+    const bool active = !need_active || c.st[pair].pcg_active;
+    double arz = 0;
+    const long long col = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (active && col < g.ncol) {
+        const size_t o = (size_t)pair * g.ps + (size_t)col * g.P;
+        const int P = g.P;
+        T y = T(0), eprev = T(0);
+        for (int l = 0; l < P; l++) {                 // forward: y into z
+            y = (__ldg(r + o + l) - eprev * y) * __ldg(w + o + l);
+            eprev = __ldg(et + o + l);
+            z[o + l] = y;
+        }
+        T zn = T(0);
+        for (int l = P - 1; l >= 0; l--) {            // backward
+            zn = z[o + l] - __ldg(f + o + l) * zn;
+            z[o + l] = zn;
+            if (INIT) p[o + l] = zn;
+            arz += (double)__ldg(r + o + l) * (double)zn;
+        }
+    }
+    if (!need_active) return;
+    double v[1] = {arz}, tot[1];
+    if (!pair_reduce<1, 0u>(c, v, tot)) return;
+    if (threadIdx.x != 0) return;
+    decide_psolve(c.st[pair], tot, INIT);
+}
+
+// z = r / d elementwise (hysco_precond_solve, Jacobi kind).
+template <typename T>
+__global__ void __launch_bounds__(256) jacobi_div_kernel(Geom g, Ctl c, const T* __restrict__ r,
+                                                         const T* __restrict__ d, T* __restrict__ z) {
+    count_launch(c);
+    const size_t po = (size_t)blockIdx.y * g.ps;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < g.Nn; t += (long long)gridDim.x * blockDim.x) {
+        z[po + t] = r[po + t] / d[po + t];
+    }
+}
+
+// p = z + beta p with the stored z (block preconditioner).
+template <typename T, int NCH>
+__global__ void __launch_bounds__(256) pcg_dir_blk_kernel(Geom g, Ctl c, const T* __restrict__ z, T* __restrict__ p) {
+    count_launch(c);
+    const int lane = threadIdx.x & 31;
+    const int pair = blockIdx.y;
+    if (!c.st[pair].pcg_active) return;
+    const T be = (T)c.st[pair].beta_c;
+    const size_t po = (size_t)pair * g.ps;
+    const int P = g.P;
+    HYSCO_FOR_COLS(g) {
+        const size_t o = po + (size_t)col * P;
+        for (int seg = 0; seg < P; seg += 32 * NCH) {
+            T zv[NCH], pv[NCH];
+#pragma unroll
+            for (int m = 0; m < NCH; m++) {
+                const int l = seg + 32 * m + lane;
+                zv[m] = l < P ? z[o + l] : T(0);
+                pv[m] = l < P ? p[o + l] : T(0);
+            }
+#pragma unroll
+            for (int m = 0; m < NCH; m++) {
+                const int l = seg + 32 * m + lane;
+                if (l < P) p[o + l] = zv[m] + be * pv[m];
             }
         }
     }

@@ -17,10 +17,12 @@ LIB_PATH = os.path.join(_PKG, "libhysco.so")
 HYSCO_OK, HYSCO_INFEASIBLE = 0, 1
 HYSCO_ERR_ARG, HYSCO_ERR_SHAPE, HYSCO_ERR_STATE, HYSCO_ERR_CUDA, HYSCO_ERR_NCCL, HYSCO_ERR_NOMEM = -1, -2, -3, -4, -5, -6
 HYSCO_F32, HYSCO_F64 = 0, 1
+HYSCO_PRECOND_JACOBI, HYSCO_PRECOND_PE_BLOCK = 0, 1
 STOP_NAMES = {0: "maxiter", 1: "grad", 2: "dJ", 3: "db", 4: "ls_fail", 5: "infeasible"}
 
 EXPORTED = ["hysco_default_solve_opts", "hysco_default_ot_opts", "hysco_create", "hysco_bind_images",
-            "hysco_ot_init", "hysco_objective_grad", "hysco_hessvec", "hysco_hess_diag", "hysco_solve",
+            "hysco_ot_init", "hysco_objective_grad", "hysco_hessvec", "hysco_hess_diag", "hysco_precond_solve",
+            "hysco_solve",
             "hysco_apply", "hysco_correct", "hysco_correct_host", "hysco_last_launch_count",
             "hysco_last_error", "hysco_destroy", "hysco_version", "hysco_profile_kernels",
             "hysco_nccl_unique_id", "hysco_create_slab", "hysco_create_loopback", "hysco_group_correct",
@@ -49,7 +51,7 @@ class hysco_solve_opts(ctypes.Structure):
     _fields_ = [("max_gn", ctypes.c_int32), ("max_pcg", ctypes.c_int32), ("pcg_rtol", ctypes.c_double),
                 ("fixed_iters", ctypes.c_int32), ("ls_max", ctypes.c_int32), ("armijo_c1", ctypes.c_double),
                 ("tol_grad_rel", ctypes.c_double), ("tol_dJ_rel", ctypes.c_double),
-                ("tol_db_rel", ctypes.c_double), ("armijo", ctypes.c_int32)]
+                ("tol_db_rel", ctypes.c_double), ("armijo", ctypes.c_int32), ("precond", ctypes.c_int32)]
 
 
 class hysco_report(ctypes.Structure):
@@ -75,6 +77,10 @@ def lib():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2403_10706_b200.build` "
                           "(there is no CPU fallback)")
+    # torch first: its bundled libnccl.so.2 then satisfies libhysco's NCCL
+    # dependency (one NCCL in the process; loading the system NCCL first would
+    # break torch's own import)
+    import torch  # noqa: F401
     L = ctypes.CDLL(LIB_PATH)
     vp, st = ctypes.c_void_p, ctypes.c_int
     L.hysco_default_solve_opts.argtypes = [ctypes.POINTER(hysco_solve_opts)]
@@ -87,6 +93,7 @@ def lib():
     L.hysco_objective_grad.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_double), vp]
     L.hysco_hessvec.argtypes = [vp, vp, vp]
     L.hysco_hess_diag.argtypes = [vp, vp]
+    L.hysco_precond_solve.argtypes = [vp, ctypes.c_int32, vp, vp]
     L.hysco_solve.argtypes = [vp, vp, ctypes.POINTER(hysco_solve_opts), ctypes.POINTER(hysco_report)]
     L.hysco_apply.argtypes = [vp, vp, vp, vp]
     L.hysco_correct.argtypes = [vp, ctypes.POINTER(hysco_ot_opts), ctypes.POINTER(hysco_solve_opts), vp, vp, vp,
@@ -94,7 +101,8 @@ def lib():
     L.hysco_correct_host.argtypes = [vp, vp, vp, ctypes.POINTER(hysco_ot_opts), ctypes.POINTER(hysco_solve_opts),
                                      vp, vp, vp, ctypes.POINTER(hysco_report)]
     for f in ("hysco_create", "hysco_bind_images", "hysco_ot_init", "hysco_objective_grad", "hysco_hessvec",
-              "hysco_hess_diag", "hysco_solve", "hysco_apply", "hysco_correct", "hysco_correct_host",
+              "hysco_hess_diag", "hysco_precond_solve", "hysco_solve", "hysco_apply", "hysco_correct",
+              "hysco_correct_host",
               "hysco_destroy"):
         getattr(L, f).restype = st
     L.hysco_destroy.argtypes = [vp]
@@ -190,6 +198,11 @@ def hysco_hessvec(ctx, q, Hq_out):
 
 def hysco_hess_diag(ctx, diag_out):
     _check(ctx, lib().hysco_hess_diag(ctx, _ptr(diag_out)))
+
+
+def hysco_precond_solve(ctx, kind, r, z_out):
+    """z = M^{-1} r at the last objective_grad b (kind: HYSCO_PRECOND_*)."""
+    _check(ctx, lib().hysco_precond_solve(ctx, int(kind), _ptr(r), _ptr(z_out)))
 
 
 def hysco_solve(ctx, b_inout, opts=None, batch=1):
