@@ -47,15 +47,35 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-reps", type=int, default=20)
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--precond", default="jacobi", choices=["jacobi", "block"],
+                    help="PCG preconditioner: Jacobi (P:198, the headline) or per-PE-column blocks (P:200)")
+    ap.add_argument("--stop", default="fixed", choices=["fixed", "paper"],
+                    help="fixed 10 GN x 10 PCG (the headline) or the paper's stop rules (P:196, P:284, R16)")
     ap.add_argument("--slab", action="store_true",
                     help="partition ONE pair of --config into slabs along dim 1 across the ranks (configs[4])")
     return ap.parse_args()
 
 
-def workload_desc(cfg, batch):
+def solver_desc(args=None):
+    pc = "Jacobi" if args is None or args.precond == "jacobi" else "PE-block"
+    if args is None or args.stop == "fixed":
+        return f"fixed 10 GN x 10 {pc}-PCG + Armijo"
+    return f"GN-{pc}-PCG with the paper's stop rules (PCG rtol 0.1, R16 GN tests, <= 50 GN) + Armijo"
+
+
+def solve_opts(H, args):
+    kw = {}
+    if args.precond == "block":
+        kw["precond"] = H.HYSCO_PRECOND_PE_BLOCK
+    if args.stop == "paper":
+        kw.update(fixed_iters=0, max_gn=50)
+    return H.default_solve_opts(**kw)
+
+
+def workload_desc(cfg, batch, args=None):
     shape, h, seed = phantom.CONFIGS[cfg]
     return {"workload": f"{cfg}: {shape[0]}x{shape[1]}x{shape[2]} cells (PE last), h={tuple(round(v, 4) for v in h)} mm, "
-                        "OT+blur+guard -> fixed 10 GN x 10 Jacobi-PCG + Armijo -> Jacobian-modulation apply",
+                        f"OT+blur+guard -> {solver_desc(args)} -> Jacobian-modulation apply",
             "pairs_per_gpu": batch, "seed": seed, "alpha": 300.0, "beta": 1e-4,
             "l2": "flushed (256 MiB write) between timed steps"}
 
@@ -269,13 +289,14 @@ def run_hysco(args):
     stream = torch.cuda.current_stream(dev)
     ctx = H.hysco_create(shape, h, B, device=local, stream=stream.cuda_stream)
     H.hysco_bind_images(ctx, Ip, Im)
+    so = solve_opts(H, args)
     b = torch.zeros((B, n1, n2, n3 + 1), dtype=torch.float32, device=dev)
     Tp = torch.zeros((B, n1, n2, n3), dtype=torch.float32, device=dev)
     Tm = torch.zeros_like(Tp)
     flush = torch.empty(256 << 18, dtype=torch.float32, device=dev)   # 256 MiB > 126 MB L2
 
     for _ in range(max(args.warmup, 0)):
-        H.hysco_correct(ctx, b, Tp, Tm, batch=B)
+        H.hysco_correct(ctx, b, Tp, Tm, solve_opts=so, batch=B)
     torch.cuda.synchronize(dev)
     if world > 1:
         torch.distributed.barrier()
@@ -290,7 +311,7 @@ def run_hysco(args):
     for k in range(args.steps):
         flush.zero_()
         ev[k][0].record(stream)
-        reps, inf = H.hysco_correct(ctx, b, Tp, Tm, batch=B)
+        reps, inf = H.hysco_correct(ctx, b, Tp, Tm, solve_opts=so, batch=B)
         ev[k][1].record(stream)
         launches += H.hysco_last_launch_count(ctx)
     torch.cuda.synchronize(dev)
@@ -318,13 +339,13 @@ def run_hysco(args):
     hTp = torch.empty((B, n1, n2, n3), dtype=torch.float32).pin_memory()
     hTm = torch.empty_like(hTp).pin_memory()
     for _ in range(2):
-        H.hysco_correct_host(ctx, hIp, hIm, hb, hTp, hTm, batch=B)
+        H.hysco_correct_host(ctx, hIp, hIm, hb, hTp, hTm, solve_opts=so, batch=B)
     e2e_ms = []
     for _ in range(max(1, args.e2e_steps)):
         flush.zero_()
         a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        H.hysco_correct_host(ctx, hIp, hIm, hb, hTp, hTm, batch=B)
+        H.hysco_correct_host(ctx, hIp, hIm, hb, hTp, hTm, solve_opts=so, batch=B)
         z.record(stream)
         z.synchronize()
         e2e_ms.append(a.elapsed_time(z))
@@ -348,7 +369,7 @@ def run_hysco(args):
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": dict(workload_desc(args.config, B), parallelism=f"dp{world} (independent pairs per rank)"),
+                "config": dict(workload_desc(args.config, B, args), parallelism=f"dp{world} (independent pairs per rank)"),
                 "clocks": clocks, "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
                 "cpu_baseline": cpu,
                 "solver": {k: r0[k] for k in ("gn_iters", "f_evals", "h_evals", "pcg_iters", "stop", "J")},

@@ -211,27 +211,24 @@ struct L {
         bfac_kernel<T><<<gblk(c), BLK_THREADS, 0, c->stream>>>(c->g, c->ctl, b(c, B_DT), b(c, B_ET), b(c, B_W),
                                                                b(c, B_F), need_active);
     }
-    template <bool INIT>
-    static void psolve(hysco_ctx c, const T* r, T* z, T* p, int need_active) {
-        psolve_kernel<T, INIT><<<gblk(c), BLK_THREADS, 0, c->stream>>>(c->g, c->ctl, b(c, B_ET), b(c, B_W),
-                                                                       b(c, B_F), r, z, p, need_active);
+    static void psolve(hysco_ctx c, const T* r, T* z) {
+        psolve_kernel<T><<<gblk(c), BLK_THREADS, 0, c->stream>>>(c->g, c->ctl, b(c, B_ET), b(c, B_W), b(c, B_F), r, z);
     }
-    static void pcg_init_blk(hysco_ctx c) {
-        NCH_SWITCH(c->nch, pcg_init_kernel<T, NCH, true><<<dim3(c->gx_nodes, c->cfg.batch), 256, 0, c->stream>>>(
-                               c->g, c->ctl, b(c, B_GRAD), b(c, B_DT), b(c, B_X), b(c, B_R), b(c, B_P)));
+    static void pcg_init_blk(hysco_ctx c, const SolveParams& sp) {
         bfac(c, 1);
-        psolve<true>(c, b(c, B_R), b(c, B_TMP), b(c, B_P), 1);
+        NCH_SWITCH(c->nch, pcg_blk_kernel<T, NCH, true><<<dim3(c->gx_nodes, c->cfg.batch), 256, 0, c->stream>>>(
+                               c->g, c->ctl, sp, b(c, B_GRAD), b(c, B_P), b(c, B_HP), b(c, B_X), b(c, B_R),
+                               b(c, B_W), b(c, B_ET), b(c, B_F), b(c, B_TMP)));
     }
     static void pcg_iter_blk(hysco_ctx c, const SolveParams& sp) {
         dim3 gr(c->gx_nodes, c->cfg.batch);
         NCH_SWITCH(c->nch,
                    matvec_kernel<T, NCH, true><<<dim3(c->gx_mv, c->cfg.batch), 256, 0, c->stream>>>(
                        c->g, c->ctl, b(c, B_DT), b(c, B_ET), b(c, B_P), b(c, B_HP));
-                   pcg_update_kernel<T, NCH, true><<<gr, 256, 0, c->stream>>>(
-                       c->g, c->ctl, sp, b(c, B_DT), b(c, B_P), b(c, B_HP), b(c, B_X), b(c, B_R)));
-        psolve<false>(c, b(c, B_R), b(c, B_TMP), nullptr, 1);
-        NCH_SWITCH(c->nch, pcg_dir_blk_kernel<T, NCH><<<gr, 256, 0, c->stream>>>(c->g, c->ctl, b(c, B_TMP),
-                                                                                  b(c, B_P)));
+                   pcg_blk_kernel<T, NCH, false><<<gr, 256, 0, c->stream>>>(
+                       c->g, c->ctl, sp, b(c, B_GRAD), b(c, B_P), b(c, B_HP), b(c, B_X), b(c, B_R), b(c, B_W),
+                       b(c, B_ET), b(c, B_F), b(c, B_TMP));
+                   pcg_dir_blk_kernel<T, NCH><<<gr, 256, 0, c->stream>>>(c->g, c->ctl, b(c, B_TMP), b(c, B_P)));
     }
     static void trial_init(hysco_ctx c) {
         NCH_SWITCH(c->nch, trial_init_kernel<T, NCH><<<dim3(c->gx_nodes, c->cfg.batch), 256, 0, c->stream>>>(
@@ -747,7 +744,7 @@ static void pcg_step(Runner& r, const SolveParams& sp, bool unrolled) {
         });
     } else if (unrolled) {   // fixed count: max_pcg iterations, kernels of finished pairs exit early
         r.seq([&] {
-            if (blk) L<T>::pcg_init_blk(c);
+            if (blk) L<T>::pcg_init_blk(c, sp);
             else L<T>::pcg_init(c);
             for (int k = 0; k < sp.max_pcg; k++) {
                 if (blk) L<T>::pcg_iter_blk(c, sp);
@@ -758,7 +755,7 @@ static void pcg_step(Runner& r, const SolveParams& sp, bool unrolled) {
     } else {
         r.handle(COND_PCG);
         r.seq([&] {
-            if (blk) L<T>::pcg_init_blk(c);
+            if (blk) L<T>::pcg_init_blk(c, sp);
             else L<T>::pcg_init(c);
         });
         r.loop(COND_PCG, [&] {
@@ -1228,10 +1225,10 @@ hysco_status hysco_precond_solve(hysco_ctx ctx, int kind, const void* d_r, void*
         }
     } else if (ctx->cfg.dtype == HYSCO_F64) {
         L<double>::bfac(ctx, 0);
-        L<double>::psolve<false>(ctx, (const double*)d_r, (double*)d_z, nullptr, 0);
+        L<double>::psolve(ctx, (const double*)d_r, (double*)d_z);
     } else {
         L<float>::bfac(ctx, 0);
-        L<float>::psolve<false>(ctx, (const float*)d_r, (float*)d_z, nullptr, 0);
+        L<float>::psolve(ctx, (const float*)d_r, (float*)d_z);
     }
     (void)nb;
     CK(cudaGetLastError());

@@ -208,20 +208,23 @@ __device__ __forceinline__ void phi3(T z, T& f0, T& f1, T& f2) {
     f2 = T(2) * z2 * (T(6) - T(3) * z2 + z2 * z2) * inv * inv * inv;
 }
 
-// Load NCH x 32 elements of a column (l < len) into registers, then store
-// them to shared memory: all loads of the column are in flight together.
+// Load a column (l < len) into registers NCH x 32 elements at a time, then
+// store them to shared memory: all loads of a segment are in flight together
+// (columns longer than NCH x 32, e.g. P = 385, take several segments).
 template <typename T, int NCH>
 __device__ __forceinline__ void stage_col(const T* __restrict__ src, T* dst, int len, int lane) {
-    T v[NCH];
+    for (int base = 0; base < len; base += 32 * NCH) {
+        T v[NCH];
 #pragma unroll
-    for (int m = 0; m < NCH; m++) {
-        const int l = 32 * m + lane;
-        v[m] = l < len ? src[l] : T(0);
-    }
+        for (int m = 0; m < NCH; m++) {
+            const int l = base + 32 * m + lane;
+            v[m] = l < len ? src[l] : T(0);
+        }
 #pragma unroll
-    for (int m = 0; m < NCH; m++) {
-        const int l = 32 * m + lane;
-        if (l < len) dst[l] = v[m];
+        for (int m = 0; m < NCH; m++) {
+            const int l = base + 32 * m + lane;
+            if (l < len) dst[l] = v[m];
+        }
     }
 }
 
@@ -231,19 +234,21 @@ __device__ __forceinline__ void stage_col(const T* __restrict__ src, T* dst, int
 template <typename T, int NCH>
 __device__ __forceinline__ void stage_bq(const T* __restrict__ src, const T* __restrict__ q, T gm, T* dst,
                                          T* __restrict__ gout, int len, int lane) {
-    T v[NCH], w[NCH];
+    for (int base = 0; base < len; base += 32 * NCH) {
+        T v[NCH], w[NCH];
 #pragma unroll
-    for (int m = 0; m < NCH; m++) {
-        const int l = 32 * m + lane;
-        v[m] = l < len ? src[l] : T(0);
-        w[m] = l < len ? q[l] : T(0);
-    }
+        for (int m = 0; m < NCH; m++) {
+            const int l = base + 32 * m + lane;
+            v[m] = l < len ? src[l] : T(0);
+            w[m] = l < len ? q[l] : T(0);
+        }
 #pragma unroll
-    for (int m = 0; m < NCH; m++) {
-        const int l = 32 * m + lane;
-        const T t = fma(gm, w[m], v[m]);
-        if (l < len) dst[l] = t;
-        if (gout && l < len) gout[l] = t;
+        for (int m = 0; m < NCH; m++) {
+            const int l = base + 32 * m + lane;
+            const T t = fma(gm, w[m], v[m]);
+            if (l < len) dst[l] = t;
+            if (gout && l < len) gout[l] = t;
+        }
     }
 }
 template <typename T, int NCH>

@@ -94,26 +94,6 @@ __device__ inline void decide_update(const SolveParams& sp, PairState& s, const 
     s.rz = tot[0];
     if (s.pcg_k >= sp.max_pcg || (!sp.fixed && s.relres < sp.pcg_rtol)) s.pcg_active = 0;
 }
-// Block-preconditioned PCG (R20): the update reduces only r.r (stop test);
-// the column solve then forms z and r.z, and beta = (r.z)_new / (r.z)_old.
-__device__ inline void decide_update_rr(const SolveParams& sp, PairState& s, const double* tot) {
-    if (!s.pcg_active) return;
-    s.pcg_k += 1;
-    s.pcg_iters += 1;
-    s.rr = tot[0];
-    s.relres = sqrt(tot[0] / s.rr0);
-    if (s.pcg_k >= sp.max_pcg || (!sp.fixed && s.relres < sp.pcg_rtol)) s.pcg_active = 0;
-}
-__device__ inline void decide_psolve(PairState& s, const double* tot, bool init) {
-    if (!s.pcg_active) return;
-    if (init) {
-        s.rz = tot[0];
-        s.beta_c = 0.0;
-    } else {
-        s.beta_c = tot[0] / s.rz;
-        s.rz = tot[0];
-    }
-}
 // Armijo start (R15): tot = [grad.q, max|q|]
 __device__ inline void decide_trial(PairState& s, const double* tot) {
     if (s.gn_active) {
@@ -220,9 +200,7 @@ __device__ __forceinline__ double jacobi_shift(const Geom& g, const ColInfo& ci)
 }
 
 // PCG start (R14): x = 0, r = -grad, z = r/M, p = z; r.z and r.r per pair.
-// BLK (block preconditioner): x = 0, r = -grad and r.r only; z, p and r.z come
-// from the column solve (psolve_kernel, init mode).
-template <typename T, int NCH, bool BLK = false>
+template <typename T, int NCH>
 __global__ void __launch_bounds__(256) pcg_init_kernel(Geom g, Ctl c, const T* __restrict__ grad,
                                                        const T* __restrict__ dt, T* __restrict__ x,
                                                        T* __restrict__ r, T* __restrict__ p) {
@@ -251,13 +229,11 @@ __global__ void __launch_bounds__(256) pcg_init_kernel(Geom g, Ctl c, const T* _
                     const int l = seg + 32 * m + lane;
                     if (l < P) {
                         const T rv = -gv[m];
+                        const T z = rv / (dv[m] + cm);
                         x[o + l] = T(0);
                         r[o + l] = rv;
-                        if (!BLK) {
-                            const T z = rv / (dv[m] + cm);
-                            p[o + l] = z;
-                            arz += (double)rv * (double)z;
-                        }
+                        p[o + l] = z;
+                        arz += (double)rv * (double)z;
                         arr += (double)rv * (double)rv;
                     }
                 }
@@ -271,13 +247,12 @@ __global__ void __launch_bounds__(256) pcg_init_kernel(Geom g, Ctl c, const T* _
         store_red(c, pair, gridDim.y, tot, 2, 0);
         return;
     }
-    decide_pcg_init(c.st[pair], tot);   // BLK: r.z is replaced by the column solve
+    decide_pcg_init(c.st[pair], tot);
     if (last_pair(c)) set_cond(c, COND_PCG, any_pair(c, gridDim.y, [](volatile PairState* q) { return q->pcg_active != 0; }));
 }
 
 // A6 PCG update: x += a p, r -= a Hp, z = r/M; r.z, r.r; beta; stop test.
-// BLK: r.r only (z and r.z come from psolve_kernel after the stop test).
-template <typename T, int NCH, bool BLK = false>
+template <typename T, int NCH>
 __global__ void __launch_bounds__(256, 4) pcg_update_kernel(Geom g, Ctl c, SolveParams sp,
                                                          const T* __restrict__ dt, const T* __restrict__ p,
                                                          const T* __restrict__ Hp, T* __restrict__ x,
@@ -314,10 +289,8 @@ __global__ void __launch_bounds__(256, 4) pcg_update_kernel(Geom g, Ctl c, Solve
                         x[o + l] = xv[m] + a * pv[m];
                         const T rn = rv[m] - a * hv[m];
                         r[o + l] = rn;
-                        if (!BLK) {
-                            const T z = rn / (dv[m] + cm);
-                            arz += (double)rn * (double)z;
-                        }
+                        const T z = rn / (dv[m] + cm);
+                        arz += (double)rn * (double)z;
                         arr += (double)rn * (double)rn;
                     }
                 }
@@ -331,12 +304,7 @@ __global__ void __launch_bounds__(256, 4) pcg_update_kernel(Geom g, Ctl c, Solve
         store_red(c, pair, gridDim.y, tot, 2, 0);
         return;
     }
-    if (BLK) {
-        const double rr[1] = {tot[1]};
-        decide_update_rr(sp, c.st[pair], rr);
-    } else {
-        decide_update(sp, c.st[pair], tot);
-    }
+    decide_update(sp, c.st[pair], tot);
     if (last_pair(c)) set_cond(c, COND_PCG, any_pair(c, gridDim.y, [](volatile PairState* q) { return q->pcg_active != 0; }));
 }
 
@@ -413,41 +381,172 @@ __global__ void __launch_bounds__(BLK_THREADS) bfac_kernel(Geom g, Ctl c, const 
     }
 }
 
-// z = B^{-1} r per column; r.z per pair.  INIT (PCG start) also sets p = z.
-// Exits for pairs whose PCG is not running (pcg_active, else need_active = 0:
-// the standalone hysco_precond_solve).
-template <typename T, bool INIT>
+// z = B^{-1} r per column (hysco_precond_solve; the PCG uses pcg_blk_kernel).
+template <typename T>
 __global__ void __launch_bounds__(BLK_THREADS) psolve_kernel(Geom g, Ctl c, const T* __restrict__ et,
                                                             const T* __restrict__ w, const T* __restrict__ f,
-                                                            const T* __restrict__ r, T* __restrict__ z,
-                                                            T* __restrict__ p, int need_active) {
+                                                            const T* __restrict__ r, T* __restrict__ z) {
     count_launch(c);
-    const int pair = blockIdx.y;
-    const bool active = !need_active || c.st[pair].pcg_active;
-    double arz = 0;
     const long long col = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (active && col < g.ncol) {
-        const size_t o = (size_t)pair * g.ps + (size_t)col * g.P;
-        const int P = g.P;
-        T y = T(0), eprev = T(0);
-        for (int l = 0; l < P; l++) {                 // forward: y into z
-            y = (__ldg(r + o + l) - eprev * y) * __ldg(w + o + l);
-            eprev = __ldg(et + o + l);
-            z[o + l] = y;
-        }
-        T zn = T(0);
-        for (int l = P - 1; l >= 0; l--) {            // backward
-            zn = z[o + l] - __ldg(f + o + l) * zn;
-            z[o + l] = zn;
-            if (INIT) p[o + l] = zn;
-            arz += (double)__ldg(r + o + l) * (double)zn;
+    if (col >= g.ncol) return;
+    const size_t o = (size_t)blockIdx.y * g.ps + (size_t)col * g.P;
+    const int P = g.P;
+    T y = T(0), eprev = T(0);
+    for (int l = 0; l < P; l++) {                 // forward: y into z
+        y = (__ldg(r + o + l) - eprev * y) * __ldg(w + o + l);
+        eprev = __ldg(et + o + l);
+        z[o + l] = y;
+    }
+    T zn = T(0);
+    for (int l = P - 1; l >= 0; l--) {            // backward
+        zn = z[o + l] - __ldg(f + o + l) * zn;
+        z[o + l] = zn;
+    }
+}
+
+// Warp-level inclusive scans of affine maps y -> A y + B over the 32 lanes of
+// a chunk (forward: lane order; backward: reverse lane order).  Composition
+// (A, B) after (A', B') = (A A', A B' + B).
+template <typename T>
+__device__ __forceinline__ void affine_scan_up(T& A, T& B, int lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const T Ap = __shfl_up_sync(FULL, A, o), Bp = __shfl_up_sync(FULL, B, o);
+        if (lane >= o) {
+            B = fma(A, Bp, B);
+            A = A * Ap;
         }
     }
-    if (!need_active) return;
-    double v[1] = {arz}, tot[1];
-    if (!pair_reduce<1, 0u>(c, v, tot)) return;
+}
+template <typename T>
+__device__ __forceinline__ void affine_scan_down(T& A, T& B, int lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const T An = __shfl_down_sync(FULL, A, o), Bn = __shfl_down_sync(FULL, B, o);
+        if (lane + o < 32) {
+            B = fma(A, Bn, B);
+            A = A * An;
+        }
+    }
+}
+
+// Block-preconditioned PCG step (R20), one warp per column, fused:
+//   ITER: x += a p, r -= a Hp;   INIT: x = 0, r = -grad;
+//   z = B^{-1} r by the Thomas recurrences written as affine scans
+//     forward  y_l = w_l r_l - (w_l et_{l-1}) y_{l-1},
+//     backward z_l = y_l - f_l z_{l+1}     (w, f from bfac_kernel);
+//   INIT also p = z;  per pair r.z and r.r -> the Jacobi path's decisions
+//   (decide_pcg_init / decide_update: beta = (r.z)_new / (r.z)_old, stop test).
+// Columns longer than one NCH x 32 segment keep y in z between the sweeps.
+template <typename T, int NCH, bool INIT>
+__global__ void __launch_bounds__(256) pcg_blk_kernel(Geom g, Ctl c, SolveParams sp, const T* __restrict__ grad,
+                                                      T* __restrict__ p, const T* __restrict__ Hp,
+                                                      T* __restrict__ x, T* __restrict__ r,
+                                                      const T* __restrict__ w, const T* __restrict__ et,
+                                                      const T* __restrict__ f, T* __restrict__ z) {
+    count_launch(c);
+    const int lane = threadIdx.x & 31;
+    const int pair = blockIdx.y;
+    const bool active = INIT ? c.st[pair].gn_active != 0 : c.st[pair].pcg_active != 0;
+    const T a = INIT ? T(0) : (T)c.st[pair].alpha_c;
+    const size_t po = (size_t)pair * g.ps;
+    const int P = g.P;
+    const bool multi = P > 32 * NCH;
+    double arz = 0, arr = 0;
+    if (active) {
+        HYSCO_FOR_COLS(g) {
+            const size_t o = po + (size_t)col * P;
+            T rv[NCH], yv[NCH];
+            T ycar = T(0), ecar = T(0);          // y and et at the node before this chunk
+            for (int seg = 0; seg < P; seg += 32 * NCH) {
+                T wv[NCH], ev[NCH];
+#pragma unroll
+                for (int m = 0; m < NCH; m++) {
+                    const int l = seg + 32 * m + lane;
+                    const bool ok = l < P;
+                    if (INIT) {
+                        rv[m] = ok ? -grad[o + l] : T(0);
+                    } else {
+                        rv[m] = ok ? r[o + l] : T(0);
+                    }
+                    wv[m] = ok ? w[o + l] : T(0);
+                    ev[m] = ok ? et[o + l] : T(0);
+                }
+                if (!INIT) {
+                    T pv[NCH], hv[NCH], xv[NCH];
+#pragma unroll
+                    for (int m = 0; m < NCH; m++) {
+                        const int l = seg + 32 * m + lane;
+                        const bool ok = l < P;
+                        pv[m] = ok ? p[o + l] : T(0);
+                        hv[m] = ok ? Hp[o + l] : T(0);
+                        xv[m] = ok ? x[o + l] : T(0);
+                    }
+#pragma unroll
+                    for (int m = 0; m < NCH; m++) {
+                        const int l = seg + 32 * m + lane;
+                        rv[m] = rv[m] - a * hv[m];
+                        if (l < P) x[o + l] = xv[m] + a * pv[m];
+                    }
+                }
+#pragma unroll
+                for (int m = 0; m < NCH; m++) {
+                    const int l = seg + 32 * m + lane;
+                    if (l < P) {
+                        r[o + l] = rv[m];
+                        if (INIT) x[o + l] = T(0);
+                    }
+                    arr += (double)rv[m] * (double)rv[m];
+                    // forward sweep over this chunk: et_{l-1} from the lane below
+                    const T eup = __shfl_up_sync(FULL, ev[m], 1);
+                    const T em = lane ? eup : ecar;
+                    T A = -wv[m] * em, B = wv[m] * rv[m];
+                    affine_scan_up(A, B, lane);
+                    const T y = fma(A, ycar, B);
+                    yv[m] = y;
+                    ycar = __shfl_sync(FULL, y, 31);
+                    ecar = __shfl_sync(FULL, ev[m], 31);
+                    if (multi && l < P) z[o + l] = y;
+                }
+            }
+            // backward sweep from the top segment down
+            T zcar = T(0);                        // z at the node after this chunk
+            const int nseg = (P + 32 * NCH - 1) / (32 * NCH);
+            for (int sgi = nseg - 1; sgi >= 0; sgi--) {
+                const int seg = sgi * 32 * NCH;
+                T fv[NCH];
+#pragma unroll
+                for (int m = 0; m < NCH; m++) {
+                    const int l = seg + 32 * m + lane;
+                    const bool ok = l < P;
+                    fv[m] = ok ? f[o + l] : T(0);
+                    if (multi) {
+                        yv[m] = ok ? z[o + l] : T(0);
+                        rv[m] = ok ? r[o + l] : T(0);
+                    }
+                }
+#pragma unroll
+                for (int mm = NCH - 1; mm >= 0; mm--) {
+                    const int l = seg + 32 * mm + lane;
+                    T A = -fv[mm], B = yv[mm];
+                    affine_scan_down(A, B, lane);
+                    const T zz = fma(A, zcar, B);
+                    zcar = __shfl_sync(FULL, zz, 0);
+                    if (l < P) {
+                        z[o + l] = zz;
+                        if (INIT) p[o + l] = zz;
+                    }
+                    arz += (double)rv[mm] * (double)zz;
+                }
+            }
+        }
+    }
+    double v[2] = {arz, arr}, tot[2];
+    if (!pair_reduce<2, 0u>(c, v, tot)) return;
     if (threadIdx.x != 0) return;
-    decide_psolve(c.st[pair], tot, INIT);
+    if (INIT) decide_pcg_init(c.st[pair], tot);
+    else decide_update(sp, c.st[pair], tot);
+    if (last_pair(c)) set_cond(c, COND_PCG, any_pair(c, gridDim.y, [](volatile PairState* q) { return q->pcg_active != 0; }));
 }
 
 // z = r / d elementwise (hysco_precond_solve, Jacobi kind).

@@ -94,6 +94,7 @@ SHAPES = [
     ("C1", (16, 16, 8), (1.25, 1.25, 1.25), 0),
     ("ragged", (5, 7, 37), (1.1, 0.9, 1.3), 5),      # n3+1 not a multiple of 32, odd everything
     ("col", (1, 3, 70), (1.0, 2.0, 1.5), 6),        # n1 = 1 (no dim-1 neighbours), 3 chunks of 32
+    ("long", (2, 3, 300), (1.25, 1.25, 1.0), 13),   # P = 301 > 8 x 32: two register segments per column
 ]
 
 
@@ -486,14 +487,34 @@ def test_block_precond_hcp3t_production_and_fixed_f32(hcp3t):
     b0 = c.nodes()
     H.hysco_ot_init(c.ctx, b0)
     b = b0.clone()
+    torch.cuda.synchronize()      # clones run on torch's stream, the context on its own
     reps, inf = H.hysco_solve(c.ctx, b, H.default_solve_opts(fixed_iters=0, max_gn=50,
                                                               precond=H.HYSCO_PRECOND_PE_BLOCK))
     assert not inf and reps[0]["stop_reason"] not in (4, 5)   # no line-search failure, feasible
     bj = b0.clone()
+    torch.cuda.synchronize()
     repj, _ = H.hysco_solve(c.ctx, bj, H.default_solve_opts())
     assert reps[0]["pcg_iters"] < 30 and reps[0]["J"] < repj[0]["J"]
     b1 = b0.clone()
+    torch.cuda.synchronize()
     r1, _ = H.hysco_solve(c.ctx, b1, H.default_solve_opts(max_gn=1, armijo=0, precond=H.HYSCO_PRECOND_PE_BLOCK))
     bref, st, rep = O.gauss_newton(Ip, Im, c.np(b0)[0], p.h, max_gn=1, fixed=True, armijo=False, precond="block")
     assert rel(c.np(b1)[0], bref) <= 1e-4
+    c.close()
+
+
+@pytest.mark.parametrize("dtype", [H.HYSCO_F32, H.HYSCO_F64], ids=["f32", "f64"])
+def test_block_precond_long_columns(dtype):
+    """Columns longer than one register segment (P = 301 > 8 x 32): the fused
+    block-PCG kernel keeps y in memory between its two sweeps."""
+    p = phantom.make_pair((3, 4, 300), (1.25, 1.25, 1.0), 13)
+    Ip, Im = rnd(p.Ip, dtype), rnd(p.Im, dtype)
+    b0 = rnd(O.ot_init(Ip, Im, p.h[2])[0], dtype)
+    c = Ctx([Ip], [Im], p.h, dtype)
+    b = c.nodes(b0)
+    reps, inf = H.hysco_solve(c.ctx, b, H.default_solve_opts(max_gn=3, armijo=0, precond=H.HYSCO_PRECOND_PE_BLOCK))
+    assert not inf
+    bref, st, rep = O.gauss_newton(Ip, Im, b0, p.h, max_gn=3, fixed=True, armijo=False, precond="block")
+    assert reps[0]["pcg_iters"] == rep["pcg_iters"]
+    assert rel(c.np(b)[0], bref) <= TOL[dtype]["solve"]
     c.close()
