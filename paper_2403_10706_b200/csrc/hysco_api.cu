@@ -77,7 +77,7 @@ struct hysco_ctx_s {
     int res_k = 0, res_grid = 0;
     size_t res_smem = 0;
     double* res_part = nullptr;
-    unsigned* res_flags = nullptr;   // [G] p-halo flags + [1] launch counter (hysco_resident.cuh)
+    unsigned* res_flags = nullptr;   // p-halo flags + launch counter (hysco_resident.cuh)
     float* res_pg = nullptr;     // ghost-padded global copy of p (halo source)
     float* res_x = nullptr;      // x of one pair in the padded resident layout
     float res_wi = 0.f, res_wj = 0.f;   // alpha hd / h1^2, alpha hd / h2^2 (in-plane Laplacian weights)
@@ -417,17 +417,18 @@ static void setup_resident(hysco_ctx ctx) {
         return;
     }
     const size_t ghost = (res_ghost_pair_floats(g) * ctx->cfg.batch + res_ghost_slack_floats(k)) * sizeof(float);
-    if (cudaMalloc(&ctx->res_part, sizeof(double) * 8 * G) != cudaSuccess ||
-        cudaMalloc(&ctx->res_flags, sizeof(unsigned) * (G + 1)) != cudaSuccess ||
+    if (G * 2 > RES_RSTRIDE) return;   // replica layout of the partials (hysco_resident.cuh)
+    if (cudaMalloc(&ctx->res_part, sizeof(double) * 3 * RES_PART_DOUBLES) != cudaSuccess ||
+        cudaMalloc(&ctx->res_flags, sizeof(unsigned) * res_flags_words(G)) != cudaSuccess ||
         cudaMalloc(&ctx->res_pg, ghost) != cudaSuccess ||
         cudaMalloc(&ctx->res_x, (size_t)g.ncol * res_pad(g.P) * sizeof(float)) != cudaSuccess) {
         cudaGetLastError();
         return;
     }
-    cudaMemset(ctx->res_part, 0, sizeof(double) * 8 * G);
-    cudaMemset(ctx->res_flags, 0, sizeof(unsigned) * G);
+    cudaMemset(ctx->res_part, 0, sizeof(double) * 3 * RES_PART_DOUBLES);
+    cudaMemset(ctx->res_flags, 0, sizeof(unsigned) * res_flags_words(G));
     const unsigned first_launch = 1;      // tags of launch 0 would match the zeroed slots
-    cudaMemcpy(ctx->res_flags + G, &first_launch, sizeof(unsigned), cudaMemcpyHostToDevice);
+    cudaMemcpy(ctx->res_flags + (size_t)G * RES_FLAG_STRIDE, &first_launch, sizeof(unsigned), cudaMemcpyHostToDevice);
     cudaMemset(ctx->res_pg, 0, ghost);   // ghost planes stay zero forever
     ctx->res_k = k;
     ctx->res_wi = (float)(g.ahd * g.ih1sq);

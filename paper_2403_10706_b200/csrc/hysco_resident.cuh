@@ -56,6 +56,16 @@ __device__ __forceinline__ int opaque(int v) {
 // bounded: a stall of ~2^26 polls traps (a kernel error, not a hang).
 // ---------------------------------------------------------------------------
 constexpr unsigned RES_SPIN_LIMIT = 1u << 26;
+// Contention: 148 pollers reading the same few cache lines serialise at one
+// L2 slice (measured: the first poll of a collect took ~4800 cycles, vs
+// ~250 for an L2 hit).  So every partial is published to RES_REPL replicas
+// RES_RSTRIDE doubles apart (different lines / slices) and CTA b polls replica
+// b % RES_REPL; the p-halo flags sit one per 128-byte line.
+constexpr int RES_REPL = 16;
+constexpr int RES_RSTRIDE = 512;             // doubles per replica (>= G x NV)
+constexpr int RES_PART_DOUBLES = RES_REPL * RES_RSTRIDE;   // one reduction buffer
+constexpr int RES_FLAG_STRIDE = 32;          // uints between flags (128 B)
+__host__ __device__ inline size_t res_flags_words(int G) { return (size_t)(G + 1) * RES_FLAG_STRIDE; }
 
 __device__ __forceinline__ unsigned res_tag(unsigned launch, int seq) { return ((launch & 7u) << 5) | ((unsigned)seq & 31u); }
 __device__ __forceinline__ double tag_value(double v, unsigned tag) {
@@ -84,7 +94,11 @@ __device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
 __device__ __forceinline__ void res_stamp(unsigned long long* tr) {
     if (tr && threadIdx.x == 0) {
         unsigned long long t;
+#ifdef RES_TRACE_CLOCK   // diagnostic builds: SM cycle counter (per-CTA durations only)
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+#else
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+#endif
         *tr = t;
     }
 }
@@ -103,25 +117,31 @@ __device__ __forceinline__ void reduce_publish(double (&v)[NV], double* __restri
         if (lane == 0) sred[k][wid] = x;
     }
     __syncthreads();
-    if (threadIdx.x < NV) {
-        const int k = threadIdx.x;
-        double x = sred[k][0];
-        for (int w = 1; w < nw; w++) x = comb<MAXMASK>(k, x, sred[k][w]);
-        st_relaxed_f64(part + blockIdx.x * NV + k, tag_value(x, tag));
+    if (wid < NV) {                          // warp k folds value k over the warps (shuffle tree)
+        const int k = wid;
+        double x = lane < nw ? sred[k][lane] : ident<MAXMASK>(k);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x = comb<MAXMASK>(k, x, __shfl_xor_sync(FULL, x, o));
+        if (lane < RES_REPL)                 // all lanes hold the total: lane r writes replica r
+            st_relaxed_f64(part + lane * RES_RSTRIDE + blockIdx.x * NV + k, tag_value(x, tag));
     }
 }
 
 // Wait for every CTA's tagged partials and fold them in fixed order (warp k
 // folds value k, identically in every CTA).  Result in out[] (all threads).
 template <int NV, unsigned MAXMASK = 0>
-__device__ __forceinline__ void reduce_collect(const double* __restrict__ part, unsigned tag, double (&out)[NV]) {
+__device__ __forceinline__ void reduce_collect(const double* __restrict__ part, unsigned tag, double (&out)[NV],
+                                               unsigned long long* dbg = nullptr) {
     constexpr int MS = 8;                    // slots per lane: up to 256 CTAs
     __shared__ double stot[NV];
     const int wid = threadIdx.x >> 5;
     if (wid < NV) {
         const int lane = threadIdx.x & 31, G = gridDim.x;
+        part += (blockIdx.x % RES_REPL) * RES_RSTRIDE;
         double v[MS];
         unsigned pending = 0;
+        unsigned long long c0 = 0, c1 = 0;
+        if (dbg) c0 = clock64();
 #pragma unroll
         for (int m = 0; m < MS; m++) {
             const int b = lane + 32 * m;
@@ -132,6 +152,10 @@ __device__ __forceinline__ void reduce_collect(const double* __restrict__ part, 
             }
         }
         unsigned spins = 0;
+        if (dbg) {
+            __syncwarp();
+            c1 = clock64();
+        }
         while (__any_sync(FULL, pending != 0)) {
             if (++spins > RES_SPIN_LIMIT) __trap();
 #pragma unroll
@@ -151,6 +175,12 @@ __device__ __forceinline__ void reduce_collect(const double* __restrict__ part, 
             x = mx ? fmax(x, y) : x + y;
         }
         if (lane == 0) stot[wid] = x;
+        if (dbg && threadIdx.x == 0) {       // diagnostic: first-poll cycles, spin cycles, spins
+            const unsigned long long c2 = clock64();
+            dbg[0] = c1 - c0;
+            dbg[8] = c2 - c1;
+            dbg[16] = spins;
+        }
     }
     __syncthreads();
 #pragma unroll
@@ -161,14 +191,14 @@ __device__ __forceinline__ void reduce_collect(const double* __restrict__ part, 
 // the CTA barrier, then a gpu-scope release by thread 0).
 __device__ __forceinline__ void halo_release(unsigned* flags, unsigned tag) {
     __syncthreads();
-    if (threadIdx.x == 0) st_release_u32(flags + blockIdx.x, tag);
+    if (threadIdx.x == 0) st_release_u32(flags + (size_t)blockIdx.x * RES_FLAG_STRIDE, tag);
 }
 // Before reading neighbours' p: acquire the flags of CTAs [blo, bhi].
 __device__ __forceinline__ void halo_acquire(const unsigned* flags, int blo, int bhi, unsigned tag) {
     if (threadIdx.x < 32) {
         for (int b = blo + (int)threadIdx.x; b <= bhi; b += 32) {
             unsigned spins = 0;
-            while (ld_acquire_u32(flags + b) != tag)
+            while (ld_acquire_u32(flags + (size_t)b * RES_FLAG_STRIDE) != tag)
                 if (++spins > RES_SPIN_LIMIT) __trap();
         }
     }
@@ -289,12 +319,12 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
         reinterpret_cast<float2*>(pgh + (size_t)pair * res_ghost_pair_floats(g) + (size_t)(c0 + n2) * Pp);
     float2* __restrict__ xp2 = reinterpret_cast<float2*>(xpad + (size_t)c0 * Pp);
     const int sI2 = n2 * GPC;                // i-neighbour distance in node pairs
-    double* part0 = gpart;                   // [G][2] r0.z0, r0.r0
-    double* part1 = gpart + 2 * gridDim.x;   // [G][1] p.Hp
-    double* part2 = gpart + 3 * gridDim.x;   // [G][2] r.z, r.r
+    double* part0 = gpart;                          // [repl][G][2] r0.z0, r0.r0 (and the Armijo start)
+    double* part1 = gpart + RES_PART_DOUBLES;       // [repl][G][1] p.Hp
+    double* part2 = gpart + 2 * RES_PART_DOUBLES;   // [repl][G][2] r.z, r.r
     const int tid = threadIdx.x;
-    // flags[0, G): p-halo flags; flags[G]: launch counter (tags, see above)
-    const unsigned launch = *reinterpret_cast<volatile unsigned*>(flags + gridDim.x);
+    // flags[b * RES_FLAG_STRIDE]: p-halo flag of CTA b; flags[G * RES_FLAG_STRIDE]: launch counter
+    const unsigned launch = *reinterpret_cast<volatile unsigned*>(flags + (size_t)gridDim.x * RES_FLAG_STRIDE);
     // CTAs owning this CTA's i-neighbour (+-n2) and j-neighbour (+-1) columns
     const int blo = res_owner(c0 - n2 > 0 ? c0 - n2 : 0, g.ncol, gridDim.x);
     const int bhi = res_owner(c1 - 1 + n2 < g.ncol ? c1 - 1 + n2 : g.ncol - 1, g.ncol, gridDim.x);
@@ -405,8 +435,12 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
 #pragma unroll
                 for (int k = 0; k < K; k++) {
                     const int o = k * NT;
+#ifdef RES_ABLATE_REMOTE   // diagnostic builds only (tools/res_trace.cu): timing without the i-halo loads
+                    const float2 a = make_float2(0.f, 0.f), b = a;
+#else
                     const float2 a = __ldcg(gc + o - sI2);
                     const float2 b = __ldcg(gc + o + sI2);
+#endif
                     const float2 c = mbit(m, RM_JMR + k) ? __ldcg(gc + o - GPC) : make_float2(0.f, 0.f);
                     const float2 d = mbit(m, RM_JPR + k) ? __ldcg(gc + o + GPC) : make_float2(0.f, 0.f);
                     float2 h = hv[k];
@@ -425,7 +459,8 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
             double v1[1] = {(double)fpq}, t1[1];
             reduce_publish<1>(v1, part1, res_tag(launch, k_it));
             if constexpr (TRACE) res_stamp(tr ? tr + 7 : nullptr);
-            reduce_collect<1>(part1, res_tag(launch, k_it), t1);
+            reduce_collect<1>(part1, res_tag(launch, k_it), t1,
+                              (TRACE && k_it < 8) ? trace + ((size_t)blockIdx.x * 16 + 12) * 8 + k_it : nullptr);
             if constexpr (TRACE) res_stamp(tr ? tr + 3 : nullptr);
             if (t1[0] <= 0.0) break;                  // breakdown (oracle pcg(): keep x)
             const float a = (float)(rz / t1[0]);
@@ -464,7 +499,11 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
                     const float2 p = s2[k * NT];
                     const float2 v = make_float2(a * p.x, a * p.y);
                     if (mbit(m, RM_VAL + k)) {
+#ifdef RES_ABLATE_X
+                        if (k_it > 0) xt[k * NT] = v;
+#else
                         if (k_it > 0) red_add2(reinterpret_cast<float*>(xt + k * NT), v);
+#endif
                         else xt[k * NT] = v;  // first update: x_1 = 0 + a p_0
                     }
                 }
@@ -489,7 +528,9 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
                     const float2 p = s2[o], z = hv[k];
                     const float2 pn = make_float2(fmaf(be, p.x, z.x), fmaf(be, p.y, z.y));
                     s2[o] = pn;
+#ifndef RES_ABLATE_GHOST
                     if (mbit(m, RM_VAL + k)) gt[o] = pn;
+#endif
                 }
             }
             if constexpr (TRACE) res_stamp(tr ? tr + 6 : nullptr);
@@ -562,7 +603,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         // every CTA read `launch` before its first publish, which CTA 0 has
         // collected, so the counter can advance now
-        *reinterpret_cast<volatile unsigned*>(flags + gridDim.x) = launch + 1;
+        *reinterpret_cast<volatile unsigned*>(flags + (size_t)gridDim.x * RES_FLAG_STRIDE) = launch + 1;
         PairState& s = c.st[pair];
         s.rz = rz;
         s.rr0 = s_rr0;

@@ -47,10 +47,10 @@ int main(int argc, char** argv) {
     PairState* st; cudaMalloc(&st, sizeof(PairState));
     PairState hs{}; hs.gn_active = 1; cudaMemcpy(st, &hs, sizeof hs, cudaMemcpyHostToDevice);
     unsigned long long* launches; cudaMalloc(&launches, 8);
-    double* part; cudaMalloc(&part, sizeof(double) * 8 * G);
-    unsigned* flags; cudaMalloc(&flags, 4 * (G + 1)); cudaMemset(flags, 0, 4 * (G + 1));
-    cudaMemset(part, 0, sizeof(double) * 8 * G);
-    { unsigned one = 1; cudaMemcpy(flags + G, &one, 4, cudaMemcpyHostToDevice); }
+    double* part; cudaMalloc(&part, sizeof(double) * 3 * RES_PART_DOUBLES);
+    unsigned* flags; cudaMalloc(&flags, 4 * res_flags_words(G)); cudaMemset(flags, 0, 4 * res_flags_words(G));
+    cudaMemset(part, 0, sizeof(double) * 3 * RES_PART_DOUBLES);
+    { unsigned one = 1; cudaMemcpy(flags + (size_t)G * RES_FLAG_STRIDE, &one, 4, cudaMemcpyHostToDevice); }
     unsigned long long* trace; cudaMalloc(&trace, sizeof(unsigned long long) * G * 16 * 8);
     cudaMemset(trace, 0, sizeof(unsigned long long) * G * 16 * 8);
     unsigned* dcond; cudaMalloc(&dcond, 4 * NCOND);
@@ -110,6 +110,18 @@ int main(int argc, char** argv) {
         }
         printf("init loads %.2f us, init reduce %.2f us, loop %.2f us (per-CTA means), start->loop end max %.2f us\n",
                a / G / 1e3, b2 / G / 1e3, c2 / G / 1e3, mx / 1e3);
+    }
+    {   // collect #1 internals (clock64 cycles): first poll, spin phase, spin count
+        double fp = 0, sp = 0, ns = 0, fpmax = 0, spmax = 0;
+        int n = 0;
+        for (int b = 0; b < G; b++)
+            for (int it = 1; it < 8; it++) {
+                const double a1 = (double)ht[((size_t)b * 16 + 12) * 8 + it], a2 = (double)ht[((size_t)b * 16 + 13) * 8 + it];
+                fp += a1; sp += a2; ns += (double)ht[((size_t)b * 16 + 14) * 8 + it];
+                fpmax = std::max(fpmax, a1); spmax = std::max(spmax, a2); n++;
+            }
+        printf("collect #1: first poll %.0f cyc (max %.0f), spin %.0f cyc (max %.0f), spins %.2f (means over CTAs x iterations)\n",
+               fp / n, fpmax, sp / n, spmax, ns / n);
     }
     // iteration period
     double per = 0;
