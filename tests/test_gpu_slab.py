@@ -35,6 +35,7 @@ def single(Ip, Im, h, dtype, so, batch):
     b = torch.zeros((batch, n1, n2, n3 + 1), dtype=TD[dtype], device=DEV)
     Tp = torch.zeros((batch, n1, n2, n3), dtype=TD[dtype], device=DEV)
     Tm = torch.zeros_like(Tp)
+    torch.cuda.synchronize()          # torch fills on its stream; the context runs on its own
     reps, _ = H.hysco_correct(ctx, b, Tp, Tm, solve_opts=so, batch=batch)
     H.hysco_destroy(ctx)
     return b.cpu().numpy(), Tp.cpu().numpy(), Tm.cpu().numpy(), reps
@@ -53,6 +54,7 @@ def grouped(Ip, Im, h, dtype, so, batch, nranks):
         bs.append(torch.zeros((batch, i1 - i0, n2, n3 + 1), dtype=TD[dtype], device=DEV))
         tps.append(torch.zeros((batch, i1 - i0, n2, n3), dtype=TD[dtype], device=DEV))
         tms.append(torch.zeros((batch, i1 - i0, n2, n3), dtype=TD[dtype], device=DEV))
+    torch.cuda.synchronize()
     reps, _ = H.hysco_group_correct(ctxs, bs, tps, tms, solve_opts=so, batch=batch)
     n_launch = [H.hysco_last_launch_count(c) for c in ctxs]
     for c in ctxs:
@@ -88,6 +90,20 @@ def test_loopback_slabs_ragged_batch_f32_vs_oracle():
         _, bref, tpr, _, rep = O.correct_pair(q.Ip.astype(np.float64), q.Im.astype(np.float64), h, armijo=False)
         assert rel(b2[k], bref) <= 1e-4 and rel(tp2[k], tpr) <= 1e-4
         assert reps[k]["gn_iters"] == rep["gn_iters"]
+
+
+def test_loopback_slabs_long_columns_f64():
+    """P = 301 > 8 x 32 (two register segments per column, like configs[4]'s
+    P = 385) through the slab path: equals the single-context solve."""
+    p = phantom.make_pair((4, 3, 300), (1.25, 1.25, 1.0), 19)
+    Ip, Im = p.Ip[None].astype(np.float64), p.Im[None].astype(np.float64)
+    so = H.default_solve_opts(max_gn=3)
+    b1, tp1, _, r1 = single(Ip, Im, p.h, H.HYSCO_F64, so, 1)
+    b2, tp2, _, r2, _ = grouped(Ip, Im, p.h, H.HYSCO_F64, so, 1, 2)
+    assert (r2[0]["gn_iters"], r2[0]["pcg_iters"]) == (r1[0]["gn_iters"], r1[0]["pcg_iters"])
+    assert rel(b2, b1) <= 1e-11 and rel(tp2, tp1) <= 1e-11
+    _, bref, _, _, rep = O.correct_pair(p.Ip.astype(np.float64), p.Im.astype(np.float64), p.h, max_gn=3)
+    assert rel(b1[0], bref) <= 1e-9
 
 
 def test_loopback_single_plane_slabs_periodic_blur():
