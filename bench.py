@@ -338,23 +338,30 @@ def run_hysco(args):
     hb = torch.empty((B, n1, n2, n3 + 1), dtype=torch.float32).pin_memory()
     hTp = torch.empty((B, n1, n2, n3), dtype=torch.float32).pin_memory()
     hTm = torch.empty_like(hTp).pin_memory()
-    for _ in range(2):
-        H.hysco_correct_host(ctx, hIp, hIm, hb, hTp, hTm, solve_opts=so, batch=B)
-    e2e_ms = []
-    for _ in range(max(1, args.e2e_steps)):
-        flush.zero_()
-        a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        H.hysco_correct_host(ctx, hIp, hIm, hb, hTp, hTm, solve_opts=so, batch=B)
-        z.record(stream)
-        z.synchronize()
-        e2e_ms.append(a.elapsed_time(z))
-    te = torch.tensor([float(np.sum(e2e_ms))], dtype=torch.float64, device=dev)
+    # e2e: the pipelined host entry (hysco_correct_host_stream) over e2e_steps
+    # items; every item's pair is copied in from pinned host memory and its b
+    # and corrected pair copied back inside the timed region (the copies of
+    # items k+1 / k-1 overlap the correction of item k on a second stream).
+    ne = max(2, args.e2e_steps)
+    H.hysco_correct_host_stream(ctx, [hIp] * 2, [hIm] * 2, [hb] * 2, [hTp] * 2, [hTm] * 2, solve_opts=so, batch=B)
+    flush.zero_()
+    torch.cuda.synchronize(dev)
+    a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    a.record(stream)
+    H.hysco_correct_host_stream(ctx, [hIp] * ne, [hIm] * ne, [hb] * ne, [hTp] * ne, [hTm] * ne,
+                                solve_opts=so, batch=B)
+    z.record(stream)
+    z.synchronize()
+    wall_ms = (time.perf_counter() - w0) * 1e3
+    te = torch.tensor([a.elapsed_time(z)], dtype=torch.float64, device=dev)
     if world > 1:
         torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
-    e2e_val = world * B * len(e2e_ms) / (float(te.item()) / 1e3)
+    e2e_val = world * B * ne / (float(te.item()) / 1e3)
     e2e = {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 2 * Nc * 4,
-           "d2h_bytes_per_step": (Nn + 2 * Nc) * 4, "ms_per_step": float(te.item()) / len(e2e_ms)}
+           "d2h_bytes_per_step": (Nn + 2 * Nc) * 4, "ms_per_step": float(te.item()) / ne,
+           "api": "hysco_correct_host_stream (copies of neighbouring items overlap the correction)",
+           "items": ne, "wall_ms_per_step": wall_ms / ne}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

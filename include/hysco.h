@@ -188,6 +188,22 @@ HYSCO_API hysco_status hysco_correct_host(hysco_ctx ctx, const void* h_Iplus, co
                                 void* h_b_out, void* h_Iplus_corr, void* h_Iminus_corr,
                                 hysco_report* reports);
 
+/* A sequence of n_items independent corrections on HOST buffers (pinned for
+ * full speed), pipelined: while item k is corrected on the context stream,
+ * item k+1's pair is copied in and item k-1's results are copied out on a
+ * second, context-owned copy stream (two device staging slots each way), so
+ * the PCIe traffic hides behind the compute.  Item k uses h_Iplus[k],
+ * h_Iminus[k] ([batch][n1][n2][n3]) and writes h_b_out[k], h_Iplus_corr[k],
+ * h_Iminus_corr[k] (each array of pointers may be NULL, or hold NULL
+ * entries, to skip that output).  reports: [n_items][batch] or NULL.
+ * Returns when every copy has completed; the first failing item's status.
+ * Not on slab contexts. */
+HYSCO_API hysco_status hysco_correct_host_stream(hysco_ctx ctx, int32_t n_items, const void* const* h_Iplus,
+                                                 const void* const* h_Iminus, const hysco_ot_opts* ot,
+                                                 const hysco_solve_opts* so, void* const* h_b_out,
+                                                 void* const* h_Iplus_corr, void* const* h_Iminus_corr,
+                                                 hysco_report* reports);
+
 /* Number of kernel launches issued by the last solve / correct call (graph
  * nodes executed, counted on the device). */
 HYSCO_API int64_t hysco_last_launch_count(hysco_ctx ctx);

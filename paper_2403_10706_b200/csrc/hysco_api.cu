@@ -47,6 +47,12 @@ struct hysco_ctx_s {
     void* own_Ip = nullptr;   // host-entry image copies
     void* own_Im = nullptr;
     void* own_Tp = nullptr;   // host-entry corrected images
+    // hysco_correct_host_stream: copy stream, 2 staging slots each way, events
+    cudaStream_t copy_stream = nullptr;
+    void* st_in[2][2] = {};       // [slot][I+, I-]
+    void* st_out[2][3] = {};      // [slot][b, T+, T-]
+    cudaEvent_t ev_h2d[2] = {}, ev_in_free[2] = {}, ev_out[2] = {}, ev_out_free[2] = {};
+    bool stream_ready = false;
     void* own_Tm = nullptr;
     PairState* st = nullptr;
     PairState* h_st = nullptr;          // pinned mirror
@@ -1329,6 +1335,86 @@ hysco_status hysco_correct_host(hysco_ctx ctx, const void* h_Iplus, const void* 
     return s;
 }
 
+static hysco_status stream_setup(hysco_ctx ctx) {
+    if (ctx->stream_ready) return HYSCO_OK;
+    const size_t nc = (size_t)ctx->cfg.batch * ctx->g.Nc * ctx->esz;
+    const size_t nn = (size_t)ctx->cfg.batch * ctx->g.Nn * ctx->esz;
+    CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; k++) {
+        CK(cudaMalloc(&ctx->st_in[k][0], nc));
+        CK(cudaMalloc(&ctx->st_in[k][1], nc));
+        CK(cudaMalloc(&ctx->st_out[k][0], nn));
+        CK(cudaMalloc(&ctx->st_out[k][1], nc));
+        CK(cudaMalloc(&ctx->st_out[k][2], nc));
+        for (cudaEvent_t* e : {&ctx->ev_h2d[k], &ctx->ev_in_free[k], &ctx->ev_out[k], &ctx->ev_out_free[k]}) {
+            CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+            CK(cudaEventRecord(*e, ctx->copy_stream));   // slots start free
+        }
+    }
+    ctx->stream_ready = true;
+    return HYSCO_OK;
+}
+
+hysco_status hysco_correct_host_stream(hysco_ctx ctx, int32_t n_items, const void* const* h_Iplus,
+                                       const void* const* h_Iminus, const hysco_ot_opts* ot,
+                                       const hysco_solve_opts* so, void* const* h_b_out,
+                                       void* const* h_Iplus_corr, void* const* h_Iminus_corr,
+                                       hysco_report* reports) {
+    CHECK_CTX();
+    if (ctx->g.slab) return set_err(ctx, HYSCO_ERR_STATE, "slab contexts support solve / correct / correct_host");
+    if (n_items < 0 || (n_items > 0 && (!h_Iplus || !h_Iminus)))
+        return set_err(ctx, HYSCO_ERR_ARG, "host image arrays must be non-NULL");
+    for (int k = 0; k < n_items; k++)
+        if (!h_Iplus[k] || !h_Iminus[k]) return set_err(ctx, HYSCO_ERR_ARG, "host images must be non-NULL");
+    if (hysco_status s0 = stream_setup(ctx)) return s0;
+    const size_t nc = (size_t)ctx->cfg.batch * ctx->g.Nc * ctx->esz;
+    const size_t nn = (size_t)ctx->cfg.batch * ctx->g.Nn * ctx->esz;
+    auto out_ptr = [](void* const* a, int k) { return a ? a[k] : nullptr; };
+    cudaStream_t cs = ctx->copy_stream, ks = ctx->stream;
+    auto h2d = [&](int k) -> cudaError_t {       // item k -> input slot k % 2 (copy stream)
+        const int sl = k & 1;
+        cudaError_t e = cudaStreamWaitEvent(cs, ctx->ev_in_free[sl], 0);
+        if (!e) e = cudaMemcpyAsync(ctx->st_in[sl][0], h_Iplus[k], nc, cudaMemcpyHostToDevice, cs);
+        if (!e) e = cudaMemcpyAsync(ctx->st_in[sl][1], h_Iminus[k], nc, cudaMemcpyHostToDevice, cs);
+        if (!e) e = cudaEventRecord(ctx->ev_h2d[sl], cs);
+        return e;
+    };
+    if (n_items > 0) CK(h2d(0));
+    if (hysco_status s0 = hysco_bind_images(ctx, ctx->own_Ip, ctx->own_Im)) return s0;
+    hysco_status first_err = HYSCO_OK;
+    for (int k = 0; k < n_items; k++) {
+        const int sl = k & 1;
+        if (k + 1 < n_items) CK(h2d(k + 1));     // next pair streams in during this correction
+        CK(cudaStreamWaitEvent(ks, ctx->ev_h2d[sl], 0));
+        CK(cudaMemcpyAsync(ctx->own_Ip, ctx->st_in[sl][0], nc, cudaMemcpyDeviceToDevice, ks));
+        CK(cudaMemcpyAsync(ctx->own_Im, ctx->st_in[sl][1], nc, cudaMemcpyDeviceToDevice, ks));
+        CK(cudaEventRecord(ctx->ev_in_free[sl], ks));
+        void *hb = out_ptr(h_b_out, k), *hp = out_ptr(h_Iplus_corr, k), *hm = out_ptr(h_Iminus_corr, k);
+        hysco_status s = solve_common(ctx, 2, ot, so, nullptr, nullptr, hp ? ctx->own_Tp : nullptr,
+                                      hm ? ctx->own_Tm : nullptr,
+                                      reports ? reports + (size_t)k * ctx->cfg.batch : nullptr);
+        if (s < 0) {
+            if (first_err == HYSCO_OK) first_err = s;
+            continue;
+        }
+        if (s != HYSCO_OK && first_err == HYSCO_OK) first_err = s;
+        // results -> output slot (compute stream), then out to the host (copy stream)
+        CK(cudaStreamWaitEvent(ks, ctx->ev_out_free[sl], 0));
+        if (hb) CK(copy_nodes(ctx, ctx->st_out[sl][0], ctx->buf[B_B], false, cudaMemcpyDeviceToDevice));
+        if (hp) CK(cudaMemcpyAsync(ctx->st_out[sl][1], ctx->own_Tp, nc, cudaMemcpyDeviceToDevice, ks));
+        if (hm) CK(cudaMemcpyAsync(ctx->st_out[sl][2], ctx->own_Tm, nc, cudaMemcpyDeviceToDevice, ks));
+        CK(cudaEventRecord(ctx->ev_out[sl], ks));
+        CK(cudaStreamWaitEvent(cs, ctx->ev_out[sl], 0));
+        if (hb) CK(cudaMemcpyAsync(hb, ctx->st_out[sl][0], nn, cudaMemcpyDeviceToHost, cs));
+        if (hp) CK(cudaMemcpyAsync(hp, ctx->st_out[sl][1], nc, cudaMemcpyDeviceToHost, cs));
+        if (hm) CK(cudaMemcpyAsync(hm, ctx->st_out[sl][2], nc, cudaMemcpyDeviceToHost, cs));
+        CK(cudaEventRecord(ctx->ev_out_free[sl], cs));
+    }
+    CK(cudaStreamSynchronize(cs));
+    CK(cudaStreamSynchronize(ks));
+    return first_err;
+}
+
 int64_t hysco_last_launch_count(hysco_ctx ctx) { return ctx ? ctx->last_launches : -1; }
 
 hysco_status hysco_nccl_unique_id(unsigned char id_out[128]) {
@@ -1559,6 +1645,15 @@ hysco_status hysco_destroy(hysco_ctx ctx) {
     if (ctx->flush) cudaFree(ctx->flush);
     if (ctx->res_part) cudaFree(ctx->res_part);
     if (ctx->res_flags) cudaFree(ctx->res_flags);
+    if (ctx->stream_ready) {
+        for (int k = 0; k < 2; k++) {
+            for (void* q : {ctx->st_in[k][0], ctx->st_in[k][1], ctx->st_out[k][0], ctx->st_out[k][1], ctx->st_out[k][2]})
+                if (q) cudaFree(q);
+            for (cudaEvent_t e : {ctx->ev_h2d[k], ctx->ev_in_free[k], ctx->ev_out[k], ctx->ev_out_free[k]})
+                if (e) cudaEventDestroy(e);
+        }
+        cudaStreamDestroy(ctx->copy_stream);
+    }
     if (ctx->res_pg) cudaFree(ctx->res_pg);
     if (ctx->res_x) cudaFree(ctx->res_x);
     if (ctx->red) cudaFree(ctx->red);

@@ -23,7 +23,8 @@ STOP_NAMES = {0: "maxiter", 1: "grad", 2: "dJ", 3: "db", 4: "ls_fail", 5: "infea
 EXPORTED = ["hysco_default_solve_opts", "hysco_default_ot_opts", "hysco_create", "hysco_bind_images",
             "hysco_ot_init", "hysco_objective_grad", "hysco_hessvec", "hysco_hess_diag", "hysco_precond_solve",
             "hysco_solve",
-            "hysco_apply", "hysco_correct", "hysco_correct_host", "hysco_last_launch_count",
+            "hysco_apply", "hysco_correct", "hysco_correct_host", "hysco_correct_host_stream",
+            "hysco_last_launch_count",
             "hysco_last_error", "hysco_destroy", "hysco_version", "hysco_profile_kernels",
             "hysco_nccl_unique_id", "hysco_create_slab", "hysco_create_loopback", "hysco_group_correct",
             "hysco_group_solve"]
@@ -100,6 +101,11 @@ def lib():
                                 ctypes.POINTER(hysco_report)]
     L.hysco_correct_host.argtypes = [vp, vp, vp, ctypes.POINTER(hysco_ot_opts), ctypes.POINTER(hysco_solve_opts),
                                      vp, vp, vp, ctypes.POINTER(hysco_report)]
+    L.hysco_correct_host_stream.argtypes = [vp, ctypes.c_int32, ctypes.POINTER(vp), ctypes.POINTER(vp),
+                                            ctypes.POINTER(hysco_ot_opts), ctypes.POINTER(hysco_solve_opts),
+                                            ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp),
+                                            ctypes.POINTER(hysco_report)]
+    L.hysco_correct_host_stream.restype = st
     for f in ("hysco_create", "hysco_bind_images", "hysco_ot_init", "hysco_objective_grad", "hysco_hessvec",
               "hysco_hess_diag", "hysco_precond_solve", "hysco_solve", "hysco_apply", "hysco_correct",
               "hysco_correct_host",
@@ -223,6 +229,29 @@ def hysco_correct(ctx, b_out=None, Ip_corr=None, Im_corr=None, ot_opts=None, sol
                                         _ptr(b_out), _ptr(Ip_corr), _ptr(Im_corr), reps),
                (HYSCO_OK, HYSCO_INFEASIBLE))
     return [r.as_dict() for r in reps], s == HYSCO_INFEASIBLE
+
+
+def hysco_correct_host_stream(ctx, Ips, Ims, b_outs=None, Ip_corrs=None, Im_corrs=None, ot_opts=None,
+                              solve_opts=None, batch=1):
+    """Pipelined corrections of len(Ips) items on host (pinned) buffers; returns
+    (reports per item, any infeasible)."""
+    n = len(Ips)
+
+    def arr(xs):
+        if xs is None:
+            return None
+        a = (ctypes.c_void_p * n)()
+        for k, x in enumerate(xs):
+            a[k] = _ptr(x)
+        return a
+    reps = (hysco_report * (n * batch))()
+    s = _check(ctx, lib().hysco_correct_host_stream(ctx, n, arr(Ips), arr(Ims),
+                                                    ctypes.byref(ot_opts) if ot_opts is not None else None,
+                                                    ctypes.byref(solve_opts) if solve_opts is not None else None,
+                                                    arr(b_outs), arr(Ip_corrs), arr(Im_corrs), reps),
+               (HYSCO_OK, HYSCO_INFEASIBLE))
+    out = [r.as_dict() for r in reps]
+    return [out[k * batch:(k + 1) * batch] for k in range(n)], s == HYSCO_INFEASIBLE
 
 
 def hysco_correct_host(ctx, Ip, Im, b_out=None, Ip_corr=None, Im_corr=None, ot_opts=None, solve_opts=None,

@@ -518,3 +518,28 @@ def test_block_precond_long_columns(dtype):
     assert reps[0]["pcg_iters"] == rep["pcg_iters"]
     assert rel(c.np(b)[0], bref) <= TOL[dtype]["solve"]
     c.close()
+
+
+def test_correct_host_stream_equals_per_item_correct():
+    """The pipelined host entry (copy-in of item k+1 and copy-out of item k-1
+    overlap the correction of item k) returns, for every item, exactly what a
+    per-item hysco_correct returns on the same pair; NULL outputs are skipped."""
+    shape, h = (10, 9, 24), (1.25, 1.25, 1.25)
+    pairs = [phantom.make_pair(shape, h, 60 + k) for k in range(3)]
+    c = Ctx([pairs[0].Ip], [pairs[0].Im], h)
+    n1, n2, n3 = shape
+    hI = [(torch.from_numpy(p.Ip[None].copy()).pin_memory(), torch.from_numpy(p.Im[None].copy()).pin_memory())
+          for p in pairs]
+    hb = [torch.zeros((1, n1, n2, n3 + 1)).pin_memory() for _ in pairs]
+    hTp = [torch.zeros((1, n1, n2, n3)).pin_memory() for _ in pairs]
+    reps, inf = H.hysco_correct_host_stream(c.ctx, [a for a, _ in hI], [m for _, m in hI], b_outs=hb,
+                                            Ip_corrs=hTp, Im_corrs=None)
+    assert not inf and len(reps) == 3
+    for k, p in enumerate(pairs):
+        ck = Ctx([p.Ip], [p.Im], h)
+        b, Tp, Tm = ck.nodes(), ck.cells(), ck.cells()
+        rk, _ = H.hysco_correct(ck.ctx, b, Tp, Tm)
+        assert torch.equal(hb[k], b.cpu()) and torch.equal(hTp[k], Tp.cpu())
+        assert reps[k][0]["J"] == rk[0]["J"] and reps[k][0]["gn_iters"] == rk[0]["gn_iters"]
+        ck.close()
+    c.close()
