@@ -417,8 +417,9 @@ def run_slab(args):
     Tp = torch.zeros((1, i1 - i0, n2, n3), dtype=torch.float32, device=dev)
     Tm = torch.zeros_like(Tp)
     flush = torch.empty(256 << 18, dtype=torch.float32, device=dev)
+    so = solve_opts(H, args)
     for _ in range(max(args.warmup, 0)):
-        H.hysco_correct(ctx, b, Tp, Tm)
+        H.hysco_correct(ctx, b, Tp, Tm, solve_opts=so)
     torch.cuda.synchronize(dev)
     if world > 1:
         torch.distributed.barrier()
@@ -432,7 +433,7 @@ def run_slab(args):
         flush.zero_()
         a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        reps, _ = H.hysco_correct(ctx, b, Tp, Tm)
+        reps, _ = H.hysco_correct(ctx, b, Tp, Tm, solve_opts=so)
         z.record(stream)
         z.synchronize()
         step_ms.append(a.elapsed_time(z))
@@ -452,7 +453,7 @@ def run_slab(args):
                 "unit": "pairs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": total / args.steps, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": dict(workload_desc(args.config, 1), parallelism=f"slab{world} along dim 1 (NCCL halo + allreduce)"),
+                "config": dict(workload_desc(args.config, 1, args), parallelism=f"slab{world} along dim 1 (NCCL halo + allreduce)"),
                 "clocks": clocks, "gpu_launches": launches,
                 "step_effective_gbs_per_gpu": step_bytes / world / (total / args.steps * 1e-3) / 1e9,
                 "solver": {k: r0[k] for k in ("gn_iters", "f_evals", "h_evals", "pcg_iters", "stop", "J")}}

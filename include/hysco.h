@@ -102,7 +102,7 @@ typedef struct {
                                 HYSCO_PRECOND_PE_BLOCK: z = B^{-1} r with B the per-PE-column
                                 tridiagonal blocks of H_J, the block-diagonal preconditioner
                                 named in P:200 (R20).  PE_BLOCK runs the streaming
-                                PCG kernels and is not available on slab contexts            */
+                                PCG kernels (column-local: slabs need no extra exchange)    */
 } hysco_solve_opts;
 
 enum { HYSCO_PRECOND_JACOBI = 0, HYSCO_PRECOND_PE_BLOCK = 1 };

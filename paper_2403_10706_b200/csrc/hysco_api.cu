@@ -150,8 +150,6 @@ static hysco_status check_opts(hysco_ctx ctx, const hysco_solve_opts& o, const h
     if (!(t.eps >= 0) || !(t.feas_cap > 0)) return set_err(ctx, HYSCO_ERR_ARG, "bad hysco_ot_opts");
     if (o.precond != HYSCO_PRECOND_JACOBI && o.precond != HYSCO_PRECOND_PE_BLOCK)
         return set_err(ctx, HYSCO_ERR_ARG, "bad hysco_solve_opts.precond");
-    if (o.precond == HYSCO_PRECOND_PE_BLOCK && ctx->g.slab)
-        return set_err(ctx, HYSCO_ERR_ARG, "the block preconditioner is not available on slab contexts");
     return HYSCO_OK;
 }
 
@@ -657,14 +655,40 @@ struct SlabRun {
     }
     void gn() {
         eval(EVAL_GN_START);
+        const bool blk = sp.precond == HYSCO_PRECOND_PE_BLOCK;   // column-local: no extra exchange (R20)
         while (cond(COND_GN)) {
-            each([&](hysco_ctx c) {
-                NCH_SWITCH(c->nch, pcg_init_kernel<T, NCH><<<gn(c), 256, 0, c->stream>>>(
-                                       c->g, c->ctl, L<T>::b(c, B_GRAD), L<T>::b(c, B_DT), L<T>::b(c, B_X),
-                                       L<T>::b(c, B_R), L<T>::b(c, B_P)));
-            });
+            if (blk) {
+                each([&](hysco_ctx c) { L<T>::pcg_init_blk(c, sp); });
+            } else {
+                each([&](hysco_ctx c) {
+                    NCH_SWITCH(c->nch, pcg_init_kernel<T, NCH><<<gn(c), 256, 0, c->stream>>>(
+                                           c->g, c->ctl, L<T>::b(c, B_GRAD), L<T>::b(c, B_DT), L<T>::b(c, B_X),
+                                           L<T>::b(c, B_R), L<T>::b(c, B_P)));
+                });
+            }
             reduce_decide(OP_PCG_INIT, 0, false);
-            while (cond(COND_PCG)) {
+            while (blk && cond(COND_PCG)) {
+                ok(comm->halo(R, B_P, false));
+                each([&](hysco_ctx c) {
+                    NCH_SWITCH(c->nch, matvec_kernel<T, NCH, true><<<dim3(c->gx_mv, c->cfg.batch), 256, 0, c->stream>>>(
+                                           c->g, c->ctl, L<T>::b(c, B_DT), L<T>::b(c, B_ET), L<T>::b(c, B_P),
+                                           L<T>::b(c, B_HP)));
+                });
+                reduce_decide(OP_MATVEC, 0, false);
+                each([&](hysco_ctx c) {
+                    NCH_SWITCH(c->nch, pcg_blk_kernel<T, NCH, false><<<gn(c), 256, 0, c->stream>>>(
+                                           c->g, c->ctl, sp, L<T>::b(c, B_GRAD), L<T>::b(c, B_P), L<T>::b(c, B_HP),
+                                           L<T>::b(c, B_X), L<T>::b(c, B_R), L<T>::b(c, B_W), L<T>::b(c, B_ET),
+                                           L<T>::b(c, B_F), L<T>::b(c, B_TMP)));
+                });
+                reduce_decide(OP_UPDATE, 0, false);
+                each([&](hysco_ctx c) {
+                    NCH_SWITCH(c->nch, pcg_dir_blk_kernel<T, NCH><<<gn(c), 256, 0, c->stream>>>(
+                                           c->g, c->ctl, L<T>::b(c, B_TMP), L<T>::b(c, B_P)));
+                });
+                if (err != cudaSuccess) return;
+            }
+            while (!blk && cond(COND_PCG)) {
                 ok(comm->halo(R, B_P, false));
                 each([&](hysco_ctx c) {
                     NCH_SWITCH(c->nch, matvec_kernel<T, NCH, true><<<dim3(c->gx_mv, c->cfg.batch), 256, 0, c->stream>>>(

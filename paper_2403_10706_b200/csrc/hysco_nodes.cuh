@@ -544,6 +544,10 @@ __global__ void __launch_bounds__(256) pcg_blk_kernel(Geom g, Ctl c, SolveParams
     double v[2] = {arz, arr}, tot[2];
     if (!pair_reduce<2, 0u>(c, v, tot)) return;
     if (threadIdx.x != 0) return;
+    if (c.defer) {                       // multi-rank: OP_PCG_INIT / OP_UPDATE after the allreduce
+        store_red(c, pair, gridDim.y, tot, 2, 0);
+        return;
+    }
     if (INIT) decide_pcg_init(c.st[pair], tot);
     else decide_update(sp, c.st[pair], tot);
     if (last_pair(c)) set_cond(c, COND_PCG, any_pair(c, gridDim.y, [](volatile PairState* q) { return q->pcg_active != 0; }));

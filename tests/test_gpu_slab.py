@@ -106,6 +106,22 @@ def test_loopback_slabs_long_columns_f64():
     assert rel(b1[0], bref) <= 1e-9
 
 
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_loopback_slabs_block_precond_f64(nranks):
+    """The block preconditioner (R20) is column-local, so slabs run it with no
+    extra exchange: equal to the single-context block solve, fixed and with the
+    paper's stop rules."""
+    p = phantom.make_pair((9, 7, 30), (1.2, 1.0, 1.1), 23)
+    Ip, Im = p.Ip[None].astype(np.float64), p.Im[None].astype(np.float64)
+    for so in (H.default_solve_opts(armijo=0, precond=H.HYSCO_PRECOND_PE_BLOCK),
+               H.default_solve_opts(fixed_iters=0, max_gn=20, precond=H.HYSCO_PRECOND_PE_BLOCK)):
+        b1, tp1, _, r1 = single(Ip, Im, p.h, H.HYSCO_F64, so, 1)
+        b2, tp2, _, r2, _ = grouped(Ip, Im, p.h, H.HYSCO_F64, so, 1, nranks)
+        assert (r2[0]["gn_iters"], r2[0]["pcg_iters"], r2[0]["stop_reason"]) == \
+            (r1[0]["gn_iters"], r1[0]["pcg_iters"], r1[0]["stop_reason"])
+        assert rel(b2, b1) <= 1e-11 and rel(tp2, tp1) <= 1e-11
+
+
 def test_loopback_single_plane_slabs_periodic_blur():
     """Every rank owns one plane: the periodic blur ring and the Neumann ends
     are all exchange-driven."""
