@@ -75,6 +75,7 @@ class Ctx:
 
     @staticmethod
     def np(t):
+        torch.cuda.synchronize()          # results written on the context stream
         return t.detach().cpu().numpy().astype(np.float64)
 
 
@@ -486,8 +487,9 @@ def test_block_precond_hcp3t_production_and_fixed_f32(hcp3t):
     c = Ctx([p.Ip], [p.Im], p.h)
     b0 = c.nodes()
     H.hysco_ot_init(c.ctx, b0)
+    torch.cuda.synchronize()      # the context runs on its own stream; torch's clone must see b0
     b = b0.clone()
-    torch.cuda.synchronize()      # clones run on torch's stream, the context on its own
+    torch.cuda.synchronize()
     reps, inf = H.hysco_solve(c.ctx, b, H.default_solve_opts(fixed_iters=0, max_gn=50,
                                                               precond=H.HYSCO_PRECOND_PE_BLOCK))
     assert not inf and reps[0]["stop_reason"] not in (4, 5)   # no line-search failure, feasible
