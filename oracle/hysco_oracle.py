@@ -590,3 +590,166 @@ def relative_improvement(Ip, Im, Tp, Tm):
     Ip = np.asarray(Ip, np.float64)
     Im = np.asarray(Im, np.float64)
     return 100.0 * (1.0 - float(np.sum((Tp - Tm) ** 2)) / float(np.sum((Ip - Im) ** 2)))
+
+
+# ---------------------------------------------------------------------------
+# ADMM.  Readings R21-R26 in DESIGN.md.
+#   F(b) = D(b) + alpha S3(b) + beta P(b)        (column-separable)
+#   G(z) = alpha (S1(z) + S2(z))                 (in-plane smoothness)
+#   b <- argmin_b F(b) + rho hd/2 ||b - z + u||^2   (Eq. x_update)
+#   z <- argmin_z G(z) + rho hd/2 ||b - z + u||^2   (Eq. z_update)
+#   u <- u + b - z                                  (Eq. u_update)
+# rho adapted as in Boyd et al. 2011 §3.4.1; stop when b, z and u all
+# change by less than a tolerance.
+# ---------------------------------------------------------------------------
+
+
+class ColState:
+    """Per-PE-column objective of the ADMM b-update and its derivatives."""
+
+
+def admm_b_objective(Ip, Im, b, v, h, alpha=ALPHA_DEFAULT, beta=BETA_DEFAULT, rho=1.0, derivs=True):
+    """Fc(b) = D + alpha S3 + beta P + rho hd/2 ||b - v||^2 per PE column (R21):
+    D, P as in `evaluate` (Eq.(2), Eq.(3)), S3 = hd/2 sum ||D3 b||^2 / h3^2 (the PE
+    part of Eq.(5)).  Returns ColState with F (per column, +inf if infeasible),
+    and with derivs: grad (nodes) and the column-tridiagonal GN Hessian
+    d (diagonal), e (H[l, l+1]) -- data (Gauss-Newton) + alpha hd D3^T D3 / h3^2
+    + beta hd/2 D^T phi'' D + rho hd I."""
+    Ip = np.asarray(Ip, np.float64)
+    Im = np.asarray(Im, np.float64)
+    b = np.asarray(b, np.float64)
+    h1, h2, h3 = (float(x) for x in h)
+    hd = h1 * h2 * h3
+    n3 = Ip.shape[-1]
+    k = np.arange(n3, dtype=np.float64)
+    cs = ColState()
+    Ab = avg_pe(b)
+    Db = diff_pe(b, h3)
+    infeas = np.any(np.abs(Db) >= 1.0, axis=-1)
+    vp, sp = interp_pe(Ip, k + Ab / h3)
+    vm, sm = interp_pe(Im, k - Ab / h3)
+    r = vp * (1.0 + Db) - vm * (1.0 - Db)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        ph = np.where(np.abs(Db) < 1.0, phi(np.where(np.abs(Db) < 1.0, Db, 0.0)), np.inf)
+    Dc = 0.5 * hd * np.sum(r * r, axis=-1)
+    S3c = 0.5 * hd * np.sum(((b[..., 1:] - b[..., :-1]) / h3) ** 2, axis=-1)
+    Pc = 0.5 * hd * np.sum(np.where(np.abs(Db) < 1.0, ph, 0.0), axis=-1)
+    Xc = 0.5 * hd * np.sum((b - v) ** 2, axis=-1)
+    cs.F = np.where(infeas, np.inf, Dc + alpha * S3c + beta * Pc + rho * Xc)
+    cs.infeasible = infeas
+    if not derivs:
+        return cs
+    Dbs = np.where(np.abs(Db) < 1.0, Db, 0.0)
+    g = (sp / h3) * (1.0 + Db) + (sm / h3) * (1.0 - Db)
+    s = vp + vm
+    LPE = diff_pe_T(diff_pe(b, h3), h3)            # D3^T D3 b / h3^2
+    cs.grad = (hd * (avg_pe_T(g * r) + diff_pe_T(s * r, h3)) + alpha * hd * LPE
+               + beta * 0.5 * hd * diff_pe_T(dphi(Dbs), h3) + rho * hd * (b - v))
+    a = g / 2.0 - s / h3
+    c = g / 2.0 + s / h3
+    p2 = d2phi(Dbs)
+    d = np.zeros(b.shape)
+    d[..., :-1] += hd * a ** 2 + beta * 0.5 * hd * p2 / h3 ** 2 + alpha * hd / h3 ** 2
+    d[..., 1:] += hd * c ** 2 + beta * 0.5 * hd * p2 / h3 ** 2 + alpha * hd / h3 ** 2
+    cs.d = d + rho * hd
+    cs.e = hd * a * c - beta * 0.5 * hd * p2 / h3 ** 2 - alpha * hd / h3 ** 2
+    return cs
+
+
+def admm_b_update(Ip, Im, b, v, h, alpha=ALPHA_DEFAULT, beta=BETA_DEFAULT, rho=1.0, inner=2,
+                  c1=1e-4, ls_max=10):
+    """b-update: `inner` Gauss-Newton steps on every PE column
+    independently.  The column system H_col q = -grad_col is tridiagonal, so the
+    per-column ("BlockPCG") solve is exact (Thomas, R23); each column takes its
+    own Armijo step gamma in {1, 1/2, ...} on its own Fc ("different step
+    sizes ... for each image column"); a column without an acceptable step keeps b."""
+    b = np.asarray(b, np.float64).copy()
+    for _ in range(inner):
+        cs = admm_b_objective(Ip, Im, b, v, h, alpha, beta, rho)
+        if np.all(cs.infeasible):
+            break
+        q = -solve_tridiag_pe(cs.d, cs.e, np.where(cs.infeasible[..., None], 0.0, cs.grad))
+        gq = np.sum(cs.grad * q, axis=-1)
+        gamma = np.ones(b.shape[:-1])
+        done = cs.infeasible.copy()
+        bn = b.copy()
+        for _t in range(ls_max):
+            cand = b + gamma[..., None] * q
+            ct = admm_b_objective(Ip, Im, cand, v, h, alpha, beta, rho, derivs=False)
+            ok = (~done) & (~ct.infeasible) & (ct.F <= cs.F + c1 * gamma * gq)
+            bn[ok] = cand[ok]
+            done |= ok
+            gamma = np.where(done, gamma, 0.5 * gamma)
+        b = bn
+    return b
+
+
+def periodic_laplacian_xy(z, h):
+    """alpha-free in-plane operator of G: sum_{d=1,2} D_d^T D_d z / h_d^2 with
+    periodic differences (the BCCB structure P:236-237 assumes), by rolls."""
+    out = np.zeros(z.shape)
+    for ax in (0, 1):
+        dz = np.roll(z, -1, axis=ax) - z                 # forward difference, periodic
+        out += (np.roll(dz, 1, axis=ax) - dz) / h[ax] ** 2
+    return out
+
+
+def admm_z_update(b, u, h, alpha=ALPHA_DEFAULT, rho=1.0):
+    """z-update: (alpha hd L_xy^per + rho hd I) z = rho hd (b + u)
+    on every PE node slice, solved by the 2-D FFT that diagonalises the periodic
+    (BCCB) operator: eigenvalues 4 sin^2(pi k / n) / h^2 per axis."""
+    n1, n2 = b.shape[0], b.shape[1]
+    lam = (4.0 * np.sin(np.pi * np.arange(n1) / n1) ** 2 / h[0] ** 2)[:, None] + \
+          (4.0 * np.sin(np.pi * np.arange(n2) / n2) ** 2 / h[1] ** 2)[None, :]
+    F = np.fft.fft2(rho * (b + u), axes=(0, 1))
+    return np.real(np.fft.ifft2(F / (alpha * lam + rho)[..., None], axes=(0, 1)))
+
+
+def admm_rho_update(rho, r_norm, s_norm, mu=10.0, tau=2.0):
+    """Residual balancing (Boyd et al. 2011 §3.4.1): returns (rho', factor)
+    where the scaled multiplier u must be multiplied by `factor` = rho/rho'."""
+    if r_norm > mu * s_norm:
+        return rho * tau, 1.0 / tau
+    if s_norm > mu * r_norm:
+        return rho / tau, tau
+    return rho, 1.0
+
+
+def admm_rho0(h, alpha=ALPHA_DEFAULT):
+    """Initial augmentation (unspecified in the paper, R24): alpha (1/h1^2 + 1/h2^2),
+    the diagonal scale of the in-plane regulariser it splits off."""
+    return alpha * (1.0 / h[0] ** 2 + 1.0 / h[1] ** 2)
+
+
+def admm(Ip, Im, b0, h, alpha=ALPHA_DEFAULT, beta=BETA_DEFAULT, rho0=None, max_iter=20, inner=2,
+         tol=1e-3, fixed=False, mu=10.0, tau=2.0):
+    """ADMM field-map solve.  z0 = b0, u0 = 0, rho0 (R24).  Per
+    iteration: b-update, z-update, u-update, residual balancing of rho (R25).
+    Stop (not fixed): ||b - b_prev||, ||z - z_prev|| and ||u - u_prev|| all
+    <= tol * max(||b||, tiny) (R26).  Returns (b, z, report)."""
+    b = np.asarray(b0, np.float64).copy()
+    z = b.copy()
+    u = np.zeros_like(b)
+    rho = admm_rho0(h, alpha) if rho0 is None else float(rho0)
+    rep = {"iters": 0, "rho": [], "r_norm": [], "s_norm": [], "stop": "maxiter"}
+    for _k in range(max_iter):
+        b_prev, z_prev, u_prev = b, z, u
+        b = admm_b_update(Ip, Im, b, z - u, h, alpha, beta, rho, inner)
+        z = admm_z_update(b, u, h, alpha, rho)
+        u = u + b - z
+        r_norm = float(np.linalg.norm(b - z))
+        s_norm = rho * float(np.linalg.norm(z - z_prev))
+        rep["iters"] += 1
+        rep["rho"].append(rho)
+        rep["r_norm"].append(r_norm)
+        rep["s_norm"].append(s_norm)
+        db = float(np.linalg.norm(b - b_prev))
+        dz = float(np.linalg.norm(z - z_prev))
+        du = float(np.linalg.norm(u - u_prev))
+        rho, f = admm_rho_update(rho, r_norm, s_norm, mu, tau)
+        u = u * f
+        if not fixed and max(db, dz, du) <= tol * max(float(np.linalg.norm(b)), 1e-300):
+            rep["stop"] = "converged"
+            break
+    rep["rho_final"] = rho
+    return b, z, rep
