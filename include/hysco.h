@@ -169,6 +169,38 @@ HYSCO_API hysco_status hysco_precond_solve(hysco_ctx ctx, int kind, const void* 
 HYSCO_API hysco_status hysco_solve(hysco_ctx ctx, void* d_b_inout, const hysco_solve_opts* opts,
                          hysco_report* reports);
 
+/* ADMM options (readings R21-R26 in DESIGN.md). */
+typedef struct {
+    int32_t max_iter;        /* ADMM iterations (fixed mode: exactly this many), default 20        */
+    int32_t inner;           /* Gauss-Newton steps per b-update (per column), default 2             */
+    int32_t ls_max;          /* Armijo tries per column step, default 10                             */
+    int32_t fixed_iters;     /* 1: no convergence stop; 0: stop when b, z, u change < tol   */
+    double tol;              /* relative change tolerance, default 1e-3 (R26)                       */
+    double rho0;             /* initial augmentation; <= 0: alpha (1/h1^2 + 1/h2^2) (R24)          */
+    double mu, tau;          /* residual balancing (Boyd et al. 2011 §3.4.1), default 10, 2 (R25)   */
+    double armijo_c1;        /* default 1e-4                                                         */
+} hysco_admm_opts;
+
+/* Per-pair ADMM result. */
+typedef struct {
+    int32_t iters;           /* ADMM iterations run                          */
+    int32_t converged;       /* 1: stopped on the change tolerance            */
+    double rho;              /* final augmentation parameter                  */
+    double r_norm, s_norm;   /* last primal / dual residual norms             */
+    double J, D, S, P;       /* objective (Eq.(6), Neumann S) at the returned b */
+} hysco_admm_report;
+
+HYSCO_API void hysco_default_admm_opts(hysco_admm_opts* o);
+
+/* ADMM field-map solve from d_b_inout (device nodes; e.g. the OT start):
+ * b-update = per-column Gauss-Newton with exact tridiagonal solves and
+ * per-column Armijo steps (no communication), z-update = periodic in-plane
+ * solve by 2-D FFTs (cuFFT) per PE node slice, u-update, residual-balancing
+ * of rho on the host between iterations.  Writes the final b.  reports:
+ * [batch] or NULL.  Not on slab contexts (the z-update is global in-plane). */
+HYSCO_API hysco_status hysco_admm(hysco_ctx ctx, void* d_b_inout, const hysco_admm_opts* opts,
+                                  hysco_admm_report* reports);
+
 /* Jacobian-modulation correction: the two corrected images
  * T[I+, b, v], T[I-, b, -v] (device cells). */
 HYSCO_API hysco_status hysco_apply(hysco_ctx ctx, const void* d_b, void* d_Iplus_corr, void* d_Iminus_corr);

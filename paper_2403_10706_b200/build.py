@@ -30,6 +30,18 @@ def nccl_dirs():
     return None, None
 
 
+def cufft_dir():
+    """torch's bundled cuFFT (one libcufft.so.11 in the process, like NCCL)."""
+    try:
+        import nvidia.cufft as nf
+        d = os.path.join(list(nf.__path__)[0], "lib")
+        if os.path.exists(os.path.join(d, "libcufft.so.11")):
+            return d
+    except Exception:
+        pass
+    return None
+
+
 def needs_build():
     if not os.path.exists(LIB):
         return True
@@ -42,7 +54,9 @@ def build(force=False, verbose=False):
     if force or needs_build():
         inc, libd = nccl_dirs()
         nccl = ["-I" + inc, "-L" + libd, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + libd] if inc else ["-lnccl"]
-        cmd = [NVCC] + FLAGS + ["-o", LIB + ".tmp", SRC] + nccl
+        fdir = cufft_dir()
+        cufft = ["-L" + fdir, "-l:libcufft.so.11", "-Xlinker", "-rpath=" + fdir] if fdir else ["-lcufft"]
+        cmd = [NVCC] + FLAGS + ["-o", LIB + ".tmp", SRC] + nccl + cufft
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)

@@ -1,0 +1,274 @@
+// hysco_admm.cuh — ADMM field-map solve (
+// readings R21-R26 in DESIGN.md), sm_100a.
+//
+//   b <- argmin F(b) + rho hd/2 ||b - z + u||^2,  F = D + alpha S3 + beta P
+//        (column-separable: one warp per PE column runs `inner` Gauss-Newton
+//        steps, each an exact tridiagonal (Thomas) solve and its own Armijo
+//        search on the column objective -- no grid-wide communication)
+//   z <- (alpha hd L_xy^per + rho hd I)^{-1} rho hd (b + u)
+//        (periodic in-plane operator, diagonalised by 2-D FFTs over (n1, n2)
+//        for every PE node slice: cuFFT R2C / C2R, batch = P, stride = P)
+//   u <- u + b - z;  residual norms per pair -> rho balancing on the host.
+#pragma once
+
+namespace hysco {
+
+constexpr int ADMM_WARPS = 4;   // columns per CTA (one warp each)
+
+// Per-warp shared scratch (elements): I+, I- padded by two zeros per side,
+// b, v = z - u, q, grad, diag, offdiag, trial b (nodes), and the cell
+// quantities a, c, r, phi', phi''.
+__host__ __device__ inline size_t admm_warp_elems(int n3) {
+    const size_t P = (size_t)n3 + 1;
+    return 2 * ((size_t)n3 + 4) + 7 * P + 5 * (size_t)n3;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum_t(T x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
+    return x;
+}
+
+// Column objective Fc at column b (shared): D + alpha S3 + beta P + rho hd/2 ||b - v||^2
+// (all lanes get it; +inf if infeasible).  With DERIVS: the cell quantities
+// and then grad, diag, offdiag of the column GN Hessian (oracle
+// admm_b_objective).
+template <typename T, bool DERIVS>
+__device__ double admm_col_eval(const Geom& g, int lane, const T* sIp, const T* sIm, const T* sb, const T* sv, T rho,
+                                T* sa, T* sc, T* sr, T* sp1, T* sp2, T* sg, T* sd, T* se) {
+    const int n3 = g.n3, P = g.P;
+    const T hd = gw<T>(g.hd, g.f_hd), ahd = gw<T>(g.ahd, g.f_ahd), bh2 = gw<T>(g.bh2, g.f_bh2);
+    const T ih3 = gw<T>(g.ih3, g.f_ih3), ih3sq = gw<T>(g.ih3sq, g.f_ih3sq);
+    double aD = 0, aS = 0, aP = 0, aX = 0;
+    int inf = 0;
+    for (int k = lane; k < n3; k += 32) {
+        const T b0 = sb[k], b1 = sb[k + 1];
+        const T Ab = T(0.5) * (b0 + b1);
+        const T Db = diff_h3(b0, b1, g);
+        double vp, vm;
+        T spl, sml;
+        gather_pm(sIp, sIm, n3, k, Ab, g, vp, vm, spl, sml);
+        const double Dbd = (double)Db;
+        const double rd = vp * (1.0 + Dbd) - vm * (1.0 - Dbd);
+        aD = fma(rd, rd, aD);
+        const T dd = (b1 - b0) * ih3;
+        aS += (double)(dd * dd);
+        T f0 = 0, p1 = 0, p2 = 0;
+        if (fabs(Db) >= T(1)) inf = 1;
+        else phi3(Db, f0, p1, p2);
+        aP += (double)f0;
+        if (DERIVS) {
+            const T gg = (spl * (T(1) + Db) + sml * (T(1) - Db)) * ih3;
+            const T s = (T)(vp + vm);
+            sa[k] = gg * T(0.5) - s * ih3;
+            sc[k] = gg * T(0.5) + s * ih3;
+            sr[k] = (T)rd;
+            sp1[k] = p1;
+            sp2[k] = p2;
+        }
+    }
+    for (int l = lane; l < P; l += 32) {
+        const double dx = (double)sb[l] - (double)sv[l];
+        aX = fma(dx, dx, aX);
+    }
+    aD = warp_sum_t(aD);
+    aS = warp_sum_t(aS);
+    aP = warp_sum_t(aP);
+    aX = warp_sum_t(aX);
+    inf = __any_sync(FULL, inf);
+    const double F = inf ? INFINITY
+                         : 0.5 * g.hd * (aD + g.alpha * aS + g.beta * aP + (double)rho * aX);
+    if (DERIVS && !inf) {
+        __syncwarp();
+        for (int l = lane; l < P; l += 32) {
+            const T bl = sb[l];
+            T gr = rho * hd * (bl - sv[l]), d = rho * hd, e = T(0);
+            if (l > 0) {
+                const int k = l - 1;
+                gr += hd * sc[k] * sr[k] + ahd * (bl - sb[l - 1]) * ih3sq + bh2 * sp1[k] * ih3;
+                d += hd * sc[k] * sc[k] + bh2 * sp2[k] * ih3sq + ahd * ih3sq;
+            }
+            if (l < n3) {
+                const int k = l;
+                gr += hd * sa[k] * sr[k] + ahd * (bl - sb[l + 1]) * ih3sq - bh2 * sp1[k] * ih3;
+                d += hd * sa[k] * sa[k] + bh2 * sp2[k] * ih3sq + ahd * ih3sq;
+                e = hd * sa[k] * sc[k] - bh2 * sp2[k] * ih3sq - ahd * ih3sq;
+            }
+            sg[l] = gr;
+            sd[l] = d;
+            se[l] = e;
+        }
+        __syncwarp();
+    }
+    return F;
+}
+
+// b-update (oracle admm_b_update): per column `inner` GN steps, Thomas solve
+// of tridiag(d, e) q = -grad (by lane 0, the oracle's recurrences), Armijo
+// on the column objective with gamma = 1, 1/2, ... (ls_max tries).
+template <typename T>
+__global__ void __launch_bounds__(32 * ADMM_WARPS) admm_b_kernel(Geom g, Ctl c, const T* __restrict__ Ip,
+                                                                const T* __restrict__ Im, T* __restrict__ b,
+                                                                const T* __restrict__ z, const T* __restrict__ u,
+                                                                const double* __restrict__ rho_p, int inner,
+                                                                double c1, int ls_max) {
+    count_launch(c);
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int pair = blockIdx.y;
+    const int n3 = g.n3, P = g.P;
+    T* base = reinterpret_cast<T*>(smem_raw) + (size_t)wid * admm_warp_elems(n3);
+    T* sIp = base + 2;
+    T* sIm = sIp + n3 + 4;
+    T* sb = sIm + n3 + 2;
+    T* sv = sb + P;
+    T* sq = sv + P;
+    T* sg = sq + P;
+    T* sd = sg + P;
+    T* se = sd + P;
+    T* sbt = se + P;
+    T* sa = sbt + P;
+    T* sc = sa + n3;
+    T* sr = sc + n3;
+    T* sp1 = sr + n3;
+    T* sp2 = sp1 + n3;
+    if (lane < 2) {
+        sIp[-2 + lane] = T(0);
+        sIp[n3 + lane] = T(0);
+        sIm[-2 + lane] = T(0);
+        sIm[n3 + lane] = T(0);
+    }
+    const T rho = (T)rho_p[pair];
+    const size_t pc = (size_t)pair * g.Nc, pn = (size_t)pair * g.ps;
+    for (long long col = (long long)blockIdx.x * ADMM_WARPS + wid; col < g.ncol;
+         col += (long long)gridDim.x * ADMM_WARPS) {
+        const size_t oc = pc + (size_t)col * n3, on = pn + (size_t)col * P;
+        for (int k = lane; k < n3; k += 32) {
+            sIp[k] = Ip[oc + k];
+            sIm[k] = Im[oc + k];
+        }
+        for (int l = lane; l < P; l += 32) {
+            sb[l] = b[on + l];
+            sv[l] = z[on + l] - u[on + l];
+        }
+        __syncwarp();
+        for (int it = 0; it < inner; it++) {
+            const double F = admm_col_eval<T, true>(g, lane, sIp, sIm, sb, sv, rho, sa, sc, sr, sp1, sp2, sg, sd, se);
+            if (!(F < INFINITY)) break;                 // infeasible column: no step
+            if (lane == 0) {                            // Thomas: y into sq, e/m into sbt
+                T m = sd[0];
+                T y = -sg[0] / m;
+                sq[0] = y;
+                sbt[0] = se[0] / m;
+                for (int l = 1; l < P; l++) {
+                    m = sd[l] - se[l - 1] * se[l - 1] / m;
+                    y = (-sg[l] - se[l - 1] * y) / m;
+                    sq[l] = y;
+                    sbt[l] = se[l] / m;
+                }
+                T zn = sq[P - 1];
+                for (int l = P - 2; l >= 0; l--) {
+                    zn = sq[l] - sbt[l] * zn;
+                    sq[l] = zn;
+                }
+            }
+            __syncwarp();
+            double gq = 0;
+            for (int l = lane; l < P; l += 32) gq += (double)sg[l] * (double)sq[l];
+            gq = warp_sum_t(gq);
+            T gamma = T(1);
+            for (int t = 0; t < ls_max; t++) {
+                for (int l = lane; l < P; l += 32) sbt[l] = sb[l] + gamma * sq[l];
+                __syncwarp();
+                const double Ft = admm_col_eval<T, false>(g, lane, sIp, sIm, sbt, sv, rho, nullptr, nullptr, nullptr,
+                                                          nullptr, nullptr, nullptr, nullptr, nullptr);
+                if (Ft < INFINITY && Ft <= F + c1 * (double)gamma * gq) {
+                    for (int l = lane; l < P; l += 32) sb[l] = sbt[l];
+                    __syncwarp();
+                    break;
+                }
+                gamma *= T(0.5);
+                __syncwarp();
+            }
+        }
+        for (int l = lane; l < P; l += 32) b[on + l] = sb[l];
+        __syncwarp();
+    }
+}
+
+// w = b + u (the z-update right-hand side before the rho scaling).
+template <typename T>
+__global__ void __launch_bounds__(256) admm_rhs_kernel(Geom g, Ctl c, const T* __restrict__ b, const T* __restrict__ u,
+                                                       T* __restrict__ w) {
+    count_launch(c);
+    const size_t po = (size_t)blockIdx.y * g.ps;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < g.Nn; t += (long long)gridDim.x * blockDim.x)
+        w[po + t] = b[po + t] + u[po + t];
+}
+
+// Spectrum scaling: X(k1, k2, l) *= rho / ((alpha lambda(k1, k2) + rho) n1 n2),
+// lambda = 4 sin^2(pi k1/n1)/h1^2 + 4 sin^2(pi k2/n2)/h2^2 (periodic L_xy).
+// Layout (cuFFT R2C, batch over l with stride P): [(k1 (n2/2+1) + k2) P + l].
+template <typename C>
+__global__ void __launch_bounds__(256) admm_zscale_kernel(Geom g, Ctl c, C* __restrict__ X,
+                                                          const double* __restrict__ rho_p, long long spec) {
+    count_launch(c);
+    const int pair = blockIdx.y;
+    const double rho = rho_p[pair];
+    const int n1 = g.n1, n2 = g.n2, P = g.P, n2h = n2 / 2 + 1;
+    const double sc = 1.0 / ((double)n1 * n2);
+    C* Xp = X + (size_t)pair * spec;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < (long long)n1 * n2h * P;
+         t += (long long)gridDim.x * blockDim.x) {
+        const long long kk = t / P;
+        const int k1 = (int)(kk / n2h), k2 = (int)(kk - (long long)k1 * n2h);
+        const double s1 = sin(M_PI * k1 / n1), s2 = sin(M_PI * k2 / n2);
+        const double lam = 4.0 * s1 * s1 * g.ih1sq + 4.0 * s2 * s2 * g.ih2sq;
+        const double f = rho / (g.alpha * lam + rho) * sc;
+        Xp[t].x *= f;
+        Xp[t].y *= f;
+    }
+}
+
+// u <- u + b - z_new, z <- z_new; per pair: ||b - z_new||^2, ||z_new - z||^2,
+// ||b - b_prev||^2, ||b||^2 (stored in c.red[pair][0..3]).
+template <typename T>
+__global__ void __launch_bounds__(256) admm_u_kernel(Geom g, Ctl c, const T* __restrict__ b,
+                                                     const T* __restrict__ bprev, const T* __restrict__ znew,
+                                                     T* __restrict__ z, T* __restrict__ u) {
+    count_launch(c);
+    const int pair = blockIdx.y;
+    const size_t po = (size_t)pair * g.ps;
+    double r2 = 0, s2 = 0, db2 = 0, bb = 0;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < g.Nn; t += (long long)gridDim.x * blockDim.x) {
+        const size_t o = po + t;
+        const T bv = b[o], zn = znew[o], zo = z[o];
+        const T du = bv - zn;
+        u[o] += du;
+        z[o] = zn;
+        r2 += (double)du * (double)du;
+        s2 += ((double)zn - (double)zo) * ((double)zn - (double)zo);
+        db2 += ((double)bv - (double)bprev[o]) * ((double)bv - (double)bprev[o]);
+        bb += (double)bv * (double)bv;
+    }
+    double v[4] = {r2, s2, db2, bb}, tot[4];
+    if (!pair_reduce<4, 0u>(c, v, tot)) return;
+    if (threadIdx.x != 0) return;
+    for (int k = 0; k < 4; k++) c.red[(size_t)pair * RED_W + k] = tot[k];
+}
+
+// u *= f[pair] (residual balancing rescales the scaled multiplier).
+template <typename T>
+__global__ void __launch_bounds__(256) admm_scale_u_kernel(Geom g, Ctl c, T* __restrict__ u,
+                                                           const double* __restrict__ f) {
+    count_launch(c);
+    const int pair = blockIdx.y;
+    const T s = (T)f[pair];
+    if (s == T(1)) return;
+    const size_t po = (size_t)pair * g.ps;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < g.Nn; t += (long long)gridDim.x * blockDim.x)
+        u[po + t] *= s;
+}
+
+}  // namespace hysco

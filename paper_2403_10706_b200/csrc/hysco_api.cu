@@ -10,8 +10,11 @@
 #include "hysco_kernels.cuh"
 
 #include <nccl.h>
+#include <cufft.h>
 
+#include <algorithm>
 #include <cstdio>
+#include <type_traits>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
@@ -53,6 +56,14 @@ struct hysco_ctx_s {
     void* st_out[2][3] = {};      // [slot][b, T+, T-]
     cudaEvent_t ev_h2d[2] = {}, ev_in_free[2] = {}, ev_out[2] = {}, ev_out_free[2] = {};
     bool stream_ready = false;
+    // hysco_admm: cuFFT plans (R2C / C2R over (n1, n2), batch P), spectrum, rho / factors
+    cufftHandle fft_fwd = 0, fft_inv = 0;
+    void* admm_spec = nullptr;
+    double* admm_rho = nullptr;     // [batch] device
+    double* admm_fac = nullptr;     // [batch] device (u rescaling)
+    size_t admm_smem = 0;
+    int admm_gx = 1;
+    bool admm_ready = false;
     void* own_Tm = nullptr;
     PairState* st = nullptr;
     PairState* h_st = nullptr;          // pinned mirror
@@ -975,6 +986,137 @@ static hysco_status setup_typed(hysco_ctx ctx) {
     return HYSCO_OK;
 }
 
+template <typename T>
+static hysco_status admm_setup(hysco_ctx ctx) {
+    if (ctx->admm_ready) return HYSCO_OK;
+    const Geom& g = ctx->g;
+    int n[2] = {g.n1, g.n2}, ine[2] = {g.n1, g.n2}, one[2] = {g.n1, g.n2 / 2 + 1};
+    const bool dbl = sizeof(T) == 8;
+    if (cufftPlanMany(&ctx->fft_fwd, 2, n, ine, g.P, 1, one, g.P, 1, dbl ? CUFFT_D2Z : CUFFT_R2C, g.P) != CUFFT_SUCCESS ||
+        cufftPlanMany(&ctx->fft_inv, 2, n, one, g.P, 1, ine, g.P, 1, dbl ? CUFFT_Z2D : CUFFT_C2R, g.P) != CUFFT_SUCCESS ||
+        cufftSetStream(ctx->fft_fwd, ctx->stream) != CUFFT_SUCCESS ||
+        cufftSetStream(ctx->fft_inv, ctx->stream) != CUFFT_SUCCESS)
+        return set_err(ctx, HYSCO_ERR_CUDA, "cuFFT plan creation failed");
+    const size_t spec = (size_t)g.n1 * (g.n2 / 2 + 1) * g.P;
+    CK(cudaMalloc(&ctx->admm_spec, spec * 2 * sizeof(T) * ctx->cfg.batch));
+    CK(cudaMalloc(&ctx->admm_rho, sizeof(double) * ctx->cfg.batch));
+    CK(cudaMalloc(&ctx->admm_fac, sizeof(double) * ctx->cfg.batch));
+    ctx->admm_smem = (size_t)ADMM_WARPS * admm_warp_elems(g.n3) * sizeof(T);
+    if (ctx->admm_smem > 227 * 1024) return set_err(ctx, HYSCO_ERR_SHAPE, "n3 too large for the ADMM column kernel");
+    CK(cudaFuncSetAttribute(admm_b_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->admm_smem));
+    int occ = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, admm_b_kernel<T>, 32 * ADMM_WARPS, ctx->admm_smem) !=
+            cudaSuccess || occ < 1)
+        occ = 1;
+    const long long work = (g.ncol + ADMM_WARPS - 1) / ADMM_WARPS;
+    const long long cap = ((long long)ctx->nsm * occ + ctx->cfg.batch - 1) / ctx->cfg.batch;
+    ctx->admm_gx = (int)std::max(1LL, std::min(work, cap));
+    ctx->admm_ready = true;
+    return HYSCO_OK;
+}
+
+template <typename T>
+static hysco_status admm_run(hysco_ctx ctx, void* d_b, const hysco_admm_opts& o, hysco_admm_report* reps) {
+    if (hysco_status s0 = admm_setup<T>(ctx)) return s0;
+    using C = typename std::conditional<sizeof(T) == 8, cufftDoubleComplex, cufftComplex>::type;
+    const Geom& g = ctx->g;
+    const int B = ctx->cfg.batch;
+    const size_t nb = (size_t)B * g.Nn * sizeof(T);
+    const long long spec = (long long)g.n1 * (g.n2 / 2 + 1) * g.P;
+    cudaStream_t st = ctx->stream;
+    T* b = L<T>::b(ctx, B_B);
+    T* bprev = L<T>::b(ctx, B_BOLD);
+    T* z = L<T>::b(ctx, B_R);
+    T* u = L<T>::b(ctx, B_P);
+    T* w = L<T>::b(ctx, B_HP);
+    T* zn = L<T>::b(ctx, B_TMP);
+    C* X = static_cast<C*>(ctx->admm_spec);
+    const double rho0 = o.rho0 > 0 ? o.rho0 : g.alpha * (g.ih1sq + g.ih2sq);
+    std::vector<double> rho(B, rho0), fac(B, 1.0), red((size_t)B * RED_W);
+    std::vector<int> iters(B, 0), conv(B, 0);
+    std::vector<double> rn(B, 0.0), sn(B, 0.0);
+    CK(cudaMemcpyAsync(b, d_b, nb, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(z, d_b, nb, cudaMemcpyDeviceToDevice, st));     // z0 = b0
+    CK(cudaMemsetAsync(u, 0, nb, st));                                  // u0 = 0
+    const dim3 gb(ctx->admm_gx, B), gn(ctx->gx_cells, B);
+    for (int k = 0; k < o.max_iter; k++) {
+        CK(cudaMemcpyAsync(ctx->admm_rho, rho.data(), sizeof(double) * B, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(bprev, b, nb, cudaMemcpyDeviceToDevice, st));
+        admm_b_kernel<T><<<gb, 32 * ADMM_WARPS, ctx->admm_smem, st>>>(g, ctx->ctl, (const T*)ctx->Ip,
+                                                                       (const T*)ctx->Im, b, z, u, ctx->admm_rho,
+                                                                       o.inner, o.armijo_c1, o.ls_max);
+        admm_rhs_kernel<T><<<gn, 256, 0, st>>>(g, ctx->ctl, b, u, w);
+        for (int p = 0; p < B; p++) {
+            cufftResult r = sizeof(T) == 8
+                                ? cufftExecD2Z(ctx->fft_fwd, (cufftDoubleReal*)(w + (size_t)p * g.ps),
+                                               (cufftDoubleComplex*)(X + (size_t)p * spec))
+                                : cufftExecR2C(ctx->fft_fwd, (cufftReal*)(w + (size_t)p * g.ps),
+                                               (cufftComplex*)(X + (size_t)p * spec));
+            if (r != CUFFT_SUCCESS) return set_err(ctx, HYSCO_ERR_CUDA, "cuFFT forward transform failed");
+        }
+        admm_zscale_kernel<C><<<gn, 256, 0, st>>>(g, ctx->ctl, X, ctx->admm_rho, spec);
+        for (int p = 0; p < B; p++) {
+            cufftResult r = sizeof(T) == 8
+                                ? cufftExecZ2D(ctx->fft_inv, (cufftDoubleComplex*)(X + (size_t)p * spec),
+                                               (cufftDoubleReal*)(zn + (size_t)p * g.ps))
+                                : cufftExecC2R(ctx->fft_inv, (cufftComplex*)(X + (size_t)p * spec),
+                                               (cufftReal*)(zn + (size_t)p * g.ps));
+            if (r != CUFFT_SUCCESS) return set_err(ctx, HYSCO_ERR_CUDA, "cuFFT inverse transform failed");
+        }
+        admm_u_kernel<T><<<gn, 256, 0, st>>>(g, ctx->ctl, b, bprev, zn, z, u);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(red.data(), ctx->red, sizeof(double) * B * RED_W, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        bool all_conv = true, any_fac = false;
+        for (int p = 0; p < B; p++) {
+            const double* t = &red[(size_t)p * RED_W];
+            const double r_norm = sqrt(t[0]), dz = sqrt(t[1]), db = sqrt(t[2]), bn = sqrt(t[3]);
+            const double s_norm = rho[p] * dz;
+            iters[p] = k + 1;
+            rn[p] = r_norm;
+            sn[p] = s_norm;
+            // residual balancing (oracle admm_rho_update)
+            fac[p] = 1.0;
+            if (r_norm > o.mu * s_norm) {
+                rho[p] *= o.tau;
+                fac[p] = 1.0 / o.tau;
+            } else if (s_norm > o.mu * r_norm) {
+                rho[p] /= o.tau;
+                fac[p] = o.tau;
+            }
+            any_fac = any_fac || fac[p] != 1.0;
+            conv[p] = std::max(db, std::max(dz, r_norm)) <= o.tol * std::max(bn, 1e-300);   // |du| = |b - z|
+            all_conv = all_conv && conv[p];
+        }
+        if (any_fac) {
+            CK(cudaMemcpyAsync(ctx->admm_fac, fac.data(), sizeof(double) * B, cudaMemcpyHostToDevice, st));
+            admm_scale_u_kernel<T><<<gn, 256, 0, st>>>(g, ctx->ctl, u, ctx->admm_fac);
+        }
+        if (!o.fixed_iters && all_conv) break;
+    }
+    CK(cudaMemcpyAsync(d_b, b, nb, cudaMemcpyDeviceToDevice, st));
+    SolveParams sp{};
+    L<T>::eval(ctx, sp, EVAL_PLAIN, b);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(ctx->h_st, ctx->st, sizeof(PairState) * B, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int p = 0; p < B; p++) {
+        if (!reps) break;
+        const PairState& s = ctx->h_st[p];
+        reps[p].iters = iters[p];
+        reps[p].converged = conv[p];
+        reps[p].rho = rho[p];
+        reps[p].r_norm = rn[p];
+        reps[p].s_norm = sn[p];
+        reps[p].J = s.J;
+        reps[p].D = s.D;
+        reps[p].S = s.S;
+        reps[p].P = s.P;
+    }
+    ctx->state_valid = false;
+    return HYSCO_OK;
+}
+
 extern "C" {
 
 void hysco_default_solve_opts(hysco_solve_opts* o) {
@@ -1265,6 +1407,33 @@ hysco_status hysco_precond_solve(hysco_ctx ctx, int kind, const void* d_r, void*
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(ctx->stream));
     return HYSCO_OK;
+}
+
+void hysco_default_admm_opts(hysco_admm_opts* o) {
+    if (!o) return;
+    o->max_iter = 20;
+    o->inner = 2;
+    o->ls_max = 10;
+    o->fixed_iters = 0;
+    o->tol = 1e-3;
+    o->rho0 = 0.0;
+    o->mu = 10.0;
+    o->tau = 2.0;
+    o->armijo_c1 = 1e-4;
+}
+
+hysco_status hysco_admm(hysco_ctx ctx, void* d_b_inout, const hysco_admm_opts* opts, hysco_admm_report* reports) {
+    CHECK_CTX();
+    if (ctx->g.slab) return set_err(ctx, HYSCO_ERR_STATE, "ADMM is not available on slab contexts");
+    if (hysco_status s = need_images(ctx)) return s;
+    if (!d_b_inout || !aligned16(d_b_inout)) return set_err(ctx, HYSCO_ERR_ARG, "d_b_inout must be 16-byte aligned");
+    hysco_admm_opts o;
+    hysco_default_admm_opts(&o);
+    if (opts) o = *opts;
+    if (o.max_iter < 0 || o.inner < 1 || o.ls_max < 1 || !(o.tol >= 0) || !(o.mu > 1) || !(o.tau > 1))
+        return set_err(ctx, HYSCO_ERR_ARG, "bad hysco_admm_opts");
+    return ctx->cfg.dtype == HYSCO_F64 ? admm_run<double>(ctx, d_b_inout, o, reports)
+                                       : admm_run<float>(ctx, d_b_inout, o, reports);
 }
 
 hysco_status hysco_apply(hysco_ctx ctx, const void* d_b, void* d_Iplus_corr, void* d_Iminus_corr) {
@@ -1669,6 +1838,12 @@ hysco_status hysco_destroy(hysco_ctx ctx) {
     if (ctx->flush) cudaFree(ctx->flush);
     if (ctx->res_part) cudaFree(ctx->res_part);
     if (ctx->res_flags) cudaFree(ctx->res_flags);
+    if (ctx->admm_ready) {
+        cufftDestroy(ctx->fft_fwd);
+        cufftDestroy(ctx->fft_inv);
+    }
+    for (void* q : {ctx->admm_spec, (void*)ctx->admm_rho, (void*)ctx->admm_fac})
+        if (q) cudaFree(q);
     if (ctx->stream_ready) {
         for (int k = 0; k < 2; k++) {
             for (void* q : {ctx->st_in[k][0], ctx->st_in[k][1], ctx->st_out[k][0], ctx->st_out[k][1], ctx->st_out[k][2]})

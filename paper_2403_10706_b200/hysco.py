@@ -20,7 +20,8 @@ HYSCO_F32, HYSCO_F64 = 0, 1
 HYSCO_PRECOND_JACOBI, HYSCO_PRECOND_PE_BLOCK = 0, 1
 STOP_NAMES = {0: "maxiter", 1: "grad", 2: "dJ", 3: "db", 4: "ls_fail", 5: "infeasible"}
 
-EXPORTED = ["hysco_default_solve_opts", "hysco_default_ot_opts", "hysco_create", "hysco_bind_images",
+EXPORTED = ["hysco_default_solve_opts", "hysco_default_ot_opts", "hysco_default_admm_opts", "hysco_admm",
+            "hysco_create", "hysco_bind_images",
             "hysco_ot_init", "hysco_objective_grad", "hysco_hessvec", "hysco_hess_diag", "hysco_precond_solve",
             "hysco_solve",
             "hysco_apply", "hysco_correct", "hysco_correct_host", "hysco_correct_host_stream",
@@ -53,6 +54,21 @@ class hysco_solve_opts(ctypes.Structure):
                 ("fixed_iters", ctypes.c_int32), ("ls_max", ctypes.c_int32), ("armijo_c1", ctypes.c_double),
                 ("tol_grad_rel", ctypes.c_double), ("tol_dJ_rel", ctypes.c_double),
                 ("tol_db_rel", ctypes.c_double), ("armijo", ctypes.c_int32), ("precond", ctypes.c_int32)]
+
+
+class hysco_admm_opts(ctypes.Structure):
+    _fields_ = [("max_iter", ctypes.c_int32), ("inner", ctypes.c_int32), ("ls_max", ctypes.c_int32),
+                ("fixed_iters", ctypes.c_int32), ("tol", ctypes.c_double), ("rho0", ctypes.c_double),
+                ("mu", ctypes.c_double), ("tau", ctypes.c_double), ("armijo_c1", ctypes.c_double)]
+
+
+class hysco_admm_report(ctypes.Structure):
+    _fields_ = [("iters", ctypes.c_int32), ("converged", ctypes.c_int32), ("rho", ctypes.c_double),
+                ("r_norm", ctypes.c_double), ("s_norm", ctypes.c_double), ("J", ctypes.c_double),
+                ("D", ctypes.c_double), ("S", ctypes.c_double), ("P", ctypes.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
 
 
 class hysco_report(ctypes.Structure):
@@ -94,6 +110,10 @@ def lib():
     L.hysco_objective_grad.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_double), vp]
     L.hysco_hessvec.argtypes = [vp, vp, vp]
     L.hysco_hess_diag.argtypes = [vp, vp]
+    L.hysco_default_admm_opts.argtypes = [ctypes.POINTER(hysco_admm_opts)]
+    L.hysco_default_admm_opts.restype = None
+    L.hysco_admm.argtypes = [vp, vp, ctypes.POINTER(hysco_admm_opts), ctypes.POINTER(hysco_admm_report)]
+    L.hysco_admm.restype = st
     L.hysco_precond_solve.argtypes = [vp, ctypes.c_int32, vp, vp]
     L.hysco_solve.argtypes = [vp, vp, ctypes.POINTER(hysco_solve_opts), ctypes.POINTER(hysco_report)]
     L.hysco_apply.argtypes = [vp, vp, vp, vp]
@@ -162,6 +182,21 @@ def default_solve_opts(**kw):
     for k, v in kw.items():
         setattr(o, k, v)
     return o
+
+
+def default_admm_opts(**kw):
+    o = hysco_admm_opts()
+    lib().hysco_default_admm_opts(ctypes.byref(o))
+    for k, v in kw.items():
+        setattr(o, k, v)
+    return o
+
+
+def hysco_admm(ctx, b_inout, opts=None, batch=1):
+    """ADMM solve from b_inout (device nodes, overwritten); returns per-pair reports."""
+    reps = (hysco_admm_report * batch)()
+    _check(ctx, lib().hysco_admm(ctx, _ptr(b_inout), ctypes.byref(opts) if opts is not None else None, reps))
+    return [r.as_dict() for r in reps]
 
 
 def default_ot_opts(**kw):
