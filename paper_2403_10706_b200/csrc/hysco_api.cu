@@ -1035,6 +1035,7 @@ static hysco_status admm_run(hysco_ctx ctx, void* d_b, const hysco_admm_opts& o,
     std::vector<double> rho(B, rho0), fac(B, 1.0), red((size_t)B * RED_W);
     std::vector<int> iters(B, 0), conv(B, 0);
     std::vector<double> rn(B, 0.0), sn(B, 0.0);
+    CK(cudaMemsetAsync(ctx->launches, 0, sizeof(unsigned long long), st));
     CK(cudaMemcpyAsync(b, d_b, nb, cudaMemcpyDeviceToDevice, st));
     CK(cudaMemcpyAsync(z, d_b, nb, cudaMemcpyDeviceToDevice, st));     // z0 = b0
     CK(cudaMemsetAsync(u, 0, nb, st));                                  // u0 = 0
@@ -1099,7 +1100,9 @@ static hysco_status admm_run(hysco_ctx ctx, void* d_b, const hysco_admm_opts& o,
     L<T>::eval(ctx, sp, EVAL_PLAIN, b);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(ctx->h_st, ctx->st, sizeof(PairState) * B, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(ctx->h_launches, ctx->launches, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    ctx->last_launches = (long long)*ctx->h_launches;   // ADMM kernels + the final evaluation (cuFFT not counted)
     for (int p = 0; p < B; p++) {
         if (!reps) break;
         const PairState& s = ctx->h_st[p];
