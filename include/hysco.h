@@ -179,6 +179,7 @@ typedef struct {
     double rho0;             /* initial augmentation; <= 0: alpha (1/h1^2 + 1/h2^2) (R24)          */
     double mu, tau;          /* residual balancing (Boyd et al. 2011 §3.4.1), default 10, 2 (R25)   */
     double armijo_c1;        /* default 1e-4                                                         */
+    double col_tol;          /* a column's GN stops when -grad.q <= col_tol |Fc|, default 1e-6 (R23) */
 } hysco_admm_opts;
 
 /* Per-pair ADMM result. */

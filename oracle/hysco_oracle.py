@@ -656,13 +656,18 @@ def admm_b_objective(Ip, Im, b, v, h, alpha=ALPHA_DEFAULT, beta=BETA_DEFAULT, rh
     return cs
 
 
+ADMM_COL_TOL = 1e-6   # R23: a column stops when the GN step predicts < 1e-6 |Fc| decrease
+
+
 def admm_b_update(Ip, Im, b, v, h, alpha=ALPHA_DEFAULT, beta=BETA_DEFAULT, rho=1.0, inner=2,
-                  c1=1e-4, ls_max=10):
+                  c1=1e-4, ls_max=10, col_tol=ADMM_COL_TOL):
     """b-update: `inner` Gauss-Newton steps on every PE column
     independently.  The column system H_col q = -grad_col is tridiagonal, so the
     per-column ("BlockPCG") solve is exact (Thomas, R23); each column takes its
     own Armijo step gamma in {1, 1/2, ...} on its own Fc ("different step
-    sizes ... for each image column"); a column without an acceptable step keeps b."""
+    sizes and stopping criteria for each image column"): a column stops when
+    the step predicts a decrease -grad.q <= col_tol |Fc| (R23); a column
+    without an acceptable step keeps b."""
     b = np.asarray(b, np.float64).copy()
     for _ in range(inner):
         cs = admm_b_objective(Ip, Im, b, v, h, alpha, beta, rho)
@@ -671,7 +676,8 @@ def admm_b_update(Ip, Im, b, v, h, alpha=ALPHA_DEFAULT, beta=BETA_DEFAULT, rho=1
         q = -solve_tridiag_pe(cs.d, cs.e, np.where(cs.infeasible[..., None], 0.0, cs.grad))
         gq = np.sum(cs.grad * q, axis=-1)
         gamma = np.ones(b.shape[:-1])
-        done = cs.infeasible.copy()
+        with np.errstate(invalid="ignore"):
+            done = cs.infeasible | (-gq <= col_tol * np.abs(np.where(cs.infeasible, 0.0, cs.F)))
         bn = b.copy()
         for _t in range(ls_max):
             cand = b + gamma[..., None] * q

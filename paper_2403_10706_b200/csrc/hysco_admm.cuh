@@ -20,7 +20,44 @@ constexpr int ADMM_WARPS = 4;   // columns per CTA (one warp each)
 // quantities a, c, r, phi', phi''.
 __host__ __device__ inline size_t admm_warp_elems(int n3) {
     const size_t P = (size_t)n3 + 1;
-    return 2 * ((size_t)n3 + 4) + 7 * P + 5 * (size_t)n3;
+    return 2 * ((size_t)n3 + 4) + 7 * P + 5 * P;   // cell arrays sized P: PCR reuses them
+}
+
+// Solve the column system tridiag(e, d, e) q = rhs by parallel cyclic
+// reduction across the warp (ceil(log2 P) steps; equation i keeps
+// a_i x_{i-s} + b_i x_i + c_i x_{i+s} = r_i).  The PCR buffers alias the cell
+// arrays (dead after the derivative pass).  Replaces the oracle's sequential
+// Thomas recurrences by an equivalent exact solve (SPD, diagonally dominant).
+template <typename T>
+__device__ __forceinline__ void pcr_solve(int lane, int P, const T* sd, const T* se, const T* rhs, T* q, T* A0, T* B0,
+                                          T* C0, T* R0, T* A1, T* B1, T* C1, T* R1) {
+    // (A1.. may alias sd / se / rhs: those are read only before the first step)
+    for (int i = lane; i < P; i += 32) {
+        A0[i] = i > 0 ? se[i - 1] : T(0);
+        B0[i] = sd[i];
+        C0[i] = i + 1 < P ? se[i] : T(0);
+        R0[i] = rhs[i];
+    }
+    __syncwarp();
+    for (int st = 1; st < P; st <<= 1) {
+        for (int i = lane; i < P; i += 32) {
+            const int im = i - st, ip = i + st;
+            const T k1 = im >= 0 ? A0[i] / B0[im] : T(0);
+            const T k2 = ip < P ? C0[i] / B0[ip] : T(0);
+            A1[i] = im >= 0 ? -A0[im] * k1 : T(0);
+            C1[i] = ip < P ? -C0[ip] * k2 : T(0);
+            B1[i] = B0[i] - (im >= 0 ? C0[im] * k1 : T(0)) - (ip < P ? A0[ip] * k2 : T(0));
+            R1[i] = R0[i] - (im >= 0 ? R0[im] * k1 : T(0)) - (ip < P ? R0[ip] * k2 : T(0));
+        }
+        __syncwarp();
+        T* t;
+        t = A0; A0 = A1; A1 = t;
+        t = B0; B0 = B1; B1 = t;
+        t = C0; C0 = C1; C1 = t;
+        t = R0; R0 = R1; R1 = t;
+    }
+    for (int i = lane; i < P; i += 32) q[i] = R0[i] / B0[i];
+    __syncwarp();
 }
 
 template <typename T>
@@ -104,15 +141,15 @@ __device__ double admm_col_eval(const Geom& g, int lane, const T* sIp, const T* 
     return F;
 }
 
-// b-update (oracle admm_b_update): per column `inner` GN steps, Thomas solve
-// of tridiag(d, e) q = -grad (by lane 0, the oracle's recurrences), Armijo
-// on the column objective with gamma = 1, 1/2, ... (ls_max tries).
+// b-update (oracle admm_b_update): per column `inner` GN steps, exact solve
+// of tridiag(d, e) q = -grad (warp PCR), the per-column stop (R23), Armijo on
+// the column objective with gamma = 1, 1/2, ... (ls_max tries).
 template <typename T>
 __global__ void __launch_bounds__(32 * ADMM_WARPS) admm_b_kernel(Geom g, Ctl c, const T* __restrict__ Ip,
                                                                 const T* __restrict__ Im, T* __restrict__ b,
                                                                 const T* __restrict__ z, const T* __restrict__ u,
                                                                 const double* __restrict__ rho_p, int inner,
-                                                                double c1, int ls_max) {
+                                                                double c1, int ls_max, double col_tol) {
     count_launch(c);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -129,10 +166,10 @@ __global__ void __launch_bounds__(32 * ADMM_WARPS) admm_b_kernel(Geom g, Ctl c, 
     T* se = sd + P;
     T* sbt = se + P;
     T* sa = sbt + P;
-    T* sc = sa + n3;
-    T* sr = sc + n3;
-    T* sp1 = sr + n3;
-    T* sp2 = sp1 + n3;
+    T* sc = sa + P;
+    T* sr = sc + P;
+    T* sp1 = sr + P;
+    T* sp2 = sp1 + P;
     if (lane < 2) {
         sIp[-2 + lane] = T(0);
         sIp[n3 + lane] = T(0);
@@ -156,27 +193,16 @@ __global__ void __launch_bounds__(32 * ADMM_WARPS) admm_b_kernel(Geom g, Ctl c, 
         for (int it = 0; it < inner; it++) {
             const double F = admm_col_eval<T, true>(g, lane, sIp, sIm, sb, sv, rho, sa, sc, sr, sp1, sp2, sg, sd, se);
             if (!(F < INFINITY)) break;                 // infeasible column: no step
-            if (lane == 0) {                            // Thomas: y into sq, e/m into sbt
-                T m = sd[0];
-                T y = -sg[0] / m;
-                sq[0] = y;
-                sbt[0] = se[0] / m;
-                for (int l = 1; l < P; l++) {
-                    m = sd[l] - se[l - 1] * se[l - 1] / m;
-                    y = (-sg[l] - se[l - 1] * y) / m;
-                    sq[l] = y;
-                    sbt[l] = se[l] / m;
-                }
-                T zn = sq[P - 1];
-                for (int l = P - 2; l >= 0; l--) {
-                    zn = sq[l] - sbt[l] * zn;
-                    sq[l] = zn;
-                }
-            }
+            for (int l = lane; l < P; l += 32) sbt[l] = -sg[l];     // rhs = -grad
+            __syncwarp();
+            // PCR double buffers: the dead cell arrays, then d, e, rhs themselves
+            // (read only by pcr_solve's set-up pass)
+            pcr_solve<T>(lane, P, sd, se, sbt, sq, sa, sc, sr, sp1, sp2, sd, se, sbt);
             __syncwarp();
             double gq = 0;
             for (int l = lane; l < P; l += 32) gq += (double)sg[l] * (double)sq[l];
             gq = warp_sum_t(gq);
+            if (-gq <= col_tol * fabs(F)) break;        // column converged (R23)
             T gamma = T(1);
             for (int t = 0; t < ls_max; t++) {
                 for (int l = lane; l < P; l += 32) sbt[l] = sb[l] + gamma * sq[l];
@@ -208,26 +234,39 @@ __global__ void __launch_bounds__(256) admm_rhs_kernel(Geom g, Ctl c, const T* _
 }
 
 // Spectrum scaling: X(k1, k2, l) *= rho / ((alpha lambda(k1, k2) + rho) n1 n2),
-// lambda = 4 sin^2(pi k1/n1)/h1^2 + 4 sin^2(pi k2/n2)/h2^2 (periodic L_xy).
-// Layout (cuFFT R2C, batch over l with stride P): [(k1 (n2/2+1) + k2) P + l].
+// lambda = 4 sin^2(pi k1/n1)/h1^2 + 4 sin^2(pi k2/n2)/h2^2 (periodic L_xy),
+// precomputed once per context in `lam`.  Layout (cuFFT R2C, batch over l
+// with stride P): [(k1 (n2/2+1) + k2) P + l]; one warp per (k1, k2) row of P.
 template <typename C>
 __global__ void __launch_bounds__(256) admm_zscale_kernel(Geom g, Ctl c, C* __restrict__ X,
-                                                          const double* __restrict__ rho_p, long long spec) {
+                                                          const double* __restrict__ rho_p,
+                                                          const double* __restrict__ lam, long long spec) {
     count_launch(c);
-    const int pair = blockIdx.y;
+    const int pair = blockIdx.y, lane = threadIdx.x & 31;
     const double rho = rho_p[pair];
-    const int n1 = g.n1, n2 = g.n2, P = g.P, n2h = n2 / 2 + 1;
-    const double sc = 1.0 / ((double)n1 * n2);
+    const int P = g.P;
+    const long long nk = (long long)g.n1 * (g.n2 / 2 + 1);
+    const double sc = 1.0 / ((double)g.n1 * g.n2);
     C* Xp = X + (size_t)pair * spec;
-    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < (long long)n1 * n2h * P;
-         t += (long long)gridDim.x * blockDim.x) {
-        const long long kk = t / P;
+    for (long long kk = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); kk < nk;
+         kk += (long long)gridDim.x * (blockDim.x >> 5)) {
+        const double f = rho / (g.alpha * lam[kk] + rho) * sc;
+        C* row = Xp + kk * P;
+        for (int l = lane; l < P; l += 32) {
+            row[l].x *= f;
+            row[l].y *= f;
+        }
+    }
+}
+
+// lambda(k1, k2) table for admm_zscale_kernel.
+__global__ void admm_lambda_kernel(Geom g, double* __restrict__ lam) {
+    const int n2h = g.n2 / 2 + 1;
+    for (long long kk = (long long)blockIdx.x * blockDim.x + threadIdx.x; kk < (long long)g.n1 * n2h;
+         kk += (long long)gridDim.x * blockDim.x) {
         const int k1 = (int)(kk / n2h), k2 = (int)(kk - (long long)k1 * n2h);
-        const double s1 = sin(M_PI * k1 / n1), s2 = sin(M_PI * k2 / n2);
-        const double lam = 4.0 * s1 * s1 * g.ih1sq + 4.0 * s2 * s2 * g.ih2sq;
-        const double f = rho / (g.alpha * lam + rho) * sc;
-        Xp[t].x *= f;
-        Xp[t].y *= f;
+        const double s1 = sin(M_PI * k1 / g.n1), s2 = sin(M_PI * k2 / g.n2);
+        lam[kk] = 4.0 * s1 * s1 * g.ih1sq + 4.0 * s2 * s2 * g.ih2sq;
     }
 }
 

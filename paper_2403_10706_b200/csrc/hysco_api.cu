@@ -61,6 +61,7 @@ struct hysco_ctx_s {
     void* admm_spec = nullptr;
     double* admm_rho = nullptr;     // [batch] device
     double* admm_fac = nullptr;     // [batch] device (u rescaling)
+    double* admm_lam = nullptr;     // [n1][n2/2+1] periodic L_xy eigenvalues
     size_t admm_smem = 0;
     int admm_gx = 1;
     bool admm_ready = false;
@@ -1001,6 +1002,9 @@ static hysco_status admm_setup(hysco_ctx ctx) {
     CK(cudaMalloc(&ctx->admm_spec, spec * 2 * sizeof(T) * ctx->cfg.batch));
     CK(cudaMalloc(&ctx->admm_rho, sizeof(double) * ctx->cfg.batch));
     CK(cudaMalloc(&ctx->admm_fac, sizeof(double) * ctx->cfg.batch));
+    CK(cudaMalloc(&ctx->admm_lam, sizeof(double) * g.n1 * (g.n2 / 2 + 1)));
+    admm_lambda_kernel<<<64, 256, 0, ctx->stream>>>(g, ctx->admm_lam);
+    CK(cudaGetLastError());
     ctx->admm_smem = (size_t)ADMM_WARPS * admm_warp_elems(g.n3) * sizeof(T);
     if (ctx->admm_smem > 227 * 1024) return set_err(ctx, HYSCO_ERR_SHAPE, "n3 too large for the ADMM column kernel");
     CK(cudaFuncSetAttribute(admm_b_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->admm_smem));
@@ -1045,7 +1049,7 @@ static hysco_status admm_run(hysco_ctx ctx, void* d_b, const hysco_admm_opts& o,
         CK(cudaMemcpyAsync(bprev, b, nb, cudaMemcpyDeviceToDevice, st));
         admm_b_kernel<T><<<gb, 32 * ADMM_WARPS, ctx->admm_smem, st>>>(g, ctx->ctl, (const T*)ctx->Ip,
                                                                        (const T*)ctx->Im, b, z, u, ctx->admm_rho,
-                                                                       o.inner, o.armijo_c1, o.ls_max);
+                                                                       o.inner, o.armijo_c1, o.ls_max, o.col_tol);
         admm_rhs_kernel<T><<<gn, 256, 0, st>>>(g, ctx->ctl, b, u, w);
         for (int p = 0; p < B; p++) {
             cufftResult r = sizeof(T) == 8
@@ -1055,7 +1059,7 @@ static hysco_status admm_run(hysco_ctx ctx, void* d_b, const hysco_admm_opts& o,
                                                (cufftComplex*)(X + (size_t)p * spec));
             if (r != CUFFT_SUCCESS) return set_err(ctx, HYSCO_ERR_CUDA, "cuFFT forward transform failed");
         }
-        admm_zscale_kernel<C><<<gn, 256, 0, st>>>(g, ctx->ctl, X, ctx->admm_rho, spec);
+        admm_zscale_kernel<C><<<gn, 256, 0, st>>>(g, ctx->ctl, X, ctx->admm_rho, ctx->admm_lam, spec);
         for (int p = 0; p < B; p++) {
             cufftResult r = sizeof(T) == 8
                                 ? cufftExecZ2D(ctx->fft_inv, (cufftDoubleComplex*)(X + (size_t)p * spec),
@@ -1423,6 +1427,7 @@ void hysco_default_admm_opts(hysco_admm_opts* o) {
     o->mu = 10.0;
     o->tau = 2.0;
     o->armijo_c1 = 1e-4;
+    o->col_tol = 1e-6;
 }
 
 hysco_status hysco_admm(hysco_ctx ctx, void* d_b_inout, const hysco_admm_opts* opts, hysco_admm_report* reports) {
@@ -1845,7 +1850,7 @@ hysco_status hysco_destroy(hysco_ctx ctx) {
         cufftDestroy(ctx->fft_fwd);
         cufftDestroy(ctx->fft_inv);
     }
-    for (void* q : {ctx->admm_spec, (void*)ctx->admm_rho, (void*)ctx->admm_fac})
+    for (void* q : {ctx->admm_spec, (void*)ctx->admm_rho, (void*)ctx->admm_fac, (void*)ctx->admm_lam})
         if (q) cudaFree(q);
     if (ctx->stream_ready) {
         for (int k = 0; k < 2; k++) {

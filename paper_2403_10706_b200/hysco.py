@@ -59,7 +59,8 @@ class hysco_solve_opts(ctypes.Structure):
 class hysco_admm_opts(ctypes.Structure):
     _fields_ = [("max_iter", ctypes.c_int32), ("inner", ctypes.c_int32), ("ls_max", ctypes.c_int32),
                 ("fixed_iters", ctypes.c_int32), ("tol", ctypes.c_double), ("rho0", ctypes.c_double),
-                ("mu", ctypes.c_double), ("tau", ctypes.c_double), ("armijo_c1", ctypes.c_double)]
+                ("mu", ctypes.c_double), ("tau", ctypes.c_double), ("armijo_c1", ctypes.c_double),
+                ("col_tol", ctypes.c_double)]
 
 
 class hysco_admm_report(ctypes.Structure):
