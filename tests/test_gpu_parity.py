@@ -271,6 +271,32 @@ def test_infeasible_and_state_errors():
     c.close()
 
 
+def test_precond_and_admm_argument_and_state_errors():
+    p = phantom.make_pair((4, 4, 8), (1, 1, 1), 1)
+    c = Ctx([p.Ip], [p.Im], (1.0, 1.0, 1.0))
+    r, z = c.nodes(np.ones((4, 4, 9))), c.nodes()
+    with pytest.raises(H.HyscoError) as e:                   # no objective_grad yet
+        H.hysco_precond_solve(c.ctx, H.HYSCO_PRECOND_PE_BLOCK, r, z)
+    assert e.value.status == H.HYSCO_ERR_STATE
+    H.hysco_objective_grad(c.ctx, c.nodes())
+    with pytest.raises(H.HyscoError) as e:                   # unknown kind
+        H.hysco_precond_solve(c.ctx, 7, r, z)
+    assert e.value.status == H.HYSCO_ERR_ARG
+    with pytest.raises(H.HyscoError) as e:                   # aliasing
+        H.hysco_precond_solve(c.ctx, H.HYSCO_PRECOND_JACOBI, r, r)
+    assert e.value.status == H.HYSCO_ERR_ARG
+    with pytest.raises(H.HyscoError) as e:
+        H.hysco_solve(c.ctx, c.nodes(), H.default_solve_opts(precond=5))
+    assert e.value.status == H.HYSCO_ERR_ARG
+    for bad in (dict(inner=0), dict(tau=1.0), dict(mu=0.5), dict(max_iter=-1)):
+        with pytest.raises(H.HyscoError) as e:
+            H.hysco_admm(c.ctx, c.nodes(), H.default_admm_opts(**bad))
+        assert e.value.status == H.HYSCO_ERR_ARG, bad
+    reps = H.hysco_admm(c.ctx, c.nodes(), H.default_admm_opts(max_iter=0))
+    assert reps[0]["iters"] == 0
+    c.close()
+
+
 def test_armijo_halving_matches_oracle():
     """A direction that overshoots: construct with a tiny alpha so the GN step
     is long and the barrier rejects gamma = 1 (R15); fp64 decisions must match."""
