@@ -263,7 +263,7 @@ __device__ __forceinline__ void stage_b(const T* __restrict__ src, const T* __re
 // = b_old + gamma q (gamma = 0 to restore, R15) is formed while staging and
 // written to bb, which replaces the separate retry kernel.
 template <typename T, int NCH>
-__global__ void __launch_bounds__(256, 4) eval_kernel(Geom g, Ctl c, SolveParams sp, int mode,
+__global__ void __launch_bounds__(256, (NCH <= 5 ? 3 : 4)) eval_kernel(Geom g, Ctl c, SolveParams sp, int mode,
                                                    const T* __restrict__ Ip, const T* __restrict__ Im,
                                                    const T* bb, const T* __restrict__ bold,
                                                    const T* __restrict__ q, T* __restrict__ grad,
