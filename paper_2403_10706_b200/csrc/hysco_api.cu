@@ -359,9 +359,9 @@ struct Runner {
 // Resident PCG (fp32): K = node slots per thread, a compile-time parameter.
 #define RES_K_SWITCH(k, ...)                                                   \
     switch (k) {                                                               \
-        case 4: { constexpr int RK = 4; __VA_ARGS__; } break;                  \
-        case 8: { constexpr int RK = 8; __VA_ARGS__; } break;                  \
-        default: { constexpr int RK = 12; __VA_ARGS__; } break;                \
+        case 6: { constexpr int RK = 6; __VA_ARGS__; } break;                  \
+        case 12: { constexpr int RK = 12; __VA_ARGS__; } break;                \
+        default: { constexpr int RK = 18; __VA_ARGS__; } break;                \
     }
 
 // bcur / bold: the trial b and b_old the fused Armijo start writes (B_B /
@@ -405,8 +405,8 @@ static void setup_resident(hysco_ctx ctx) {
     const long long ncl_max = (g.ncol + G - 1) / G;
     const long long nqmax = ncl_max * (res_pad(g.P) / 2);   // node pairs per CTA
     const long long need_k = (nqmax + RES_THREADS - 1) / RES_THREADS;
-    if (need_k > 12) return;
-    const int k = need_k <= 4 ? 4 : need_k <= 8 ? 8 : 12;
+    if (need_k > RES_KMAX) return;
+    const int k = need_k <= 6 ? 6 : need_k <= 12 ? 12 : 18;
     const size_t smem = res_smem_bytes(k);   // layout: hysco_resident.cuh
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->cfg.device);

@@ -25,7 +25,8 @@
 
 namespace hysco {
 
-constexpr int RES_THREADS = 768;   // 24 warps (6 per SM sub-partition): 80 registers per thread
+constexpr int RES_THREADS = 512;   // 16 warps: 128 registers per thread, 18 node-pair slots without spills
+constexpr int RES_KMAX = 18;       // slots per thread (capacity 18 x 512 node pairs per SM)
 
 // Opaque copy: stops ptxas from hoisting per-slot index math (and everything
 // derived from it) out of the PCG iteration loop, which would keep ~15
@@ -244,8 +245,7 @@ struct FastDiv {
 // node count (zero padding), so a thread handles a pair of consecutive nodes
 // of one column with 64-bit shared / global accesses, and in-plane
 // neighbours (+-Pp, +-n2 Pp) stay 8-byte aligned.  (Groups of 4 would need
-// 3 % more padding at P = 145 and 8 more registers per slot, which does not
-// fit the 80-register budget of 24 warps.)
+// 3 % more padding at P = 145 and 8 more registers per slot.)
 __host__ __device__ inline int res_pad(int P) { return (P + 1) & ~1; }
 
 // Global copy of p used for the in-plane halo: per pair (n1 + 2) x n2 x Pp
@@ -267,8 +267,17 @@ __host__ __device__ inline size_t res_ghost_slack_floats(int K) { return (size_t
 
 // slot-mask fields (bit f + k for slot k < 12): pair valid, j-1 neighbour in
 // this CTA, j+1 in this CTA, j-1 neighbour in the previous CTA, j+1 in the next
-enum { RM_VAL = 0, RM_JML = 12, RM_JPL = 24, RM_JMR = 36, RM_JPR = 48 };
-__device__ __forceinline__ bool mbit(unsigned long long m, int b) { return (m >> b) & 1ull; }
+enum { RM_VAL = 0, RM_JML = RES_KMAX, RM_JPL = 2 * RES_KMAX, RM_JMR = 3 * RES_KMAX, RM_JPR = 4 * RES_KMAX };
+struct SlotMask {                            // 5 fields x RES_KMAX slots = 90 bits
+    unsigned long long lo, hi;
+};
+__device__ __forceinline__ bool mbit(const SlotMask& m, int b) {
+    return b < 64 ? ((m.lo >> b) & 1ull) != 0 : ((m.hi >> (b - 64)) & 1ull) != 0;
+}
+__device__ __forceinline__ void mset(SlotMask& m, int b) {
+    if (b < 64) m.lo |= 1ull << b;
+    else m.hi |= 1ull << (b - 64);
+}
 __device__ __forceinline__ unsigned long long opaque64(unsigned long long v) {
     unsigned long long r;
     asm volatile("mov.b64 %0, %1;" : "=l"(r) : "l"(v));
@@ -284,7 +293,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
                         unsigned* __restrict__ flags, float wi, float wj, float* __restrict__ bcur,
                         float* __restrict__ bold, int batch, unsigned long long* trace = nullptr) {
     constexpr int NT = RES_THREADS;
-    static_assert(K <= 12, "slot masks hold 12 slots per field");
+    static_assert(K <= RES_KMAX, "slot masks hold RES_KMAX slots per field");
     count_launch(c);
     if (!c.st[pair].gn_active) {             // uniform over the grid: no step, no search
         if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -330,7 +339,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
     const int bhi = res_owner(c1 - 1 + n2 < g.ncol ? c1 - 1 + n2 : g.ncol - 1, g.ncol, gridDim.x);
 
     if (tid < 6) smem_f[tid < 2 ? tid : tid < 4 ? 2 + KNT2 + (tid - 2) : 4 + 2 * KNT2 + (tid - 4)] = 0.f;
-    unsigned long long msk = 0;
+    SlotMask msk{0ull, 0ull};
     float2 r[K], hv[K];
     float frz = 0.f, frr = 0.f;
     {
@@ -356,9 +365,9 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
                     ev.y = et[o + 1];
                     rv.y = -grad[o + 1];
                 }
-                msk |= 1ull << (RM_VAL + k);
-                if (j > 0) msk |= 1ull << ((cl > 0 ? RM_JML : RM_JMR) + k);
-                if (j < n2 - 1) msk |= 1ull << ((cl < ncl - 1 ? RM_JPL : RM_JPR) + k);
+                mset(msk, RM_VAL + k);
+                if (j > 0) mset(msk, (cl > 0 ? RM_JML : RM_JMR) + k);
+                if (j < n2 - 1) mset(msk, (cl < ncl - 1 ? RM_JPL : RM_JPR) + k);
                 const float2 z = make_float2(precond(rv.x, Mv.x), precond(rv.y, Mv.y));
                 frz = fmaf(rv.x, z.x, frz);
                 frz = fmaf(rv.y, z.y, frz);
@@ -401,7 +410,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
             // all loads of a phase can be in flight together.
             {
                 const int t0 = opaque(tid);
-                const unsigned long long m = opaque64(msk);
+                const SlotMask m{opaque64(msk.lo), opaque64(msk.hi)};
                 const float2* s2 = sp2 + t0;
                 const float2* m2 = sM2 + t0;
                 const float2* e2 = se2 + t0;
@@ -429,7 +438,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
             float fpq = 0.f;
             {
                 const int t0 = opaque(tid);
-                const unsigned long long m = opaque64(msk);
+                const SlotMask m{opaque64(msk.lo), opaque64(msk.hi)};
                 const float2* gc = pgc2 + t0;
                 const float2* s2 = sp2 + t0;
 #pragma unroll
@@ -491,7 +500,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
             // L2 adds; x feeds no reduction)
             {
                 const int t0 = opaque(tid);
-                const unsigned long long m = opaque64(msk);
+                const SlotMask m{opaque64(msk.lo), opaque64(msk.hi)};
                 const float2* s2 = sp2 + t0;
                 float2* xt = xp2 + t0;
 #pragma unroll
@@ -519,7 +528,7 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
             const float be = (float)beta;
             {
                 const int t0 = opaque(tid);
-                const unsigned long long m = opaque64(msk);
+                const SlotMask m{opaque64(msk.lo), opaque64(msk.hi)};
                 float2* s2 = sp2 + t0;
                 float2* gt = pgc2 + t0;
 #pragma unroll
