@@ -19,7 +19,8 @@ Pins: every function here is checked in tests/test_oracle_*.py against closed
 forms, invariants, brute force and the hand-derived worked example in
 tests/golden/.  The one result with no independent pin is the field map after
 a fixed number of GN-PCG iterations on a synthetic pair (parity unpinned as a
-whole; pinned only through its pinned pieces), see DESIGN.md.
+whole; pinned only through its pinned pieces), see DESIGN.md.  Push-forward /
+least-squares pins: tests/test_oracle_lsq.py.
 """
 from __future__ import annotations
 
@@ -759,3 +760,79 @@ def admm(Ip, Im, b0, h, alpha=ALPHA_DEFAULT, beta=BETA_DEFAULT, rho0=None, max_i
             break
     rep["rho_final"] = rho
     return b, z, rep
+
+
+# ---------------------------------------------------------------------------
+# Push-forward matrices, distortion simulation and least-squares correction
+# (SURVEY §8(f) NEXT-3).  Readings R27-R29 in DESIGN.md.
+#   True cell k (centre at index position k) is carried by the distortion to
+#   u_k = k + sign (A b)_k / h3 (the map x -> x + sign b(x) v of Eq.(1),
+#   P:72-76, in index units); its unit mass is split between the distorted
+#   cells next to u_k with hat weights (R27):
+#       A[j, k] = max(0, 1 - |u_k - j|),   j, k = 0..n3-1,
+#   mass landing outside [0, n3) is dropped.  The distorted image is I = A t.
+#   Least squares (R28, R29): t = argmin ||A+ t - i+||^2 + ||A- t - i-||^2
+#   + lambda ||D1 t||^2 per PE column, D1 the forward difference in index
+#   units, i.e. the normal equations
+#       (A+^T A+ + A-^T A- + lambda L1) t = A+^T i+ + A-^T i-,
+#   L1 = D1^T D1 (1-D Neumann Laplacian).
+# ---------------------------------------------------------------------------
+
+LSQ_LAMBDA_DEFAULT = 0.05   # R29
+
+
+def push_forward_matrix(bcol, h3, sign):
+    """Dense n3 x n3 push-forward matrix of one PE column (R27).
+    bcol: nodes (n3+1,) in mm."""
+    bcol = np.asarray(bcol, np.float64)
+    n3 = bcol.shape[0] - 1
+    u = np.arange(n3, dtype=np.float64) + sign * avg_pe(bcol) / h3
+    j = np.arange(n3, dtype=np.float64)
+    return np.maximum(0.0, 1.0 - np.abs(u[None, :] - j[:, None]))
+
+
+def push_forward(T, b, h3, sign):
+    """Distorted image I = A t per PE column of the true image T:
+    T cells (..., n3), b nodes (..., n3+1)."""
+    T = np.asarray(T, np.float64)
+    b = np.asarray(b, np.float64)
+    out = np.zeros_like(T)
+    for idx in np.ndindex(T.shape[:-1]):
+        out[idx] = push_forward_matrix(b[idx], h3, sign) @ T[idx]
+    return out
+
+
+def simulate_pair(T, b, h3):
+    """The distorted pair (I+, I-) of a true image under field map b."""
+    return push_forward(T, b, h3, +1.0), push_forward(T, b, h3, -1.0)
+
+
+def neumann_laplacian_1d(n):
+    """L1 = D1^T D1 for the (n-1) x n forward difference D1 (index units):
+    tridiagonal [1 -1; -1 2 -1; ...; -1 1] (R28)."""
+    L = np.zeros((n, n))
+    for k in range(n):
+        if k > 0:
+            L[k, k] += 1.0
+            L[k, k - 1] -= 1.0
+        if k < n - 1:
+            L[k, k] += 1.0
+            L[k, k + 1] -= 1.0
+    return L
+
+
+def lsq_correct(Ip, Im, b, h3, lam=LSQ_LAMBDA_DEFAULT):
+    """Least-squares correction (R28): per PE column the exact solution
+    of the normal equations above (dense direct solve)."""
+    Ip = np.asarray(Ip, np.float64)
+    Im = np.asarray(Im, np.float64)
+    b = np.asarray(b, np.float64)
+    n3 = Ip.shape[-1]
+    L1 = neumann_laplacian_1d(n3)
+    out = np.zeros_like(Ip)
+    for idx in np.ndindex(Ip.shape[:-1]):
+        Ap = push_forward_matrix(b[idx], h3, +1.0)
+        Am = push_forward_matrix(b[idx], h3, -1.0)
+        N = Ap.T @ Ap + Am.T @ Am + lam * L1
+        out[idx] = np.linalg.solve(N, Ap.T @ Ip[idx] + Am.T @ Im[idx])
+    return out

@@ -56,7 +56,8 @@ def build(force=False, verbose=False):
         nccl = ["-I" + inc, "-L" + libd, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + libd] if inc else ["-lnccl"]
         fdir = cufft_dir()
         cufft = ["-L" + fdir, "-l:libcufft.so.11", "-Xlinker", "-rpath=" + fdir] if fdir else ["-lcufft"]
-        cmd = [NVCC] + FLAGS + ["-o", LIB + ".tmp", SRC] + nccl + cufft
+        extra = os.environ.get("HYSCO_NVCC_EXTRA", "").split()   # diagnostic variants (tools/ab_bench.sh)
+        cmd = [NVCC] + FLAGS + extra + ["-o", LIB + ".tmp", SRC] + nccl + cufft
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)

@@ -359,9 +359,9 @@ struct Runner {
 // Resident PCG (fp32): K = node slots per thread, a compile-time parameter.
 #define RES_K_SWITCH(k, ...)                                                   \
     switch (k) {                                                               \
-        case 6: { constexpr int RK = 6; __VA_ARGS__; } break;                  \
-        case 12: { constexpr int RK = 12; __VA_ARGS__; } break;                \
-        default: { constexpr int RK = 18; __VA_ARGS__; } break;                \
+        case RES_KMAX / 3: { constexpr int RK = RES_KMAX / 3; __VA_ARGS__; } break; \
+        case 2 * RES_KMAX / 3: { constexpr int RK = 2 * RES_KMAX / 3; __VA_ARGS__; } break; \
+        default: { constexpr int RK = RES_KMAX; __VA_ARGS__; } break;          \
     }
 
 // bcur / bold: the trial b and b_old the fused Armijo start writes (B_B /
@@ -406,7 +406,7 @@ static void setup_resident(hysco_ctx ctx) {
     const long long nqmax = ncl_max * (res_pad(g.P) / 2);   // node pairs per CTA
     const long long need_k = (nqmax + RES_THREADS - 1) / RES_THREADS;
     if (need_k > RES_KMAX) return;
-    const int k = need_k <= 6 ? 6 : need_k <= 12 ? 12 : 18;
+    const int k = need_k <= RES_KMAX / 3 ? RES_KMAX / 3 : need_k <= 2 * RES_KMAX / 3 ? 2 * RES_KMAX / 3 : RES_KMAX;
     const size_t smem = res_smem_bytes(k);   // layout: hysco_resident.cuh
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->cfg.device);

@@ -25,8 +25,13 @@
 
 namespace hysco {
 
-constexpr int RES_THREADS = 512;   // 16 warps: 128 registers per thread, 18 node-pair slots without spills
-constexpr int RES_KMAX = 18;       // slots per thread (capacity 18 x 512 node pairs per SM)
+#ifndef RES_THREADS_DEF
+#define RES_THREADS_DEF 512
+#define RES_KMAX_DEF 18
+#endif
+constexpr int RES_THREADS = RES_THREADS_DEF;  // 16 warps: 128 registers per thread, 18 node-pair slots without spills
+constexpr int RES_KMAX = RES_KMAX_DEF;        // slots per thread (capacity 18 x 512 node pairs per SM)
+static_assert(RES_KMAX % 3 == 0 && 5 * RES_KMAX <= 128, "three slot-count variants; 5 mask fields in 128 bits");
 
 // Opaque copy: stops ptxas from hoisting per-slot index math (and everything
 // derived from it) out of the PCG iteration loop, which would keep ~15

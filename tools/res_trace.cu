@@ -23,9 +23,9 @@ int main(int argc, char** argv) {
     g.ahd = g.alpha * g.hd; g.bh2 = 0.5e-4 * g.hd;
     g.ih1sq = g.ih2sq = g.ih3sq = 1 / (1.25 * 1.25); g.ih3 = 1 / 1.25; geom_finish(g);
     int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-    const int G = nsm, NT = RES_THREADS, K = 18;
+    const int G = nsm, NT = RES_THREADS, K = RES_KMAX;
     const long long ncl = (g.ncol + G - 1) / G, knt = (long long)K * NT;
-    if (ncl * (res_pad(g.P) / 2) > knt) { printf("does not fit K=18\n"); return 1; }
+    if (ncl * (res_pad(g.P) / 2) > knt) { printf("does not fit K=RES_KMAX\n"); return 1; }
     size_t Nn = g.Nn;
     std::vector<float> hdt(Nn), het(Nn), hg(Nn);
     srand(1);
@@ -39,7 +39,7 @@ int main(int argc, char** argv) {
     cudaMalloc(&xpad, (size_t)g.ncol * res_pad(g.P) * 4);
     float *bb, *bo; cudaMalloc(&bb, Nn * 4); cudaMalloc(&bo, Nn * 4); cudaMemset(bb, 0, Nn * 4);
     const float wi = (float)(g.ahd * g.ih1sq), wj = (float)(g.ahd * g.ih2sq);
-    size_t ghost = res_ghost_pair_floats(g) + res_ghost_slack_floats(18);
+    size_t ghost = res_ghost_pair_floats(g) + res_ghost_slack_floats(RES_KMAX);
     cudaMalloc(&pgh, ghost * 4); cudaMemset(pgh, 0, ghost * 4);
     cudaMemcpy(dt, hdt.data(), Nn * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(et, het.data(), Nn * 4, cudaMemcpyHostToDevice);
@@ -56,9 +56,9 @@ int main(int argc, char** argv) {
     unsigned* dcond; cudaMalloc(&dcond, 4 * NCOND);
     Ctl c{}; c.st = st; c.launches = launches; c.dcond = dcond; c.use_graph = 0;
     SolveParams sp{}; sp.max_pcg = 10; sp.fixed = 1;
-    const size_t smem = res_smem_bytes(18);
-    cudaFuncSetAttribute(pcg_resident_kernel<18, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(pcg_resident_kernel<18, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem = res_smem_bytes(RES_KMAX);
+    cudaFuncSetAttribute(pcg_resident_kernel<RES_KMAX, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(pcg_resident_kernel<RES_KMAX, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(G); cfg.blockDim = dim3(NT); cfg.dynamicSmemBytes = smem; cfg.stream = 0;
     cudaLaunchAttribute at[1]; at[0].id = cudaLaunchAttributeCooperative; at[0].val.cooperative = 1;
@@ -67,12 +67,12 @@ int main(int argc, char** argv) {
     float ms_notrace = 0, ms_trace = 0;
     for (int rep = 0; rep < 7; rep++) {
         cudaEventRecord(e0);
-        cudaLaunchKernelEx(&cfg, pcg_resident_kernel<18, true>, g, c, sp, 0, (const float*)grad, (const float*)dt,
+        cudaLaunchKernelEx(&cfg, pcg_resident_kernel<RES_KMAX, true>, g, c, sp, 0, (const float*)grad, (const float*)dt,
                            (const float*)et, x, xpad, pgh, part, flags, wi, wj, bb, bo, 1, (unsigned long long*)nullptr);
         cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms_notrace, e0, e1);
     }
     cudaEventRecord(e0);
-    cudaLaunchKernelEx(&cfg, pcg_resident_kernel<18, true, true>, g, c, sp, 0, (const float*)grad, (const float*)dt,
+    cudaLaunchKernelEx(&cfg, pcg_resident_kernel<RES_KMAX, true, true>, g, c, sp, 0, (const float*)grad, (const float*)dt,
                        (const float*)et, x, xpad, pgh, part, flags, wi, wj, bb, bo, 1, trace);
     cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms_trace, e0, e1);
     printf("err=%s  kernel %.1f us (untraced), %.1f us (traced), grid %d x %d, K %d\n",
