@@ -206,6 +206,43 @@ HYSCO_API hysco_status hysco_admm(hysco_ctx ctx, void* d_b_inout, const hysco_ad
  * T[I+, b, v], T[I-, b, -v] (device cells). */
 HYSCO_API hysco_status hysco_apply(hysco_ctx ctx, const void* d_b, void* d_Iplus_corr, void* d_Iminus_corr);
 
+/* Distortion simulation: I+ = A+ T, I- = A- T per PE column, A+-
+ * the push-forward matrices of b (R27: true cell k moves to k +- (A b)_k/h3 in
+ * index units, its unit mass split between the two nearest distorted cells
+ * with hat weights, mass leaving the field of view dropped).  d_b: device
+ * nodes; d_T, d_Iplus, d_Iminus: device cells (must not alias).  Synchronises
+ * the context stream.  Returns HYSCO_INFEASIBLE if some column has |Db| >= 1
+ * (its outputs are then undefined).  Not on slab contexts. */
+HYSCO_API hysco_status hysco_push_forward(hysco_ctx ctx, const void* d_b, const void* d_T, void* d_Iplus,
+                                          void* d_Iminus);
+
+/* Least-squares correction options (R28, R29). */
+typedef struct {
+    double lambda;           /* weight of ||D1 t||^2 (1-D Neumann, index units), default 0.05 (R29) */
+    int32_t max_iter;        /* PCG iterations per column, default 200                              */
+    double rtol;             /* stop at ||r|| <= rtol ||rhs||; 0 = 1e-6 (f32) / 1e-12 (f64)          */
+} hysco_lsq_opts;
+
+/* Per-pair least-squares report. */
+typedef struct {
+    int32_t max_iters;       /* most PCG iterations any column used            */
+    int64_t unconverged;     /* columns that hit max_iter before rtol           */
+    int64_t infeasible;      /* columns with |Db| >= 1 (output set to 0)        */
+    double max_relres;       /* largest final ||r|| / ||rhs|| over the columns */
+} hysco_lsq_report;
+
+HYSCO_API void hysco_default_lsq_opts(hysco_lsq_opts* o);
+
+/* Least-squares correction (R28): one corrected image t per pair,
+ * per PE column the solution of (A+^T A+ + A-^T A- + lambda L1) t =
+ * A+^T i+ + A-^T i- for the bound pair (i+, i-) and field map b (device
+ * nodes), by Jacobi-PCG per column (one warp each).  d_T_out: device cells
+ * [batch][n1][n2][n3].  reports: [batch] or NULL.  Synchronises the context
+ * stream.  Returns HYSCO_INFEASIBLE if some column has |Db| >= 1.  Not on
+ * slab contexts. */
+HYSCO_API hysco_status hysco_lsq_correct(hysco_ctx ctx, const void* d_b, const hysco_lsq_opts* opts,
+                                         void* d_T_out, hysco_lsq_report* reports);
+
 /* The whole path in one call on device buffers: OT init (+blur, guard) ->
  * GN-PCG -> apply.  Any output pointer may be NULL. */
 HYSCO_API hysco_status hysco_correct(hysco_ctx ctx, const hysco_ot_opts* ot, const hysco_solve_opts* so,

@@ -1285,6 +1285,70 @@ static hysco_status create_impl(const hysco_config* cfg, const SlabSpec* slab, v
     return HYSCO_OK;
 }
 
+
+// ---- push-forward simulation / least-squares correction (NEXT-3, R27-R29) ----
+template <typename T, typename K>
+static hysco_status lsq_grid(hysco_ctx ctx, K kern, int nT, int* gx, size_t* smem) {
+    const Geom& g = ctx->g;
+    *smem = (size_t)LSQ_WARPS * lsq_warp_bytes<T>(g.n3, nT);
+    if (*smem > 227 * 1024) return set_err(ctx, HYSCO_ERR_SHAPE, "n3 too large for the least-squares column kernels");
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem));
+    int occ = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * LSQ_WARPS, *smem) != cudaSuccess || occ < 1)
+        occ = 1;
+    const long long work = (g.ncol + LSQ_WARPS - 1) / LSQ_WARPS;
+    const long long cap = ((long long)ctx->nsm * occ + ctx->cfg.batch - 1) / ctx->cfg.batch;
+    *gx = (int)std::max(1LL, std::min(work, cap));
+    return HYSCO_OK;
+}
+
+template <typename T>
+static hysco_status push_forward_run(hysco_ctx ctx, const void* b, const void* t, void* ip, void* im) {
+    int gx;
+    size_t smem;
+    if (hysco_status s = lsq_grid<T>(ctx, push_forward_kernel<T>, 6, &gx, &smem)) return s;
+    const int B = ctx->cfg.batch;
+    CK(cudaMemsetAsync(ctx->red, 0, sizeof(double) * RED_W * B, ctx->stream));
+    push_forward_kernel<T><<<dim3(gx, B), 32 * LSQ_WARPS, smem, ctx->stream>>>(
+        ctx->g, ctx->ctl, (const T*)b, (const T*)t, (T*)ip, (T*)im);
+    CK(cudaGetLastError());
+    std::vector<double> red((size_t)B * RED_W);
+    CK(cudaMemcpyAsync(red.data(), ctx->red, sizeof(double) * B * RED_W, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (int p = 0; p < B; p++)
+        if (red[(size_t)p * RED_W + LSQ_ST_INFEAS] > 0) return HYSCO_INFEASIBLE;
+    return HYSCO_OK;
+}
+
+template <typename T>
+static hysco_status lsq_run(hysco_ctx ctx, const void* b, const hysco_lsq_opts& o, void* tout,
+                            hysco_lsq_report* reps) {
+    int gx;
+    size_t smem;
+    if (hysco_status s = lsq_grid<T>(ctx, lsq_kernel<T>, 9, &gx, &smem)) return s;
+    const int B = ctx->cfg.batch;
+    const double rtol = o.rtol > 0 ? o.rtol : (sizeof(T) == 8 ? 1e-12 : 1e-6);
+    CK(cudaMemsetAsync(ctx->red, 0, sizeof(double) * RED_W * B, ctx->stream));
+    lsq_kernel<T><<<dim3(gx, B), 32 * LSQ_WARPS, smem, ctx->stream>>>(
+        ctx->g, ctx->ctl, (const T*)b, (const T*)ctx->Ip, (const T*)ctx->Im, (T*)tout, o.lambda, o.max_iter, rtol);
+    CK(cudaGetLastError());
+    std::vector<double> red((size_t)B * RED_W);
+    CK(cudaMemcpyAsync(red.data(), ctx->red, sizeof(double) * B * RED_W, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    bool infeas = false;
+    for (int p = 0; p < B; p++) {
+        const double* t = &red[(size_t)p * RED_W];
+        if (reps) {
+            reps[p].max_iters = (int32_t)t[LSQ_ST_ITERS];
+            reps[p].unconverged = (int64_t)t[LSQ_ST_UNCONV];
+            reps[p].infeasible = (int64_t)t[LSQ_ST_INFEAS];
+            reps[p].max_relres = t[LSQ_ST_RELRES];
+        }
+        infeas |= t[LSQ_ST_INFEAS] > 0;
+    }
+    return infeas ? HYSCO_INFEASIBLE : HYSCO_OK;
+}
+
 extern "C" {
 
 hysco_status hysco_create(const hysco_config* cfg, void* cuda_stream, hysco_ctx* out) {
@@ -1442,6 +1506,39 @@ hysco_status hysco_admm(hysco_ctx ctx, void* d_b_inout, const hysco_admm_opts* o
         return set_err(ctx, HYSCO_ERR_ARG, "bad hysco_admm_opts");
     return ctx->cfg.dtype == HYSCO_F64 ? admm_run<double>(ctx, d_b_inout, o, reports)
                                        : admm_run<float>(ctx, d_b_inout, o, reports);
+}
+
+void hysco_default_lsq_opts(hysco_lsq_opts* o) {
+    if (!o) return;
+    o->lambda = 0.05;
+    o->max_iter = 200;
+    o->rtol = 0.0;
+}
+
+hysco_status hysco_push_forward(hysco_ctx ctx, const void* d_b, const void* d_T, void* d_Iplus, void* d_Iminus) {
+    CHECK_CTX();
+    if (ctx->g.slab) return set_err(ctx, HYSCO_ERR_STATE, "slab contexts support solve / correct / correct_host");
+    if (!d_b || !d_T || !d_Iplus || !d_Iminus || !aligned16(d_b) || !aligned16(d_T) || !aligned16(d_Iplus) ||
+        !aligned16(d_Iminus))
+        return set_err(ctx, HYSCO_ERR_ARG, "pointers must be non-NULL and 16-byte aligned");
+    return ctx->cfg.dtype == HYSCO_F64 ? push_forward_run<double>(ctx, d_b, d_T, d_Iplus, d_Iminus)
+                                       : push_forward_run<float>(ctx, d_b, d_T, d_Iplus, d_Iminus);
+}
+
+hysco_status hysco_lsq_correct(hysco_ctx ctx, const void* d_b, const hysco_lsq_opts* opts, void* d_T_out,
+                               hysco_lsq_report* reports) {
+    CHECK_CTX();
+    if (ctx->g.slab) return set_err(ctx, HYSCO_ERR_STATE, "slab contexts support solve / correct / correct_host");
+    if (hysco_status s = need_images(ctx)) return s;
+    if (!d_b || !d_T_out || !aligned16(d_b) || !aligned16(d_T_out))
+        return set_err(ctx, HYSCO_ERR_ARG, "pointers must be non-NULL and 16-byte aligned");
+    hysco_lsq_opts o;
+    hysco_default_lsq_opts(&o);
+    if (opts) o = *opts;
+    if (!(o.lambda >= 0) || o.max_iter < 0 || !(o.rtol >= 0))
+        return set_err(ctx, HYSCO_ERR_ARG, "bad hysco_lsq_opts");
+    return ctx->cfg.dtype == HYSCO_F64 ? lsq_run<double>(ctx, d_b, o, d_T_out, reports)
+                                       : lsq_run<float>(ctx, d_b, o, d_T_out, reports);
 }
 
 hysco_status hysco_apply(hysco_ctx ctx, const void* d_b, void* d_Iplus_corr, void* d_Iminus_corr) {

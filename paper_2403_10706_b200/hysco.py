@@ -28,7 +28,7 @@ EXPORTED = ["hysco_default_solve_opts", "hysco_default_ot_opts", "hysco_default_
             "hysco_last_launch_count",
             "hysco_last_error", "hysco_destroy", "hysco_version", "hysco_profile_kernels",
             "hysco_nccl_unique_id", "hysco_create_slab", "hysco_create_loopback", "hysco_group_correct",
-            "hysco_group_solve"]
+            "hysco_group_solve", "hysco_push_forward", "hysco_default_lsq_opts", "hysco_lsq_correct"]
 PROF_NAMES = ["matvec", "pcg_update", "pcg_dir", "eval", "pcg_resident", "trial_init"]
 
 
@@ -67,6 +67,18 @@ class hysco_admm_report(ctypes.Structure):
     _fields_ = [("iters", ctypes.c_int32), ("converged", ctypes.c_int32), ("rho", ctypes.c_double),
                 ("r_norm", ctypes.c_double), ("s_norm", ctypes.c_double), ("J", ctypes.c_double),
                 ("D", ctypes.c_double), ("S", ctypes.c_double), ("P", ctypes.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class hysco_lsq_opts(ctypes.Structure):
+    _fields_ = [("lam", ctypes.c_double), ("max_iter", ctypes.c_int32), ("rtol", ctypes.c_double)]
+
+
+class hysco_lsq_report(ctypes.Structure):
+    _fields_ = [("max_iters", ctypes.c_int32), ("unconverged", ctypes.c_int64), ("infeasible", ctypes.c_int64),
+                ("max_relres", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -115,6 +127,12 @@ def lib():
     L.hysco_default_admm_opts.restype = None
     L.hysco_admm.argtypes = [vp, vp, ctypes.POINTER(hysco_admm_opts), ctypes.POINTER(hysco_admm_report)]
     L.hysco_admm.restype = st
+    L.hysco_push_forward.argtypes = [vp, vp, vp, vp, vp]
+    L.hysco_push_forward.restype = st
+    L.hysco_default_lsq_opts.argtypes = [ctypes.POINTER(hysco_lsq_opts)]
+    L.hysco_default_lsq_opts.restype = None
+    L.hysco_lsq_correct.argtypes = [vp, vp, ctypes.POINTER(hysco_lsq_opts), vp, ctypes.POINTER(hysco_lsq_report)]
+    L.hysco_lsq_correct.restype = st
     L.hysco_precond_solve.argtypes = [vp, ctypes.c_int32, vp, vp]
     L.hysco_solve.argtypes = [vp, vp, ctypes.POINTER(hysco_solve_opts), ctypes.POINTER(hysco_report)]
     L.hysco_apply.argtypes = [vp, vp, vp, vp]
@@ -198,6 +216,30 @@ def hysco_admm(ctx, b_inout, opts=None, batch=1):
     reps = (hysco_admm_report * batch)()
     _check(ctx, lib().hysco_admm(ctx, _ptr(b_inout), ctypes.byref(opts) if opts is not None else None, reps))
     return [r.as_dict() for r in reps]
+
+
+def default_lsq_opts(**kw):
+    """hysco_lsq_opts with the library defaults; `lam` is the C field `lambda`."""
+    o = hysco_lsq_opts()
+    lib().hysco_default_lsq_opts(ctypes.byref(o))
+    for k, v in kw.items():
+        setattr(o, k, v)
+    return o
+
+
+def hysco_push_forward(ctx, b, T, Ip_out, Im_out):
+    """Distortion simulation I+- = A+- T (device tensors); returns True if some column was infeasible."""
+    s = _check(ctx, lib().hysco_push_forward(ctx, _ptr(b), _ptr(T), _ptr(Ip_out), _ptr(Im_out)),
+               (HYSCO_OK, HYSCO_INFEASIBLE))
+    return s == HYSCO_INFEASIBLE
+
+
+def hysco_lsq_correct(ctx, b, T_out, opts=None, batch=1):
+    """Least-squares correction of the bound pair into T_out; returns (reports, infeasible)."""
+    reps = (hysco_lsq_report * batch)()
+    s = _check(ctx, lib().hysco_lsq_correct(ctx, _ptr(b), ctypes.byref(opts) if opts is not None else None,
+                                            _ptr(T_out), reps), (HYSCO_OK, HYSCO_INFEASIBLE))
+    return [r.as_dict() for r in reps], s == HYSCO_INFEASIBLE
 
 
 def default_ot_opts(**kw):
