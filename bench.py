@@ -53,6 +53,9 @@ def parse():
                     help="fixed 10 GN x 10 PCG (the headline) or the paper's stop rules (P:196, P:284, R16)")
     ap.add_argument("--solver", default="gn", choices=["gn", "admm"],
                     help="Gauss-Newton-PCG (the headline, P:183-199) or ADMM (P:203-239) with the paper-style stop")
+    ap.add_argument("--stage", default="path", choices=["path", "lsq"],
+                    help="the GN path (default) or the NEXT-3 stage: push-forward simulation of the pair from the "
+                         "true image + least-squares correction (P:289, P:331)")
     ap.add_argument("--slab", action="store_true",
                     help="partition ONE pair of --config into slabs along dim 1 across the ranks (configs[4])")
     return ap.parse_args()
@@ -453,6 +456,84 @@ def run_admm(args):
         print(json.dumps(line), flush=True)
 
 
+def run_lsq(args):
+    """NEXT-3 mode (not the headline): per step the distorted pair is simulated
+    from the synthetic true image and field map by push-forward and
+    corrected by least squares (R28, lambda = 0.05), both through the
+    C ABI.  Timed with CUDA events on the context stream; each kernel timed
+    alone as well."""
+    import torch
+    from paper_2403_10706_b200 import hysco as H
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    shape, h, seed = phantom.CONFIGS[args.config]
+    n1, n2, n3 = shape
+    p = phantom.make_pair(shape, h, seed + 1000 * rank)
+    T = torch.from_numpy(p.I_true[None].astype(np.float32)).to(dev)
+    b = torch.from_numpy(p.b_true[None].astype(np.float32)).to(dev)
+    Ip, Im, out = torch.zeros_like(T), torch.zeros_like(T), torch.zeros_like(T)
+    stream = torch.cuda.current_stream(dev)
+    ctx = H.hysco_create(shape, h, 1, device=local, stream=stream.cuda_stream)
+    H.hysco_bind_images(ctx, Ip, Im)
+    lo = H.default_lsq_opts()
+    flush = torch.empty(256 << 18, dtype=torch.float32, device=dev)
+    torch.cuda.synchronize(dev)
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)          # noqa: E731
+    rep = None
+    for _ in range(max(args.warmup, 0)):
+        H.hysco_push_forward(ctx, b, T, Ip, Im)
+        rep, _ = H.hysco_lsq_correct(ctx, b, out, lo)
+    torch.cuda.synchronize(dev)
+    err = float(torch.linalg.norm(out - T) / torch.linalg.norm(T))
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)
+    ms, ms_pf, ms_lsq, launches = [], [], [], 0
+    for _ in range(args.steps):
+        flush.zero_()
+        a, m, z = ev(), ev(), ev()
+        a.record(stream)
+        H.hysco_push_forward(ctx, b, T, Ip, Im)
+        launches += H.hysco_last_launch_count(ctx)
+        m.record(stream)
+        rep, _ = H.hysco_lsq_correct(ctx, b, out, lo)
+        launches += H.hysco_last_launch_count(ctx)
+        z.record(stream)
+        z.synchronize()
+        ms.append(a.elapsed_time(z))
+        ms_pf.append(a.elapsed_time(m))
+        ms_lsq.append(m.elapsed_time(z))
+    clocks = clk.stop()
+    H.hysco_destroy(ctx)
+    if rank == 0:
+        tot = float(np.sum(ms))
+        Nc, Nn = n1 * n2 * n3, n1 * n2 * (n3 + 1)
+        pf_bytes, lsq_bytes = 4 * (3 * Nc + Nn), 4 * (3 * Nc + Nn)
+        peak, peak_src = peaks()
+        t_pf, t_lsq = float(np.mean(ms_pf)), float(np.mean(ms_lsq))
+        line = {"metric": "volume pairs simulated + least-squares corrected/sec", "value": world * args.steps / (tot / 1e3),
+                "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": tot / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f32", "data": "synthetic",
+                "config": {"workload": f"{args.config}: push-forward simulation of I+- from the true image and "
+                                       "field map (P:331, R27) -> least-squares correction (P:289, R28, "
+                                       "lambda 0.05, Jacobi-PCG to rtol 1e-6 per PE column)",
+                           "pairs_per_gpu": 1, "seed": seed, "l2": "flushed (256 MiB write) between timed steps",
+                           "parallelism": f"dp{world} (independent pairs per rank)"},
+                "clocks": clocks, "gpu_launches": launches,
+                "kernels_ms": {"push_forward": t_pf, "lsq": t_lsq},
+                "roofline": {"bound": "latency (per-column PCG in shared memory)",
+                             "hbm_view": {"push_forward_GBs": pf_bytes / (t_pf * 1e6),
+                                          "lsq_GBs": lsq_bytes / (t_lsq * 1e6), "peak": peak, "peak_src": peak_src,
+                                          "bytes_per_pair": {"push_forward": pf_bytes, "lsq": lsq_bytes}}},
+                "lsq_report": rep[0], "rel_error_vs_true_image": err,
+                "note": "mode line (not the headline); kernel times include the host read of the per-pair stats"}
+        print(json.dumps(line), flush=True)
+
+
 def run_slab(args):
     """Strong scaling of ONE large pair (BASELINE.json configs[4]): rank r owns
     planes slab_bounds(n1, N, r) of dim 1; libhysco exchanges one halo plane and
@@ -532,6 +613,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.stage == "lsq":
+        run_lsq(args)
     elif args.solver == "admm":
         run_admm(args)
     elif args.slab:

@@ -1309,12 +1309,16 @@ static hysco_status push_forward_run(hysco_ctx ctx, const void* b, const void* t
     if (hysco_status s = lsq_grid<T>(ctx, push_forward_kernel<T>, 6, &gx, &smem)) return s;
     const int B = ctx->cfg.batch;
     CK(cudaMemsetAsync(ctx->red, 0, sizeof(double) * RED_W * B, ctx->stream));
+    CK(cudaMemsetAsync(ctx->launches, 0, sizeof(unsigned long long), ctx->stream));
     push_forward_kernel<T><<<dim3(gx, B), 32 * LSQ_WARPS, smem, ctx->stream>>>(
         ctx->g, ctx->ctl, (const T*)b, (const T*)t, (T*)ip, (T*)im);
     CK(cudaGetLastError());
     std::vector<double> red((size_t)B * RED_W);
     CK(cudaMemcpyAsync(red.data(), ctx->red, sizeof(double) * B * RED_W, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->h_launches, ctx->launches, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                       ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    ctx->last_launches = (long long)*ctx->h_launches;
     for (int p = 0; p < B; p++)
         if (red[(size_t)p * RED_W + LSQ_ST_INFEAS] > 0) return HYSCO_INFEASIBLE;
     return HYSCO_OK;
@@ -1329,12 +1333,16 @@ static hysco_status lsq_run(hysco_ctx ctx, const void* b, const hysco_lsq_opts& 
     const int B = ctx->cfg.batch;
     const double rtol = o.rtol > 0 ? o.rtol : (sizeof(T) == 8 ? 1e-12 : 1e-6);
     CK(cudaMemsetAsync(ctx->red, 0, sizeof(double) * RED_W * B, ctx->stream));
+    CK(cudaMemsetAsync(ctx->launches, 0, sizeof(unsigned long long), ctx->stream));
     lsq_kernel<T><<<dim3(gx, B), 32 * LSQ_WARPS, smem, ctx->stream>>>(
         ctx->g, ctx->ctl, (const T*)b, (const T*)ctx->Ip, (const T*)ctx->Im, (T*)tout, o.lambda, o.max_iter, rtol);
     CK(cudaGetLastError());
     std::vector<double> red((size_t)B * RED_W);
     CK(cudaMemcpyAsync(red.data(), ctx->red, sizeof(double) * B * RED_W, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->h_launches, ctx->launches, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                       ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    ctx->last_launches = (long long)*ctx->h_launches;
     bool infeas = false;
     for (int p = 0; p < B; p++) {
         const double* t = &red[(size_t)p * RED_W];

@@ -229,7 +229,9 @@ def test_hcp3t_lsq_and_push_forward_sampled_columns():
     Pp, Pm, out = torch.zeros_like(Ip), torch.zeros_like(Ip), torch.zeros_like(Ip)
     torch.cuda.synchronize()
     assert not H.hysco_push_forward(c, bt, Ip, Pp, Pm)
+    assert H.hysco_last_launch_count(c) == 1
     reps, infeas = H.hysco_lsq_correct(c, bt, out, None)
+    assert H.hysco_last_launch_count(c) == 1
     assert not infeas and reps[0]["unconverged"] == 0, reps
     rng = np.random.default_rng(0)
     cols = [(int(rng.integers(shape[0])), int(rng.integers(shape[1]))) for _ in range(64)]
