@@ -53,9 +53,10 @@ def parse():
                     help="fixed 10 GN x 10 PCG (the headline) or the paper's stop rules (P:196, P:284, R16)")
     ap.add_argument("--solver", default="gn", choices=["gn", "admm"],
                     help="Gauss-Newton-PCG (the headline, P:183-199) or ADMM (P:203-239) with the paper-style stop")
-    ap.add_argument("--stage", default="path", choices=["path", "lsq"],
+    ap.add_argument("--stage", default="path", choices=["path", "lsq", "cli"],
                     help="the GN path (default) or the NEXT-3 stage: push-forward simulation of the pair from the "
-                         "true image + least-squares correction (P:289, P:331)")
+                         "true image + least-squares correction (P:289, P:331); or the whole command-line run "
+                         "(NIfTI .nii.gz in/out, P:291-295; the paper's 'Run' column)")
     ap.add_argument("--slab", action="store_true",
                     help="partition ONE pair of --config into slabs along dim 1 across the ranks (configs[4])")
     return ap.parse_args()
@@ -534,6 +535,63 @@ def run_lsq(args):
         print(json.dumps(line), flush=True)
 
 
+def run_cli(args):
+    """NEXT-4 mode (not the headline): the command-line front-end end to end
+    on the --config pair written as gzip NIfTI files with the PE axis along y
+    (the file order needs the GPU permutation): read + decompress, H2D,
+    permute, OT + GN-PCG (paper stop rules) + Jacobian correction, permute
+    back, D2H, compress + write fieldmap / plus / minus.  Wall clock of
+    cli.main() per step (the paper's 'Run' time includes its I/O, T3)."""
+    import tempfile
+    from paper_2403_10706_b200 import cli
+    from paper_2403_10706_b200 import hysco as H
+
+    shape, h, seed = phantom.CONFIGS[args.config]
+    p = phantom.make_pair(shape, h, seed)
+    d = tempfile.mkdtemp(prefix="hysco_cli_")
+    info = H.hysco_nifti_info()
+    n1, n2, n3 = shape                                   # file (nx, ny, nz) = (n2, n3, n1): PE on y
+    for k, (n, hh) in enumerate(((n2, h[1]), (n3, h[2]), (n1, h[0]))):
+        info.dim[k] = n
+        info.pixdim[k] = hh
+    info.qfac = 1.0
+    for name, img in (("p", p.Ip), ("m", p.Im)):
+        H.hysco_nifti_write(os.path.join(d, name + ".nii.gz"), np.ascontiguousarray(img.transpose(0, 2, 1)), info)
+    argv = [os.path.join(d, "p.nii.gz"), os.path.join(d, "m.nii.gz"), "--pe-axis", "2", "--out",
+            os.path.join(d, "o")]
+    import contextlib
+    import io
+    for _ in range(max(args.warmup, 0)):
+        with contextlib.redirect_stdout(io.StringIO()):
+            cli.main(argv)
+    secs, stages = [], []
+    for _ in range(args.steps):
+        buf = io.StringIO()
+        t0 = time.perf_counter()
+        with contextlib.redirect_stdout(buf):
+            cli.main(argv)
+        secs.append(time.perf_counter() - t0)
+        stages.append(json.loads(buf.getvalue().strip().splitlines()[-1])["seconds"])
+    last = json.loads(buf.getvalue().strip().splitlines()[-1])
+    import subprocess
+    t0 = time.perf_counter()                            # like the paper's Linux `time` of the CLI: cold process
+    subprocess.run([sys.executable, "-m", "paper_2403_10706_b200.cli"] + argv, check=True, cwd=ROOT,
+                   stdout=subprocess.DEVNULL)
+    cold = time.perf_counter() - t0
+    line = {"metric": "command-line run time per pair (NIfTI .nii.gz in and out)", "value": float(np.median(secs)),
+            "unit": "s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * float(np.median(secs)), "higher_is_better": False, "scaling": "none",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{args.config} as gzip NIfTI, PE along the file's y axis: python -m "
+                                   "paper_2403_10706_b200.cli (OT + GN-PCG with the paper's stop rules + Jacobian "
+                                   "correction), wall clock in-process (CUDA context already up)"},
+            "stage_seconds_median": {k: float(np.median([s[k] for s in stages])) for k in stages[0]},
+            "cold_process_s": cold, "paper_run_s_context": {"3T": 10.37, "7T": 13.62, "source": "T3 (RTX A6000)"},
+            "report": last["report"],
+            "note": "mode line (not the headline); the paper's T3 'Run' column is the same pipeline incl. I/O"}
+    print(json.dumps(line), flush=True)
+
+
 def run_slab(args):
     """Strong scaling of ONE large pair (BASELINE.json configs[4]): rank r owns
     planes slab_bounds(n1, N, r) of dim 1; libhysco exchanges one halo plane and
@@ -615,6 +673,8 @@ def main():
         run_reference(args)
     elif args.stage == "lsq":
         run_lsq(args)
+    elif args.stage == "cli":
+        run_cli(args)
     elif args.solver == "admm":
         run_admm(args)
     elif args.slab:

@@ -5,8 +5,10 @@ import subprocess
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 SRC = os.path.join(PKG, "csrc", "hysco_api.cu")
+SRC_IO = os.path.join(PKG, "csrc", "hysco_io.cu")
 DEPS = [os.path.join(PKG, "csrc", f) for f in sorted(os.listdir(os.path.join(PKG, "csrc")))] + \
-       [os.path.join(ROOT, "include", "hysco.h"), os.path.abspath(__file__)]
+       [os.path.join(ROOT, "include", "hysco.h"), os.path.join(ROOT, "include", "hysco_io.h"),
+        os.path.abspath(__file__)]
 LIB = os.path.join(PKG, "libhysco.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
@@ -57,7 +59,7 @@ def build(force=False, verbose=False):
         fdir = cufft_dir()
         cufft = ["-L" + fdir, "-l:libcufft.so.11", "-Xlinker", "-rpath=" + fdir] if fdir else ["-lcufft"]
         extra = os.environ.get("HYSCO_NVCC_EXTRA", "").split()   # diagnostic variants (tools/ab_bench.sh)
-        cmd = [NVCC] + FLAGS + extra + ["-o", LIB + ".tmp", SRC] + nccl + cufft
+        cmd = [NVCC] + FLAGS + extra + ["-o", LIB + ".tmp", SRC, SRC_IO] + nccl + cufft + ["-lz"]
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)

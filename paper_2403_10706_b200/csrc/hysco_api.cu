@@ -7,6 +7,7 @@
 // same kernels exists for drivers without conditional nodes (HYSCO_NO_GRAPH=1
 // forces it).
 #include "hysco.h"
+#include "hysco_io.h"
 #include "hysco_kernels.cuh"
 
 #include <nccl.h>
@@ -1547,6 +1548,23 @@ hysco_status hysco_lsq_correct(hysco_ctx ctx, const void* d_b, const hysco_lsq_o
         return set_err(ctx, HYSCO_ERR_ARG, "bad hysco_lsq_opts");
     return ctx->cfg.dtype == HYSCO_F64 ? lsq_run<double>(ctx, d_b, o, d_T_out, reports)
                                        : lsq_run<float>(ctx, d_b, o, d_T_out, reports);
+}
+
+hysco_status hysco_fieldmap_cells(hysco_ctx ctx, const void* d_b, void* d_out) {
+    CHECK_CTX();
+    if (ctx->g.slab) return set_err(ctx, HYSCO_ERR_STATE, "slab contexts support solve / correct / correct_host");
+    if (!d_b || !d_out || !aligned16(d_b) || !aligned16(d_out))
+        return set_err(ctx, HYSCO_ERR_ARG, "pointers must be non-NULL and 16-byte aligned");
+    const long long total = (long long)ctx->cfg.batch * ctx->g.Nc;
+    const int grid = (int)std::min<long long>((total + 255) / 256, (long long)ctx->nsm * 8);
+    if (ctx->cfg.dtype == HYSCO_F64)
+        fieldmap_cells_kernel<double><<<grid, 256, 0, ctx->stream>>>(ctx->g, ctx->ctl, (const double*)d_b,
+                                                                    (double*)d_out, total);
+    else
+        fieldmap_cells_kernel<float><<<grid, 256, 0, ctx->stream>>>(ctx->g, ctx->ctl, (const float*)d_b,
+                                                                   (float*)d_out, total);
+    CK(cudaGetLastError());
+    return HYSCO_OK;
 }
 
 hysco_status hysco_apply(hysco_ctx ctx, const void* d_b, void* d_Iplus_corr, void* d_Iminus_corr) {

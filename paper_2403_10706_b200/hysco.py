@@ -28,7 +28,10 @@ EXPORTED = ["hysco_default_solve_opts", "hysco_default_ot_opts", "hysco_default_
             "hysco_last_launch_count",
             "hysco_last_error", "hysco_destroy", "hysco_version", "hysco_profile_kernels",
             "hysco_nccl_unique_id", "hysco_create_slab", "hysco_create_loopback", "hysco_group_correct",
-            "hysco_group_solve", "hysco_push_forward", "hysco_default_lsq_opts", "hysco_lsq_correct"]
+            "hysco_group_solve", "hysco_push_forward", "hysco_default_lsq_opts", "hysco_lsq_correct",
+            # front-end (include/hysco_io.h)
+            "hysco_nifti_info_read", "hysco_nifti_read", "hysco_nifti_write", "hysco_io_last_error", "hysco_pe_shape",
+            "hysco_permute_pe", "hysco_fieldmap_cells"]
 PROF_NAMES = ["matvec", "pcg_update", "pcg_dir", "eval", "pcg_resident", "trial_init"]
 
 
@@ -82,6 +85,13 @@ class hysco_lsq_report(ctypes.Structure):
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class hysco_nifti_info(ctypes.Structure):
+    _fields_ = [("dim", ctypes.c_int64 * 3), ("pixdim", ctypes.c_double * 3), ("datatype", ctypes.c_int32),
+                ("scl_slope", ctypes.c_double), ("scl_inter", ctypes.c_double), ("qform_code", ctypes.c_int32),
+                ("sform_code", ctypes.c_int32), ("qfac", ctypes.c_double), ("quatern", ctypes.c_double * 3),
+                ("qoffset", ctypes.c_double * 3), ("srow", ctypes.c_double * 12)]
 
 
 class hysco_report(ctypes.Structure):
@@ -153,6 +163,17 @@ def lib():
     L.hysco_destroy.argtypes = [vp]
     L.hysco_last_launch_count.argtypes = [vp]
     L.hysco_last_launch_count.restype = ctypes.c_int64
+    NI = ctypes.POINTER(hysco_nifti_info)
+    L.hysco_nifti_info_read.argtypes = [ctypes.c_char_p, NI]
+    L.hysco_nifti_read.argtypes = [ctypes.c_char_p, ctypes.c_int, vp, ctypes.c_int64, NI]
+    L.hysco_nifti_write.argtypes = [ctypes.c_char_p, ctypes.c_int, vp, NI]
+    L.hysco_io_last_error.argtypes = []
+    L.hysco_io_last_error.restype = ctypes.c_char_p
+    L.hysco_pe_shape.argtypes = [ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_double), ctypes.c_int32,
+                                 ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_double)]
+    L.hysco_permute_pe.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_int64), ctypes.c_int32, ctypes.c_int32,
+                                   ctypes.c_int, ctypes.c_int64, vp]
+    L.hysco_fieldmap_cells.argtypes = [vp, vp, vp]
     L.hysco_last_error.argtypes = [vp]
     L.hysco_last_error.restype = ctypes.c_char_p
     L.hysco_profile_kernels.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_double)]
@@ -431,3 +452,54 @@ def hysco_destroy(ctx):
 
 def hysco_version():
     return int(lib().hysco_version())
+
+
+# ---- front-end (include/hysco_io.h; NEXT-4) --------------------------------
+
+def _io_check(s):
+    if s != HYSCO_OK:
+        raise HyscoError(s, lib().hysco_io_last_error().decode())
+    return s
+
+
+def hysco_nifti_info_read(path):
+    info = hysco_nifti_info()
+    _io_check(lib().hysco_nifti_info_read(os.fsencode(path), ctypes.byref(info)))
+    return info
+
+
+def hysco_nifti_read(path, dtype=HYSCO_F32):
+    """Voxel data as a C array [nz][ny][nx] of dtype (scaled), and the header."""
+    info = hysco_nifti_info_read(path)
+    nx, ny, nz = info.dim
+    out = np.empty((nz, ny, nx), dtype=np.float64 if dtype == HYSCO_F64 else np.float32)
+    _io_check(lib().hysco_nifti_read(os.fsencode(path), dtype, _ptr(out), out.size, ctypes.byref(info)))
+    return out, info
+
+
+def hysco_nifti_write(path, data, info):
+    """data: C array [nz][ny][nx] of float32 / float64; dims, voxel sizes, geometry from info."""
+    dtype = HYSCO_F64 if data.dtype == np.float64 else HYSCO_F32
+    assert data.dtype in (np.float32, np.float64) and data.shape == (info.dim[2], info.dim[1], info.dim[0])
+    _io_check(lib().hysco_nifti_write(os.fsencode(path), dtype, _ptr(np.ascontiguousarray(data)),
+                                      ctypes.byref(info)))
+
+
+def hysco_pe_shape(dims, pixdim, pe_axis):
+    """Kernel layout (n1, n2, n3) and voxel sizes of a volume with NIfTI dims whose PE axis is pe_axis."""
+    d = (ctypes.c_int64 * 3)(*[int(x) for x in dims])
+    p = (ctypes.c_double * 3)(*[float(x) for x in pixdim])
+    n = (ctypes.c_int64 * 3)()
+    h = (ctypes.c_double * 3)()
+    _io_check(lib().hysco_pe_shape(d, p, int(pe_axis), n, h))
+    return tuple(n), tuple(h)
+
+
+def hysco_permute_pe(d_in, d_out, dims, pe_axis, inverse=False, dtype=HYSCO_F32, batch=1, stream=None):
+    d = (ctypes.c_int64 * 3)(*[int(x) for x in dims])
+    _io_check(lib().hysco_permute_pe(_ptr(d_in), _ptr(d_out), d, int(pe_axis), int(bool(inverse)), dtype,
+                                     int(batch), stream))
+
+
+def hysco_fieldmap_cells(ctx, b, out):
+    _check(ctx, lib().hysco_fieldmap_cells(ctx, _ptr(b), _ptr(out)))

@@ -1,5 +1,5 @@
 """C-ABI checks that need no GPU: the library builds, loads and exports every
-symbol include/hysco.h declares; host-side defaults and argument validation."""
+symbol include/hysco.h and include/hysco_io.h declare; host-side defaults and argument validation."""
 import ctypes
 import os
 import re
@@ -13,7 +13,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def _declared():
-    src = open(os.path.join(ROOT, "include", "hysco.h")).read()
+    src = "".join(open(os.path.join(ROOT, "include", f)).read() for f in ("hysco.h", "hysco_io.h"))
     return sorted(set(re.findall(r"HYSCO_API[^;(]*?\b(hysco_[a-z_]+)\s*\(", src)))
 
 

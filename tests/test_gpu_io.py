@@ -1,0 +1,126 @@
+"""GPU side of the front-end (NEXT-4, R30-R31): the PE-last permutation kernel
+(bit-exact against numpy transposes), the cell-centred field map (against the
+oracle's averaging operator A), and the command line run end to end
+(NIfTI in -> permute -> OT + GN + corrections -> permute back -> NIfTI out),
+which must reproduce the direct C-ABI run on numpy-permuted arrays bit for
+bit, with corrected images matching the oracle's Eq.(1) transform."""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import hysco_oracle as O          # noqa: E402
+from paper_2403_10706_b200 import hysco as H  # noqa: E402
+from synth import phantom                      # noqa: E402
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+TO_KERNEL = {1: (0, 1, 2), 2: (0, 2, 1), 3: (1, 2, 0)}   # file [nz][ny][nx] -> kernel layout (R30)
+
+
+def _dev(a):
+    t = torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+    torch.cuda.synchronize()
+    return t
+
+
+@pytest.mark.parametrize("dims", [(37, 5, 70), (33, 65, 17), (1, 40, 3)], ids=lambda d: "x".join(map(str, d)))
+@pytest.mark.parametrize("pe", [1, 2, 3])
+@pytest.mark.parametrize("dt", [np.float32, np.float64], ids=["f32", "f64"])
+def test_permute_pe_bitwise(dims, pe, dt):
+    nx, ny, nz = dims
+    rng = np.random.default_rng(pe)
+    a = rng.standard_normal((2, nz, ny, nx)).astype(dt)
+    dtype = H.HYSCO_F64 if dt == np.float64 else H.HYSCO_F32
+    src = _dev(a)
+    fwd = torch.empty_like(src)
+    H.hysco_permute_pe(src, fwd, dims, pe, False, dtype, batch=2)
+    torch.cuda.synchronize()
+    perm = TO_KERNEL[pe]
+    expect = np.stack([x.transpose(perm) for x in a])
+    n, _ = H.hysco_pe_shape(dims, (1, 1, 1), pe)
+    assert expect.shape[1:] == tuple(n)
+    assert np.array_equal(fwd.cpu().numpy().reshape(expect.shape), expect)
+    back = torch.empty_like(src)
+    H.hysco_permute_pe(fwd, back, dims, pe, True, dtype, batch=2)
+    torch.cuda.synchronize()
+    assert np.array_equal(back.cpu().numpy(), a)
+
+
+@pytest.mark.parametrize("dtype", [H.HYSCO_F32, H.HYSCO_F64], ids=["f32", "f64"])
+def test_fieldmap_cells(dtype):
+    shape = (5, 7, 37)
+    nd = np.float64 if dtype == H.HYSCO_F64 else np.float32
+    b = np.stack([phantom.random_feasible_b(shape, 1.25, seed=s, amp=0.7) for s in (1, 2)]).astype(nd)
+    c = H.hysco_create(shape, (1.1, 1.2, 1.25), 2, dtype=dtype)
+    out = torch.zeros((2,) + shape, dtype=torch.float64 if dtype == H.HYSCO_F64 else torch.float32, device=DEV)
+    torch.cuda.synchronize()
+    H.hysco_fieldmap_cells(c, _dev(b), out)
+    torch.cuda.synchronize()
+    ref = O.avg_pe(b.astype(np.float64))
+    tol = 1e-15 if dtype == H.HYSCO_F64 else 1e-7
+    assert np.max(np.abs(out.cpu().numpy() - ref)) <= tol * np.max(np.abs(ref))
+    H.hysco_destroy(c)
+
+
+def _info(dims, pix):
+    i = H.hysco_nifti_info()
+    for k in range(3):
+        i.dim[k] = dims[k]
+        i.pixdim[k] = pix[k]
+    i.qfac = 1.0
+    i.sform_code = 1
+    i.srow[:] = [pix[0], 0, 0, 0, 0, pix[1], 0, 0, 0, 0, pix[2], 0]
+    return i
+
+
+@pytest.mark.parametrize("pe", [2, 3])
+def test_cli_end_to_end_matches_direct_api(tmp_path, pe):
+    kshape = (10, 12, 24)                            # kernel layout (n1, n2, n3), PE last
+    hk = (1.5, 1.4, 1.25)
+    pair = phantom.make_pair(kshape, hk, seed=3)
+    inv = np.argsort(TO_KERNEL[pe])                  # kernel -> file
+    Ipf = np.ascontiguousarray(pair.Ip.transpose(inv))
+    Imf = np.ascontiguousarray(pair.Im.transpose(inv))
+    nz, ny, nx = Ipf.shape
+    # voxel sizes of the file axes so that hysco_pe_shape gives back hk
+    pix = [0.0, 0.0, 0.0]
+    file_axis_of = {1: (2, 1, 0), 2: (2, 0, 1), 3: (1, 0, 2)}[pe]   # NIfTI axis (0 = x) of n1, n2, n3
+    for k in range(3):
+        pix[file_axis_of[k]] = hk[k]
+    info = _info((nx, ny, nz), pix)
+    H.hysco_nifti_write(str(tmp_path / "p.nii.gz"), Ipf, info)
+    H.hysco_nifti_write(str(tmp_path / "m.nii.gz"), Imf, info)
+    out = str(tmp_path / "o")
+    r = subprocess.run([sys.executable, "-m", "paper_2403_10706_b200.cli", str(tmp_path / "p.nii.gz"),
+                        str(tmp_path / "m.nii.gz"), "--pe-axis", str(pe), "--out", out, "--stop", "fixed",
+                        "--correction", "both"], capture_output=True, text=True, cwd=ROOT, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["kernel_shape"] == list(kshape)
+    got = {k: H.hysco_nifti_read(f"{out}_{k}.nii.gz")[0] for k in ("fieldmap", "plus", "minus", "lsq")}
+
+    # direct C-ABI run on the kernel-layout arrays
+    c = H.hysco_create(kshape, hk, 1)
+    Ip, Im = _dev(pair.Ip[None]), _dev(pair.Im[None])
+    H.hysco_bind_images(c, Ip, Im)
+    b = torch.zeros((1,) + kshape[:2] + (kshape[2] + 1,), device=DEV)
+    Tp, Tm, Tl, fm = (torch.zeros_like(Ip) for _ in range(4))
+    torch.cuda.synchronize()
+    H.hysco_correct(c, b, Tp, Tm, H.default_ot_opts(), H.default_solve_opts())
+    H.hysco_lsq_correct(c, b, Tl, H.default_lsq_opts())
+    H.hysco_fieldmap_cells(c, b, fm)
+    torch.cuda.synchronize()
+    H.hysco_destroy(c)
+    for k, t in (("fieldmap", fm), ("plus", Tp), ("minus", Tm), ("lsq", Tl)):
+        assert np.array_equal(got[k], t.cpu().numpy()[0].transpose(inv)), k
+    bn = b.cpu().numpy()[0].astype(np.float64)
+    rp, rm = O.apply_correction(pair.Ip.astype(np.float64), pair.Im.astype(np.float64), bn, hk[2])
+    assert np.linalg.norm(got["plus"].transpose(TO_KERNEL[pe]) - rp) <= 1e-5 * np.linalg.norm(rp)
+    assert np.linalg.norm(got["minus"].transpose(TO_KERNEL[pe]) - rm) <= 1e-5 * np.linalg.norm(rm)
