@@ -48,7 +48,7 @@ HYSCO_API hysco_status hysco_nifti_read(const char* path, hysco_dtype dtype, voi
                                         hysco_nifti_info* info);
 
 /* Write a NIfTI-1 single file (gzip-compressed iff path ends in ".gz": level
- * 1, as independent 4 MiB gzip members compressed by parallel host threads and
+ * 1, as independent 1 MiB gzip members compressed by parallel host threads and
  * concatenated, which any gzip reader reads as one stream) with
  * the dims, voxel sizes and qform / sform of info, datatype float32 (16) or
  * float64 (64) per dtype, scl_slope 1, scl_inter 0, vox_offset 352, units mm.

@@ -22,6 +22,7 @@ import json
 import os
 import sys
 import time
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
@@ -67,8 +68,11 @@ def main(argv=None):
     nvox = dims[0] * dims[1] * dims[2]
     host = torch.empty((2, nvox), dtype=tdt, pin_memory=True)
     L = H.lib()
-    for k, path in enumerate((args.plus, args.minus)):
-        H._io_check(L.hysco_nifti_read(os.fsencode(path), dtype, ctypes.c_void_p(host[k].data_ptr()), nvox, None))
+    with ThreadPoolExecutor(2) as ex:            # the two files decompress concurrently (ctypes drops the GIL)
+        st = list(ex.map(lambda k: L.hysco_nifti_read(os.fsencode((args.plus, args.minus)[k]), dtype,
+                                                      ctypes.c_void_p(host[k].data_ptr()), nvox, None), (0, 1)))
+    for s in st:
+        H._io_check(s)
     t_read = time.perf_counter()
 
     torch.cuda.set_device(args.device)
@@ -111,12 +115,11 @@ def main(argv=None):
     names = ["fieldmap", "plus", "minus", "lsq"]
     keep = [0] + ([1, 2] if args.correction in ("jacobian", "both") else []) + \
         ([3] if args.correction in ("lsq", "both") else [])
-    files = []
     shape_file = (dims[2], dims[1], dims[0])
-    for k in keep:
-        path = f"{args.out}_{names[k]}{ext}"
-        H.hysco_nifti_write(path, res[k].numpy().reshape(shape_file), info_p)
-        files.append(path)
+    files = [f"{args.out}_{names[k]}{ext}" for k in keep]
+    with ThreadPoolExecutor(len(keep)) as ex:
+        list(ex.map(lambda kp: H.hysco_nifti_write(kp[1], res[kp[0]].numpy().reshape(shape_file), info_p),
+                    zip(keep, files)))
     t_write = time.perf_counter()
     print(json.dumps({"files": files, "kernel_shape": list(n), "pe_axis": args.pe_axis, "infeasible": bool(infeas),
                       "seconds": {"read": t_read - t0, "gpu": t_gpu - t_read, "write": t_write - t_gpu,

@@ -249,13 +249,13 @@ hysco_status hysco_nifti_write(const char* path, hysco_dtype dtype, const void* 
     const size_t nb = n * (f64 ? 8 : 4);
     const unsigned char* src = (const unsigned char*)host_data;
     if (gz) {
-        // Independent gzip members of <= 4 MiB compressed by parallel threads at
+        // Independent gzip members of <= 1 MiB compressed by parallel threads at
         // level 1 (nibabel's default), concatenated: RFC 1952 allows several
         // members and zlib's gzread (and gunzip) reads them as one stream.
         std::vector<unsigned char> all(sizeof h + nb);
         memcpy(all.data(), h, sizeof h);
         memcpy(all.data() + sizeof h, src, nb);
-        const size_t CH = (size_t)4 << 20, nch = (all.size() + CH - 1) / CH;
+        const size_t CH = (size_t)1 << 20, nch = (all.size() + CH - 1) / CH;
         std::vector<std::vector<unsigned char>> out(nch);
         std::vector<int> ok(nch, 0);
         const unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 16u));
