@@ -81,8 +81,12 @@ int main(int argc, char** argv) {
     cudaMemcpy(ht.data(), trace, ht.size() * 8, cudaMemcpyDeviceToHost);
     // stamp slots in time order within an iteration; the last phase ends at the next iteration's slot 0
     const int order[8] = {0, 1, 2, 7, 3, 4, 5, 6};
-    const char* names[8] = {"iter start", "local Hp + halo wait", "remote Hp", "publish #1 (p.Hp)",
-                            "collect #1", "U-phase + publish #2", "x upd + collect #2", "D-phase + release"};
+    // phase k runs from stamp order[k] to stamp order[k + 1] (slot 0 = loop top,
+    // 1 = after halo_acquire, 2 = after the remote loads, 7 = after publish #1,
+    // 3 = after collect #1, 4 = after publish #2, 5 = after collect #2, 6 = after the p update)
+    const char* names[8] = {"local Hp + halo acquire", "remote Hp + p.Hp", "publish #1 (p.Hp)", "collect #1",
+                            "U-phase + publish #2", "x upd + collect #2", "p update (D-phase)",
+                            "release + loop top"};
     // per phase: span = max_cta(end) - min_cta(start); per-CTA mean/max/min of (end - start)
     for (int k = 0; k < 8; k++) {
         double span = 0, mean_cta = 0, max_cta = 0, min_cta = 1e30;
