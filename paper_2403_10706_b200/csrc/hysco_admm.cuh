@@ -149,8 +149,10 @@ __global__ void __launch_bounds__(32 * ADMM_WARPS) admm_b_kernel(Geom g, Ctl c, 
                                                                 const T* __restrict__ Im, T* __restrict__ b,
                                                                 const T* __restrict__ z, const T* __restrict__ u,
                                                                 const double* __restrict__ rho_p, int inner,
-                                                                double c1, int ls_max, double col_tol) {
+                                                                double c1, int ls_max, double col_tol,
+                                                                const unsigned* __restrict__ done) {
     count_launch(c);
+    if (*done) return;                       // ADMM already stopped (iteration enqueued ahead of the host check)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int pair = blockIdx.y;
@@ -226,8 +228,9 @@ __global__ void __launch_bounds__(32 * ADMM_WARPS) admm_b_kernel(Geom g, Ctl c, 
 // w = b + u (the z-update right-hand side before the rho scaling).
 template <typename T>
 __global__ void __launch_bounds__(256) admm_rhs_kernel(Geom g, Ctl c, const T* __restrict__ b, const T* __restrict__ u,
-                                                       T* __restrict__ w) {
+                                                       T* __restrict__ w, const unsigned* __restrict__ done) {
     count_launch(c);
+    if (*done) return;
     const size_t po = (size_t)blockIdx.y * g.ps;
     for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < g.Nn; t += (long long)gridDim.x * blockDim.x)
         w[po + t] = b[po + t] + u[po + t];
@@ -240,8 +243,10 @@ __global__ void __launch_bounds__(256) admm_rhs_kernel(Geom g, Ctl c, const T* _
 template <typename C>
 __global__ void __launch_bounds__(256) admm_zscale_kernel(Geom g, Ctl c, C* __restrict__ X,
                                                           const double* __restrict__ rho_p,
-                                                          const double* __restrict__ lam, long long spec) {
+                                                          const double* __restrict__ lam, long long spec,
+                                                          const unsigned* __restrict__ done) {
     count_launch(c);
+    if (*done) return;
     const int pair = blockIdx.y, lane = threadIdx.x & 31;
     const double rho = rho_p[pair];
     const int P = g.P;
@@ -275,8 +280,10 @@ __global__ void admm_lambda_kernel(Geom g, double* __restrict__ lam) {
 template <typename T>
 __global__ void __launch_bounds__(256) admm_u_kernel(Geom g, Ctl c, const T* __restrict__ b,
                                                      const T* __restrict__ bprev, const T* __restrict__ znew,
-                                                     T* __restrict__ z, T* __restrict__ u) {
+                                                     T* __restrict__ z, T* __restrict__ u,
+                                                     const unsigned* __restrict__ done) {
     count_launch(c);
+    if (*done) return;
     const int pair = blockIdx.y;
     const size_t po = (size_t)pair * g.ps;
     double r2 = 0, s2 = 0, db2 = 0, bb = 0;
@@ -295,6 +302,46 @@ __global__ void __launch_bounds__(256) admm_u_kernel(Geom g, Ctl c, const T* __r
     if (!pair_reduce<4, 0u>(c, v, tot)) return;
     if (threadIdx.x != 0) return;
     for (int k = 0; k < 4; k++) c.red[(size_t)pair * RED_W + k] = tot[k];
+}
+
+// Residual balancing and the stop test on the device, after admm_u_kernel's
+// pair totals r^2, |dz|^2, |db|^2, |b|^2 (oracle admm_rho_update and admm();
+// R25, R26; |du| = |b - z| = r).  stat[pair][4] = iterations, r_norm, s_norm,
+// converged.  Sets *done when every pair converged (not in fixed mode); once
+// done, only resets fac so that the following admm_scale_u_kernel is a no-op.
+__global__ void admm_balance_kernel(Ctl c, int B, double* __restrict__ rho, double* __restrict__ fac,
+                                    double* __restrict__ stat, unsigned* __restrict__ done, int it, double mu,
+                                    double tau, double tol, int fixed) {
+    count_launch(c);
+    const bool stopped = *done != 0;
+    bool all_conv = true;
+    for (int p = threadIdx.x; p < B; p += blockDim.x) {
+        if (stopped) {
+            fac[p] = 1.0;
+            continue;
+        }
+        const double* t = c.red + (size_t)p * RED_W;
+        const double r_norm = sqrt(t[0]), dz = sqrt(t[1]), db = sqrt(t[2]), bn = sqrt(t[3]);
+        const double s_norm = rho[p] * dz;
+        double f = 1.0;
+        if (r_norm > mu * s_norm) {
+            rho[p] *= tau;
+            f = 1.0 / tau;
+        } else if (s_norm > mu * r_norm) {
+            rho[p] /= tau;
+            f = tau;
+        }
+        fac[p] = f;
+        const bool conv = fmax(db, fmax(dz, r_norm)) <= tol * fmax(bn, 1e-300);
+        double* st = stat + (size_t)p * 4;
+        st[0] = it + 1;
+        st[1] = r_norm;
+        st[2] = s_norm;
+        st[3] = conv ? 1.0 : 0.0;
+        all_conv = all_conv && conv;
+    }
+    all_conv = __syncthreads_and(all_conv);
+    if (threadIdx.x == 0 && !stopped && all_conv && !fixed) *done = 1u;
 }
 
 // u *= f[pair] (residual balancing rescales the scaled multiplier).

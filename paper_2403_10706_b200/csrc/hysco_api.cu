@@ -63,6 +63,10 @@ struct hysco_ctx_s {
     double* admm_rho = nullptr;     // [batch] device
     double* admm_fac = nullptr;     // [batch] device (u rescaling)
     double* admm_lam = nullptr;     // [n1][n2/2+1] periodic L_xy eigenvalues
+    double* admm_stat = nullptr;    // [batch][4] iterations, r_norm, s_norm, converged (device)
+    unsigned* admm_done = nullptr;  // device stop flag of the running ADMM solve
+    unsigned* h_admm_done = nullptr;                // [2] pinned copies of the flag
+    cudaEvent_t admm_ev[2] = {nullptr, nullptr};    // recorded after each copy
     size_t admm_smem = 0;
     int admm_gx = 1;
     bool admm_ready = false;
@@ -1004,6 +1008,10 @@ static hysco_status admm_setup(hysco_ctx ctx) {
     CK(cudaMalloc(&ctx->admm_rho, sizeof(double) * ctx->cfg.batch));
     CK(cudaMalloc(&ctx->admm_fac, sizeof(double) * ctx->cfg.batch));
     CK(cudaMalloc(&ctx->admm_lam, sizeof(double) * g.n1 * (g.n2 / 2 + 1)));
+    CK(cudaMalloc(&ctx->admm_stat, sizeof(double) * 4 * ctx->cfg.batch));
+    CK(cudaMalloc(&ctx->admm_done, sizeof(unsigned)));
+    CK(cudaMallocHost(&ctx->h_admm_done, 2 * sizeof(unsigned)));
+    for (int k = 0; k < 2; k++) CK(cudaEventCreateWithFlags(&ctx->admm_ev[k], cudaEventDisableTiming));
     admm_lambda_kernel<<<64, 256, 0, ctx->stream>>>(g, ctx->admm_lam);
     CK(cudaGetLastError());
     ctx->admm_smem = (size_t)ADMM_WARPS * admm_warp_elems(g.n3) * sizeof(T);
@@ -1037,21 +1045,32 @@ static hysco_status admm_run(hysco_ctx ctx, void* d_b, const hysco_admm_opts& o,
     T* zn = L<T>::b(ctx, B_TMP);
     C* X = static_cast<C*>(ctx->admm_spec);
     const double rho0 = o.rho0 > 0 ? o.rho0 : g.alpha * (g.ih1sq + g.ih2sq);
-    std::vector<double> rho(B, rho0), fac(B, 1.0), red((size_t)B * RED_W);
-    std::vector<int> iters(B, 0), conv(B, 0);
-    std::vector<double> rn(B, 0.0), sn(B, 0.0);
+    std::vector<double> rho(B, rho0), stat((size_t)4 * B, 0.0);
     CK(cudaMemsetAsync(ctx->launches, 0, sizeof(unsigned long long), st));
+    CK(cudaMemcpyAsync(ctx->admm_rho, rho.data(), sizeof(double) * B, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(ctx->admm_done, 0, sizeof(unsigned), st));
+    CK(cudaMemsetAsync(ctx->admm_stat, 0, sizeof(double) * 4 * B, st));
     CK(cudaMemcpyAsync(b, d_b, nb, cudaMemcpyDeviceToDevice, st));
     CK(cudaMemcpyAsync(z, d_b, nb, cudaMemcpyDeviceToDevice, st));     // z0 = b0
     CK(cudaMemsetAsync(u, 0, nb, st));                                  // u0 = 0
     const dim3 gb(ctx->admm_gx, B), gn(ctx->gx_cells, B);
+    const unsigned* done = ctx->admm_done;
+    // The loop runs without a host round trip per iteration: residual balancing
+    // and the stop test are admm_balance_kernel's; the host enqueues iteration
+    // k after seeing the stop flag of iteration k - 2 (pinned copy + event), so
+    // the GPU stays one iteration ahead.  Kernels of an iteration enqueued after
+    // the stop are no-ops (only its two cuFFT calls still run, on scratch).
     for (int k = 0; k < o.max_iter; k++) {
-        CK(cudaMemcpyAsync(ctx->admm_rho, rho.data(), sizeof(double) * B, cudaMemcpyHostToDevice, st));
+        if (!o.fixed_iters && k >= 2) {
+            CK(cudaEventSynchronize(ctx->admm_ev[k & 1]));
+            if (ctx->h_admm_done[k & 1]) break;
+        }
         CK(cudaMemcpyAsync(bprev, b, nb, cudaMemcpyDeviceToDevice, st));
         admm_b_kernel<T><<<gb, 32 * ADMM_WARPS, ctx->admm_smem, st>>>(g, ctx->ctl, (const T*)ctx->Ip,
                                                                        (const T*)ctx->Im, b, z, u, ctx->admm_rho,
-                                                                       o.inner, o.armijo_c1, o.ls_max, o.col_tol);
-        admm_rhs_kernel<T><<<gn, 256, 0, st>>>(g, ctx->ctl, b, u, w);
+                                                                       o.inner, o.armijo_c1, o.ls_max, o.col_tol,
+                                                                       done);
+        admm_rhs_kernel<T><<<gn, 256, 0, st>>>(g, ctx->ctl, b, u, w, done);
         for (int p = 0; p < B; p++) {
             cufftResult r = sizeof(T) == 8
                                 ? cufftExecD2Z(ctx->fft_fwd, (cufftDoubleReal*)(w + (size_t)p * g.ps),
@@ -1060,7 +1079,7 @@ static hysco_status admm_run(hysco_ctx ctx, void* d_b, const hysco_admm_opts& o,
                                                (cufftComplex*)(X + (size_t)p * spec));
             if (r != CUFFT_SUCCESS) return set_err(ctx, HYSCO_ERR_CUDA, "cuFFT forward transform failed");
         }
-        admm_zscale_kernel<C><<<gn, 256, 0, st>>>(g, ctx->ctl, X, ctx->admm_rho, ctx->admm_lam, spec);
+        admm_zscale_kernel<C><<<gn, 256, 0, st>>>(g, ctx->ctl, X, ctx->admm_rho, ctx->admm_lam, spec, done);
         for (int p = 0; p < B; p++) {
             cufftResult r = sizeof(T) == 8
                                 ? cufftExecZ2D(ctx->fft_inv, (cufftDoubleComplex*)(X + (size_t)p * spec),
@@ -1069,37 +1088,19 @@ static hysco_status admm_run(hysco_ctx ctx, void* d_b, const hysco_admm_opts& o,
                                                (cufftReal*)(zn + (size_t)p * g.ps));
             if (r != CUFFT_SUCCESS) return set_err(ctx, HYSCO_ERR_CUDA, "cuFFT inverse transform failed");
         }
-        admm_u_kernel<T><<<gn, 256, 0, st>>>(g, ctx->ctl, b, bprev, zn, z, u);
+        admm_u_kernel<T><<<gn, 256, 0, st>>>(g, ctx->ctl, b, bprev, zn, z, u, done);
+        admm_balance_kernel<<<1, 256, 0, st>>>(ctx->ctl, B, ctx->admm_rho, ctx->admm_fac, ctx->admm_stat,
+                                               ctx->admm_done, k, o.mu, o.tau, o.tol, o.fixed_iters);
+        admm_scale_u_kernel<T><<<gn, 256, 0, st>>>(g, ctx->ctl, u, ctx->admm_fac);
         CK(cudaGetLastError());
-        CK(cudaMemcpyAsync(red.data(), ctx->red, sizeof(double) * B * RED_W, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        bool all_conv = true, any_fac = false;
-        for (int p = 0; p < B; p++) {
-            const double* t = &red[(size_t)p * RED_W];
-            const double r_norm = sqrt(t[0]), dz = sqrt(t[1]), db = sqrt(t[2]), bn = sqrt(t[3]);
-            const double s_norm = rho[p] * dz;
-            iters[p] = k + 1;
-            rn[p] = r_norm;
-            sn[p] = s_norm;
-            // residual balancing (oracle admm_rho_update)
-            fac[p] = 1.0;
-            if (r_norm > o.mu * s_norm) {
-                rho[p] *= o.tau;
-                fac[p] = 1.0 / o.tau;
-            } else if (s_norm > o.mu * r_norm) {
-                rho[p] /= o.tau;
-                fac[p] = o.tau;
-            }
-            any_fac = any_fac || fac[p] != 1.0;
-            conv[p] = std::max(db, std::max(dz, r_norm)) <= o.tol * std::max(bn, 1e-300);   // |du| = |b - z|
-            all_conv = all_conv && conv[p];
+        if (!o.fixed_iters) {
+            CK(cudaMemcpyAsync(&ctx->h_admm_done[k & 1], ctx->admm_done, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                               st));
+            CK(cudaEventRecord(ctx->admm_ev[k & 1], st));
         }
-        if (any_fac) {
-            CK(cudaMemcpyAsync(ctx->admm_fac, fac.data(), sizeof(double) * B, cudaMemcpyHostToDevice, st));
-            admm_scale_u_kernel<T><<<gn, 256, 0, st>>>(g, ctx->ctl, u, ctx->admm_fac);
-        }
-        if (!o.fixed_iters && all_conv) break;
     }
+    CK(cudaMemcpyAsync(stat.data(), ctx->admm_stat, sizeof(double) * 4 * B, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(rho.data(), ctx->admm_rho, sizeof(double) * B, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(d_b, b, nb, cudaMemcpyDeviceToDevice, st));
     SolveParams sp{};
     L<T>::eval(ctx, sp, EVAL_PLAIN, b);
@@ -1111,11 +1112,11 @@ static hysco_status admm_run(hysco_ctx ctx, void* d_b, const hysco_admm_opts& o,
     for (int p = 0; p < B; p++) {
         if (!reps) break;
         const PairState& s = ctx->h_st[p];
-        reps[p].iters = iters[p];
-        reps[p].converged = conv[p];
+        reps[p].iters = (int32_t)stat[4 * p + 0];
+        reps[p].converged = stat[4 * p + 3] != 0.0;
         reps[p].rho = rho[p];
-        reps[p].r_norm = rn[p];
-        reps[p].s_norm = sn[p];
+        reps[p].r_norm = stat[4 * p + 1];
+        reps[p].s_norm = stat[4 * p + 2];
         reps[p].J = s.J;
         reps[p].D = s.D;
         reps[p].S = s.S;
@@ -1973,7 +1974,11 @@ hysco_status hysco_destroy(hysco_ctx ctx) {
         cufftDestroy(ctx->fft_fwd);
         cufftDestroy(ctx->fft_inv);
     }
-    for (void* q : {ctx->admm_spec, (void*)ctx->admm_rho, (void*)ctx->admm_fac, (void*)ctx->admm_lam})
+    for (int k = 0; k < 2; k++)
+        if (ctx->admm_ev[k]) cudaEventDestroy(ctx->admm_ev[k]);
+    if (ctx->h_admm_done) cudaFreeHost(ctx->h_admm_done);
+    for (void* q : {ctx->admm_spec, (void*)ctx->admm_rho, (void*)ctx->admm_fac, (void*)ctx->admm_lam,
+                    (void*)ctx->admm_stat, (void*)ctx->admm_done})
         if (q) cudaFree(q);
     if (ctx->stream_ready) {
         for (int k = 0; k < 2; k++) {
