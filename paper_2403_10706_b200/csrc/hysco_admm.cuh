@@ -60,6 +60,118 @@ __device__ __forceinline__ void pcr_solve(int lane, int P, const T* sd, const T*
     __syncwarp();
 }
 
+// Register-resident PCR for P <= 32 E: lane owns equations i = lane + 32 m,
+// m < E.  At step st the partner equations i -+ st are fetched by shuffle
+// (st < 32: same m from lane -+ st, or m -+ 1 across the lane wrap) or by
+// register index (st = 32 q: same lane, m -+ q); each owner supplies 1 / b_i,
+// so a step costs one reciprocal and eight shuffles per equation and no
+// shared memory.  Same elimination as pcr_solve (k1 = a_i / b_{i-s},
+// k2 = c_i / b_{i+s}); the divisions become multiplications by the
+// partners' reciprocals (<= 1 ulp per step).
+template <typename T, int E, int ST, int DIR>
+__device__ __forceinline__ void pcr_fetch(const T (&x)[E], T (&out)[E], int lane) {
+    if constexpr (ST < 32) {
+        T y[E];
+        const int src = (lane + DIR * ST) & 31;
+#pragma unroll
+        for (int m = 0; m < E; m++) y[m] = __shfl_sync(FULL, x[m], src);
+        const bool wrap = DIR < 0 ? lane < ST : lane + ST >= 32;
+#pragma unroll
+        for (int m = 0; m < E; m++) {
+            T alt = T(0);
+            if constexpr (DIR < 0) {
+                if (m >= 1) alt = y[m >= 1 ? m - 1 : 0];
+            } else {
+                if (m + 1 < E) alt = y[m + 1 < E ? m + 1 : 0];
+            }
+            out[m] = wrap ? alt : y[m];
+        }
+    } else {
+        constexpr int q = ST / 32;
+#pragma unroll
+        for (int m = 0; m < E; m++) {
+            const int j = m + DIR * q;
+            out[m] = (j >= 0 && j < E) ? x[(j >= 0 && j < E) ? j : 0] : T(0);
+        }
+    }
+}
+
+template <typename T, int E, int ST>
+__device__ __forceinline__ void pcr_step(int lane, int P, T (&A)[E], T (&B)[E], T (&C)[E], T (&R)[E]) {
+    if (ST >= P) return;
+    T rB[E], a1[E], b1[E], c1[E], r1[E], X[E], Y[E], Z[E], W[E];
+#pragma unroll
+    for (int m = 0; m < E; m++) rB[m] = T(1) / B[m];
+    // partner i - st: a1 = -a_{i-s} k1, b -= c_{i-s} k1, r -= r_{i-s} k1
+    pcr_fetch<T, E, ST, -1>(rB, W, lane);
+    pcr_fetch<T, E, ST, -1>(A, X, lane);
+    pcr_fetch<T, E, ST, -1>(C, Y, lane);
+    pcr_fetch<T, E, ST, -1>(R, Z, lane);
+#pragma unroll
+    for (int m = 0; m < E; m++) {
+        const bool hm = lane + 32 * m - ST >= 0;
+        const T k1 = hm ? A[m] * W[m] : T(0);
+        a1[m] = hm ? -X[m] * k1 : T(0);
+        b1[m] = B[m] - (hm ? Y[m] * k1 : T(0));
+        r1[m] = R[m] - (hm ? Z[m] * k1 : T(0));
+    }
+    // partner i + st: c1 = -c_{i+s} k2, b -= a_{i+s} k2, r -= r_{i+s} k2
+    pcr_fetch<T, E, ST, +1>(rB, W, lane);
+    pcr_fetch<T, E, ST, +1>(A, X, lane);
+    pcr_fetch<T, E, ST, +1>(C, Y, lane);
+    pcr_fetch<T, E, ST, +1>(R, Z, lane);
+#pragma unroll
+    for (int m = 0; m < E; m++) {
+        const int i = lane + 32 * m;
+        const bool hp = i + ST < P, v = i < P;
+        const T k2 = hp ? C[m] * W[m] : T(0);
+        c1[m] = hp ? -Y[m] * k2 : T(0);
+        b1[m] -= hp ? X[m] * k2 : T(0);
+        r1[m] -= hp ? Z[m] * k2 : T(0);
+        A[m] = v ? a1[m] : T(0);
+        B[m] = v ? b1[m] : T(1);
+        C[m] = v ? c1[m] : T(0);
+        R[m] = v ? r1[m] : T(0);
+    }
+}
+
+template <typename T, int E>
+__device__ void pcr_solve_reg(int lane, int P, const T* sd, const T* se, const T* rhs, T* q) {
+    T A[E], B[E], C[E], R[E];
+#pragma unroll
+    for (int m = 0; m < E; m++) {
+        const int i = lane + 32 * m;
+        const bool v = i < P;
+        A[m] = v && i > 0 ? se[i - 1] : T(0);
+        B[m] = v ? sd[i] : T(1);
+        C[m] = v && i + 1 < P ? se[i] : T(0);
+        R[m] = v ? rhs[i] : T(0);
+    }
+    pcr_step<T, E, 1>(lane, P, A, B, C, R);
+    pcr_step<T, E, 2>(lane, P, A, B, C, R);
+    pcr_step<T, E, 4>(lane, P, A, B, C, R);
+    pcr_step<T, E, 8>(lane, P, A, B, C, R);
+    pcr_step<T, E, 16>(lane, P, A, B, C, R);
+    if constexpr (E > 1) pcr_step<T, E, 32>(lane, P, A, B, C, R);
+    if constexpr (E > 2) pcr_step<T, E, 64>(lane, P, A, B, C, R);
+    if constexpr (E > 4) pcr_step<T, E, 128>(lane, P, A, B, C, R);
+#pragma unroll
+    for (int m = 0; m < E; m++) {
+        const int i = lane + 32 * m;
+        if (i < P) q[i] = R[m] / B[m];
+    }
+    __syncwarp();
+}
+
+// Column solve: registers when the kernel is instantiated for E = ceil(P / 32)
+// (E = 0: shared-memory PCR, any P).
+template <typename T, int E>
+__device__ __forceinline__ void col_tridiag_solve(int lane, int P, const T* sd, const T* se, const T* rhs, T* q,
+                                                  T* A0, T* B0, T* C0, T* R0, T* A1, T* B1, T* C1, T* R1) {
+    if constexpr (E > 0) pcr_solve_reg<T, E>(lane, P, sd, se, rhs, q);
+    else pcr_solve<T>(lane, P, sd, se, rhs, q, A0, B0, C0, R0, A1, B1, C1, R1);
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_sum_t(T x) {
 #pragma unroll
@@ -144,7 +256,7 @@ __device__ double admm_col_eval(const Geom& g, int lane, const T* sIp, const T* 
 // b-update (oracle admm_b_update): per column `inner` GN steps, exact solve
 // of tridiag(d, e) q = -grad (warp PCR), the per-column stop (R23), Armijo on
 // the column objective with gamma = 1, 1/2, ... (ls_max tries).
-template <typename T>
+template <typename T, int E>
 __global__ void __launch_bounds__(32 * ADMM_WARPS) admm_b_kernel(Geom g, Ctl c, const T* __restrict__ Ip,
                                                                 const T* __restrict__ Im, T* __restrict__ b,
                                                                 const T* __restrict__ z, const T* __restrict__ u,
@@ -199,7 +311,11 @@ __global__ void __launch_bounds__(32 * ADMM_WARPS) admm_b_kernel(Geom g, Ctl c, 
             __syncwarp();
             // PCR double buffers: the dead cell arrays, then d, e, rhs themselves
             // (read only by pcr_solve's set-up pass)
-            pcr_solve<T>(lane, P, sd, se, sbt, sq, sa, sc, sr, sp1, sp2, sd, se, sbt);
+#ifdef ADMM_ABLATE_PCR   // diagnostic builds only: timing without the tridiagonal solve (results invalid)
+            for (int l = lane; l < P; l += 32) sq[l] = sbt[l] / sd[l];
+#else
+            col_tridiag_solve<T, E>(lane, P, sd, se, sbt, sq, sa, sc, sr, sp1, sp2, sd, se, sbt);
+#endif
             __syncwarp();
             double gq = 0;
             for (int l = lane; l < P; l += 32) gq += (double)sg[l] * (double)sq[l];

@@ -69,6 +69,7 @@ struct hysco_ctx_s {
     cudaEvent_t admm_ev[2] = {nullptr, nullptr};    // recorded after each copy
     size_t admm_smem = 0;
     int admm_gx = 1;
+    int admm_e = 0;                 // admm_b_kernel register-PCR width ceil(P / 32), 0 = shared-memory PCR
     bool admm_ready = false;
     void* own_Tm = nullptr;
     PairState* st = nullptr;
@@ -992,6 +993,20 @@ static hysco_status setup_typed(hysco_ctx ctx) {
     return HYSCO_OK;
 }
 
+// admm_b_kernel is instantiated per E = ceil(P / 32) <= 8 (register PCR), 0 beyond
+#define ADMM_E_SWITCH(e, ...)                                                 \
+    switch (e) {                                                              \
+        case 1: { constexpr int AE = 1; __VA_ARGS__; } break;                 \
+        case 2: { constexpr int AE = 2; __VA_ARGS__; } break;                 \
+        case 3: { constexpr int AE = 3; __VA_ARGS__; } break;                 \
+        case 4: { constexpr int AE = 4; __VA_ARGS__; } break;                 \
+        case 5: { constexpr int AE = 5; __VA_ARGS__; } break;                 \
+        case 6: { constexpr int AE = 6; __VA_ARGS__; } break;                 \
+        case 7: { constexpr int AE = 7; __VA_ARGS__; } break;                 \
+        case 8: { constexpr int AE = 8; __VA_ARGS__; } break;                 \
+        default: { constexpr int AE = 0; __VA_ARGS__; } break;                \
+    }
+
 template <typename T>
 static hysco_status admm_setup(hysco_ctx ctx) {
     if (ctx->admm_ready) return HYSCO_OK;
@@ -1016,11 +1031,17 @@ static hysco_status admm_setup(hysco_ctx ctx) {
     CK(cudaGetLastError());
     ctx->admm_smem = (size_t)ADMM_WARPS * admm_warp_elems(g.n3) * sizeof(T);
     if (ctx->admm_smem > 227 * 1024) return set_err(ctx, HYSCO_ERR_SHAPE, "n3 too large for the ADMM column kernel");
-    CK(cudaFuncSetAttribute(admm_b_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->admm_smem));
+    ctx->admm_e = (g.P + 31) / 32 <= 8 ? (g.P + 31) / 32 : 0;
     int occ = 1;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, admm_b_kernel<T>, 32 * ADMM_WARPS, ctx->admm_smem) !=
-            cudaSuccess || occ < 1)
-        occ = 1;
+    cudaError_t ea = cudaSuccess;
+    ADMM_E_SWITCH(ctx->admm_e,
+                  ea = cudaFuncSetAttribute(admm_b_kernel<T, AE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)ctx->admm_smem);
+                  if (ea == cudaSuccess &&
+                      (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, admm_b_kernel<T, AE>, 32 * ADMM_WARPS,
+                                                                     ctx->admm_smem) != cudaSuccess || occ < 1))
+                      occ = 1)
+    CK(ea);
     const long long work = (g.ncol + ADMM_WARPS - 1) / ADMM_WARPS;
     const long long cap = ((long long)ctx->nsm * occ + ctx->cfg.batch - 1) / ctx->cfg.batch;
     ctx->admm_gx = (int)std::max(1LL, std::min(work, cap));
@@ -1066,10 +1087,10 @@ static hysco_status admm_run(hysco_ctx ctx, void* d_b, const hysco_admm_opts& o,
             if (ctx->h_admm_done[k & 1]) break;
         }
         CK(cudaMemcpyAsync(bprev, b, nb, cudaMemcpyDeviceToDevice, st));
-        admm_b_kernel<T><<<gb, 32 * ADMM_WARPS, ctx->admm_smem, st>>>(g, ctx->ctl, (const T*)ctx->Ip,
-                                                                       (const T*)ctx->Im, b, z, u, ctx->admm_rho,
-                                                                       o.inner, o.armijo_c1, o.ls_max, o.col_tol,
-                                                                       done);
+        ADMM_E_SWITCH(ctx->admm_e,
+                      admm_b_kernel<T, AE><<<gb, 32 * ADMM_WARPS, ctx->admm_smem, st>>>(
+                          g, ctx->ctl, (const T*)ctx->Ip, (const T*)ctx->Im, b, z, u, ctx->admm_rho, o.inner,
+                          o.armijo_c1, o.ls_max, o.col_tol, done))
         admm_rhs_kernel<T><<<gn, 256, 0, st>>>(g, ctx->ctl, b, u, w, done);
         for (int p = 0; p < B; p++) {
             cufftResult r = sizeof(T) == 8

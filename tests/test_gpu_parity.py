@@ -576,8 +576,9 @@ def test_correct_host_stream_equals_per_item_correct():
 # ---------------------------------------------------------------- ADMM (R21-R26)
 
 @pytest.mark.parametrize("dtype", [H.HYSCO_F64, H.HYSCO_F32], ids=["f64", "f32"])
-@pytest.mark.parametrize("shape,seed", [((12, 10, 24), 3), ((5, 7, 37), 5), ((2, 3, 300), 13)],
-                         ids=["small", "ragged", "long"])
+@pytest.mark.parametrize("shape,seed", [((12, 10, 24), 3), ((5, 7, 37), 5), ((3, 4, 100), 9), ((4, 5, 144), 7),
+                                        ((2, 3, 300), 13)],
+                         ids=["small", "ragged", "e4", "hcp_col", "long"])
 def test_admm_fixed_parity(dtype, shape, seed):
     """Fixed ADMM iterations from the same OT start: b-update (per-column GN,
     exact Thomas, per-column Armijo), cuFFT z-update, u-update and residual
