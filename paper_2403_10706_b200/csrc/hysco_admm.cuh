@@ -14,6 +14,9 @@
 namespace hysco {
 
 constexpr int ADMM_WARPS = 4;   // columns per CTA (one warp each)
+#ifndef ADMM_MINB
+#define ADMM_MINB 5   // fp32 admm_b_kernel: >= 5 CTAs per SM (<= 102 registers; measured 73.7 vs 68 pairs/s at 1)
+#endif
 
 // Per-warp shared scratch (elements): I+, I- padded by two zeros per side,
 // b, v = z - u, q, grad, diag, offdiag, trial b (nodes), and the cell
@@ -257,7 +260,7 @@ __device__ double admm_col_eval(const Geom& g, int lane, const T* sIp, const T* 
 // of tridiag(d, e) q = -grad (warp PCR), the per-column stop (R23), Armijo on
 // the column objective with gamma = 1, 1/2, ... (ls_max tries).
 template <typename T, int E>
-__global__ void __launch_bounds__(32 * ADMM_WARPS) admm_b_kernel(Geom g, Ctl c, const T* __restrict__ Ip,
+__global__ void __launch_bounds__(32 * ADMM_WARPS, sizeof(T) == 4 ? ADMM_MINB : 1) admm_b_kernel(Geom g, Ctl c, const T* __restrict__ Ip,
                                                                 const T* __restrict__ Im, T* __restrict__ b,
                                                                 const T* __restrict__ z, const T* __restrict__ u,
                                                                 const double* __restrict__ rho_p, int inner,
