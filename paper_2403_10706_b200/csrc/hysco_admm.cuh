@@ -406,16 +406,34 @@ __global__ void __launch_bounds__(256) admm_u_kernel(Geom g, Ctl c, const T* __r
     const int pair = blockIdx.y;
     const size_t po = (size_t)pair * g.ps;
     double r2 = 0, s2 = 0, db2 = 0, bb = 0;
-    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < g.Nn; t += (long long)gridDim.x * blockDim.x) {
-        const size_t o = po + t;
-        const T bv = b[o], zn = znew[o], zo = z[o];
-        const T du = bv - zn;
-        u[o] += du;
-        z[o] = zn;
-        r2 += (double)du * (double)du;
-        s2 += ((double)zn - (double)zo) * ((double)zn - (double)zo);
-        db2 += ((double)bv - (double)bprev[o]) * ((double)bv - (double)bprev[o]);
-        bb += (double)bv * (double)bv;
+    // unrolled by 4 (independent loads in flight; the kernel is load-latency
+    // bound: ncu long-scoreboard 77 % with one element per loop trip)
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; t0 < g.Nn; t0 += 4 * stride) {
+        T bv[4], zn[4], zo[4], uo[4], bp[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const long long t = t0 + j * stride;
+            const size_t o = po + (t < g.Nn ? t : 0);
+            bv[j] = b[o];
+            zn[j] = znew[o];
+            zo[j] = z[o];
+            uo[j] = u[o];
+            bp[j] = bprev[o];
+        }
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const long long t = t0 + j * stride;
+            if (t >= g.Nn) break;
+            const size_t o = po + t;
+            const T du = bv[j] - zn[j];
+            u[o] = uo[j] + du;
+            z[o] = zn[j];
+            r2 += (double)du * (double)du;
+            s2 += ((double)zn[j] - (double)zo[j]) * ((double)zn[j] - (double)zo[j]);
+            db2 += ((double)bv[j] - (double)bp[j]) * ((double)bv[j] - (double)bp[j]);
+            bb += (double)bv[j] * (double)bv[j];
+        }
     }
     double v[4] = {r2, s2, db2, bb}, tot[4];
     if (!pair_reduce<4, 0u>(c, v, tot)) return;
