@@ -46,7 +46,8 @@ def parse():
     ap.add_argument("--batch", type=int, default=1, help="pairs per GPU per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-reps", type=int, default=20)
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=None,
+                    help="items timed through the host entry (default: --steps, one item per step)")
     ap.add_argument("--precond", default="jacobi", choices=["jacobi", "block"],
                     help="PCG preconditioner: Jacobi (P:198, the headline) or per-PE-column blocks (P:200)")
     ap.add_argument("--stop", default="fixed", choices=["fixed", "paper"],
@@ -348,7 +349,7 @@ def run_hysco(args):
     # items; every item's pair is copied in from pinned host memory and its b
     # and corrected pair copied back inside the timed region (the copies of
     # items k+1 / k-1 overlap the correction of item k on a second stream).
-    ne = max(2, args.e2e_steps)
+    ne = max(2, args.e2e_steps if args.e2e_steps is not None else args.steps)
     H.hysco_correct_host_stream(ctx, [hIp] * 2, [hIm] * 2, [hb] * 2, [hTp] * 2, [hTm] * 2, solve_opts=so, batch=B)
     flush.zero_()
     torch.cuda.synchronize(dev)
