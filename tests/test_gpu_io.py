@@ -124,3 +124,45 @@ def test_cli_end_to_end_matches_direct_api(tmp_path, pe):
     rp, rm = O.apply_correction(pair.Ip.astype(np.float64), pair.Im.astype(np.float64), bn, hk[2])
     assert np.linalg.norm(got["plus"].transpose(TO_KERNEL[pe]) - rp) <= 1e-5 * np.linalg.norm(rp)
     assert np.linalg.norm(got["minus"].transpose(TO_KERNEL[pe]) - rm) <= 1e-5 * np.linalg.norm(rm)
+
+
+@pytest.mark.parametrize("opts", [["--solver", "admm", "--correction", "lsq", "--pe-axis", "3"],
+                                  ["--precond", "block", "--dtype", "f64", "--pe-axis", "1", "--no-gzip"]],
+                         ids=["admm_lsq_pe3", "block_f64_pe1_plain"])
+def test_cli_option_paths(tmp_path, opts):
+    """Other CLI paths: outputs exist with the file's shape and voxel sizes and
+    are finite; the Jacobian-corrected pair (when written) agrees better than
+    the input pair; every least-squares column converged."""
+    kshape = (8, 10, 20)
+    hk = (1.5, 1.4, 1.25)
+    pair = phantom.make_pair(kshape, hk, seed=4)
+    pe = int(opts[opts.index("--pe-axis") + 1])
+    inv = np.argsort(TO_KERNEL[pe])
+    Ipf = np.ascontiguousarray(pair.Ip.transpose(inv))
+    Imf = np.ascontiguousarray(pair.Im.transpose(inv))
+    nz, ny, nx = Ipf.shape
+    pix = [0.0, 0.0, 0.0]
+    for k in range(3):
+        pix[{1: (2, 1, 0), 2: (2, 0, 1), 3: (1, 0, 2)}[pe][k]] = hk[k]
+    info = _info((nx, ny, nz), pix)
+    H.hysco_nifti_write(str(tmp_path / "p.nii.gz"), Ipf, info)
+    H.hysco_nifti_write(str(tmp_path / "m.nii.gz"), Imf, info)
+    out = str(tmp_path / "o")
+    r = subprocess.run([sys.executable, "-m", "paper_2403_10706_b200.cli", str(tmp_path / "p.nii.gz"),
+                        str(tmp_path / "m.nii.gz"), "--out", out] + opts,
+                       capture_output=True, text=True, cwd=ROOT, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["kernel_shape"] == list(kshape) and not line["infeasible"]
+    ext = ".nii" if "--no-gzip" in opts else ".nii.gz"
+    names = ["fieldmap"] + (["lsq"] if "lsq" in opts else ["plus", "minus"])
+    for k in names:
+        v, i2 = H.hysco_nifti_read(f"{out}_{k}{ext}", H.HYSCO_F64)
+        assert v.shape == (nz, ny, nx) and np.isfinite(v).all()
+        assert np.allclose(tuple(i2.pixdim), pix, rtol=1e-6)
+    if "plus" in names:
+        tp = H.hysco_nifti_read(f"{out}_plus{ext}", H.HYSCO_F64)[0]
+        tm = H.hysco_nifti_read(f"{out}_minus{ext}", H.HYSCO_F64)[0]
+        assert O.relative_improvement(Ipf, Imf, tp, tm) > 50.0
+    if "lsq" in names:
+        assert line["report"]["lsq"]["unconverged"] == 0
