@@ -212,7 +212,8 @@ HYSCO_API hysco_status hysco_apply(hysco_ctx ctx, const void* d_b, void* d_Iplus
  * with hat weights, mass leaving the field of view dropped).  d_b: device
  * nodes; d_T, d_Iplus, d_Iminus: device cells (must not alias).  Synchronises
  * the context stream.  Returns HYSCO_INFEASIBLE if some column has |Db| >= 1
- * (its outputs are then undefined).  Not on slab contexts. */
+ * (its outputs are then undefined).  Column-local: on a slab context every
+ * pointer is the rank's dense slab and no data is exchanged. */
 HYSCO_API hysco_status hysco_push_forward(hysco_ctx ctx, const void* d_b, const void* d_T, void* d_Iplus,
                                           void* d_Iminus);
 
@@ -238,8 +239,9 @@ HYSCO_API void hysco_default_lsq_opts(hysco_lsq_opts* o);
  * A+^T i+ + A-^T i- for the bound pair (i+, i-) and field map b (device
  * nodes), by Jacobi-PCG per column (one warp each).  d_T_out: device cells
  * [batch][n1][n2][n3].  reports: [batch] or NULL.  Synchronises the context
- * stream.  Returns HYSCO_INFEASIBLE if some column has |Db| >= 1.  Not on
- * slab contexts. */
+ * stream.  Returns HYSCO_INFEASIBLE if some column has |Db| >= 1.  Column-
+ * local: on a slab context it corrects the rank's dense slab with no exchange
+ * and the reports describe the rank's columns. */
 HYSCO_API hysco_status hysco_lsq_correct(hysco_ctx ctx, const void* d_b, const hysco_lsq_opts* opts,
                                          void* d_T_out, hysco_lsq_report* reports);
 

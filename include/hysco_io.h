@@ -78,7 +78,8 @@ HYSCO_API hysco_status hysco_permute_pe(const void* d_in, void* d_out, const int
 
 /* Field map at the cell centres, (A b)_k = (b_k + b_{k+1}) / 2 in mm along +v
  * (the output grid of the images, R31).  d_b: device nodes, d_out:
- * device cells of the context's shape and dtype. */
+ * device cells of the context's shape and dtype (on a slab context: the
+ * rank's dense slab). */
 HYSCO_API hysco_status hysco_fieldmap_cells(hysco_ctx ctx, const void* d_b, void* d_out);
 
 #ifdef __cplusplus

@@ -1548,7 +1548,7 @@ void hysco_default_lsq_opts(hysco_lsq_opts* o) {
 
 hysco_status hysco_push_forward(hysco_ctx ctx, const void* d_b, const void* d_T, void* d_Iplus, void* d_Iminus) {
     CHECK_CTX();
-    if (ctx->g.slab) return set_err(ctx, HYSCO_ERR_STATE, "slab contexts support solve / correct / correct_host");
+    // column-local: on a slab context it runs on the rank's planes, no exchange
     if (!d_b || !d_T || !d_Iplus || !d_Iminus || !aligned16(d_b) || !aligned16(d_T) || !aligned16(d_Iplus) ||
         !aligned16(d_Iminus))
         return set_err(ctx, HYSCO_ERR_ARG, "pointers must be non-NULL and 16-byte aligned");
@@ -1559,7 +1559,7 @@ hysco_status hysco_push_forward(hysco_ctx ctx, const void* d_b, const void* d_T,
 hysco_status hysco_lsq_correct(hysco_ctx ctx, const void* d_b, const hysco_lsq_opts* opts, void* d_T_out,
                                hysco_lsq_report* reports) {
     CHECK_CTX();
-    if (ctx->g.slab) return set_err(ctx, HYSCO_ERR_STATE, "slab contexts support solve / correct / correct_host");
+    // column-local: on a slab context it runs on the rank's planes, no exchange
     if (hysco_status s = need_images(ctx)) return s;
     if (!d_b || !d_T_out || !aligned16(d_b) || !aligned16(d_T_out))
         return set_err(ctx, HYSCO_ERR_ARG, "pointers must be non-NULL and 16-byte aligned");
@@ -1574,7 +1574,7 @@ hysco_status hysco_lsq_correct(hysco_ctx ctx, const void* d_b, const hysco_lsq_o
 
 hysco_status hysco_fieldmap_cells(hysco_ctx ctx, const void* d_b, void* d_out) {
     CHECK_CTX();
-    if (ctx->g.slab) return set_err(ctx, HYSCO_ERR_STATE, "slab contexts support solve / correct / correct_host");
+    // column-local: on a slab context it runs on the rank's planes, no exchange
     if (!d_b || !d_out || !aligned16(d_b) || !aligned16(d_out))
         return set_err(ctx, HYSCO_ERR_ARG, "pointers must be non-NULL and 16-byte aligned");
     const long long total = (long long)ctx->cfg.batch * ctx->g.Nc;

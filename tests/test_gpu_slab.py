@@ -161,3 +161,48 @@ def test_loopback_hcp3t_four_slabs():
     b2, tp2, _, r2, _ = grouped(p.Ip[None], p.Im[None], p.h, H.HYSCO_F32, so, 1, 4)
     assert rel(b2, b1) <= 1e-5 and rel(tp2, tp1) <= 1e-5
     assert r2[0]["pcg_iters"] == r1[0]["pcg_iters"] == 30
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_loopback_slabs_push_forward_and_lsq_equal_single(nranks):
+    """NEXT-3 on slab contexts: column-local, so the concatenated slabs equal
+    the single-context result bit for bit (no exchange)."""
+    shape = (7, 5, 30)
+    h = (1.1, 1.2, 1.25)
+    rng = np.random.default_rng(3)
+    T = rng.uniform(0, 2, (1,) + shape).astype(np.float32)
+    b = phantom.random_feasible_b(shape, h[2], seed=6, amp=0.6)[None].astype(np.float32)
+    n1 = shape[0]
+    c = H.hysco_create(shape, h, 1)
+    tT, tb = torch.from_numpy(T).to(DEV), torch.from_numpy(b).to(DEV)
+    Ip, Im, out = torch.zeros_like(tT), torch.zeros_like(tT), torch.zeros_like(tT)
+    torch.cuda.synchronize()
+    H.hysco_push_forward(c, tb, tT, Ip, Im)
+    H.hysco_bind_images(c, Ip, Im)
+    torch.cuda.synchronize()
+    H.hysco_lsq_correct(c, tb, out)
+    torch.cuda.synchronize()
+    ref_p, ref_m, ref_t = Ip.cpu().numpy(), Im.cpu().numpy(), out.cpu().numpy()
+    H.hysco_destroy(c)
+    ctxs = H.hysco_create_loopback(shape, h, nranks)
+    got_p, got_m, got_t, keep = [], [], [], []
+    for r, cx in enumerate(ctxs):
+        i0, i1 = H.slab_bounds(n1, nranks, r)
+        sT = torch.from_numpy(np.ascontiguousarray(T[:, i0:i1])).to(DEV)
+        sb = torch.from_numpy(np.ascontiguousarray(b[:, i0:i1])).to(DEV)
+        sp, sm, so_ = torch.zeros_like(sT), torch.zeros_like(sT), torch.zeros_like(sT)
+        torch.cuda.synchronize()
+        H.hysco_push_forward(cx, sb, sT, sp, sm)
+        H.hysco_bind_images(cx, sp, sm)
+        torch.cuda.synchronize()
+        H.hysco_lsq_correct(cx, sb, so_)
+        torch.cuda.synchronize()
+        keep += [sT, sb, sp, sm, so_]
+        got_p.append(sp.cpu().numpy())
+        got_m.append(sm.cpu().numpy())
+        got_t.append(so_.cpu().numpy())
+    for cx in ctxs:
+        H.hysco_destroy(cx)
+    assert np.array_equal(np.concatenate(got_p, axis=1), ref_p)
+    assert np.array_equal(np.concatenate(got_m, axis=1), ref_m)
+    assert np.array_equal(np.concatenate(got_t, axis=1), ref_t)
