@@ -513,30 +513,42 @@ def ot_init(Ip, Im, h3, eps=1e-3, blur=True, feas_cap=0.95, vec=True):
 STOP_MAXITER, STOP_GRAD, STOP_DJ, STOP_DB, STOP_LSFAIL, STOP_INFEASIBLE = 0, 1, 2, 3, 4, 5
 
 
-def gauss_newton(Ip, Im, b0, h, alpha=ALPHA_DEFAULT, beta=BETA_DEFAULT, max_gn=10,
-                 max_pcg=10, pcg_tol=0.1, fixed=True, c1=1e-4, ls_max=10,
-                 tol_grad_rel=1e-2, tol_dJ_rel=1e-4, tol_db_rel=1e-3, log=None, armijo=True,
-                 precond="jacobi"):
-    """b_{k+1} = b_k + gamma_k q_k with H_J q_k = -grad J (Eq.(7)).
+def gn_armijo(objective, hess_of, precond_of, b0, h3, max_gn=10, max_pcg=10, pcg_tol=0.1,
+              fixed=True, c1=1e-4, ls_max=10, tol_grad_rel=1e-2, tol_dJ_rel=1e-4,
+              tol_db_rel=1e-3, log=None, armijo=True):
+    """The Gauss-Newton iteration with Armijo line search of P:183-199, written
+    for any objective (so its control flow is pinned on objectives with closed
+    forms, tests/test_oracle_gn_control.py).
 
-    fixed=True: exactly max_gn GN steps of exactly max_pcg PCG iterations
-    (parity / timing mode, R14, R16); fixed=False: the paper's stopping rules
-    with DESIGN.md's tolerances (R16).  armijo=False accepts the full step
-    unless infeasible (halving only for feasibility): the parity mode of R15.
-    precond: "jacobi" (the paper's default, P:198) or "block" (P:200, R20).
+    objective(b) -> state with .J, .grad (None if infeasible), .infeasible
+    (and optionally .D, .S, .P); hess_of(state) -> v -> H v (the GN Hessian,
+    P:186); precond_of(state) -> the PCG preconditioner (diagonal or callable).
+
+    Per GN step (Eq.(7)): q from PCG on H q = -grad (x0 = 0, R14),
+    then Armijo (R15): gamma = 1, 1/2, ... (at most ls_max trials)
+    until b + gamma q is feasible and J(b + gamma q) <= J(b) + c1 gamma grad.q;
+    no acceptable trial -> stop with LS_FAIL (b unchanged).  Stop rules (P:284,
+    "norm of the gradient, change in loss function or field map", tolerances
+    R16), tested in this order after each accepted step unless `fixed`:
+    ||grad|| <= tol_grad_rel ||grad(b0)||, |J_old - J| <= tol_dJ_rel |J_old|,
+    max|gamma q| <= tol_db_rel h3.  armijo=False accepts the first feasible
+    trial (the parity mode of R15).  An infeasible b0 stops before any step.
     """
     b = np.asarray(b0, np.float64).copy()
-    st = evaluate(Ip, Im, b, h, alpha, beta)
+    st = objective(b)
     rep = {"gn_iters": 0, "f_evals": 1, "h_evals": 0, "pcg_iters": 0, "ls_halvings": 0,
            "stop_reason": STOP_MAXITER, "history": []}
+
+    def parts(s):
+        return {k: getattr(s, k, np.nan) for k in ("J", "D", "S", "P")}
+
     if st.infeasible:
         rep["stop_reason"] = STOP_INFEASIBLE
-        rep.update(J=st.J, D=st.D, S=st.S, P=st.P, grad_norm=np.nan)
+        rep.update(grad_norm=np.nan, **parts(st))
         return b, st, rep
     g0 = float(np.linalg.norm(st.grad))
     for it in range(max_gn):
-        M = make_precond(st, precond)
-        q, npcg, nmv, rel = pcg(lambda v: hessvec(st, v), -st.grad, M, max_pcg, pcg_tol, fixed)
+        q, npcg, nmv, rel = pcg(hess_of(st), -st.grad, precond_of(st), max_pcg, pcg_tol, fixed)
         rep["h_evals"] += nmv
         rep["pcg_iters"] += npcg
         gq = float(np.sum(st.grad * q))
@@ -544,7 +556,7 @@ def gauss_newton(Ip, Im, b0, h, alpha=ALPHA_DEFAULT, beta=BETA_DEFAULT, max_gn=1
         accepted = False
         for t in range(ls_max):                     # Armijo (R15)
             bt = b + gamma * q
-            stt = evaluate(Ip, Im, bt, h, alpha, beta)
+            stt = objective(bt)
             rep["f_evals"] += 1
             if (not stt.infeasible) and (not armijo or stt.J <= st.J + c1 * gamma * gq):
                 accepted = True
@@ -558,8 +570,7 @@ def gauss_newton(Ip, Im, b0, h, alpha=ALPHA_DEFAULT, beta=BETA_DEFAULT, max_gn=1
         J_old = st.J
         b, st = bt, stt
         rep["gn_iters"] += 1
-        rep["history"].append({"J": st.J, "D": st.D, "S": st.S, "P": st.P, "gamma": gamma,
-                               "pcg_iters": npcg, "relres": rel})
+        rep["history"].append(dict(parts(st), gamma=gamma, pcg_iters=npcg, relres=rel))
         if log is not None:
             log(rep["history"][-1])
         if not fixed:
@@ -569,11 +580,33 @@ def gauss_newton(Ip, Im, b0, h, alpha=ALPHA_DEFAULT, beta=BETA_DEFAULT, max_gn=1
             if abs(J_old - st.J) <= tol_dJ_rel * abs(J_old):
                 rep["stop_reason"] = STOP_DJ
                 break
-            if float(np.max(np.abs(gamma * q))) <= tol_db_rel * h[2]:
+            if float(np.max(np.abs(gamma * q))) <= tol_db_rel * h3:
                 rep["stop_reason"] = STOP_DB
                 break
-    rep.update(J=st.J, D=st.D, S=st.S, P=st.P, grad_norm=float(np.linalg.norm(st.grad)))
+    rep.update(grad_norm=float(np.linalg.norm(st.grad)), **parts(st))
     return b, st, rep
+
+
+def gauss_newton(Ip, Im, b0, h, alpha=ALPHA_DEFAULT, beta=BETA_DEFAULT, max_gn=10,
+                 max_pcg=10, pcg_tol=0.1, fixed=True, c1=1e-4, ls_max=10,
+                 tol_grad_rel=1e-2, tol_dJ_rel=1e-4, tol_db_rel=1e-3, log=None, armijo=True,
+                 precond="jacobi"):
+    """b_{k+1} = b_k + gamma_k q_k with H_J q_k = -grad J (Eq.(7)) on
+    the field-map objective J = D + alpha S + beta P (evaluate()), GN
+    Hessian hessvec() and its preconditioner (make_precond()).
+
+    fixed=True: exactly max_gn GN steps of exactly max_pcg PCG iterations
+    (parity / timing mode, R14, R16); fixed=False: the paper's stopping rules
+    with DESIGN.md's tolerances (R16).  armijo=False accepts the full step
+    unless infeasible (halving only for feasibility): the parity mode of R15.
+    precond: "jacobi" (the paper's default, P:198) or "block" (P:200, R20).
+    """
+    return gn_armijo(lambda b: evaluate(Ip, Im, b, h, alpha, beta),
+                     lambda st: (lambda v: hessvec(st, v)),
+                     lambda st: make_precond(st, precond),
+                     b0, h[2], max_gn=max_gn, max_pcg=max_pcg, pcg_tol=pcg_tol, fixed=fixed, c1=c1,
+                     ls_max=ls_max, tol_grad_rel=tol_grad_rel, tol_dJ_rel=tol_dJ_rel,
+                     tol_db_rel=tol_db_rel, log=log, armijo=armijo)
 
 
 def correct_pair(Ip, Im, h, alpha=ALPHA_DEFAULT, beta=BETA_DEFAULT, max_gn=10, max_pcg=10,

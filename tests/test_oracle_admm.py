@@ -142,3 +142,40 @@ def test_admm_reduces_objective_on_synthetic_pair():
     st = O.evaluate(Ip, Im, b, p.h)
     assert np.isfinite(st.J) and st.J < 0.2 * J0
     assert rep["iters"] == 15 and rep["r_norm"][-1] < rep["r_norm"][0]
+
+
+def test_b_update_column_stop_rule_col_tol():
+    """R23 column stop ("different step sizes and stopping criteria for each
+    image column"): a column takes no step when its GN step predicts a decrease
+    -grad.q <= col_tol |Fc|.  On the quadratic column objective of the test
+    above (zero images, beta = 0) from b = 0 the GN step is exact, q = A^{-1}
+    rho hd v, so the ratio -grad.q / Fc(0) = 2 v^T (rho hd A^{-1}) v / ||v||^2
+    has a dense-algebra closed form: 2 for a constant column (D3 v = 0) and
+    small for an oscillating one.  With col_tol between the two ratios the
+    oscillating columns stay exactly 0 and the constant columns reach the
+    minimiser; col_tol = 0 moves every column, col_tol = inf none."""
+    shape = (1, 4, 9)
+    n = shape[2] + 1
+    v = np.zeros((1, 4, n))
+    v[0, 0] = 0.7                                   # constant
+    v[0, 1] = -0.3
+    v[0, 2] = 0.2 * (-1.0) ** np.arange(n)          # oscillating
+    v[0, 3] = 0.1 * np.cos(np.pi * np.arange(n) * 0.9)
+    alpha, rho = 300.0, 50.0
+    hd = H[0] * H[1] * H[2]
+    D = (np.eye(n, k=1)[:-1] - np.eye(n)[:-1]) / H[2]
+    A = alpha * hd * D.T @ D + rho * hd * np.eye(n)
+    ratio = [2.0 * v[0, j] @ np.linalg.solve(A, rho * hd * v[0, j]) / (v[0, j] @ v[0, j]) for j in range(4)]
+    assert ratio[0] > 1.999 and ratio[1] > 1.999 and ratio[2] < 0.5 and ratio[3] < 0.5, ratio
+    Z = np.zeros(shape)
+    kw = dict(alpha=alpha, beta=0.0, rho=rho, inner=1)
+    b = O.admm_b_update(Z, Z, np.zeros_like(v), v, H, col_tol=1.0, **kw)
+    for j in range(4):
+        if ratio[j] <= 1.0:
+            assert np.array_equal(b[0, j], np.zeros(n)), j
+        else:
+            assert np.allclose(b[0, j], np.linalg.solve(A, rho * hd * v[0, j]), rtol=1e-10, atol=1e-13), j
+    b = O.admm_b_update(Z, Z, np.zeros_like(v), v, H, col_tol=0.0, **kw)
+    assert all(np.abs(b[0, j]).max() > 0 for j in range(4))
+    b = O.admm_b_update(Z, Z, np.zeros_like(v), v, H, col_tol=np.inf, **kw)
+    assert np.array_equal(b, np.zeros_like(v))
