@@ -82,6 +82,12 @@ HYSCO_API hysco_status hysco_permute_pe(const void* d_in, void* d_out, const int
  * rank's dense slab). */
 HYSCO_API hysco_status hysco_fieldmap_cells(hysco_ctx ctx, const void* d_b, void* d_out);
 
+/* Same field map in a chosen unit: HYSCO_FIELDMAP_MM (= hysco_fieldmap_cells)
+ * or HYSCO_FIELDMAP_VOXEL, the displacement in voxels along +v of the PE axis,
+ * (A b)_k / h3 (the CLI's default output, R31).  Other values: HYSCO_ERR_ARG. */
+enum { HYSCO_FIELDMAP_MM = 0, HYSCO_FIELDMAP_VOXEL = 1 };
+HYSCO_API hysco_status hysco_fieldmap_cells_units(hysco_ctx ctx, const void* d_b, void* d_out, int32_t units);
+
 #ifdef __cplusplus
 }
 #endif

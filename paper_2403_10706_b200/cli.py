@@ -7,7 +7,8 @@ PE axis last on the GPU, estimates the field map (OT init + blur +
 guard -> Gauss-Newton-PCG or ADMM), corrects (Jacobian modulation and / or
 least squares), moves the results back to the file's axis order and writes
 
-    OUT_fieldmap.nii.gz   field map at the cell centres, mm along +PE (R31)
+    OUT_fieldmap.nii.gz   field map at the cell centres, voxel displacement along
+                          +PE of the file's PE axis (--fieldmap-units mm: mm; R31)
     OUT_plus.nii.gz       Jacobian-modulation corrected I+   
     OUT_minus.nii.gz      Jacobian-modulation corrected I-
     OUT_lsq.nii.gz        least-squares corrected image      (--correction lsq|both)
@@ -15,6 +16,11 @@ least squares), moves the results back to the file's axis order and writes
 with the geometry of the PLUS file.  Every numeric step is a libhysco call;
 this module only parses arguments and moves buffers.  Prints one JSON line
 with the stage timings and the solver report.
+
+Exit status: 0 success; 2 bad arguments or mismatched image sizes; 3 the field
+map is infeasible (|d_v b| >= 1 somewhere: the OT start, the GN or ADMM
+result, or a least-squares column), nothing is written; 4 an I/O error
+(unreadable / malformed input, unwritable output).
 """
 import argparse
 import ctypes
@@ -48,7 +54,17 @@ def parse(argv=None):
     ap.add_argument("--no-blur", action="store_true")
     ap.add_argument("--device", type=int, default=0)
     ap.add_argument("--no-gzip", action="store_true", help="write .nii instead of .nii.gz")
+    ap.add_argument("--fieldmap-units", default="voxel", choices=["voxel", "mm"],
+                    help="unit of OUT_fieldmap: voxel displacement (default) or mm, along +PE (R31)")
     return ap.parse_args(argv)
+
+
+EXIT_OK, EXIT_ARGS, EXIT_INFEASIBLE, EXIT_IO = 0, 2, 3, 4
+
+
+def _fail(code, msg):
+    print(f"hysco: {msg}", file=sys.stderr, flush=True)
+    return code
 
 
 def main(argv=None):
@@ -59,20 +75,29 @@ def main(argv=None):
     t0 = time.perf_counter()
     dtype = H.HYSCO_F64 if args.dtype == "f64" else H.HYSCO_F32
     tdt = torch.float64 if dtype == H.HYSCO_F64 else torch.float32
-    info_p = H.hysco_nifti_info_read(args.plus)
-    info_m = H.hysco_nifti_info_read(args.minus)
+    try:
+        info_p = H.hysco_nifti_info_read(args.plus)
+        info_m = H.hysco_nifti_info_read(args.minus)
+    except H.HyscoError as e:
+        return _fail(EXIT_IO, str(e))
     dims = tuple(info_p.dim)
     if tuple(info_m.dim) != dims:
-        raise SystemExit(f"image sizes differ: {dims} vs {tuple(info_m.dim)}")
+        return _fail(EXIT_ARGS, f"image sizes differ: {dims} vs {tuple(info_m.dim)}")
     n, h = H.hysco_pe_shape(dims, tuple(info_p.pixdim), args.pe_axis)
     nvox = dims[0] * dims[1] * dims[2]
     host = torch.empty((4, nvox), dtype=tdt, pin_memory=True)    # rows 0-1: the pair in; rows 0-3: results out
     L = H.lib()
+
+    def read(k):
+        # the I/O error message is thread-local in libhysco: fetch it in this worker
+        s = L.hysco_nifti_read(os.fsencode((args.plus, args.minus)[k]), dtype, ctypes.c_void_p(host[k].data_ptr()),
+                               nvox, None)
+        return None if s == H.HYSCO_OK else f"{(args.plus, args.minus)[k]}: {L.hysco_io_last_error().decode()}"
+
     with ThreadPoolExecutor(2) as ex:            # the two files decompress concurrently (ctypes drops the GIL)
-        st = list(ex.map(lambda k: L.hysco_nifti_read(os.fsencode((args.plus, args.minus)[k]), dtype,
-                                                      ctypes.c_void_p(host[k].data_ptr()), nvox, None), (0, 1)))
-    for s in st:
-        H._io_check(s)
+        errs = [e for e in ex.map(read, (0, 1)) if e]
+    if errs:
+        return _fail(EXIT_IO, "; ".join(errs))
     t_read = time.perf_counter()
 
     torch.cuda.set_device(args.device)
@@ -93,15 +118,18 @@ def main(argv=None):
                                       else H.HYSCO_PRECOND_JACOBI)
             reps, infeas = H.hysco_correct(ctx, b, outs[1:2], outs[2:3], ot, so)
             report = dict(reps[0], stop=H.STOP_NAMES.get(reps[0]["stop_reason"], "?"))
+            infeas = bool(infeas) or not np.isfinite(report["J"])
         else:
             H.hysco_ot_init(ctx, b, ot)
             report = H.hysco_admm(ctx, b, H.default_admm_opts(fixed_iters=1 if args.stop == "fixed" else 0))[0]
             H.hysco_apply(ctx, b, outs[1:2], outs[2:3])
-            infeas = False
-        if args.correction in ("lsq", "both"):
-            lrep, _ = H.hysco_lsq_correct(ctx, b, outs[3:4], H.default_lsq_opts(lam=args.lsq_lambda))
+            infeas = not np.isfinite(report["J"])        # ADMM reports J = +inf at an infeasible b
+        if args.correction in ("lsq", "both") and not infeas:
+            lrep, linf = H.hysco_lsq_correct(ctx, b, outs[3:4], H.default_lsq_opts(lam=args.lsq_lambda))
             report["lsq"] = lrep[0]
-        H.hysco_fieldmap_cells(ctx, b, outs[0:1])
+            infeas = bool(linf) or lrep[0]["infeasible"] > 0
+        H.hysco_fieldmap_cells(ctx, b, outs[0:1],
+                               H.HYSCO_FIELDMAP_VOXEL if args.fieldmap_units == "voxel" else H.HYSCO_FIELDMAP_MM)
         back = torch.empty((4, nvox), dtype=tdt, device=dev)
         H.hysco_permute_pe(outs, back, dims, args.pe_axis, True, dtype, batch=4, stream=stream.cuda_stream)
         res = host                                   # one pinned buffer per run (pinning costs ~ms per 10 MB)
@@ -110,6 +138,11 @@ def main(argv=None):
     finally:
         H.hysco_destroy(ctx)
     t_gpu = time.perf_counter()
+    if infeas:
+        print(json.dumps({"files": [], "infeasible": True, "report": {k: v for k, v in report.items()
+                                                                       if not isinstance(v, float) or np.isfinite(v)}}),
+              flush=True)
+        return _fail(EXIT_INFEASIBLE, "infeasible field map (|d_v b| >= 1): nothing written")
 
     ext = ".nii" if args.no_gzip else ".nii.gz"
     names = ["fieldmap", "plus", "minus", "lsq"]
@@ -117,16 +150,26 @@ def main(argv=None):
         ([3] if args.correction in ("lsq", "both") else [])
     shape_file = (dims[2], dims[1], dims[0])
     files = [f"{args.out}_{names[k]}{ext}" for k in keep]
+
+    def write(kp):
+        try:
+            H.hysco_nifti_write(kp[1], res[kp[0]].numpy().reshape(shape_file), info_p)
+        except H.HyscoError as e:            # message fetched on this worker thread (thread-local)
+            return f"{kp[1]}: {e}"
+        return None
+
     with ThreadPoolExecutor(len(keep)) as ex:
-        list(ex.map(lambda kp: H.hysco_nifti_write(kp[1], res[kp[0]].numpy().reshape(shape_file), info_p),
-                    zip(keep, files)))
+        errs = [e for e in ex.map(write, zip(keep, files)) if e]
+    if errs:
+        return _fail(EXIT_IO, "; ".join(errs))
     t_write = time.perf_counter()
-    print(json.dumps({"files": files, "kernel_shape": list(n), "pe_axis": args.pe_axis, "infeasible": bool(infeas),
+    print(json.dumps({"files": files, "kernel_shape": list(n), "pe_axis": args.pe_axis, "infeasible": False,
+                      "fieldmap_units": args.fieldmap_units,
                       "seconds": {"read": t_read - t0, "gpu": t_gpu - t_read, "write": t_write - t_gpu,
                                   "total": t_write - t0},
                       "report": {k: v for k, v in report.items() if not isinstance(v, float) or np.isfinite(v)}}),
           flush=True)
-    return 0
+    return EXIT_OK
 
 
 if __name__ == "__main__":

@@ -267,7 +267,8 @@ __global__ void __launch_bounds__(32 * ADMM_WARPS, sizeof(T) == 4 ? ADMM_MINB : 
                                                                 double c1, int ls_max, double col_tol,
                                                                 const unsigned* __restrict__ done) {
     count_launch(c);
-    if (*done) return;                       // ADMM already stopped (iteration enqueued ahead of the host check)
+    // ADMM already stopped (iteration enqueued ahead of the host check) or this pair converged
+    if (done[0] || done[1 + blockIdx.y]) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int pair = blockIdx.y;
@@ -349,7 +350,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) admm_rhs_kernel(Geom g, Ctl c, const T* __restrict__ b, const T* __restrict__ u,
                                                        T* __restrict__ w, const unsigned* __restrict__ done) {
     count_launch(c);
-    if (*done) return;
+    if (done[0] || done[1 + blockIdx.y]) return;   // stopped, or this pair converged (per-pair stop, R26)
     const size_t po = (size_t)blockIdx.y * g.ps;
     for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < g.Nn; t += (long long)gridDim.x * blockDim.x)
         w[po + t] = b[po + t] + u[po + t];
@@ -365,7 +366,7 @@ __global__ void __launch_bounds__(256) admm_zscale_kernel(Geom g, Ctl c, C* __re
                                                           const double* __restrict__ lam, long long spec,
                                                           const unsigned* __restrict__ done) {
     count_launch(c);
-    if (*done) return;
+    if (done[0] || done[1 + blockIdx.y]) return;   // stopped, or this pair converged (per-pair stop, R26)
     const int pair = blockIdx.y, lane = threadIdx.x & 31;
     const double rho = rho_p[pair];
     const int P = g.P;
@@ -402,7 +403,7 @@ __global__ void __launch_bounds__(256) admm_u_kernel(Geom g, Ctl c, const T* __r
                                                      T* __restrict__ z, T* __restrict__ u,
                                                      const unsigned* __restrict__ done) {
     count_launch(c);
-    if (*done) return;
+    if (done[0] || done[1 + blockIdx.y]) return;   // stopped, or this pair converged (per-pair stop, R26)
     const int pair = blockIdx.y;
     const size_t po = (size_t)pair * g.ps;
     double r2 = 0, s2 = 0, db2 = 0, bb = 0;
@@ -444,16 +445,18 @@ __global__ void __launch_bounds__(256) admm_u_kernel(Geom g, Ctl c, const T* __r
 // Residual balancing and the stop test on the device, after admm_u_kernel's
 // pair totals r^2, |dz|^2, |db|^2, |b|^2 (oracle admm_rho_update and admm();
 // R25, R26; |du| = |b - z| = r).  stat[pair][4] = iterations, r_norm, s_norm,
-// converged.  Sets *done when every pair converged (not in fixed mode); once
-// done, only resets fac so that the following admm_scale_u_kernel is a no-op.
+// converged.  done[1 + p]: pair p converged (not in fixed mode) -- its kernels
+// return at once from then on, so every pair stops on its own test like the
+// oracle's admm(); done[0]: every pair converged (the host's early exit).  A
+// stopped pair only gets fac = 1, so admm_scale_u_kernel leaves its u alone.
 __global__ void admm_balance_kernel(Ctl c, int B, double* __restrict__ rho, double* __restrict__ fac,
                                     double* __restrict__ stat, unsigned* __restrict__ done, int it, double mu,
                                     double tau, double tol, int fixed) {
     count_launch(c);
-    const bool stopped = *done != 0;
+    const bool stopped = done[0] != 0;
     bool all_conv = true;
     for (int p = threadIdx.x; p < B; p += blockDim.x) {
-        if (stopped) {
+        if (stopped || done[1 + p]) {
             fac[p] = 1.0;
             continue;
         }
@@ -475,10 +478,11 @@ __global__ void admm_balance_kernel(Ctl c, int B, double* __restrict__ rho, doub
         st[1] = r_norm;
         st[2] = s_norm;
         st[3] = conv ? 1.0 : 0.0;
+        if (conv && !fixed) done[1 + p] = 1u;
         all_conv = all_conv && conv;
     }
     all_conv = __syncthreads_and(all_conv);
-    if (threadIdx.x == 0 && !stopped && all_conv && !fixed) *done = 1u;
+    if (threadIdx.x == 0 && !stopped && all_conv && !fixed) done[0] = 1u;
 }
 
 // u *= f[pair] (residual balancing rescales the scaled multiplier).

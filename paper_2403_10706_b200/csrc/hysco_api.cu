@@ -64,7 +64,7 @@ struct hysco_ctx_s {
     double* admm_fac = nullptr;     // [batch] device (u rescaling)
     double* admm_lam = nullptr;     // [n1][n2/2+1] periodic L_xy eigenvalues
     double* admm_stat = nullptr;    // [batch][4] iterations, r_norm, s_norm, converged (device)
-    unsigned* admm_done = nullptr;  // device stop flag of the running ADMM solve
+    unsigned* admm_done = nullptr;  // device stop flags of the running ADMM solve: [0] all, [1 + p] pair p
     unsigned* h_admm_done = nullptr;                // [2] pinned copies of the flag
     cudaEvent_t admm_ev[2] = {nullptr, nullptr};    // recorded after each copy
     size_t admm_smem = 0;
@@ -1024,7 +1024,7 @@ static hysco_status admm_setup(hysco_ctx ctx) {
     CK(cudaMalloc(&ctx->admm_fac, sizeof(double) * ctx->cfg.batch));
     CK(cudaMalloc(&ctx->admm_lam, sizeof(double) * g.n1 * (g.n2 / 2 + 1)));
     CK(cudaMalloc(&ctx->admm_stat, sizeof(double) * 4 * ctx->cfg.batch));
-    CK(cudaMalloc(&ctx->admm_done, sizeof(unsigned)));
+    CK(cudaMalloc(&ctx->admm_done, sizeof(unsigned) * (1 + ctx->cfg.batch)));
     CK(cudaMallocHost(&ctx->h_admm_done, 2 * sizeof(unsigned)));
     for (int k = 0; k < 2; k++) CK(cudaEventCreateWithFlags(&ctx->admm_ev[k], cudaEventDisableTiming));
     admm_lambda_kernel<<<64, 256, 0, ctx->stream>>>(g, ctx->admm_lam);
@@ -1069,7 +1069,7 @@ static hysco_status admm_run(hysco_ctx ctx, void* d_b, const hysco_admm_opts& o,
     std::vector<double> rho(B, rho0), stat((size_t)4 * B, 0.0);
     CK(cudaMemsetAsync(ctx->launches, 0, sizeof(unsigned long long), st));
     CK(cudaMemcpyAsync(ctx->admm_rho, rho.data(), sizeof(double) * B, cudaMemcpyHostToDevice, st));
-    CK(cudaMemsetAsync(ctx->admm_done, 0, sizeof(unsigned), st));
+    CK(cudaMemsetAsync(ctx->admm_done, 0, sizeof(unsigned) * (1 + B), st));
     CK(cudaMemsetAsync(ctx->admm_stat, 0, sizeof(double) * 4 * B, st));
     CK(cudaMemcpyAsync(b, d_b, nb, cudaMemcpyDeviceToDevice, st));
     CK(cudaMemcpyAsync(z, d_b, nb, cudaMemcpyDeviceToDevice, st));     // z0 = b0
@@ -1573,7 +1573,14 @@ hysco_status hysco_lsq_correct(hysco_ctx ctx, const void* d_b, const hysco_lsq_o
 }
 
 hysco_status hysco_fieldmap_cells(hysco_ctx ctx, const void* d_b, void* d_out) {
+    return hysco_fieldmap_cells_units(ctx, d_b, d_out, HYSCO_FIELDMAP_MM);
+}
+
+hysco_status hysco_fieldmap_cells_units(hysco_ctx ctx, const void* d_b, void* d_out, int32_t units) {
     CHECK_CTX();
+    if (units != HYSCO_FIELDMAP_MM && units != HYSCO_FIELDMAP_VOXEL)
+        return set_err(ctx, HYSCO_ERR_ARG, "units must be HYSCO_FIELDMAP_MM or HYSCO_FIELDMAP_VOXEL");
+    const double scale = units == HYSCO_FIELDMAP_VOXEL ? 1.0 / ctx->g.h3 : 1.0;
     // column-local: on a slab context it runs on the rank's planes, no exchange
     if (!d_b || !d_out || !aligned16(d_b) || !aligned16(d_out))
         return set_err(ctx, HYSCO_ERR_ARG, "pointers must be non-NULL and 16-byte aligned");
@@ -1581,10 +1588,10 @@ hysco_status hysco_fieldmap_cells(hysco_ctx ctx, const void* d_b, void* d_out) {
     const int grid = (int)std::min<long long>((total + 255) / 256, (long long)ctx->nsm * 8);
     if (ctx->cfg.dtype == HYSCO_F64)
         fieldmap_cells_kernel<double><<<grid, 256, 0, ctx->stream>>>(ctx->g, ctx->ctl, (const double*)d_b,
-                                                                    (double*)d_out, total);
+                                                                    (double*)d_out, total, scale);
     else
         fieldmap_cells_kernel<float><<<grid, 256, 0, ctx->stream>>>(ctx->g, ctx->ctl, (const float*)d_b,
-                                                                   (float*)d_out, total);
+                                                                   (float*)d_out, total, (float)scale);
     CK(cudaGetLastError());
     return HYSCO_OK;
 }

@@ -797,15 +797,17 @@ __global__ void __launch_bounds__(256) guard_scale_kernel(Geom g, Ctl c, T* __re
 }
 
 // Field map at the cell centres, (A b)_k = (b_k + b_{k+1}) / 2 (output of
-// the front-end, hysco_io.h).  Grid-stride over cells of all pairs.
+// the front-end, hysco_io.h), times `scale` (1: mm; 1/h3: voxels, R31).
+// Grid-stride over cells of all pairs.
 template <typename T>
-__global__ void fieldmap_cells_kernel(Geom g, Ctl c, const T* __restrict__ b, T* __restrict__ out, long long total) {
+__global__ void fieldmap_cells_kernel(Geom g, Ctl c, const T* __restrict__ b, T* __restrict__ out, long long total,
+                                      T scale) {
     count_launch(c);
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
         const long long col = i / g.n3, k = i - col * g.n3;    // col runs over pairs x columns
         const T* bc = b + col * g.P;
-        out[i] = T(0.5) * (bc[k] + bc[k + 1]);
+        out[i] = scale * (T(0.5) * (bc[k] + bc[k + 1]));
     }
 }
 

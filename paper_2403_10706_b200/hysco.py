@@ -31,7 +31,7 @@ EXPORTED = ["hysco_default_solve_opts", "hysco_default_ot_opts", "hysco_default_
             "hysco_group_solve", "hysco_push_forward", "hysco_default_lsq_opts", "hysco_lsq_correct",
             # front-end (include/hysco_io.h)
             "hysco_nifti_info_read", "hysco_nifti_read", "hysco_nifti_write", "hysco_io_last_error", "hysco_pe_shape",
-            "hysco_permute_pe", "hysco_fieldmap_cells"]
+            "hysco_permute_pe", "hysco_fieldmap_cells", "hysco_fieldmap_cells_units"]
 PROF_NAMES = ["matvec", "pcg_update", "pcg_dir", "eval", "pcg_resident", "trial_init"]
 
 
@@ -174,6 +174,7 @@ def lib():
     L.hysco_permute_pe.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_int64), ctypes.c_int32, ctypes.c_int32,
                                    ctypes.c_int, ctypes.c_int64, vp]
     L.hysco_fieldmap_cells.argtypes = [vp, vp, vp]
+    L.hysco_fieldmap_cells_units.argtypes = [vp, vp, vp, ctypes.c_int32]
     L.hysco_last_error.argtypes = [vp]
     L.hysco_last_error.restype = ctypes.c_char_p
     L.hysco_profile_kernels.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_double)]
@@ -481,8 +482,8 @@ def hysco_nifti_write(path, data, info):
     """data: C array [nz][ny][nx] of float32 / float64; dims, voxel sizes, geometry from info."""
     dtype = HYSCO_F64 if data.dtype == np.float64 else HYSCO_F32
     assert data.dtype in (np.float32, np.float64) and data.shape == (info.dim[2], info.dim[1], info.dim[0])
-    _io_check(lib().hysco_nifti_write(os.fsencode(path), dtype, _ptr(np.ascontiguousarray(data)),
-                                      ctypes.byref(info)))
+    arr = np.ascontiguousarray(data)      # a copy for non-contiguous views: keep it alive across the call
+    _io_check(lib().hysco_nifti_write(os.fsencode(path), dtype, _ptr(arr), ctypes.byref(info)))
 
 
 def hysco_pe_shape(dims, pixdim, pe_axis):
@@ -501,5 +502,13 @@ def hysco_permute_pe(d_in, d_out, dims, pe_axis, inverse=False, dtype=HYSCO_F32,
                                      int(batch), stream))
 
 
-def hysco_fieldmap_cells(ctx, b, out):
-    _check(ctx, lib().hysco_fieldmap_cells(ctx, _ptr(b), _ptr(out)))
+HYSCO_FIELDMAP_MM, HYSCO_FIELDMAP_VOXEL = 0, 1
+
+
+def hysco_fieldmap_cells(ctx, b, out, units=None):
+    """Field map at the cell centres: mm along +PE (units None / HYSCO_FIELDMAP_MM)
+    or voxels (HYSCO_FIELDMAP_VOXEL)."""
+    if units is None:
+        _check(ctx, lib().hysco_fieldmap_cells(ctx, _ptr(b), _ptr(out)))
+    else:
+        _check(ctx, lib().hysco_fieldmap_cells_units(ctx, _ptr(b), _ptr(out), int(units)))

@@ -66,6 +66,16 @@ def test_fieldmap_cells(dtype):
     ref = O.avg_pe(b.astype(np.float64))
     tol = 1e-15 if dtype == H.HYSCO_F64 else 1e-7
     assert np.max(np.abs(out.cpu().numpy() - ref)) <= tol * np.max(np.abs(ref))
+    mm = out.cpu().numpy().copy()
+    H.hysco_fieldmap_cells(c, _dev(b), out, H.HYSCO_FIELDMAP_MM)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), mm)
+    H.hysco_fieldmap_cells(c, _dev(b), out, H.HYSCO_FIELDMAP_VOXEL)     # R31: voxels along +PE
+    torch.cuda.synchronize()
+    assert np.max(np.abs(out.cpu().numpy() - ref / 1.25)) <= tol * np.max(np.abs(ref / 1.25))
+    with pytest.raises(H.HyscoError) as e:
+        H.hysco_fieldmap_cells(c, _dev(b), out, 7)
+    assert e.value.status == H.HYSCO_ERR_ARG
     H.hysco_destroy(c)
 
 
@@ -115,7 +125,7 @@ def test_cli_end_to_end_matches_direct_api(tmp_path, pe):
     torch.cuda.synchronize()
     H.hysco_correct(c, b, Tp, Tm, H.default_ot_opts(), H.default_solve_opts())
     H.hysco_lsq_correct(c, b, Tl, H.default_lsq_opts())
-    H.hysco_fieldmap_cells(c, b, fm)
+    H.hysco_fieldmap_cells(c, b, fm, H.HYSCO_FIELDMAP_VOXEL)     # the CLI's default unit (R31)
     torch.cuda.synchronize()
     H.hysco_destroy(c)
     for k, t in (("fieldmap", fm), ("plus", Tp), ("minus", Tm), ("lsq", Tl)):
@@ -166,3 +176,21 @@ def test_cli_option_paths(tmp_path, opts):
         assert O.relative_improvement(Ipf, Imf, tp, tm) > 50.0
     if "lsq" in names:
         assert line["report"]["lsq"]["unconverged"] == 0
+
+
+def test_cli_io_error_in_reader_thread_and_unwritable_output(tmp_path):
+    """Exit 4 with the file name and libhysco's message (fetched on the reader
+    thread: the message is thread-local) for a truncated input, and for an
+    output prefix in a directory that does not exist."""
+    a = phantom.make_pair((6, 5, 12), (1.25, 1.25, 1.25), seed=2).Ip
+    info = _info((12, 5, 6), (1.25, 1.25, 1.25))
+    H.hysco_nifti_write(str(tmp_path / "a.nii"), a, info)
+    (tmp_path / "t.nii").write_bytes((tmp_path / "a.nii").read_bytes()[:600])
+    r = subprocess.run([sys.executable, "-m", "paper_2403_10706_b200.cli", str(tmp_path / "a.nii"),
+                        str(tmp_path / "t.nii"), "--pe-axis", "1", "--out", str(tmp_path / "o")],
+                       capture_output=True, text=True, cwd=ROOT, timeout=600)
+    assert r.returncode == 4 and "t.nii" in r.stderr and "trunc" in r.stderr.lower(), r.stderr[-500:]
+    r = subprocess.run([sys.executable, "-m", "paper_2403_10706_b200.cli", str(tmp_path / "a.nii"),
+                        str(tmp_path / "a.nii"), "--pe-axis", "1", "--out", str(tmp_path / "no" / "o")],
+                       capture_output=True, text=True, cwd=ROOT, timeout=600)
+    assert r.returncode == 4 and "fieldmap" in r.stderr, r.stderr[-500:]

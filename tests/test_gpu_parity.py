@@ -83,12 +83,11 @@ def rnd(x, dtype):
     return np.asarray(x).astype(ND[dtype]).astype(np.float64)
 
 
-def ls_mode(dtype):
-    """Armijo's accept test compares J values whose difference falls below fp32
-    resolution in late fixed-count GN steps, so fp32 parity runs use the
-    full-step-unless-infeasible mode on BOTH sides (R15 parity mode); the fp64
-    build keeps Armijo and must take the same decisions as the oracle."""
-    return 1 if dtype == H.HYSCO_F64 else 0
+ARMIJO = pytest.mark.parametrize("armijo", [1, 0], ids=["armijo", "fullstep"])
+"""Armijo on (the production default, P:191, R15) and the full-step-unless-
+infeasible parity mode (R15) on both sides.  On these instances no Armijo
+decision sits within 6e-5 relative of its threshold (oracle trace; fp32
+rounding of J is ~1e-7), so fp32 must take the oracle's decisions too."""
 
 
 SHAPES = [
@@ -161,17 +160,18 @@ def test_apply_parity(pair, dtype):
     c.close()
 
 
+@ARMIJO
 @pytest.mark.parametrize("dtype", [H.HYSCO_F32, H.HYSCO_F64], ids=["f32", "f64"])
-def test_solve_fixed_parity(pair, dtype):
+def test_solve_fixed_parity(pair, dtype, armijo):
     """Fixed 10 GN x 10 PCG from the same b0: field map and objective (BASELINE configs[0])."""
     Ip, Im = rnd(pair.Ip, dtype), rnd(pair.Im, dtype)
     b0, _ = O.ot_init(Ip, Im, pair.h[2])
     b0 = rnd(b0, dtype)
     c = Ctx([Ip], [Im], pair.h, dtype)
     b = c.nodes(b0)
-    reps, inf = H.hysco_solve(c.ctx, b, H.default_solve_opts(armijo=ls_mode(dtype)))
+    reps, inf = H.hysco_solve(c.ctx, b, H.default_solve_opts(armijo=armijo))
     assert not inf
-    bref, st, rep = O.gauss_newton(Ip, Im, b0, pair.h, fixed=True, armijo=bool(ls_mode(dtype)))
+    bref, st, rep = O.gauss_newton(Ip, Im, b0, pair.h, fixed=True, armijo=bool(armijo))
     r = reps[0]
     assert (r["gn_iters"], r["pcg_iters"], r["h_evals"], r["f_evals"], r["ls_halvings"]) == \
         (rep["gn_iters"], rep["pcg_iters"], rep["h_evals"], rep["f_evals"], rep["ls_halvings"])
@@ -180,16 +180,17 @@ def test_solve_fixed_parity(pair, dtype):
     c.close()
 
 
+@ARMIJO
 @pytest.mark.parametrize("dtype", [H.HYSCO_F32, H.HYSCO_F64], ids=["f32", "f64"])
-def test_correct_pipeline_parity(pair, dtype):
+def test_correct_pipeline_parity(pair, dtype, armijo):
     """The whole path: OT + blur + guard -> 10x10 GN-PCG -> apply."""
     Ip, Im = rnd(pair.Ip, dtype), rnd(pair.Im, dtype)
     c = Ctx([Ip], [Im], pair.h, dtype)
     b, Tp, Tm = c.nodes(), c.cells(), c.cells()
-    reps, inf = H.hysco_correct(c.ctx, b, Tp, Tm, solve_opts=H.default_solve_opts(armijo=ls_mode(dtype)))
+    reps, inf = H.hysco_correct(c.ctx, b, Tp, Tm, solve_opts=H.default_solve_opts(armijo=armijo))
     assert not inf
-    b0r, bref, Tpr, Tmr, rep = O.correct_pair(Ip, Im, pair.h, armijo=bool(ls_mode(dtype)))
-    assert reps[0]["ls_halvings"] == rep["ls_halvings"]
+    b0r, bref, Tpr, Tmr, rep = O.correct_pair(Ip, Im, pair.h, armijo=bool(armijo))
+    assert (reps[0]["ls_halvings"], reps[0]["f_evals"]) == (rep["ls_halvings"], rep["f_evals"])
     tol = TOL[dtype]["solve"]
     assert rel(c.np(b)[0], bref) <= tol
     assert rel(c.np(Tp)[0], Tpr) <= tol and rel(c.np(Tm)[0], Tmr) <= tol
@@ -335,8 +336,9 @@ def test_graph_and_host_loop_bitwise_equal(monkeypatch):
 RESIDENT_CASES = ["C1_16x16x8", "C2_hcp3t", (60, 40, 16), (50, 30, 15), (84, 37, 10), (400, 2, 10), (25, 8, 24)]
 
 
+@ARMIJO
 @pytest.mark.parametrize("cfg", RESIDENT_CASES, ids=[str(c) for c in RESIDENT_CASES])
-def test_resident_pcg_matches_streaming(monkeypatch, cfg):
+def test_resident_pcg_matches_streaming(monkeypatch, cfg, armijo):
     """The on-chip-resident PCG (one cooperative launch per GN step) and the
     streaming PCG kernels compute the same iteration (reduction order aside)."""
     p = phantom.make_config(cfg) if isinstance(cfg, str) else phantom.make_pair(cfg, (1.25, 1.25, 1.25), 11)
@@ -345,7 +347,7 @@ def test_resident_pcg_matches_streaming(monkeypatch, cfg):
         monkeypatch.setenv("HYSCO_NO_RESIDENT", nr)
         c = Ctx([p.Ip], [p.Im], p.h)
         b, Tp, Tm = c.nodes(), c.cells(), c.cells()
-        reps, _ = H.hysco_correct(c.ctx, b, Tp, Tm, solve_opts=H.default_solve_opts(armijo=0))
+        reps, _ = H.hysco_correct(c.ctx, b, Tp, Tm, solve_opts=H.default_solve_opts(armijo=armijo))
         out.append((c.np(b)[0], reps[0], H.hysco_last_launch_count(c.ctx)))
         c.close()
     (b_res, r_res, n_res), (b_str, r_str, n_str) = out
@@ -353,10 +355,11 @@ def test_resident_pcg_matches_streaming(monkeypatch, cfg):
     # alpha/beta round differently; after 10 unconverged GN steps b and J move
     # at first order in that rounding -- both gated at the kernel tolerance
     assert rel(b_res, b_str) <= 1e-5
-    assert (r_res["pcg_iters"], r_res["h_evals"], r_res["gn_iters"]) == (r_str["pcg_iters"], r_str["h_evals"], r_str["gn_iters"])
+    keys = ("pcg_iters", "h_evals", "gn_iters", "f_evals", "ls_halvings")
+    assert tuple(r_res[k] for k in keys) == tuple(r_str[k] for k in keys)
     assert relS(r_res["J"], r_str["J"]) <= 1e-5
     # resident: one launch per GN step instead of pcg_init + 10 x (matvec, update, dir) + trial_init
-    assert n_str - n_res == 10 * 31
+    assert n_str - n_res == 10 * 31 and r_res["f_evals"] == r_str["f_evals"]
 
 
 def test_repeat_calls_deterministic_and_host_entry_equal():
@@ -618,4 +621,28 @@ def test_admm_hcp3t_converges_and_reduces_objective(hcp3t):
     r = H.hysco_admm(c.ctx, b, H.default_admm_opts(max_iter=30))[0]
     assert np.isfinite(r["J"]) and r["J"] < 0.5 * j0[0, 0]
     assert r["iters"] >= 1 and r["r_norm"] < np.linalg.norm(c.np(b))
+    c.close()
+
+
+def test_admm_batch_paper_stop_per_pair_vs_oracle():
+    """Paper-style ADMM stop (R26) in a batch of two pairs that converge
+    at different iterations: each pair stops on its own test (per-pair done
+    flags), so each equals the oracle's single-pair admm(fixed=False) -- same
+    iteration count, same rho, same b (fp64)."""
+    shape, h = (10, 9, 24), (1.25, 1.25, 1.1)
+    pairs = [phantom.make_pair(shape, h, s) for s in (31, 33)]
+    Ips = [p.Ip.astype(np.float64) for p in pairs]
+    Ims = [p.Im.astype(np.float64) for p in pairs]
+    b0 = np.stack([O.ot_init(a, m, h[2])[0] for a, m in zip(Ips, Ims)])
+    refs = [O.admm(a, m, b0[k], h, max_iter=60, fixed=False, tol=1e-2) for k, (a, m) in enumerate(zip(Ips, Ims))]
+    its = [r[2]["iters"] for r in refs]
+    assert all(r[2]["stop"] == "converged" for r in refs) and its[0] != its[1], its
+    c = Ctx(Ips, Ims, h, H.HYSCO_F64)
+    b = c.nodes(b0)
+    reps = H.hysco_admm(c.ctx, b, H.default_admm_opts(max_iter=60, tol=1e-2), batch=2)
+    got = c.np(b)
+    for k in range(2):
+        assert reps[k]["iters"] == its[k] and reps[k]["converged"] == 1
+        assert abs(reps[k]["rho"] - refs[k][2]["rho_final"]) <= 1e-12 * refs[k][2]["rho_final"]
+        assert rel(got[k], refs[k][0]) <= 1e-6      # ~45 coupled iterations (fp64 drift, see test_admm_fixed_parity)
     c.close()

@@ -171,3 +171,42 @@ def test_large_gzip_is_multi_member_and_standard(tmp_path):
     assert open(p, "rb").read().count(b"\x1f\x8b\x08") >= 2         # more than one member
     b, _ = H.hysco_nifti_read(p)
     assert np.array_equal(a, b)
+
+
+def test_write_non_contiguous_view_keeps_data_alive(tmp_path):
+    """A transposed / strided array is copied to C order for the C call; the
+    copy must outlive the call (the file holds the view's values, not freed
+    memory).  Large enough that a freed buffer would be unmapped."""
+    rng = np.random.default_rng(5)
+    base = rng.standard_normal((60, 70, 80)).astype(np.float32)
+    for view in (base.transpose(2, 1, 0), base[::2, :, ::2]):
+        assert not view.flags["C_CONTIGUOUS"]
+        nz, ny, nx = view.shape
+        p = str(tmp_path / "v.nii.gz")
+        H.hysco_nifti_write(p, view, _info((nx, ny, nz)))
+        back, _ = H.hysco_nifti_read(p)
+        assert np.array_equal(back, view)
+
+
+def _cli(tmp_path, *argv):
+    import subprocess
+    import sys
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    return subprocess.run([sys.executable, "-m", "paper_2403_10706_b200.cli", *argv], capture_output=True,
+                          text=True, cwd=root, timeout=300)
+
+
+def test_cli_exit_codes_before_the_gpu(tmp_path):
+    """The CLI's documented exit status (cli.py): 4 for an unreadable input, 2
+    for images of different sizes; both are decided before any GPU work."""
+    a = np.ones((4, 5, 6), np.float32)
+    H.hysco_nifti_write(str(tmp_path / "a.nii"), a, _info((6, 5, 4)))
+    H.hysco_nifti_write(str(tmp_path / "b.nii"), np.ones((4, 5, 7), np.float32), _info((7, 5, 4)))
+    r = _cli(tmp_path, str(tmp_path / "a.nii"), str(tmp_path / "missing.nii"), "--pe-axis", "2", "--out",
+             str(tmp_path / "o"))
+    assert r.returncode == 4 and "missing.nii" in r.stderr
+    r = _cli(tmp_path, str(tmp_path / "a.nii"), str(tmp_path / "b.nii"), "--pe-axis", "2", "--out",
+             str(tmp_path / "o"))
+    assert r.returncode == 2 and "differ" in r.stderr
+    assert not list(tmp_path.glob("o_*"))
