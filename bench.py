@@ -145,42 +145,61 @@ def dist_env():
 
 # ---------------------------------------------------------------- CPU oracle timing (reference)
 
-def oracle_sample(pair, planes=None):
-    """Time the oracle (as it stands) on a bounded sample of the workload and
-    extrapolate seconds per pair = t_OT + 10 t_GN + t_apply, scaled by the
-    fraction of planes sampled.  Returns (seconds_per_pair, description)."""
+def host_info():
+    """Host CPU model and the cores this process may run on."""
+    model = "?"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    try:
+        aff = len(os.sched_getaffinity(0))
+    except Exception:
+        aff = None
+    return {"cpu_model": model, "os_cpu_count": os.cpu_count(), "affinity_cpus": aff}
+
+
+def oracle_sample(pair, planes):
+    """Time the oracle, as it stands, on a bounded sample of the workload: the
+    WHOLE path (OT + blur + guard -> fixed 10 GN x 10 Jacobi-PCG + Armijo ->
+    apply, O.correct_pair) on the slab of planes [0, planes) of dim 1 of the
+    pair, a volume of its own.  Seconds per pair = the slab's time x n1 /
+    planes (the path's work is linear in the number of PE columns).  BLAS /
+    OpenMP pools are limited to one thread.  Returns (s_per_pair, desc, wall)."""
     from oracle import hysco_oracle as O
+    from threadpoolctl import threadpool_limits
     n1 = pair.Ip.shape[0]
-    planes = n1 if planes is None else max(2, min(n1, planes))
+    planes = max(2, min(n1, int(planes)))
     Ip = pair.Ip[:planes].astype(np.float64)
     Im = pair.Im[:planes].astype(np.float64)
-    h = pair.h
-    t0 = time.perf_counter()
-    b0, _ = O.ot_init(Ip, Im, h[2])
-    t1 = time.perf_counter()
-    b, st, rep = O.gauss_newton(Ip, Im, b0, h, max_gn=1, max_pcg=10, fixed=True)
-    t2 = time.perf_counter()
-    O.apply_correction(Ip, Im, b, h[2])
-    t3 = time.perf_counter()
-    scale = n1 / planes
-    per_pair = ((t1 - t0) + 10 * (t2 - t1) + (t3 - t2)) * scale
-    desc = (f"oracle OT+blur, 1 GN step (10 PCG + Armijo eval), apply on {planes}/{n1} planes of the "
-            f"{pair.Ip.shape} pair; per pair = (t_OT + 10 t_GN + t_apply) x {scale:.3g}")
-    return per_pair, desc, t3 - t0
+    with threadpool_limits(limits=1):
+        t0 = time.perf_counter()
+        O.correct_pair(Ip, Im, pair.h)
+        wall = time.perf_counter() - t0
+    desc = (f"oracle (NumPy fp64, 1 thread) whole path OT+blur+guard -> 10 GN x 10 PCG + Armijo -> apply on "
+            f"planes [0, {planes}) of the {tuple(pair.Ip.shape)} pair; per pair = time x {n1}/{planes}")
+    return wall * n1 / planes, desc, wall
+
+
+def oracle_planes_for(pair, seconds):
+    """Planes whose oracle sample takes about `seconds` (probe on 4 planes)."""
+    _, _, w4 = oracle_sample(pair, 4)
+    return int(max(2, min(pair.Ip.shape[0], round(4 * seconds / max(w4, 1e-3)))))
 
 
 def run_reference(args):
+    """The reference arm of this tier: the CPU oracle as it stands, each step a
+    bounded sample of the workload (oracle_sample), on rank 0 only."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
     shape, h, seed = phantom.CONFIGS[args.config]
     pair = phantom.make_pair(shape, h, seed)
-    # bounded: size the sample so (steps + warmup) samples take ~2 minutes
-    per_plane = None
-    probe, _, tp = oracle_sample(pair, planes=8)
-    per_plane = tp / 8
-    planes = int(max(2, min(shape[0], 120.0 / max(args.steps + args.warmup, 1) / per_plane)))
+    # bounded: the whole --steps K --warmup W run takes ~2-3 minutes
+    planes = oracle_planes_for(pair, 150.0 / max(args.steps + args.warmup, 1))
     for _ in range(args.warmup):
         oracle_sample(pair, planes)
     vals, ms = [], []
@@ -191,12 +210,11 @@ def run_reference(args):
         ms.append(wall * 1e3)
     spp = float(np.mean(vals))
     v = 1.0 / spp
-    cores = 1
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.mean(ms)),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": workload_desc(args.config, 1),
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+            "data": "synthetic", "config": dict(workload_desc(args.config, 1), parallelism="dp1 (independent pairs per rank)"),
+            "cpu_baseline": dict({"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc}, **host_info()),
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
     print(json.dumps(line), flush=True)
@@ -213,60 +231,131 @@ FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
 RESIDENT_FLOPS_PER_NODE_ITER = 28
 
 
+_L2PK = {}
+
+
+def l2_peak_gbs():
+    """Measured L2 bandwidth: torch copy of a 24 MiB buffer into another (48 MiB
+    working set, L2-resident), read + write bytes, best of 50 (CUDA events)."""
+    if _L2PK:
+        return _L2PK
+    import torch
+    n = 24 << 18
+    a = torch.ones(n, device="cuda")
+    b = torch.empty_like(a)
+    for _ in range(5):
+        b.copy_(a)
+    best = None
+    for _ in range(50):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        b.copy_(a)
+        e1.record()
+        e1.synchronize()
+        t = e0.elapsed_time(e1)
+        best = t if best is None else min(best, t)
+    _L2PK.update(gbs=2 * 4 * n / (best * 1e-3) / 1e9,
+                 how="measured live: torch copy of 24 MiB (48 MiB read + write working set, L2-resident), best of 50")
+    return _L2PK
+
+
+def ncu_kernel_summary(config, name):
+    """profiles/ncu_summary.json entry of kernel `name` on workload `config`
+    (ncu --set full of this round's build, per launch; make_ncu_summary.py)."""
+    try:
+        summ = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        return summ.get("configs", {}).get(config, {}).get(name)
+    except Exception:
+        return None
+
+
 def roofline_entry(H, ctx, args, r0, B, shape, ms_per_step):
     """The kernel with the largest share of a step, timed by hysco_profile_kernels
     (each hot kernel re-launched on the context stream, same grid and buffers,
-    CUDA events per launch; cold = L2 flushed before each launch)."""
+    CUDA events per launch; cold = L2 flushed before each launch).  DESIGN.md §10."""
     n1, n2, n3 = shape
     prof_cold = H.hysco_profile_kernels(ctx, args.profile_reps, flush_l2=True)
     prof_warm = H.hysco_profile_kernels(ctx, args.profile_reps, flush_l2=False)
     Nn, Nc = B * n1 * n2 * (n3 + 1), B * n1 * n2 * n3
     resident = prof_warm["pcg_resident"] > 0
+    l2pcg = prof_warm.get("pcg_l2", -1) > 0
     gn = r0["gn_iters"]
     if resident:   # one cooperative launch per GN step runs all PCG iterations and the Armijo start
         per_step = {"pcg_resident": gn, "eval": r0["f_evals"]}
+    elif l2pcg:    # the same with the PCG state in L2 (hysco_l2pcg.cuh)
+        per_step = {"pcg_l2": gn, "eval": r0["f_evals"]}
     else:
         per_step = {"matvec": r0["h_evals"], "pcg_update": r0["pcg_iters"], "pcg_dir": r0["pcg_iters"],
                     "eval": r0["f_evals"], "trial_init": gn}
+    # algorithmic bytes per launch of the streaming kernels (DESIGN.md §7 table)
     algo_bytes = {"matvec": 16 * Nn, "pcg_update": 28 * Nn, "pcg_dir": 16 * Nn, "eval": 16 * Nn + 8 * Nc,
                   "trial_init": 20 * Nn}
     share = {k: prof_warm[k] * per_step[k] / ms_per_step for k in per_step}
     dom = max(share, key=share.get)
-    traffic = None
-    try:
-        summ = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
-        traffic = summ.get("kernels", {}).get(dom, {}).get("dram_bytes_per_launch")
-    except Exception:
-        pass
     hbm_peak, peak_src = peaks()
-    out = {"kernel": dom, "kernel_share_of_step": share, "traffic": traffic,
+    out = {"kernel": dom, "kernel_share_of_step": share,
            "avg_launch_ms_cold_l2": prof_cold[dom], "avg_launch_ms_warm_l2": prof_warm[dom],
            "launches_per_step": per_step}
+    ncu = ncu_kernel_summary(args.config, dom)
+    out["traffic"] = ncu.get("dram_bytes_per_launch") if ncu else None
     if dom == "pcg_resident":
-        # Algorithmic bytes of the work one launch does (SURVEY §8(d4)): per PCG
-        # iteration matvec 24 + update 28 B/node, and the Armijo start 20 B/node
-        # (g, b read; b_old, b, q written).  The kernel keeps the PCG operands on
-        # chip (ncu DRAM bytes per launch = `traffic`), so frac > 1 means it beats
-        # the HBM roofline of any streaming PCG; the FP32-pipe view is kept below.
-        its = r0["pcg_iters"] / max(gn, 1)
-        byts = (52 * its + 20) * Nn
-        ach = byts / (prof_warm[dom] * 1e-3) / 1e9
+        # The resident PCG keeps p, M, et on chip (shared memory) and r, z in
+        # registers: its DRAM traffic is the per-launch in/out only, so it is not
+        # HBM-bound.  Its limit is the per-iteration dependency chain (p-halo
+        # exchange with the neighbour CTAs, two grid-wide all-reduces): the
+        # roofline is that chain's MEASURED floor -- the same launch running
+        # only the synchronisation, no arithmetic or data movement
+        # (hysco_profile_kernels slot 6) -- against the measured iteration time.
+        its = max(r0["pcg_iters"] / max(gn, 1), 1.0)
+        it_us = prof_warm[dom] * 1e3 / its
+        floor_us = prof_warm["resident_sync_floor"] * 1e3 / 10.0
         flops = RESIDENT_FLOPS_PER_NODE_ITER * Nn * its
         ach_f = flops / (prof_warm[dom] * 1e-3) / 1e12
-        out.update({"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
-                    "algorithmic_bytes_per_launch": byts, "peak_source": peak_src,
-                    "note": "on-chip-resident PCG: algorithmic bytes of 10 streaming PCG iterations + Armijo "
-                            "start vs the measured HBM peak; actual DRAM bytes per launch in `traffic` "
-                            "(DESIGN.md §7, §10)",
-                    "alu_view": {"achieved": ach_f, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
-                                 "frac": ach_f / FP32_PEAK_TFLOPS, "algorithmic_flops_per_launch": flops,
-                                 "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 x 1.965 GHz"}})
+        out.update({"bound": "latency", "achieved": it_us, "peak": floor_us, "unit": "us per PCG iteration",
+                    "frac": floor_us / it_us,
+                    "peak_source": "measured live: pcg_sync_floor_kernel, the resident launch's synchronisation "
+                                   "chain alone (DESIGN.md §10)",
+                    "note": "frac = floor / achieved (time-like: lower is better)",
+                    "physical": {
+                        "fp32_pipe": {"achieved_tflops": ach_f, "peak_tflops": FP32_PEAK_TFLOPS,
+                                      "frac": ach_f / FP32_PEAK_TFLOPS,
+                                      "flops_per_launch": flops, "peak_source": "148 SMs x 128 FP32 lanes x 2 x 1.965 GHz"},
+                        "dram": ({"bytes_per_launch": ncu["dram_bytes_per_launch"],
+                                  "achieved_gbs": ncu["dram_bytes_per_launch"] / (prof_warm[dom] * 1e-3) / 1e9,
+                                  "peak_gbs": hbm_peak,
+                                  "frac": ncu["dram_bytes_per_launch"] / (prof_warm[dom] * 1e-3) / 1e9 / hbm_peak}
+                                 if ncu and ncu.get("dram_bytes_per_launch") else None),
+                        "sm_throughput_frac": (ncu.get("sm_throughput_pct") / 100.0
+                                               if ncu and ncu.get("sm_throughput_pct") is not None else None),
+                        "source": "ncu --set full of this build (profiles/ncu_summary.json) for dram / sm; "
+                                  "fp32 from the live launch time"}})
+    elif dom == "pcg_l2":
+        # PCG state (p, dt, et, r, x, Hp) L2-resident across the launch: the
+        # bytes it moves per launch are the streaming kernels' (SURVEY §8(d4):
+        # per iteration matvec 16 + update 28 + direction 16 B/node, start and
+        # Armijo start 20 + 20 B/node), served by L2; the roofline is the
+        # MEASURED L2 bandwidth (l2_peak_gbs), DRAM traffic in `traffic`
+        its = max(r0["pcg_iters"] / max(gn, 1), 1.0)
+        byts = (60 * its + 40) * Nn
+        ach = byts / (prof_warm[dom] * 1e-3) / 1e9
+        l2pk = l2_peak_gbs()
+        out.update({"bound": "l2", "achieved": ach, "peak": l2pk["gbs"], "unit": "GB/s", "frac": ach / l2pk["gbs"],
+                    "algorithmic_bytes_per_launch": byts, "peak_source": l2pk["how"],
+                    "hbm_view": {"achieved_gbs": ach, "peak_gbs": hbm_peak, "frac": ach / hbm_peak,
+                                 "note": "algorithmic bytes over the HBM peak: > 1 means the kernel beats any "
+                                         "HBM-streaming PCG; not a physical fraction"},
+                    "us_per_iteration": prof_warm[dom] * 1e3 / its})
     else:
         ach = algo_bytes[dom] / (prof_cold[dom] * 1e-3) / 1e9
         out.update({"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
                     "algorithmic_bytes_per_launch": algo_bytes[dom], "peak_source": peak_src,
                     "achieved_warm_l2": algo_bytes[dom] / (prof_warm[dom] * 1e-3) / 1e9})
-    # the HBM-bound kernels of the step, for context
+    # whole step against HBM: SURVEY §8(d4) bytes of a streaming fixed 10 x 10 solve
+    step_bytes = (r0["pcg_iters"] * 52 + r0["f_evals"] * 32 + gn * 16 + 40) * Nn
+    out["step_view"] = {"algorithmic_bytes": step_bytes, "achieved_gbs": step_bytes / (ms_per_step * 1e-3) / 1e9,
+                        "frac_of_hbm_peak": step_bytes / (ms_per_step * 1e-3) / 1e9 / hbm_peak,
+                        "note": "SURVEY §8(d4) bytes a streaming implementation of the step must move, / step time"}
+    # the HBM-bound kernels of the step, for context (cold L2)
     out["hbm_kernels"] = {k: {"GBps_cold": algo_bytes[k] / (prof_cold[k] * 1e-3) / 1e9,
                               "frac_cold": algo_bytes[k] / (prof_cold[k] * 1e-3) / 1e9 / hbm_peak}
                           for k in ("eval", "trial_init", "matvec", "pcg_update", "pcg_dir")}
@@ -328,6 +417,9 @@ def run_hysco(args):
     clocks = clk.stop()
     step_ms = [a.elapsed_time(z) for a, z in ev]
     total_ms = float(np.sum(step_ms))
+    step_stats = {"median": float(np.median(step_ms)), "p10": float(np.percentile(step_ms, 10)),
+                  "p90": float(np.percentile(step_ms, 90)), "min": float(np.min(step_ms)),
+                  "max": float(np.max(step_ms))}
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -335,6 +427,24 @@ def run_hysco(args):
     value = world * B * args.steps / (total_max / 1e3)
     ms_per_step = total_max / args.steps
 
+    # correction quality of the timed result (pair 0): relative improvement of
+    # the SSD and the field-map error against the analytic b_true,
+    # everywhere and inside the object (I_true > 10 % of its max)
+    torch.cuda.synchronize(dev)
+    bh = b[0].double().cpu().numpy()
+    Tph, Tmh = Tp[0].double().cpu().numpy(), Tm[0].double().cpu().numpy()
+    p0 = pairs[0]
+    d0 = float(np.sum((p0.Ip.astype(np.float64) - p0.Im.astype(np.float64)) ** 2))
+    mask_c = p0.I_true > 0.1 * p0.I_true.max()
+    mask_n = np.zeros(bh.shape, bool)
+    mask_n[..., :-1] |= mask_c
+    mask_n[..., 1:] |= mask_c
+    quality = {"relative_improvement_pct": 100.0 * (1.0 - float(np.sum((Tph - Tmh) ** 2)) / d0),
+               "fieldmap_rel_l2_vs_true": float(np.linalg.norm(bh - p0.b_true) / np.linalg.norm(p0.b_true)),
+               "fieldmap_rel_l2_vs_true_in_object": float(np.linalg.norm((bh - p0.b_true)[mask_n]) /
+                                                          np.linalg.norm(p0.b_true[mask_n])),
+               "fieldmap_max_abs_err_mm_in_object": float(np.abs(bh - p0.b_true)[mask_n].max()),
+               "object_mask": "I_true > 0.1 max (cells; nodes touching them)", "pair": "rank 0, pair 0"}
     roofline = roofline_entry(H, ctx, args, reps[0], B, (n1, n2, n3), ms_per_step)
     r0 = reps[0]
     Nn, Nc = B * n1 * n2 * (n3 + 1), B * n1 * n2 * n3
@@ -372,11 +482,9 @@ def run_hysco(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        os.environ.setdefault("OMP_NUM_THREADS", "1")
-        spp, desc, _ = oracle_sample(pairs[0])
-        cpu = {"value": 1.0 / spp, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
-               "threads_note": "NumPy elementwise, single-threaded (OMP_NUM_THREADS=1)",
-               "host_cpus": os.cpu_count()}
+        spp, desc, wall = oracle_sample(pairs[0], oracle_planes_for(pairs[0], 15.0))
+        cpu = dict({"value": 1.0 / spp, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
+                    "sample_seconds": wall}, **host_info())
 
     H.hysco_destroy(ctx)
     if rank == 0:
@@ -384,6 +492,7 @@ def run_hysco(args):
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": dict(workload_desc(args.config, B, args), parallelism=f"dp{world} (independent pairs per rank)"),
+                "step_ms": step_stats, "quality": quality,
                 "clocks": clocks, "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
                 "cpu_baseline": cpu,
                 "solver": {k: r0[k] for k in ("gn_iters", "f_evals", "h_evals", "pcg_iters", "stop", "J")},
@@ -668,8 +777,23 @@ def run_slab(args):
         torch.distributed.destroy_process_group()
 
 
+def self_launch(args):
+    """`bench.py --gpus N` run without torchrun (no WORLD_SIZE): re-run this
+    script under torch.distributed.run with N ranks, one per GPU (the
+    contract's launch), and return its exit status."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     if args.impl == "reference":
         run_reference(args)
     elif args.stage == "lsq":

@@ -165,7 +165,10 @@ HYSCO_API hysco_status hysco_precond_solve(hysco_ctx ctx, int kind, const void* 
 /* Gauss-Newton with Jacobi-PCG and Armijo from b (in/out, device
  * nodes).  reports: host array [batch] (may be NULL).  The whole solve runs as
  * one CUDA graph with device-side control flow.  Returns HYSCO_INFEASIBLE
- * without iterating if some pair's b is infeasible. */
+ * without iterating if some pair's b is infeasible.  Afterwards the Hessian
+ * state is at the final b (hysco_hessvec may follow), except after a batch
+ * (batch > 1) solve on the on-chip-resident path, which runs the pairs one
+ * after another on shared scratch: call hysco_objective_grad first. */
 HYSCO_API hysco_status hysco_solve(hysco_ctx ctx, void* d_b_inout, const hysco_solve_opts* opts,
                          hysco_report* reports);
 
@@ -286,12 +289,19 @@ HYSCO_API int64_t hysco_last_launch_count(hysco_ctx ctx);
  * avg_ms (host, [HYSCO_NPROF]) receives the mean launch duration of:
  * [0] matvec (A5, PCG mode), [1] pcg_update (A6), [2] pcg_dir, [3] eval (A4),
  * [4] the on-chip-resident PCG (one launch = one GN step's 10-iteration PCG
- * solve per pair; -1 if this context does not use it), [5] trial_init (A7).
+ * solve per pair; -1 if this context does not use it), [5] trial_init (A7),
+ * [6] the resident PCG's synchronisation floor: a launch of the same grid and
+ * shared memory running only its per-iteration dependency chain (p-halo
+ * acquire, two tagged all-reduces, p-halo release) for 10 iterations, no
+ * arithmetic or data movement (-1 without the resident path), [7] the
+ * persistent L2-resident PCG (one launch = one GN step's 10-iteration PCG
+ * solve per pair, hysco_l2pcg.cuh; -1 if this context does not use it).
  * flush_l2 != 0: a 256 MiB scratch write (> the 126 MB L2) precedes every
  * timed launch (outside the events), i.e. cold-cache HBM-bound timings.
  * Clobbers the PCG scratch (not b, not the images). */
 enum { HYSCO_PROF_MATVEC = 0, HYSCO_PROF_UPDATE = 1, HYSCO_PROF_DIR = 2, HYSCO_PROF_EVAL = 3,
-       HYSCO_PROF_RESIDENT = 4, HYSCO_PROF_TRIAL = 5, HYSCO_NPROF = 6 };
+       HYSCO_PROF_RESIDENT = 4, HYSCO_PROF_TRIAL = 5, HYSCO_PROF_RES_SYNC = 6, HYSCO_PROF_L2PCG = 7,
+       HYSCO_NPROF = 8 };
 HYSCO_API hysco_status hysco_profile_kernels(hysco_ctx ctx, int32_t reps, int32_t flush_l2, double* avg_ms);
 
 /* ---- Multi-GPU slab decomposition along dim 1 (north_star:

@@ -83,8 +83,16 @@ struct hysco_ctx_s {
     unsigned* h_cond = nullptr;
     Ctl ctl{};
     int gx_nodes = 1, gx_mv = 1, gx_cells = 1, gx_eval = 1, gx_apply = 1, gx_ot = 1;
+    // launch view (PairView): the launchers address pairs [vp, vp + vb); the
+    // resident path runs a batch pair by pair (one pair's arrays stay in L2
+    // across its whole GN loop) with vb = 1 and the one-pair grids gx1
+    int vb = 1;
+    size_t vp = 0;
+    bool vshare = false;
+    bool last_per_pair = false;   // the last solve ran pair by pair on shared scratch
+    int gx1[6] = {1, 1, 1, 1, 1, 1};
     int nch = 5;              // 32-node chunks per column segment of the node kernels
-    size_t smem_eval = 0, smem_ot = 0;
+    size_t smem_eval = 0, smem_ot = 0, smem_apply = 0;
     bool state_valid = false;
     bool poisoned = false;
     bool no_graph = false;
@@ -105,6 +113,9 @@ struct hysco_ctx_s {
     float* res_pg = nullptr;     // ghost-padded global copy of p (halo source)
     float* res_x = nullptr;      // x of one pair in the padded resident layout
     float res_wi = 0.f, res_wj = 0.f;   // alpha hd / h1^2, alpha hd / h2^2 (in-plane Laplacian weights)
+    // persistent L2-resident PCG (hysco_l2pcg.cuh): one CTA per SM, shares res_part / res_flags
+    bool l2pcg = false;
+    int l2_grid = 0;
     // slab decomposition (multi-rank)
     size_t plane_off = 0;        // elements from a pair's buffer start to local plane 0
     int rank = 0, nranks = 1;
@@ -143,6 +154,10 @@ static hysco_status cuda_fail(hysco_ctx c, cudaError_t e, const char* what, int 
     } while (0)
 
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+static bool getenv_is1(const char* n) {
+    const char* e = getenv(n);
+    return e && e[0] == '1';
+}
 
 static SolveParams to_params(const hysco_solve_opts& o, const hysco_ot_opts& t) {
     SolveParams s{};
@@ -204,23 +219,27 @@ static int pick_nch(int P) { return P <= 64 ? 2 : P <= 128 ? 4 : P <= 160 ? 5 : 
 
 template <typename T>
 struct L {
-    static T* b(hysco_ctx c, int k) { return static_cast<T*>(c->buf[k]) + c->plane_off; }
+    // per-pair view: b is the pair's own; the scratch arrays are pair 0's,
+    // shared by the pairs run one after another (their L2 lines are reused)
+    static T* b(hysco_ctx c, int k) {
+        return static_cast<T*>(c->buf[k]) + c->plane_off + (k == B_B || !c->vshare ? c->vp : 0) * c->g.ps;
+    }
 
     // bold / q given: a TRIAL evaluation forms the retry b itself (no ls_retry launch)
     static void eval(hysco_ctx c, const SolveParams& sp, int mode, const T* bsrc, const T* bold = nullptr,
                      const T* q = nullptr) {
-        NCH_SWITCH(c->nch, eval_kernel<T, NCH><<<dim3(c->gx_eval, c->cfg.batch), 256, c->smem_eval, c->stream>>>(
+        NCH_SWITCH(c->nch, eval_kernel<T, NCH><<<dim3(c->gx_eval, c->vb), 256, c->smem_eval, c->stream>>>(
                                c->g, c->ctl, sp, mode, (const T*)c->Ip, (const T*)c->Im, bsrc, bold, q,
                                b(c, B_GRAD), b(c, B_DT), b(c, B_ET)));
     }
     static void pcg_init(hysco_ctx c) {
-        NCH_SWITCH(c->nch, pcg_init_kernel<T, NCH><<<dim3(c->gx_nodes, c->cfg.batch), 256, 0, c->stream>>>(
+        NCH_SWITCH(c->nch, pcg_init_kernel<T, NCH><<<dim3(c->gx_nodes, c->vb), 256, 0, c->stream>>>(
                                c->g, c->ctl, b(c, B_GRAD), b(c, B_DT), b(c, B_X), b(c, B_R), b(c, B_P)));
     }
     static void pcg_iter(hysco_ctx c, const SolveParams& sp) {
-        dim3 gr(c->gx_nodes, c->cfg.batch);
+        dim3 gr(c->gx_nodes, c->vb);
         NCH_SWITCH(c->nch,
-                   matvec_kernel<T, NCH, true><<<dim3(c->gx_mv, c->cfg.batch), 256, 0, c->stream>>>(
+                   matvec_kernel<T, NCH, true><<<dim3(c->gx_mv, c->vb), 256, 0, c->stream>>>(
                        c->g, c->ctl, b(c, B_DT), b(c, B_ET), b(c, B_P), b(c, B_HP));
                    pcg_update_kernel<T, NCH><<<gr, 256, 0, c->stream>>>(c->g, c->ctl, sp, b(c, B_DT), b(c, B_P),
                                                                        b(c, B_HP), b(c, B_X), b(c, B_R));
@@ -228,7 +247,7 @@ struct L {
                                                                     b(c, B_P)));
     }
     // block preconditioner (R20): factor once per GN step, solve per iteration
-    static dim3 gblk(hysco_ctx c) { return dim3((unsigned)((c->g.ncol + BLK_THREADS - 1) / BLK_THREADS), c->cfg.batch); }
+    static dim3 gblk(hysco_ctx c) { return dim3((unsigned)((c->g.ncol + BLK_THREADS - 1) / BLK_THREADS), c->vb); }
     static void bfac(hysco_ctx c, int need_active) {
         bfac_kernel<T><<<gblk(c), BLK_THREADS, 0, c->stream>>>(c->g, c->ctl, b(c, B_DT), b(c, B_ET), b(c, B_W),
                                                                b(c, B_F), need_active);
@@ -238,14 +257,14 @@ struct L {
     }
     static void pcg_init_blk(hysco_ctx c, const SolveParams& sp) {
         bfac(c, 1);
-        NCH_SWITCH(c->nch, pcg_blk_kernel<T, NCH, true><<<dim3(c->gx_nodes, c->cfg.batch), 256, 0, c->stream>>>(
+        NCH_SWITCH(c->nch, pcg_blk_kernel<T, NCH, true><<<dim3(c->gx_nodes, c->vb), 256, 0, c->stream>>>(
                                c->g, c->ctl, sp, b(c, B_GRAD), b(c, B_P), b(c, B_HP), b(c, B_X), b(c, B_R),
                                b(c, B_W), b(c, B_ET), b(c, B_F), b(c, B_TMP)));
     }
     static void pcg_iter_blk(hysco_ctx c, const SolveParams& sp) {
-        dim3 gr(c->gx_nodes, c->cfg.batch);
+        dim3 gr(c->gx_nodes, c->vb);
         NCH_SWITCH(c->nch,
-                   matvec_kernel<T, NCH, true><<<dim3(c->gx_mv, c->cfg.batch), 256, 0, c->stream>>>(
+                   matvec_kernel<T, NCH, true><<<dim3(c->gx_mv, c->vb), 256, 0, c->stream>>>(
                        c->g, c->ctl, b(c, B_DT), b(c, B_ET), b(c, B_P), b(c, B_HP));
                    pcg_blk_kernel<T, NCH, false><<<gr, 256, 0, c->stream>>>(
                        c->g, c->ctl, sp, b(c, B_GRAD), b(c, B_P), b(c, B_HP), b(c, B_X), b(c, B_R), b(c, B_W),
@@ -253,30 +272,30 @@ struct L {
                    pcg_dir_blk_kernel<T, NCH><<<gr, 256, 0, c->stream>>>(c->g, c->ctl, b(c, B_TMP), b(c, B_P)));
     }
     static void trial_init(hysco_ctx c) {
-        NCH_SWITCH(c->nch, trial_init_kernel<T, NCH><<<dim3(c->gx_nodes, c->cfg.batch), 256, 0, c->stream>>>(
+        NCH_SWITCH(c->nch, trial_init_kernel<T, NCH><<<dim3(c->gx_nodes, c->vb), 256, 0, c->stream>>>(
                                c->g, c->ctl, b(c, B_GRAD), b(c, B_X), b(c, B_B), b(c, B_BOLD)));
     }
     static void ls_body(hysco_ctx c, const SolveParams& sp) { eval(c, sp, EVAL_TRIAL, b(c, B_B), b(c, B_BOLD), b(c, B_X)); }
     static void matvec_plain(hysco_ctx c, const T* q, T* Hq) {
-        NCH_SWITCH(c->nch, matvec_kernel<T, NCH, false><<<dim3(c->gx_mv, c->cfg.batch), 256, 0, c->stream>>>(
+        NCH_SWITCH(c->nch, matvec_kernel<T, NCH, false><<<dim3(c->gx_mv, c->vb), 256, 0, c->stream>>>(
                                c->g, c->ctl, b(c, B_DT), b(c, B_ET), q, Hq));
     }
     static void diag(hysco_ctx c, T* out) {
-        NCH_SWITCH(c->nch, hess_diag_kernel<T, NCH><<<dim3(c->gx_nodes, c->cfg.batch), 256, 0, c->stream>>>(
+        NCH_SWITCH(c->nch, hess_diag_kernel<T, NCH><<<dim3(c->gx_nodes, c->vb), 256, 0, c->stream>>>(
                                c->g, c->ctl, b(c, B_DT), out));
     }
     static void apply(hysco_ctx c, const T* bsrc, T* Tp, T* Tm, T* bout = nullptr) {
-        apply_kernel<T><<<dim3(c->gx_apply, c->cfg.batch), 256, c->smem_eval, c->stream>>>(
+        apply_kernel<T><<<dim3(c->gx_apply, c->vb), 256, c->smem_apply, c->stream>>>(
             c->g, c->ctl, (const T*)c->Ip, (const T*)c->Im, bsrc, Tp, Tm, bout);
     }
     // OT init (+blur, guard) into buffer B_B
     static void ot(hysco_ctx c, const SolveParams& sp, int blur) {
         const T* Ip = (const T*)c->Ip;
         const T* Im = (const T*)c->Im;
-        dim3 gn(c->gx_nodes, c->cfg.batch);
-        ot_minmax_kernel<T><<<dim3(c->gx_cells, c->cfg.batch), 256, 0, c->stream>>>(c->g, c->ctl, sp, Ip, Im);
+        dim3 gn(c->gx_nodes, c->vb);
+        ot_minmax_kernel<T><<<dim3(c->gx_cells, c->vb), 256, 0, c->stream>>>(c->g, c->ctl, sp, Ip, Im);
         T* dst = blur ? b(c, B_TMP) : b(c, B_B);
-        ot_column_kernel<T><<<dim3(c->gx_ot, c->cfg.batch), 256, c->smem_ot, c->stream>>>(c->g, c->ctl, Ip, Im, dst);
+        ot_column_kernel<T><<<dim3(c->gx_ot, c->vb), 256, c->smem_ot, c->stream>>>(c->g, c->ctl, Ip, Im, dst);
         if (blur) {
             const double e = exp(-0.5), w0 = e / (1.0 + 2.0 * e), w1 = 1.0 / (1.0 + 2.0 * e);
             blur_axis_kernel<T, 1><<<gn, 256, 0, c->stream>>>(c->g, c->ctl, 0, w0, w1, b(c, B_TMP), b(c, B_R));
@@ -383,8 +402,10 @@ static void launch_resident(hysco_ctx c, const SolveParams& sp, int pair, float*
     at[0].val.cooperative = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;   // co-residency of all CTAs (the spin waits rely on it)
-    float* const* B = reinterpret_cast<float* const*>(c->buf);
-    const int nb = c->cfg.batch;
+    float* B[NBUF];
+    for (int k = 0; k < NBUF; k++)   // the view's first pair (scratch shared in a per-pair view, L<T>::b)
+        B[k] = static_cast<float*>(c->buf[k]) + (k == B_B || !c->vshare ? c->vp : 0) * c->g.ps;
+    const int nb = c->vb;
     if (sp.fixed) {
         RES_K_SWITCH(c->res_k, cudaLaunchKernelEx(&cfg, pcg_resident_kernel<RK, true>, c->g, c->ctl, sp, pair,
                                                   (const float*)B[B_GRAD], (const float*)B[B_DT],
@@ -398,6 +419,79 @@ static void launch_resident(hysco_ctx c, const SolveParams& sp, int pair, float*
                                                   c->res_part, c->res_flags, c->res_wi, c->res_wj, bcur, bold,
                                                   nb, (unsigned long long*)nullptr));
     }
+}
+
+// Persistent L2-resident PCG (hysco_l2pcg.cuh) for pair `pair` of the view.
+template <typename T>
+static void launch_l2pcg(hysco_ctx c, const SolveParams& sp, int pair) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(c->l2_grid, 1, 1);
+    cfg.blockDim = dim3(L2P_THREADS, 1, 1);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;   // co-residency of all CTAs (the spin waits rely on it)
+    T* B[NBUF];
+    for (int k = 0; k < NBUF; k++) B[k] = L<T>::b(c, k);
+    const int nb = c->vb;
+    NCH_SWITCH(c->nch, {
+        if (sp.fixed)
+            cudaLaunchKernelEx(&cfg, pcg_l2_kernel<T, NCH, true>, c->g, c->ctl, sp, pair, (const T*)B[B_GRAD],
+                               (const T*)B[B_DT], (const T*)B[B_ET], B[B_X], B[B_R], B[B_P], B[B_HP], B[B_B],
+                               B[B_BOLD], c->res_part, c->res_flags, nb);
+        else
+            cudaLaunchKernelEx(&cfg, pcg_l2_kernel<T, NCH, false>, c->g, c->ctl, sp, pair, (const T*)B[B_GRAD],
+                               (const T*)B[B_DT], (const T*)B[B_ET], B[B_X], B[B_R], B[B_P], B[B_HP], B[B_B],
+                               B[B_BOLD], c->res_part, c->res_flags, nb);
+    });
+}
+
+// Shared synchronisation buffers of the persistent PCG kernels (tagged
+// all-reduce partials, p-halo flags + launch counter).
+static bool alloc_persistent_sync(hysco_ctx ctx) {
+    if (ctx->res_part) return true;
+    const int G = ctx->nsm;
+    if (cudaMalloc(&ctx->res_part, sizeof(double) * 3 * RES_PART_DOUBLES) != cudaSuccess ||
+        cudaMalloc(&ctx->res_flags, sizeof(unsigned) * res_flags_words(G)) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    cudaMemset(ctx->res_part, 0, sizeof(double) * 3 * RES_PART_DOUBLES);
+    cudaMemset(ctx->res_flags, 0, sizeof(unsigned) * res_flags_words(G));
+    const unsigned first_launch = 1;      // tags of launch 0 would match the zeroed slots
+    cudaMemcpy(ctx->res_flags + (size_t)G * RES_FLAG_STRIDE, &first_launch, sizeof(unsigned), cudaMemcpyHostToDevice);
+    return true;
+}
+
+// The L2-resident persistent PCG, opt-in (HYSCO_L2PCG=1), when the
+// shared-memory one does not apply and every pair has >= 1 column per SM.
+// Measured at 7T (PCG working set 127 MB ~ the L2): 78 us per iteration,
+// no faster than the three streaming kernels (the per-column arithmetic,
+// not the launch boundaries, bounds both), so it is not the
+// default.  Not on slab contexts (their exchanges are host-driven).
+template <typename T>
+static void setup_l2pcg(hysco_ctx ctx) {
+    ctx->l2pcg = false;
+    const char* e = getenv("HYSCO_L2PCG");
+    if (!(e && e[0] == '1') || ctx->resident || ctx->g.slab) return;
+    const Geom& g = ctx->g;
+    const int G = ctx->nsm;
+    if (g.ncol < G || G * 2 > RES_RSTRIDE) return;
+    int occ = 0;
+    NCH_SWITCH(ctx->nch, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pcg_l2_kernel<T, NCH, true>,
+                                                                       L2P_THREADS, 0));
+    int occ2 = 0;
+    NCH_SWITCH(ctx->nch, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, pcg_l2_kernel<T, NCH, false>,
+                                                                       L2P_THREADS, 0));
+    if (occ < 1 || occ2 < 1 || !alloc_persistent_sync(ctx)) {
+        cudaGetLastError();
+        return;
+    }
+    ctx->l2_grid = G;
+    ctx->l2pcg = true;
 }
 
 // Decide whether the PCG state of one pair fits on chip.
@@ -426,6 +520,9 @@ static void setup_resident(hysco_ctx ctx) {
         if (err == cudaSuccess)
             err = cudaFuncSetAttribute(pcg_resident_kernel<RK, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
+        if (err == cudaSuccess)
+            err = cudaFuncSetAttribute(pcg_sync_floor_kernel<RK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
     });
     if (err != cudaSuccess) {
         cudaGetLastError();
@@ -440,17 +537,11 @@ static void setup_resident(hysco_ctx ctx) {
     }
     const size_t ghost = (res_ghost_pair_floats(g) * ctx->cfg.batch + res_ghost_slack_floats(k)) * sizeof(float);
     if (G * 2 > RES_RSTRIDE) return;   // replica layout of the partials (hysco_resident.cuh)
-    if (cudaMalloc(&ctx->res_part, sizeof(double) * 3 * RES_PART_DOUBLES) != cudaSuccess ||
-        cudaMalloc(&ctx->res_flags, sizeof(unsigned) * res_flags_words(G)) != cudaSuccess ||
-        cudaMalloc(&ctx->res_pg, ghost) != cudaSuccess ||
+    if (!alloc_persistent_sync(ctx) || cudaMalloc(&ctx->res_pg, ghost) != cudaSuccess ||
         cudaMalloc(&ctx->res_x, (size_t)g.ncol * res_pad(g.P) * sizeof(float)) != cudaSuccess) {
         cudaGetLastError();
         return;
     }
-    cudaMemset(ctx->res_part, 0, sizeof(double) * 3 * RES_PART_DOUBLES);
-    cudaMemset(ctx->res_flags, 0, sizeof(unsigned) * res_flags_words(G));
-    const unsigned first_launch = 1;      // tags of launch 0 would match the zeroed slots
-    cudaMemcpy(ctx->res_flags + (size_t)G * RES_FLAG_STRIDE, &first_launch, sizeof(unsigned), cudaMemcpyHostToDevice);
     cudaMemset(ctx->res_pg, 0, ghost);   // ghost planes stay zero forever
     ctx->res_k = k;
     ctx->res_wi = (float)(g.ahd * g.ih1sq);
@@ -787,9 +878,13 @@ static void pcg_step(Runner& r, const SolveParams& sp, bool unrolled) {
     const bool blk = sp.precond == HYSCO_PRECOND_PE_BLOCK;
     if (c->resident && !blk) {   // PCG + the Armijo start (trial_init) in one launch per pair
         r.seq([&] {
-            for (int p = 0; p < c->cfg.batch; p++)
+            for (int p = 0; p < c->vb; p++)
                 launch_resident(c, sp, p, reinterpret_cast<float*>(L<T>::b(c, B_B)),
                                 reinterpret_cast<float*>(L<T>::b(c, B_BOLD)));
+        });
+    } else if (c->l2pcg && !blk) {   // the same, state in L2 (hysco_l2pcg.cuh)
+        r.seq([&] {
+            for (int p = 0; p < c->vb; p++) launch_l2pcg<T>(c, sp, p);
         });
     } else if (unrolled) {   // fixed count: max_pcg iterations, kernels of finished pairs exit early
         r.seq([&] {
@@ -847,26 +942,84 @@ static void gn_sequence(Runner& r, const SolveParams& sp) {
     });
 }
 
+// Narrow the launchers to pair p of a batch context (scoped): buffers, images
+// and the per-pair control state (PairState, block partials, last-block
+// counters) are offset to pair p, grids are the one-pair grids.
+struct PairView {
+    hysco_ctx c;
+    Ctl ctl;
+    const void *Ip, *Im;
+    int gx[6];
+    PairView(hysco_ctx ctx, int p) : c(ctx), ctl(ctx->ctl), Ip(ctx->Ip), Im(ctx->Im) {
+        int* g[6] = {&c->gx_nodes, &c->gx_mv, &c->gx_cells, &c->gx_eval, &c->gx_apply, &c->gx_ot};
+        for (int k = 0; k < 6; k++) {
+            gx[k] = *g[k];
+            *g[k] = c->gx1[k];
+        }
+        c->vb = 1;
+        c->vp = (size_t)p;
+        c->vshare = true;
+        c->ctl.st += p;
+        c->ctl.part += (size_t)p * c->ctl.part_stride;
+        c->ctl.ctr += p;
+        c->Ip = static_cast<const char*>(Ip) + (size_t)p * c->g.Nc * c->esz;
+        c->Im = static_cast<const char*>(Im) + (size_t)p * c->g.Nc * c->esz;
+    }
+    ~PairView() {
+        int* g[6] = {&c->gx_nodes, &c->gx_mv, &c->gx_cells, &c->gx_eval, &c->gx_apply, &c->gx_ot};
+        for (int k = 0; k < 6; k++) *g[k] = gx[k];
+        c->vb = (int)c->cfg.batch;
+        c->vp = 0;
+        c->vshare = false;
+        c->ctl.st = ctl.st;
+        c->ctl.part = ctl.part;
+        c->ctl.ctr = ctl.ctr;
+        c->Ip = Ip;
+        c->Im = Im;
+    }
+};
+
 // Build (kind 1: solve b in place; kind 2: correct = OT + solve + apply) and
-// run either as a cached graph or host-looped.
+// run either as a cached graph or host-looped.  With the resident PCG a batch
+// runs pair by pair (the whole path of pair 0, then pair 1, ...): one pair's
+// node arrays (~130 MB at 3T) then stay L2-resident between its kernels, so
+// a pair costs the same in a batch as alone.
 template <typename T>
 static hysco_status run_path(hysco_ctx ctx, const GraphKey& key, void* b_io, void* b_out, void* Tp, void* Tm) {
-    const size_t nb = (size_t)ctx->cfg.batch * ctx->g.Nn * ctx->esz;
-    auto body = [&](Runner& r) {
+    const bool per_pair = (ctx->resident || ctx->l2pcg) && ctx->cfg.batch > 1 && key.sp.precond != HYSCO_PRECOND_PE_BLOCK &&
+                          !getenv_is1("HYSCO_BATCHED");
+    ctx->last_per_pair = per_pair;
+    auto body1 = [&](Runner& r) {
+        const size_t nb = (size_t)ctx->vb * ctx->g.Nn * ctx->esz;
+        const size_t on = ctx->vp * ctx->g.Nn * ctx->esz, oc = ctx->vp * ctx->g.Nc * ctx->esz;
+        char* bio = b_io ? static_cast<char*>(b_io) + on : nullptr;
+        char* bo = b_out ? static_cast<char*>(b_out) + on : nullptr;
+        T* tp = Tp ? reinterpret_cast<T*>(static_cast<char*>(Tp) + oc) : nullptr;
+        T* tm = Tm ? reinterpret_cast<T*>(static_cast<char*>(Tm) + oc) : nullptr;
         if (key.kind == 1) {
-            r.seq([&] { cudaMemcpyAsync(ctx->buf[B_B], b_io, nb, cudaMemcpyDeviceToDevice, ctx->stream); });
+            r.seq([&] { cudaMemcpyAsync(L<T>::b(ctx, B_B), bio, nb, cudaMemcpyDeviceToDevice, ctx->stream); });
         } else {
             r.seq([&] { L<T>::ot(ctx, key.sp, key.blur); });
         }
         gn_sequence<T>(r, key.sp);
         r.seq([&] {
             if (key.kind == 1) {
-                cudaMemcpyAsync(b_io, ctx->buf[B_B], nb, cudaMemcpyDeviceToDevice, ctx->stream);
+                cudaMemcpyAsync(bio, L<T>::b(ctx, B_B), nb, cudaMemcpyDeviceToDevice, ctx->stream);
             } else {
-                if (Tp || Tm) L<T>::apply(ctx, L<T>::b(ctx, B_B), (T*)Tp, (T*)Tm, (T*)b_out);   // also copies b out
-                else if (b_out) cudaMemcpyAsync(b_out, ctx->buf[B_B], nb, cudaMemcpyDeviceToDevice, ctx->stream);
+                if (tp || tm) L<T>::apply(ctx, L<T>::b(ctx, B_B), tp, tm, (T*)bo);   // also copies b out
+                else if (bo) cudaMemcpyAsync(bo, L<T>::b(ctx, B_B), nb, cudaMemcpyDeviceToDevice, ctx->stream);
             }
         });
+    };
+    auto body = [&](Runner& r) {
+        if (!per_pair) {
+            body1(r);
+            return;
+        }
+        for (int p = 0; p < ctx->cfg.batch; p++) {
+            PairView v(ctx, p);
+            body1(r);
+        }
     };
     CK(cudaMemsetAsync(ctx->launches, 0, sizeof(unsigned long long), ctx->stream));
     bool use_graph = !ctx->no_graph && !ctx->graph_broken;
@@ -958,13 +1111,14 @@ template <typename T>
 static hysco_status setup_typed(hysco_ctx ctx) {
     const Geom& g = ctx->g;
     const long long batch = ctx->cfg.batch;
-    ctx->smem_eval = eval_smem_elems(g.n3) * sizeof(T);   // eval tile staging (also covers apply's columns)
+    ctx->smem_eval = eval_smem_elems(g.n3) * sizeof(T);   // eval tile staging
+    ctx->smem_apply = apply_smem_elems(g.n3) * sizeof(T);
     ctx->smem_ot = (size_t)8 * 2 * g.P * sizeof(double);
-    if (ctx->smem_eval > 227 * 1024 || ctx->smem_ot > 227 * 1024)
+    if (ctx->smem_eval > 227 * 1024 || ctx->smem_ot > 227 * 1024 || ctx->smem_apply > 227 * 1024)
         return set_err(ctx, HYSCO_ERR_SHAPE, "n3 too large for the column-in-shared-memory kernels");
     NCH_SWITCH(pick_nch(g.P), CK(cudaFuncSetAttribute(eval_kernel<T, NCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                       (int)ctx->smem_eval)));
-    CK(cudaFuncSetAttribute(apply_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->smem_eval));
+    CK(cudaFuncSetAttribute(apply_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->smem_apply));
     CK(cudaFuncSetAttribute(ot_column_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->smem_ot));
     auto per_pair = [&](long long work_blocks, int occ) {
         long long cap = ((long long)ctx->nsm * occ + batch - 1) / batch;
@@ -985,10 +1139,23 @@ static hysco_status setup_typed(hysco_ctx ctx) {
     int occ_e = 1;
     NCH_SWITCH(ctx->nch, occ_e = occ_blocks(eval_kernel<T, NCH>, 256, ctx->smem_eval));
     ctx->gx_eval = per_pair((g.ncol + 7) / 8, occ_e);
-    ctx->gx_apply = per_pair((g.ncol + 7) / 8, occ_blocks(apply_kernel<T>, 256, ctx->smem_eval));
+    ctx->gx_apply = per_pair((g.ncol + 7) / 8, occ_blocks(apply_kernel<T>, 256, ctx->smem_apply));
     ctx->gx_ot = per_pair((g.ncol + 7) / 8, occ_blocks(ot_column_kernel<T>, 256, ctx->smem_ot));
+    // one-pair grids (PairView)
+    auto one = [&](long long work_blocks, int occ) {
+        long long gx = std::min<long long>(work_blocks, (long long)ctx->nsm * occ);
+        return (int)(gx < 1 ? 1 : gx);
+    };
+    ctx->gx1[0] = one((g.ncol + 7) / 8, occ_n);
+    ctx->gx1[1] = one((g.ncol + 7) / 8, occ_m);
+    ctx->gx1[2] = one((g.Nc + 255) / 256, occ_n);
+    ctx->gx1[3] = one((g.ncol + 7) / 8, occ_e);
+    ctx->gx1[4] = one((g.ncol + 7) / 8, occ_blocks(apply_kernel<T>, 256, ctx->smem_apply));
+    ctx->gx1[5] = one((g.ncol + 7) / 8, occ_blocks(ot_column_kernel<T>, 256, ctx->smem_ot));
+    ctx->vb = (int)batch;
     int mx = ctx->gx_nodes;
     for (int v : {ctx->gx_mv, ctx->gx_cells, ctx->gx_eval, ctx->gx_apply, ctx->gx_ot}) mx = v > mx ? v : mx;
+    for (int v : ctx->gx1) mx = v > mx ? v : mx;
     ctx->ctl.part_stride = mx * 8;
     return HYSCO_OK;
 }
@@ -1304,6 +1471,10 @@ static hysco_status create_impl(const hysco_config* cfg, const SlabSpec* slab, v
     ctx->ctl.red = ctx->red;
     ctx->ctl.defer = g.slab ? 1 : 0;     // slab runs are host-orchestrated: always decide after the allreduce
     if (!g.slab) setup_resident(ctx);
+    if (!g.slab) {
+        if (cfg->dtype == HYSCO_F64) setup_l2pcg<double>(ctx);
+        else setup_l2pcg<float>(ctx);
+    }
     *out = ctx;
     return HYSCO_OK;
 }
@@ -1647,7 +1818,9 @@ static hysco_status solve_common(hysco_ctx ctx, int kind, const hysco_ot_opts* o
     if (s != HYSCO_OK) return s;
     bool inf = false;
     fill_reports(ctx, reports, &inf);
-    ctx->state_valid = !inf;
+    // a pair-by-pair batch solve shares the Hessian scratch between pairs:
+    // only the last pair's parts survive, so hessvec needs a new objective_grad
+    ctx->state_valid = !inf && !ctx->last_per_pair;
     return inf ? HYSCO_INFEASIBLE : HYSCO_OK;
 }
 
@@ -1946,6 +2119,36 @@ static hysco_status profile_typed(hysco_ctx ctx, int reps, int flush_l2, double*
                                         reinterpret_cast<float*>(L<T>::b(ctx, B_HP)));
                     break;
                 }
+                case HYSCO_PROF_RES_SYNC: {
+                    if (!ctx->resident) break;
+                    cudaLaunchConfig_t cfg = {};
+                    cfg.gridDim = dim3(ctx->res_grid, 1, 1);
+                    cfg.blockDim = dim3(RES_THREADS, 1, 1);
+                    cfg.dynamicSmemBytes = ctx->res_smem;   // same occupancy as the real kernel
+                    cfg.stream = ctx->stream;
+                    cudaLaunchAttribute at[1];
+                    at[0].id = cudaLaunchAttributeCooperative;
+                    at[0].val.cooperative = 1;
+                    cfg.attrs = at;
+                    cfg.numAttrs = 1;
+                    RES_K_SWITCH(ctx->res_k, CK(cudaLaunchKernelEx(&cfg, pcg_sync_floor_kernel<RK>, ctx->g, 10,
+                                                                   ctx->res_part, ctx->res_flags)));
+                    break;
+                }
+                case HYSCO_PROF_L2PCG: {
+                    if (!ctx->l2pcg) break;
+                    SolveParams rp = sp;
+                    rp.max_pcg = 10;          // one GN step's PCG solve
+                    // the Armijo start writes b_old / b: point them at scratch for the profile
+                    void* sb = ctx->buf[B_B];
+                    void* so = ctx->buf[B_BOLD];
+                    ctx->buf[B_B] = ctx->buf[B_TMP];
+                    ctx->buf[B_BOLD] = ctx->buf[B_W];
+                    for (int p = 0; p < ctx->cfg.batch; p++) launch_l2pcg<T>(ctx, rp, p);
+                    ctx->buf[B_B] = sb;
+                    ctx->buf[B_BOLD] = so;
+                    break;
+                }
                 case HYSCO_PROF_TRIAL:
                     NCH_SWITCH(ctx->nch, trial_init_kernel<T, NCH><<<gr, 256, 0, ctx->stream>>>(
                                              ctx->g, ctx->ctl, L<T>::b(ctx, B_GRAD), L<T>::b(ctx, B_X),
@@ -1961,7 +2164,10 @@ static hysco_status profile_typed(hysco_ctx ctx, int reps, int flush_l2, double*
             CK(cudaEventElapsedTime(&ms, e0, e1));
             acc += ms;
         }
-        avg_ms[k] = (k == HYSCO_PROF_RESIDENT && !ctx->resident) ? -1.0 : acc / reps;
+        avg_ms[k] = ((k == HYSCO_PROF_RESIDENT || k == HYSCO_PROF_RES_SYNC) && !ctx->resident) ||
+                            (k == HYSCO_PROF_L2PCG && !ctx->l2pcg)
+                        ? -1.0
+                        : acc / reps;
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);

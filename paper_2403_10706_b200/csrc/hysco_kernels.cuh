@@ -146,6 +146,8 @@ __host__ __device__ inline size_t eval_smem_elems(int n3) {
     const size_t P = (size_t)n3 + 1;
     return (3 * EV_CT + 2) * P + 2 * EV_CT * ((size_t)n3 + 4);
 }
+// apply_kernel: per warp the column's I+, I- and b
+__host__ __device__ inline size_t apply_smem_elems(int n3) { return (size_t)EV_CT * (2 * (size_t)n3 + n3 + 1); }
 
 // One cell's two gathers (I+ at k + Ab/h3, I- at k - Ab/h3) from columns
 // padded with two zeros on each side (index kk clamped to [-2, n3] reads the
@@ -612,6 +614,7 @@ __global__ void __launch_bounds__(256) ot_column_kernel(Geom g, Ctl c, const T* 
 
 #include "hysco_nodes.cuh"
 #include "hysco_resident.cuh"
+#include "hysco_l2pcg.cuh"
 #include "hysco_admm.cuh"
 #include "hysco_lsq.cuh"
 

@@ -629,4 +629,44 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
     }
 }
 
+// Synchronisation floor of the resident PCG (profiling only, bench.py's
+// roofline): the same launch (grid, block, dynamic shared memory, hence one
+// CTA per SM) and per-iteration dependency chain of pcg_resident_kernel --
+// neighbourhood p-halo acquire, tagged all-reduce of p.Hp, tagged all-reduce
+// of (r.z, r.r), p-halo release -- with every slot loop (the arithmetic and
+// the shared / L2 data movement) removed.  Its time per iteration is the
+// latency floor a PCG iteration on this chip layout cannot go below.
+template <int K>
+__global__ void __launch_bounds__(RES_THREADS, 1)
+    pcg_sync_floor_kernel(Geom g, int iters, double* __restrict__ gpart, unsigned* __restrict__ flags) {
+    const long long c0 = (long long)blockIdx.x * g.ncol / gridDim.x;
+    const long long c1 = (long long)(blockIdx.x + 1) * g.ncol / gridDim.x;
+    const int n2 = g.n2;
+    const unsigned launch = *reinterpret_cast<volatile unsigned*>(flags + (size_t)gridDim.x * RES_FLAG_STRIDE);
+    const int blo = res_owner(c0 - n2 > 0 ? c0 - n2 : 0, g.ncol, gridDim.x);
+    const int bhi = res_owner(c1 - 1 + n2 < g.ncol ? c1 - 1 + n2 : g.ncol - 1, g.ncol, gridDim.x);
+    double* part0 = gpart;
+    double* part1 = gpart + RES_PART_DOUBLES;
+    double* part2 = gpart + 2 * RES_PART_DOUBLES;
+    double v2[2] = {1.0, 1.0}, t2[2];
+    halo_release(flags, res_tag(launch, 0));
+    reduce_publish<2>(v2, part0, res_tag(launch, 0));
+    reduce_collect<2>(part0, res_tag(launch, 0), t2);
+    for (int k = 0; k < iters; k++) {
+        halo_acquire(flags, blo, bhi, res_tag(launch, k));
+        double v1[1] = {t2[0]}, t1[1];
+        reduce_publish<1>(v1, part1, res_tag(launch, k));
+        reduce_collect<1>(part1, res_tag(launch, k), t1);
+        double v3[2] = {t1[0], t2[1]};
+        reduce_publish<2>(v3, part2, res_tag(launch, k));
+        reduce_collect<2>(part2, res_tag(launch, k), t2);
+        if (k + 1 < iters) halo_release(flags, res_tag(launch, k + 1));
+    }
+    double v4[2] = {t2[0], t2[1]}, t4[2];
+    reduce_publish<2, 0x2u>(v4, part0, res_tag(launch, 31));
+    reduce_collect<2, 0x2u>(part0, res_tag(launch, 31), t4);
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        *reinterpret_cast<volatile unsigned*>(flags + (size_t)gridDim.x * RES_FLAG_STRIDE) = launch + 1;
+}
+
 }  // namespace hysco

@@ -32,7 +32,8 @@ EXPORTED = ["hysco_default_solve_opts", "hysco_default_ot_opts", "hysco_default_
             # front-end (include/hysco_io.h)
             "hysco_nifti_info_read", "hysco_nifti_read", "hysco_nifti_write", "hysco_io_last_error", "hysco_pe_shape",
             "hysco_permute_pe", "hysco_fieldmap_cells", "hysco_fieldmap_cells_units"]
-PROF_NAMES = ["matvec", "pcg_update", "pcg_dir", "eval", "pcg_resident", "trial_init"]
+PROF_NAMES = ["matvec", "pcg_update", "pcg_dir", "eval", "pcg_resident", "trial_init", "resident_sync_floor",
+              "pcg_l2"]
 
 
 class HyscoError(RuntimeError):

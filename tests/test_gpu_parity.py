@@ -343,6 +343,7 @@ def test_resident_pcg_matches_streaming(monkeypatch, cfg, armijo):
     streaming PCG kernels compute the same iteration (reduction order aside)."""
     p = phantom.make_config(cfg) if isinstance(cfg, str) else phantom.make_pair(cfg, (1.25, 1.25, 1.25), 11)
     out = []
+    monkeypatch.setenv("HYSCO_L2PCG", "0")      # the streaming kernels, not the L2-resident PCG
     for nr in ("0", "1"):
         monkeypatch.setenv("HYSCO_NO_RESIDENT", nr)
         c = Ctx([p.Ip], [p.Im], p.h)
@@ -360,6 +361,40 @@ def test_resident_pcg_matches_streaming(monkeypatch, cfg, armijo):
     assert relS(r_res["J"], r_str["J"]) <= 1e-5
     # resident: one launch per GN step instead of pcg_init + 10 x (matvec, update, dir) + trial_init
     assert n_str - n_res == 10 * 31 and r_res["f_evals"] == r_str["f_evals"]
+
+
+L2_CASES = ["C1_16x16x8", (60, 40, 16), (50, 30, 15), (84, 37, 10), (400, 2, 10), (25, 8, 24)]
+
+
+@ARMIJO
+@pytest.mark.parametrize("dtype", [H.HYSCO_F32, H.HYSCO_F64], ids=["f32", "f64"])
+@pytest.mark.parametrize("cfg", L2_CASES, ids=[str(c) for c in L2_CASES])
+def test_l2_persistent_pcg_matches_streaming(monkeypatch, cfg, dtype, armijo):
+    """The persistent L2-resident PCG (hysco_l2pcg.cuh: one cooperative launch
+    per GN step, tagged all-reduces and p-halo flags between CTAs) and the
+    streaming PCG kernels compute the same iteration (fp64 sums in another
+    order): same decisions, field map and J to the kernel tolerance; and the
+    whole path against the oracle."""
+    p = phantom.make_config(cfg) if isinstance(cfg, str) else phantom.make_pair(cfg, (1.25, 1.25, 1.25), 11)
+    Ip, Im = rnd(p.Ip, dtype), rnd(p.Im, dtype)
+    monkeypatch.setenv("HYSCO_NO_RESIDENT", "1")
+    out = []
+    for l2 in ("1", "0"):
+        monkeypatch.setenv("HYSCO_L2PCG", l2)
+        c = Ctx([Ip], [Im], p.h, dtype)
+        b, Tp, Tm = c.nodes(), c.cells(), c.cells()
+        reps, _ = H.hysco_correct(c.ctx, b, Tp, Tm, solve_opts=H.default_solve_opts(armijo=armijo))
+        out.append((c.np(b)[0], c.np(Tp)[0], reps[0], H.hysco_last_launch_count(c.ctx)))
+        c.close()
+    (b_l2, T_l2, r_l2, n_l2), (b_s, T_s, r_s, n_s) = out
+    keys = ("pcg_iters", "h_evals", "gn_iters", "f_evals", "ls_halvings")
+    assert tuple(r_l2[k] for k in keys) == tuple(r_s[k] for k in keys)
+    tol = 1e-5 if dtype == H.HYSCO_F32 else 1e-11
+    assert rel(b_l2, b_s) <= tol and relS(r_l2["J"], r_s["J"]) <= tol
+    assert n_s - n_l2 == r_s["gn_iters"] * 31          # one launch per GN step instead of 32
+    _, bref, Tpr, _, rep = O.correct_pair(Ip, Im, p.h, armijo=bool(armijo))
+    assert r_l2["f_evals"] == rep["f_evals"]
+    assert rel(b_l2, bref) <= TOL[dtype]["solve"] and rel(T_l2, Tpr) <= TOL[dtype]["solve"]
 
 
 def test_repeat_calls_deterministic_and_host_entry_equal():
@@ -645,4 +680,28 @@ def test_admm_batch_paper_stop_per_pair_vs_oracle():
         assert reps[k]["iters"] == its[k] and reps[k]["converged"] == 1
         assert abs(reps[k]["rho"] - refs[k][2]["rho_final"]) <= 1e-12 * refs[k][2]["rho_final"]
         assert rel(got[k], refs[k][0]) <= 1e-6      # ~45 coupled iterations (fp64 drift, see test_admm_fixed_parity)
+    c.close()
+
+
+@pytest.mark.parametrize("armijo", [1, 0], ids=["armijo", "fullstep"])
+def test_resident_batch_runs_pair_by_pair_equal_to_single(armijo):
+    """A batch on the resident path runs pair by pair (PairView: each pair's
+    whole path, its arrays L2-resident): every pair's result is bitwise the
+    single-pair context's, and the batched-launch variant (HYSCO_BATCHED=1)
+    agrees to the kernel tolerance."""
+    shape, h = (60, 40, 16), (1.25, 1.25, 1.25)
+    pairs = [phantom.make_pair(shape, h, 70 + k) for k in range(3)]
+    so = H.default_solve_opts(armijo=armijo)
+    c = Ctx([p.Ip for p in pairs], [p.Im for p in pairs], h)
+    b, Tp, Tm = c.nodes(), c.cells(), c.cells()
+    reps, inf = H.hysco_correct(c.ctx, b, Tp, Tm, solve_opts=so, batch=3)
+    n = H.hysco_last_launch_count(c.ctx)
+    assert not inf and n < 3 * 100
+    for k, p in enumerate(pairs):
+        c1 = Ctx([p.Ip], [p.Im], h)
+        b1, Tp1, Tm1 = c1.nodes(), c1.cells(), c1.cells()
+        r1, _ = H.hysco_correct(c1.ctx, b1, Tp1, Tm1, solve_opts=so)
+        assert np.array_equal(c.np(b)[k], c1.np(b1)[0]) and np.array_equal(c.np(Tm)[k], c1.np(Tm1)[0])
+        assert reps[k]["J"] == r1[0]["J"] and reps[k]["f_evals"] == r1[0]["f_evals"]
+        c1.close()
     c.close()
