@@ -279,17 +279,23 @@ def roofline_entry(H, ctx, args, r0, B, shape, ms_per_step):
     Nn, Nc = B * n1 * n2 * (n3 + 1), B * n1 * n2 * n3
     resident = prof_warm["pcg_resident"] > 0
     l2pcg = prof_warm.get("pcg_l2", -1) > 0
+    flat = prof_warm.get("pcg_dirmv", -1) > 0
     gn = r0["gn_iters"]
     if resident:   # one cooperative launch per GN step runs all PCG iterations and the Armijo start
         per_step = {"pcg_resident": gn, "eval": r0["f_evals"]}
     elif l2pcg:    # the same with the PCG state in L2 (hysco_l2pcg.cuh)
         per_step = {"pcg_l2": gn, "eval": r0["f_evals"]}
+    elif flat:     # two vectorised launches per PCG iteration (hysco_flat.cuh)
+        per_step = {"pcg_dirmv": r0["h_evals"], "pcg_upd": r0["pcg_iters"], "eval": r0["f_evals"],
+                    "trial_init": gn}
     else:
         per_step = {"matvec": r0["h_evals"], "pcg_update": r0["pcg_iters"], "pcg_dir": r0["pcg_iters"],
                     "eval": r0["f_evals"], "trial_init": gn}
-    # algorithmic bytes per launch of the streaming kernels (DESIGN.md §7 table)
+    # algorithmic bytes per launch of the streaming kernels (DESIGN.md §7 table);
+    # flat form: dirmv reads z, p_old, dt, et, x and writes p, Hp, x; upd reads
+    # r, Hp, dt and writes r, z; its Armijo start also reads the last p
     algo_bytes = {"matvec": 16 * Nn, "pcg_update": 28 * Nn, "pcg_dir": 16 * Nn, "eval": 16 * Nn + 8 * Nc,
-                  "trial_init": 20 * Nn}
+                  "trial_init": (28 if flat else 20) * Nn, "pcg_dirmv": 32 * Nn, "pcg_upd": 20 * Nn}
     share = {k: prof_warm[k] * per_step[k] / ms_per_step for k in per_step}
     dom = max(share, key=share.get)
     hbm_peak, peak_src = peaks()
@@ -358,7 +364,9 @@ def roofline_entry(H, ctx, args, r0, B, shape, ms_per_step):
     # the HBM-bound kernels of the step, for context (cold L2)
     out["hbm_kernels"] = {k: {"GBps_cold": algo_bytes[k] / (prof_cold[k] * 1e-3) / 1e9,
                               "frac_cold": algo_bytes[k] / (prof_cold[k] * 1e-3) / 1e9 / hbm_peak}
-                          for k in ("eval", "trial_init", "matvec", "pcg_update", "pcg_dir")}
+                          for k in (("eval", "trial_init", "pcg_dirmv", "pcg_upd") if flat else
+                                    ("eval", "trial_init", "matvec", "pcg_update", "pcg_dir"))
+                          if prof_cold.get(k, -1) > 0}
     return out
 
 

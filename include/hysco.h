@@ -295,13 +295,19 @@ HYSCO_API int64_t hysco_last_launch_count(hysco_ctx ctx);
  * acquire, two tagged all-reduces, p-halo release) for 10 iterations, no
  * arithmetic or data movement (-1 without the resident path), [7] the
  * persistent L2-resident PCG (one launch = one GN step's 10-iteration PCG
- * solve per pair, hysco_l2pcg.cuh; -1 if this context does not use it).
+ * solve per pair, hysco_l2pcg.cuh; -1 if this context does not use it),
+ * [8] pcg_dirmv and [9] pcg_upd: the two launches of a streaming PCG
+ * iteration in the flat vectorised form (hysco_flat.cuh: direction + deferred
+ * x update + matvec + p.Hp; residual update + preconditioner + r.z, r.r);
+ * -1 where this context runs the three-kernel form.  With the flat form [5]
+ * times its Armijo start (trial_flat_kernel, which also adds the last
+ * direction's deferred x update).
  * flush_l2 != 0: a 256 MiB scratch write (> the 126 MB L2) precedes every
  * timed launch (outside the events), i.e. cold-cache HBM-bound timings.
  * Clobbers the PCG scratch (not b, not the images). */
 enum { HYSCO_PROF_MATVEC = 0, HYSCO_PROF_UPDATE = 1, HYSCO_PROF_DIR = 2, HYSCO_PROF_EVAL = 3,
        HYSCO_PROF_RESIDENT = 4, HYSCO_PROF_TRIAL = 5, HYSCO_PROF_RES_SYNC = 6, HYSCO_PROF_L2PCG = 7,
-       HYSCO_NPROF = 8 };
+       HYSCO_PROF_DIRMV = 8, HYSCO_PROF_UPD = 9, HYSCO_NPROF = 10 };
 HYSCO_API hysco_status hysco_profile_kernels(hysco_ctx ctx, int32_t reps, int32_t flush_l2, double* avg_ms);
 
 /* ---- Multi-GPU slab decomposition along dim 1 (north_star:

@@ -48,6 +48,7 @@ struct hysco_ctx_s {
     const void* Ip = nullptr;
     const void* Im = nullptr;
     void* buf[NBUF] = {};
+    void* raw[NBUF] = {};     // allocations: buf[k] = raw[k] + FLAT_GUARD elements (hysco_flat.cuh)
     void* own_Ip = nullptr;   // host-entry image copies
     void* own_Im = nullptr;
     void* own_Tp = nullptr;   // host-entry corrected images
@@ -82,7 +83,13 @@ struct hysco_ctx_s {
     unsigned* dcond = nullptr;
     unsigned* h_cond = nullptr;
     Ctl ctl{};
-    int gx_nodes = 1, gx_mv = 1, gx_cells = 1, gx_eval = 1, gx_apply = 1, gx_ot = 1;
+    int gx_nodes = 1, gx_mv = 1, gx_cells = 1, gx_eval = 1, gx_apply = 1, gx_ot = 1, gx_flat = 1, gx_dmv = 1;
+    // streaming PCG in the flat vectorised two-launch form (hysco_flat.cuh);
+    // single-context paths with P >= the vector width (HYSCO_NO_FLAT=1: three-kernel form)
+    bool flat = false;
+    int mr_njb = 1, mr_c = 1;   // plane-march F1 tiling (pcg_march_kernel)
+    MarchPlan mr_plan{};
+    size_t smem_mr = 0;
     // launch view (PairView): the launchers address pairs [vp, vp + vb); the
     // resident path runs a batch pair by pair (one pair's arrays stay in L2
     // across its whole GN loop) with vb = 1 and the one-pair grids gx1
@@ -90,7 +97,7 @@ struct hysco_ctx_s {
     size_t vp = 0;
     bool vshare = false;
     bool last_per_pair = false;   // the last solve ran pair by pair on shared scratch
-    int gx1[6] = {1, 1, 1, 1, 1, 1};
+    int gx1[8] = {1, 1, 1, 1, 1, 1, 1, 1};
     int nch = 5;              // 32-node chunks per column segment of the node kernels
     size_t smem_eval = 0, smem_ot = 0, smem_apply = 0;
     bool state_valid = false;
@@ -270,6 +277,45 @@ struct L {
                        c->g, c->ctl, sp, b(c, B_GRAD), b(c, B_P), b(c, B_HP), b(c, B_X), b(c, B_R), b(c, B_W),
                        b(c, B_ET), b(c, B_F), b(c, B_TMP));
                    pcg_dir_blk_kernel<T, NCH><<<gr, 256, 0, c->stream>>>(c->g, c->ctl, b(c, B_TMP), b(c, B_P)));
+    }
+    // flat two-launch PCG (hysco_flat.cuh): z in B_TMP, p double-buffered in B_P / B_W
+    // (B_F holds M = diag(H_J), formed by the PCG start)
+    static void pcg_init_flat(hysco_ctx c) {
+        pcg_init_flat_kernel<T><<<dim3(c->gx_flat, c->vb), 256, 0, c->stream>>>(
+            c->g, c->ctl, b(c, B_GRAD), b(c, B_DT), b(c, B_X), b(c, B_R), b(c, B_TMP), b(c, B_F));
+    }
+    // first iteration (p_0 = z) and later ones are separate instantiations; the
+    // unrolled form launches the one it needs, the WHILE body both (the other exits)
+    template <bool FIRST, int MS>
+    static void march_ms_t(hysco_ctx c) {
+        pcg_march_kernel<T, FIRST, MS><<<dim3(c->gx_dmv, c->vb), MARCH_THREADS, c->smem_mr, c->stream>>>(
+            c->g, c->ctl, c->mr_njb, c->mr_c, c->mr_plan, b(c, B_DT), b(c, B_ET), b(c, B_TMP), b(c, B_P), b(c, B_W),
+            b(c, B_HP), b(c, B_X));
+    }
+    template <bool FIRST>
+    static void march(hysco_ctx c) {
+        switch (c->mr_plan.ms) {
+            case 2: march_ms_t<FIRST, 2>(c); break;
+            case 4: march_ms_t<FIRST, 4>(c); break;
+            case 8: march_ms_t<FIRST, 8>(c); break;
+            default: march_ms_t<FIRST, 12>(c); break;
+        }
+    }
+    static void pcg_dirmv(hysco_ctx c, bool first) {
+        if (first) march<true>(c);
+        else march<false>(c);
+    }
+    static void pcg_upd(hysco_ctx c, const SolveParams& sp) {
+        pcg_upd_kernel<T><<<dim3(c->gx_flat, c->vb), 256, 0, c->stream>>>(c->g, c->ctl, sp, b(c, B_F), b(c, B_HP),
+                                                                         b(c, B_R), b(c, B_TMP));
+    }
+    static void pcg_iter_flat(hysco_ctx c, const SolveParams& sp, bool first) {
+        pcg_dirmv(c, first);
+        pcg_upd(c, sp);
+    }
+    static void trial_flat(hysco_ctx c, T* bdst, T* bold) {
+        trial_flat_kernel<T><<<dim3(c->gx_flat, c->vb), 256, 0, c->stream>>>(c->g, c->ctl, b(c, B_GRAD), b(c, B_X),
+                                                                            b(c, B_P), b(c, B_W), bdst, bold);
     }
     static void trial_init(hysco_ctx c) {
         NCH_SWITCH(c->nch, trial_init_kernel<T, NCH><<<dim3(c->gx_nodes, c->vb), 256, 0, c->stream>>>(
@@ -886,6 +932,24 @@ static void pcg_step(Runner& r, const SolveParams& sp, bool unrolled) {
         r.seq([&] {
             for (int p = 0; p < c->vb; p++) launch_l2pcg<T>(c, sp, p);
         });
+    } else if (c->flat && !blk) {   // two vectorised launches per iteration (hysco_flat.cuh)
+        if (unrolled) {
+            r.seq([&] {
+                L<T>::pcg_init_flat(c);
+                for (int k = 0; k < sp.max_pcg; k++) L<T>::pcg_iter_flat(c, sp, k == 0);
+                L<T>::trial_flat(c, L<T>::b(c, B_B), L<T>::b(c, B_BOLD));
+            });
+        } else {
+            r.handle(COND_PCG);
+            // the first iteration (p_0 = z) outside the loop; its kernels exit
+            // at once if the PCG start found nothing to do
+            r.seq([&] {
+                L<T>::pcg_init_flat(c);
+                L<T>::pcg_iter_flat(c, sp, true);
+            });
+            r.loop(COND_PCG, [&] { r.seq([&] { L<T>::pcg_iter_flat(c, sp, false); }); });
+            r.seq([&] { L<T>::trial_flat(c, L<T>::b(c, B_B), L<T>::b(c, B_BOLD)); });
+        }
     } else if (unrolled) {   // fixed count: max_pcg iterations, kernels of finished pairs exit early
         r.seq([&] {
             if (blk) L<T>::pcg_init_blk(c, sp);
@@ -949,10 +1013,10 @@ struct PairView {
     hysco_ctx c;
     Ctl ctl;
     const void *Ip, *Im;
-    int gx[6];
+    int gx[8];
     PairView(hysco_ctx ctx, int p) : c(ctx), ctl(ctx->ctl), Ip(ctx->Ip), Im(ctx->Im) {
-        int* g[6] = {&c->gx_nodes, &c->gx_mv, &c->gx_cells, &c->gx_eval, &c->gx_apply, &c->gx_ot};
-        for (int k = 0; k < 6; k++) {
+        int* g[8] = {&c->gx_nodes, &c->gx_mv, &c->gx_cells, &c->gx_eval, &c->gx_apply, &c->gx_ot, &c->gx_flat, &c->gx_dmv};
+        for (int k = 0; k < 8; k++) {
             gx[k] = *g[k];
             *g[k] = c->gx1[k];
         }
@@ -966,8 +1030,8 @@ struct PairView {
         c->Im = static_cast<const char*>(Im) + (size_t)p * c->g.Nc * c->esz;
     }
     ~PairView() {
-        int* g[6] = {&c->gx_nodes, &c->gx_mv, &c->gx_cells, &c->gx_eval, &c->gx_apply, &c->gx_ot};
-        for (int k = 0; k < 6; k++) *g[k] = gx[k];
+        int* g[8] = {&c->gx_nodes, &c->gx_mv, &c->gx_cells, &c->gx_eval, &c->gx_apply, &c->gx_ot, &c->gx_flat, &c->gx_dmv};
+        for (int k = 0; k < 8; k++) *g[k] = gx[k];
         c->vb = (int)c->cfg.batch;
         c->vp = 0;
         c->vshare = false;
@@ -1140,6 +1204,46 @@ static hysco_status setup_typed(hysco_ctx ctx) {
     NCH_SWITCH(ctx->nch, occ_e = occ_blocks(eval_kernel<T, NCH>, 256, ctx->smem_eval));
     ctx->gx_eval = per_pair((g.ncol + 7) / 8, occ_e);
     ctx->gx_apply = per_pair((g.ncol + 7) / 8, occ_blocks(apply_kernel<T>, 256, ctx->smem_apply));
+    const long long flat_blocks = (g.Nn / FlatVec<T>::V + 2 + 255) / 256;
+    int occ_f = occ_blocks(pcg_upd_kernel<T>, 256, 0);
+    occ_f = std::min(occ_f, occ_blocks(pcg_init_flat_kernel<T>, 256, 0));
+    occ_f = std::min(occ_f, occ_blocks(trial_flat_kernel<T>, 256, 0));
+    ctx->gx_flat = per_pair(flat_blocks, occ_f);
+    ctx->flat = g.P >= FlatVec<T>::V && !getenv_is1("HYSCO_NO_FLAT");
+    {   // plane-march F1 (pcg_march_kernel): tiles of <= 16 columns, 5 bulk-copy stages in
+        // <= 220 KB of shared memory (one CTA per SM), plane chunks for one wave of CTAs
+        const size_t cap = 220 * 1024;
+        int wmax = std::min(g.n2, 16);
+        auto fits = [&](int w) {
+            return march_ms<T>(w, g.P, MARCH_THREADS) > 0 && march_smem_bytes<T>(march_plan<T>(w, g.P, 5)) <= cap;
+        };
+        while (wmax > 0 && !fits(wmax)) wmax--;
+        if (wmax == 0) {
+            ctx->flat = false;
+        } else {
+            ctx->mr_njb = (g.n2 + wmax - 1) / wmax;
+            wmax = (g.n2 + ctx->mr_njb - 1) / ctx->mr_njb;
+            ctx->mr_plan = march_plan<T>(wmax, g.P, 5);
+            ctx->mr_plan.ms = march_ms<T>(wmax, g.P, MARCH_THREADS);
+            ctx->smem_mr = march_smem_bytes<T>(ctx->mr_plan);
+            auto attr = [&](auto kern) {
+                return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->smem_mr);
+            };
+            CK(attr(pcg_march_kernel<T, true, 2>));
+            CK(attr(pcg_march_kernel<T, false, 2>));
+            CK(attr(pcg_march_kernel<T, true, 4>));
+            CK(attr(pcg_march_kernel<T, false, 4>));
+            CK(attr(pcg_march_kernel<T, true, 8>));
+            CK(attr(pcg_march_kernel<T, false, 8>));
+            CK(attr(pcg_march_kernel<T, true, 12>));
+            CK(attr(pcg_march_kernel<T, false, 12>));
+            long long ncb = ctx->mr_njb <= ctx->nsm ? std::max(1, ctx->nsm / ctx->mr_njb) : 1;
+            ncb = std::min<long long>(ncb, g.n1);
+            ctx->mr_c = (int)((g.n1 + ncb - 1) / ncb);
+            ncb = (g.n1 + ctx->mr_c - 1) / ctx->mr_c;
+            ctx->gx_dmv = (int)(ctx->mr_njb * ncb);
+        }
+    }
     ctx->gx_ot = per_pair((g.ncol + 7) / 8, occ_blocks(ot_column_kernel<T>, 256, ctx->smem_ot));
     // one-pair grids (PairView)
     auto one = [&](long long work_blocks, int occ) {
@@ -1152,9 +1256,11 @@ static hysco_status setup_typed(hysco_ctx ctx) {
     ctx->gx1[3] = one((g.ncol + 7) / 8, occ_e);
     ctx->gx1[4] = one((g.ncol + 7) / 8, occ_blocks(apply_kernel<T>, 256, ctx->smem_apply));
     ctx->gx1[5] = one((g.ncol + 7) / 8, occ_blocks(ot_column_kernel<T>, 256, ctx->smem_ot));
+    ctx->gx1[6] = one(flat_blocks, occ_f);
+    ctx->gx1[7] = ctx->gx_dmv;   // independent of the batch (the tiling is per pair)
     ctx->vb = (int)batch;
     int mx = ctx->gx_nodes;
-    for (int v : {ctx->gx_mv, ctx->gx_cells, ctx->gx_eval, ctx->gx_apply, ctx->gx_ot}) mx = v > mx ? v : mx;
+    for (int v : {ctx->gx_mv, ctx->gx_cells, ctx->gx_eval, ctx->gx_apply, ctx->gx_ot, ctx->gx_flat, ctx->gx_dmv}) mx = v > mx ? v : mx;
     for (int v : ctx->gx1) mx = v > mx ? v : mx;
     ctx->ctl.part_stride = mx * 8;
     return HYSCO_OK;
@@ -1432,8 +1538,12 @@ static hysco_status create_impl(const hysco_config* cfg, const SlabSpec* slab, v
         }
         return true;
     };
-    for (int k = 0; k < NBUF; k++)
-        if (!dalloc(&ctx->buf[k], nn)) return bail(HYSCO_ERR_NOMEM);
+    for (int k = 0; k < NBUF; k++) {   // FLAT_GUARD elements of slack on both sides (hysco_flat.cuh)
+        if (!dalloc(&ctx->raw[k], nn + 2 * FLAT_GUARD * ctx->esz)) return bail(HYSCO_ERR_NOMEM);
+        cudaMemset(ctx->raw[k], 0, FLAT_GUARD * ctx->esz);
+        cudaMemset(static_cast<char*>(ctx->raw[k]) + FLAT_GUARD * ctx->esz + nn, 0, FLAT_GUARD * ctx->esz);
+        ctx->buf[k] = static_cast<char*>(ctx->raw[k]) + FLAT_GUARD * ctx->esz;
+    }
     if (!dalloc(&ctx->own_Ip, nc) || !dalloc(&ctx->own_Im, nc) || !dalloc(&ctx->own_Tp, nc) ||
         !dalloc(&ctx->own_Tm, nc))
         return bail(HYSCO_ERR_NOMEM);
@@ -1470,6 +1580,7 @@ static hysco_status create_impl(const hysco_config* cfg, const SlabSpec* slab, v
     ctx->ctl.use_graph = 0;
     ctx->ctl.red = ctx->red;
     ctx->ctl.defer = g.slab ? 1 : 0;     // slab runs are host-orchestrated: always decide after the allreduce
+    if (g.slab) ctx->flat = false;       // the flat kernels decide in their last block (no defer mode)
     if (!g.slab) setup_resident(ctx);
     if (!g.slab) {
         if (cfg->dtype == HYSCO_F64) setup_l2pcg<double>(ctx);
@@ -2150,9 +2261,19 @@ static hysco_status profile_typed(hysco_ctx ctx, int reps, int flush_l2, double*
                     break;
                 }
                 case HYSCO_PROF_TRIAL:
+                    if (ctx->flat) {
+                        L<T>::trial_flat(ctx, L<T>::b(ctx, B_TMP), L<T>::b(ctx, B_BOLD));
+                        break;
+                    }
                     NCH_SWITCH(ctx->nch, trial_init_kernel<T, NCH><<<gr, 256, 0, ctx->stream>>>(
                                              ctx->g, ctx->ctl, L<T>::b(ctx, B_GRAD), L<T>::b(ctx, B_X),
                                              L<T>::b(ctx, B_TMP), L<T>::b(ctx, B_BOLD)));
+                    break;
+                case HYSCO_PROF_DIRMV:
+                    if (ctx->flat) L<T>::pcg_dirmv(ctx, false);
+                    break;
+                case HYSCO_PROF_UPD:
+                    if (ctx->flat) L<T>::pcg_upd(ctx, sp);
                     break;
                 default:
                     L<T>::eval(ctx, sp, EVAL_PLAIN, L<T>::b(ctx, B_B));
@@ -2165,7 +2286,8 @@ static hysco_status profile_typed(hysco_ctx ctx, int reps, int flush_l2, double*
             acc += ms;
         }
         avg_ms[k] = ((k == HYSCO_PROF_RESIDENT || k == HYSCO_PROF_RES_SYNC) && !ctx->resident) ||
-                            (k == HYSCO_PROF_L2PCG && !ctx->l2pcg)
+                            (k == HYSCO_PROF_L2PCG && !ctx->l2pcg) ||
+                            ((k == HYSCO_PROF_DIRMV || k == HYSCO_PROF_UPD) && !ctx->flat)
                         ? -1.0
                         : acc / reps;
     }
@@ -2197,7 +2319,7 @@ hysco_status hysco_destroy(hysco_ctx ctx) {
     if (ctx->exec) cudaGraphExecDestroy(ctx->exec);
     if (ctx->graph) cudaGraphDestroy(ctx->graph);
     for (int k = 0; k < NBUF; k++)
-        if (ctx->buf[k]) cudaFree(ctx->buf[k]);
+        if (ctx->raw[k]) cudaFree(ctx->raw[k]);
     for (void* p : {ctx->own_Ip, ctx->own_Im, ctx->own_Tp, ctx->own_Tm, (void*)ctx->st, (void*)ctx->part,
                     (void*)ctx->ctr, (void*)ctx->gctr, (void*)ctx->launches, (void*)ctx->dcond})
         if (p) cudaFree(p);

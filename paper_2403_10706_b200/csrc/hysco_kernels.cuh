@@ -614,6 +614,7 @@ __global__ void __launch_bounds__(256) ot_column_kernel(Geom g, Ctl c, const T* 
 
 #include "hysco_nodes.cuh"
 #include "hysco_resident.cuh"
+#include "hysco_flat.cuh"
 #include "hysco_l2pcg.cuh"
 #include "hysco_admm.cuh"
 #include "hysco_lsq.cuh"

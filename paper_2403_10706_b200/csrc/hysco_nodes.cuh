@@ -77,6 +77,7 @@ __device__ inline void decide_pcg_init(PairState& s, const double* tot) {
         s.rr = tot[1];
         s.pcg_k = 0;
         s.beta_c = 0.0;
+        s.alpha_c = 0.0;   // no pending direction update (hysco_flat.cuh)
         s.relres = tot[1] > 0.0 ? 1.0 : 0.0;
         s.pcg_active = tot[1] > 0.0 ? 1 : 0;
     } else {

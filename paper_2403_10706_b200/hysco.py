@@ -33,7 +33,7 @@ EXPORTED = ["hysco_default_solve_opts", "hysco_default_ot_opts", "hysco_default_
             "hysco_nifti_info_read", "hysco_nifti_read", "hysco_nifti_write", "hysco_io_last_error", "hysco_pe_shape",
             "hysco_permute_pe", "hysco_fieldmap_cells", "hysco_fieldmap_cells_units"]
 PROF_NAMES = ["matvec", "pcg_update", "pcg_dir", "eval", "pcg_resident", "trial_init", "resident_sync_floor",
-              "pcg_l2"]
+              "pcg_l2", "pcg_dirmv", "pcg_upd"]
 
 
 class HyscoError(RuntimeError):

@@ -36,6 +36,54 @@ def rel(a, ref):
     return np.linalg.norm(a - ref) / (n if n > 0 else 1.0)
 
 
+def rel_floor(a, ref, floor):
+    """Relative L2 with the denominator floored at `floor` (an RMS of 1e-3 mm
+    over the array): for a near-zero field map (the phantom barely distorts a
+    10-cell column, ||b|| ~ 1e-6 .. 1e-20 mm) the plain relative error (R18)
+    measures only fp64 rounding of a vanishing solution."""
+    a = np.asarray(a, np.float64)
+    ref = np.asarray(ref, np.float64)
+    return np.linalg.norm(a - ref) / max(np.linalg.norm(ref), floor)
+
+
+def oracle_sensitivity(Ip, Im, h, bref, eps=1e-15, **kw):
+    """Relative change of the oracle's own field map when its fp64 inputs are
+    perturbed at rounding level (eps relative: 1e-15 for fp64, 1e-7 for fp32;
+    seeded): the conditioning of the instance.  A fixed 10 GN x 10 PCG run with Armijo halvings can amplify
+    rounding by ~1e7 (84 x 37 x 10: 1.7e-8), so no fp64 implementation that
+    sums in another order can be held closer than that to the oracle."""
+    rng = np.random.default_rng(1234)
+    Ip2 = Ip * (1 + eps * rng.standard_normal(Ip.shape))
+    Im2 = Im * (1 + eps * rng.standard_normal(Im.shape))
+    b2 = O.correct_pair(Ip2, Im2, h, **kw)[1]
+    return rel(b2, bref)
+
+
+def gpu_gpu_tol(Ip, Im, h, dtype, **kw):
+    """Tolerance between two GPU paths that compute the same iteration with
+    different rounding (reduction order, r / M vs r (1 / M)): the kernel
+    tolerance (fp32 1e-5, fp64 1e-11), never tighter than 10x the oracle's
+    response to input perturbations at the dtype's rounding level: a short
+    column (n3 = 3, 10) or a paper-stop run of up to 30 GN steps amplifies
+    fp32 rounding far above 1e-5."""
+    Ip = np.asarray(Ip, np.float64)
+    Im = np.asarray(Im, np.float64)
+    f32 = dtype == H.HYSCO_F32
+    bref = O.correct_pair(Ip, Im, h, **kw)[1]
+    sens = oracle_sensitivity(Ip, Im, h, bref, eps=1e-7 if f32 else 1e-15, **kw)
+    return max(1e-5 if f32 else 1e-11, 10 * sens)
+
+
+def pcg_launches(shape, dtype):
+    """Launches of one streaming GN step's PCG + Armijo start: the flat
+    two-launch form (hysco_flat.cuh: init + 10 x (dirmv, upd) + trial) when the
+    column holds at least one 16-byte vector of nodes, else the three-kernel
+    form (init + 10 x (matvec, update, dir) + trial)."""
+    V = 4 if dtype == H.HYSCO_F32 else 2
+    flat = shape[2] + 1 >= V and os.environ.get("HYSCO_NO_FLAT", "0") != "1"
+    return 22 if flat else 32
+
+
 def relS(a, ref):
     return abs(a - ref) / max(abs(ref), 1e-300)
 
@@ -199,7 +247,7 @@ def test_correct_pipeline_parity(pair, dtype, armijo):
     # + 1 eval + 10 x (PCG + eval) + apply and one more eval per Armijo
     # halving, where PCG is pcg_init + 10 x (matvec, update, dir) + trial_init streaming,
     # or 1 launch (PCG and the Armijo start) when the resident PCG applies
-    pcg = 32 if n > 200 else 1
+    pcg = pcg_launches(pair.Ip.shape, dtype) if n > 100 else 1
     assert n == 6 + 1 + 10 * (pcg + 1) + 1 + reps[0]["ls_halvings"]
     c.close()
 
@@ -355,12 +403,62 @@ def test_resident_pcg_matches_streaming(monkeypatch, cfg, armijo):
     # fp32 reduction order differs (per-CTA partials vs per-block partials), so
     # alpha/beta round differently; after 10 unconverged GN steps b and J move
     # at first order in that rounding -- both gated at the kernel tolerance
-    assert rel(b_res, b_str) <= 1e-5
+    # ... and never tighter than the instance's response to fp32-level input
+    # perturbations (400 x 2 x 10: 4.6e-4, an ill-conditioned 10-step run)
+    Ip64, Im64 = p.Ip.astype(np.float64), p.Im.astype(np.float64)
+    bref = O.correct_pair(Ip64, Im64, p.h, armijo=bool(armijo))[1]
+    tol = max(1e-5, 10 * oracle_sensitivity(Ip64, Im64, p.h, bref, eps=1e-7, armijo=bool(armijo)))
+    assert rel_floor(b_res, b_str, 1e-3 * p.h[2] * np.sqrt(b_res.size)) <= tol
     keys = ("pcg_iters", "h_evals", "gn_iters", "f_evals", "ls_halvings")
     assert tuple(r_res[k] for k in keys) == tuple(r_str[k] for k in keys)
-    assert relS(r_res["J"], r_str["J"]) <= 1e-5
+    assert relS(r_res["J"], r_str["J"]) <= tol
     # resident: one launch per GN step instead of pcg_init + 10 x (matvec, update, dir) + trial_init
-    assert n_str - n_res == 10 * 31 and r_res["f_evals"] == r_str["f_evals"]
+    assert n_str - n_res == 10 * (pcg_launches(p.Ip.shape, H.HYSCO_F32) - 1) and r_res["f_evals"] == r_str["f_evals"]
+
+
+FLAT_CASES = [((5, 7, 37), 2), ((6, 5, 24), 3), ((4, 3, 42), 2), ((3, 4, 15), 3), ((1, 3, 70), 1), ((7, 6, 3), 2)]
+
+
+@pytest.mark.parametrize("stop", ["fixed", "paper"])
+@pytest.mark.parametrize("dtype", [H.HYSCO_F32, H.HYSCO_F64], ids=["f32", "f64"])
+@pytest.mark.parametrize("shape,batch", FLAT_CASES, ids=[str(c[0]) for c in FLAT_CASES])
+def test_flat_pcg_matches_three_kernel_form(monkeypatch, shape, batch, dtype, stop):
+    """The flat vectorised two-launch PCG (hysco_flat.cuh: p formed inside the
+    matvec, x += alpha p deferred to the next launch, p double-buffered by the
+    device-side iteration parity) and the three-kernel form (matvec, update,
+    direction) compute the same iteration: same decisions and
+    counters, field map and J to the kernel tolerance (fp64 sums in another
+    order).  The shapes cover every misalignment of P and n2 P modulo the
+    vector width, misaligned pair offsets in a batch, n1 = 1, and P = 4 (one
+    vector per column); both the unrolled fixed-count and the WHILE-loop
+    (paper stop rules) forms."""
+    h = (1.2, 1.0, 1.1)
+    pairs = [phantom.make_pair(shape, h, 40 + k) for k in range(batch)]
+    Ips = [rnd(q.Ip, dtype) for q in pairs]
+    Ims = [rnd(q.Im, dtype) for q in pairs]
+    so = H.default_solve_opts() if stop == "fixed" else H.default_solve_opts(fixed_iters=0, max_gn=30)
+    monkeypatch.setenv("HYSCO_NO_RESIDENT", "1")
+    monkeypatch.setenv("HYSCO_L2PCG", "0")
+    out = []
+    for nf in ("0", "1"):
+        monkeypatch.setenv("HYSCO_NO_FLAT", nf)
+        c = Ctx(Ips, Ims, h, dtype)
+        b, Tp, Tm = c.nodes(), c.cells(), c.cells()
+        reps, inf = H.hysco_correct(c.ctx, b, Tp, Tm, solve_opts=so, batch=batch)
+        assert not inf
+        out.append((c.np(b), c.np(Tp), reps, H.hysco_last_launch_count(c.ctx)))
+        c.close()
+    (bf, Tf, rf, nf_), (b3, T3, r3, n3_) = out
+    keys = ("pcg_iters", "h_evals", "gn_iters", "f_evals", "ls_halvings", "stop_reason")
+    kw = {} if stop == "fixed" else dict(max_gn=30, fixed=False)
+    for k in range(batch):
+        tol = gpu_gpu_tol(Ips[k], Ims[k], h, dtype, **kw)
+        assert tuple(rf[k][x] for x in keys) == tuple(r3[k][x] for x in keys)
+        assert relS(rf[k]["J"], r3[k]["J"]) <= tol
+        assert rel_floor(bf[k], b3[k], 1e-3 * h[2] * np.sqrt(bf[k].size)) <= tol
+        assert rel(Tf[k], T3[k]) <= tol
+    if stop == "fixed" and shape[2] + 1 >= (4 if dtype == H.HYSCO_F32 else 2):
+        assert n3_ - nf_ == 10 * 10            # one launch fewer per PCG iteration
 
 
 L2_CASES = ["C1_16x16x8", (60, 40, 16), (50, 30, 15), (84, 37, 10), (400, 2, 10), (25, 8, 24)]
@@ -389,12 +487,16 @@ def test_l2_persistent_pcg_matches_streaming(monkeypatch, cfg, dtype, armijo):
     (b_l2, T_l2, r_l2, n_l2), (b_s, T_s, r_s, n_s) = out
     keys = ("pcg_iters", "h_evals", "gn_iters", "f_evals", "ls_halvings")
     assert tuple(r_l2[k] for k in keys) == tuple(r_s[k] for k in keys)
-    tol = 1e-5 if dtype == H.HYSCO_F32 else 1e-11
-    assert rel(b_l2, b_s) <= tol and relS(r_l2["J"], r_s["J"]) <= tol
-    assert n_s - n_l2 == r_s["gn_iters"] * 31          # one launch per GN step instead of 32
+    tol = gpu_gpu_tol(Ip, Im, p.h, dtype, armijo=bool(armijo))
+    assert rel_floor(b_l2, b_s, 1e-3 * p.h[2] * np.sqrt(b_s.size)) <= tol and relS(r_l2["J"], r_s["J"]) <= tol
+    assert n_s - n_l2 == r_s["gn_iters"] * (pcg_launches(p.Ip.shape, dtype) - 1)   # one launch per GN step
     _, bref, Tpr, _, rep = O.correct_pair(Ip, Im, p.h, armijo=bool(armijo))
     assert r_l2["f_evals"] == rep["f_evals"]
-    assert rel(b_l2, bref) <= TOL[dtype]["solve"] and rel(T_l2, Tpr) <= TOL[dtype]["solve"]
+    tol_s = TOL[dtype]["solve"]
+    if dtype == H.HYSCO_F64:       # never tighter than the instance's own rounding sensitivity
+        tol_s = max(tol_s, 10 * oracle_sensitivity(Ip, Im, p.h, bref, armijo=bool(armijo)))
+    assert rel_floor(b_l2, bref, 1e-3 * p.h[2] * np.sqrt(bref.size)) <= tol_s
+    assert rel(T_l2, Tpr) <= tol_s
 
 
 def test_repeat_calls_deterministic_and_host_entry_equal():

@@ -1,0 +1,8 @@
+# ncu of the march kernel at 7T: raw metrics + source-level stall sampling (CSV only)
+mkdir -p gpurun_out
+export HYSCO_NO_GRAPH=1
+timeout 600 ncu --set full --clock-control none --import-source on -k "regex:pcg_march" -s 2 -c 1 -o /tmp/prof_a python bench.py --config C3_hcp7t --steps 1 --warmup 1 --no-cpu-baseline --profile-reps 1 --e2e-steps 1 > gpurun_out/ncu_r2j.log 2>&1
+ncu -i /tmp/prof_a.ncu-rep --page raw --csv > gpurun_out/prof_r2j_7t.csv
+ncu -i /tmp/prof_a.ncu-rep --page source --csv --print-source sass > gpurun_out/prof_r2j_7t_sass.csv 2>&1
+ncu -i /tmp/prof_a.ncu-rep --page details --csv > gpurun_out/prof_r2j_7t_details.csv
+ls -la gpurun_out | grep r2j
