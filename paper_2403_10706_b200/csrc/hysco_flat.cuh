@@ -288,7 +288,7 @@ __host__ __device__ inline size_t march_smem_bytes(const MarchPlan& m) {
     return march_stage_bytes<T>(m) * m.nst + 16 * 8;   // + the stage barriers
 }
 
-constexpr int MARCH_THREADS = 256;   // one CTA per SM (shared memory), 8 warps
+constexpr int MARCH_THREADS = 512;   // one CTA per SM (shared memory), 16 warps
 
 // FIRST (k = 0): p_0 = z, no p_{-1}, no x update.  MS: node slots per thread
 // (the tile's own nodes of one plane, (jb - ja) P <= MS * MARCH_THREADS); every
