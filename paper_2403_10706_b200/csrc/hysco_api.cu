@@ -128,6 +128,11 @@ struct hysco_ctx_s {
     int rank = 0, nranks = 1;
     double* red = nullptr;       // [2][batch][RED_W] pair totals for the allreduce
     struct CommBase* comm = nullptr;
+    // slab path: recorded graph segments (run_slab_path) and the call shape they belong to
+    std::vector<cudaGraphExec_t> seg_exec;
+    std::vector<const void*> seg_key;
+    SolveParams seg_sp{};
+    bool seg_valid = false;
 };
 
 static hysco_status set_err(hysco_ctx c, hysco_status s, const std::string& m) {
@@ -743,13 +748,77 @@ struct NcclComm : CommBase {
     }
 };
 
-// Host-orchestrated multi-rank path: `R` = the contexts this process drives
-// (one for NCCL, all ranks for the loopback group).
+// Multi-rank path: `R` = the contexts this process drives (one for NCCL, all
+// ranks of a loopback group on one stream).  Straight-line parts -- OT, every
+// GN step's PCG (fixed counts: unrolled) with its halo exchanges, allreduces
+// and device-side decisions, the Armijo start -- are recorded once as CUDA
+// graph segments (NCCL calls captured with the kernels) and replayed; only
+// the loops whose trip count the device decides (the Armijo search; with the
+// paper's stop rules also the GN and PCG loops) run on the host, one stream
+// synchronisation per loop test.  A fixed 10 x 10 solve thus synchronises
+// once per GN step instead of once per PCG iteration.  HYSCO_NO_GRAPH=1 runs
+// every part eagerly.
+struct SegExec {
+    hysco_ctx c;                          // primary context: stream, segment cache
+    bool graph = true;
+    bool build = false;                   // recording (else replaying the cache)
+    bool open = false, pending = false;
+    int in_loop = 0;
+    size_t idx = 0;
+    cudaError_t err = cudaSuccess;
+    void ok(cudaError_t e) {
+        if (err == cudaSuccess && e != cudaSuccess) err = e;
+    }
+    template <typename F>
+    void seq(F fn) {
+        if (err != cudaSuccess) return;
+        if (!graph || in_loop) {
+            fn();
+            ok(cudaGetLastError());
+            return;
+        }
+        if (!build) {
+            pending = true;
+            return;
+        }
+        if (!open) {
+            ok(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed));
+            open = true;
+        }
+        fn();
+        ok(cudaGetLastError());
+    }
+    void flush() {
+        if (!graph || in_loop) return;
+        if (build && open) {
+            cudaGraph_t gr = nullptr;
+            cudaError_t e = cudaStreamEndCapture(c->stream, &gr);
+            open = false;
+            ok(e);
+            cudaGraphExec_t ex = nullptr;
+            if (err == cudaSuccess) ok(cudaGraphInstantiate(&ex, gr, 0));
+            if (gr) cudaGraphDestroy(gr);
+            if (err != cudaSuccess) return;
+            c->seg_exec.push_back(ex);
+            ok(cudaGraphLaunch(ex, c->stream));
+            idx++;
+        } else if (!build && pending) {
+            if (idx >= c->seg_exec.size()) {
+                ok(cudaErrorInvalidValue);
+                return;
+            }
+            ok(cudaGraphLaunch(c->seg_exec[idx++], c->stream));
+            pending = false;
+        }
+    }
+};
+
 template <typename T>
 struct SlabRun {
     std::vector<hysco_ctx>& R;
     CommBase* comm;
     SolveParams sp;
+    SegExec& x;
     cudaError_t err = cudaSuccess;
 
     void ok(cudaError_t e) {
@@ -766,11 +835,27 @@ struct SlabRun {
             decide_kernel<<<1, 256, 0, c->stream>>>(c->g, c->ctl, sp, op, mode, (int)c->cfg.batch);
         });
     }
+    template <typename F>
+    void seq(F fn) {
+        x.seq([&] { fn(); });
+        ok(x.err);
+    }
+    // a device-decided loop test: flush the recorded segment, read the flag
     bool cond(int slot) {
+        x.flush();
+        ok(x.err);
         hysco_ctx c = R[0];
         ok(cudaMemcpyAsync(c->h_cond + slot, c->dcond + slot, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
         for (hysco_ctx d : R) ok(cudaStreamSynchronize(d->stream));
         return err == cudaSuccess && c->h_cond[slot] != 0;
+    }
+    template <typename F>
+    void loop(int slot, F body) {
+        x.flush();
+        ok(x.err);
+        x.in_loop++;
+        while (err == cudaSuccess && cond(slot)) body();
+        x.in_loop--;
     }
     static dim3 gn(hysco_ctx c) { return dim3(c->gx_nodes, c->cfg.batch); }
 
@@ -808,78 +893,95 @@ struct SlabRun {
         each([&](hysco_ctx c) { L<T>::eval(c, sp, mode, L<T>::b(c, B_B)); });
         reduce_decide(OP_EVAL, mode, false);
     }
-    void gn() {
-        eval(EVAL_GN_START);
-        const bool blk = sp.precond == HYSCO_PRECOND_PE_BLOCK;   // column-local: no extra exchange (R20)
-        while (cond(COND_GN)) {
-            if (blk) {
-                each([&](hysco_ctx c) { L<T>::pcg_init_blk(c, sp); });
-            } else {
-                each([&](hysco_ctx c) {
-                    NCH_SWITCH(c->nch, pcg_init_kernel<T, NCH><<<gn(c), 256, 0, c->stream>>>(
-                                           c->g, c->ctl, L<T>::b(c, B_GRAD), L<T>::b(c, B_DT), L<T>::b(c, B_X),
-                                           L<T>::b(c, B_R), L<T>::b(c, B_P)));
-                });
-            }
-            reduce_decide(OP_PCG_INIT, 0, false);
-            while (blk && cond(COND_PCG)) {
-                ok(comm->halo(R, B_P, false));
-                each([&](hysco_ctx c) {
-                    NCH_SWITCH(c->nch, matvec_kernel<T, NCH, true><<<dim3(c->gx_mv, c->cfg.batch), 256, 0, c->stream>>>(
-                                           c->g, c->ctl, L<T>::b(c, B_DT), L<T>::b(c, B_ET), L<T>::b(c, B_P),
-                                           L<T>::b(c, B_HP)));
-                });
-                reduce_decide(OP_MATVEC, 0, false);
-                each([&](hysco_ctx c) {
-                    NCH_SWITCH(c->nch, pcg_blk_kernel<T, NCH, false><<<gn(c), 256, 0, c->stream>>>(
-                                           c->g, c->ctl, sp, L<T>::b(c, B_GRAD), L<T>::b(c, B_P), L<T>::b(c, B_HP),
-                                           L<T>::b(c, B_X), L<T>::b(c, B_R), L<T>::b(c, B_W), L<T>::b(c, B_ET),
-                                           L<T>::b(c, B_F), L<T>::b(c, B_TMP)));
-                });
-                reduce_decide(OP_UPDATE, 0, false);
-                each([&](hysco_ctx c) {
-                    NCH_SWITCH(c->nch, pcg_dir_blk_kernel<T, NCH><<<gn(c), 256, 0, c->stream>>>(
-                                           c->g, c->ctl, L<T>::b(c, B_TMP), L<T>::b(c, B_P)));
-                });
-                if (err != cudaSuccess) return;
-            }
-            while (!blk && cond(COND_PCG)) {
-                ok(comm->halo(R, B_P, false));
-                each([&](hysco_ctx c) {
-                    NCH_SWITCH(c->nch, matvec_kernel<T, NCH, true><<<dim3(c->gx_mv, c->cfg.batch), 256, 0, c->stream>>>(
-                                           c->g, c->ctl, L<T>::b(c, B_DT), L<T>::b(c, B_ET), L<T>::b(c, B_P),
-                                           L<T>::b(c, B_HP)));
-                });
-                reduce_decide(OP_MATVEC, 0, false);
-                each([&](hysco_ctx c) {
-                    NCH_SWITCH(c->nch, pcg_update_kernel<T, NCH><<<gn(c), 256, 0, c->stream>>>(
-                                           c->g, c->ctl, sp, L<T>::b(c, B_DT), L<T>::b(c, B_P), L<T>::b(c, B_HP),
-                                           L<T>::b(c, B_X), L<T>::b(c, B_R)));
-                });
-                reduce_decide(OP_UPDATE, 0, false);
-                each([&](hysco_ctx c) {
-                    NCH_SWITCH(c->nch, pcg_dir_kernel<T, NCH><<<gn(c), 256, 0, c->stream>>>(
-                                           c->g, c->ctl, L<T>::b(c, B_DT), L<T>::b(c, B_R), L<T>::b(c, B_P)));
-                });
-                if (err != cudaSuccess) return;
-            }
+    void pcg_init(bool blk) {
+        if (blk) {
+            each([&](hysco_ctx c) { L<T>::pcg_init_blk(c, sp); });
+        } else {
             each([&](hysco_ctx c) {
-                NCH_SWITCH(c->nch, trial_init_kernel<T, NCH><<<gn(c), 256, 0, c->stream>>>(
-                                       c->g, c->ctl, L<T>::b(c, B_GRAD), L<T>::b(c, B_X), L<T>::b(c, B_B),
-                                       L<T>::b(c, B_BOLD)));
+                NCH_SWITCH(c->nch, pcg_init_kernel<T, NCH><<<gn(c), 256, 0, c->stream>>>(
+                                       c->g, c->ctl, L<T>::b(c, B_GRAD), L<T>::b(c, B_DT), L<T>::b(c, B_X),
+                                       L<T>::b(c, B_R), L<T>::b(c, B_P)));
             });
-            reduce_decide(OP_TRIAL, 0, true);
-            while (cond(COND_LS)) {
+        }
+        reduce_decide(OP_PCG_INIT, 0, false);
+    }
+    // one PCG iteration: p halo, matvec, allreduce + decision,
+    // update (block: with the column Thomas solve, R20), allreduce + decision,
+    // direction
+    void pcg_iter(bool blk) {
+        ok(comm->halo(R, B_P, false));
+        each([&](hysco_ctx c) {
+            NCH_SWITCH(c->nch, matvec_kernel<T, NCH, true><<<dim3(c->gx_mv, c->cfg.batch), 256, 0, c->stream>>>(
+                                   c->g, c->ctl, L<T>::b(c, B_DT), L<T>::b(c, B_ET), L<T>::b(c, B_P),
+                                   L<T>::b(c, B_HP)));
+        });
+        reduce_decide(OP_MATVEC, 0, false);
+        if (blk) {
+            each([&](hysco_ctx c) {
+                NCH_SWITCH(c->nch, pcg_blk_kernel<T, NCH, false><<<gn(c), 256, 0, c->stream>>>(
+                                       c->g, c->ctl, sp, L<T>::b(c, B_GRAD), L<T>::b(c, B_P), L<T>::b(c, B_HP),
+                                       L<T>::b(c, B_X), L<T>::b(c, B_R), L<T>::b(c, B_W), L<T>::b(c, B_ET),
+                                       L<T>::b(c, B_F), L<T>::b(c, B_TMP)));
+            });
+            reduce_decide(OP_UPDATE, 0, false);
+            each([&](hysco_ctx c) {
+                NCH_SWITCH(c->nch, pcg_dir_blk_kernel<T, NCH><<<gn(c), 256, 0, c->stream>>>(
+                                       c->g, c->ctl, L<T>::b(c, B_TMP), L<T>::b(c, B_P)));
+            });
+        } else {
+            each([&](hysco_ctx c) {
+                NCH_SWITCH(c->nch, pcg_update_kernel<T, NCH><<<gn(c), 256, 0, c->stream>>>(
+                                       c->g, c->ctl, sp, L<T>::b(c, B_DT), L<T>::b(c, B_P), L<T>::b(c, B_HP),
+                                       L<T>::b(c, B_X), L<T>::b(c, B_R)));
+            });
+            reduce_decide(OP_UPDATE, 0, false);
+            each([&](hysco_ctx c) {
+                NCH_SWITCH(c->nch, pcg_dir_kernel<T, NCH><<<gn(c), 256, 0, c->stream>>>(
+                                       c->g, c->ctl, L<T>::b(c, B_DT), L<T>::b(c, B_R), L<T>::b(c, B_P)));
+            });
+        }
+    }
+    void trial_start() {
+        each([&](hysco_ctx c) {
+            NCH_SWITCH(c->nch, trial_init_kernel<T, NCH><<<gn(c), 256, 0, c->stream>>>(
+                                   c->g, c->ctl, L<T>::b(c, B_GRAD), L<T>::b(c, B_X), L<T>::b(c, B_B),
+                                   L<T>::b(c, B_BOLD)));
+        });
+        reduce_decide(OP_TRIAL, 0, true);
+    }
+    // Armijo search (R15): trial evaluation, then b = b_old + gamma q for the next try
+    void line_search() {
+        loop(COND_LS, [&] {
+            seq([&] {
                 eval(EVAL_TRIAL);
                 each([&](hysco_ctx c) {
                     NCH_SWITCH(c->nch, ls_retry_kernel<T, NCH><<<gn(c), 256, 0, c->stream>>>(
                                            c->g, c->ctl, L<T>::b(c, B_X), L<T>::b(c, B_BOLD), L<T>::b(c, B_B)));
                 });
-                if (err != cudaSuccess) return;
+            });
+        });
+    }
+    void gn() {
+        const bool blk = sp.precond == HYSCO_PRECOND_PE_BLOCK;   // column-local: no extra exchange (R20)
+        seq([&] { eval(EVAL_GN_START); });
+        if (sp.fixed) {   // fixed counts (R14-R16): GN steps and PCG iterations unrolled into the segments
+            for (int k = 0; k < sp.max_gn && err == cudaSuccess; k++) {
+                seq([&] {
+                    pcg_init(blk);
+                    for (int it = 0; it < sp.max_pcg; it++) pcg_iter(blk);
+                    trial_start();
+                });
+                line_search();
             }
-            each([&](hysco_ctx c) { gn_tail_kernel<<<1, 32, 0, c->stream>>>(c->ctl, (int)c->cfg.batch); });
-            if (err != cudaSuccess) return;
+            return;
         }
+        loop(COND_GN, [&] {   // paper stop rules: device-decided trip counts
+            seq([&] { pcg_init(blk); });
+            loop(COND_PCG, [&] { seq([&] { pcg_iter(blk); }); });
+            seq([&] { trial_start(); });
+            line_search();
+            seq([&] { each([&](hysco_ctx c) { gn_tail_kernel<<<1, 32, 0, c->stream>>>(c->ctl, (int)c->cfg.batch); }); });
+        });
     }
 };
 
@@ -887,22 +989,60 @@ struct SlabRun {
 template <typename T>
 static hysco_status run_slab_path(std::vector<hysco_ctx>& R, CommBase* comm, int kind, const SolveParams& sp,
                                   int blur, void* const* b_io, void* const* b_out, void* const* Tp, void* const* Tm) {
-    SlabRun<T> run{R, comm, sp};
+    hysco_ctx c0 = R[0];
+    // segment cache of the primary context, valid for the same call shape
+    std::vector<const void*> key;
+    key.push_back((const void*)(uintptr_t)kind);
+    key.push_back((const void*)(uintptr_t)blur);
+    key.push_back((const void*)(uintptr_t)R.size());
     for (size_t r = 0; r < R.size(); r++) {
-        hysco_ctx c = R[r];
-        run.ok(cudaMemsetAsync(c->launches, 0, sizeof(unsigned long long), c->stream));
-        if (kind == 1) run.ok(copy_nodes(c, c->buf[B_B], b_io[r], true, cudaMemcpyDeviceToDevice));
+        key.push_back(R[r]);
+        key.push_back(b_io ? b_io[r] : nullptr);
+        key.push_back(b_out ? b_out[r] : nullptr);
+        key.push_back(Tp ? Tp[r] : nullptr);
+        key.push_back(Tm ? Tm[r] : nullptr);
+        key.push_back(R[r]->Ip);
+        key.push_back(R[r]->Im);
     }
-    if (kind == 2) run.ot(blur);
+    SegExec x{c0};
+    x.graph = !c0->no_graph && !getenv_is1("HYSCO_NO_GRAPH");
+    const bool hit = c0->seg_valid && c0->seg_key == key && memcmp(&c0->seg_sp, &sp, sizeof sp) == 0;
+    if (x.graph && !hit) {
+        for (cudaGraphExec_t e : c0->seg_exec) cudaGraphExecDestroy(e);
+        c0->seg_exec.clear();
+        c0->seg_valid = false;
+    }
+    x.build = x.graph && !hit;
+    SlabRun<T> run{R, comm, sp, x};
+    run.seq([&] {
+        for (size_t r = 0; r < R.size(); r++) {
+            hysco_ctx c = R[r];
+            run.ok(cudaMemsetAsync(c->launches, 0, sizeof(unsigned long long), c->stream));
+            if (kind == 1) run.ok(copy_nodes(c, c->buf[B_B], b_io[r], true, cudaMemcpyDeviceToDevice));
+        }
+        if (kind == 2) run.ot(blur);
+    });
     run.gn();
+    run.seq([&] {
+        for (size_t r = 0; r < R.size(); r++) {
+            hysco_ctx c = R[r];
+            if (kind == 1) run.ok(copy_nodes(c, b_io[r], c->buf[B_B], false, cudaMemcpyDeviceToDevice));
+            if (kind == 2) {
+                if ((Tp && Tp[r]) || (Tm && Tm[r]))
+                    L<T>::apply(c, L<T>::b(c, B_B), (T*)(Tp ? Tp[r] : nullptr), (T*)(Tm ? Tm[r] : nullptr));
+                if (b_out && b_out[r]) run.ok(copy_nodes(c, b_out[r], c->buf[B_B], false, cudaMemcpyDeviceToDevice));
+            }
+        }
+    });
+    x.flush();
+    run.ok(x.err);
+    if (x.build && run.err == cudaSuccess) {
+        c0->seg_key = key;
+        c0->seg_sp = sp;
+        c0->seg_valid = true;
+    }
     for (size_t r = 0; r < R.size(); r++) {
         hysco_ctx c = R[r];
-        if (kind == 1) run.ok(copy_nodes(c, b_io[r], c->buf[B_B], false, cudaMemcpyDeviceToDevice));
-        if (kind == 2) {
-            if ((Tp && Tp[r]) || (Tm && Tm[r]))
-                L<T>::apply(c, L<T>::b(c, B_B), (T*)(Tp ? Tp[r] : nullptr), (T*)(Tm ? Tm[r] : nullptr));
-            if (b_out && b_out[r]) run.ok(copy_nodes(c, b_out[r], c->buf[B_B], false, cudaMemcpyDeviceToDevice));
-        }
         run.ok(cudaGetLastError());
         run.ok(cudaMemcpyAsync(c->h_st, c->st, sizeof(PairState) * c->cfg.batch, cudaMemcpyDeviceToHost, c->stream));
         run.ok(cudaMemcpyAsync(c->h_launches, c->launches, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
@@ -910,8 +1050,18 @@ static hysco_status run_slab_path(std::vector<hysco_ctx>& R, CommBase* comm, int
     }
     for (hysco_ctx c : R) run.ok(cudaStreamSynchronize(c->stream));
     if (run.err != cudaSuccess) {
-        for (hysco_ctx c : R) cuda_fail(c, run.err, "slab solve", __LINE__);
-        return HYSCO_ERR_CUDA;
+        cudaStreamCaptureStatus cs;
+        if (cudaStreamIsCapturing(c0->stream, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+            cudaGraph_t tmp;
+            cudaStreamEndCapture(c0->stream, &tmp);
+            if (tmp) cudaGraphDestroy(tmp);
+        }
+        for (cudaGraphExec_t e : c0->seg_exec) cudaGraphExecDestroy(e);
+        c0->seg_exec.clear();
+        c0->seg_valid = false;
+        const bool nccl = dynamic_cast<NcclComm*>(comm) && static_cast<NcclComm*>(comm)->last != ncclSuccess;
+        for (hysco_ctx c : R) cuda_fail(c, run.err, nccl ? "slab solve (NCCL)" : "slab solve", __LINE__);
+        return nccl ? HYSCO_ERR_NCCL : HYSCO_ERR_CUDA;
     }
     for (hysco_ctx c : R) c->last_launches = (long long)*c->h_launches;
     return HYSCO_OK;
@@ -2318,6 +2468,7 @@ hysco_status hysco_destroy(hysco_ctx ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->exec) cudaGraphExecDestroy(ctx->exec);
     if (ctx->graph) cudaGraphDestroy(ctx->graph);
+    for (cudaGraphExec_t e : ctx->seg_exec) cudaGraphExecDestroy(e);
     for (int k = 0; k < NBUF; k++)
         if (ctx->raw[k]) cudaFree(ctx->raw[k]);
     for (void* p : {ctx->own_Ip, ctx->own_Im, ctx->own_Tp, ctx->own_Tm, (void*)ctx->st, (void*)ctx->part,
