@@ -893,7 +893,17 @@ struct SlabRun {
         each([&](hysco_ctx c) { L<T>::eval(c, sp, mode, L<T>::b(c, B_B)); });
         reduce_decide(OP_EVAL, mode, false);
     }
+    // flat two-launch form on slabs (hysco_flat.cuh, defer mode): the march
+    // reads z_k and p_{k-1} on the halo planes, so z is exchanged after the
+    // PCG start and every residual update, p_k after every march
+    bool flat() const { return R[0]->flat && sp.precond != HYSCO_PRECOND_PE_BLOCK; }
     void pcg_init(bool blk) {
+        if (flat()) {
+            each([&](hysco_ctx c) { L<T>::pcg_init_flat(c); });
+            reduce_decide(OP_PCG_INIT, 0, false);
+            ok(comm->halo(R, B_TMP, false));
+            return;
+        }
         if (blk) {
             each([&](hysco_ctx c) { L<T>::pcg_init_blk(c, sp); });
         } else {
@@ -908,7 +918,16 @@ struct SlabRun {
     // one PCG iteration: p halo, matvec, allreduce + decision,
     // update (block: with the column Thomas solve, R20), allreduce + decision,
     // direction
-    void pcg_iter(bool blk) {
+    void pcg_iter(bool blk, int k) {
+        if (flat()) {
+            each([&](hysco_ctx c) { L<T>::pcg_dirmv(c, k == 0); });
+            reduce_decide(OP_MATVEC, 0, false);
+            ok(comm->halo(R, (k & 1) ? B_W : B_P, false));   // p_k for the next march
+            each([&](hysco_ctx c) { L<T>::pcg_upd(c, sp); });
+            reduce_decide(OP_UPDATE, 0, false);
+            ok(comm->halo(R, B_TMP, false));                  // z_{k+1}
+            return;
+        }
         ok(comm->halo(R, B_P, false));
         each([&](hysco_ctx c) {
             NCH_SWITCH(c->nch, matvec_kernel<T, NCH, true><<<dim3(c->gx_mv, c->cfg.batch), 256, 0, c->stream>>>(
@@ -942,6 +961,11 @@ struct SlabRun {
         }
     }
     void trial_start() {
+        if (flat()) {
+            each([&](hysco_ctx c) { L<T>::trial_flat(c, L<T>::b(c, B_B), L<T>::b(c, B_BOLD)); });
+            reduce_decide(OP_TRIAL, 0, true);
+            return;
+        }
         each([&](hysco_ctx c) {
             NCH_SWITCH(c->nch, trial_init_kernel<T, NCH><<<gn(c), 256, 0, c->stream>>>(
                                    c->g, c->ctl, L<T>::b(c, B_GRAD), L<T>::b(c, B_X), L<T>::b(c, B_B),
@@ -968,7 +992,7 @@ struct SlabRun {
             for (int k = 0; k < sp.max_gn && err == cudaSuccess; k++) {
                 seq([&] {
                     pcg_init(blk);
-                    for (int it = 0; it < sp.max_pcg; it++) pcg_iter(blk);
+                    for (int it = 0; it < sp.max_pcg; it++) pcg_iter(blk, it);
                     trial_start();
                 });
                 line_search();
@@ -977,7 +1001,8 @@ struct SlabRun {
         }
         loop(COND_GN, [&] {   // paper stop rules: device-decided trip counts
             seq([&] { pcg_init(blk); });
-            loop(COND_PCG, [&] { seq([&] { pcg_iter(blk); }); });
+            int it = 0;   // host iteration count = the device's pcg_k while the loop runs
+            loop(COND_PCG, [&] { seq([&] { pcg_iter(blk, it++); }); });
             seq([&] { trial_start(); });
             line_search();
             seq([&] { each([&](hysco_ctx c) { gn_tail_kernel<<<1, 32, 0, c->stream>>>(c->ctl, (int)c->cfg.batch); }); });
@@ -1730,7 +1755,6 @@ static hysco_status create_impl(const hysco_config* cfg, const SlabSpec* slab, v
     ctx->ctl.use_graph = 0;
     ctx->ctl.red = ctx->red;
     ctx->ctl.defer = g.slab ? 1 : 0;     // slab runs are host-orchestrated: always decide after the allreduce
-    if (g.slab) ctx->flat = false;       // the flat kernels decide in their last block (no defer mode)
     if (!g.slab) setup_resident(ctx);
     if (!g.slab) {
         if (cfg->dtype == HYSCO_F64) setup_l2pcg<double>(ctx);

@@ -209,6 +209,10 @@ __global__ void __launch_bounds__(256) pcg_init_flat_kernel(Geom g, Ctl c, const
     double v[2] = {arz, arr}, tot[2];
     if (!pair_reduce<2, 0u>(c, v, tot)) return;
     if (threadIdx.x != 0) return;
+    if (c.defer) {                       // slab: OP_PCG_INIT after the allreduce
+        store_red(c, pair, gridDim.y, tot, 2, 0);
+        return;
+    }
     decide_pcg_init(c.st[pair], tot);
     if (last_pair(c)) set_cond(c, COND_PCG, any_pair(c, gridDim.y, [](volatile PairState* q) { return q->pcg_active != 0; }));
 }
@@ -329,20 +333,24 @@ __global__ void __launch_bounds__(MARCH_THREADS, 1) pcg_march_kernel(Geom g, Ctl
         const int nown = (jb - ja) * P, nwin = (jh - jl + 1) * P;
         const int SE = 2 * mp.la + 3 * mp.lb;                             // stage pitch (elements)
         constexpr int Q = 16 / (int)sizeof(T);
-        const int q0 = ia > 0 ? ia - 1 : 0, qend = ib < n1 ? ib + 1 : n1;   // planes loaded: [q0, qend)
+        // planes loaded: [q0, qend); on a slab the halo planes -1 / n1 (exchanged
+        // copies of the neighbouring ranks' boundary planes) where they exist
+        const int q0 = ia > 0 ? ia - 1 : (has_im(g, 0) ? -1 : 0);
+        const int qend = ib < n1 ? ib + 1 : (has_ip(g, n1 - 1) ? n1 + 1 : n1);
         // misalignment (elements below a 16-byte boundary) of plane q's windows:
         // (mis(0) + q (n2 P mod Q)) mod Q
         const long long plane = (long long)n2 * P;
         const int dq = (int)(plane % Q);
         const int mA0 = (int)(((uintptr_t)(zp + (size_t)jl * P) / sizeof(T)) % Q);
         const int mB0 = (int)(((uintptr_t)(zp + (size_t)ja * P - 1) / sizeof(T)) % Q);
-        auto misA = [&](int q) { return (mA0 + q * dq) % Q; };
-        auto misB = [&](int q) { return (mB0 + q * dq) % Q; };
+        auto misA = [&](int q) { return ((mA0 + q * dq) % Q + Q) % Q; };
+        auto misB = [&](int q) { return ((mB0 + q * dq) % Q + Q) % Q; };
         auto issue = [&](int q) {   // one thread: the stage of plane q
             const int s = (q - q0) % mp.nst;
             T* S = stage0 + (size_t)s * SE;
             const int dA = misA(q), dB = misB(q);
-            const size_t gA = (size_t)q * plane + (size_t)jl * P - dA, gB = (size_t)q * plane + (size_t)ja * P - 1 - dB;
+            const long long gA = (long long)q * plane + (long long)jl * P - dA;
+            const long long gB = (long long)q * plane + (long long)ja * P - 1 - dB;
             const unsigned bA = (unsigned)(((nwin + dA) + Q - 1) / Q * 16);
             const unsigned bB = (unsigned)(((nown + 1 + dB) + Q - 1) / Q * 16);
             const bool own = q >= ia && q < ib;
@@ -451,6 +459,10 @@ __global__ void __launch_bounds__(MARCH_THREADS, 1) pcg_march_kernel(Geom g, Ctl
     double v[1] = {acc}, tot[1];
     if (!pair_reduce<1, 0u>(c, v, tot)) return;
     if (threadIdx.x != 0) return;
+    if (c.defer) {                       // slab: OP_MATVEC after the allreduce
+        store_red(c, pair, gridDim.y, tot, 1, 0);
+        return;
+    }
     decide_matvec(c.st[pair], tot);
 }
 
@@ -508,6 +520,10 @@ __global__ void __launch_bounds__(256) pcg_upd_kernel(Geom g, Ctl c, SolveParams
     double v[2] = {arz, arr}, tot[2];
     if (!pair_reduce<2, 0u>(c, v, tot)) return;
     if (threadIdx.x != 0) return;
+    if (c.defer) {                       // slab: OP_UPDATE after the allreduce
+        store_red(c, pair, gridDim.y, tot, 2, 0);
+        return;
+    }
     decide_update(sp, c.st[pair], tot);
     if (last_pair(c)) set_cond(c, COND_PCG, any_pair(c, gridDim.y, [](volatile PairState* q) { return q->pcg_active != 0; }));
 }
@@ -586,6 +602,10 @@ __global__ void __launch_bounds__(256) trial_flat_kernel(Geom g, Ctl c, const T*
     double v[2] = {agq, aqm}, tot[2];
     if (!pair_reduce<2, 0x2u>(c, v, tot)) return;
     if (threadIdx.x != 0) return;
+    if (c.defer) {                       // slab: OP_TRIAL after the allreduce
+        store_red(c, pair, gridDim.y, tot, 1, 1);
+        return;
+    }
     decide_trial(c.st[pair], tot);
     if (last_pair(c)) set_cond(c, COND_LS, any_pair(c, gridDim.y, [](volatile PairState* q2) { return q2->ls_active != 0; }));
 }
