@@ -1396,7 +1396,22 @@ static hysco_status setup_typed(hysco_ctx ctx) {
         if (wmax == 0) {
             ctx->flat = false;
         } else {
-            ctx->mr_njb = (g.n2 + wmax - 1) / wmax;
+            // column tiles: the widest (fewest halo columns, largest copies) unless its
+            // nJB x floor(nsm / nJB) tiles leave > 10 % of the SMs idle; then, among
+            // nJB up to twice that, the one filling the most SMs (C5: 128 -> 148 CTAs;
+            // 7T keeps 14 x 10 = 140, narrower tiles measured slower)
+            const int njb0 = (g.n2 + wmax - 1) / wmax;
+            auto used = [&](int nj) {
+                return nj <= ctx->nsm ? nj * std::min(std::max(1, ctx->nsm / nj), g.n1) : ctx->nsm;
+            };
+            int best = njb0, bestu = used(njb0);
+            if (10 * bestu < 9 * std::min(ctx->nsm, g.n1 * njb0))
+                for (int nj = njb0 + 1; nj <= std::min(2 * njb0, g.n2); nj++)
+                    if (used(nj) > bestu) {
+                        bestu = used(nj);
+                        best = nj;
+                    }
+            ctx->mr_njb = best;
             wmax = (g.n2 + ctx->mr_njb - 1) / ctx->mr_njb;
             ctx->mr_plan = march_plan<T>(wmax, g.P, 5);
             ctx->mr_plan.ms = march_ms<T>(wmax, g.P, MARCH_THREADS);
