@@ -14,7 +14,9 @@ import sys
 
 NAMES = {"pcg_resident_kernel": "pcg_resident", "eval_kernel": "eval", "matvec_kernel": "matvec",
          "pcg_update_kernel": "pcg_update", "pcg_dir_kernel": "pcg_dir", "trial_init_kernel": "trial_init",
-         "pcg_mvdir_kernel": "pcg_mvdir", "pcg_sync_floor_kernel": "resident_sync_floor"}
+         "pcg_mvdir_kernel": "pcg_mvdir", "pcg_sync_floor_kernel": "resident_sync_floor",
+         "pcg_march_kernel": "pcg_dirmv", "pcg_upd_kernel": "pcg_upd", "trial_flat_kernel": "trial_init",
+         "pcg_init_flat_kernel": "pcg_init"}
 
 
 def mean(v):
@@ -26,10 +28,11 @@ def main(args):
     out_path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "ncu_summary.json")
     out = {"configs": {}, "note": __doc__.strip().splitlines()[0]}
     for a in args:
-        cfg, path = a.split("=", 1)
-        src = json.load(open(path))
-        ent = {}
-        for short, launches in src["kernels"].items():
+        cfg, paths = a.split("=", 1)
+        ent = out["configs"].setdefault(cfg, {})
+        for path in paths.split("+"):     # later files win for kernels in several
+          src = json.load(open(path))
+          for short, launches in src["kernels"].items():
             name = NAMES.get(short)
             if not name:
                 continue
@@ -47,7 +50,6 @@ def main(args):
                 "top_stalls": dict(list(ls[0].get("stall_share", {}).items())[:4]),
                 "source": path,
             }
-        out["configs"][cfg] = ent
     json.dump(out, open(out_path, "w"), indent=1)
     print(json.dumps(out, indent=1)[:3000])
 
