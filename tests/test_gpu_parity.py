@@ -738,9 +738,36 @@ def test_admm_fixed_parity(dtype, shape, seed):
     # numpy's pocketfft summation order) and per-column Newton steps whose
     # rounding the coupled iteration amplifies ~1e2-1e3x over the run (fp64
     # measured 4e-9 after 8 iterations; fp32 1.4e-4 after 4 on 12x10x24)
-    tol = 1e-8 if dtype == H.HYSCO_F64 else 3e-4
+    tol = 1e-12 if dtype == H.HYSCO_F64 else 3e-4
     assert rel(c.np(b)[0], bref) <= tol
     assert relS(r["J"], O.evaluate(Ip, Im, bref, p.h).J) <= tol
+    c.close()
+
+
+ADMM_LONG = [((12, 10, 24), 3, True), ((5, 7, 37), 5, True), ((4, 5, 144), 7, True), ((24, 20, 48), 9, False)]
+
+
+@pytest.mark.parametrize("dtype", [H.HYSCO_F64, H.HYSCO_F32], ids=["f64", "f32"])
+@pytest.mark.parametrize("shape,seed,f32_gate", ADMM_LONG, ids=[str(c[0]) for c in ADMM_LONG])
+def test_admm_bench_iteration_count_parity(dtype, shape, seed, f32_gate):
+    """ADMM at the bench's iteration count (33 to the 1e-3 change tolerance at
+    3T) as fixed iterations vs the oracle: fp64 to 1e-12 (measured 3e-14); fp32
+    to north_star's 1e-4 where the per-column Armijo / stop decisions of the
+    fp32 b-update do not flip against the oracle's fp64 ones -- the fp32
+    error is 1e-7 until a column decision flips, then jumps to 3e-5..1e-4
+    (12x10x24 from 4 iterations, 24x20x48 from 16; profiles/admm_f32_error_r2.json),
+    so 24x20x48 (9.97e-5 at 33) is checked in fp64 only."""
+    if dtype == H.HYSCO_F32 and not f32_gate:
+        pytest.skip("fp32 decision flip puts this instance at the gate (profiles/admm_f32_error_r2.json)")
+    p = phantom.make_pair(shape, (1.25, 1.25, 1.1), seed)
+    Ip, Im = rnd(p.Ip, dtype), rnd(p.Im, dtype)
+    b0 = rnd(O.ot_init(Ip, Im, p.h[2])[0], dtype)
+    c = Ctx([Ip], [Im], p.h, dtype)
+    b = c.nodes(b0)
+    reps = H.hysco_admm(c.ctx, b, H.default_admm_opts(max_iter=33, fixed_iters=1))
+    bref, zref, rep = O.admm(Ip, Im, b0, p.h, max_iter=33, fixed=True)
+    assert reps[0]["iters"] == 33 and reps[0]["rho"] == rep["rho_final"]
+    assert rel(c.np(b)[0], bref) <= (1e-12 if dtype == H.HYSCO_F64 else 1e-4)
     c.close()
 
 
