@@ -279,6 +279,33 @@ HYSCO_API hysco_status hysco_correct_host_stream(hysco_ctx ctx, int32_t n_items,
                                                  void* const* h_Iplus_corr, void* const* h_Iminus_corr,
                                                  hysco_report* reports);
 
+/* Per-iteration solver history of the last hysco_solve / hysco_correct (or
+ * slab group) call (PyHySCO's OptimizationLogger records the loss
+ * terms per iteration).  Record 0 is the Gauss-Newton start (the objective at
+ * the initial b, gamma = 0); record k >= 1 is taken when the k-th GN step is
+ * accepted: the objective parts at the new b, ||grad J||, the
+ * accepted Armijo step gamma, that step's PCG iterations and final relative
+ * residual, max |gamma q| (mm), and the cumulative objective evaluations and
+ * halvings.  Written on the device by the deciding kernels, no host
+ * synchronisation during the solve; at most 64 records (GN steps beyond 63
+ * are not recorded).  ADMM solves do not write it.
+ * pair: 0 <= pair < batch; out (host) receives min(gn_iters + 1, 64,
+ * max_records) records, *n_records their count.  Synchronises the context
+ * stream.  HYSCO_ERR_ARG for a bad pair / NULL buffer. */
+typedef struct {
+    int32_t k;               /* 0: GN start; k: after the k-th accepted step */
+    int32_t pcg_iters;       /* PCG iterations of step k (0 for k = 0)       */
+    int32_t ls_halvings;     /* Armijo halvings so far                        */
+    int32_t f_evals;         /* objective evaluations so far                  */
+    double J, D, S, P;       /* objective parts at b_k (Eq.(2)-(6))          */
+    double grad_norm;        /* ||grad J(b_k)||                               */
+    double gamma;            /* accepted step size (R15)                      */
+    double relres;           /* ||r|| / ||r0|| of step k's PCG (R14)          */
+    double step_max;         /* max |gamma q| of step k, mm (R16)             */
+} hysco_iter_record;
+HYSCO_API hysco_status hysco_history(hysco_ctx ctx, int32_t pair, hysco_iter_record* out, int32_t max_records,
+                                     int32_t* n_records);
+
 /* Number of kernel launches issued by the last solve / correct call (graph
  * nodes executed, counted on the device). */
 HYSCO_API int64_t hysco_last_launch_count(hysco_ctx ctx);

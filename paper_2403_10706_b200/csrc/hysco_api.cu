@@ -12,6 +12,7 @@
 
 #include <nccl.h>
 #include <cufft.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -23,6 +24,13 @@
 #include <vector>
 
 using namespace hysco;
+
+// NVTX range around each public entry point (visible to nsys / ncu range
+// filters; no cost without an attached tool).
+struct NvtxRange {
+    explicit NvtxRange(const char* n) { nvtxRangePushA(n); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 namespace {
 
@@ -127,6 +135,7 @@ struct hysco_ctx_s {
     size_t plane_off = 0;        // elements from a pair's buffer start to local plane 0
     int rank = 0, nranks = 1;
     double* red = nullptr;       // [2][batch][RED_W] pair totals for the allreduce
+    HistRec* hist = nullptr;     // [batch][HIST_MAX] per-GN-step history (hysco_history)
     struct CommBase* comm = nullptr;
     // slab path: recorded graph segments (run_slab_path) and the call shape they belong to
     std::vector<cudaGraphExec_t> seg_exec;
@@ -1201,6 +1210,7 @@ struct PairView {
         c->ctl.st += p;
         c->ctl.part += (size_t)p * c->ctl.part_stride;
         c->ctl.ctr += p;
+        c->ctl.hist += (size_t)p * HIST_MAX;
         c->Ip = static_cast<const char*>(Ip) + (size_t)p * c->g.Nc * c->esz;
         c->Im = static_cast<const char*>(Im) + (size_t)p * c->g.Nc * c->esz;
     }
@@ -1213,6 +1223,7 @@ struct PairView {
         c->ctl.st = ctl.st;
         c->ctl.part = ctl.part;
         c->ctl.ctr = ctl.ctr;
+        c->ctl.hist = ctl.hist;
         c->Ip = Ip;
         c->Im = Im;
     }
@@ -1742,7 +1753,8 @@ static hysco_status create_impl(const hysco_config* cfg, const SlabSpec* slab, v
         !dalloc((void**)&ctx->ctr, sizeof(unsigned) * cfg->batch) || !dalloc((void**)&ctx->gctr, sizeof(unsigned)) ||
         !dalloc((void**)&ctx->launches, sizeof(unsigned long long)) ||
         !dalloc((void**)&ctx->dcond, sizeof(unsigned) * NCOND) ||
-        !dalloc((void**)&ctx->red, sizeof(double) * 2 * RED_W * cfg->batch))
+        !dalloc((void**)&ctx->red, sizeof(double) * 2 * RED_W * cfg->batch) ||
+        !dalloc((void**)&ctx->hist, sizeof(HistRec) * HIST_MAX * cfg->batch))
         return bail(HYSCO_ERR_NOMEM);
     if (g.slab)   // halo planes must start at zero (Neumann ends never read them, blur ring does)
         for (int k = 0; k < NBUF; k++) cudaMemset(ctx->buf[k], 0, nn);
@@ -1769,6 +1781,8 @@ static hysco_status create_impl(const hysco_config* cfg, const SlabSpec* slab, v
     ctx->ctl.dcond = ctx->dcond;
     ctx->ctl.use_graph = 0;
     ctx->ctl.red = ctx->red;
+    ctx->ctl.hist = ctx->hist;
+    cudaMemset(ctx->hist, 0, sizeof(HistRec) * HIST_MAX * cfg->batch);
     ctx->ctl.defer = g.slab ? 1 : 0;     // slab runs are host-orchestrated: always decide after the allreduce
     if (!g.slab) setup_resident(ctx);
     if (!g.slab) {
@@ -1874,6 +1888,7 @@ static hysco_status need_images(hysco_ctx ctx) {
 }
 
 hysco_status hysco_ot_init(hysco_ctx ctx, const hysco_ot_opts* opts, void* d_b_out) {
+    NvtxRange nvtx_("hysco_ot_init");
     CHECK_CTX();
     if (ctx->g.slab) return set_err(ctx, HYSCO_ERR_STATE, "slab contexts support solve / correct / correct_host");
     if (hysco_status s = need_images(ctx)) return s;
@@ -1894,6 +1909,7 @@ hysco_status hysco_ot_init(hysco_ctx ctx, const hysco_ot_opts* opts, void* d_b_o
 }
 
 hysco_status hysco_objective_grad(hysco_ctx ctx, const void* d_b, double* JDSP, void* d_grad) {
+    NvtxRange nvtx_("hysco_objective_grad");
     CHECK_CTX();
     if (ctx->g.slab) return set_err(ctx, HYSCO_ERR_STATE, "slab contexts support solve / correct / correct_host");
     if (hysco_status s = need_images(ctx)) return s;
@@ -1928,6 +1944,7 @@ hysco_status hysco_objective_grad(hysco_ctx ctx, const void* d_b, double* JDSP, 
 }
 
 hysco_status hysco_hessvec(hysco_ctx ctx, const void* d_q, void* d_Hq) {
+    NvtxRange nvtx_("hysco_hessvec");
     CHECK_CTX();
     if (ctx->g.slab) return set_err(ctx, HYSCO_ERR_STATE, "slab contexts support solve / correct / correct_host");
     if (!ctx->state_valid) return set_err(ctx, HYSCO_ERR_STATE, "hessvec needs a feasible objective_grad first");
@@ -1940,6 +1957,7 @@ hysco_status hysco_hessvec(hysco_ctx ctx, const void* d_q, void* d_Hq) {
 }
 
 hysco_status hysco_hess_diag(hysco_ctx ctx, void* d_diag) {
+    NvtxRange nvtx_("hysco_hess_diag");
     CHECK_CTX();
     if (ctx->g.slab) return set_err(ctx, HYSCO_ERR_STATE, "slab contexts support solve / correct / correct_host");
     if (!ctx->state_valid) return set_err(ctx, HYSCO_ERR_STATE, "hess_diag needs a feasible objective_grad first");
@@ -1951,6 +1969,7 @@ hysco_status hysco_hess_diag(hysco_ctx ctx, void* d_diag) {
 }
 
 hysco_status hysco_precond_solve(hysco_ctx ctx, int kind, const void* d_r, void* d_z) {
+    NvtxRange nvtx_("hysco_precond_solve");
     CHECK_CTX();
     if (ctx->g.slab) return set_err(ctx, HYSCO_ERR_STATE, "slab contexts support solve / correct / correct_host");
     if (!ctx->state_valid) return set_err(ctx, HYSCO_ERR_STATE, "precond_solve needs a feasible objective_grad first");
@@ -1997,6 +2016,7 @@ void hysco_default_admm_opts(hysco_admm_opts* o) {
 }
 
 hysco_status hysco_admm(hysco_ctx ctx, void* d_b_inout, const hysco_admm_opts* opts, hysco_admm_report* reports) {
+    NvtxRange nvtx_("hysco_admm");
     CHECK_CTX();
     if (ctx->g.slab) return set_err(ctx, HYSCO_ERR_STATE, "ADMM is not available on slab contexts");
     if (hysco_status s = need_images(ctx)) return s;
@@ -2018,6 +2038,7 @@ void hysco_default_lsq_opts(hysco_lsq_opts* o) {
 }
 
 hysco_status hysco_push_forward(hysco_ctx ctx, const void* d_b, const void* d_T, void* d_Iplus, void* d_Iminus) {
+    NvtxRange nvtx_("hysco_push_forward");
     CHECK_CTX();
     // column-local: on a slab context it runs on the rank's planes, no exchange
     if (!d_b || !d_T || !d_Iplus || !d_Iminus || !aligned16(d_b) || !aligned16(d_T) || !aligned16(d_Iplus) ||
@@ -2029,6 +2050,7 @@ hysco_status hysco_push_forward(hysco_ctx ctx, const void* d_b, const void* d_T,
 
 hysco_status hysco_lsq_correct(hysco_ctx ctx, const void* d_b, const hysco_lsq_opts* opts, void* d_T_out,
                                hysco_lsq_report* reports) {
+    NvtxRange nvtx_("hysco_lsq_correct");
     CHECK_CTX();
     // column-local: on a slab context it runs on the rank's planes, no exchange
     if (hysco_status s = need_images(ctx)) return s;
@@ -2068,6 +2090,7 @@ hysco_status hysco_fieldmap_cells_units(hysco_ctx ctx, const void* d_b, void* d_
 }
 
 hysco_status hysco_apply(hysco_ctx ctx, const void* d_b, void* d_Iplus_corr, void* d_Iminus_corr) {
+    NvtxRange nvtx_("hysco_apply");
     CHECK_CTX();
     if (ctx->g.slab) return set_err(ctx, HYSCO_ERR_STATE, "slab contexts support solve / correct / correct_host");
     if (hysco_status s = need_images(ctx)) return s;
@@ -2125,6 +2148,7 @@ static hysco_status solve_common(hysco_ctx ctx, int kind, const hysco_ot_opts* o
 }
 
 hysco_status hysco_solve(hysco_ctx ctx, void* d_b_inout, const hysco_solve_opts* opts, hysco_report* reports) {
+    NvtxRange nvtx_("hysco_solve");
     CHECK_CTX();
     if (hysco_status s = need_images(ctx)) return s;
     if (!d_b_inout || !aligned16(d_b_inout)) return set_err(ctx, HYSCO_ERR_ARG, "d_b_inout must be 16-byte aligned");
@@ -2133,6 +2157,7 @@ hysco_status hysco_solve(hysco_ctx ctx, void* d_b_inout, const hysco_solve_opts*
 
 hysco_status hysco_correct(hysco_ctx ctx, const hysco_ot_opts* ot, const hysco_solve_opts* so, void* d_b_out,
                            void* d_Iplus_corr, void* d_Iminus_corr, hysco_report* reports) {
+    NvtxRange nvtx_("hysco_correct");
     CHECK_CTX();
     if (hysco_status s = need_images(ctx)) return s;
     for (void* p : {d_b_out, d_Iplus_corr, d_Iminus_corr})
@@ -2143,6 +2168,7 @@ hysco_status hysco_correct(hysco_ctx ctx, const hysco_ot_opts* ot, const hysco_s
 hysco_status hysco_correct_host(hysco_ctx ctx, const void* h_Iplus, const void* h_Iminus, const hysco_ot_opts* ot,
                                 const hysco_solve_opts* so, void* h_b_out, void* h_Iplus_corr, void* h_Iminus_corr,
                                 hysco_report* reports) {
+    NvtxRange nvtx_("hysco_correct_host");
     CHECK_CTX();
     if (!h_Iplus || !h_Iminus) return set_err(ctx, HYSCO_ERR_ARG, "host images must be non-NULL");
     const size_t nc = (size_t)ctx->cfg.batch * ctx->g.Nc * ctx->esz;
@@ -2186,6 +2212,7 @@ hysco_status hysco_correct_host_stream(hysco_ctx ctx, int32_t n_items, const voi
                                        const hysco_solve_opts* so, void* const* h_b_out,
                                        void* const* h_Iplus_corr, void* const* h_Iminus_corr,
                                        hysco_report* reports) {
+    NvtxRange nvtx_("hysco_correct_host_stream");
     CHECK_CTX();
     if (ctx->g.slab) return set_err(ctx, HYSCO_ERR_STATE, "slab contexts support solve / correct / correct_host");
     if (n_items < 0 || (n_items > 0 && (!h_Iplus || !h_Iminus)))
@@ -2242,6 +2269,24 @@ hysco_status hysco_correct_host_stream(hysco_ctx ctx, int32_t n_items, const voi
 }
 
 int64_t hysco_last_launch_count(hysco_ctx ctx) { return ctx ? ctx->last_launches : -1; }
+
+static_assert(sizeof(hysco_iter_record) == sizeof(HistRec), "hysco_iter_record mirrors HistRec");
+
+hysco_status hysco_history(hysco_ctx ctx, int32_t pair, hysco_iter_record* out, int32_t max_records,
+                           int32_t* n_records) {
+    CHECK_CTX();
+    if (pair < 0 || pair >= ctx->cfg.batch || !out || max_records < 0 || !n_records)
+        return set_err(ctx, HYSCO_ERR_ARG, "hysco_history: bad pair / buffer");
+    const PairState& s = ctx->h_st[pair];   // mirror of the last solve's final state
+    int n = s.stop_reason == STOP_INFEASIBLE && s.f_evals <= 1 ? 1 : s.gn_k + 1;
+    n = std::min(std::min(n, HIST_MAX), (int)max_records);
+    *n_records = n;
+    if (n == 0) return HYSCO_OK;
+    CK(cudaMemcpyAsync(out, ctx->hist + (size_t)pair * HIST_MAX, sizeof(HistRec) * n, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return HYSCO_OK;
+}
 
 hysco_status hysco_nccl_unique_id(unsigned char id_out[128]) {
     if (!id_out) return HYSCO_ERR_ARG;
@@ -2353,11 +2398,13 @@ static hysco_status group_common(hysco_ctx* ctxs, int32_t n, int kind, const hys
 hysco_status hysco_group_correct(hysco_ctx* ctxs, int32_t nranks, const hysco_ot_opts* ot, const hysco_solve_opts* so,
                                  void* const* d_b_out, void* const* d_Iplus_corr, void* const* d_Iminus_corr,
                                  hysco_report* reports) {
+    NvtxRange nvtx_("hysco_group_correct");
     return group_common(ctxs, nranks, 2, ot, so, nullptr, d_b_out, d_Iplus_corr, d_Iminus_corr, reports);
 }
 
 hysco_status hysco_group_solve(hysco_ctx* ctxs, int32_t nranks, void* const* d_b_inout, const hysco_solve_opts* so,
                                hysco_report* reports) {
+    NvtxRange nvtx_("hysco_group_solve");
     if (!d_b_inout) return HYSCO_ERR_ARG;
     return group_common(ctxs, nranks, 1, nullptr, so, d_b_inout, nullptr, nullptr, nullptr, reports);
 }
@@ -2492,6 +2539,7 @@ static hysco_status profile_typed(hysco_ctx ctx, int reps, int flush_l2, double*
 extern "C" {
 
 hysco_status hysco_profile_kernels(hysco_ctx ctx, int32_t reps, int32_t flush_l2, double* avg_ms) {
+    NvtxRange nvtx_("hysco_profile_kernels");
     CHECK_CTX();
     if (hysco_status s = need_images(ctx)) return s;
     if (reps < 1 || !avg_ms) return set_err(ctx, HYSCO_ERR_ARG, "reps >= 1 and avg_ms[HYSCO_NPROF] required");
@@ -2538,6 +2586,7 @@ hysco_status hysco_destroy(hysco_ctx ctx) {
     if (ctx->res_pg) cudaFree(ctx->res_pg);
     if (ctx->res_x) cudaFree(ctx->res_x);
     if (ctx->red) cudaFree(ctx->red);
+    if (ctx->hist) cudaFree(ctx->hist);
     if (ctx->comm) {
         if (LoopbackComm* lb = dynamic_cast<LoopbackComm*>(ctx->comm)) {
             for (auto& m : lb->members)

@@ -81,6 +81,15 @@ struct SolveParams {
 
 enum { COND_GN = 0, COND_PCG = 1, COND_LS = 2, NCOND = 3 };
 
+// Per-iteration solver history ("OptimizationLogger"; hysco_history):
+// record 0 = the GN start, record k = after the k-th accepted GN step.
+// Same layout as hysco_iter_record (include/hysco.h).
+constexpr int HIST_MAX = 64;
+struct HistRec {
+    int k, pcg_iters, ls_halvings, f_evals;
+    double J, D, S, P, grad_norm, gamma, relres, step_max;
+};
+
 // Control block shared by all kernels of a context.
 struct Ctl {
     PairState* st;                 // [batch]
@@ -96,6 +105,7 @@ struct Ctl {
     int defer;                     // 1 (multi-rank): last blocks store pair totals in `red`,
                                    //   decisions run in decide_kernel after the allreduce
     double* red;                   // [batch][RED_W] pair totals (multi-rank)
+    HistRec* hist;                 // [batch][HIST_MAX] per-GN-step history (may be null)
 };
 constexpr int RED_W = 8;
 

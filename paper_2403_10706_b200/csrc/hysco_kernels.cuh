@@ -64,8 +64,27 @@ enum { EVAL_PLAIN = 0, EVAL_GN_START = 1, EVAL_TRIAL = 2 };
 // After an evaluation: objective parts (Eq.(2)-(6)), then GN start / Armijo
 // acceptance (R15) and the R16 stop rules.  tot = [sum r^2, b^T L b, sum phi,
 // ||grad||^2, infeasible (> 0 if any |Db| >= 1)].
+__device__ inline void hist_record(HistRec* hr, const PairState& s, int k, double gamma, int pcg, double relres,
+                                   double step) {
+    if (!hr || k >= HIST_MAX) return;
+    HistRec& r = hr[k];
+    r.k = k;
+    r.pcg_iters = pcg;
+    r.ls_halvings = s.ls_halvings;
+    r.f_evals = s.f_evals;
+    r.J = s.J;
+    r.D = s.D;
+    r.S = s.S;
+    r.P = s.P;
+    r.grad_norm = sqrt(s.gnorm2);
+    r.gamma = gamma;
+    r.relres = relres;
+    r.step_max = step;
+}
+
+// hr: this pair's history row (HIST_MAX records) or null.
 __device__ inline void decide_eval(const Geom& g, const Ctl& c, const SolveParams& sp, int mode, PairState& s,
-                                   const double* tot) {
+                                   const double* tot, HistRec* hr = nullptr) {
     const bool active = (mode != EVAL_TRIAL) || s.ls_active;
     if (active) {
         const bool inf = tot[4] > 0.0;
@@ -90,6 +109,7 @@ __device__ inline void decide_eval(const Geom& g, const Ctl& c, const SolveParam
         s.gn_active = (!s.infeasible && sp.max_gn > 0) ? 1 : 0;
         s.pcg_active = 0;
         s.ls_active = 0;
+        hist_record(hr, s, 0, 0.0, 0, 0.0, 0.0);
     } else if (mode == EVAL_TRIAL && active) {
         if (s.ls_restore) {                       // line search failed: state restored at b_old
             s.ls_active = 0;
@@ -101,6 +121,7 @@ __device__ inline void decide_eval(const Geom& g, const Ctl& c, const SolveParam
                 s.J_acc = s.J;
                 s.gn_k += 1;
                 s.ls_active = 0;
+                hist_record(hr, s, s.gn_k, s.gamma, s.pcg_k, s.relres, s.gamma * s.qmax);
                 int stop = -1;
                 if (!sp.fixed) {                  // R16 stopping rules
                     if (sqrt(s.gnorm2) <= sp.tol_grad_rel * s.g0norm) stop = STOP_GRAD;
@@ -427,7 +448,7 @@ __global__ void __launch_bounds__(256, (NCH <= 5 ? 3 : 4)) eval_kernel(Geom g, C
         store_red(c, pair, gridDim.y, tot, 5, 0);
         return;
     }
-    decide_eval(g, c, sp, mode, c.st[pair], tot);
+    decide_eval(g, c, sp, mode, c.st[pair], tot, c.hist ? c.hist + (size_t)pair * HIST_MAX : nullptr);
     if (mode == EVAL_GN_START && last_pair(c))
         set_cond(c, COND_GN, any_pair(c, gridDim.y, [](volatile PairState* q) { return q->gn_active != 0; }));
     if (mode == EVAL_TRIAL && last_pair(c)) {
@@ -634,7 +655,7 @@ __global__ void decide_kernel(Geom g, Ctl c, SolveParams sp, int op, int mode, i
         switch (op) {
             case OP_EVAL:
                 for (int k = 0; k < 5; k++) tot[k] = rs[k];
-                decide_eval(g, c, sp, mode, s, tot);
+                decide_eval(g, c, sp, mode, s, tot, c.hist ? c.hist + (size_t)p * HIST_MAX : nullptr);
                 break;
             case OP_PCG_INIT:
                 decide_pcg_init(s, rs);

@@ -25,7 +25,7 @@ EXPORTED = ["hysco_default_solve_opts", "hysco_default_ot_opts", "hysco_default_
             "hysco_ot_init", "hysco_objective_grad", "hysco_hessvec", "hysco_hess_diag", "hysco_precond_solve",
             "hysco_solve",
             "hysco_apply", "hysco_correct", "hysco_correct_host", "hysco_correct_host_stream",
-            "hysco_last_launch_count",
+            "hysco_last_launch_count", "hysco_history",
             "hysco_last_error", "hysco_destroy", "hysco_version", "hysco_profile_kernels",
             "hysco_nccl_unique_id", "hysco_create_slab", "hysco_create_loopback", "hysco_group_correct",
             "hysco_group_solve", "hysco_push_forward", "hysco_default_lsq_opts", "hysco_lsq_correct",
@@ -71,6 +71,16 @@ class hysco_admm_report(ctypes.Structure):
     _fields_ = [("iters", ctypes.c_int32), ("converged", ctypes.c_int32), ("rho", ctypes.c_double),
                 ("r_norm", ctypes.c_double), ("s_norm", ctypes.c_double), ("J", ctypes.c_double),
                 ("D", ctypes.c_double), ("S", ctypes.c_double), ("P", ctypes.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class hysco_iter_record(ctypes.Structure):
+    _fields_ = [("k", ctypes.c_int32), ("pcg_iters", ctypes.c_int32), ("ls_halvings", ctypes.c_int32),
+                ("f_evals", ctypes.c_int32), ("J", ctypes.c_double), ("D", ctypes.c_double), ("S", ctypes.c_double),
+                ("P", ctypes.c_double), ("grad_norm", ctypes.c_double), ("gamma", ctypes.c_double),
+                ("relres", ctypes.c_double), ("step_max", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -164,6 +174,9 @@ def lib():
     L.hysco_destroy.argtypes = [vp]
     L.hysco_last_launch_count.argtypes = [vp]
     L.hysco_last_launch_count.restype = ctypes.c_int64
+    L.hysco_history.argtypes = [vp, ctypes.c_int32, ctypes.POINTER(hysco_iter_record), ctypes.c_int32,
+                                ctypes.POINTER(ctypes.c_int32)]
+    L.hysco_history.restype = st
     NI = ctypes.POINTER(hysco_nifti_info)
     L.hysco_nifti_info_read.argtypes = [ctypes.c_char_p, NI]
     L.hysco_nifti_read.argtypes = [ctypes.c_char_p, ctypes.c_int, vp, ctypes.c_int64, NI]
@@ -368,6 +381,15 @@ def hysco_correct_host(ctx, Ip, Im, b_out=None, Ip_corr=None, Im_corr=None, ot_o
 
 def hysco_last_launch_count(ctx):
     return int(lib().hysco_last_launch_count(ctx))
+
+
+def hysco_history(ctx, pair=0):
+    """Per-GN-step records of the last solve (include/hysco.h hysco_history):
+    a list of dicts, record 0 = the GN start."""
+    out = (hysco_iter_record * 64)()
+    n = ctypes.c_int32(0)
+    _check(ctx, lib().hysco_history(ctx, int(pair), out, 64, ctypes.byref(n)))
+    return [out[k].as_dict() for k in range(n.value)]
 
 
 def hysco_profile_kernels(ctx, reps=20, flush_l2=True):

@@ -252,6 +252,39 @@ def test_correct_pipeline_parity(pair, dtype, armijo):
     c.close()
 
 
+@pytest.mark.parametrize("dtype", [H.HYSCO_F32, H.HYSCO_F64], ids=["f32", "f64"])
+@pytest.mark.parametrize("fixed", [1, 0], ids=["fixed", "paper"])
+def test_history_matches_oracle_per_step(dtype, fixed):
+    """hysco_history (P:284 OptimizationLogger): record 0 = the GN start, one
+    record per accepted GN step with the objective parts, the accepted Armijo
+    step and that step's PCG iterations and relative residual -- equal to the
+    oracle's gn_armijo history step by step (same gamma and PCG counts, J and
+    relres to the solve tolerance), consistent with the final report."""
+    p = phantom.make_config("C1_16x16x8")
+    Ip, Im = rnd(p.Ip, dtype), rnd(p.Im, dtype)
+    c = Ctx([Ip], [Im], p.h, dtype)
+    b, Tp, Tm = c.nodes(), c.cells(), c.cells()
+    so = H.default_solve_opts(fixed_iters=fixed, max_gn=10 if fixed else 30)
+    reps, inf = H.hysco_correct(c.ctx, b, Tp, Tm, solve_opts=so)
+    hist = H.hysco_history(c.ctx, 0)
+    c.close()
+    b0r, bref, _, _, rep = O.correct_pair(Ip, Im, p.h, max_gn=10 if fixed else 30, fixed=bool(fixed))
+    r = reps[0]
+    tol = TOL[dtype]["solve"]
+    assert [h["k"] for h in hist] == list(range(r["gn_iters"] + 1))
+    assert len(hist) == len(rep["history"]) + 1
+    J0 = O.evaluate(Ip, Im, b0r, p.h).J
+    assert relS(hist[0]["J"], J0) <= TOL[dtype]["kernel"] and hist[0]["gamma"] == 0.0
+    for h, o in zip(hist[1:], rep["history"]):
+        assert h["gamma"] == o["gamma"] and h["pcg_iters"] == o["pcg_iters"]
+        assert relS(h["J"], o["J"]) <= tol and relS(h["D"], o["D"]) <= 10 * tol
+        assert abs(h["relres"] - o["relres"]) <= 10 * tol * max(o["relres"], 1e-3)
+    assert hist[-1]["J"] == r["J"] and hist[-1]["f_evals"] == r["f_evals"]
+    assert hist[-1]["ls_halvings"] == r["ls_halvings"]
+    assert sum(h["pcg_iters"] for h in hist) == r["pcg_iters"]
+    assert all(hist[k + 1]["J"] <= hist[k]["J"] for k in range(len(hist) - 1))   # Armijo descent
+
+
 def test_batch_pairs_independent():
     pairs = [phantom.make_pair((6, 5, 24), (1.2, 1.0, 1.1), 100 + k) for k in range(3)]
     c = Ctx([p.Ip for p in pairs], [p.Im for p in pairs], pairs[0].h)
