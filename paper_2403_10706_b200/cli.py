@@ -53,6 +53,8 @@ def parse(argv=None):
     ap.add_argument("--dtype", default="f32", choices=["f32", "f64"])
     ap.add_argument("--no-blur", action="store_true")
     ap.add_argument("--device", type=int, default=0)
+    ap.add_argument("--log-iters", action="store_true",
+                    help="per-GN-step history (objective parts, gamma, PCG iterations; P:284) to stderr and the report")
     ap.add_argument("--no-gzip", action="store_true", help="write .nii instead of .nii.gz")
     ap.add_argument("--fieldmap-units", default="voxel", choices=["voxel", "mm"],
                     help="unit of OUT_fieldmap: voxel displacement (default) or mm, along +PE (R31)")
@@ -118,6 +120,12 @@ def main(argv=None):
                                       else H.HYSCO_PRECOND_JACOBI)
             reps, infeas = H.hysco_correct(ctx, b, outs[1:2], outs[2:3], ot, so)
             report = dict(reps[0], stop=H.STOP_NAMES.get(reps[0]["stop_reason"], "?"))
+            if args.log_iters:                   # PyHySCO's OptimizationLogger
+                report["history"] = H.hysco_history(ctx, 0)
+                for r in report["history"]:
+                    print(f"hysco: GN {r['k']:3d}  J {r['J']:.6e}  D {r['D']:.4e}  S {r['S']:.4e}  P {r['P']:.4e}  "
+                          f"|grad| {r['grad_norm']:.3e}  gamma {r['gamma']:.4g}  pcg {r['pcg_iters']}  "
+                          f"relres {r['relres']:.3e}", file=sys.stderr, flush=True)
             infeas = bool(infeas) or not np.isfinite(report["J"])
         else:
             H.hysco_ot_init(ctx, b, ot)

@@ -137,8 +137,9 @@ def test_cli_end_to_end_matches_direct_api(tmp_path, pe):
 
 
 @pytest.mark.parametrize("opts", [["--solver", "admm", "--correction", "lsq", "--pe-axis", "3"],
-                                  ["--precond", "block", "--dtype", "f64", "--pe-axis", "1", "--no-gzip"]],
-                         ids=["admm_lsq_pe3", "block_f64_pe1_plain"])
+                                  ["--precond", "block", "--dtype", "f64", "--pe-axis", "1", "--no-gzip"],
+                                  ["--log-iters", "--pe-axis", "2"]],
+                         ids=["admm_lsq_pe3", "block_f64_pe1_plain", "log_iters_pe2"])
 def test_cli_option_paths(tmp_path, opts):
     """Other CLI paths: outputs exist with the file's shape and voxel sizes and
     are finite; the Jacobian-corrected pair (when written) agrees better than
@@ -176,6 +177,11 @@ def test_cli_option_paths(tmp_path, opts):
         assert O.relative_improvement(Ipf, Imf, tp, tm) > 50.0
     if "lsq" in names:
         assert line["report"]["lsq"]["unconverged"] == 0
+    if "--log-iters" in opts:                    # one record per accepted GN step, descending J
+        hist = line["report"]["history"]
+        assert [h["k"] for h in hist] == list(range(line["report"]["gn_iters"] + 1))
+        assert all(hist[k + 1]["J"] <= hist[k]["J"] for k in range(len(hist) - 1))
+        assert r.stderr.count("hysco: GN ") == len(hist)
 
 
 def test_cli_io_error_in_reader_thread_and_unwritable_output(tmp_path):
