@@ -199,9 +199,12 @@ HYSCO_API void hysco_default_admm_opts(hysco_admm_opts* o);
 /* ADMM field-map solve from d_b_inout (device nodes; e.g. the OT start):
  * b-update = per-column Gauss-Newton with exact tridiagonal solves and
  * per-column Armijo steps (no communication), z-update = periodic in-plane
- * solve by 2-D FFTs (cuFFT) per PE node slice, u-update, residual-balancing
- * of rho on the host between iterations.  Writes the final b.  reports:
- * [batch] or NULL.  Not on slab contexts (the z-update is global in-plane). */
+ * solve by 2-D FFTs (cuFFT) per PE node slice, u-update, residual balancing
+ * of rho and the stop test on the device.  Writes the final b.  reports:
+ * [batch] or NULL.  On an NCCL slab context: this rank's part of the slab
+ * ADMM (transposed z-update, see hysco_group_admm; every rank calls it with
+ * its dense slab); on loopback slab contexts HYSCO_ERR_STATE (use
+ * hysco_group_admm). */
 HYSCO_API hysco_status hysco_admm(hysco_ctx ctx, void* d_b_inout, const hysco_admm_opts* opts,
                                   hysco_admm_report* reports);
 
@@ -360,6 +363,21 @@ HYSCO_API hysco_status hysco_create_slab(const hysco_config* cfg, int32_t rank, 
  * allreduce by a fixed-order device sum).  For testing the slab path on one GPU. */
 HYSCO_API hysco_status hysco_create_loopback(const hysco_config* cfg, int32_t nranks, void* cuda_stream,
                                              hysco_ctx* out);
+
+/* ADMM (hysco_admm, R21-R26) on slabs.  The b-update is column-local on every
+ * rank; the u-update's residual norms are allreduced before the (identical)
+ * residual-balancing decision; the z-update -- the periodic in-plane 2-D
+ * solve (R22), which the split along dim 1 cuts -- runs after a
+ * transpose: rank r receives all n1 planes of its range of PE nodes
+ * [r P / N, (r + 1) P / N) (P = n3 + 1 >= N), transforms with cuFFT, scales and
+ * returns the planes (strided device copies in a loopback group, NCCL send /
+ * receive across processes; hysco_admm on an NCCL slab context runs the same
+ * path with its communicator).  ctxs: a loopback group in rank order;
+ * d_b_inout[r]: rank r's dense slab of nodes [batch][n1_r][n2][n3+1] (device,
+ * overwritten).  Reports as hysco_admm (J of the whole volume).  Equal to the
+ * single-context ADMM up to FFT summation order. */
+HYSCO_API hysco_status hysco_group_admm(hysco_ctx* ctxs, int32_t nranks, void* const* d_b_inout,
+                                        const hysco_admm_opts* opts, hysco_admm_report* reports);
 
 /* Run a loopback group (all ranks, in rank order); per-rank device pointers. */
 HYSCO_API hysco_status hysco_group_correct(hysco_ctx* ctxs, int32_t nranks, const hysco_ot_opts* ot,

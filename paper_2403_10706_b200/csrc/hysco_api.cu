@@ -80,6 +80,7 @@ struct hysco_ctx_s {
     int admm_gx = 1;
     int admm_e = 0;                 // admm_b_kernel register-PCR width ceil(P / 32), 0 = shared-memory PCR
     bool admm_ready = false;
+    struct AdmmSlab* admm_slab = nullptr;   // slab ADMM (transposed z-update), admm_slab_run
     void* own_Tm = nullptr;
     PairState* st = nullptr;
     PairState* h_st = nullptr;          // pinned mirror
@@ -164,6 +165,12 @@ static hysco_status cuda_fail(hysco_ctx c, cudaError_t e, const char* what, int 
     do {                                                                     \
         cudaError_t e_ = (call);                                             \
         if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call, __LINE__);   \
+    } while (0)
+
+#define CK_C(c_, call)                                                        \
+    do {                                                                      \
+        cudaError_t e_ = (call);                                              \
+        if (e_ != cudaSuccess) return cuda_fail((c_), e_, #call, __LINE__);   \
     } while (0)
 
 #define CHECK_CTX()                                                                          \
@@ -1621,6 +1628,371 @@ static hysco_status admm_run(hysco_ctx ctx, void* d_b, const hysco_admm_opts& o,
     return HYSCO_OK;
 }
 
+// ---------------------------------------------------------------------------
+// ADMM on slabs (NEXT-2 at scale, "could be more scalable for datasets
+// of considerably higher resolution"; R21-R26).  The b-update is column-local
+// and runs on every rank's slab; the u-update is elementwise with its residual
+// norms allreduced before the (identical) residual-balancing decision; the
+// z-update -- a 2-D periodic solve over (n1, n2) per PE node l, which the slab
+// split along dim 1 cuts -- runs after a transpose: every rank receives all
+// n1 planes of its range of PE nodes [l0_r, l1_r) (l split evenly over the
+// ranks), layout [n1][n2][Pl] (the batched-R2C layout of the single-context
+// path with P -> Pl), transforms, scales, transforms back and returns the
+// planes.  Each transpose is one strided 2-D copy per (pair, peer): a device
+// copy between the members of a loopback group, NCCL send / receive (with a
+// packed staging buffer) across processes.
+// ---------------------------------------------------------------------------
+struct AdmmSlab {
+    int N = 1, me = 0;
+    std::vector<int> i0, n1l;      // every rank's planes
+    std::vector<int> l0, pl;       // every rank's PE-node range
+    int n1g = 0;
+    void* wT = nullptr;            // [B][n1g][n2][Pl]   (also the returned z)
+    void* spec = nullptr;          // [B][n1g][n2/2+1][Pl] complex
+    void* stage = nullptr;         // NCCL: [B][n1_local][n2][P] packing / receive buffer
+    double* lam = nullptr;         // [n1g][n2/2+1]
+    cufftHandle fwd = 0, inv = 0;
+    bool plans = false;
+};
+
+static void admm_slab_free(hysco_ctx ctx);
+
+template <typename T>
+static hysco_status admm_slab_setup(hysco_ctx ctx, const std::vector<int>& i0, const std::vector<int>& n1l) {
+    if (ctx->admm_slab) return HYSCO_OK;
+    const Geom& g = ctx->g;
+    AdmmSlab* a = new AdmmSlab();
+    ctx->admm_slab = a;
+    a->N = (int)i0.size();
+    a->me = ctx->rank;
+    a->i0 = i0;
+    a->n1l = n1l;
+    a->n1g = g.n1g;
+    for (int r = 0; r < a->N; r++) {
+        a->l0.push_back((int)((long long)r * g.P / a->N));
+        a->pl.push_back((int)((long long)(r + 1) * g.P / a->N) - a->l0.back());
+    }
+    const int Pl = a->pl[a->me];
+    if (Pl < 1) return set_err(ctx, HYSCO_ERR_SHAPE, "slab ADMM needs n3 + 1 >= number of ranks");
+    const int B = (int)ctx->cfg.batch;
+    const size_t nT = (size_t)a->n1g * g.n2 * Pl, nS = (size_t)a->n1g * (g.n2 / 2 + 1) * Pl;
+    CK(cudaMalloc(&a->wT, nT * sizeof(T) * B));
+    CK(cudaMalloc(&a->spec, nS * 2 * sizeof(T) * B));
+    CK(cudaMalloc(&a->stage, (size_t)g.n1 * g.n2 * g.P * sizeof(T) * B));
+    CK(cudaMalloc(&a->lam, sizeof(double) * a->n1g * (g.n2 / 2 + 1)));
+    Geom gg = g;
+    gg.n1 = a->n1g;                  // the periodic in-plane eigenvalues of the whole volume
+    admm_lambda_kernel<<<64, 256, 0, ctx->stream>>>(gg, a->lam);
+    CK(cudaGetLastError());
+    int n[2] = {a->n1g, g.n2}, ine[2] = {a->n1g, g.n2}, one[2] = {a->n1g, g.n2 / 2 + 1};
+    const bool dbl = sizeof(T) == 8;
+    if (cufftPlanMany(&a->fwd, 2, n, ine, Pl, 1, one, Pl, 1, dbl ? CUFFT_D2Z : CUFFT_R2C, Pl) != CUFFT_SUCCESS ||
+        cufftPlanMany(&a->inv, 2, n, one, Pl, 1, ine, Pl, 1, dbl ? CUFFT_Z2D : CUFFT_C2R, Pl) != CUFFT_SUCCESS ||
+        cufftSetStream(a->fwd, ctx->stream) != CUFFT_SUCCESS || cufftSetStream(a->inv, ctx->stream) != CUFFT_SUCCESS)
+        return set_err(ctx, HYSCO_ERR_CUDA, "cuFFT plan creation failed (slab ADMM)");
+    a->plans = true;
+    // the single-context ADMM state (rho, factors, stats, stop flags) is reused
+    CK(cudaMalloc(&ctx->admm_rho, sizeof(double) * B));
+    CK(cudaMalloc(&ctx->admm_fac, sizeof(double) * B));
+    CK(cudaMalloc(&ctx->admm_stat, sizeof(double) * 4 * B));
+    CK(cudaMalloc(&ctx->admm_done, sizeof(unsigned) * (1 + B)));
+    CK(cudaMallocHost(&ctx->h_admm_done, 2 * sizeof(unsigned)));
+    for (int k = 0; k < 2; k++) CK(cudaEventCreateWithFlags(&ctx->admm_ev[k], cudaEventDisableTiming));
+    ctx->admm_smem = (size_t)ADMM_WARPS * admm_warp_elems(g.n3) * sizeof(T);
+    if (ctx->admm_smem > 227 * 1024) return set_err(ctx, HYSCO_ERR_SHAPE, "n3 too large for the ADMM column kernel");
+    ctx->admm_e = (g.P + 31) / 32 <= 8 ? (g.P + 31) / 32 : 0;
+    int occ = 1;
+    cudaError_t ea = cudaSuccess;
+    ADMM_E_SWITCH(ctx->admm_e,
+                  ea = cudaFuncSetAttribute(admm_b_kernel<T, AE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)ctx->admm_smem);
+                  if (ea == cudaSuccess &&
+                      (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, admm_b_kernel<T, AE>, 32 * ADMM_WARPS,
+                                                                     ctx->admm_smem) != cudaSuccess || occ < 1))
+                      occ = 1)
+    CK(ea);
+    const long long work = (g.ncol + ADMM_WARPS - 1) / ADMM_WARPS;
+    const long long cap = ((long long)ctx->nsm * occ + B - 1) / B;
+    ctx->admm_gx = (int)std::max(1LL, std::min(work, cap));
+    return HYSCO_OK;
+}
+
+// Forward transpose: w (slabs, [n1_r][n2][P] per pair) -> wT of every rank
+// ([n1g][n2][Pl_r'] per pair); backward: zT -> zn on the slabs.
+template <typename T>
+static cudaError_t admm_transpose(std::vector<hysco_ctx>& R, CommBase* comm, bool forward, int kw, int kz) {
+    hysco_ctx c0 = R[0];
+    const Geom& g = c0->g;
+    const size_t es = sizeof(T);
+    const int B = (int)c0->cfg.batch;
+    NcclComm* nc1 = dynamic_cast<NcclComm*>(comm);
+    if (dynamic_cast<LoopbackComm*>(comm) || (nc1 && nc1->n == 1)) {   // all ranks' buffers on this device
+        const int N = (int)R.size();
+        for (int r = 0; r < N; r++)
+            for (int q = 0; q < N; q++) {
+                hysco_ctx cr = R[r], cq = R[q];
+                AdmmSlab *ar = cr->admm_slab, *aq = cq->admm_slab;
+                const size_t nTq = (size_t)aq->n1g * g.n2 * aq->pl[q];
+                for (int p = 0; p < B; p++) {
+                    T* slab = L<T>::b(cr, forward ? kw : kz) + (size_t)p * cr->g.ps + ar->l0[q];
+                    T* tq = static_cast<T*>(aq->wT) + (size_t)p * nTq + (size_t)ar->i0[r] * g.n2 * aq->pl[q];
+                    cudaError_t e = forward
+                        ? cudaMemcpy2DAsync(tq, aq->pl[q] * es, slab, (size_t)g.P * es, aq->pl[q] * es,
+                                            (size_t)cr->g.n1 * g.n2, cudaMemcpyDeviceToDevice, c0->stream)
+                        : cudaMemcpy2DAsync(slab, (size_t)g.P * es, tq, aq->pl[q] * es, aq->pl[q] * es,
+                                            (size_t)cr->g.n1 * g.n2, cudaMemcpyDeviceToDevice, c0->stream);
+                    if (e != cudaSuccess) return e;
+                }
+            }
+        return cudaSuccess;
+    }
+    NcclComm* nc = dynamic_cast<NcclComm*>(comm);
+    if (!nc) return cudaErrorInvalidValue;
+    hysco_ctx c = R[0];
+    AdmmSlab* a = c->admm_slab;
+    const int N = a->N, me = a->me;
+    const ncclDataType_t ty = es == 8 ? ncclDouble : ncclFloat;
+    const size_t nT = (size_t)a->n1g * g.n2 * a->pl[me];
+    const size_t nloc = (size_t)g.n1 * g.n2;      // columns of this slab
+    T* st = static_cast<T*>(a->stage);
+    for (int p = 0; p < B; p++) {
+        T* slab = L<T>::b(c, forward ? kw : kz) + (size_t)p * g.ps;
+        T* tme = static_cast<T*>(a->wT) + (size_t)p * nT;
+        T* stp = st + (size_t)p * nloc * g.P;     // packed blocks [q][n1_local n2][Pl_q]
+        if (forward) {
+            for (int q = 0; q < N; q++) {         // pack this slab's l-range of rank q
+                cudaError_t e = cudaMemcpy2DAsync(stp + nloc * a->l0[q], a->pl[q] * es, slab + a->l0[q], (size_t)g.P * es,
+                                                  a->pl[q] * es, nloc, cudaMemcpyDeviceToDevice, c->stream);
+                if (e != cudaSuccess) return e;
+            }
+            if ((nc->last = ncclGroupStart()) != ncclSuccess) return cudaErrorUnknown;
+            for (int q = 0; q < N; q++) {
+                nc->last = ncclSend(stp + nloc * a->l0[q], nloc * a->pl[q], ty, q, nc->comm, c->stream);
+                nc->last = ncclRecv(tme + (size_t)a->i0[q] * g.n2 * a->pl[me], (size_t)a->n1l[q] * g.n2 * a->pl[me], ty, q,
+                                    nc->comm, c->stream);
+            }
+            if ((nc->last = ncclGroupEnd()) != ncclSuccess) return cudaErrorUnknown;
+        } else {
+            if ((nc->last = ncclGroupStart()) != ncclSuccess) return cudaErrorUnknown;
+            for (int q = 0; q < N; q++) {
+                nc->last = ncclSend(tme + (size_t)a->i0[q] * g.n2 * a->pl[me], (size_t)a->n1l[q] * g.n2 * a->pl[me], ty, q,
+                                    nc->comm, c->stream);
+                nc->last = ncclRecv(stp + nloc * a->l0[q], nloc * a->pl[q], ty, q, nc->comm, c->stream);
+            }
+            if ((nc->last = ncclGroupEnd()) != ncclSuccess) return cudaErrorUnknown;
+            for (int q = 0; q < N; q++) {         // unpack rank q's l-range
+                cudaError_t e = cudaMemcpy2DAsync(slab + a->l0[q], (size_t)g.P * es, stp + nloc * a->l0[q], a->pl[q] * es,
+                                                  a->pl[q] * es, nloc, cudaMemcpyDeviceToDevice, c->stream);
+                if (e != cudaSuccess) return e;
+            }
+        }
+    }
+    return cudaSuccess;
+}
+
+// Spectrum scaling on the transposed layout [(k1 (n2/2+1) + k2) Pl + l].
+template <typename C>
+__global__ void __launch_bounds__(256) admm_zscale_t_kernel(Geom g, Ctl c, C* __restrict__ X,
+                                                            const double* __restrict__ rho_p,
+                                                            const double* __restrict__ lam, int n1g, int Pl,
+                                                            long long spec, const unsigned* __restrict__ done) {
+    count_launch(c);
+    if (done[0] || done[1 + blockIdx.y]) return;
+    const int pair = blockIdx.y, lane = threadIdx.x & 31;
+    const double rho = rho_p[pair];
+    const long long nk = (long long)n1g * (g.n2 / 2 + 1);
+    const double sc = 1.0 / ((double)n1g * g.n2);
+    C* Xp = X + (size_t)pair * spec;
+    for (long long kk = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); kk < nk;
+         kk += (long long)gridDim.x * (blockDim.x >> 5)) {
+        const double f = rho / (g.alpha * lam[kk] + rho) * sc;
+        C* row = Xp + kk * Pl;
+        for (int l = lane; l < Pl; l += 32) {
+            row[l].x *= f;
+            row[l].y *= f;
+        }
+    }
+}
+
+template <typename T>
+static hysco_status admm_slab_run(std::vector<hysco_ctx>& R, CommBase* comm, const hysco_admm_opts& o,
+                                  void* const* d_b, hysco_admm_report* reps) {
+    using C = typename std::conditional<sizeof(T) == 8, cufftDoubleComplex, cufftComplex>::type;
+    hysco_ctx c0 = R[0];
+    const int B = (int)c0->cfg.batch;
+    // every rank's planes: loopback members directly, NCCL ranks by an allgather
+    std::vector<int> i0, n1l;
+    if (dynamic_cast<LoopbackComm*>(comm)) {
+        for (hysco_ctx c : R) {
+            i0.push_back(c->g.i0);
+            n1l.push_back(c->g.n1);
+        }
+    } else {
+        NcclComm* nc = dynamic_cast<NcclComm*>(comm);
+        if (!nc) return set_err(c0, HYSCO_ERR_STATE, "slab ADMM needs a loopback group or an NCCL slab context");
+        i0.assign(nc->n, 0);
+        n1l.assign(nc->n, 0);
+        if (nc->n == 1) {
+            i0[0] = c0->g.i0;
+            n1l[0] = c0->g.n1;
+        } else if (!c0->admm_slab) {
+            int* d = nullptr;
+            CK_C(c0, cudaMalloc(&d, sizeof(int) * 2 * (nc->n + 1)));
+            int mine[2] = {c0->g.i0, c0->g.n1};
+            CK_C(c0, cudaMemcpy(d, mine, sizeof mine, cudaMemcpyHostToDevice));
+            if ((nc->last = ncclAllGather(d, d + 2, 2, ncclInt32, nc->comm, c0->stream)) != ncclSuccess) {
+                cudaFree(d);
+                return set_err(c0, HYSCO_ERR_NCCL, "ncclAllGather of the slab bounds failed");
+            }
+            std::vector<int> h(2 * nc->n);
+            CK_C(c0, cudaMemcpyAsync(h.data(), d + 2, sizeof(int) * 2 * nc->n, cudaMemcpyDeviceToHost, c0->stream));
+            CK_C(c0, cudaStreamSynchronize(c0->stream));
+            cudaFree(d);
+            for (int r = 0; r < nc->n; r++) {
+                i0[r] = h[2 * r];
+                n1l[r] = h[2 * r + 1];
+            }
+        }
+    }
+    for (hysco_ctx c : R)
+        if (hysco_status s = admm_slab_setup<T>(c, i0, n1l)) return s;
+    const Geom& g = c0->g;
+    const double rho0 = o.rho0 > 0 ? o.rho0 : g.alpha * (g.ih1sq + g.ih2sq);
+    std::vector<double> rho(B, rho0), stat((size_t)4 * B, 0.0);
+    cudaError_t err = cudaSuccess;
+    auto ok = [&](cudaError_t e) {
+        if (err == cudaSuccess && e != cudaSuccess) err = e;
+    };
+    for (size_t r = 0; r < R.size(); r++) {
+        hysco_ctx c = R[r];
+        const size_t nbl = (size_t)B * c->g.Nn * sizeof(T);
+        ok(cudaMemsetAsync(c->launches, 0, sizeof(unsigned long long), c->stream));
+        ok(cudaMemcpyAsync(c->admm_rho, rho.data(), sizeof(double) * B, cudaMemcpyHostToDevice, c->stream));
+        ok(cudaMemsetAsync(c->admm_done, 0, sizeof(unsigned) * (1 + B), c->stream));
+        ok(cudaMemsetAsync(c->admm_stat, 0, sizeof(double) * 4 * B, c->stream));
+        ok(copy_nodes(c, c->buf[B_B], d_b[r], true, cudaMemcpyDeviceToDevice));
+        ok(copy_nodes(c, c->buf[B_R], d_b[r], true, cudaMemcpyDeviceToDevice));   // z0 = b0
+        for (int p = 0; p < B; p++)                                                 // u0 = 0
+            ok(cudaMemsetAsync(L<T>::b(c, B_P) + (size_t)p * c->g.ps, 0, c->g.Nn * sizeof(T), c->stream));
+        (void)nbl;
+    }
+    for (int k = 0; k < o.max_iter && err == cudaSuccess; k++) {
+        if (!o.fixed_iters && k >= 2) {      // every rank holds the same stop flags (identical decisions)
+            ok(cudaEventSynchronize(c0->admm_ev[k & 1]));
+            if (c0->h_admm_done[k & 1]) break;
+        }
+        for (hysco_ctx c : R) {
+            const dim3 gb(c->admm_gx, B), gn(c->gx_cells, B);
+            for (int p = 0; p < B; p++)
+                ok(cudaMemcpyAsync(L<T>::b(c, B_BOLD) + (size_t)p * c->g.ps, L<T>::b(c, B_B) + (size_t)p * c->g.ps,
+                                   c->g.Nn * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
+            ADMM_E_SWITCH(c->admm_e,
+                          admm_b_kernel<T, AE><<<gb, 32 * ADMM_WARPS, c->admm_smem, c->stream>>>(
+                              c->g, c->ctl, (const T*)c->Ip, (const T*)c->Im, L<T>::b(c, B_B), L<T>::b(c, B_R),
+                              L<T>::b(c, B_P), c->admm_rho, o.inner, o.armijo_c1, o.ls_max, o.col_tol, c->admm_done))
+            admm_rhs_kernel<T><<<gn, 256, 0, c->stream>>>(c->g, c->ctl, L<T>::b(c, B_B), L<T>::b(c, B_P),
+                                                           L<T>::b(c, B_HP), c->admm_done);
+        }
+        ok(cudaGetLastError());
+        ok(admm_transpose<T>(R, comm, true, B_HP, B_TMP));
+        for (hysco_ctx c : R) {
+            AdmmSlab* a = c->admm_slab;
+            const int Pl = a->pl[a->me];
+            const long long nT = (long long)a->n1g * g.n2 * Pl, nS = (long long)a->n1g * (g.n2 / 2 + 1) * Pl;
+            for (int p = 0; p < B; p++) {
+                T* wt = static_cast<T*>(a->wT) + (size_t)p * nT;
+                C* X = static_cast<C*>(a->spec) + (size_t)p * nS;
+                cufftResult r = sizeof(T) == 8 ? cufftExecD2Z(a->fwd, (cufftDoubleReal*)wt, (cufftDoubleComplex*)X)
+                                               : cufftExecR2C(a->fwd, (cufftReal*)wt, (cufftComplex*)X);
+                if (r != CUFFT_SUCCESS) return set_err(c, HYSCO_ERR_CUDA, "cuFFT forward transform failed (slab)");
+            }
+            admm_zscale_t_kernel<C><<<dim3(c->gx_cells, B), 256, 0, c->stream>>>(
+                c->g, c->ctl, static_cast<C*>(a->spec), c->admm_rho, a->lam, a->n1g, Pl, nS, c->admm_done);
+            for (int p = 0; p < B; p++) {
+                T* wt = static_cast<T*>(a->wT) + (size_t)p * nT;
+                C* X = static_cast<C*>(a->spec) + (size_t)p * nS;
+                cufftResult r = sizeof(T) == 8 ? cufftExecZ2D(a->inv, (cufftDoubleComplex*)X, (cufftDoubleReal*)wt)
+                                               : cufftExecC2R(a->inv, (cufftComplex*)X, (cufftReal*)wt);
+                if (r != CUFFT_SUCCESS) return set_err(c, HYSCO_ERR_CUDA, "cuFFT inverse transform failed (slab)");
+            }
+        }
+        ok(cudaGetLastError());
+        ok(admm_transpose<T>(R, comm, false, B_HP, B_TMP));   // z_new on the slabs
+        for (hysco_ctx c : R) {
+            const dim3 gn(c->gx_cells, B);
+            admm_u_kernel<T><<<gn, 256, 0, c->stream>>>(c->g, c->ctl, L<T>::b(c, B_B), L<T>::b(c, B_BOLD),
+                                                         L<T>::b(c, B_TMP), L<T>::b(c, B_R), L<T>::b(c, B_P),
+                                                         c->admm_done);
+        }
+        ok(cudaGetLastError());
+        ok(comm->allreduce(R, false));        // residual norms of the whole volume
+        for (hysco_ctx c : R) {
+            const dim3 gn(c->gx_cells, B);
+            admm_balance_kernel<<<1, 256, 0, c->stream>>>(c->ctl, B, c->admm_rho, c->admm_fac, c->admm_stat,
+                                                           c->admm_done, k, o.mu, o.tau, o.tol, o.fixed_iters);
+            admm_scale_u_kernel<T><<<gn, 256, 0, c->stream>>>(c->g, c->ctl, L<T>::b(c, B_P), c->admm_fac);
+        }
+        ok(cudaGetLastError());
+        if (!o.fixed_iters) {
+            ok(cudaMemcpyAsync(&c0->h_admm_done[k & 1], c0->admm_done, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                               c0->stream));
+            ok(cudaEventRecord(c0->admm_ev[k & 1], c0->stream));
+        }
+    }
+    // b out, then the objective of the result (slab evaluation: halo, allreduce, decision)
+    for (size_t r = 0; r < R.size(); r++) ok(copy_nodes(R[r], d_b[r], R[r]->buf[B_B], false, cudaMemcpyDeviceToDevice));
+    {
+        SegExec x{c0};
+        x.graph = false;
+        SolveParams sp{};
+        SlabRun<T> run{R, comm, sp, x};
+        run.eval(EVAL_PLAIN);
+        ok(run.err);
+    }
+    ok(cudaMemcpyAsync(stat.data(), c0->admm_stat, sizeof(double) * 4 * B, cudaMemcpyDeviceToHost, c0->stream));
+    ok(cudaMemcpyAsync(rho.data(), c0->admm_rho, sizeof(double) * B, cudaMemcpyDeviceToHost, c0->stream));
+    for (hysco_ctx c : R) {
+        ok(cudaMemcpyAsync(c->h_st, c->st, sizeof(PairState) * B, cudaMemcpyDeviceToHost, c->stream));
+        ok(cudaMemcpyAsync(c->h_launches, c->launches, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+    }
+    for (hysco_ctx c : R) ok(cudaStreamSynchronize(c->stream));
+    if (err != cudaSuccess) {
+        const bool nccl = dynamic_cast<NcclComm*>(comm) && static_cast<NcclComm*>(comm)->last != ncclSuccess;
+        for (hysco_ctx c : R) cuda_fail(c, err, nccl ? "slab ADMM (NCCL)" : "slab ADMM", __LINE__);
+        return nccl ? HYSCO_ERR_NCCL : HYSCO_ERR_CUDA;
+    }
+    for (hysco_ctx c : R) {
+        c->last_launches = (long long)*c->h_launches;
+        c->state_valid = false;
+    }
+    for (int p = 0; p < B && reps; p++) {
+        const PairState& s = c0->h_st[p];
+        reps[p].iters = (int32_t)stat[4 * p + 0];
+        reps[p].converged = stat[4 * p + 3] != 0.0;
+        reps[p].rho = rho[p];
+        reps[p].r_norm = stat[4 * p + 1];
+        reps[p].s_norm = stat[4 * p + 2];
+        reps[p].J = s.J;
+        reps[p].D = s.D;
+        reps[p].S = s.S;
+        reps[p].P = s.P;
+    }
+    return HYSCO_OK;
+}
+
+static void admm_slab_free(hysco_ctx ctx) {
+    AdmmSlab* a = ctx->admm_slab;
+    if (!a) return;
+    if (a->plans) {
+        cufftDestroy(a->fwd);
+        cufftDestroy(a->inv);
+    }
+    for (void* q : {a->wT, a->spec, a->stage, (void*)a->lam})
+        if (q) cudaFree(q);
+    delete a;
+    ctx->admm_slab = nullptr;
+}
+
 extern "C" {
 
 void hysco_default_solve_opts(hysco_solve_opts* o) {
@@ -2018,7 +2390,6 @@ void hysco_default_admm_opts(hysco_admm_opts* o) {
 hysco_status hysco_admm(hysco_ctx ctx, void* d_b_inout, const hysco_admm_opts* opts, hysco_admm_report* reports) {
     NvtxRange nvtx_("hysco_admm");
     CHECK_CTX();
-    if (ctx->g.slab) return set_err(ctx, HYSCO_ERR_STATE, "ADMM is not available on slab contexts");
     if (hysco_status s = need_images(ctx)) return s;
     if (!d_b_inout || !aligned16(d_b_inout)) return set_err(ctx, HYSCO_ERR_ARG, "d_b_inout must be 16-byte aligned");
     hysco_admm_opts o;
@@ -2026,8 +2397,39 @@ hysco_status hysco_admm(hysco_ctx ctx, void* d_b_inout, const hysco_admm_opts* o
     if (opts) o = *opts;
     if (o.max_iter < 0 || o.inner < 1 || o.ls_max < 1 || !(o.tol >= 0) || !(o.mu > 1) || !(o.tau > 1))
         return set_err(ctx, HYSCO_ERR_ARG, "bad hysco_admm_opts");
+    if (ctx->g.slab) {   // one rank of a multi-process slab group (NCCL transposes)
+        if (!dynamic_cast<NcclComm*>(ctx->comm))
+            return set_err(ctx, HYSCO_ERR_STATE, "loopback slab contexts run ADMM with hysco_group_admm");
+        std::vector<hysco_ctx> R{ctx};
+        void* const bi[1] = {d_b_inout};
+        return ctx->cfg.dtype == HYSCO_F64 ? admm_slab_run<double>(R, ctx->comm, o, bi, reports)
+                                           : admm_slab_run<float>(R, ctx->comm, o, bi, reports);
+    }
     return ctx->cfg.dtype == HYSCO_F64 ? admm_run<double>(ctx, d_b_inout, o, reports)
                                        : admm_run<float>(ctx, d_b_inout, o, reports);
+}
+
+hysco_status hysco_group_admm(hysco_ctx* ctxs, int32_t nranks, void* const* d_b_inout, const hysco_admm_opts* opts,
+                              hysco_admm_report* reports) {
+    NvtxRange nvtx_("hysco_group_admm");
+    if (!ctxs || nranks < 1 || !d_b_inout) return HYSCO_ERR_ARG;
+    LoopbackComm* lb = dynamic_cast<LoopbackComm*>(ctxs[0]->comm);
+    if (!lb || (int)lb->members.size() != nranks) return set_err(ctxs[0], HYSCO_ERR_STATE, "not a loopback group");
+    for (int r = 0; r < nranks; r++) {
+        if (ctxs[r] != lb->members[r]) return set_err(ctxs[0], HYSCO_ERR_ARG, "contexts must be passed in rank order");
+        if (ctxs[r]->poisoned) return HYSCO_ERR_CUDA;
+        if (hysco_status s = need_images(ctxs[r])) return s;
+        if (!d_b_inout[r]) return HYSCO_ERR_ARG;
+    }
+    hysco_admm_opts o;
+    hysco_default_admm_opts(&o);
+    if (opts) o = *opts;
+    if (o.max_iter < 0 || o.inner < 1 || o.ls_max < 1 || !(o.tol >= 0) || !(o.mu > 1) || !(o.tau > 1))
+        return set_err(ctxs[0], HYSCO_ERR_ARG, "bad hysco_admm_opts");
+    std::vector<hysco_ctx> R(ctxs, ctxs + nranks);
+    cudaSetDevice(ctxs[0]->cfg.device);
+    return ctxs[0]->cfg.dtype == HYSCO_F64 ? admm_slab_run<double>(R, lb, o, d_b_inout, reports)
+                                           : admm_slab_run<float>(R, lb, o, d_b_inout, reports);
 }
 
 void hysco_default_lsq_opts(hysco_lsq_opts* o) {
@@ -2563,6 +2965,7 @@ hysco_status hysco_destroy(hysco_ctx ctx) {
         if (p) cudaFree(p);
     if (ctx->flush) cudaFree(ctx->flush);
     if (ctx->res_part) cudaFree(ctx->res_part);
+    admm_slab_free(ctx);
     if (ctx->res_flags) cudaFree(ctx->res_flags);
     if (ctx->admm_ready) {
         cufftDestroy(ctx->fft_fwd);

@@ -28,7 +28,7 @@ EXPORTED = ["hysco_default_solve_opts", "hysco_default_ot_opts", "hysco_default_
             "hysco_last_launch_count", "hysco_history",
             "hysco_last_error", "hysco_destroy", "hysco_version", "hysco_profile_kernels",
             "hysco_nccl_unique_id", "hysco_create_slab", "hysco_create_loopback", "hysco_group_correct",
-            "hysco_group_solve", "hysco_push_forward", "hysco_default_lsq_opts", "hysco_lsq_correct",
+            "hysco_group_solve", "hysco_group_admm", "hysco_push_forward", "hysco_default_lsq_opts", "hysco_lsq_correct",
             # front-end (include/hysco_io.h)
             "hysco_nifti_info_read", "hysco_nifti_read", "hysco_nifti_write", "hysco_io_last_error", "hysco_pe_shape",
             "hysco_permute_pe", "hysco_fieldmap_cells", "hysco_fieldmap_cells_units"]
@@ -207,6 +207,9 @@ def lib():
     L.hysco_group_solve.argtypes = [ctypes.POINTER(vp), ctypes.c_int32, ctypes.POINTER(vp),
                                     ctypes.POINTER(hysco_solve_opts), ctypes.POINTER(hysco_report)]
     L.hysco_group_solve.restype = st
+    L.hysco_group_admm.argtypes = [ctypes.POINTER(vp), ctypes.c_int32, ctypes.POINTER(vp),
+                                   ctypes.POINTER(hysco_admm_opts), ctypes.POINTER(hysco_admm_report)]
+    L.hysco_group_admm.restype = st
     L.hysco_version.argtypes = []
     L.hysco_version.restype = ctypes.c_int32
     _lib = L
@@ -453,6 +456,17 @@ def hysco_group_correct(ctxs, b_out=None, Ip_corr=None, Im_corr=None, ot_opts=No
                                                   _ptrs(b_out, n), _ptrs(Ip_corr, n), _ptrs(Im_corr, n), reps),
                (HYSCO_OK, HYSCO_INFEASIBLE))
     return [r.as_dict() for r in reps], s == HYSCO_INFEASIBLE
+
+
+def hysco_group_admm(ctxs, b_inout, opts=None, batch=1):
+    """ADMM on a loopback slab group (the transposed z-update, include/hysco.h):
+    b_inout[r] = rank r's dense slab of nodes (overwritten); per-pair reports."""
+    n = len(ctxs)
+    cs = (ctypes.c_void_p * n)(*ctxs)
+    reps = (hysco_admm_report * batch)()
+    _check(ctxs[0], lib().hysco_group_admm(cs, n, _ptrs(b_inout, n), ctypes.byref(opts) if opts is not None else None,
+                                           reps))
+    return [r.as_dict() for r in reps]
 
 
 def hysco_group_solve(ctxs, b_inout, solve_opts=None, batch=1):

@@ -206,3 +206,87 @@ def test_loopback_slabs_push_forward_and_lsq_equal_single(nranks):
     assert np.array_equal(np.concatenate(got_p, axis=1), ref_p)
     assert np.array_equal(np.concatenate(got_m, axis=1), ref_m)
     assert np.array_equal(np.concatenate(got_t, axis=1), ref_t)
+
+
+def admm_single(Ip, Im, b0, h, dtype, ao, batch):
+    n1, n2, n3 = Ip.shape[1:]
+    ctx = H.hysco_create((n1, n2, n3), h, batch, dtype=dtype)
+    tIp = torch.from_numpy(Ip.astype(ND[dtype])).to(DEV)
+    tIm = torch.from_numpy(Im.astype(ND[dtype])).to(DEV)
+    H.hysco_bind_images(ctx, tIp, tIm)
+    b = torch.from_numpy(np.ascontiguousarray(b0).astype(ND[dtype])).to(DEV)
+    torch.cuda.synchronize()
+    reps = H.hysco_admm(ctx, b, ao, batch=batch)
+    torch.cuda.synchronize()
+    H.hysco_destroy(ctx)
+    return b.cpu().numpy(), reps
+
+
+def admm_grouped(Ip, Im, b0, h, dtype, ao, batch, nranks):
+    n1, n2, n3 = Ip.shape[1:]
+    ctxs = H.hysco_create_loopback((n1, n2, n3), h, nranks, batch=batch, dtype=dtype)
+    keep, bs = [], []
+    for r, c in enumerate(ctxs):
+        i0, i1 = H.slab_bounds(n1, nranks, r)
+        tIp = torch.from_numpy(np.ascontiguousarray(Ip[:, i0:i1]).astype(ND[dtype])).to(DEV)
+        tIm = torch.from_numpy(np.ascontiguousarray(Im[:, i0:i1]).astype(ND[dtype])).to(DEV)
+        keep += [tIp, tIm]
+        H.hysco_bind_images(c, tIp, tIm)
+        bs.append(torch.from_numpy(np.ascontiguousarray(b0[:, i0:i1]).astype(ND[dtype])).to(DEV))
+    torch.cuda.synchronize()
+    reps = H.hysco_group_admm(ctxs, bs, ao, batch=batch)
+    torch.cuda.synchronize()
+    for c in ctxs:
+        H.hysco_destroy(c)
+    return np.concatenate([t.cpu().numpy() for t in bs], axis=1), reps
+
+
+ADMM_SLAB = [(1, (8, 6, 20), 2), (2, (8, 6, 20), 2), (3, (7, 5, 24), 1), (4, (12, 10, 24), 1)]
+
+
+@pytest.mark.parametrize("stop", ["fixed", "paper"])
+@pytest.mark.parametrize("dtype", [H.HYSCO_F64, H.HYSCO_F32], ids=["f64", "f32"])
+@pytest.mark.parametrize("nranks,shape,batch", ADMM_SLAB, ids=[f"r{c[0]}-{c[1]}" for c in ADMM_SLAB])
+def test_loopback_admm_equals_single(nranks, shape, batch, dtype, stop):
+    """ADMM on slabs (hysco_group_admm): the column-local b-update on every
+    slab, the transposed z-update (every rank transforms all n1 planes of its
+    range of PE nodes), allreduced residual norms -- equal to the
+    single-context ADMM (same iterations, rho and stop decisions; b to fp64
+    summation order / the fp32 gate) and, in fp64, to the oracle."""
+    h = (1.25, 1.1, 1.2)
+    pairs = [phantom.make_pair(shape, h, 60 + k) for k in range(batch)]
+    Ip = np.stack([q.Ip for q in pairs]).astype(ND[dtype]).astype(np.float64)
+    Im = np.stack([q.Im for q in pairs]).astype(ND[dtype]).astype(np.float64)
+    b0 = np.stack([O.ot_init(Ip[k], Im[k], h[2])[0] for k in range(batch)]).astype(ND[dtype]).astype(np.float64)
+    ao = H.default_admm_opts(max_iter=12, fixed_iters=1) if stop == "fixed" else H.default_admm_opts(max_iter=50)
+    b1, r1 = admm_single(Ip, Im, b0, h, dtype, ao, batch)
+    b2, r2 = admm_grouped(Ip, Im, b0, h, dtype, ao, batch, nranks)
+    tol = 1e-11 if dtype == H.HYSCO_F64 else 1e-4
+    for k in range(batch):
+        assert (r2[k]["iters"], r2[k]["converged"]) == (r1[k]["iters"], r1[k]["converged"])
+        assert abs(r2[k]["rho"] - r1[k]["rho"]) <= 1e-12 * r1[k]["rho"]
+        assert rel(b2[k], b1[k]) <= tol
+        assert abs(r2[k]["J"] - r1[k]["J"]) <= tol * abs(r1[k]["J"])
+        if dtype == H.HYSCO_F64 and stop == "fixed":
+            bref, _, rep = O.admm(Ip[k], Im[k], b0[k], h, max_iter=12, fixed=True)
+            assert rel(b2[k], bref) <= 1e-12
+
+
+def test_nccl_slab_one_rank_admm_equals_single():
+    """hysco_admm on an NCCL slab context (one rank: the transposes are NCCL
+    self send / receive) equals the single-context ADMM."""
+    p = phantom.make_pair((8, 6, 20), (1.25, 1.1, 1.2), 61)
+    Ip, Im = p.Ip[None].astype(np.float64), p.Im[None].astype(np.float64)
+    b0 = O.ot_init(Ip[0], Im[0], p.h[2])[0][None]
+    ao = H.default_admm_opts(max_iter=10, fixed_iters=1)
+    b1, r1 = admm_single(Ip, Im, b0, p.h, H.HYSCO_F64, ao, 1)
+    n1, n2, n3 = Ip.shape[1:]
+    ctx = H.hysco_create_slab((n1, n2, n3), p.h, 0, 1, n1, 0, dtype=H.HYSCO_F64)
+    tIp, tIm = torch.from_numpy(Ip).to(DEV), torch.from_numpy(Im).to(DEV)
+    H.hysco_bind_images(ctx, tIp, tIm)
+    b = torch.from_numpy(np.ascontiguousarray(b0)).to(DEV)
+    torch.cuda.synchronize()
+    r2 = H.hysco_admm(ctx, b, ao)
+    torch.cuda.synchronize()
+    H.hysco_destroy(ctx)
+    assert r2[0]["iters"] == r1[0]["iters"] and rel(b.cpu().numpy(), b1) <= 1e-11
