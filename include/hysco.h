@@ -313,6 +313,14 @@ HYSCO_API hysco_status hysco_history(hysco_ctx ctx, int32_t pair, hysco_iter_rec
  * nodes executed, counted on the device). */
 HYSCO_API int64_t hysco_last_launch_count(hysco_ctx ctx);
 
+/* Which Jacobi-PCG implementation the context's solves use (fixed at create,
+ * DESIGN.md §7): 0 streaming kernels, 1 on-chip-resident PCG over 1-D strips
+ * of consecutive PE columns per SM, 2 on-chip-resident PCG over 2-D column
+ * tiles, 3 L2-resident persistent PCG; -1 for a NULL context.  tile_out
+ * (4 int32, may be NULL) receives (TI, TJ, TH, TW) for path 2 -- TI x TJ
+ * tiles of TH x TW columns -- else zeros. */
+HYSCO_API int32_t hysco_pcg_path(hysco_ctx ctx, int32_t* tile_out);
+
 /* Profiling hook for the roofline figures: after a solve, re-launches each
  * hot kernel `reps` times on the context stream in the solve's launch
  * configuration and on its buffers, timing each launch with CUDA events.

@@ -123,6 +123,8 @@ struct hysco_ctx_s {
     // on-chip-resident PCG (hysco_resident.cuh): fp32, one CTA per SM
     bool resident = false;
     int res_k = 0, res_grid = 0;
+    bool res_tiled = false;      // 2-D tiles of columns per CTA (hysco_resident.cuh ResTile)
+    ResTile res_tile{0, 0, 0, 0};
     size_t res_smem = 0;
     double* res_part = nullptr;
     unsigned* res_flags = nullptr;   // p-halo flags + launch counter (hysco_resident.cuh)
@@ -473,19 +475,26 @@ static void launch_resident(hysco_ctx c, const SolveParams& sp, int pair, float*
     for (int k = 0; k < NBUF; k++)   // the view's first pair (scratch shared in a per-pair view, L<T>::b)
         B[k] = static_cast<float*>(c->buf[k]) + (k == B_B || !c->vshare ? c->vp : 0) * c->g.ps;
     const int nb = c->vb;
-    if (sp.fixed) {
-        RES_K_SWITCH(c->res_k, cudaLaunchKernelEx(&cfg, pcg_resident_kernel<RK, true>, c->g, c->ctl, sp, pair,
-                                                  (const float*)B[B_GRAD], (const float*)B[B_DT],
-                                                  (const float*)B[B_ET], B[B_X], c->res_x, c->res_pg,
-                                                  c->res_part, c->res_flags, c->res_wi, c->res_wj, bcur, bold,
-                                                  nb, (unsigned long long*)nullptr));
+#define RES_LAUNCH(FX, TL)                                                                                        \
+    RES_K_SWITCH(c->res_k, cudaLaunchKernelEx(&cfg, pcg_resident_kernel<RK, FX, false, TL>, c->g, c->ctl, sp, pair, \
+                                              (const float*)B[B_GRAD], (const float*)B[B_DT],                     \
+                                              (const float*)B[B_ET], B[B_X], c->res_x, c->res_pg, c->res_part,    \
+                                              c->res_flags, c->res_wi, c->res_wj, bcur, bold, nb,                 \
+                                              (unsigned long long*)nullptr, c->res_tile))
+    if (c->res_tiled) {
+        if (sp.fixed) {
+            RES_LAUNCH(true, true);
+        } else {
+            RES_LAUNCH(false, true);
+        }
     } else {
-        RES_K_SWITCH(c->res_k, cudaLaunchKernelEx(&cfg, pcg_resident_kernel<RK, false>, c->g, c->ctl, sp, pair,
-                                                  (const float*)B[B_GRAD], (const float*)B[B_DT],
-                                                  (const float*)B[B_ET], B[B_X], c->res_x, c->res_pg,
-                                                  c->res_part, c->res_flags, c->res_wi, c->res_wj, bcur, bold,
-                                                  nb, (unsigned long long*)nullptr));
+        if (sp.fixed) {
+            RES_LAUNCH(true, false);
+        } else {
+            RES_LAUNCH(false, false);
+        }
     }
+#undef RES_LAUNCH
 }
 
 // Persistent L2-resident PCG (hysco_l2pcg.cuh) for pair `pair` of the view.
@@ -521,12 +530,12 @@ static void launch_l2pcg(hysco_ctx c, const SolveParams& sp, int pair) {
 static bool alloc_persistent_sync(hysco_ctx ctx) {
     if (ctx->res_part) return true;
     const int G = ctx->nsm;
-    if (cudaMalloc(&ctx->res_part, sizeof(double) * 3 * RES_PART_DOUBLES) != cudaSuccess ||
+    if (cudaMalloc(&ctx->res_part, sizeof(double) * (3 * RES_PART_DOUBLES + RES_LIMB_DOUBLES)) != cudaSuccess ||
         cudaMalloc(&ctx->res_flags, sizeof(unsigned) * res_flags_words(G)) != cudaSuccess) {
         cudaGetLastError();
         return false;
     }
-    cudaMemset(ctx->res_part, 0, sizeof(double) * 3 * RES_PART_DOUBLES);
+    cudaMemset(ctx->res_part, 0, sizeof(double) * (3 * RES_PART_DOUBLES + RES_LIMB_DOUBLES));
     cudaMemset(ctx->res_flags, 0, sizeof(unsigned) * res_flags_words(G));
     const unsigned first_launch = 1;      // tags of launch 0 would match the zeroed slots
     cudaMemcpy(ctx->res_flags + (size_t)G * RES_FLAG_STRIDE, &first_launch, sizeof(unsigned), cudaMemcpyHostToDevice);
@@ -569,11 +578,37 @@ static void setup_resident(hysco_ctx ctx) {
     const Geom& g = ctx->g;
     const int G = ctx->nsm;
     if (g.ncol < G) return;
+    if (G >= 256) return;                // one arrival byte in the limb all-reduce words
     const long long ncl_max = (g.ncol + G - 1) / G;
     const long long nqmax = ncl_max * (res_pad(g.P) / 2);   // node pairs per CTA
     const long long need_k = (nqmax + RES_THREADS - 1) / RES_THREADS;
     if (need_k > RES_KMAX) return;
     const int k = need_k <= RES_KMAX / 3 ? RES_KMAX / 3 : need_k <= 2 * RES_KMAX / 3 ? 2 * RES_KMAX / 3 : RES_KMAX;
+    // 2-D tiles (hysco_resident.cuh ResTile): an exact tiling n1 = TI TH, n2 = TJ TW
+    // with TI TJ CTAs (>= 95 % of the SMs, <= G), TH TW columns in the same slot
+    // count k, TW GPC <= NT and (TH - 1) TW GPC >= (k - 1) NT; fewest perimeter
+    // columns (2 TH + 2 TW) wins.  HYSCO_RES_TILED=0: 1-D strips.
+    ctx->res_tiled = false;
+    if (!(getenv("HYSCO_RES_TILED") && getenv("HYSCO_RES_TILED")[0] == '0') && g.slab == 0) {
+        const int GPC = res_pad(g.P) / 2;
+        long long best = -1;
+        for (int TH = 1; TH <= g.n1; TH++) {
+            if (g.n1 % TH) continue;
+            for (int TW = 1; TW <= g.n2; TW++) {
+                if (g.n2 % TW) continue;
+                const long long tiles = (long long)(g.n1 / TH) * (g.n2 / TW);
+                const long long twg = (long long)TW * GPC, nq = (long long)TH * twg;
+                if (tiles > G || tiles * 20 < (long long)G * 19 || nq > (long long)k * RES_THREADS) continue;
+                if (twg > RES_THREADS || (TH - 1) * twg < (long long)(k - 1) * RES_THREADS) continue;
+                const long long cost = 2LL * TH + 2LL * TW;
+                if (best < 0 || cost < best) {
+                    best = cost;
+                    ctx->res_tile = ResTile{g.n1 / TH, g.n2 / TW, TH, TW};
+                }
+            }
+        }
+        ctx->res_tiled = best >= 0;
+    }
     const size_t smem = res_smem_bytes(k);   // layout: hysco_resident.cuh
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->cfg.device);
@@ -582,14 +617,12 @@ static void setup_resident(hysco_ctx ctx) {
     if (smem + fa.sharedSizeBytes > (size_t)optin) return;
     cudaError_t err = cudaSuccess;
     RES_K_SWITCH(k, {
-        err = cudaFuncSetAttribute(pcg_resident_kernel<RK, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem);
-        if (err == cudaSuccess)
-            err = cudaFuncSetAttribute(pcg_resident_kernel<RK, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
-        if (err == cudaSuccess)
-            err = cudaFuncSetAttribute(pcg_sync_floor_kernel<RK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+        const void* fns[6] = {(const void*)pcg_resident_kernel<RK, false>, (const void*)pcg_resident_kernel<RK, true>,
+                              (const void*)pcg_resident_kernel<RK, false, false, true>,
+                              (const void*)pcg_resident_kernel<RK, true, false, true>,
+                              (const void*)pcg_sync_floor_kernel<RK>, (const void*)pcg_sync_floor_kernel<RK, true>};
+        for (int f = 0; f < 6 && err == cudaSuccess; f++)
+            err = cudaFuncSetAttribute(fns[f], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     });
     if (err != cudaSuccess) {
         cudaGetLastError();
@@ -602,10 +635,14 @@ static void setup_resident(hysco_ctx ctx) {
         cudaGetLastError();
         return;
     }
-    const size_t ghost = (res_ghost_pair_floats(g) * ctx->cfg.batch + res_ghost_slack_floats(k)) * sizeof(float);
+    const size_t ghost =
+        std::max(res_ghost_pair_floats(g) * ctx->cfg.batch + res_ghost_slack_floats(k),
+                 ctx->res_tiled ? res_tiled_ghost_floats(G, k) * ctx->cfg.batch : (size_t)0) * sizeof(float);
+    const size_t xpadb = std::max((size_t)g.ncol * res_pad(g.P), ctx->res_tiled ? res_tiled_ghost_floats(G, k) : (size_t)0) *
+                         sizeof(float);
     if (G * 2 > RES_RSTRIDE) return;   // replica layout of the partials (hysco_resident.cuh)
     if (!alloc_persistent_sync(ctx) || cudaMalloc(&ctx->res_pg, ghost) != cudaSuccess ||
-        cudaMalloc(&ctx->res_x, (size_t)g.ncol * res_pad(g.P) * sizeof(float)) != cudaSuccess) {
+        cudaMalloc(&ctx->res_x, xpadb) != cudaSuccess) {
         cudaGetLastError();
         return;
     }
@@ -613,7 +650,7 @@ static void setup_resident(hysco_ctx ctx) {
     ctx->res_k = k;
     ctx->res_wi = (float)(g.ahd * g.ih1sq);
     ctx->res_wj = (float)(g.ahd * g.ih2sq);
-    ctx->res_grid = G;
+    ctx->res_grid = ctx->res_tiled ? ctx->res_tile.TI * ctx->res_tile.TJ : G;
     ctx->res_smem = smem;
     ctx->resident = true;
 }
@@ -2672,6 +2709,19 @@ hysco_status hysco_correct_host_stream(hysco_ctx ctx, int32_t n_items, const voi
 
 int64_t hysco_last_launch_count(hysco_ctx ctx) { return ctx ? ctx->last_launches : -1; }
 
+int32_t hysco_pcg_path(hysco_ctx ctx, int32_t* tile_out) {
+    if (!ctx) return -1;
+    if (tile_out) {
+        const bool t = ctx->resident && ctx->res_tiled;
+        tile_out[0] = t ? ctx->res_tile.TI : 0;
+        tile_out[1] = t ? ctx->res_tile.TJ : 0;
+        tile_out[2] = t ? ctx->res_tile.TH : 0;
+        tile_out[3] = t ? ctx->res_tile.TW : 0;
+    }
+    if (ctx->resident) return ctx->res_tiled ? 2 : 1;
+    return ctx->l2pcg ? 3 : 0;
+}
+
 static_assert(sizeof(hysco_iter_record) == sizeof(HistRec), "hysco_iter_record mirrors HistRec");
 
 hysco_status hysco_history(hysco_ctx ctx, int32_t pair, hysco_iter_record* out, int32_t max_records,
@@ -2880,8 +2930,15 @@ static hysco_status profile_typed(hysco_ctx ctx, int reps, int flush_l2, double*
                     at[0].val.cooperative = 1;
                     cfg.attrs = at;
                     cfg.numAttrs = 1;
-                    RES_K_SWITCH(ctx->res_k, CK(cudaLaunchKernelEx(&cfg, pcg_sync_floor_kernel<RK>, ctx->g, 10,
-                                                                   ctx->res_part, ctx->res_flags)));
+                    if (ctx->res_tiled) {
+                        RES_K_SWITCH(ctx->res_k, CK(cudaLaunchKernelEx(&cfg, pcg_sync_floor_kernel<RK, true>, ctx->g,
+                                                                       10, ctx->res_part, ctx->res_flags,
+                                                                       ctx->res_tile)));
+                    } else {
+                        RES_K_SWITCH(ctx->res_k, CK(cudaLaunchKernelEx(&cfg, pcg_sync_floor_kernel<RK>, ctx->g, 10,
+                                                                       ctx->res_part, ctx->res_flags,
+                                                                       ResTile{0, 0, 0, 0})));
+                    }
                     break;
                 }
                 case HYSCO_PROF_L2PCG: {

@@ -18,8 +18,10 @@
 //     CTA-boundary j-neighbours from L2); p.Hp -> all-reduce
 //   r, z = r/M, r.z, r.r -> publish;  x += a p (L2 adds);  collect
 //   p = z + beta p (shared + global copy) -> release this CTA's p flag
-// Reductions: deterministic fixed-order fold of per-CTA partials performed
-// identically by every CTA, so all CTAs take the same alpha/beta/stop decisions.
+// Reductions: exact integer (fixed-point limb) all-reduces for the PCG
+// scalars, a deterministic fixed-order fold of tagged per-CTA partials for
+// the Armijo start (it has a max): every CTA takes the same alpha / beta /
+// stop decisions, and the results are bitwise reproducible.
 #pragma once
 
 
@@ -44,7 +46,8 @@ __device__ __forceinline__ int opaque(int v) {
 // ---------------------------------------------------------------------------
 // Synchronisation without grid barriers.  The launch is cooperative (all CTAs
 // co-resident), but no cooperative_groups grid sync is used:
-//  * all-reduce: every CTA publishes its fp64 partial with ONE 64-bit store
+//  * all-reduce (the Armijo start; the PCG scalars use the limb all-reduce
+//    below): every CTA publishes its fp64 partial with ONE 64-bit store
 //    whose low 8 mantissa bits carry a tag (launch, iteration); readers poll
 //    the slots until every tag matches and fold them in a fixed order.  The
 //    data is its own flag, so an all-reduce costs one publish and one poll
@@ -193,6 +196,106 @@ __device__ __forceinline__ void reduce_collect(const double* __restrict__ part, 
     for (int k = 0; k < NV; k++) out[k] = stot[k];
 }
 
+// ---------------------------------------------------------------------------
+// Exact fixed-point all-reduce on integer atomics (the per-iteration PCG
+// reductions).  Measured on B200 (tools/sync_bench.cu, 148 x 512 threads):
+// the tagged all-poll above costs ~3.4 us per all-reduce, a release/acquire
+// barrier 1.2 us, this 1.0-1.4 us.  Each value v of a CTA is divided by a
+// power of two 2^e that every CTA derives from the same previous value, and
+// q = v 2^-e (|q| < 2^59) is split EXACTLY into four signed 40-bit limbs of
+// weights 2^20, 2^-20, 2^-60, 2^-100 (floor / subtract / scale: exact fp64
+// steps; the last limb rounds below 2^-100).  Limb w is added to its own
+// 64-bit word as (w << 8) + 1 with one red.add: the word's low byte counts
+// the arrivals, its upper bits sum the limbs (integer: exact and independent
+// of the arrival order).  A fifth word per value counts non-finite or
+// out-of-range partials (result NaN).  Readers poll the words until all G
+// arrivals are in and evaluate the same integer sums identically, so every
+// CTA takes the same decisions and the result is bitwise reproducible.
+// Words are never reset: a reader takes the difference to the word's value
+// after the previous use (kept in shared memory).  Two parity sets: a CTA
+// adds to set s for reduction n + 2 only after reduction n + 1 completed,
+// i.e. after every CTA read reduction n.  Needs G < 256 (one arrival byte).
+// ---------------------------------------------------------------------------
+constexpr int RES_LIMB_W = 16;               // words per parity set (5 per value, NV <= 2)
+constexpr int RES_LIMB_DOUBLES = 64;         // allocation after the three poll buffers (2 sets + pad)
+__device__ __forceinline__ void red_add_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+// Binary exponent of the scale for a value expected near `prev` (same in
+// every CTA: prev is an all-reduced result).
+__device__ __forceinline__ int limb_exp(double prev) {
+    return (prev != 0.0 && isfinite(prev)) ? ilogb(prev) : 0;
+}
+// Read the words' current values (before this launch's first limb reduction;
+// the caller's next __syncthreads orders the loads before any arrival).
+__device__ __forceinline__ void limb_init(const unsigned long long* words, unsigned long long* s_prev) {
+    if (threadIdx.x < 2 * RES_LIMB_W) s_prev[threadIdx.x] = ld_relaxed_u64(words + threadIdx.x);
+}
+template <int NV>
+__device__ __forceinline__ void limb_publish(double (&v)[NV], const int (&ex)[NV], unsigned long long* words, int par) {
+    __shared__ double sred[NV][32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int k = 0; k < NV; k++) {
+        double x = v[k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
+        if (lane == 0) sred[k][wid] = x;
+    }
+    __syncthreads();
+    if (wid < NV) {
+        const int k = wid;
+        double x = lane < nw ? sred[k][lane] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
+        if (lane < 5) {
+            const double q = ldexp(x, -ex[k]);
+            const bool bad = !(fabs(q) < 0x1p59);          // also NaN
+            long long limb = 0;
+            if (!bad) {
+                const double t3 = q * 0x1p-20, l3 = floor(t3);
+                const double t2 = (t3 - l3) * 0x1p40, l2 = floor(t2);
+                const double t1 = (t2 - l2) * 0x1p40, l1 = floor(t1);
+                const double l0 = rint((t1 - l1) * 0x1p40);
+                const double lv = lane == 3 ? l3 : lane == 2 ? l2 : lane == 1 ? l1 : l0;
+                limb = (long long)lv;
+            }
+            const long long add = lane < 4 ? limb * 256 + 1 : (long long)bad * 256 + 1;
+            red_add_u64(words + par * RES_LIMB_W + 5 * k + lane, (unsigned long long)add);
+        }
+    }
+}
+template <int NV>
+__device__ __forceinline__ void limb_collect(const unsigned long long* words, int par, const int (&ex)[NV],
+                                             unsigned long long* s_prev, double (&out)[NV]) {
+    __shared__ double stot[NV];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (wid < NV && lane < 5) {
+        const int G = gridDim.x, w = par * RES_LIMB_W + 5 * wid + lane;
+        const unsigned long long pv = s_prev[w];
+        unsigned long long cur;
+        unsigned spins = 0;
+        while ((((cur = ld_relaxed_u64(words + w)) - pv) & 255ull) != (unsigned long long)G)
+            if (++spins > RES_SPIN_LIMIT) __trap();
+        s_prev[w] = cur;
+        const double L = (double)(((long long)(cur - pv) - G) >> 8);   // exact: |.| < 2^49
+        const double L0 = __shfl_sync(0x1fu, L, 0), L1 = __shfl_sync(0x1fu, L, 1);
+        const double L2 = __shfl_sync(0x1fu, L, 2), L3 = __shfl_sync(0x1fu, L, 3);
+        const double nbad = __shfl_sync(0x1fu, L, 4);
+        if (lane == 0)
+            stot[wid] = nbad != 0.0 ? __longlong_as_double(0x7ff8000000000000ll)
+                                    : ldexp(((L3 * 0x1p20 + L2 * 0x1p-20) + L1 * 0x1p-60) + L0 * 0x1p-100, ex[wid]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < NV; k++) out[k] = stot[k];
+}
+
 // After this CTA's p stores: release its flag (all threads' stores ordered by
 // the CTA barrier, then a gpu-scope release by thread 0).
 __device__ __forceinline__ void halo_release(unsigned* flags, unsigned tag) {
@@ -289,14 +392,52 @@ __device__ __forceinline__ unsigned long long opaque64(unsigned long long v) {
     return r;
 }
 
+// 2-D tiles (TILED kernels): CTA b = ti TJ + tj owns the TH x TW columns
+// (i0 + li, j0 + lj), i0 = ti TH, j0 = tj TW (exact tiling: n1 = TI TH,
+// n2 = TJ TW), numbered cl = li TW + lj in shared memory.  Against 1-D strips
+// of consecutive columns (whose i-neighbours all live in the neighbouring
+// CTAs), only the tile's perimeter talks to other CTAs: at the HCP 3T shape
+// (tiles 42 x 3, 4 x 37 = 148) the L2 halo loads drop to 90 of 254 columns
+// per CTA and the global copy of p is stored only for the 86 perimeter
+// columns (tools/res_trace.cu ablations: halo loads cost 2.6 us and the copy
+// stores 2.8 us of a 14.6 us iteration).  The global copy is kept per CTA in
+// the CTA's own slot order (KNT node pairs per CTA), so a neighbour tile's
+// value sits at a per-CTA constant offset from the reader's own slot:
+//   j - 1 (lj = 0)      -> CTA b - 1,  slot q + (TW - 1) GPC
+//   j + 1 (lj = TW - 1) -> CTA b + 1,  slot q - (TW - 1) GPC
+//   i - 1 (li = 0)      -> CTA b - TJ, slot q + (TH - 1) TW GPC
+//   i + 1 (li = TH - 1) -> CTA b + TJ, slot q - (TH - 1) TW GPC
+// In-tile neighbours are shared-memory reads at q -+ GPC (j) and q -+ TW GPC
+// (i).  The host picks tiles with TW GPC <= NT and (TH - 1) TW GPC >=
+// (K - 1) NT, so only slot 0 holds first-row and only slot K - 1 last-row
+// pairs: the i-direction needs no mask bits.
+struct ResTile {
+    int TI, TJ, TH, TW;
+};
+__host__ __device__ inline size_t res_tiled_ghost_floats(int G, int K) { return (size_t)G * 2 * K * RES_THREADS; }
+
+// Before reading neighbours' p: acquire the flags of the (up to 4) listed CTAs.
+__device__ __forceinline__ void halo_acquire_list(const unsigned* flags, const int (&nb)[4], unsigned tag) {
+    if (threadIdx.x < 4) {
+        const int b = nb[threadIdx.x];
+        if (b >= 0) {
+            unsigned spins = 0;
+            while (ld_acquire_u32(flags + (size_t)b * RES_FLAG_STRIDE) != tag)
+                if (++spins > RES_SPIN_LIMIT) __trap();
+        }
+    }
+    __syncthreads();
+}
+
 // TRACE: phase stamps for tools/res_trace.cu (compiled out of the library's kernel).
-template <int K, bool FIXED, bool TRACE = false>
+template <int K, bool FIXED, bool TRACE = false, bool TILED = false>
 __global__ void __launch_bounds__(RES_THREADS, 1)
     pcg_resident_kernel(Geom g, Ctl c, SolveParams sp, int pair, const float* __restrict__ grad,
                         const float* __restrict__ dt, const float* __restrict__ et, float* __restrict__ x,
                         float* __restrict__ xpad, float* __restrict__ pgh, double* __restrict__ gpart,
                         unsigned* __restrict__ flags, float wi, float wj, float* __restrict__ bcur,
-                        float* __restrict__ bold, int batch, unsigned long long* trace = nullptr) {
+                        float* __restrict__ bold, int batch, unsigned long long* trace = nullptr,
+                        ResTile tl = ResTile{0, 0, 0, 0}) {
     constexpr int NT = RES_THREADS;
     static_assert(K <= RES_KMAX, "slot masks hold RES_KMAX slots per field");
     count_launch(c);
@@ -312,9 +453,13 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
     if constexpr (TRACE) res_stamp(trk);
     extern __shared__ __align__(16) float smem_f[];
     const int P = g.P, Pp = res_pad(P), GPC = Pp >> 1, n2 = g.n2;
-    const long long c0 = (long long)blockIdx.x * g.ncol / gridDim.x;
-    const long long c1 = (long long)(blockIdx.x + 1) * g.ncol / gridDim.x;
-    const int ncl = (int)(c1 - c0);
+    // strips: columns [c0, c1); tiles: (ti, tj), TWG = pairs per tile row, RL = first last-row pair
+    const int b = blockIdx.x;
+    const int ti = TILED ? b / tl.TJ : 0, tj = TILED ? b - ti * tl.TJ : 0;
+    const int TWG = TILED ? tl.TW * GPC : 0, RL = TILED ? (tl.TH - 1) * TWG : 0;
+    const long long c0 = TILED ? 0 : (long long)b * g.ncol / gridDim.x;
+    const long long c1 = TILED ? 0 : (long long)(b + 1) * g.ncol / gridDim.x;
+    const int ncl = TILED ? tl.TH * tl.TW : (int)(c1 - c0);
     const int nq = ncl * GPC;                // node pairs owned by this CTA
     // shared layout (floats): [guard 2][p: KNT pairs][guard 2][M: KNT pairs][guard 2][et: KNT pairs]
     // Padding nodes (l >= P, and slots past the CTA's columns) have M = 1,
@@ -329,21 +474,34 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
     float2* se2 = reinterpret_cast<float2*>(se);
     const size_t n0 = (size_t)pair * g.ps + (size_t)c0 * P;
     // this CTA's first node in the ghost-padded global copy of p, and in xpad
+    // (tiles: its own KNT-pair regions of both)
     float2* __restrict__ pgc2 =
-        reinterpret_cast<float2*>(pgh + (size_t)pair * res_ghost_pair_floats(g) + (size_t)(c0 + n2) * Pp);
-    float2* __restrict__ xp2 = reinterpret_cast<float2*>(xpad + (size_t)c0 * Pp);
-    const int sI2 = n2 * GPC;                // i-neighbour distance in node pairs
+        TILED ? reinterpret_cast<float2*>(pgh + (size_t)pair * res_tiled_ghost_floats(gridDim.x, K) +
+                                          (size_t)b * KNT2)
+              : reinterpret_cast<float2*>(pgh + (size_t)pair * res_ghost_pair_floats(g) + (size_t)(c0 + n2) * Pp);
+    float2* __restrict__ xp2 = reinterpret_cast<float2*>(xpad + (TILED ? (size_t)b * KNT2 : (size_t)c0 * Pp));
+    const int sI2 = n2 * GPC;                // i-neighbour distance in node pairs (strips)
+    // tiles: offsets (in pairs) of the neighbour tiles' copies, relative to this CTA's
+    const long long oJM = -(long long)KNT2 / 2 + (long long)(tl.TW - 1) * GPC;
+    const long long oJP = (long long)KNT2 / 2 - (long long)(tl.TW - 1) * GPC;
+    const long long oIM = -(long long)tl.TJ * (KNT2 / 2) + RL;
+    const long long oIP = (long long)tl.TJ * (KNT2 / 2) - RL;
+    const bool hasIM = TILED && ti > 0, hasIP = TILED && ti < tl.TI - 1;
     double* part0 = gpart;                          // [repl][G][2] r0.z0, r0.r0 (and the Armijo start)
-    double* part1 = gpart + RES_PART_DOUBLES;       // [repl][G][1] p.Hp
-    double* part2 = gpart + 2 * RES_PART_DOUBLES;   // [repl][G][2] r.z, r.r
+    // limb words: set 0 p.Hp, set 1 (r0.z0, r0.r0) and (r.z, r.r) -- exact integer all-reduces
+    unsigned long long* lw = reinterpret_cast<unsigned long long*>(gpart + 3 * RES_PART_DOUBLES);
+    __shared__ unsigned long long s_prev[2 * RES_LIMB_W];
     const int tid = threadIdx.x;
     // flags[b * RES_FLAG_STRIDE]: p-halo flag of CTA b; flags[G * RES_FLAG_STRIDE]: launch counter
     const unsigned launch = *reinterpret_cast<volatile unsigned*>(flags + (size_t)gridDim.x * RES_FLAG_STRIDE);
     // CTAs owning this CTA's i-neighbour (+-n2) and j-neighbour (+-1) columns
-    const int blo = res_owner(c0 - n2 > 0 ? c0 - n2 : 0, g.ncol, gridDim.x);
-    const int bhi = res_owner(c1 - 1 + n2 < g.ncol ? c1 - 1 + n2 : g.ncol - 1, g.ncol, gridDim.x);
+    const int blo = TILED ? 0 : res_owner(c0 - n2 > 0 ? c0 - n2 : 0, g.ncol, gridDim.x);
+    const int bhi = TILED ? 0 : res_owner(c1 - 1 + n2 < g.ncol ? c1 - 1 + n2 : g.ncol - 1, g.ncol, gridDim.x);
+    const int nbl[4] = {TILED && tj > 0 ? b - 1 : -1, TILED && tj < tl.TJ - 1 ? b + 1 : -1, hasIM ? b - tl.TJ : -1,
+                        hasIP ? b + tl.TJ : -1};
 
     if (tid < 6) smem_f[tid < 2 ? tid : tid < 4 ? 2 + KNT2 + (tid - 2) : 4 + 2 * KNT2 + (tid - 4)] = 0.f;
+    limb_init(lw, s_prev);                   // before the start publish (halo_release's barrier)
     SlotMask msk{0ull, 0ull};
     float2 r[K], hv[K];
     float frz = 0.f, frr = 0.f;
@@ -358,10 +516,19 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
             if (q < nq) {
                 const int cl = fdG.div(q);
                 const int l0 = 2 * (q - cl * GPC);
-                const long long col = c0 + cl;
-                const int i = fdN2.div((int)col), j = (int)col - i * n2;
+                int i, j, lj = 0;
+                if constexpr (TILED) {
+                    const int li = cl / tl.TW;
+                    lj = cl - li * tl.TW;
+                    i = ti * tl.TH + li;
+                    j = tj * tl.TW + lj;
+                } else {
+                    const long long col = c0 + cl;
+                    i = fdN2.div((int)col);
+                    j = (int)col - i * n2;
+                }
                 const float dl = (float)(g.ahd * diag_lxy(g, i, j));
-                const size_t o = n0 + (size_t)cl * P + l0;
+                const size_t o = TILED ? (size_t)pair * g.ps + ((size_t)i * n2 + j) * P + l0 : n0 + (size_t)cl * P + l0;
                 Mv.x = dt[o] + dl;
                 ev.x = et[o];
                 rv.x = -grad[o];
@@ -371,8 +538,13 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
                     rv.y = -grad[o + 1];
                 }
                 mset(msk, RM_VAL + k);
-                if (j > 0) mset(msk, (cl > 0 ? RM_JML : RM_JMR) + k);
-                if (j < n2 - 1) mset(msk, (cl < ncl - 1 ? RM_JPL : RM_JPR) + k);
+                if constexpr (TILED) {               // j-neighbours: in the tile, or the next tile's
+                    if (j > 0) mset(msk, (lj > 0 ? RM_JML : RM_JMR) + k);
+                    if (j < n2 - 1) mset(msk, (lj < tl.TW - 1 ? RM_JPL : RM_JPR) + k);
+                } else {
+                    if (j > 0) mset(msk, (cl > 0 ? RM_JML : RM_JMR) + k);
+                    if (j < n2 - 1) mset(msk, (cl < ncl - 1 ? RM_JPL : RM_JPR) + k);
+                }
                 const float2 z = make_float2(precond(rv.x, Mv.x), precond(rv.y, Mv.y));
                 frz = fmaf(rv.x, z.x, frz);
                 frz = fmaf(rv.y, z.y, frz);
@@ -392,8 +564,12 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
     double v2[2] = {(double)frz, (double)frr}, t2[2];
     if constexpr (TRACE) res_stamp(trk + 1);
     halo_release(flags, res_tag(launch, 0));  // p0 published
-    reduce_publish<2>(v2, part0, res_tag(launch, 0));
-    reduce_collect<2>(part0, res_tag(launch, 0), t2);
+    {   // r0.z0, r0.r0 on limbs, scaled by ||grad||^2 (= r0.r0) of the evaluation
+        const int e0 = limb_exp(c.st[pair].gnorm2);
+        const int ex0[2] = {e0, e0};
+        limb_publish<2>(v2, ex0, lw, 1);
+        limb_collect<2>(lw, 1, ex0, s_prev, t2);
+    }
     if constexpr (TRACE) res_stamp(trk + 2);
     // Loop state kept out of registers (the r / Hp slots need 48 of the 80):
     // rr0 and the last r.r live in shared memory; the H-evaluation count, "x
@@ -433,10 +609,20 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
                     const float2 b = mbit(m, RM_JPL + k) ? s2[o + GPC] : make_float2(0.f, 0.f);
                     h.x = fmaf(-wj, a.x + b.x, h.x);
                     h.y = fmaf(-wj, a.y + b.y, h.y);
+                    if constexpr (TILED) {           // in-tile i-neighbours (first / last row: remote)
+                        float2 ia, ib;
+                        if (k == 0) ia = t0 >= TWG ? s2[o - TWG] : make_float2(0.f, 0.f);
+                        else ia = s2[o - TWG];
+                        if (k == K - 1) ib = t0 + o < RL ? s2[o + TWG] : make_float2(0.f, 0.f);
+                        else ib = s2[o + TWG];
+                        h.x = fmaf(-wi, ia.x + ib.x, h.x);
+                        h.y = fmaf(-wi, ia.y + ib.y, h.y);
+                    }
                     hv[k] = h;
                 }
             }
-            halo_acquire(flags, blo, bhi, res_tag(launch, k_it));   // neighbours' p_k
+            if constexpr (TILED) halo_acquire_list(flags, nbl, res_tag(launch, k_it));
+            else halo_acquire(flags, blo, bhi, res_tag(launch, k_it));   // neighbours' p_k
             if constexpr (TRACE) res_stamp(tr ? tr + 1 : nullptr);
             // ---- remote part: i-neighbours (and j-neighbours across the CTA
             // boundary) from the global copy; p.Hp
@@ -449,14 +635,20 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
 #pragma unroll
                 for (int k = 0; k < K; k++) {
                     const int o = k * NT;
-#ifdef RES_ABLATE_REMOTE   // diagnostic builds only (tools/res_trace.cu): timing without the i-halo loads
-                    const float2 a = make_float2(0.f, 0.f), b = a;
-#else
-                    const float2 a = __ldcg(gc + o - sI2);
-                    const float2 b = __ldcg(gc + o + sI2);
+                    float2 a = make_float2(0.f, 0.f), b = a, c = a, d = a;
+                    if constexpr (TILED) {           // perimeter only: the neighbour tiles' copies
+                        if (k == 0 && hasIM && t0 < TWG) a = __ldcg(gc + oIM);
+                        if (k == K - 1 && hasIP && t0 + o >= RL && t0 + o < nq) b = __ldcg(gc + o + oIP);
+                        if (mbit(m, RM_JMR + k)) c = __ldcg(gc + o + oJM);
+                        if (mbit(m, RM_JPR + k)) d = __ldcg(gc + o + oJP);
+                    } else {
+#ifndef RES_ABLATE_REMOTE   // diagnostic builds only (tools/res_trace.cu): timing without the i-halo loads
+                        a = __ldcg(gc + o - sI2);
+                        b = __ldcg(gc + o + sI2);
 #endif
-                    const float2 c = mbit(m, RM_JMR + k) ? __ldcg(gc + o - GPC) : make_float2(0.f, 0.f);
-                    const float2 d = mbit(m, RM_JPR + k) ? __ldcg(gc + o + GPC) : make_float2(0.f, 0.f);
+                        if (mbit(m, RM_JMR + k)) c = __ldcg(gc + o - GPC);
+                        if (mbit(m, RM_JPR + k)) d = __ldcg(gc + o + GPC);
+                    }
                     float2 h = hv[k];
                     h.x = fmaf(-wi, a.x + b.x, fmaf(-wj, c.x + d.x, h.x));
                     h.y = fmaf(-wi, a.y + b.y, fmaf(-wj, c.y + d.y, h.y));
@@ -471,10 +663,10 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
             }
             if constexpr (TRACE) res_stamp(tr ? tr + 2 : nullptr);
             double v1[1] = {(double)fpq}, t1[1];
-            reduce_publish<1>(v1, part1, res_tag(launch, k_it));
+            const int ex1[1] = {limb_exp(rz)};        // p.Hp = rz / alpha
+            limb_publish<1>(v1, ex1, lw, 0);
             if constexpr (TRACE) res_stamp(tr ? tr + 7 : nullptr);
-            reduce_collect<1>(part1, res_tag(launch, k_it), t1,
-                              (TRACE && k_it < 8) ? trace + ((size_t)blockIdx.x * 16 + 12) * 8 + k_it : nullptr);
+            limb_collect<1>(lw, 0, ex1, s_prev, t1);
             if constexpr (TRACE) res_stamp(tr ? tr + 3 : nullptr);
             if (t1[0] <= 0.0) break;                  // breakdown (oracle pcg(): keep x)
             const float a = (float)(rz / t1[0]);
@@ -499,7 +691,8 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
                 }
             }
             double v3[2] = {(double)frz2, (double)frr2}, t3[2];
-            reduce_publish<2>(v3, part2, res_tag(launch, k_it));
+            const int ex3[2] = {limb_exp(rz), limb_exp(s_rr)};
+            limb_publish<2>(v3, ex3, lw, 1);
             if constexpr (TRACE) res_stamp(tr ? tr + 4 : nullptr);
             // ---- x += a p while the r.z / r.r partials gather (fire-and-forget
             // L2 adds; x feeds no reduction)
@@ -522,10 +715,10 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
                     }
                 }
             }
-            reduce_collect<2>(part2, res_tag(launch, k_it), t3);
+            limb_collect<2>(lw, 1, ex3, s_prev, t3);
             if constexpr (TRACE) res_stamp(tr ? tr + 5 : nullptr);
             k_it += 1;
-            if (tid == 0) s_rr = t3[1];
+            if (tid == 0) s_rr = t3[1];              // (ex3 read it before limb_publish's barrier)
             const double beta = t3[0] / rz;
             rz = t3[0];
             if (k_it >= sp.max_pcg || (!FIXED && sqrt(t3[1] / s_rr0) < sp.pcg_rtol)) break;
@@ -543,7 +736,14 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
                     const float2 pn = make_float2(fmaf(be, p.x, z.x), fmaf(be, p.y, z.y));
                     s2[o] = pn;
 #ifndef RES_ABLATE_GHOST
-                    if (mbit(m, RM_VAL + k)) gt[o] = pn;
+                    if constexpr (TILED) {           // only the perimeter is read by other CTAs
+                        const bool bnd = mbit(m, RM_JMR + k) || mbit(m, RM_JPR + k) ||
+                                         (k == 0 && hasIM && t0 < TWG) ||
+                                         (k == K - 1 && hasIP && t0 + o >= RL && t0 + o < nq);
+                        if (bnd) gt[o] = pn;
+                    } else {
+                        if (mbit(m, RM_VAL + k)) gt[o] = pn;
+                    }
 #endif
                 }
             }
@@ -559,7 +759,41 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
     double agq = 0.0, aqm = 0.0;
     __threadfence();
     __syncthreads();
-    {
+    if constexpr (TILED) {
+        // tiles: TH runs of TW P contiguous nodes; flattened over the CTA so
+        // every warp access is 32 consecutive nodes of one run (coalesced)
+        const int RW = tl.TW * P, Nb = tl.TH * RW;
+        FastDiv fdR, fdP;
+        fdR.init((unsigned)RW);
+        fdP.init((unsigned)P);
+        const size_t base = (size_t)pair * g.ps + ((size_t)ti * tl.TH * n2 + (size_t)tj * tl.TW) * P;
+        const float* xq = xpad + (size_t)b * KNT2;
+        constexpr int U = 4;
+        for (int e0 = tid; e0 < Nb; e0 += U * NT) {
+            float qv[U], gv[U], bv[U];
+            size_t o[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int e = min(e0 + u * NT, Nb - 1);
+                const int row = fdR.div(e), t = e - row * RW;
+                const int cj = fdP.div(t), l = t - cj * P;
+                o[u] = base + (size_t)row * n2 * P + t;
+                qv[u] = k_it == 0 ? 0.f : __ldcg(xq + (size_t)(row * tl.TW + cj) * Pp + l);
+                gv[u] = grad[o[u]];
+                bv[u] = bcur[o[u]];
+            }
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                if (e0 + u * NT < Nb) {
+                    agq += (double)gv[u] * (double)qv[u];
+                    aqm = fmax(aqm, (double)fabsf(qv[u]));
+                    x[o[u]] = qv[u];
+                    bold[o[u]] = bv[u];
+                    bcur[o[u]] = bv[u] + qv[u];
+                }
+            }
+        }
+    } else {
         const int Nb = ncl * P;              // this CTA's nodes, from n0
         FastDiv fdP;
         fdP.init((unsigned)P);
@@ -636,30 +870,41 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
 // of (r.z, r.r), p-halo release -- with every slot loop (the arithmetic and
 // the shared / L2 data movement) removed.  Its time per iteration is the
 // latency floor a PCG iteration on this chip layout cannot go below.
-template <int K>
+template <int K, bool TILED = false>
 __global__ void __launch_bounds__(RES_THREADS, 1)
-    pcg_sync_floor_kernel(Geom g, int iters, double* __restrict__ gpart, unsigned* __restrict__ flags) {
+    pcg_sync_floor_kernel(Geom g, int iters, double* __restrict__ gpart, unsigned* __restrict__ flags,
+                          ResTile tl = ResTile{0, 0, 0, 0}) {
     const long long c0 = (long long)blockIdx.x * g.ncol / gridDim.x;
     const long long c1 = (long long)(blockIdx.x + 1) * g.ncol / gridDim.x;
-    const int n2 = g.n2;
+    const int n2 = g.n2, b = blockIdx.x;
+    const int ti = TILED ? b / tl.TJ : 0, tj = TILED ? b - ti * tl.TJ : 0;
     const unsigned launch = *reinterpret_cast<volatile unsigned*>(flags + (size_t)gridDim.x * RES_FLAG_STRIDE);
-    const int blo = res_owner(c0 - n2 > 0 ? c0 - n2 : 0, g.ncol, gridDim.x);
-    const int bhi = res_owner(c1 - 1 + n2 < g.ncol ? c1 - 1 + n2 : g.ncol - 1, g.ncol, gridDim.x);
+    const int blo = TILED ? 0 : res_owner(c0 - n2 > 0 ? c0 - n2 : 0, g.ncol, gridDim.x);
+    const int bhi = TILED ? 0 : res_owner(c1 - 1 + n2 < g.ncol ? c1 - 1 + n2 : g.ncol - 1, g.ncol, gridDim.x);
+    const int nbl[4] = {TILED && tj > 0 ? b - 1 : -1, TILED && tj < tl.TJ - 1 ? b + 1 : -1,
+                        TILED && ti > 0 ? b - tl.TJ : -1, TILED && ti < tl.TI - 1 ? b + tl.TJ : -1};
     double* part0 = gpart;
-    double* part1 = gpart + RES_PART_DOUBLES;
-    double* part2 = gpart + 2 * RES_PART_DOUBLES;
+    unsigned long long* lw = reinterpret_cast<unsigned long long*>(gpart + 3 * RES_PART_DOUBLES);
+    __shared__ unsigned long long s_prev[2 * RES_LIMB_W];
+    limb_init(lw, s_prev);
     double v2[2] = {1.0, 1.0}, t2[2];
     halo_release(flags, res_tag(launch, 0));
-    reduce_publish<2>(v2, part0, res_tag(launch, 0));
-    reduce_collect<2>(part0, res_tag(launch, 0), t2);
+    {
+        const int ex0[2] = {0, 0};
+        limb_publish<2>(v2, ex0, lw, 1);
+        limb_collect<2>(lw, 1, ex0, s_prev, t2);
+    }
     for (int k = 0; k < iters; k++) {
-        halo_acquire(flags, blo, bhi, res_tag(launch, k));
+        if constexpr (TILED) halo_acquire_list(flags, nbl, res_tag(launch, k));
+        else halo_acquire(flags, blo, bhi, res_tag(launch, k));
         double v1[1] = {t2[0]}, t1[1];
-        reduce_publish<1>(v1, part1, res_tag(launch, k));
-        reduce_collect<1>(part1, res_tag(launch, k), t1);
+        const int ex1[1] = {limb_exp(t2[0])};
+        limb_publish<1>(v1, ex1, lw, 0);
+        limb_collect<1>(lw, 0, ex1, s_prev, t1);
         double v3[2] = {t1[0], t2[1]};
-        reduce_publish<2>(v3, part2, res_tag(launch, k));
-        reduce_collect<2>(part2, res_tag(launch, k), t2);
+        const int ex3[2] = {limb_exp(t1[0]), limb_exp(t2[1])};
+        limb_publish<2>(v3, ex3, lw, 1);
+        limb_collect<2>(lw, 1, ex3, s_prev, t2);
         if (k + 1 < iters) halo_release(flags, res_tag(launch, k + 1));
     }
     double v4[2] = {t2[0], t2[1]}, t4[2];

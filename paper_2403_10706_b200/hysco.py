@@ -25,7 +25,7 @@ EXPORTED = ["hysco_default_solve_opts", "hysco_default_ot_opts", "hysco_default_
             "hysco_ot_init", "hysco_objective_grad", "hysco_hessvec", "hysco_hess_diag", "hysco_precond_solve",
             "hysco_solve",
             "hysco_apply", "hysco_correct", "hysco_correct_host", "hysco_correct_host_stream",
-            "hysco_last_launch_count", "hysco_history",
+            "hysco_last_launch_count", "hysco_pcg_path", "hysco_history",
             "hysco_last_error", "hysco_destroy", "hysco_version", "hysco_profile_kernels",
             "hysco_nccl_unique_id", "hysco_create_slab", "hysco_create_loopback", "hysco_group_correct",
             "hysco_group_solve", "hysco_group_admm", "hysco_push_forward", "hysco_default_lsq_opts", "hysco_lsq_correct",
@@ -174,6 +174,8 @@ def lib():
     L.hysco_destroy.argtypes = [vp]
     L.hysco_last_launch_count.argtypes = [vp]
     L.hysco_last_launch_count.restype = ctypes.c_int64
+    L.hysco_pcg_path.argtypes = [vp, ctypes.POINTER(ctypes.c_int32)]
+    L.hysco_pcg_path.restype = ctypes.c_int32
     L.hysco_history.argtypes = [vp, ctypes.c_int32, ctypes.POINTER(hysco_iter_record), ctypes.c_int32,
                                 ctypes.POINTER(ctypes.c_int32)]
     L.hysco_history.restype = st
@@ -384,6 +386,16 @@ def hysco_correct_host(ctx, Ip, Im, b_out=None, Ip_corr=None, Im_corr=None, ot_o
 
 def hysco_last_launch_count(ctx):
     return int(lib().hysco_last_launch_count(ctx))
+
+
+PCG_PATHS = {0: "streaming", 1: "resident-strips", 2: "resident-tiles", 3: "l2-resident"}
+
+
+def hysco_pcg_path(ctx):
+    """(path name, (TI, TJ, TH, TW)) of the context's PCG (include/hysco.h)."""
+    t = (ctypes.c_int32 * 4)()
+    k = int(lib().hysco_pcg_path(ctx, t))
+    return PCG_PATHS.get(k, "none"), tuple(int(v) for v in t)
 
 
 def hysco_history(ctx, pair=0):

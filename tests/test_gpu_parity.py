@@ -449,6 +449,41 @@ def test_resident_pcg_matches_streaming(monkeypatch, cfg, armijo):
     assert n_str - n_res == 10 * (pcg_launches(p.Ip.shape, H.HYSCO_F32) - 1) and r_res["f_evals"] == r_str["f_evals"]
 
 
+# shapes with an exact 2-D tiling of the columns over ~148 CTAs (hysco_resident.cuh
+# ResTile): the HCP 3T shape (4 x 37 tiles of 42 x 3 columns, odd P = 145) and a
+# short-column shape (37 x 4 tiles of 16 x 30 columns, P = 11, K = 6 slots)
+TILED_CASES = [("C2_hcp3t", (4, 37, 42, 3)), ((592, 120, 10), (37, 4, 16, 30))]
+
+
+@pytest.mark.parametrize("cfg,tile", TILED_CASES, ids=[str(c[0]) for c in TILED_CASES])
+@pytest.mark.parametrize("max_gn", [1, 3])
+def test_tiled_resident_matches_strips(monkeypatch, cfg, tile, max_gn):
+    """The resident PCG over 2-D column tiles (perimeter-only halo through L2,
+    in-tile i- and j-neighbours from shared memory) computes the same
+    iteration as over 1-D strips of consecutive columns: same decisions and
+    counters, b within the kernel tolerance after 1 and 3 GN steps (Armijo on)."""
+    if torch.cuda.get_device_properties(0).multi_processor_count != 148:
+        pytest.skip("the tilings are chosen for 148 SMs")
+    p = phantom.make_config(cfg) if isinstance(cfg, str) else phantom.make_pair(cfg, (1.25, 1.25, 1.25), 11)
+    so = H.default_solve_opts(max_gn=max_gn)
+    out = []
+    for tiled in ("1", "0"):
+        monkeypatch.setenv("HYSCO_RES_TILED", tiled)
+        c = Ctx([p.Ip], [p.Im], p.h)
+        path, t = H.hysco_pcg_path(c.ctx)
+        assert (path, t) == (("resident-tiles", tile) if tiled == "1" else ("resident-strips", (0, 0, 0, 0)))
+        b, Tp, Tm = c.nodes(), c.cells(), c.cells()
+        reps, inf = H.hysco_correct(c.ctx, b, Tp, Tm, solve_opts=so)
+        assert not inf
+        out.append((c.np(b)[0], c.np(Tp)[0], reps[0]))
+        c.close()
+    (bt, Tt, rt), (bs, Ts, rs) = out
+    keys = ("pcg_iters", "h_evals", "gn_iters", "f_evals", "ls_halvings", "stop_reason")
+    assert tuple(rt[k] for k in keys) == tuple(rs[k] for k in keys)
+    assert rel(bt, bs) <= 1e-5 and rel(Tt, Ts) <= 1e-5
+    assert relS(rt["J"], rs["J"]) <= 1e-6
+
+
 FLAT_CASES = [((5, 7, 37), 2), ((6, 5, 24), 3), ((4, 3, 42), 2), ((3, 4, 15), 3), ((1, 3, 70), 1), ((7, 6, 3), 2)]
 
 
