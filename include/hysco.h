@@ -274,8 +274,13 @@ HYSCO_API hysco_status hysco_correct_host(hysco_ctx ctx, const void* h_Iplus, co
  * h_Iminus[k] ([batch][n1][n2][n3]) and writes h_b_out[k], h_Iplus_corr[k],
  * h_Iminus_corr[k] (each array of pointers may be NULL, or hold NULL
  * entries, to skip that output).  reports: [n_items][batch] or NULL.
- * Returns when every copy has completed; the first failing item's status.
- * Not on slab contexts. */
+ * Each item's correction reads its pair in place from its input staging
+ * slot and writes its results in place to its output slot (the two slots'
+ * graphs stay cached), and the host does not synchronise between items: the
+ * per-item reports are gathered once at the end.  The context is left bound
+ * to the last item's input slot.
+ * Returns when every copy has completed; the first failing item's status
+ * (errors before HYSCO_INFEASIBLE).  Not on slab contexts. */
 HYSCO_API hysco_status hysco_correct_host_stream(hysco_ctx ctx, int32_t n_items, const void* const* h_Iplus,
                                                  const void* const* h_Iminus, const hysco_ot_opts* ot,
                                                  const hysco_solve_opts* so, void* const* h_b_out,

@@ -89,6 +89,16 @@ struct hysco_ctx_s {
     unsigned* gctr = nullptr;
     unsigned long long* launches = nullptr;
     unsigned long long* h_launches = nullptr;
+    // hysco_correct_host_stream: per-item pinned readback slots; while set,
+    // run_path copies the final PairState / launch count there asynchronously
+    // and returns without synchronising (the items then run back to back)
+    PairState* defer_st = nullptr;
+    unsigned long long* defer_launch = nullptr;
+    PairState* h_items = nullptr;
+    unsigned long long* h_items_l = nullptr;
+    PairState* d_items = nullptr;              // device snapshots (one kernel per item, read once at the end)
+    unsigned long long* d_items_l = nullptr;
+    long long h_items_cap = 0;
     unsigned* dcond = nullptr;
     unsigned* h_cond = nullptr;
     Ctl ctl{};
@@ -118,6 +128,12 @@ struct hysco_ctx_s {
     cudaGraphExec_t exec = nullptr;
     GraphKey key{};
     bool have_key = false;
+    // a second cached graph (hysco_correct_host_stream alternates two staging
+    // slots, i.e. two pointer sets): swapped with the current one on a hit
+    cudaGraph_t graph2 = nullptr;
+    cudaGraphExec_t exec2 = nullptr;
+    GraphKey key2{};
+    bool have_key2 = false;
     long long last_launches = 0;
     void* flush = nullptr;    // profiling-only L2 flush scratch
     // on-chip-resident PCG (hysco_resident.cuh): fp32, one CTA per SM
@@ -1278,6 +1294,22 @@ struct PairView {
 // runs pair by pair (the whole path of pair 0, then pair 1, ...): one pair's
 // node arrays (~130 MB at 3T) then stay L2-resident between its kernels, so
 // a pair costs the same in a batch as alone.
+// hysco_correct_host_stream: copy the final per-pair states and the launch
+// count of one item into its snapshot slot and reset the count for the next
+// item -- one tiny kernel instead of a host synchronisation per item.
+__global__ void state_snapshot_kernel(const PairState* __restrict__ st, int B, unsigned long long* launches,
+                                      PairState* __restrict__ dst, unsigned long long* __restrict__ dl) {
+    const int n = (int)(B * sizeof(PairState) / sizeof(int));
+    const int* a = reinterpret_cast<const int*>(st);
+    int* d = reinterpret_cast<int*>(dst);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) d[i] = a[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        *dl = *launches;
+        *launches = 0;
+    }
+}
+
 template <typename T>
 static hysco_status run_path(hysco_ctx ctx, const GraphKey& key, void* b_io, void* b_out, void* Tp, void* Tm) {
     const bool per_pair = (ctx->resident || ctx->l2pcg) && ctx->cfg.batch > 1 && key.sp.precond != HYSCO_PRECOND_PE_BLOCK &&
@@ -1315,13 +1347,30 @@ static hysco_status run_path(hysco_ctx ctx, const GraphKey& key, void* b_io, voi
             body1(r);
         }
     };
-    CK(cudaMemsetAsync(ctx->launches, 0, sizeof(unsigned long long), ctx->stream));
+    // (deferred readback: the previous item's snapshot kernel reset the count)
+    if (!ctx->defer_st) CK(cudaMemsetAsync(ctx->launches, 0, sizeof(unsigned long long), ctx->stream));
     bool use_graph = !ctx->no_graph && !ctx->graph_broken;
     if (use_graph) {
         bool hit = ctx->have_key && memcmp(&ctx->key, &key, sizeof key) == 0 && ctx->exec;
+        if (!hit && ctx->have_key2 && memcmp(&ctx->key2, &key, sizeof key) == 0 && ctx->exec2) {
+            std::swap(ctx->graph, ctx->graph2);
+            std::swap(ctx->exec, ctx->exec2);
+            std::swap(ctx->key, ctx->key2);
+            std::swap(ctx->have_key, ctx->have_key2);
+            hit = true;
+        }
         if (!hit) {
-            if (ctx->exec) cudaGraphExecDestroy(ctx->exec);
-            if (ctx->graph) cudaGraphDestroy(ctx->graph);
+            // the current graph becomes the spare; the old spare goes
+            if (ctx->exec2) cudaGraphExecDestroy(ctx->exec2);
+            if (ctx->graph2) cudaGraphDestroy(ctx->graph2);
+            ctx->exec2 = ctx->have_key ? ctx->exec : nullptr;
+            ctx->graph2 = ctx->have_key ? ctx->graph : nullptr;
+            ctx->key2 = ctx->key;
+            ctx->have_key2 = ctx->have_key && ctx->exec2;
+            if (!ctx->have_key) {
+                if (ctx->exec) cudaGraphExecDestroy(ctx->exec);
+                if (ctx->graph) cudaGraphDestroy(ctx->graph);
+            }
             ctx->exec = nullptr;
             ctx->graph = nullptr;
             ctx->have_key = false;
@@ -1362,6 +1411,12 @@ static hysco_status run_path(hysco_ctx ctx, const GraphKey& key, void* b_io, voi
         ctx->ctl.use_graph = 0;
         body(r);
         if (r.err != cudaSuccess) return cuda_fail(ctx, r.err, "host-loop solve", __LINE__);
+    }
+    if (ctx->defer_st) {   // the caller reads all items' snapshots after one synchronisation
+        state_snapshot_kernel<<<1, 128, 0, ctx->stream>>>(ctx->st, ctx->cfg.batch, ctx->launches, ctx->defer_st,
+                                                          ctx->defer_launch);
+        CK(cudaGetLastError());
+        return HYSCO_OK;
     }
     CK(cudaMemcpyAsync(ctx->h_st, ctx->st, sizeof(PairState) * ctx->cfg.batch, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaMemcpyAsync(ctx->h_launches, ctx->launches, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
@@ -1442,8 +1497,9 @@ static hysco_status setup_typed(hysco_ctx ctx) {
     ctx->flat = g.P >= FlatVec<T>::V && !getenv_is1("HYSCO_NO_FLAT");
     {   // plane-march F1 (pcg_march_kernel): tiles of <= 16 columns, 5 bulk-copy stages in
         // <= 220 KB of shared memory (one CTA per SM), plane chunks for one wave of CTAs
-        const size_t cap = 220 * 1024;
+        const size_t cap = 220 * 1024 / MARCH_CPS;
         int wmax = std::min(g.n2, 16);
+        const int mslots = ctx->nsm * MARCH_CPS;   // co-resident march CTAs
         auto fits = [&](int w) {
             return march_ms<T>(w, g.P, MARCH_THREADS) > 0 && march_smem_bytes<T>(march_plan<T>(w, g.P, 5)) <= cap;
         };
@@ -1457,10 +1513,10 @@ static hysco_status setup_typed(hysco_ctx ctx) {
             // 7T keeps 14 x 10 = 140, narrower tiles measured slower)
             const int njb0 = (g.n2 + wmax - 1) / wmax;
             auto used = [&](int nj) {
-                return nj <= ctx->nsm ? nj * std::min(std::max(1, ctx->nsm / nj), g.n1) : ctx->nsm;
+                return nj <= mslots ? nj * std::min(std::max(1, mslots / nj), g.n1) : mslots;
             };
             int best = njb0, bestu = used(njb0);
-            if (10 * bestu < 9 * std::min(ctx->nsm, g.n1 * njb0))
+            if (10 * bestu < 9 * std::min(mslots, g.n1 * njb0))
                 for (int nj = njb0 + 1; nj <= std::min(2 * njb0, g.n2); nj++)
                     if (used(nj) > bestu) {
                         bestu = used(nj);
@@ -1482,7 +1538,7 @@ static hysco_status setup_typed(hysco_ctx ctx) {
             CK(attr(pcg_march_kernel<T, false, 8>));
             CK(attr(pcg_march_kernel<T, true, 12>));
             CK(attr(pcg_march_kernel<T, false, 12>));
-            long long ncb = ctx->mr_njb <= ctx->nsm ? std::max(1, ctx->nsm / ctx->mr_njb) : 1;
+            long long ncb = ctx->mr_njb <= mslots ? std::max(1, mslots / ctx->mr_njb) : 1;
             ncb = std::min<long long>(ncb, g.n1);
             ctx->mr_c = (int)((g.n1 + ncb - 1) / ncb);
             ncb = (g.n1 + ctx->mr_c - 1) / ctx->mr_c;
@@ -2284,7 +2340,7 @@ hysco_status hysco_bind_images(hysco_ctx ctx, const void* d_Iplus, const void* d
     CHECK_CTX();
     if (!d_Iplus || !d_Iminus || !aligned16(d_Iplus) || !aligned16(d_Iminus))
         return set_err(ctx, HYSCO_ERR_ARG, "image pointers must be non-NULL and 16-byte aligned");
-    if (d_Iplus != ctx->Ip || d_Iminus != ctx->Im) ctx->have_key = false;   // graphs bake pointers
+    // (graphs bake the image pointers; the cache key holds them)
     ctx->Ip = d_Iplus;
     ctx->Im = d_Iminus;
     ctx->state_valid = false;
@@ -2578,6 +2634,7 @@ static hysco_status solve_common(hysco_ctx ctx, int kind, const hysco_ot_opts* o
                                         : run_path<float>(ctx, key, b_io, b_out, Tp, Tm);
     }
     if (s != HYSCO_OK) return s;
+    if (ctx->defer_st) return HYSCO_OK;   // reports after the caller's synchronisation
     bool inf = false;
     fill_reports(ctx, reports, &inf);
     // a pair-by-pair batch solve shares the Hessian scratch between pairs:
@@ -2671,30 +2728,58 @@ hysco_status hysco_correct_host_stream(hysco_ctx ctx, int32_t n_items, const voi
         if (!e) e = cudaEventRecord(ctx->ev_h2d[sl], cs);
         return e;
     };
+    const int B = ctx->cfg.batch;
+    if ((long long)n_items * B > ctx->h_items_cap) {   // per-item readback slots (pinned, kept)
+        if (ctx->h_items) cudaFreeHost(ctx->h_items);
+        if (ctx->h_items_l) cudaFreeHost(ctx->h_items_l);
+        ctx->h_items = nullptr;
+        ctx->h_items_l = nullptr;
+        ctx->h_items_cap = 0;
+        const long long cap = std::max<long long>((long long)n_items * B, 8LL * B);
+        if (ctx->d_items) cudaFree(ctx->d_items);
+        if (ctx->d_items_l) cudaFree(ctx->d_items_l);
+        ctx->d_items = nullptr;
+        ctx->d_items_l = nullptr;
+        CK(cudaMallocHost((void**)&ctx->h_items, sizeof(PairState) * cap));
+        CK(cudaMallocHost((void**)&ctx->h_items_l, sizeof(unsigned long long) * cap));
+        CK(cudaMalloc((void**)&ctx->d_items, sizeof(PairState) * cap));
+        CK(cudaMalloc((void**)&ctx->d_items_l, sizeof(unsigned long long) * cap));
+        ctx->h_items_cap = cap;
+    }
+    CK(cudaMemsetAsync(ctx->launches, 0, sizeof(unsigned long long), ctx->stream));   // item 0's count
     if (n_items > 0) CK(h2d(0));
-    if (hysco_status s0 = hysco_bind_images(ctx, ctx->own_Ip, ctx->own_Im)) return s0;
     hysco_status first_err = HYSCO_OK;
+    std::vector<char> ran(n_items, 0);
+    struct DeferOff {   // the readback redirection ends with this call, however it returns
+        hysco_ctx c;
+        ~DeferOff() {
+            c->defer_st = nullptr;
+            c->defer_launch = nullptr;
+        }
+    } defer_off{ctx};
+    // Item k runs on staging slot sl = k % 2: its images are read in place from
+    // the input slot and its results written in place to the output slot (the
+    // two slots' pointer sets are the context's two cached graphs), so no
+    // device-to-device staging copies sit on the compute stream.
     for (int k = 0; k < n_items; k++) {
         const int sl = k & 1;
         if (k + 1 < n_items) CK(h2d(k + 1));     // next pair streams in during this correction
         CK(cudaStreamWaitEvent(ks, ctx->ev_h2d[sl], 0));
-        CK(cudaMemcpyAsync(ctx->own_Ip, ctx->st_in[sl][0], nc, cudaMemcpyDeviceToDevice, ks));
-        CK(cudaMemcpyAsync(ctx->own_Im, ctx->st_in[sl][1], nc, cudaMemcpyDeviceToDevice, ks));
-        CK(cudaEventRecord(ctx->ev_in_free[sl], ks));
+        CK(cudaStreamWaitEvent(ks, ctx->ev_out_free[sl], 0));   // item k - 2's results are out
+        if (hysco_status s0 = hysco_bind_images(ctx, ctx->st_in[sl][0], ctx->st_in[sl][1])) return s0;
         void *hb = out_ptr(h_b_out, k), *hp = out_ptr(h_Iplus_corr, k), *hm = out_ptr(h_Iminus_corr, k);
-        hysco_status s = solve_common(ctx, 2, ot, so, nullptr, nullptr, hp ? ctx->own_Tp : nullptr,
-                                      hm ? ctx->own_Tm : nullptr,
-                                      reports ? reports + (size_t)k * ctx->cfg.batch : nullptr);
+        ctx->defer_st = ctx->d_items + (size_t)k * B;
+        ctx->defer_launch = ctx->d_items_l + k;
+        hysco_status s = solve_common(ctx, 2, ot, so, nullptr, hb ? ctx->st_out[sl][0] : nullptr,
+                                      hp ? ctx->st_out[sl][1] : nullptr, hm ? ctx->st_out[sl][2] : nullptr, nullptr);
+        CK(cudaEventRecord(ctx->ev_in_free[sl], ks));
         if (s < 0) {
             if (first_err == HYSCO_OK) first_err = s;
             continue;
         }
         if (s != HYSCO_OK && first_err == HYSCO_OK) first_err = s;
-        // results -> output slot (compute stream), then out to the host (copy stream)
-        CK(cudaStreamWaitEvent(ks, ctx->ev_out_free[sl], 0));
-        if (hb) CK(copy_nodes(ctx, ctx->st_out[sl][0], ctx->buf[B_B], false, cudaMemcpyDeviceToDevice));
-        if (hp) CK(cudaMemcpyAsync(ctx->st_out[sl][1], ctx->own_Tp, nc, cudaMemcpyDeviceToDevice, ks));
-        if (hm) CK(cudaMemcpyAsync(ctx->st_out[sl][2], ctx->own_Tm, nc, cudaMemcpyDeviceToDevice, ks));
+        ran[k] = 1;
+        // results out to the host (copy stream)
         CK(cudaEventRecord(ctx->ev_out[sl], ks));
         CK(cudaStreamWaitEvent(cs, ctx->ev_out[sl], 0));
         if (hb) CK(cudaMemcpyAsync(hb, ctx->st_out[sl][0], nn, cudaMemcpyDeviceToHost, cs));
@@ -2702,8 +2787,25 @@ hysco_status hysco_correct_host_stream(hysco_ctx ctx, int32_t n_items, const voi
         if (hm) CK(cudaMemcpyAsync(hm, ctx->st_out[sl][2], nc, cudaMemcpyDeviceToHost, cs));
         CK(cudaEventRecord(ctx->ev_out_free[sl], cs));
     }
+    if (n_items > 0) {
+        CK(cudaMemcpyAsync(ctx->h_items, ctx->d_items, sizeof(PairState) * (size_t)n_items * B,
+                           cudaMemcpyDeviceToHost, ks));
+        CK(cudaMemcpyAsync(ctx->h_items_l, ctx->d_items_l, sizeof(unsigned long long) * n_items,
+                           cudaMemcpyDeviceToHost, ks));
+    }
     CK(cudaStreamSynchronize(cs));
     CK(cudaStreamSynchronize(ks));
+    // reports and the state mirror from the per-item readbacks (in item order)
+    ctx->state_valid = false;
+    for (int k = 0; k < n_items; k++) {
+        if (!ran[k]) continue;
+        memcpy(ctx->h_st, ctx->h_items + (size_t)k * B, sizeof(PairState) * B);
+        ctx->last_launches = (long long)ctx->h_items_l[k];
+        bool inf = false;
+        fill_reports(ctx, reports ? reports + (size_t)k * B : nullptr, &inf);
+        if (inf && first_err == HYSCO_OK) first_err = HYSCO_INFEASIBLE;
+        ctx->state_valid = k == n_items - 1 && !inf && !ctx->last_per_pair;   // as after hysco_correct
+    }
     return first_err;
 }
 
@@ -3014,6 +3116,8 @@ hysco_status hysco_destroy(hysco_ctx ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->exec) cudaGraphExecDestroy(ctx->exec);
     if (ctx->graph) cudaGraphDestroy(ctx->graph);
+    if (ctx->exec2) cudaGraphExecDestroy(ctx->exec2);
+    if (ctx->graph2) cudaGraphDestroy(ctx->graph2);
     for (cudaGraphExec_t e : ctx->seg_exec) cudaGraphExecDestroy(e);
     for (int k = 0; k < NBUF; k++)
         if (ctx->raw[k]) cudaFree(ctx->raw[k]);
@@ -3058,6 +3162,10 @@ hysco_status hysco_destroy(hysco_ctx ctx) {
     }
     if (ctx->h_st) cudaFreeHost(ctx->h_st);
     if (ctx->h_launches) cudaFreeHost(ctx->h_launches);
+    if (ctx->h_items) cudaFreeHost(ctx->h_items);
+    if (ctx->h_items_l) cudaFreeHost(ctx->h_items_l);
+    if (ctx->d_items) cudaFree(ctx->d_items);
+    if (ctx->d_items_l) cudaFree(ctx->d_items_l);
     if (ctx->h_cond) cudaFreeHost(ctx->h_cond);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     cudaGetLastError();

@@ -313,7 +313,11 @@ __host__ __device__ inline size_t march_smem_bytes(const MarchPlan& m) {
     return march_stage_bytes<T>(m) * m.nst + 16 * 8;   // + the stage barriers
 }
 
-constexpr int MARCH_THREADS = 512;   // one CTA per SM (shared memory), 16 warps
+#ifndef HYSCO_MARCH_CPS
+#define HYSCO_MARCH_CPS 1   // march CTAs per SM (each with 1 / CPS of the shared memory and threads)
+#endif
+constexpr int MARCH_CPS = HYSCO_MARCH_CPS;
+constexpr int MARCH_THREADS = 512 / MARCH_CPS;   // CPS = 1: one CTA per SM (shared memory), 16 warps
 
 // FIRST (k = 0): p_0 = z, no p_{-1}, no x update.  MS: node slots per thread
 // (the tile's own nodes of one plane, (jb - ja) P <= MS * MARCH_THREADS); every
@@ -321,7 +325,7 @@ constexpr int MARCH_THREADS = 512;   // one CTA per SM (shared memory), 16 warps
 // flags are computed once, and the MS independent nodes of a slot loop give
 // the two warps per scheduler instruction-level parallelism.
 template <typename T, bool FIRST, int MS>
-__global__ void __launch_bounds__(MARCH_THREADS, 1) pcg_march_kernel(Geom g, Ctl c, int nJB, int C, MarchPlan mp,
+__global__ void __launch_bounds__(MARCH_THREADS, MARCH_CPS) pcg_march_kernel(Geom g, Ctl c, int nJB, int C, MarchPlan mp,
                                                                      const T* __restrict__ dt,
                                                                      const T* __restrict__ et,
                                                                      const T* __restrict__ z, T* __restrict__ pbuf0,
