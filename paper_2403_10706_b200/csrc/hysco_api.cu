@@ -1231,6 +1231,27 @@ template <typename T>
 static void gn_sequence(Runner& r, const SolveParams& sp) {
     hysco_ctx c = r.c;
     const char* e = getenv("HYSCO_GRAPH_LOOPS");
+    if (sp.fixed && r.graph && !(e && e[0] == '1') && c->resident && sp.precond != HYSCO_PRECOND_PE_BLOCK &&
+        !getenv_is1("HYSCO_LS_WHILE")) {
+        // resident PCG (one launch per GN step): max_gn unrolled slots of
+        // (PCG step, trial / retry evaluation) with no conditional node inside;
+        // a rejected trial's retry takes the next slot (whose PCG launch then
+        // does nothing: pcg_step_active), and one WHILE node after the slots
+        // finishes what the retries displaced (not entered when none did).
+        // Each conditional node costs ~8 us of device-side scheduling (CUPTI
+        // timeline: the gap before every resident launch after a WHILE node).
+        r.handle(COND_GN);
+        r.seq([&] { L<T>::eval(c, sp, EVAL_GN_START, L<T>::b(c, B_B)); });
+        for (int k = 0; k < sp.max_gn; k++) {
+            pcg_step<T>(r, sp, true);
+            r.seq([&] { L<T>::ls_body(c, sp); });
+        }
+        r.loop(COND_GN, [&] {
+            pcg_step<T>(r, sp, true);
+            r.seq([&] { L<T>::ls_body(c, sp); });
+        });
+        return;
+    }
     if (sp.fixed && r.graph && !(e && e[0] == '1')) {
         r.seq([&] { L<T>::eval(c, sp, EVAL_GN_START, L<T>::b(c, B_B)); });
         for (int k = 0; k < sp.max_gn; k++) {

@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(256) pcg_init_flat_kernel(Geom g, Ctl c, const
     constexpr int V = FlatVec<T>::V;
     count_launch(c);
     const int pair = blockIdx.y;
-    const bool active = c.st[pair].gn_active != 0;
+    const bool active = pcg_step_active(c.st[pair]);
     const size_t po = (size_t)pair * g.ps;
     double arz = 0, arr = 0;
     if (active) {
@@ -577,7 +577,7 @@ __global__ void __launch_bounds__(256) trial_flat_kernel(Geom g, Ctl c, const T*
     count_launch(c);
     const int pair = blockIdx.y;
     const PairState& st = c.st[pair];
-    const bool active = st.gn_active != 0;
+    const bool active = pcg_step_active(st);
     double agq = 0, aqm = 0;
     if (active) {
         const T ap = (T)st.alpha_c;

@@ -37,9 +37,9 @@ __global__ void __launch_bounds__(L2P_THREADS, 1)
                   T* __restrict__ Hp, T* __restrict__ bcur, T* __restrict__ bold, double* __restrict__ gpart,
                   unsigned* __restrict__ flags, int batch) {
     count_launch(c);
-    if (!c.st[pair].gn_active) {             // uniform over the grid: no step, no search
+    if (!pcg_step_active(c.st[pair])) {      // uniform over the grid: no step (finished, or a search pending)
         if (blockIdx.x == 0 && threadIdx.x == 0) {
-            c.st[pair].ls_active = 0;
+            if (!c.st[pair].gn_active) c.st[pair].ls_active = 0;
             if (pair == batch - 1)
                 set_cond(c, COND_LS, any_pair(c, batch, [](volatile PairState* q2) { return q2->ls_active != 0; }));
         }

@@ -69,9 +69,13 @@ __device__ inline void decide_matvec(PairState& s, const double* tot) {
         s.h_evals += 1;
     }
 }
+// A pair takes a PCG step when it has a GN step to take and no Armijo search
+// pending: in the unrolled resident graph (gn_sequence) a rejected trial's
+// retry takes the next step's slot, whose PCG kernels then do nothing.
+__device__ __forceinline__ bool pcg_step_active(const PairState& s) { return s.gn_active && !s.ls_active; }
 // PCG start (R14): tot = [r.z, r.r]
 __device__ inline void decide_pcg_init(PairState& s, const double* tot) {
-    if (s.gn_active) {
+    if (pcg_step_active(s)) {
         s.rz = tot[0];
         s.rr0 = tot[1];
         s.rr = tot[1];
@@ -97,16 +101,16 @@ __device__ inline void decide_update(const SolveParams& sp, PairState& s, const 
 }
 // Armijo start (R15): tot = [grad.q, max|q|]
 __device__ inline void decide_trial(PairState& s, const double* tot) {
-    if (s.gn_active) {
+    if (pcg_step_active(s)) {
         s.gq = tot[0];
         s.qmax = tot[1];
         s.gamma = 1.0;
         s.ls_tries = 0;
         s.ls_restore = 0;
         s.ls_active = 1;
-    } else {
+    } else if (!s.gn_active) {
         s.ls_active = 0;
-    }
+    }                                   // (a pending search keeps its state)
 }
 // feasibility guard (R10): tot = [max |Db0|]
 __device__ inline void decide_guard(const SolveParams& sp, PairState& s, const double* tot) {
@@ -208,7 +212,7 @@ __global__ void __launch_bounds__(256) pcg_init_kernel(Geom g, Ctl c, const T* _
     count_launch(c);
     const int lane = threadIdx.x & 31;
     const int pair = blockIdx.y;
-    const bool active = c.st[pair].gn_active != 0;
+    const bool active = pcg_step_active(c.st[pair]);
     const size_t po = (size_t)pair * g.ps;
     const int P = g.P;
     double arz = 0, arr = 0;
@@ -361,7 +365,7 @@ __global__ void __launch_bounds__(BLK_THREADS) bfac_kernel(Geom g, Ctl c, const 
                                                           T* __restrict__ f, int need_active) {
     count_launch(c);
     const int pair = blockIdx.y;
-    if (need_active && !c.st[pair].gn_active) return;
+    if (need_active && !pcg_step_active(c.st[pair])) return;
     const long long col = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (col >= g.ncol) return;
     const ColInfo ci = col_info(g, col);
@@ -448,7 +452,7 @@ __global__ void __launch_bounds__(256) pcg_blk_kernel(Geom g, Ctl c, SolveParams
     count_launch(c);
     const int lane = threadIdx.x & 31;
     const int pair = blockIdx.y;
-    const bool active = INIT ? c.st[pair].gn_active != 0 : c.st[pair].pcg_active != 0;
+    const bool active = INIT ? pcg_step_active(c.st[pair]) : c.st[pair].pcg_active != 0;
     const T a = INIT ? T(0) : (T)c.st[pair].alpha_c;
     const size_t po = (size_t)pair * g.ps;
     const int P = g.P;
@@ -602,7 +606,7 @@ __global__ void __launch_bounds__(256) trial_init_kernel(Geom g, Ctl c, const T*
     count_launch(c);
     const int lane = threadIdx.x & 31;
     const int pair = blockIdx.y;
-    const bool active = c.st[pair].gn_active != 0;
+    const bool active = pcg_step_active(c.st[pair]);
     const size_t po = (size_t)pair * g.ps;
     const int P = g.P;
     double agq = 0, aqm = 0;

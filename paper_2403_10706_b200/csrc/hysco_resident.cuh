@@ -441,9 +441,9 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
     constexpr int NT = RES_THREADS;
     static_assert(K <= RES_KMAX, "slot masks hold RES_KMAX slots per field");
     count_launch(c);
-    if (!c.st[pair].gn_active) {             // uniform over the grid: no step, no search
+    if (!pcg_step_active(c.st[pair])) {      // uniform over the grid: no step (finished, or a search pending)
         if (blockIdx.x == 0 && threadIdx.x == 0) {
-            c.st[pair].ls_active = 0;
+            if (!c.st[pair].gn_active) c.st[pair].ls_active = 0;
             if (pair == batch - 1)
                 set_cond(c, COND_LS, any_pair(c, batch, [](volatile PairState* q2) { return q2->ls_active != 0; }));
         }
