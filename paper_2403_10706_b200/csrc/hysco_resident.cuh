@@ -706,7 +706,9 @@ __global__ void __launch_bounds__(RES_THREADS, 1)
                     const float2 p = s2[k * NT];
                     const float2 v = make_float2(a * p.x, a * p.y);
                     if (mbit(m, RM_VAL + k)) {
-#ifdef RES_ABLATE_X
+#if defined(RES_ABLATE_XNONE)   // diagnostic builds only: timing without any x traffic (q invalid)
+                        if (v.x == 12345.f) xt[k * NT] = v;
+#elif defined(RES_ABLATE_X)
                         if (k_it > 0) xt[k * NT] = v;
 #else
                         if (k_it > 0) red_add2(reinterpret_cast<float*>(xt + k * NT), v);

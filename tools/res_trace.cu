@@ -76,6 +76,7 @@ int main(int argc, char** argv) {
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     float ms_notrace = 0, ms_trace = 0;
     for (int rep = 0; rep < 7; rep++) {
+        cudaMemcpy(st, &hs, sizeof hs, cudaMemcpyHostToDevice);   // a fresh GN step (no search pending)
         cudaEventRecord(e0);
         if (tiled)
             cudaLaunchKernelEx(&cfg, pcg_resident_kernel<RES_KMAX, true, false, true>, g, c, sp, 0, (const float*)grad,
@@ -86,6 +87,7 @@ int main(int argc, char** argv) {
                                (const float*)et, x, xpad, pgh, part, flags, wi, wj, bb, bo, 1, (unsigned long long*)nullptr, tl);
         cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms_notrace, e0, e1);
     }
+    cudaMemcpy(st, &hs, sizeof hs, cudaMemcpyHostToDevice);
     cudaEventRecord(e0);
     if (tiled)
         cudaLaunchKernelEx(&cfg, pcg_resident_kernel<RES_KMAX, true, true, true>, g, c, sp, 0, (const float*)grad,
@@ -182,6 +184,7 @@ int main(int argc, char** argv) {
         c2.gridDim = dim3(G);
         cudaMemset(bb, 0, Nn * 4);
         cudaMemset(pgh, 0, ghost * 4);   // the strip layout's zero ghost planes (the tiled runs used the buffer)
+        cudaMemcpy(st, &hs, sizeof hs, cudaMemcpyHostToDevice);
         cudaLaunchKernelEx(&c2, pcg_resident_kernel<RES_KMAX, true>, g, c, sp, 0, (const float*)grad, (const float*)dt,
                            (const float*)et, x, xpad, pgh, part, flags, wi, wj, bb, bo, 1, (unsigned long long*)nullptr, tl);
         cudaDeviceSynchronize();
