@@ -17,23 +17,24 @@ from synth import phantom
 
 def main():
     cfg = sys.argv[1] if len(sys.argv) > 1 else "C2_hcp3t"
+    B = int(sys.argv[2]) if len(sys.argv) > 2 else 1      # pairs per context (batch)
     p = phantom.make_config(cfg)
     n1, n2, n3 = p.Ip.shape
     dev = "cuda:0"
-    Ip = torch.from_numpy(p.Ip[None]).to(dev)
-    Im = torch.from_numpy(p.Im[None]).to(dev)
+    Ip = torch.from_numpy(p.Ip[None]).to(dev).repeat(B, 1, 1, 1).contiguous()
+    Im = torch.from_numpy(p.Im[None]).to(dev).repeat(B, 1, 1, 1).contiguous()
     stream = torch.cuda.current_stream()
-    ctx = H.hysco_create((n1, n2, n3), p.h, 1, device=0, stream=stream.cuda_stream)
+    ctx = H.hysco_create((n1, n2, n3), p.h, B, device=0, stream=stream.cuda_stream)
     H.hysco_bind_images(ctx, Ip, Im)
-    b = torch.zeros((1, n1, n2, n3 + 1), device=dev)
-    Tp = torch.zeros((1, n1, n2, n3), device=dev)
+    b = torch.zeros((B, n1, n2, n3 + 1), device=dev)
+    Tp = torch.zeros((B, n1, n2, n3), device=dev)
     Tm = torch.zeros_like(Tp)
     for _ in range(3):
-        H.hysco_correct(ctx, b, Tp, Tm)
+        H.hysco_correct(ctx, b, Tp, Tm, batch=B)
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         for _ in range(2):
-            H.hysco_correct(ctx, b, Tp, Tm)
+            H.hysco_correct(ctx, b, Tp, Tm, batch=B)
         torch.cuda.synchronize()
     path = os.path.join(ROOT, "gpurun_out", "timeline_trace.json")
     os.makedirs(os.path.dirname(path), exist_ok=True)
