@@ -504,6 +504,9 @@ def run_hysco(args):
                 "clocks": clocks, "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
                 "cpu_baseline": cpu,
                 "solver": {k: r0[k] for k in ("gn_iters", "f_evals", "h_evals", "pcg_iters", "stop", "J")},
+                # a batch holds B different synthetic pairs (seeds), whose Armijo
+                # searches differ: objective evaluations per pair of the last step
+                **({"f_evals_per_pair": [int(r["f_evals"]) for r in reps]} if B > 1 else {}),
                 "paper_context": {"seconds_per_pair": 4.38, "pairs_per_s": 1 / 4.38,
                                   "hardware": "GPU inferred RTX A6000, fp32, real HCP 3T data",
                                   "source": "PAPER.md Table 3 (P:476)"}}
