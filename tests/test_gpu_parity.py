@@ -489,6 +489,32 @@ def test_tiled_resident_matches_strips(monkeypatch, cfg, tile, max_gn):
     assert relS(rt["J"], rs["J"]) <= 1e-6
 
 
+def test_tiled_resident_paper_stop_matches_strips(monkeypatch):
+    """The CLI default (the paper's stop rules, P:196 / P:284, R14, R16) on the
+    tiled resident kernel's early-exit variant (pcg_resident_kernel<K, false,
+    false, true>) at the 3T shape: same stop reason, counters and field map as
+    over strips."""
+    if torch.cuda.get_device_properties(0).multi_processor_count != 148:
+        pytest.skip("the tilings are chosen for 148 SMs")
+    p = phantom.make_config("C2_hcp3t")
+    so = H.default_solve_opts(fixed_iters=0, max_gn=50)
+    out = []
+    for tiled in ("1", "0"):
+        monkeypatch.setenv("HYSCO_RES_TILED", tiled)
+        c = Ctx([p.Ip], [p.Im], p.h)
+        assert H.hysco_pcg_path(c.ctx)[0] == ("resident-tiles" if tiled == "1" else "resident-strips")
+        b, Tp, Tm = c.nodes(), c.cells(), c.cells()
+        reps, inf = H.hysco_correct(c.ctx, b, Tp, Tm, solve_opts=so)
+        assert not inf
+        out.append((c.np(b)[0], reps[0]))
+        c.close()
+    (bt, rt), (bs, rs) = out
+    keys = ("pcg_iters", "h_evals", "gn_iters", "f_evals", "ls_halvings", "stop_reason")
+    assert tuple(rt[k] for k in keys) == tuple(rs[k] for k in keys)
+    assert rt["gn_iters"] > 10                                # the stop rules, not a fixed count, ended it
+    assert rel(bt, bs) <= 1e-5
+
+
 FLAT_CASES = [((5, 7, 37), 2), ((6, 5, 24), 3), ((4, 3, 42), 2), ((3, 4, 15), 3), ((1, 3, 70), 1), ((7, 6, 3), 2)]
 
 
