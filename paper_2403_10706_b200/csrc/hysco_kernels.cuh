@@ -522,7 +522,27 @@ __global__ void __launch_bounds__(256) ot_minmax_kernel(Geom g, Ctl c, SolvePara
     const int pair = blockIdx.y;
     const size_t pc = (size_t)pair * g.Nc;
     double mn = -INFINITY, mx = -INFINITY;   // max of (-v) and max of v
-    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < g.Nc;
+    long long t0 = 0;
+    if constexpr (sizeof(T) == 4) {          // 16-byte loads, max / min in fp32 (exact; widened once)
+        const T* a = Ip + pc;
+        const T* b = Im + pc;
+        if (((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0) {
+            float fmn = -INFINITY, fmx = -INFINITY;
+            const long long n4 = g.Nc / 4;
+            for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < n4;
+                 v += (long long)gridDim.x * blockDim.x) {
+                const float4 x = __ldg(reinterpret_cast<const float4*>(a) + v);
+                const float4 y = __ldg(reinterpret_cast<const float4*>(b) + v);
+                fmx = fmaxf(fmx, fmaxf(fmaxf(fmaxf(x.x, x.y), fmaxf(x.z, x.w)), fmaxf(fmaxf(y.x, y.y), fmaxf(y.z, y.w))));
+                fmn = fmaxf(fmn, fmaxf(fmaxf(fmaxf(-x.x, -x.y), fmaxf(-x.z, -x.w)),
+                                       fmaxf(fmaxf(-y.x, -y.y), fmaxf(-y.z, -y.w))));
+            }
+            mn = (double)fmn;
+            mx = (double)fmx;
+            t0 = n4 * 4;
+        }
+    }
+    for (long long t = t0 + (long long)blockIdx.x * blockDim.x + threadIdx.x; t < g.Nc;
          t += (long long)gridDim.x * blockDim.x) {
         const double a = (double)Ip[pc + t], b = (double)Im[pc + t];
         mn = fmax(mn, fmax(-a, -b));
