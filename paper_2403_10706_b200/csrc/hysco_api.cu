@@ -325,28 +325,30 @@ struct L {
     }
     // first iteration (p_0 = z) and later ones are separate instantiations; the
     // unrolled form launches the one it needs, the WHILE body both (the other exits)
+    // fuse: (slab, defer mode) apply the preceding allreduced decision in the
+    // kernel instead of a decide_kernel launch (hysco_flat.cuh)
     template <bool FIRST, int MS>
-    static void march_ms_t(hysco_ctx c) {
+    static void march_ms_t(hysco_ctx c, int fuse, const SolveParams& sp) {
         pcg_march_kernel<T, FIRST, MS><<<dim3(c->gx_dmv, c->vb), MARCH_THREADS, c->smem_mr, c->stream>>>(
             c->g, c->ctl, c->mr_njb, c->mr_c, c->mr_plan, b(c, B_DT), b(c, B_ET), b(c, B_TMP), b(c, B_P), b(c, B_W),
-            b(c, B_HP), b(c, B_X));
+            b(c, B_HP), b(c, B_X), fuse, sp);
     }
     template <bool FIRST>
-    static void march(hysco_ctx c) {
+    static void march(hysco_ctx c, int fuse, const SolveParams& sp) {
         switch (c->mr_plan.ms) {
-            case 2: march_ms_t<FIRST, 2>(c); break;
-            case 4: march_ms_t<FIRST, 4>(c); break;
-            case 8: march_ms_t<FIRST, 8>(c); break;
-            default: march_ms_t<FIRST, 12>(c); break;
+            case 2: march_ms_t<FIRST, 2>(c, fuse, sp); break;
+            case 4: march_ms_t<FIRST, 4>(c, fuse, sp); break;
+            case 8: march_ms_t<FIRST, 8>(c, fuse, sp); break;
+            default: march_ms_t<FIRST, 12>(c, fuse, sp); break;
         }
     }
-    static void pcg_dirmv(hysco_ctx c, bool first) {
-        if (first) march<true>(c);
-        else march<false>(c);
+    static void pcg_dirmv(hysco_ctx c, bool first, int fuse = 0, const SolveParams& sp = SolveParams{}) {
+        if (first) march<true>(c, 0, sp);
+        else march<false>(c, fuse, sp);
     }
-    static void pcg_upd(hysco_ctx c, const SolveParams& sp) {
+    static void pcg_upd(hysco_ctx c, const SolveParams& sp, int fuse = 0) {
         pcg_upd_kernel<T><<<dim3(c->gx_flat, c->vb), 256, 0, c->stream>>>(c->g, c->ctl, sp, b(c, B_F), b(c, B_HP),
-                                                                         b(c, B_R), b(c, B_TMP));
+                                                                         b(c, B_R), b(c, B_TMP), fuse);
     }
     static void pcg_iter_flat(hysco_ctx c, const SolveParams& sp, bool first) {
         pcg_dirmv(c, first);
@@ -987,13 +989,20 @@ struct SlabRun {
     // one PCG iteration: p halo, matvec, allreduce + decision,
     // update (block: with the column Thomas solve, R20), allreduce + decision,
     // direction
+    // fixed counts: the march / update apply the preceding allreduced decision
+    // themselves (no decide_kernel launch), except after the last update, whose
+    // decision the Armijo start needs committed
+    bool fuse() const { return sp.fixed && !getenv_is1("HYSCO_SLAB_NO_FUSE"); }
     void pcg_iter(bool blk, int k) {
         if (flat()) {
-            each([&](hysco_ctx c) { L<T>::pcg_dirmv(c, k == 0); });
-            reduce_decide(OP_MATVEC, 0, false);
+            const bool fz = fuse();
+            each([&](hysco_ctx c) { L<T>::pcg_dirmv(c, k == 0, fz && k > 0 ? 1 : 0, sp); });
+            if (fz) ok(comm->allreduce(R, false));
+            else reduce_decide(OP_MATVEC, 0, false);
             ok(comm->halo(R, (k & 1) ? B_W : B_P, false));   // p_k for the next march
-            each([&](hysco_ctx c) { L<T>::pcg_upd(c, sp); });
-            reduce_decide(OP_UPDATE, 0, false);
+            each([&](hysco_ctx c) { L<T>::pcg_upd(c, sp, fz ? 1 : 0); });
+            if (fz && k + 1 < sp.max_pcg) ok(comm->allreduce(R, false));
+            else reduce_decide(OP_UPDATE, 0, false);
             ok(comm->halo(R, B_TMP, false));                  // z_{k+1}
             return;
         }

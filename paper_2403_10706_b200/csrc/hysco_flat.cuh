@@ -324,13 +324,19 @@ constexpr int MARCH_THREADS = 512 / MARCH_CPS;   // CPS = 1: one CTA per SM (sha
 // thread keeps the same nodes in every plane, so their offsets and Neumann
 // flags are computed once, and the MS independent nodes of a slot loop give
 // the two warps per scheduler instruction-level parallelism.
+// fuse_up (slab path, defer mode, fixed counts): the previous residual
+// update's decision (decide_update on the allreduced r.z, r.r in c.red) is
+// not a separate decide_kernel launch: every CTA derives k, beta and the
+// active flag from the pre-decision state and the totals, and the last CTA
+// commits decide_update before it stores this launch's own partial totals.
 template <typename T, bool FIRST, int MS>
 __global__ void __launch_bounds__(MARCH_THREADS, MARCH_CPS) pcg_march_kernel(Geom g, Ctl c, int nJB, int C, MarchPlan mp,
                                                                      const T* __restrict__ dt,
                                                                      const T* __restrict__ et,
                                                                      const T* __restrict__ z, T* __restrict__ pbuf0,
                                                                      T* __restrict__ pbuf1, T* __restrict__ Hp,
-                                                                     T* __restrict__ x) {
+                                                                     T* __restrict__ x, int fuse_up = 0,
+                                                                     SolveParams sp = SolveParams{}) {
     extern __shared__ __align__(128) unsigned char march_raw[];
     unsigned long long* bars = reinterpret_cast<unsigned long long*>(march_raw);
     T* stage0 = reinterpret_cast<T*>(march_raw + 16 * 8);
@@ -343,10 +349,22 @@ __global__ void __launch_bounds__(MARCH_THREADS, MARCH_CPS) pcg_march_kernel(Geo
     const int bj = blockIdx.x % nJB, bc = blockIdx.x / nJB;
     const int n1 = g.n1, n2 = g.n2, P = g.P;
     const int ia = bc * C, ib = min(ia + C, n1);
+    // the decision this launch starts from: committed state, or (fuse_up)
+    // decide_update applied locally to the allreduced totals
+    bool pact = st.pcg_active != 0;
+    int kk = st.pcg_k;
+    double bet = st.beta_c;
+    const double* upd_tot = c.red + (size_t)pair * RED_W;
+    if (fuse_up && pact) {
+        kk = st.pcg_k + 1;
+        bet = upd_tot[0] / st.rz;
+        const double relres = sqrt(upd_tot[1] / st.rr0);
+        pact = !(kk >= sp.max_pcg || (!sp.fixed && relres < sp.pcg_rtol));
+    }
     // a launch of the other FIRST variant for this iteration parity does nothing
-    if (st.pcg_active && ia < n1 && ((st.pcg_k == 0) == FIRST)) {
-        const int k = st.pcg_k;
-        const T be = FIRST ? T(0) : (T)st.beta_c, ap = (T)st.alpha_c;
+    if (pact && ia < n1 && ((kk == 0) == FIRST)) {
+        const int k = kk;
+        const T be = FIRST ? T(0) : (T)bet, ap = (T)st.alpha_c;
         const size_t po = (size_t)pair * g.ps;
         T* __restrict__ pnew = ((k & 1) ? pbuf1 : pbuf0) + po;
         const T* __restrict__ pold = ((k & 1) ? pbuf0 : pbuf1) + po;
@@ -496,6 +514,10 @@ __global__ void __launch_bounds__(MARCH_THREADS, MARCH_CPS) pcg_march_kernel(Geo
     double v[1] = {acc}, tot[1];
     if (!pair_reduce<1, 0u>(c, v, tot)) return;
     if (threadIdx.x != 0) return;
+    if (fuse_up) {                       // every CTA has read the totals: commit their decision
+        double ut[2] = {upd_tot[0], upd_tot[1]};
+        decide_update(sp, c.st[pair], ut);
+    }
     if (c.defer) {                       // slab: OP_MATVEC after the allreduce
         store_red(c, pair, gridDim.y, tot, 1, 0);
         return;
@@ -505,15 +527,27 @@ __global__ void __launch_bounds__(MARCH_THREADS, MARCH_CPS) pcg_march_kernel(Geo
 
 // F2: r -= alpha Hp, z = r / M; r.z, r.r -> beta, stop test.  Pure streaming
 // (M from pcg_init_flat_kernel): 20 B per node.
+// fuse_mv (slab path, defer mode): the march's decision (decide_matvec on the
+// allreduced p.Hp) applied locally by every block, committed by the last.
 template <typename T>
 __global__ void __launch_bounds__(256) pcg_upd_kernel(Geom g, Ctl c, SolveParams sp, const T* __restrict__ mdiag,
                                                       const T* __restrict__ Hp, T* __restrict__ r,
-                                                      T* __restrict__ z) {
+                                                      T* __restrict__ z, int fuse_mv = 0) {
     constexpr int V = FlatVec<T>::V;
     count_launch(c);
     const int pair = blockIdx.y;
-    const bool active = c.st[pair].pcg_active != 0;
-    const T a = (T)c.st[pair].alpha_c;
+    bool active = c.st[pair].pcg_active != 0;
+    double al = c.st[pair].alpha_c;
+    const double mv_tot = fuse_mv ? c.red[(size_t)pair * RED_W] : 0.0;
+    if (fuse_mv && active) {
+        if (mv_tot <= 0.0) {             // breakdown (decide_matvec)
+            active = false;
+            al = 0.0;
+        } else {
+            al = c.st[pair].rz / mv_tot;
+        }
+    }
+    const T a = (T)al;
     const size_t po = (size_t)pair * g.ps;
     double arz = 0, arr = 0;
     if (active) {
@@ -557,6 +591,10 @@ __global__ void __launch_bounds__(256) pcg_upd_kernel(Geom g, Ctl c, SolveParams
     double v[2] = {arz, arr}, tot[2];
     if (!pair_reduce<2, 0u>(c, v, tot)) return;
     if (threadIdx.x != 0) return;
+    if (fuse_mv) {                       // every block has read the totals: commit their decision
+        double mt[1] = {mv_tot};
+        decide_matvec(c.st[pair], mt);
+    }
     if (c.defer) {                       // slab: OP_UPDATE after the allreduce
         store_red(c, pair, gridDim.y, tot, 2, 0);
         return;
