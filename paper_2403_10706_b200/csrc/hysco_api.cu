@@ -1262,12 +1262,21 @@ static void gn_sequence(Runner& r, const SolveParams& sp) {
         return;
     }
     if (sp.fixed && r.graph && !(e && e[0] == '1')) {
+        // a conditional node whose body runs costs ~95 us of device-side
+        // scheduling (CUPTI timeline, 7T), so the first ls_unroll retries of a
+        // search are plain launches (an evaluation with no search pending exits
+        // at once, ~4 us) and only further ones go through the WHILE node
+        const char* eu = getenv("HYSCO_LS_UNROLL");
+        const int ls_unroll = eu ? std::max(0, atoi(eu)) : 2;
         r.seq([&] { L<T>::eval(c, sp, EVAL_GN_START, L<T>::b(c, B_B)); });
         for (int k = 0; k < sp.max_gn; k++) {
             pcg_step<T>(r, sp, true);
             r.handle(COND_LS);
-            r.seq([&] { L<T>::ls_body(c, sp); });                              // first trial (gamma = 1)
-            r.loop(COND_LS, [&] { r.seq([&] { L<T>::ls_body(c, sp); }); });   // halvings, restore
+            r.seq([&] {
+                L<T>::ls_body(c, sp);                                          // first trial (gamma = 1)
+                for (int u = 0; u < ls_unroll; u++) L<T>::ls_body(c, sp);     // first halvings / restore
+            });
+            r.loop(COND_LS, [&] { r.seq([&] { L<T>::ls_body(c, sp); }); });   // further halvings
         }
         return;
     }

@@ -292,6 +292,17 @@ __global__ void __launch_bounds__(256, (NCH <= 5 ? 3 : 4)) eval_kernel(Geom g, C
                                                    const T* __restrict__ q, T* __restrict__ grad,
                                                    T* __restrict__ dt, T* __restrict__ et) {
     count_launch(c);
+    if (mode == EVAL_TRIAL && !c.defer) {    // no search pending in any pair (an unrolled retry slot):
+        bool any = false;                    // leave at once -- no reduction, no decision -- after
+        for (int p = 0; p < (int)gridDim.y; p++) any |= c.st[p].ls_active != 0;   // setting the loop
+        if (!any) {                          // conditions a completed evaluation would have set
+            if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+                set_cond(c, COND_LS, 0u);
+                set_cond(c, COND_GN, any_pair(c, gridDim.y, [](volatile PairState* q) { return q->gn_active != 0; }));
+            }
+            return;
+        }
+    }
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int pair = blockIdx.y;
