@@ -274,7 +274,7 @@ struct L {
     // bold / q given: a TRIAL evaluation forms the retry b itself (no ls_retry launch)
     static void eval(hysco_ctx c, const SolveParams& sp, int mode, const T* bsrc, const T* bold = nullptr,
                      const T* q = nullptr) {
-        NCH_SWITCH(c->nch, eval_kernel<T, NCH><<<dim3(c->gx_eval, c->vb), 256, c->smem_eval, c->stream>>>(
+        NCH_SWITCH(c->nch, eval_kernel<T, NCH><<<dim3(c->gx_eval, c->vb), 32 * EV_CT, c->smem_eval, c->stream>>>(
                                c->g, c->ctl, sp, mode, (const T*)c->Ip, (const T*)c->Im, bsrc, bold, q,
                                b(c, B_GRAD), b(c, B_DT), b(c, B_ET)));
     }
@@ -1525,8 +1525,8 @@ static hysco_status setup_typed(hysco_ctx ctx) {
     ctx->gx_mv = per_pair((g.ncol + 7) / 8, occ_m);
     ctx->gx_cells = per_pair((g.Nc + 255) / 256, occ_n);
     int occ_e = 1;
-    NCH_SWITCH(ctx->nch, occ_e = occ_blocks(eval_kernel<T, NCH>, 256, ctx->smem_eval));
-    ctx->gx_eval = per_pair((g.ncol + 7) / 8, occ_e);
+    NCH_SWITCH(ctx->nch, occ_e = occ_blocks(eval_kernel<T, NCH>, 32 * EV_CT, ctx->smem_eval));
+    ctx->gx_eval = per_pair((g.ncol + EV_CT - 1) / EV_CT, occ_e);
     ctx->gx_apply = per_pair((g.ncol + 7) / 8, occ_blocks(apply_kernel<T>, 256, ctx->smem_apply));
     const long long flat_blocks = (g.Nn / FlatVec<T>::V + 2 + 255) / 256;
     int occ_f = occ_blocks(pcg_upd_kernel<T>, 256, 0);
@@ -1593,7 +1593,7 @@ static hysco_status setup_typed(hysco_ctx ctx) {
     ctx->gx1[0] = one((g.ncol + 7) / 8, occ_n);
     ctx->gx1[1] = one((g.ncol + 7) / 8, occ_m);
     ctx->gx1[2] = one((g.Nc + 255) / 256, occ_n);
-    ctx->gx1[3] = one((g.ncol + 7) / 8, occ_e);
+    ctx->gx1[3] = one((g.ncol + EV_CT - 1) / EV_CT, occ_e);
     ctx->gx1[4] = one((g.ncol + 7) / 8, occ_blocks(apply_kernel<T>, 256, ctx->smem_apply));
     ctx->gx1[5] = one((g.ncol + 7) / 8, occ_blocks(ot_column_kernel<T>, 256, ctx->smem_ot));
     ctx->gx1[6] = one(flat_blocks, occ_f);

@@ -160,7 +160,10 @@ __device__ inline void decide_eval(const Geom& g, const Ctl& c, const SolveParam
 // Scalars D, S, P and ||grad||^2 reduce per pair; TRIAL mode also takes the
 // Armijo decision (R15).
 // ---------------------------------------------------------------------------
-constexpr int EV_CT = 8;   // columns per tile = warps per CTA
+#ifndef EV_CT_DEF
+#define EV_CT_DEF 8
+#endif
+constexpr int EV_CT = EV_CT_DEF;   // columns per tile = warps per CTA
 
 // Shared-memory elements of one eval tile (hysco_api.cu sizes the launch with this).
 __host__ __device__ inline size_t eval_smem_elems(int n3) {
@@ -168,7 +171,7 @@ __host__ __device__ inline size_t eval_smem_elems(int n3) {
     return (3 * EV_CT + 2) * P + 2 * EV_CT * ((size_t)n3 + 4);
 }
 // apply_kernel: per warp the column's I+, I- and b
-__host__ __device__ inline size_t apply_smem_elems(int n3) { return (size_t)EV_CT * (2 * (size_t)n3 + n3 + 1); }
+__host__ __device__ inline size_t apply_smem_elems(int n3) { return (size_t)8 * (2 * (size_t)n3 + n3 + 1); }   // 8 warps (256 threads)
 
 // One cell's two gathers (I+ at k + Ab/h3, I- at k - Ab/h3) from columns
 // padded with two zeros on each side (index kk clamped to [-2, n3] reads the
@@ -286,7 +289,7 @@ __device__ __forceinline__ void stage_b(const T* __restrict__ src, const T* __re
 // = b_old + gamma q (gamma = 0 to restore, R15) is formed while staging and
 // written to bb, which replaces the separate retry kernel.
 template <typename T, int NCH>
-__global__ void __launch_bounds__(256, (NCH <= 5 ? 3 : 4)) eval_kernel(Geom g, Ctl c, SolveParams sp, int mode,
+__global__ void __launch_bounds__(32 * EV_CT, (NCH <= 5 ? 3 : 4) * 8 / EV_CT) eval_kernel(Geom g, Ctl c, SolveParams sp, int mode,
                                                    const T* __restrict__ Ip, const T* __restrict__ Im,
                                                    const T* bb, const T* __restrict__ bold,
                                                    const T* __restrict__ q, T* __restrict__ grad,
